@@ -1,0 +1,404 @@
+/*
+ * xscat_gpu.h — C ABI of the B200-native Monte Carlo scatter / primary
+ * forward projector (drop-in for the reference xscat projector path).
+ *
+ * The reference (`/root/reference/proj`, "REF") has no FFI: its boundary is
+ * the C++ API in include/xscat/transport.hpp:69-116 and
+ * include/xscat/postprocess.hpp:13-41.  Every entry point below replaces one
+ * of those functions; the citation is given per declaration.  Plain pointers
+ * and sizes only; no C++ or torch types cross this boundary.
+ *
+ * Conventions
+ *  - Every function returns an xs_status; XS_OK == 0.  Non-zero codes map
+ *    one-to-one onto the exception types REF throws (see xs_status), and the
+ *    message REF would have put into e.what() is available from
+ *    xs_last_error(ctx) (ctx may be NULL for context-free calls: the message
+ *    is then thread-local).
+ *  - Host buffers are owned by the caller.  Device buffers created by the
+ *    library are owned by the context.  One context = one CUDA device + one
+ *    stream; a context is not thread-safe, distinct contexts are.
+ *  - Images are fp64, row-major, index iv*nu + iu (REF detector_image.hpp:11-22).
+ *  - Voxel arrays are x-fastest, index ix + nx*(iy + ny*iz) (REF phantom.hpp:14-37).
+ */
+#ifndef XSCAT_GPU_H
+#define XSCAT_GPU_H
+
+#include <math.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define XS_ABI_VERSION 1
+
+/* ------------------------------------------------------------------ status */
+typedef enum xs_status {
+    XS_OK = 0,
+    XS_E_RUNTIME = 1,          /* REF throws std::runtime_error            */
+    XS_E_OUT_OF_RANGE = 2,     /* REF throws std::out_of_range             */
+    XS_E_INVALID_ARGUMENT = 3, /* REF throws std::invalid_argument         */
+    XS_E_DOMAIN = 4,           /* REF throws std::domain_error             */
+    XS_E_CUDA = 5,             /* CUDA runtime failure (no REF counterpart) */
+    XS_E_UNSUPPORTED = 6       /* input beyond the device path's limits    */
+} xs_status;
+
+/* ------------------------------------------------------------ input types */
+
+/* One strictly-increasing 1-D table (REF table.hpp:15-95). */
+typedef struct xs_table {
+    int32_t n;
+    const double* x;
+    const double* y;
+} xs_table;
+
+/* REF material.hpp:15-32.  The F^2 dq^2 CDF (REF material.cpp:107-125) is
+ * derived by the library from f_factor; callers do not supply it. */
+typedef struct xs_material {
+    const char* name;
+    double z_eff;
+    double density_ref;
+    xs_table mu;          /* keV -> cm^2/g, log-log        */
+    xs_table sigma_incoh; /* keV -> barn, log-log          */
+    xs_table sigma_coh;   /* keV -> barn, log-log          */
+    xs_table sigma_pe;    /* keV -> barn, log-log          */
+    xs_table s_factor;    /* 1/A -> S, linear, clamp z_eff */
+    xs_table f_factor;    /* 1/A -> F, linear, clamped     */
+} xs_material;
+
+/* REF VoxelPhantom (phantom.hpp:14-37).  materials[0] is the vacuum
+ * sentinel (its tables are ignored and may be empty). */
+typedef struct xs_phantom {
+    int32_t dims[3];
+    double voxel_size[3]; /* cm */
+    double origin[3];     /* low corner, cm */
+    const uint8_t* material_id;
+    const float* density; /* g/cm^3 */
+    int32_t n_materials;  /* including vacuum at index 0 */
+    const xs_material* materials;
+} xs_phantom;
+
+/* REF ScanGeometry (scan_geometry.hpp:20-40). */
+typedef struct xs_geometry {
+    double sdd;
+    double sod;
+    int32_t nu;
+    int32_t nv;
+    double pixel_pitch;
+    int32_t n_angles;
+    const double* angles; /* radians, strictly increasing in [0, 2pi) */
+} xs_geometry;
+
+/* REF Spectrum (spectrum.hpp:14-26). */
+typedef struct xs_spectrum {
+    int32_t n_bins;
+    const double* energy_kev;
+    const double* weight;
+} xs_spectrum;
+
+/* REF DetectorResponse (detector_response.hpp:11-24). */
+typedef struct xs_response {
+    xs_table dqe;
+    xs_table deposit;
+} xs_response;
+
+/* REF SimConfig (transport.hpp:22-31); same defaults via xs_sim_config_default. */
+typedef struct xs_sim_config {
+    uint64_t photons_total;
+    int32_t splitting;
+    double roulette_survival;
+    double roulette_wmin_rel;
+    int32_t step_voxels;
+    int32_t max_interactions;
+    uint64_t seed;
+    int32_t track_variance;
+} xs_sim_config;
+
+/* REF WeightLedger (transport.hpp:38-56). */
+typedef struct xs_ledger {
+    double initial;
+    double escaped;
+    double absorbed;
+    double culled;
+    double roulette_killed;
+    double roulette_boost;
+} xs_ledger;
+
+/* REF SimResult (transport.hpp:58-64).  image (nu*nv) is required;
+ * variance (nu*nv) is written only when track_variance and non-NULL. */
+typedef struct xs_scatter_result {
+    double* image;
+    double* variance;
+    xs_ledger ledger;
+    uint64_t histories;
+    double total;
+    double total_std_error;
+} xs_scatter_result;
+
+/* Per-launch device counters (the roofline numerator). */
+typedef struct xs_launch_stats {
+    uint64_t free_path_steps;  /* voxel visits of the free-path walks          */
+    uint64_t scoring_steps;    /* voxel visits (or midpoint samples) of scoring rays */
+    uint64_t histories;        /* histories processed by the launch          */
+    uint64_t scoring_rays;     /* next-event pseudo-particles traced          */
+    uint64_t interactions;     /* Compton + Rayleigh + photoelectric events   */
+    double kernel_ms;          /* transport kernel time, CUDA events          */
+    int32_t voxel_format;      /* 0 = 4-bit palette, 1 = 8-bit palette, 2 = raw id+density */
+    int32_t palette_size;
+} xs_launch_stats;
+
+typedef struct xs_context xs_context;
+
+/* ------------------------------------------------- deterministic accumulator
+ *
+ * Scatter tallies are accumulated as exact integers so the result is
+ * bit-identical for any thread schedule and any number of GPUs.  A
+ * non-negative real x is stored relative to a power-of-two unit U as three
+ * 32-bit limbs of the 96-bit fixed-point number x/U * 2^64:
+ *   limb2 = floor(x/U), limb1 = next 32 bits, limb0 = last 32 bits (rounded).
+ * Each limb is added into its own uint64 slot, so a slot absorbs 2^32 adds
+ * without overflow and limb sums from several GPUs can be added by a plain
+ * integer sum-reduce (NCCL ncclUint64/ncclInt64 ncclSum).
+ *
+ * Layout of one accumulator buffer (uint64 words), see xs_accum_layout():
+ *   image    : 4 words per pixel  {limb0, limb1, limb2, 0}   unit U_img
+ *   variance : 4 words per pixel  (track_variance only)      unit U_img^2
+ *   bins     : 8 words per bin    {T limbs[3], T^2 limbs[3], 0, 0}
+ *   ledger   : 6 x 4 words        initial, escaped, absorbed, culled,
+ *                                 roulette_killed, roulette_boost; unit U_w
+ *   diag     : 8 words            launch counters (xs_launch_stats order)
+ */
+typedef struct xs_accum_layout {
+    uint64_t n_pixels;
+    uint64_t off_image;
+    uint64_t off_variance; /* == off_bins when variance is not tracked */
+    uint64_t off_bins;
+    uint64_t off_ledger;
+    uint64_t off_diag;
+    uint64_t words;
+} xs_accum_layout;
+
+static inline xs_accum_layout xs_accum_layout_make(int32_t nu, int32_t nv, int32_t n_bins,
+                                                   int32_t track_variance)
+{
+    xs_accum_layout l;
+    l.n_pixels = (uint64_t)nu * (uint64_t)nv;
+    l.off_image = 0;
+    l.off_variance = 4 * l.n_pixels;
+    l.off_bins = l.off_variance + (track_variance ? 4 * l.n_pixels : 0);
+    l.off_ledger = l.off_bins + 8 * (uint64_t)n_bins;
+    l.off_diag = l.off_ledger + 24;
+    l.words = l.off_diag + 8;
+    return l;
+}
+
+/* Power-of-two units of the fixed-point tallies; functions of the inputs
+ * only (never of the GPU count), so every split of the history range
+ * produces limbs in the same units.
+ *   U_img = 2^floor(log2(sum_b w_b / sdd^2))   (flat-field scale; response <= 1)
+ *   U_w   = 2^ceil(log2(max_b(w_b / M_b) * A_det / sdd^2))   (bound on w0)   */
+typedef struct xs_accum_units {
+    int32_t log2_img;
+    int32_t log2_w;
+} xs_accum_units;
+
+static inline int32_t xs__floor_log2(double v)
+{
+    int e = 0;
+    if (!(v > 0.0) || !isfinite(v))
+        return 0;
+    (void)frexp(v, &e); /* v = m 2^e, m in [0.5, 1) */
+    return (int32_t)(e - 1);
+}
+
+static inline int32_t xs__ceil_log2(double v)
+{
+    int e = 0;
+    double m;
+    if (!(v > 0.0) || !isfinite(v))
+        return 0;
+    m = frexp(v, &e);
+    return (int32_t)(m == 0.5 ? e - 1 : e);
+}
+
+static inline xs_accum_units xs_accum_units_make(const xs_geometry* g, const xs_spectrum* s,
+                                                 const uint64_t* photons_per_bin)
+{
+    xs_accum_units u;
+    double wsum = 0.0, wmax = 0.0;
+    const double sdd2 = g->sdd * g->sdd;
+    const double area = (double)g->nu * (double)g->nv * g->pixel_pitch * g->pixel_pitch;
+    int32_t b;
+    for (b = 0; b < s->n_bins; ++b) {
+        wsum += s->weight[b];
+        if (photons_per_bin[b] > 0) {
+            const double r = s->weight[b] / (double)photons_per_bin[b];
+            if (r > wmax)
+                wmax = r;
+        }
+    }
+    u.log2_img = xs__floor_log2(wsum / sdd2);
+    u.log2_w = xs__ceil_log2(wmax * area / sdd2);
+    return u;
+}
+
+/* Splits q = x/U (0 <= q < 2^32) into the three limbs; every step is exact
+ * in IEEE binary64 except the final round-half-even, so host and device
+ * produce identical limbs.  Returns 0 on success, 1 if q is out of range. */
+static inline int xs_quantize(double q, uint64_t limb[3])
+{
+    double i2, r, r1, i1, r2;
+    if (!(q >= 0.0) || !(q < 4294967296.0))
+        return 1;
+    i2 = floor(q);
+    r = q - i2;
+    r1 = r * 4294967296.0;
+    i1 = floor(r1);
+    r2 = (r1 - i1) * 4294967296.0;
+    limb[2] = (uint64_t)i2;
+    limb[1] = (uint64_t)i1;
+    limb[0] = (uint64_t)nearbyint(r2);
+    return 0;
+}
+
+/* Exact limb sum back to a double in units of U (deterministic rounding). */
+static inline double xs_dequantize(const uint64_t* s, int32_t log2_unit)
+{
+    /* S = s2*2^64 + s1*2^32 + s0 as a 128-bit integer (hi, lo) */
+    uint64_t lo = s[0];
+    uint64_t hi = s[2];
+    uint64_t t = s[1] << 32;
+    uint64_t c = s[1] >> 32;
+    uint64_t lo2 = lo + t;
+    hi += c + (lo2 < lo ? 1u : 0u);
+    lo = lo2;
+    return ldexp((double)hi * 18446744073709551616.0 + (double)lo, log2_unit - 64);
+}
+
+/* ------------------------------------------------------------ host helpers */
+
+const char* xs_version(void);
+int xs_abi_version(void);
+
+/* Thread-local message of the last failing call (context-free calls). */
+const char* xs_last_error(const xs_context* ctx);
+
+/* REF SimConfig{} defaults (transport.hpp:22-31). */
+void xs_sim_config_default(xs_sim_config* cfg);
+
+/* REF validate_sim_config (transport.cpp:26-40). */
+int xs_validate_sim_config(const xs_sim_config* cfg);
+
+/* REF apportion_photons (transport.cpp:42-64); counts has n_bins entries. */
+int xs_apportion_photons(const xs_spectrum* spec, uint64_t photons_total, uint64_t* counts);
+
+/* REF point_detector_score (transport.cpp:66-71). */
+double xs_point_detector_score(double response_factor, double p_dir, double weight,
+                               double n_pixels, double d2, double tau);
+
+/* Finalize a (possibly reduced) accumulator on the host, no GPU needed:
+ * REF simulate_scatter_stats ordered reduction + SE + variance
+ * (transport.cpp:289-322).  hist_begin/hist_end is the global history range
+ * the accumulator covers (the whole range after a reduce). */
+int xs_scatter_finalize_host(const xs_geometry* g, const xs_spectrum* spec,
+                             const xs_sim_config* cfg, const uint64_t* accum,
+                             uint64_t hist_begin, uint64_t hist_end, xs_scatter_result* out);
+
+/* Total number of histories (sum of apportioned photons) of a run. */
+int xs_history_count(const xs_spectrum* spec, uint64_t photons_total, uint64_t* n_histories);
+
+/* Savitzky-Golay helpers (REF postprocess.cpp:11-102). */
+int xs_validate_sg_spec(int32_t window, int32_t polyorder);
+int xs_default_sg_spec(int32_t nu, int32_t nv, int32_t* window, int32_t* polyorder);
+int xs_sg_kernel(int32_t left, int32_t right, int32_t polyorder, double* out /* left+right+1 */);
+
+/* --------------------------------------------------------------- context */
+
+int xs_device_count(int32_t* n);
+int xs_ctx_create(int32_t device, xs_context** out);
+void xs_ctx_destroy(xs_context* ctx);
+/* Use an external CUDA stream (cudaStream_t as void*); NULL restores the
+ * context's own stream. */
+int xs_ctx_set_stream(xs_context* ctx, void* cuda_stream);
+int xs_ctx_synchronize(xs_context* ctx);
+
+/* Scene upload: REF passes the phantom and response by const& to every
+ * projector call; here they are uploaded once and reused until replaced.
+ * xs_upload_phantom validates like REF validate_phantom (phantom.cpp:33-56)
+ * and re-encodes the grid into the device voxel format. */
+int xs_upload_phantom(xs_context* ctx, const xs_phantom* ph);
+int xs_upload_response(xs_context* ctx, const xs_response* resp);
+
+/* ---------------------------------------------------------- the projector */
+
+/* REF simulate_scatter_stats (transport.hpp:89-91, transport.cpp:246-324):
+ * whole history range on this device, host outputs. */
+int xs_simulate_scatter_stats(xs_context* ctx, const xs_geometry* g, int32_t angle_idx,
+                              const xs_spectrum* spec, const xs_sim_config* cfg,
+                              xs_scatter_result* out);
+
+/* REF simulate_primary (transport.hpp:100-102, transport.cpp:333-377):
+ * image_host has nu*nv doubles. */
+int xs_simulate_primary(xs_context* ctx, const xs_geometry* g, int32_t angle_idx,
+                        const xs_spectrum* spec, const xs_sim_config* cfg, double* image_host);
+
+/* REF run_scan (transport.hpp:112-116, transport.cpp:379-422).  what: 0 =
+ * primary, 1 = scatter, 2 = both (ScanQuantity order).  primary_out /
+ * scatter_out hold n_subset*nu*nv doubles (angle-major) or NULL when not
+ * requested; seconds_per_angle (n_subset) may be NULL. */
+int xs_run_scan(xs_context* ctx, const xs_geometry* g, const xs_spectrum* spec,
+                const xs_sim_config* cfg, const int32_t* angle_subset, int32_t n_subset,
+                int32_t what, double* primary_out, double* scatter_out,
+                double* seconds_per_angle);
+
+/* Device-level split of simulate_scatter_stats for photon-batch sharding
+ * across GPUs: accumulate histories [hist_begin, hist_end) of the global
+ * bin-major history order into the device buffer d_accum (layout above;
+ * the caller zeroes it once, calls may add into the same buffer).  After a
+ * sum-reduce of the buffers of all ranks, xs_scatter_finalize_device (or
+ * xs_scatter_finalize_host on a D2H copy) produces the SimResult. */
+int xs_scatter_accumulate_device(xs_context* ctx, const xs_geometry* g, int32_t angle_idx,
+                                 const xs_spectrum* spec, const xs_sim_config* cfg,
+                                 uint64_t hist_begin, uint64_t hist_end, uint64_t* d_accum);
+int xs_scatter_finalize_device(xs_context* ctx, const xs_geometry* g, const xs_spectrum* spec,
+                               const xs_sim_config* cfg, const uint64_t* d_accum,
+                               uint64_t hist_begin, uint64_t hist_end, xs_scatter_result* out,
+                               double* d_image /* optional device copy, nu*nv */);
+
+/* Deterministic primary into a device buffer (nu*nv doubles). */
+int xs_primary_device(xs_context* ctx, const xs_geometry* g, int32_t angle_idx,
+                      const xs_spectrum* spec, const xs_sim_config* cfg, double* d_image);
+
+/* Counters of the last scatter launch. */
+int xs_last_launch_stats(const xs_context* ctx, xs_launch_stats* out);
+
+/* -------------------------------------------------------- post-processing
+ * REF postprocess.hpp:17-41, batched over n_images images of one grid.
+ * device_ptrs = 0: in/out are host pointers; 1: device pointers. */
+
+/* REF sg_smooth (postprocess.cpp:124-145). */
+int xs_sg_smooth(xs_context* ctx, const double* in, double* out, int32_t nu, int32_t nv,
+                 int32_t n_images, int32_t window, int32_t polyorder, int32_t device_ptrs);
+
+/* REF interpolate_angles (postprocess.cpp:147-196): in holds n_src images at
+ * src_angles, out receives n_tgt images at tgt_angles. */
+int xs_interpolate_angles(xs_context* ctx, const double* in, const double* src_angles,
+                          int32_t n_src, double* out, const double* tgt_angles, int32_t n_tgt,
+                          int32_t nu, int32_t nv, int32_t device_ptrs);
+
+/* REF upsample_image (postprocess.cpp:235-252). */
+int xs_upsample_image(xs_context* ctx, const double* in, int32_t nu, int32_t nv,
+                      int32_t n_images, double* out, int32_t nu_out, int32_t nv_out,
+                      int32_t device_ptrs);
+
+/* REF downsample_average (postprocess.cpp:254-271). */
+int xs_downsample_average(xs_context* ctx, const double* in, int32_t nu, int32_t nv,
+                          int32_t n_images, double* out, int32_t nu_out, int32_t nv_out,
+                          int32_t device_ptrs);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* XSCAT_GPU_H */

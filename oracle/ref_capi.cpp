@@ -1,0 +1,484 @@
+// ref_capi.cpp — TEST INFRASTRUCTURE ONLY.
+//
+// Thin extern "C" shim that lets the tests and bench.py's CPU baseline call
+// the *unmodified* reference library (/root/reference/proj/src, compiled by
+// oracle/Makefile into oracle/_ref/libxscat_ref.so) with the same xs_* POD
+// structs the product C ABI takes.  Nothing here re-implements physics: each
+// entry point converts the structs to the reference types and calls the
+// reference function named in its comment.
+#include <cstdio>
+#include <cstring>
+#include <filesystem>
+#include <stdexcept>
+#include <string>
+#include <unistd.h>
+
+#include "../include/xscat_gpu.h"
+#include "support/oracles.hpp" // reference tests/support (analog oracle)
+#include "xscat/cross_sections.hpp"
+#include "xscat/material.hpp"
+#include "xscat/postprocess.hpp"
+#include "xscat/samplers.hpp"
+#include "xscat/synthetic.hpp"
+#include "xscat/trace.hpp"
+#include "xscat/transport.hpp"
+
+using namespace xscat;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F>
+int guarded(F&& f)
+{
+    try {
+        f();
+        return XS_OK;
+    } catch (const std::out_of_range& e) {
+        g_err = e.what();
+        return XS_E_OUT_OF_RANGE;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return XS_E_INVALID_ARGUMENT;
+    } catch (const std::domain_error& e) {
+        g_err = e.what();
+        return XS_E_DOMAIN;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return XS_E_RUNTIME;
+    }
+}
+
+Table1D table(const xs_table& t, const std::string& label)
+{
+    return Table1D(std::vector<double>(t.x, t.x + t.n), std::vector<double>(t.y, t.y + t.n),
+                   label);
+}
+
+// Builds a reference Material; the F^2 dq^2 CDF is private to
+// material.cpp, so the material goes through save_material/load_material
+// (exact %.17g round trip), which is also how the reference fills it.
+Material material(const xs_material& m)
+{
+    Material mm;
+    mm.name = m.name ? m.name : "material";
+    mm.z_eff = m.z_eff;
+    mm.density_ref = m.density_ref;
+    mm.mu = table(m.mu, mm.name + ".mu");
+    mm.sigma_incoh = table(m.sigma_incoh, mm.name + ".incoherent");
+    mm.sigma_coh = table(m.sigma_coh, mm.name + ".coherent");
+    mm.sigma_pe = table(m.sigma_pe, mm.name + ".photoelectric");
+    mm.s_factor = table(m.s_factor, mm.name + ".S");
+    mm.f_factor = table(m.f_factor, mm.name + ".F");
+    char path[256];
+    std::snprintf(path, sizeof path, "/tmp/xscat_ref_mat_%d_%p.mat", static_cast<int>(getpid()),
+                  static_cast<const void*>(&m));
+    save_material(mm, path);
+    Material out = load_material(path);
+    std::filesystem::remove(path);
+    return out;
+}
+
+VoxelPhantom phantom(const xs_phantom& p)
+{
+    VoxelPhantom ph;
+    ph.dims = {p.dims[0], p.dims[1], p.dims[2]};
+    ph.voxel_size = {p.voxel_size[0], p.voxel_size[1], p.voxel_size[2]};
+    ph.origin = {p.origin[0], p.origin[1], p.origin[2]};
+    const std::size_t n = ph.voxel_count();
+    ph.material_id.assign(p.material_id, p.material_id + n);
+    ph.density.assign(p.density, p.density + n);
+    ph.materials.push_back(vacuum_material());
+    for (int i = 1; i < p.n_materials; ++i)
+        ph.materials.push_back(material(p.materials[i]));
+    return ph;
+}
+
+ScanGeometry geometry(const xs_geometry& g)
+{
+    ScanGeometry s;
+    s.sdd = g.sdd;
+    s.sod = g.sod;
+    s.nu = g.nu;
+    s.nv = g.nv;
+    s.pixel_pitch = g.pixel_pitch;
+    s.angles.assign(g.angles, g.angles + g.n_angles);
+    return s;
+}
+
+Spectrum spectrum(const xs_spectrum& s)
+{
+    Spectrum out;
+    for (int i = 0; i < s.n_bins; ++i)
+        out.bins.push_back({s.energy_kev[i], s.weight[i]});
+    return out;
+}
+
+DetectorResponse response(const xs_response& r)
+{
+    return DetectorResponse{table(r.dqe, "dqe"), table(r.deposit, "deposit")};
+}
+
+SimConfig config(const xs_sim_config& c)
+{
+    SimConfig s;
+    s.photons_total = c.photons_total;
+    s.splitting = c.splitting;
+    s.roulette_survival = c.roulette_survival;
+    s.roulette_wmin_rel = c.roulette_wmin_rel;
+    s.step_voxels = c.step_voxels;
+    s.max_interactions = c.max_interactions;
+    s.seed = c.seed;
+    s.track_variance = c.track_variance != 0;
+    return s;
+}
+
+void export_phantom(const VoxelPhantom& ph, int32_t* dims, double* voxel, double* origin,
+                    uint8_t* ids, float* dens)
+{
+    for (int a = 0; a < 3; ++a)
+        dims[a] = ph.dims[a];
+    voxel[0] = ph.voxel_size.x;
+    voxel[1] = ph.voxel_size.y;
+    voxel[2] = ph.voxel_size.z;
+    origin[0] = ph.origin.x;
+    origin[1] = ph.origin.y;
+    origin[2] = ph.origin.z;
+    if (ids)
+        std::memcpy(ids, ph.material_id.data(), ph.material_id.size());
+    if (dens)
+        std::memcpy(dens, ph.density.data(), ph.density.size() * sizeof(float));
+}
+
+} // namespace
+
+extern "C" {
+
+const char* xr_last_error(void) { return g_err.c_str(); }
+
+// transport.cpp:246-324
+int xr_simulate_scatter_stats(const xs_phantom* ph, const xs_geometry* g, int32_t angle_idx,
+                              const xs_spectrum* spec, const xs_response* resp,
+                              const xs_sim_config* cfg, int32_t workers, xs_scatter_result* out)
+{
+    return guarded([&] {
+        const SimResult r = simulate_scatter_stats(phantom(*ph), geometry(*g), angle_idx,
+                                                   spectrum(*spec), response(*resp),
+                                                   config(*cfg), workers);
+        std::memcpy(out->image, r.image.values.data(), r.image.values.size() * sizeof(double));
+        if (out->variance && r.image.variance)
+            std::memcpy(out->variance, r.image.variance->data(),
+                        r.image.variance->size() * sizeof(double));
+        out->ledger = {r.ledger.initial, r.ledger.escaped,         r.ledger.absorbed,
+                       r.ledger.culled,  r.ledger.roulette_killed, r.ledger.roulette_boost};
+        out->histories = r.histories;
+        out->total = r.total;
+        out->total_std_error = r.total_std_error;
+    });
+}
+
+// Scene-cached variant for repeated timing (bench.py --impl reference): the
+// phantom/material conversion happens once, outside the timed calls.
+struct xr_scene {
+    VoxelPhantom ph;
+    DetectorResponse resp;
+};
+
+void* xr_scene_create(const xs_phantom* ph, const xs_response* resp)
+{
+    xr_scene* s = nullptr;
+    const int st = guarded([&] { s = new xr_scene{phantom(*ph), response(*resp)}; });
+    return st == XS_OK ? s : nullptr;
+}
+
+void xr_scene_destroy(void* s) { delete static_cast<xr_scene*>(s); }
+
+int xr_scene_simulate_scatter(void* scene, const xs_geometry* g, int32_t angle_idx,
+                              const xs_spectrum* spec, const xs_sim_config* cfg, int32_t workers,
+                              xs_scatter_result* out)
+{
+    const xr_scene* s = static_cast<const xr_scene*>(scene);
+    return guarded([&] {
+        const SimResult r = simulate_scatter_stats(s->ph, geometry(*g), angle_idx,
+                                                   spectrum(*spec), s->resp, config(*cfg),
+                                                   workers);
+        if (out->image)
+            std::memcpy(out->image, r.image.values.data(),
+                        r.image.values.size() * sizeof(double));
+        out->ledger = {r.ledger.initial, r.ledger.escaped,         r.ledger.absorbed,
+                       r.ledger.culled,  r.ledger.roulette_killed, r.ledger.roulette_boost};
+        out->histories = r.histories;
+        out->total = r.total;
+        out->total_std_error = r.total_std_error;
+    });
+}
+
+int xr_scene_simulate_primary(void* scene, const xs_geometry* g, int32_t angle_idx,
+                              const xs_spectrum* spec, const xs_sim_config* cfg, int32_t workers,
+                              double* image)
+{
+    const xr_scene* s = static_cast<const xr_scene*>(scene);
+    return guarded([&] {
+        const DetectorImage im = simulate_primary(s->ph, geometry(*g), angle_idx,
+                                                  spectrum(*spec), s->resp, config(*cfg),
+                                                  workers);
+        std::memcpy(image, im.values.data(), im.values.size() * sizeof(double));
+    });
+}
+
+// transport.cpp:333-377
+int xr_simulate_primary(const xs_phantom* ph, const xs_geometry* g, int32_t angle_idx,
+                        const xs_spectrum* spec, const xs_response* resp,
+                        const xs_sim_config* cfg, int32_t workers, double* image)
+{
+    return guarded([&] {
+        const DetectorImage im = simulate_primary(phantom(*ph), geometry(*g), angle_idx,
+                                                  spectrum(*spec), response(*resp),
+                                                  config(*cfg), workers);
+        std::memcpy(image, im.values.data(), im.values.size() * sizeof(double));
+    });
+}
+
+// transport.cpp:42-64
+int xr_apportion_photons(const xs_spectrum* spec, uint64_t photons_total, uint64_t* counts)
+{
+    return guarded([&] {
+        const auto c = apportion_photons(spectrum(*spec), photons_total);
+        std::memcpy(counts, c.data(), c.size() * sizeof(uint64_t));
+    });
+}
+
+// tests/support/oracles.hpp:140-228 (analog surface-crossing estimator)
+int xr_analog_scatter(const xs_phantom* ph, const xs_geometry* g, int32_t angle_idx,
+                      const xs_spectrum* spec, const xs_response* resp, uint64_t n_histories,
+                      uint64_t seed, double* image, double* total, double* se)
+{
+    return guarded([&] {
+        const auto r = testsupport::analog_scatter_oracle(phantom(*ph), geometry(*g), angle_idx,
+                                                          spectrum(*spec), response(*resp),
+                                                          n_histories, seed);
+        if (image)
+            std::memcpy(image, r.image.values.data(), r.image.values.size() * sizeof(double));
+        *total = r.total;
+        *se = r.total_std_error;
+    });
+}
+
+// tests/support/oracles.hpp:27-81
+int xr_trace_sorted_crossings(const xs_phantom* ph, const double o[3], const double d[3],
+                              double energy_kev, double* tau)
+{
+    return guarded([&] {
+        *tau = testsupport::trace_oracle_sorted_crossings(
+            phantom(*ph), Ray{{o[0], o[1], o[2]}, {d[0], d[1], d[2]}}, energy_kev);
+    });
+}
+
+// trace.cpp:107-161
+int xr_trace_attenuation(const xs_phantom* ph, const double o[3], const double d[3],
+                         double energy_kev, int32_t step_voxels, double* tau)
+{
+    return guarded([&] {
+        *tau = trace_attenuation(phantom(*ph), Ray{{o[0], o[1], o[2]}, {d[0], d[1], d[2]}},
+                                 energy_kev, step_voxels);
+    });
+}
+
+// trace.cpp:163-187
+int xr_trace_rho_lengths(const xs_phantom* ph, const double o[3], const double d[3],
+                         double* rho_len)
+{
+    return guarded([&] {
+        std::vector<double> out;
+        const VoxelPhantom p = phantom(*ph);
+        trace_rho_lengths(p, Ray{{o[0], o[1], o[2]}, {d[0], d[1], d[2]}}, out);
+        std::memcpy(rho_len, out.data(), out.size() * sizeof(double));
+    });
+}
+
+// trace.cpp:189-230
+int xr_sample_free_path(const xs_phantom* ph, const double o[3], const double d[3],
+                        double energy_kev, double u, int32_t* escaped, double point[3],
+                        int32_t voxel[3])
+{
+    return guarded([&] {
+        const FreePathResult r = sample_free_path(
+            phantom(*ph), Ray{{o[0], o[1], o[2]}, {d[0], d[1], d[2]}}, energy_kev, u);
+        *escaped = r.escaped ? 1 : 0;
+        point[0] = r.point.x;
+        point[1] = r.point.y;
+        point[2] = r.point.z;
+        voxel[0] = r.ix;
+        voxel[1] = r.iy;
+        voxel[2] = r.iz;
+    });
+}
+
+// cross_sections.cpp:56-79
+int xr_p_lambda(const xs_material* m, int32_t compton, double e, double theta, double* p)
+{
+    return guarded([&] {
+        const Material mm = material(*m);
+        *p = compton ? p_lambda_compton(mm, e, theta) : p_lambda_rayleigh(mm, e, theta);
+    });
+}
+
+// samplers.cpp:32-52 (stream of acceptance criterion 1: CounterRng(seed, 0, 0, 0))
+int xr_sample_compton(const xs_material* m, double e, uint64_t seed, int64_t n, double* theta,
+                      double* phi, double* alpha_prime)
+{
+    return guarded([&] {
+        const Material mm = material(*m);
+        CounterRng rng(seed, 0, 0, 0);
+        for (int64_t i = 0; i < n; ++i) {
+            const ComptonSample s = sample_compton(mm, e, rng);
+            theta[i] = s.theta;
+            if (phi)
+                phi[i] = s.phi;
+            if (alpha_prime)
+                alpha_prime[i] = s.alpha_prime;
+        }
+    });
+}
+
+// samplers.cpp:106-125
+int xr_sample_rayleigh(const xs_material* m, double e, uint64_t seed, int64_t n, double* theta,
+                       double* phi)
+{
+    return guarded([&] {
+        const Material mm = material(*m);
+        CounterRng rng(seed, 0, 0, 0);
+        for (int64_t i = 0; i < n; ++i) {
+            const RayleighSample s = sample_rayleigh(mm, e, rng);
+            theta[i] = s.theta;
+            if (phi)
+                phi[i] = s.phi;
+        }
+    });
+}
+
+// material.cpp:107-125 via load_material
+int xr_f2_q2_cdf(const xs_material* m, double* out)
+{
+    return guarded([&] {
+        const Material mm = material(*m);
+        std::memcpy(out, mm.f2_q2_cdf.data(), mm.f2_q2_cdf.size() * sizeof(double));
+    });
+}
+
+// rng.hpp:29-35
+void xr_rng_uniform(uint64_t seed, uint32_t angle, uint32_t bin, uint32_t photon, int64_t n,
+                    double* out)
+{
+    CounterRng rng(seed, angle, bin, photon);
+    for (int64_t i = 0; i < n; ++i)
+        out[i] = rng.uniform();
+}
+
+// postprocess.cpp:28-102
+int xr_sg_kernel(int32_t left, int32_t right, int32_t polyorder, double* out)
+{
+    return guarded([&] {
+        const auto k = sg_kernel(left, right, polyorder);
+        std::memcpy(out, k.data(), k.size() * sizeof(double));
+    });
+}
+
+int xr_default_sg_spec(int32_t nu, int32_t nv, int32_t* window, int32_t* polyorder)
+{
+    const SgFilterSpec s = default_sg_spec(nu, nv);
+    *window = s.window;
+    *polyorder = s.polyorder;
+    return XS_OK;
+}
+
+static DetectorImage image_from(const double* in, int nu, int nv)
+{
+    DetectorImage im(nu, nv);
+    std::memcpy(im.values.data(), in, im.values.size() * sizeof(double));
+    return im;
+}
+
+// postprocess.cpp:124-145
+int xr_sg_smooth(const double* in, double* out, int32_t nu, int32_t nv, int32_t window,
+                 int32_t polyorder)
+{
+    return guarded([&] {
+        const DetectorImage r = sg_smooth(image_from(in, nu, nv), SgFilterSpec{window, polyorder});
+        std::memcpy(out, r.values.data(), r.values.size() * sizeof(double));
+    });
+}
+
+// postprocess.cpp:147-196
+int xr_interpolate_angles(const double* in, const double* src, int32_t n_src, double* out,
+                          const double* tgt, int32_t n_tgt, int32_t nu, int32_t nv)
+{
+    return guarded([&] {
+        ProjectionStack s = make_stack(nu, nv, std::vector<double>(src, src + n_src));
+        const std::size_t np = static_cast<std::size_t>(nu) * nv;
+        for (int i = 0; i < n_src; ++i)
+            s.images[i] = image_from(in + i * np, nu, nv);
+        const ProjectionStack r = interpolate_angles(s, std::vector<double>(tgt, tgt + n_tgt));
+        for (int i = 0; i < n_tgt; ++i)
+            std::memcpy(out + i * np, r.images[i].values.data(), np * sizeof(double));
+    });
+}
+
+// postprocess.cpp:235-252
+int xr_upsample_image(const double* in, int32_t nu, int32_t nv, double* out, int32_t nu_out,
+                      int32_t nv_out)
+{
+    return guarded([&] {
+        const DetectorImage r = upsample_image(image_from(in, nu, nv), nu_out, nv_out);
+        std::memcpy(out, r.values.data(), r.values.size() * sizeof(double));
+    });
+}
+
+// postprocess.cpp:254-271
+int xr_downsample_average(const double* in, int32_t nu, int32_t nv, double* out,
+                          int32_t nu_out, int32_t nv_out)
+{
+    return guarded([&] {
+        const DetectorImage r = downsample_average(image_from(in, nu, nv), nu_out, nv_out);
+        std::memcpy(out, r.values.data(), r.values.size() * sizeof(double));
+    });
+}
+
+// synthetic.cpp:101-178: phantom generators, to pin the host-side fixtures.
+// kind 0 cube(edge), 1 cylinder(radius, height), 2 rods(body_r, height,
+// n_rods, rod_r, ring_r, rod_density), 3 cylinder_head(insert_density).
+int xr_make_phantom(int32_t kind, int32_t n, double voxel_cm, const double* params,
+                    double density, int32_t* dims, double* voxel, double* origin, uint8_t* ids,
+                    float* dens)
+{
+    return guarded([&] {
+        Material m;
+        m.name = "m";
+        m.z_eff = 1;
+        m.density_ref = 1;
+        m.mu = Table1D({1.0, 2.0}, {1.0, 1.0});
+        Material m2 = m;
+        m2.name = "m2";
+        VoxelPhantom ph;
+        switch (kind) {
+        case 0:
+            ph = make_cube_phantom(n, voxel_cm, params[0], m, density);
+            break;
+        case 1:
+            ph = make_cylinder_phantom(n, voxel_cm, params[0], params[1], m, density);
+            break;
+        case 2:
+            ph = make_rods_phantom(n, voxel_cm, params[0], params[1], m, density,
+                                   static_cast<int>(params[2]), params[3], params[4], m2,
+                                   params[5]);
+            break;
+        default:
+            ph = make_cylinder_head_phantom(n, voxel_cm, m, density, m2, params[0]);
+            break;
+        }
+        export_phantom(ph, dims, voxel, origin, ids, dens);
+    });
+}
+
+} // extern "C"
