@@ -1,0 +1,1060 @@
+// capi.cu — the extern "C" boundary of libxscatgpu.so (include/xscat_gpu.h).
+//
+// Owns a per-device context (stream, device buffers, uploaded scene), the
+// re-encoding of the phantom into the device voxel format, kernel launches,
+// and the mapping of device error records to REF's exception types/messages.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "host_common.h"
+#include "xs_types.h"
+
+namespace xsd {
+cudaError_t launch_transport(const TransportParams& P, int grid, int block, size_t smem, cudaStream_t s);
+cudaError_t transport_set_smem(size_t smem);
+cudaError_t transport_occupancy(int fmt, int block, size_t smem, int* blocks_per_sm);
+cudaError_t launch_primary(const PrimaryParams& P, cudaStream_t s);
+cudaError_t launch_finalize_image(const unsigned long long* acc, uint64_t off_image, uint64_t off_var,
+                                  uint64_t npix, int log2_img, double n_hist, int track_var,
+                                  double* image, double* var, cudaStream_t s);
+cudaError_t launch_sg(const double* in, double* tmp, double* out, int nu, int nv, int n_images,
+                      int half, const double* K, cudaStream_t s);
+cudaError_t launch_interp(const double* in, double* out, const InterpEntry* tab, int n_tgt,
+                          size_t npix, cudaStream_t s);
+cudaError_t launch_upsample(const double* in, double* tmp, double* out, int nu, int nv,
+                            int n_images, int nu_out, int nv_out, cudaStream_t s);
+cudaError_t launch_downsample(const double* in, double* out, int nu, int nv, int n_images,
+                              int nu_out, int nv_out, cudaStream_t s);
+} // namespace xsd
+
+using xsh::Error;
+using xsh::fail;
+
+namespace {
+
+constexpr double kPi = 3.14159265358979323846;
+
+void cuda_check(cudaError_t e, const char* what)
+{
+    if (e != cudaSuccess)
+        fail(XS_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+// Growable device buffer.
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    void reserve(size_t count)
+    {
+        if (count <= n && p)
+            return;
+        if (p)
+            cudaFree(p);
+        p = nullptr;
+        n = 0;
+        cuda_check(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)), "cudaMalloc");
+        n = count;
+    }
+    void release()
+    {
+        if (p)
+            cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+
+// Host copy of a table (the C-ABI inputs are borrowed pointers).
+struct HTab {
+    std::vector<double> x, y;
+    xs_table view() const { return xs_table{static_cast<int32_t>(x.size()), x.data(), y.data()}; }
+    void set(const xs_table& t)
+    {
+        x.assign(t.x, t.x + std::max(t.n, 0));
+        y.assign(t.y, t.y + std::max(t.n, 0));
+    }
+};
+
+struct HMat {
+    std::string name;
+    double z_eff = 0, density_ref = 0;
+    HTab t[6];
+    xs_material view() const
+    {
+        xs_material m;
+        m.name = name.c_str();
+        m.z_eff = z_eff;
+        m.density_ref = density_ref;
+        m.mu = t[0].view();
+        m.sigma_incoh = t[1].view();
+        m.sigma_coh = t[2].view();
+        m.sigma_pe = t[3].view();
+        m.s_factor = t[4].view();
+        m.f_factor = t[5].view();
+        return m;
+    }
+};
+
+} // namespace
+
+struct xs_context {
+    int device = 0;
+    int sm_count = 148;
+    cudaStream_t own = nullptr, stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    std::string err;
+
+    // scene
+    bool have_phantom = false, have_response = false;
+    xsd::Grid grid{};
+    int n_mats = 0;
+    std::vector<HMat> mats;
+    HTab resp_dqe, resp_dep;
+    xsd::MatDesc mat_desc[xsd::kMaxMaterials]{};
+    xsd::TabDesc resp_desc{};
+    int n_pal = 0;
+    uint8_t pal_mat[xsd::kMaxPalette]{};
+    float pal_dens[xsd::kMaxPalette]{};
+    DevBuf<uint8_t> vox;
+    DevBuf<float> dens;
+    DevBuf<double> tabs;
+
+    // scratch
+    DevBuf<unsigned long long> accum;
+    DevBuf<uint64_t> bin_start, bin_count;
+    DevBuf<double> bin_e, bin_w, prim_atten, prim_w, prim_resp;
+    DevBuf<unsigned long long> pool;
+    DevBuf<xsd::DevStatus> status;
+    DevBuf<uint32_t> var_pix;
+    DevBuf<double> var_val;
+    DevBuf<double> img, var, pp_a, pp_b, pp_c, pp_k;
+    DevBuf<xsd::InterpEntry> interp_tab;
+    size_t smem_attr = 0;
+
+    xs_launch_stats last{};
+    int walk_thresh = 8;
+    int grab = 64;
+};
+
+namespace {
+
+// --------------------------------------------------------------- plumbing
+template <typename F>
+int guard(xs_context* ctx, F&& f)
+{
+    try {
+        if (ctx)
+            cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        f();
+        return XS_OK;
+    } catch (const Error& e) {
+        if (ctx)
+            ctx->err = e.msg;
+        return xsh::set_error(e.code, e.msg);
+    } catch (const std::exception& e) {
+        if (ctx)
+            ctx->err = e.what();
+        return xsh::set_error(XS_E_RUNTIME, e.what());
+    }
+}
+
+void rebuild_tables(xs_context* c)
+{
+    std::vector<double> buf;
+    std::vector<xs_material> views(c->mats.size());
+    for (size_t i = 0; i < c->mats.size(); ++i)
+        views[i] = c->mats[i].view();
+    if (!views.empty())
+        xsh::pack_materials(views.data(), static_cast<int>(views.size()), buf, c->mat_desc);
+    if (c->have_response)
+        c->resp_desc = xsh::pack_table(c->resp_dep.view(), buf);
+    if (buf.empty())
+        buf.push_back(0.0);
+    c->tabs.reserve(buf.size());
+    cuda_check(cudaMemcpyAsync(c->tabs.p, buf.data(), buf.size() * sizeof(double),
+                               cudaMemcpyHostToDevice, c->stream),
+               "upload tables");
+    cuda_check(cudaStreamSynchronize(c->stream), "upload tables");
+}
+
+void require_scene(const xs_context* c)
+{
+    if (!c->have_phantom)
+        fail(XS_E_RUNTIME, "xscat-gpu: no phantom uploaded (xs_upload_phantom)");
+    if (!c->have_response)
+        fail(XS_E_RUNTIME, "xscat-gpu: no detector response uploaded (xs_upload_response)");
+}
+
+void check_angle(const xs_geometry& g, int angle_idx, const char* who)
+{
+    if (angle_idx < 0 || angle_idx >= g.n_angles)
+        fail(XS_E_OUT_OF_RANGE, "%s: angle index out of range", who);
+}
+
+// Maps the device error record onto REF's exception type + message.
+void check_status(xs_context* c, int angle_idx, const xs_spectrum* spec)
+{
+    xsd::DevStatus s;
+    cuda_check(cudaMemcpyAsync(&s, c->status.p, sizeof s, cudaMemcpyDeviceToHost, c->stream),
+               "status readback");
+    cuda_check(cudaStreamSynchronize(c->stream), "kernel execution");
+    if (s.code == 0)
+        return;
+    const double e = s.energy;
+    switch (s.what) {
+    case xsd::kErrNonFinite:
+        fail(XS_E_RUNTIME,
+             "simulate_scatter: non-finite contribution (angle %d, bin %d, E %f keV) - physics "
+             "tables corrupt?",
+             angle_idx, s.bin, e);
+    case xsd::kErrTableRange:
+        fail(XS_E_OUT_OF_RANGE, "table: query %f outside the tabulated range", e);
+    case xsd::kErrTallyOverflow:
+        fail(XS_E_RUNTIME, "simulate_scatter: fixed-point tally overflow (value %g)", s.value);
+    case xsd::kErrSigmaIncoh:
+        fail(XS_E_RUNTIME, "p_lambda_compton: vanishing incoherent cross section at %f keV", e);
+    case xsd::kErrSigmaCoh:
+        fail(XS_E_RUNTIME, "p_lambda_rayleigh: vanishing coherent cross section at %f keV", e);
+    case xsd::kErrSigmaAll: {
+        const int m = static_cast<int>(s.value);
+        fail(XS_E_RUNTIME, "select_interaction: all cross sections vanish at %f keV in %s", e,
+             (m >= 0 && m < (int)c->mats.size()) ? c->mats[m].name.c_str() : "?");
+    }
+    case xsd::kErrComptonS:
+        fail(XS_E_RUNTIME, "sample_compton: S vanishes over the kinematic range at %f keV", e);
+    case xsd::kErrRayleighF:
+        fail(XS_E_RUNTIME, "sample_rayleigh: F vanishes over the kinematic range at %f keV", e);
+    default:
+        if (s.code == XS_E_INVALID_ARGUMENT)
+            fail(XS_E_INVALID_ARGUMENT, "trace: non-finite ray");
+        fail(s.code, "device error %d", s.what);
+    }
+    (void)spec;
+}
+
+// ------------------------------------------------------ phantom encoding
+struct PairKey {
+    uint8_t id;
+    uint32_t dens_bits;
+    bool operator==(const PairKey& o) const { return id == o.id && dens_bits == o.dens_bits; }
+    bool operator<(const PairKey& o) const
+    {
+        return id != o.id ? id < o.id : dens_bits < o.dens_bits;
+    }
+};
+
+struct ScanResult {
+    size_t first_bad = SIZE_MAX;
+    int bad_code = 0;
+    std::string bad_msg;
+    std::vector<PairKey> pairs; // up to 257 distinct
+};
+
+// REF validate_phantom (phantom.cpp:33-56) fused with palette discovery.
+void scan_phantom(const xs_phantom& ph, const std::vector<int>& has_tables, ScanResult& out)
+{
+    const size_t n = (size_t)ph.dims[0] * ph.dims[1] * ph.dims[2];
+    const unsigned nt = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    std::vector<ScanResult> part(nt);
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < nt; ++t)
+        th.emplace_back([&, t] {
+            ScanResult& r = part[t];
+            const size_t b = n * t / nt, e = n * (t + 1) / nt;
+            PairKey last{255, 0xFFFFFFFFu};
+            bool have_last = false;
+            for (size_t i = b; i < e; ++i) {
+                const uint8_t id = ph.material_id[i];
+                const float d = ph.density[i];
+                uint32_t bits;
+                std::memcpy(&bits, &d, 4);
+                if (have_last && last.id == id && last.dens_bits == bits)
+                    continue;
+                if (id >= ph.n_materials) {
+                    r.first_bad = i;
+                    r.bad_code = 1;
+                    r.bad_msg = "phantom: material id " + std::to_string(id) + " has no loaded material";
+                    return;
+                }
+                if (id != 0 && !has_tables[id]) {
+                    r.first_bad = i;
+                    r.bad_msg = "phantom: material id " + std::to_string(id) + " (" +
+                                std::string(ph.materials[id].name ? ph.materials[id].name : "?") +
+                                ") has no tables";
+                    return;
+                }
+                if (!(d >= 0.0f)) {
+                    r.first_bad = i;
+                    r.bad_msg = "phantom: negative density";
+                    return;
+                }
+                if (id == 0 && d != 0.0f) {
+                    r.first_bad = i;
+                    r.bad_msg = "phantom: vacuum voxel with nonzero density";
+                    return;
+                }
+                const PairKey k{id, bits};
+                last = k;
+                have_last = true;
+                if (r.pairs.size() <= (size_t)xsd::kMaxPalette &&
+                    std::find(r.pairs.begin(), r.pairs.end(), k) == r.pairs.end())
+                    r.pairs.push_back(k);
+            }
+        });
+    for (auto& t : th)
+        t.join();
+    for (auto& r : part) {
+        if (r.first_bad < out.first_bad) {
+            out.first_bad = r.first_bad;
+            out.bad_msg = r.bad_msg;
+        }
+        for (const auto& k : r.pairs)
+            if (out.pairs.size() <= (size_t)xsd::kMaxPalette &&
+                std::find(out.pairs.begin(), out.pairs.end(), k) == out.pairs.end())
+                out.pairs.push_back(k);
+    }
+    std::sort(out.pairs.begin(), out.pairs.end());
+}
+
+// Re-encodes the x-fastest grid into 4x4x4 bricks (P4 nibbles / P8 bytes /
+// raw id + density), parallel over brick layers.
+void encode_phantom(const xs_phantom& ph, int fmt, const std::vector<PairKey>& pal,
+                    std::vector<uint8_t>& vox, std::vector<float>& dens, int nbx, int nby, int nbz)
+{
+    const int nx = ph.dims[0], ny = ph.dims[1], nz = ph.dims[2];
+    const size_t n_bricks = (size_t)nbx * nby * nbz;
+    if (fmt == xsd::kFmtP4)
+        vox.assign(n_bricks * 32, 0);
+    else
+        vox.assign(n_bricks * 64, 0);
+    if (fmt == xsd::kFmtRaw)
+        dens.assign(n_bricks * 64, 0.0f);
+    const unsigned nt = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    std::atomic<int> next{0};
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < nt; ++t)
+        th.emplace_back([&] {
+            for (;;) {
+                const int bz = next.fetch_add(1);
+                if (bz >= nbz)
+                    return;
+                PairKey last{255, 0xFFFFFFFFu};
+                int last_code = 0;
+                for (int z = bz * 4; z < std::min(nz, bz * 4 + 4); ++z)
+                    for (int y = 0; y < ny; ++y)
+                        for (int x = 0; x < nx; ++x) {
+                            const size_t src = (size_t)x + (size_t)nx * ((size_t)y + (size_t)ny * z);
+                            const size_t brick =
+                                (size_t)(x >> 2) + (size_t)nbx * ((size_t)(y >> 2) + (size_t)nby * (z >> 2));
+                            const size_t cell =
+                                (brick << 6) | (size_t)((x & 3) | ((y & 3) << 2) | ((z & 3) << 4));
+                            const uint8_t id = ph.material_id[src];
+                            if (fmt == xsd::kFmtRaw) {
+                                vox[cell] = id;
+                                dens[cell] = ph.density[src];
+                                continue;
+                            }
+                            uint32_t bits;
+                            std::memcpy(&bits, &ph.density[src], 4);
+                            int code = last_code;
+                            if (!(last.id == id && last.dens_bits == bits)) {
+                                const PairKey k{id, bits};
+                                code = (int)(std::lower_bound(pal.begin(), pal.end(), k) - pal.begin());
+                                last = k;
+                                last_code = code;
+                            }
+                            if (fmt == xsd::kFmtP4)
+                                vox[cell >> 1] |= (uint8_t)(code << ((cell & 1) * 4));
+                            else
+                                vox[cell] = (uint8_t)code;
+                        }
+            }
+        });
+    for (auto& t : th)
+        t.join();
+}
+
+// --------------------------------------------------------- scatter launch
+struct Plan {
+    std::vector<uint64_t> counts, start;
+    xs_accum_units units;
+    xs_accum_layout layout;
+    uint64_t n_hist;
+};
+
+Plan make_plan(const xs_geometry& g, const xs_spectrum& spec, const xs_sim_config& cfg)
+{
+    Plan p;
+    if (spec.n_bins > xsd::kMaxBins)
+        fail(XS_E_UNSUPPORTED, "xscat-gpu: at most %d spectrum bins supported", xsd::kMaxBins);
+    p.counts = xsh::apportion(spec, cfg.photons_total);
+    p.start.resize(spec.n_bins + 1);
+    p.start[0] = 0;
+    for (int b = 0; b < spec.n_bins; ++b)
+        p.start[b + 1] = p.start[b] + p.counts[b];
+    p.n_hist = p.start[spec.n_bins];
+    p.units = xs_accum_units_make(&g, &spec, p.counts.data());
+    p.layout = xs_accum_layout_make(g.nu, g.nv, spec.n_bins, cfg.track_variance);
+    return p;
+}
+
+void validate_call(const xs_geometry& g, int angle, const xs_spectrum& spec,
+                   const xs_sim_config& cfg, const char* who)
+{
+    xsh::validate_sim_config(cfg);
+    xsh::validate_spectrum(spec);
+    xsh::validate_geometry(g);
+    check_angle(g, angle, who);
+}
+
+void accumulate(xs_context* c, const xs_geometry& g, int angle, const xs_spectrum& spec,
+                const xs_sim_config& cfg, uint64_t h0, uint64_t h1, unsigned long long* d_accum)
+{
+    require_scene(c);
+    const Plan plan = make_plan(g, spec, cfg);
+    if (h1 > plan.n_hist)
+        h1 = plan.n_hist;
+    if (h0 >= h1) {
+        c->last = xs_launch_stats{};
+        return;
+    }
+    const int nb = spec.n_bins;
+    c->bin_start.reserve(nb + 1);
+    c->bin_count.reserve(nb);
+    c->bin_e.reserve(nb);
+    c->bin_w.reserve(nb);
+    c->pool.reserve(1);
+    c->status.reserve(1);
+    cudaStream_t s = c->stream;
+    cuda_check(cudaMemcpyAsync(c->bin_start.p, plan.start.data(), (nb + 1) * 8, cudaMemcpyHostToDevice, s), "H2D");
+    cuda_check(cudaMemcpyAsync(c->bin_count.p, plan.counts.data(), nb * 8, cudaMemcpyHostToDevice, s), "H2D");
+    cuda_check(cudaMemcpyAsync(c->bin_e.p, spec.energy_kev, nb * 8, cudaMemcpyHostToDevice, s), "H2D");
+    cuda_check(cudaMemcpyAsync(c->bin_w.p, spec.weight, nb * 8, cudaMemcpyHostToDevice, s), "H2D");
+    cuda_check(cudaMemsetAsync(c->pool.p, 0, 8, s), "memset");
+    cuda_check(cudaMemsetAsync(c->status.p, 0, sizeof(xsd::DevStatus), s), "memset");
+
+    xsd::TransportParams P;
+    std::memset(&P, 0, sizeof P);
+    P.G = c->grid;
+    P.tabs = c->tabs.p;
+    P.n_mats = c->n_mats;
+    P.n_pal = c->n_pal;
+    std::memcpy(P.mats, c->mat_desc, sizeof P.mats);
+    std::memcpy(P.pal_mat, c->pal_mat, sizeof P.pal_mat);
+    std::memcpy(P.pal_dens, c->pal_dens, sizeof P.pal_dens);
+    P.resp_deposit = c->resp_desc;
+    const xsh::Frame f = xsh::frame_of(g, angle);
+    for (int a = 0; a < 3; ++a) {
+        P.src[a] = f.src[a];
+        P.center[a] = f.center[a];
+        P.uaxis[a] = f.uaxis[a];
+        P.normal[a] = f.normal[a];
+    }
+    P.nu = g.nu;
+    P.nv = g.nv;
+    P.pitch = g.pixel_pitch;
+    P.det_area = g.nu * g.nv * g.pixel_pitch * g.pixel_pitch; // REF detector_area()
+    P.n_pixels = static_cast<double>(g.nu) * g.nv;
+    P.n_bins = nb;
+    P.bin_energy = c->bin_e.p;
+    P.bin_weight = c->bin_w.p;
+    P.bin_start = c->bin_start.p;
+    P.bin_count = c->bin_count.p;
+    P.k0 = static_cast<uint32_t>(cfg.seed);
+    P.k1 = static_cast<uint32_t>(cfg.seed >> 32);
+    P.angle = static_cast<uint32_t>(angle);
+    P.splitting = cfg.splitting;
+    P.survival = cfg.roulette_survival;
+    P.wmin_rel = cfg.roulette_wmin_rel;
+    P.step_voxels = cfg.step_voxels;
+    P.max_inter = cfg.max_interactions;
+    P.track_var = cfg.track_variance ? 1 : 0;
+    P.march_h = cfg.step_voxels *
+                std::min({c->grid.hx, c->grid.hy, c->grid.hz}); // REF trace.cpp:117
+    P.accum = d_accum;
+    P.off_image = plan.layout.off_image;
+    P.off_var = plan.layout.off_variance;
+    P.off_bins = plan.layout.off_bins;
+    P.off_ledger = plan.layout.off_ledger;
+    P.off_diag = plan.layout.off_diag;
+    P.log2_img = plan.units.log2_img;
+    P.log2_w = plan.units.log2_w;
+    P.h_begin = h0;
+    P.h_end = h1;
+    P.pool = c->pool.p;
+    P.grab = c->grab;
+    P.walk_thresh = c->walk_thresh;
+    P.status = c->status.p;
+
+    const int block = 256;
+    const int n_tab = c->grid.fmt == xsd::kFmtP4 ? c->n_pal : c->n_mats;
+    const size_t smem = (size_t)n_tab * block * 8 + (size_t)(8 * nb + 32) * 8 + (size_t)(nb + 1) * 8;
+    if (smem > c->smem_attr) {
+        cuda_check(xsd::transport_set_smem(std::max<size_t>(smem, 48 * 1024)), "smem attribute");
+        c->smem_attr = std::max<size_t>(smem, 48 * 1024);
+    }
+    int per_sm = 0;
+    cuda_check(xsd::transport_occupancy(c->grid.fmt, block, smem, &per_sm), "occupancy");
+    per_sm = std::max(per_sm, 1);
+    int grid = c->sm_count * per_sm;
+    // no more threads than histories (small launches)
+    const uint64_t n = h1 - h0;
+    if ((uint64_t)grid * block > n)
+        grid = (int)std::max<uint64_t>(1, (n + block - 1) / block);
+    if (cfg.track_variance) {
+        const uint64_t cap = (uint64_t)cfg.splitting * (uint64_t)cfg.max_interactions;
+        if (cap > (1u << 20))
+            fail(XS_E_UNSUPPORTED, "xscat-gpu: splitting*max_interactions too large for variance tracking");
+        P.var_cap = (int32_t)cap;
+        c->var_pix.reserve((size_t)grid * block * cap);
+        c->var_val.reserve((size_t)grid * block * cap);
+        P.var_pix = c->var_pix.p;
+        P.var_val = c->var_val.p;
+    }
+    cuda_check(cudaEventRecord(c->ev0, s), "event");
+    cuda_check(xsd::launch_transport(P, grid, block, smem, s), "transport launch");
+    cuda_check(cudaEventRecord(c->ev1, s), "event");
+    check_status(c, angle, &spec);
+    float ms = 0.f;
+    cuda_check(cudaEventElapsedTime(&ms, c->ev0, c->ev1), "event time");
+    c->last.kernel_ms = ms;
+    c->last.voxel_format = c->grid.fmt;
+    c->last.palette_size = c->n_pal;
+}
+
+void finalize(xs_context* c, const xs_geometry& g, const xs_spectrum& spec, const xs_sim_config& cfg,
+              const unsigned long long* d_accum, uint64_t h0, uint64_t h1, xs_scatter_result* out,
+              double* d_image)
+{
+    const Plan plan = make_plan(g, spec, cfg);
+    if (h1 > plan.n_hist)
+        h1 = plan.n_hist;
+    const xs_accum_layout& L = plan.layout;
+    cudaStream_t s = c->stream;
+    // statistics words (bins, ledger, diag) -> host
+    const size_t tail = L.words - L.off_bins;
+    std::vector<uint64_t> stats(tail);
+    cuda_check(cudaMemcpyAsync(stats.data(), d_accum + L.off_bins, tail * 8, cudaMemcpyDeviceToHost, s),
+               "D2H stats");
+    cuda_check(cudaStreamSynchronize(s), "D2H stats");
+    xsh::finalize_stats(spec, plan.counts, h0, h1, stats.data(), stats.data() + (L.off_ledger - L.off_bins),
+                        plan.units, out);
+    const uint64_t* diag = stats.data() + (L.off_diag - L.off_bins);
+    c->last.free_path_steps = diag[0];
+    c->last.scoring_steps = diag[1];
+    c->last.histories = diag[2];
+    c->last.scoring_rays = diag[3];
+    c->last.interactions = diag[4];
+
+    double* img = d_image;
+    if (!img) {
+        c->img.reserve(L.n_pixels);
+        img = c->img.p;
+    }
+    double* var = nullptr;
+    if (cfg.track_variance) {
+        c->var.reserve(L.n_pixels);
+        var = c->var.p;
+    }
+    cuda_check(xsd::launch_finalize_image(d_accum, L.off_image, L.off_variance, L.n_pixels,
+                                          plan.units.log2_img, static_cast<double>(out->histories),
+                                          cfg.track_variance, img, var, s),
+               "finalize launch");
+    if (out->image)
+        cuda_check(cudaMemcpyAsync(out->image, img, L.n_pixels * 8, cudaMemcpyDeviceToHost, s), "D2H image");
+    if (var && out->variance)
+        cuda_check(cudaMemcpyAsync(out->variance, var, L.n_pixels * 8, cudaMemcpyDeviceToHost, s),
+                   "D2H variance");
+    cuda_check(cudaStreamSynchronize(s), "finalize");
+}
+
+void primary(xs_context* c, const xs_geometry& g, int angle, const xs_spectrum& spec, double* d_image)
+{
+    require_scene(c);
+    const int nb = spec.n_bins, nm = c->n_mats;
+    // REF simulate_primary :343-353 (host glibc loglog, exactly REF's values)
+    std::vector<double> atten((size_t)nb * nm, 0.0), w(nb), resp(nb);
+    for (int b = 0; b < nb; ++b) {
+        resp[b] = xsh::linear(c->resp_dep.view(), spec.energy_kev[b]) / spec.energy_kev[b];
+        w[b] = spec.weight[b];
+        for (int m = 1; m < nm; ++m)
+            if (!c->mats[m].t[0].x.empty())
+                atten[(size_t)b * nm + m] = xsh::loglog(c->mats[m].t[0].view(), spec.energy_kev[b]);
+    }
+    c->prim_atten.reserve(atten.size());
+    c->prim_w.reserve(nb);
+    c->prim_resp.reserve(nb);
+    cudaStream_t s = c->stream;
+    cuda_check(cudaMemcpyAsync(c->prim_atten.p, atten.data(), atten.size() * 8, cudaMemcpyHostToDevice, s), "H2D");
+    cuda_check(cudaMemcpyAsync(c->prim_w.p, w.data(), nb * 8, cudaMemcpyHostToDevice, s), "H2D");
+    cuda_check(cudaMemcpyAsync(c->prim_resp.p, resp.data(), nb * 8, cudaMemcpyHostToDevice, s), "H2D");
+    xsd::PrimaryParams P;
+    std::memset(&P, 0, sizeof P);
+    P.G = c->grid;
+    P.n_mats = nm;
+    P.n_pal = c->n_pal;
+    std::memcpy(P.pal_mat, c->pal_mat, sizeof P.pal_mat);
+    std::memcpy(P.pal_dens, c->pal_dens, sizeof P.pal_dens);
+    const xsh::Frame f = xsh::frame_of(g, angle);
+    for (int a = 0; a < 3; ++a) {
+        P.src[a] = f.src[a];
+        P.center[a] = f.center[a];
+        P.uaxis[a] = f.uaxis[a];
+    }
+    P.nu = g.nu;
+    P.nv = g.nv;
+    P.pitch = g.pixel_pitch;
+    P.n_bins = nb;
+    P.atten = c->prim_atten.p;
+    P.wresp = c->prim_w.p;
+    P.response = c->prim_resp.p;
+    P.image = d_image;
+    cuda_check(xsd::launch_primary(P, s), "primary launch");
+    cuda_check(cudaStreamSynchronize(s), "primary");
+}
+
+} // namespace
+
+// ========================================================== extern "C"
+extern "C" {
+
+const char* xs_last_error(const xs_context* ctx)
+{
+    return ctx ? ctx->err.c_str() : xsh::thread_error();
+}
+
+int xs_device_count(int32_t* n)
+{
+    return guard(nullptr, [&] {
+        int c = 0;
+        cuda_check(cudaGetDeviceCount(&c), "cudaGetDeviceCount");
+        *n = c;
+    });
+}
+
+int xs_ctx_create(int32_t device, xs_context** out)
+{
+    *out = nullptr;
+    return guard(nullptr, [&] {
+        int n = 0;
+        cuda_check(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+        if (device < 0 || device >= n)
+            fail(XS_E_OUT_OF_RANGE, "xs_ctx_create: device %d out of range (%d devices)", device, n);
+        cuda_check(cudaSetDevice(device), "cudaSetDevice");
+        auto* c = new xs_context();
+        c->device = device;
+        cudaDeviceProp prop;
+        cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+        c->sm_count = prop.multiProcessorCount;
+        cuda_check(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking), "stream");
+        c->stream = c->own;
+        cuda_check(cudaEventCreate(&c->ev0), "event");
+        cuda_check(cudaEventCreate(&c->ev1), "event");
+        if (const char* e = std::getenv("XSCAT_WALK_THRESH"))
+            c->walk_thresh = std::max(1, std::min(32, std::atoi(e)));
+        if (const char* e = std::getenv("XSCAT_GRAB"))
+            c->grab = std::max(1, std::atoi(e));
+        *out = c;
+    });
+}
+
+void xs_ctx_destroy(xs_context* c)
+{
+    if (!c)
+        return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    for (auto* b : {&c->img, &c->var, &c->pp_a, &c->pp_b, &c->pp_c, &c->pp_k, &c->bin_e, &c->bin_w,
+                    &c->prim_atten, &c->prim_w, &c->prim_resp, &c->tabs, &c->var_val})
+        b->release();
+    c->vox.release();
+    c->dens.release();
+    c->accum.release();
+    c->bin_start.release();
+    c->bin_count.release();
+    c->pool.release();
+    c->status.release();
+    c->var_pix.release();
+    c->interp_tab.release();
+    if (c->ev0)
+        cudaEventDestroy(c->ev0);
+    if (c->ev1)
+        cudaEventDestroy(c->ev1);
+    if (c->own)
+        cudaStreamDestroy(c->own);
+    delete c;
+}
+
+int xs_ctx_set_stream(xs_context* c, void* stream)
+{
+    return guard(c, [&] { c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own; });
+}
+
+int xs_ctx_synchronize(xs_context* c)
+{
+    return guard(c, [&] { cuda_check(cudaStreamSynchronize(c->stream), "synchronize"); });
+}
+
+int xs_upload_phantom(xs_context* c, const xs_phantom* ph)
+{
+    return guard(c, [&] {
+        if (ph->dims[0] <= 0 || ph->dims[1] <= 0 || ph->dims[2] <= 0)
+            fail(XS_E_RUNTIME, "phantom: dims must be positive");
+        if (!(ph->voxel_size[0] > 0.0 && ph->voxel_size[1] > 0.0 && ph->voxel_size[2] > 0.0))
+            fail(XS_E_RUNTIME, "phantom: voxel size must be positive");
+        if (ph->n_materials <= 0 || !ph->materials)
+            fail(XS_E_RUNTIME, "phantom: no material table");
+        if (ph->n_materials > xsd::kMaxMaterials)
+            fail(XS_E_UNSUPPORTED, "xscat-gpu: at most %d materials (incl. vacuum) supported",
+                 xsd::kMaxMaterials);
+        const size_t nvox = (size_t)ph->dims[0] * ph->dims[1] * ph->dims[2];
+        if (nvox > (size_t)1 << 32)
+            fail(XS_E_UNSUPPORTED, "xscat-gpu: at most 2^32 voxels supported");
+        std::vector<int> has_tables(ph->n_materials, 0);
+        for (int m = 1; m < ph->n_materials; ++m)
+            has_tables[m] = ph->materials[m].mu.n > 0;
+        ScanResult scan;
+        scan_phantom(*ph, has_tables, scan);
+        if (scan.first_bad != SIZE_MAX)
+            fail(XS_E_RUNTIME, "%s", scan.bad_msg.c_str());
+
+        const int n_pairs = (int)scan.pairs.size();
+        const int fmt = n_pairs <= 16 ? xsd::kFmtP4 : (n_pairs <= 256 ? xsd::kFmtP8 : xsd::kFmtRaw);
+        xsd::Grid G{};
+        G.nx = ph->dims[0];
+        G.ny = ph->dims[1];
+        G.nz = ph->dims[2];
+        G.nbx = (G.nx + 3) / 4;
+        G.nby = (G.ny + 3) / 4;
+        G.nbz = (G.nz + 3) / 4;
+        G.ox = ph->origin[0];
+        G.oy = ph->origin[1];
+        G.oz = ph->origin[2];
+        G.hx = ph->voxel_size[0];
+        G.hy = ph->voxel_size[1];
+        G.hz = ph->voxel_size[2];
+        G.ihx = 1.0 / G.hx;
+        G.ihy = 1.0 / G.hy;
+        G.ihz = 1.0 / G.hz;
+        // REF VoxelPhantom::extent: dims * voxel_size, then origin + extent
+        G.ux = G.ox + G.nx * G.hx;
+        G.uy = G.oy + G.ny * G.hy;
+        G.uz = G.oz + G.nz * G.hz;
+        G.fmt = fmt;
+        G.n_codes = fmt == xsd::kFmtRaw ? 0 : n_pairs;
+
+        std::vector<uint8_t> vox;
+        std::vector<float> dens;
+        encode_phantom(*ph, fmt, scan.pairs, vox, dens, G.nbx, G.nby, G.nbz);
+
+        c->n_pal = fmt == xsd::kFmtRaw ? 0 : n_pairs;
+        std::memset(c->pal_mat, 0, sizeof c->pal_mat);
+        std::memset(c->pal_dens, 0, sizeof c->pal_dens);
+        for (int k = 0; k < c->n_pal; ++k) {
+            c->pal_mat[k] = scan.pairs[k].id;
+            std::memcpy(&c->pal_dens[k], &scan.pairs[k].dens_bits, 4);
+        }
+        c->vox.reserve(vox.size());
+        cuda_check(cudaMemcpyAsync(c->vox.p, vox.data(), vox.size(), cudaMemcpyHostToDevice, c->stream),
+                   "upload voxels");
+        if (fmt == xsd::kFmtRaw) {
+            c->dens.reserve(dens.size());
+            cuda_check(cudaMemcpyAsync(c->dens.p, dens.data(), dens.size() * 4, cudaMemcpyHostToDevice,
+                                       c->stream),
+                       "upload densities");
+        }
+        cuda_check(cudaStreamSynchronize(c->stream), "upload phantom");
+        G.vox = c->vox.p;
+        G.dens = fmt == xsd::kFmtRaw ? c->dens.p : nullptr;
+        c->grid = G;
+        c->n_mats = ph->n_materials;
+        c->mats.assign(ph->n_materials, HMat{});
+        for (int m = 0; m < ph->n_materials; ++m) {
+            const xs_material& src = ph->materials[m];
+            HMat& d = c->mats[m];
+            d.name = src.name ? src.name : (m == 0 ? "vacuum" : "?");
+            d.z_eff = src.z_eff;
+            d.density_ref = src.density_ref;
+            if (m == 0 || src.mu.n <= 0)
+                continue;
+            d.t[0].set(src.mu);
+            d.t[1].set(src.sigma_incoh);
+            d.t[2].set(src.sigma_coh);
+            d.t[3].set(src.sigma_pe);
+            d.t[4].set(src.s_factor);
+            d.t[5].set(src.f_factor);
+        }
+        rebuild_tables(c);
+        c->have_phantom = true;
+    });
+}
+
+int xs_upload_response(xs_context* c, const xs_response* r)
+{
+    return guard(c, [&] {
+        if (r->dqe.n <= 0 || r->deposit.n <= 0)
+            fail(XS_E_RUNTIME, "detector response: empty table");
+        c->resp_dqe.set(r->dqe);
+        c->resp_dep.set(r->deposit);
+        c->have_response = true;
+        rebuild_tables(c);
+    });
+}
+
+int xs_scatter_accumulate_device(xs_context* c, const xs_geometry* g, int32_t angle,
+                                 const xs_spectrum* spec, const xs_sim_config* cfg,
+                                 uint64_t h0, uint64_t h1, uint64_t* d_accum)
+{
+    return guard(c, [&] {
+        validate_call(*g, angle, *spec, *cfg, "simulate_scatter");
+        accumulate(c, *g, angle, *spec, *cfg, h0, h1, reinterpret_cast<unsigned long long*>(d_accum));
+    });
+}
+
+int xs_scatter_finalize_device(xs_context* c, const xs_geometry* g, const xs_spectrum* spec,
+                               const xs_sim_config* cfg, const uint64_t* d_accum, uint64_t h0,
+                               uint64_t h1, xs_scatter_result* out, double* d_image)
+{
+    return guard(c, [&] {
+        xsh::validate_sim_config(*cfg);
+        xsh::validate_spectrum(*spec);
+        xsh::validate_geometry(*g);
+        finalize(c, *g, *spec, *cfg, reinterpret_cast<const unsigned long long*>(d_accum), h0, h1, out,
+                 d_image);
+    });
+}
+
+int xs_simulate_scatter_stats(xs_context* c, const xs_geometry* g, int32_t angle,
+                              const xs_spectrum* spec, const xs_sim_config* cfg,
+                              xs_scatter_result* out)
+{
+    return guard(c, [&] {
+        validate_call(*g, angle, *spec, *cfg, "simulate_scatter");
+        const Plan plan = make_plan(*g, *spec, *cfg);
+        c->accum.reserve(plan.layout.words);
+        cuda_check(cudaMemsetAsync(c->accum.p, 0, plan.layout.words * 8, c->stream), "memset accum");
+        accumulate(c, *g, angle, *spec, *cfg, 0, plan.n_hist, c->accum.p);
+        finalize(c, *g, *spec, *cfg, c->accum.p, 0, plan.n_hist, out, nullptr);
+    });
+}
+
+int xs_primary_device(xs_context* c, const xs_geometry* g, int32_t angle, const xs_spectrum* spec,
+                      const xs_sim_config* cfg, double* d_image)
+{
+    return guard(c, [&] {
+        validate_call(*g, angle, *spec, *cfg, "simulate_primary");
+        primary(c, *g, angle, *spec, d_image);
+    });
+}
+
+int xs_simulate_primary(xs_context* c, const xs_geometry* g, int32_t angle, const xs_spectrum* spec,
+                        const xs_sim_config* cfg, double* image_host)
+{
+    return guard(c, [&] {
+        validate_call(*g, angle, *spec, *cfg, "simulate_primary");
+        const size_t np = (size_t)g->nu * g->nv;
+        c->img.reserve(np);
+        primary(c, *g, angle, *spec, c->img.p);
+        cuda_check(cudaMemcpyAsync(image_host, c->img.p, np * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+        cuda_check(cudaStreamSynchronize(c->stream), "D2H");
+    });
+}
+
+int xs_run_scan(xs_context* c, const xs_geometry* g, const xs_spectrum* spec, const xs_sim_config* cfg,
+                const int32_t* subset, int32_t n_subset, int32_t what, double* primary_out,
+                double* scatter_out, double* seconds)
+{
+    return guard(c, [&] {
+        if (n_subset <= 0)
+            fail(XS_E_RUNTIME, "run_scan: empty angle subset");
+        xsh::validate_sim_config(*cfg);
+        xsh::validate_geometry(*g);
+        for (int i = 0; i < n_subset; ++i)
+            if (subset[i] < 0 || subset[i] >= g->n_angles)
+                fail(XS_E_OUT_OF_RANGE, "run_scan: angle index %d out of range", subset[i]);
+        const bool want_primary = what != 1, want_scatter = what != 0;
+        const size_t np = (size_t)g->nu * g->nv;
+        for (int i = 0; i < n_subset; ++i) {
+            const auto t0 = std::chrono::steady_clock::now();
+            try {
+                if (want_scatter) {
+                    validate_call(*g, subset[i], *spec, *cfg, "simulate_scatter");
+                    const Plan plan = make_plan(*g, *spec, *cfg);
+                    c->accum.reserve(plan.layout.words);
+                    cuda_check(cudaMemsetAsync(c->accum.p, 0, plan.layout.words * 8, c->stream), "memset");
+                    accumulate(c, *g, subset[i], *spec, *cfg, 0, plan.n_hist, c->accum.p);
+                    xs_scatter_result r{};
+                    r.image = scatter_out ? scatter_out + (size_t)i * np : nullptr;
+                    finalize(c, *g, *spec, *cfg, c->accum.p, 0, plan.n_hist, &r, nullptr);
+                }
+                if (want_primary) {
+                    validate_call(*g, subset[i], *spec, *cfg, "simulate_primary");
+                    c->img.reserve(np);
+                    primary(c, *g, subset[i], *spec, c->img.p);
+                    if (primary_out)
+                        cuda_check(cudaMemcpyAsync(primary_out + (size_t)i * np, c->img.p, np * 8,
+                                                   cudaMemcpyDeviceToHost, c->stream),
+                                   "D2H");
+                    cuda_check(cudaStreamSynchronize(c->stream), "D2H");
+                }
+            } catch (const Error& e) {
+                fail(XS_E_RUNTIME, "run_scan: angle index %d: %s", subset[i], e.msg.c_str());
+            }
+            if (seconds)
+                seconds[i] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        }
+    });
+}
+
+int xs_last_launch_stats(const xs_context* c, xs_launch_stats* out)
+{
+    *out = c->last;
+    return XS_OK;
+}
+
+// ------------------------------------------------------------ postprocess
+namespace {
+struct Staged {
+    const double* in;
+    double* out;
+};
+
+// Host-pointer mode: stage through context buffers.
+Staged stage(xs_context* c, const double* in, size_t n_in, double* out, size_t n_out, bool device)
+{
+    if (device)
+        return {in, out};
+    c->pp_a.reserve(n_in);
+    c->pp_b.reserve(n_out);
+    cuda_check(cudaMemcpyAsync(c->pp_a.p, in, n_in * 8, cudaMemcpyHostToDevice, c->stream), "H2D");
+    return {c->pp_a.p, c->pp_b.p};
+}
+
+void unstage(xs_context* c, const Staged& s, double* out, size_t n_out, bool device)
+{
+    if (!device)
+        cuda_check(cudaMemcpyAsync(out, s.out, n_out * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    cuda_check(cudaStreamSynchronize(c->stream), "postprocess");
+}
+} // namespace
+
+int xs_sg_smooth(xs_context* c, const double* in, double* out, int32_t nu, int32_t nv, int32_t n_images,
+                 int32_t window, int32_t polyorder, int32_t device_ptrs)
+{
+    return guard(c, [&] {
+        xsh::validate_sg(window, polyorder);
+        if (nu < window || nv < window)
+            fail(XS_E_RUNTIME, "sg_smooth: image dims smaller than filter window");
+        const int half = window / 2, W = 2 * half + 1;
+        std::vector<double> K((size_t)(half + 1) * (half + 1) * W, 0.0);
+        for (int l = 0; l <= half; ++l)
+            for (int r = 0; r <= half; ++r) {
+                const auto k = xsh::sg_kernel(l, r, polyorder);
+                std::copy(k.begin(), k.end(), K.begin() + (size_t)(l * (half + 1) + r) * W);
+            }
+        c->pp_k.reserve(K.size());
+        cuda_check(cudaMemcpyAsync(c->pp_k.p, K.data(), K.size() * 8, cudaMemcpyHostToDevice, c->stream), "H2D");
+        const size_t n = (size_t)nu * nv * n_images;
+        const Staged s = stage(c, in, n, out, n, device_ptrs != 0);
+        c->pp_c.reserve(n);
+        cuda_check(xsd::launch_sg(s.in, c->pp_c.p, s.out, nu, nv, n_images, half, c->pp_k.p, c->stream), "sg");
+        unstage(c, s, out, n, device_ptrs != 0);
+    });
+}
+
+int xs_interpolate_angles(xs_context* c, const double* in, const double* src, int32_t n_src, double* out,
+                          const double* tgt, int32_t n_tgt, int32_t nu, int32_t nv, int32_t device_ptrs)
+{
+    return guard(c, [&] {
+        for (int i = 1; i < n_src; ++i)
+            if (!(src[i] > src[i - 1]))
+                fail(XS_E_RUNTIME, "interpolate_angles: source angles not sorted");
+        for (int i = 1; i < n_tgt; ++i)
+            if (!(tgt[i] > tgt[i - 1]))
+                fail(XS_E_RUNTIME, "interpolate_angles: target angles not sorted");
+        // REF postprocess.cpp:160-192 bracket selection on the host
+        std::vector<xsd::InterpEntry> tab(n_tgt);
+        const double period = 2.0 * kPi;
+        for (int t = 0; t < n_tgt; ++t) {
+            const double b = tgt[t];
+            const double* lb = std::lower_bound(src, src + n_src, b);
+            if (lb != src + n_src && *lb == b) {
+                tab[t] = {(int)(lb - src), (int)(lb - src), 1, 0.0};
+                continue;
+            }
+            if (n_src < 2)
+                fail(XS_E_RUNTIME, "interpolate_angles: missing bracket for angle %f", b);
+            int hi = (int)(lb - src), lo;
+            double a_lo, a_hi;
+            if (hi == 0) {
+                lo = n_src - 1;
+                a_lo = src[lo] - period;
+                a_hi = src[0];
+            } else if (hi == n_src) {
+                lo = n_src - 1;
+                hi = 0;
+                a_lo = src[lo];
+                a_hi = src[0] + period;
+            } else {
+                lo = hi - 1;
+                a_lo = src[lo];
+                a_hi = src[hi];
+            }
+            tab[t] = {lo, hi, 0, (b - a_lo) / (a_hi - a_lo)};
+        }
+        if (n_tgt == 0)
+            return;
+        c->interp_tab.reserve(n_tgt);
+        cuda_check(cudaMemcpyAsync(c->interp_tab.p, tab.data(), n_tgt * sizeof(xsd::InterpEntry),
+                                   cudaMemcpyHostToDevice, c->stream),
+                   "H2D");
+        const size_t np = (size_t)nu * nv;
+        const Staged s = stage(c, in, np * n_src, out, np * n_tgt, device_ptrs != 0);
+        cuda_check(xsd::launch_interp(s.in, s.out, c->interp_tab.p, n_tgt, np, c->stream), "interp");
+        unstage(c, s, out, np * n_tgt, device_ptrs != 0);
+    });
+}
+
+int xs_upsample_image(xs_context* c, const double* in, int32_t nu, int32_t nv, int32_t n_images,
+                      double* out, int32_t nu_out, int32_t nv_out, int32_t device_ptrs)
+{
+    return guard(c, [&] {
+        if (nu_out < nu || nv_out < nv)
+            fail(XS_E_RUNTIME, "upsample_image: target dims must be >= source dims");
+        if (nu < 1 || nv < 1)
+            fail(XS_E_RUNTIME, "upsample_image: degenerate source");
+        const size_t n_in = (size_t)nu * nv * n_images, n_out = (size_t)nu_out * nv_out * n_images;
+        const Staged s = stage(c, in, n_in, out, n_out, device_ptrs != 0);
+        c->pp_c.reserve((size_t)nu_out * nv * n_images);
+        cuda_check(xsd::launch_upsample(s.in, c->pp_c.p, s.out, nu, nv, n_images, nu_out, nv_out, c->stream),
+                   "upsample");
+        unstage(c, s, out, n_out, device_ptrs != 0);
+    });
+}
+
+int xs_downsample_average(xs_context* c, const double* in, int32_t nu, int32_t nv, int32_t n_images,
+                          double* out, int32_t nu_out, int32_t nv_out, int32_t device_ptrs)
+{
+    return guard(c, [&] {
+        if (nu_out > nu || nv_out > nv || nu_out < 1 || nv_out < 1)
+            fail(XS_E_RUNTIME, "downsample_average: bad target dims");
+        const size_t n_in = (size_t)nu * nv * n_images, n_out = (size_t)nu_out * nv_out * n_images;
+        const Staged s = stage(c, in, n_in, out, n_out, device_ptrs != 0);
+        cuda_check(xsd::launch_downsample(s.in, s.out, nu, nv, n_images, nu_out, nv_out, c->stream),
+                   "downsample");
+        unstage(c, s, out, n_out, device_ptrs != 0);
+    });
+}
+
+} // extern "C"

@@ -1,0 +1,335 @@
+"""The projector API, mirroring REF include/xscat/transport.hpp:69-116 and
+include/xscat/postprocess.hpp:13-41, executed by libxscatgpu.so on a B200.
+
+Free functions keep REF's signatures (``workers`` is accepted and ignored:
+results are worker- and GPU-count independent by construction).  They take
+the phantom on every call like REF does and therefore upload it every call;
+use :class:`Projector` to upload a scene once and run many projections.
+
+There is no CPU fallback: without the CUDA library or a CUDA device every
+call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import time
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+
+from . import _capi as A
+from . import inputs as I
+
+
+@dataclasses.dataclass
+class WeightLedger:
+    """REF WeightLedger (transport.hpp:38-56)."""
+
+    initial: float = 0.0
+    escaped: float = 0.0
+    absorbed: float = 0.0
+    culled: float = 0.0
+    roulette_killed: float = 0.0
+    roulette_boost: float = 0.0
+
+
+@dataclasses.dataclass
+class SimResult:
+    """REF SimResult (transport.hpp:58-64); image is (nv, nu) fp64."""
+
+    image: np.ndarray
+    variance: Optional[np.ndarray]
+    ledger: WeightLedger
+    histories: int
+    total: float
+    total_std_error: float
+    stats: Optional[Dict[str, float]] = None
+
+
+@dataclasses.dataclass
+class ProjectionStack:
+    """REF ProjectionStack (detector_image.hpp:28-34): images (n, nv, nu)."""
+
+    angle_values: np.ndarray
+    images: np.ndarray
+
+    @property
+    def n_angles(self):
+        return int(self.images.shape[0])
+
+
+@dataclasses.dataclass
+class ScanResult:
+    """REF ScanResult (transport.hpp:104-110)."""
+
+    primary: Optional[ProjectionStack]
+    scatter: Optional[ProjectionStack]
+    seconds_per_angle: List[float]
+
+
+PRIMARY, SCATTER, BOTH = 0, 1, 2  # REF ScanQuantity
+
+
+def device_count() -> int:
+    n = C.c_int32()
+    A.check(A.lib().xs_device_count(C.byref(n)))
+    return n.value
+
+
+class Context:
+    """One CUDA device + stream + uploaded scene (an ``xs_context``)."""
+
+    def __init__(self, device: int = 0):
+        L = A.lib()
+        h = C.c_void_p()
+        A.check(L.xs_ctx_create(device, C.byref(h)))
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if self.h:
+            A.lib().xs_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def check(self, st):
+        A.check(st, self.h)
+
+    def set_stream(self, cuda_stream_ptr: int):
+        self.check(A.lib().xs_ctx_set_stream(self.h, C.c_void_p(cuda_stream_ptr)))
+
+    def upload(self, ph: I.VoxelPhantom, resp: I.DetectorResponse):
+        pk = A.Packed()
+        self.check(A.lib().xs_upload_phantom(self.h, C.byref(pk.phantom(ph))))
+        self.check(A.lib().xs_upload_response(self.h, C.byref(pk.response(resp))))
+
+    def launch_stats(self) -> Dict[str, float]:
+        s = A.XsLaunchStats()
+        self.check(A.lib().xs_last_launch_stats(self.h, C.byref(s)))
+        return {k: getattr(s, k) for k, _ in A.XsLaunchStats._fields_}
+
+
+_contexts: Dict[int, Context] = {}
+
+
+def default_context(device: int = 0) -> Context:
+    if device not in _contexts:
+        _contexts[device] = Context(device)
+    return _contexts[device]
+
+
+def _result(img, var, res, g, stats=None) -> SimResult:
+    return SimResult(img.reshape(g.nv, g.nu), None if var is None else var.reshape(g.nv, g.nu),
+                     WeightLedger(*[getattr(res.ledger, k) for k, _ in A.XsLedger._fields_]),
+                     int(res.histories), float(res.total), float(res.total_std_error), stats)
+
+
+class Projector:
+    """A scene (phantom + detector response) resident on one GPU."""
+
+    def __init__(self, phantom: I.VoxelPhantom, response: I.DetectorResponse,
+                 ctx: Optional[Context] = None, device: int = 0):
+        self.ctx = ctx or default_context(device)
+        self.phantom = phantom
+        self.response = response
+        self.ctx.upload(phantom, response)
+
+    # REF simulate_scatter_stats (transport.cpp:246-324)
+    def scatter_stats(self, g: I.ScanGeometry, angle_idx: int, spec: I.Spectrum,
+                      cfg: I.SimConfig) -> SimResult:
+        pk = A.Packed()
+        img = np.empty(g.nu * g.nv)
+        var = np.empty(g.nu * g.nv) if cfg.track_variance else None
+        res = A.XsScatterResult()
+        res.image = A.dptr(img)
+        res.variance = A.dptr(var) if var is not None else None
+        self.ctx.check(A.lib().xs_simulate_scatter_stats(
+            self.ctx.h, C.byref(pk.geometry(g)), angle_idx, C.byref(pk.spectrum(spec)),
+            C.byref(pk.config(cfg)), C.byref(res)))
+        return _result(img, var, res, g, self.ctx.launch_stats())
+
+    # REF simulate_primary (transport.cpp:333-377)
+    def primary(self, g: I.ScanGeometry, angle_idx: int, spec: I.Spectrum,
+                cfg: Optional[I.SimConfig] = None) -> np.ndarray:
+        pk = A.Packed()
+        img = np.empty(g.nu * g.nv)
+        self.ctx.check(A.lib().xs_simulate_primary(
+            self.ctx.h, C.byref(pk.geometry(g)), angle_idx, C.byref(pk.spectrum(spec)),
+            C.byref(pk.config(cfg or I.SimConfig())), A.dptr(img)))
+        return img.reshape(g.nv, g.nu)
+
+    # REF run_scan (transport.cpp:379-422)
+    def run_scan(self, g: I.ScanGeometry, spec: I.Spectrum, cfg: I.SimConfig,
+                 angle_subset: Sequence[int], what: int = BOTH) -> ScanResult:
+        pk = A.Packed()
+        sub = np.ascontiguousarray(np.asarray(angle_subset, dtype=np.int32))
+        n = int(sub.size)
+        np_ = g.nu * g.nv
+        prim = np.empty((max(n, 1), g.nv, g.nu)) if what != SCATTER else None
+        scat = np.empty((max(n, 1), g.nv, g.nu)) if what != PRIMARY else None
+        secs = np.zeros(max(n, 1))
+        self.ctx.check(A.lib().xs_run_scan(
+            self.ctx.h, C.byref(pk.geometry(g)), C.byref(pk.spectrum(spec)),
+            C.byref(pk.config(cfg)), sub.ctypes.data_as(C.POINTER(C.c_int32)), n, what,
+            A.dptr(prim) if prim is not None else None,
+            A.dptr(scat) if scat is not None else None, A.dptr(secs)))
+        angles = g.angles[sub] if n else np.zeros(0)
+        return ScanResult(None if prim is None else ProjectionStack(angles, prim[:n]),
+                          None if scat is None else ProjectionStack(angles, scat[:n]),
+                          list(secs[:n]))
+
+    # device-level split (photon batches across GPUs)
+    def accumulate(self, g, angle_idx, spec, cfg, hist_begin, hist_end, d_accum_ptr: int):
+        pk = A.Packed()
+        self.ctx.check(A.lib().xs_scatter_accumulate_device(
+            self.ctx.h, C.byref(pk.geometry(g)), angle_idx, C.byref(pk.spectrum(spec)),
+            C.byref(pk.config(cfg)), hist_begin, hist_end, C.c_void_p(d_accum_ptr)))
+
+    def finalize(self, g, spec, cfg, d_accum_ptr: int, hist_begin, hist_end) -> SimResult:
+        pk = A.Packed()
+        img = np.empty(g.nu * g.nv)
+        var = np.empty(g.nu * g.nv) if cfg.track_variance else None
+        res = A.XsScatterResult()
+        res.image = A.dptr(img)
+        res.variance = A.dptr(var) if var is not None else None
+        self.ctx.check(A.lib().xs_scatter_finalize_device(
+            self.ctx.h, C.byref(pk.geometry(g)), C.byref(pk.spectrum(spec)),
+            C.byref(pk.config(cfg)), C.c_void_p(d_accum_ptr), hist_begin, hist_end,
+            C.byref(res), None))
+        return _result(img, var, res, g, self.ctx.launch_stats())
+
+
+# ------------------------------------------------ REF-signature free functions
+def simulate_scatter_stats(ph, g, angle_idx, spec, resp, cfg, workers: int = 1,
+                           device: int = 0) -> SimResult:
+    return Projector(ph, resp, device=device).scatter_stats(g, angle_idx, spec, cfg)
+
+
+def simulate_scatter(ph, g, angle_idx, spec, resp, cfg, workers: int = 1, device: int = 0):
+    return simulate_scatter_stats(ph, g, angle_idx, spec, resp, cfg, workers, device).image
+
+
+def simulate_primary(ph, g, angle_idx, spec, resp, cfg=None, workers: int = 1, device: int = 0):
+    return Projector(ph, resp, device=device).primary(g, angle_idx, spec, cfg)
+
+
+def run_scan(ph, g, spec, resp, cfg, angle_subset, what=BOTH, workers: int = 1,
+             device: int = 0) -> ScanResult:
+    return Projector(ph, resp, device=device).run_scan(g, spec, cfg, angle_subset, what)
+
+
+def apportion_photons(spec: I.Spectrum, photons_total: int) -> np.ndarray:
+    """REF apportion_photons (transport.cpp:42-64)."""
+    pk = A.Packed()
+    out = np.zeros(spec.n_bins, np.uint64)
+    A.check(A.lib().xs_apportion_photons(C.byref(pk.spectrum(spec)), int(photons_total),
+                                         out.ctypes.data_as(A.c_u64_p)))
+    return out
+
+
+def history_count(spec: I.Spectrum, photons_total: int) -> int:
+    pk = A.Packed()
+    n = C.c_uint64()
+    A.check(A.lib().xs_history_count(C.byref(pk.spectrum(spec)), int(photons_total),
+                                     C.byref(n)))
+    return int(n.value)
+
+
+def point_detector_score(response_factor, p_dir, weight, n_pixels, d2, tau) -> float:
+    """REF point_detector_score (transport.cpp:66-71)."""
+    return A.lib().xs_point_detector_score(response_factor, p_dir, weight, n_pixels, d2, tau)
+
+
+def finalize_host(g, spec, cfg, accum: np.ndarray, hist_begin: int, hist_end: int) -> SimResult:
+    """Finalize a (reduced) fixed-point accumulator on the host (no GPU)."""
+    pk = A.Packed()
+    accum = np.ascontiguousarray(accum, dtype=np.uint64)
+    img = np.empty(g.nu * g.nv)
+    var = np.empty(g.nu * g.nv) if cfg.track_variance else None
+    res = A.XsScatterResult()
+    res.image = A.dptr(img)
+    res.variance = A.dptr(var) if var is not None else None
+    A.check(A.lib().xs_scatter_finalize_host(
+        C.byref(pk.geometry(g)), C.byref(pk.spectrum(spec)), C.byref(pk.config(cfg)),
+        accum.ctypes.data_as(A.c_u64_p), hist_begin, hist_end, C.byref(res)))
+    return _result(img, var, res, g)
+
+
+# ------------------------------------------------------------ post-processing
+@dataclasses.dataclass
+class SgFilterSpec:
+    """REF SgFilterSpec (postprocess.hpp:8-11)."""
+
+    window: int = 15
+    polyorder: int = 3
+
+
+def validate_sg_spec(f: SgFilterSpec) -> None:
+    A.check(A.lib().xs_validate_sg_spec(f.window, f.polyorder))
+
+
+def default_sg_spec(nu: int, nv: int) -> SgFilterSpec:
+    w, p = C.c_int32(), C.c_int32()
+    A.check(A.lib().xs_default_sg_spec(nu, nv, C.byref(w), C.byref(p)))
+    return SgFilterSpec(w.value, p.value)
+
+
+def sg_kernel(left: int, right: int, polyorder: int) -> np.ndarray:
+    out = np.empty(left + right + 1)
+    A.check(A.lib().xs_sg_kernel(left, right, polyorder, A.dptr(out)))
+    return out
+
+
+def _as_stack(x):
+    a = np.ascontiguousarray(x, dtype=np.float64)
+    return (a[None], True) if a.ndim == 2 else (a, False)
+
+
+def sg_smooth(img, f: SgFilterSpec, ctx: Optional[Context] = None) -> np.ndarray:
+    """REF sg_smooth (postprocess.cpp:124-145); img (nv, nu) or a stack (n, nv, nu)."""
+    ctx = ctx or default_context()
+    a, single = _as_stack(img)
+    out = np.empty_like(a)
+    ctx.check(A.lib().xs_sg_smooth(ctx.h, a.ctypes.data, out.ctypes.data, a.shape[2], a.shape[1],
+                                   a.shape[0], f.window, f.polyorder, 0))
+    return out[0] if single else out
+
+
+def interpolate_angles(stack: ProjectionStack, target_angles,
+                       ctx: Optional[Context] = None) -> ProjectionStack:
+    """REF interpolate_angles (postprocess.cpp:147-196)."""
+    ctx = ctx or default_context()
+    imgs = np.ascontiguousarray(stack.images, dtype=np.float64)
+    src = np.ascontiguousarray(stack.angle_values, dtype=np.float64)
+    tgt = np.ascontiguousarray(target_angles, dtype=np.float64)
+    n, nv, nu = imgs.shape
+    out = np.empty((tgt.size, nv, nu))
+    ctx.check(A.lib().xs_interpolate_angles(ctx.h, imgs.ctypes.data, A.dptr(src), n,
+                                            out.ctypes.data, A.dptr(tgt), tgt.size, nu, nv, 0))
+    return ProjectionStack(tgt.copy(), out)
+
+
+def upsample_image(img, nu_out: int, nv_out: int, ctx: Optional[Context] = None) -> np.ndarray:
+    """REF upsample_image (postprocess.cpp:235-252)."""
+    ctx = ctx or default_context()
+    a, single = _as_stack(img)
+    out = np.empty((a.shape[0], nv_out, nu_out))
+    ctx.check(A.lib().xs_upsample_image(ctx.h, a.ctypes.data, a.shape[2], a.shape[1], a.shape[0],
+                                        out.ctypes.data, nu_out, nv_out, 0))
+    return out[0] if single else out
+
+
+def downsample_average(img, nu_out: int, nv_out: int, ctx: Optional[Context] = None) -> np.ndarray:
+    """REF downsample_average (postprocess.cpp:254-271)."""
+    ctx = ctx or default_context()
+    a, single = _as_stack(img)
+    out = np.empty((a.shape[0], nv_out, nu_out))
+    ctx.check(A.lib().xs_downsample_average(ctx.h, a.ctypes.data, a.shape[2], a.shape[1],
+                                            a.shape[0], out.ctypes.data, nu_out, nv_out, 0))
+    return out[0] if single else out
