@@ -20,9 +20,10 @@
 #include "xs_types.h"
 
 namespace xsd {
-cudaError_t launch_transport(const TransportParams& P, int grid, int block, size_t smem, cudaStream_t s);
-cudaError_t transport_set_smem(size_t smem);
-cudaError_t transport_occupancy(int fmt, int block, size_t smem, int* blocks_per_sm);
+size_t transport_smem_bytes(const TransportParams& P);
+int transport_block_size();
+cudaError_t transport_prepare(const TransportParams& P, size_t smem, int* blocks_per_sm);
+cudaError_t launch_transport(const TransportParams& P, int grid, size_t smem, cudaStream_t s);
 cudaError_t launch_primary(const PrimaryParams& P, cudaStream_t s);
 cudaError_t launch_finalize_image(const unsigned long long* acc, uint64_t off_image, uint64_t off_var,
                                   uint64_t npix, int log2_img, double n_hist, int track_var,
@@ -140,10 +141,11 @@ struct xs_context {
     DevBuf<double> var_val;
     DevBuf<double> img, var, pp_a, pp_b, pp_c, pp_k;
     DevBuf<xsd::InterpEntry> interp_tab;
-    size_t smem_attr = 0;
+    uint32_t queue_len = 512;
+    int max_slots = 64;
 
     xs_launch_stats last{};
-    int walk_thresh = 8;
+    int walk_thresh = 28;
     int grab = 64;
 };
 
@@ -497,33 +499,40 @@ void accumulate(xs_context* c, const xs_geometry& g, int angle, const xs_spectru
     P.walk_thresh = c->walk_thresh;
     P.status = c->status.p;
 
-    const int block = 256;
-    const int n_tab = c->grid.fmt == xsd::kFmtP4 ? c->n_pal : c->n_mats;
-    const size_t smem = (size_t)n_tab * block * 8 + (size_t)(8 * nb + 32) * 8 + (size_t)(nb + 1) * 8;
-    if (smem > c->smem_attr) {
-        cuda_check(xsd::transport_set_smem(std::max<size_t>(smem, 48 * 1024)), "smem attribute");
-        c->smem_attr = std::max<size_t>(smem, 48 * 1024);
-    }
+    // warp-queue geometry: H live histories per warp, FIFO of Q tasks; the
+    // FIFO never holds more than H * (splitting + 1) tasks (see transport.cu)
+    uint32_t Q = c->queue_len;
+    while (Q < (uint32_t)cfg.splitting + 1)
+        Q <<= 1;
+    int H = (int)(Q / (uint32_t)(cfg.splitting + 1));
+    H = std::max(1, std::min(H, std::min(64, c->max_slots)));
+    P.slots_per_warp = H;
+    P.queue_len = (int32_t)Q;
+    const int block = xsd::transport_block_size();
+    const size_t smem = xsd::transport_smem_bytes(P);
     int per_sm = 0;
-    cuda_check(xsd::transport_occupancy(c->grid.fmt, block, smem, &per_sm), "occupancy");
-    per_sm = std::max(per_sm, 1);
+    cuda_check(xsd::transport_prepare(P, smem, &per_sm), "transport occupancy");
+    if (per_sm < 1)
+        fail(XS_E_UNSUPPORTED, "xscat-gpu: transport kernel does not fit (%zu B shared memory)", smem);
     int grid = c->sm_count * per_sm;
-    // no more threads than histories (small launches)
-    const uint64_t n = h1 - h0;
-    if ((uint64_t)grid * block > n)
-        grid = (int)std::max<uint64_t>(1, (n + block - 1) / block);
+    const uint64_t n = h1 - h0; // no more warps than needed for small launches
+    const uint64_t warps_needed = (n + H - 1) / H;
+    const uint64_t blocks_needed = std::max<uint64_t>(1, (warps_needed + block / 32 - 1) / (block / 32));
+    if ((uint64_t)grid > blocks_needed)
+        grid = (int)blocks_needed;
     if (cfg.track_variance) {
         const uint64_t cap = (uint64_t)cfg.splitting * (uint64_t)cfg.max_interactions;
         if (cap > (1u << 20))
             fail(XS_E_UNSUPPORTED, "xscat-gpu: splitting*max_interactions too large for variance tracking");
         P.var_cap = (int32_t)cap;
-        c->var_pix.reserve((size_t)grid * block * cap);
-        c->var_val.reserve((size_t)grid * block * cap);
+        const size_t entries = (size_t)grid * (block / 32) * H * cap;
+        c->var_pix.reserve(entries);
+        c->var_val.reserve(entries);
         P.var_pix = c->var_pix.p;
         P.var_val = c->var_val.p;
     }
     cuda_check(cudaEventRecord(c->ev0, s), "event");
-    cuda_check(xsd::launch_transport(P, grid, block, smem, s), "transport launch");
+    cuda_check(xsd::launch_transport(P, grid, smem, s), "transport launch");
     cuda_check(cudaEventRecord(c->ev1, s), "event");
     check_status(c, angle, &spec);
     float ms = 0.f;
@@ -665,6 +674,14 @@ int xs_ctx_create(int32_t device, xs_context** out)
             c->walk_thresh = std::max(1, std::min(32, std::atoi(e)));
         if (const char* e = std::getenv("XSCAT_GRAB"))
             c->grab = std::max(1, std::atoi(e));
+        if (const char* e = std::getenv("XSCAT_QUEUE")) {
+            uint32_t q = 16;
+            while (q < (uint32_t)std::max(16, std::atoi(e)))
+                q <<= 1;
+            c->queue_len = q;
+        }
+        if (const char* e = std::getenv("XSCAT_SLOTS"))
+            c->max_slots = std::max(1, std::min(64, std::atoi(e)));
         *out = c;
     });
 }

@@ -1,317 +1,257 @@
-// transport.cu — Monte Carlo scatter transport, primary projector and the
-// tally finalize kernels.
+// transport.cu — Monte Carlo scatter transport (REF transport.cpp:114-324).
 //
-// Scatter (REF transport.cpp:114-242 run_history, :246-324 simulate_scatter_stats):
-// a persistent kernel; every lane owns one photon history at a time and runs
-// the reference's per-history state machine (emission -> exact free-path walk
-// -> interaction -> `splitting` next-event scoring rays -> continuation ->
-// cap / roulette).  The voxel walks, which are >95 % of the work, run in
-// warp-synchronous lockstep: a warp steps all its walking lanes together and
-// leaves the walk phase only when enough lanes wait for event processing, at
-// which point those lanes advance their state machines and refill from a
-// warp-aggregated history pool.  Tallies are fixed-point integers (see
-// include/xscat_gpu.h), so the result does not depend on the schedule or on
-// how the history range is split across GPUs.
-#include <cfloat>
-#include <math_constants.h>
+// Design (B200): a persistent kernel whose warps are independent "ray
+// engines".  Each warp owns, in shared memory,
+//   * H history slots: the photon state of a live history (position,
+//     direction, energy, weight, its Philox stream) plus the record of its
+//     last interaction, and
+//   * a FIFO of ray tasks (8 bytes each): "free path of history s" or
+//     "next-event scoring ray of history s towards pixel p".
+// A history's event logic (REF run_history) runs when its free-path ray
+// completes: it samples the interaction, draws the `splitting` scoring pixels
+// (same Philox order as REF), pushes one scoring task per pixel, samples the
+// continuation and pushes its next free path.  Scoring rays do not change the
+// photon, so they are fire-and-forget tasks that any lane of the warp traces.
+// All 32 lanes therefore pull independent rays from one queue and walk them in
+// lockstep, which keeps the SIMT lanes busy (a one-history-per-lane design
+// idles most of them; see profiles/).  FIFO order guarantees that the
+// scoring rays of an interaction start (and copy its record) before the
+// history's next free path can complete and overwrite it.
+//
+// Tallies are fixed-point integers (include/xscat_gpu.h): per-pixel limbs in
+// global memory, per-history totals in the slot, per-bin and ledger sums in
+// shared memory, so results are independent of the schedule and of how the
+// history range is split across GPUs.
 #include <cmath>
 
-#include "xs_device.cuh"
+#include "physics.cuh"
 
 namespace xsd {
 
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
+constexpr int kWarps = 4; // warps per block
+constexpr int kBlock = 32 * kWarps;
 
-enum State : int {
-    ST_FETCH = 0,
-    ST_INIT,
-    ST_FREE,
-    ST_AFTER_FREE,
-    ST_SCORE,
-    ST_AFTER_SCORE,
-    ST_CONT,
-    ST_END,
-    ST_WALK,
-    ST_DONE
+enum : int { T_NONE = -1, T_FREE = 0, T_SCORE = 1 };
+enum : int { K_PE = 0, K_COMPTON = 1, K_RAYLEIGH = 2 };
+
+// ------------------------------------------------------------ smem layout
+struct __align__(8) Slot {
+    double px, py, pz, dx, dy, dz; // photon position / direction
+    double E, W, wmin, target;     // energy, weight, roulette floor, -ln u of the pending free path
+    double ox, oy, oz;             // last interaction point
+    double ix, iy, iz;             // incoming direction at it
+    double e_in, w_split;          // energy at it, weight per pseudo-particle
+    unsigned long long T[3];       // history total, fixed-point limbs (unit U_img)
+    uint32_t r_photon, r_bin, r_block, r_pos, r_b0, r_b1, r_b2, r_b3; // Philox stream
+    int32_t bin, gen, kind, mat;
+    int32_t pending;               // queued/in-flight scoring rays + 1 while alive
+    int32_t n_var;                 // variance scratch entries
 };
 
-enum Kind : int { K_PE = 0, K_COMPTON = 1, K_RAYLEIGH = 2 };
-
-struct V3 {
-    double x, y, z;
+struct WarpHdr {
+    uint32_t tail;
+    uint32_t pad;
+    unsigned long long free_mask;
 };
 
-__device__ __forceinline__ V3 v3(double x, double y, double z) { return V3{x, y, z}; }
-__device__ __forceinline__ V3 operator+(V3 a, V3 b) { return v3(a.x + b.x, a.y + b.y, a.z + b.z); }
-__device__ __forceinline__ V3 operator-(V3 a, V3 b) { return v3(a.x - b.x, a.y - b.y, a.z - b.z); }
-__device__ __forceinline__ V3 operator*(V3 a, double s) { return v3(a.x * s, a.y * s, a.z * s); }
-__device__ __forceinline__ V3 operator/(V3 a, double s) { return v3(a.x / s, a.y / s, a.z / s); }
-__device__ __forceinline__ double dot(V3 a, V3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
-__device__ __forceinline__ V3 cross(V3 a, V3 b)
+__device__ __forceinline__ Rng load_rng(const Slot& s)
 {
-    return v3(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
-}
-__device__ __forceinline__ V3 normalized(V3 v) { return v / sqrt(dot(v, v)); }
-
-// REF samplers.cpp:127-134
-__device__ __forceinline__ V3 rotate_direction(V3 dir, double theta, double phi)
-{
-    const V3 pick = fabs(dir.x) < 0.5 ? v3(1.0, 0.0, 0.0) : v3(0.0, 1.0, 0.0);
-    const V3 e1 = normalized(cross(dir, pick));
-    const V3 e2 = cross(dir, e1);
-    const double st = sin(theta), ct = cos(theta);
-    return normalized(dir * ct + (e1 * cos(phi) + e2 * sin(phi)) * st);
+    Rng r;
+    r.photon = s.r_photon;
+    r.bin = s.r_bin;
+    r.block = s.r_block;
+    r.pos = s.r_pos;
+    r.b0 = s.r_b0;
+    r.b1 = s.r_b1;
+    r.b2 = s.r_b2;
+    r.b3 = s.r_b3;
+    return r;
 }
 
-// ------------------------------------------------------------ physics helpers
-__device__ __forceinline__ double momentum_transfer(double e, double theta)
+__device__ __forceinline__ void store_rng(Slot& s, const Rng& r)
 {
-    return sin(0.5 * theta) * e / kHc; // cross_sections.cpp:19-22
+    s.r_photon = r.photon;
+    s.r_bin = r.bin;
+    s.r_block = r.block;
+    s.r_pos = r.pos;
+    s.r_b0 = r.b0;
+    s.r_b1 = r.b1;
+    s.r_b2 = r.b2;
+    s.r_b3 = r.b3;
 }
 
-__device__ __forceinline__ double compton_ratio(double e, double theta)
-{
-    const double alpha = e / kMec2; // cross_sections.cpp:24-28
-    return 1.0 / (1.0 + alpha * (1.0 - cos(theta)));
-}
+// ----------------------------------------------------------------- mu table
+// Linear attenuation lookup for the current ray's energy.  REG: <= 4 palette
+// entries held in registers (4-bit palette); otherwise a per-lane table in
+// shared memory: palette entries (P4) or mass attenuation per material
+// (P8 / raw, multiplied by the voxel density at lookup).  Values are the
+// products REF MuField forms (trace.cpp:10-20).
+template <int FMT, bool REG>
+struct MuTab {
+    double t0, t1, t2, t3;
+    double* T;
+    double energy;
 
-__device__ __forceinline__ double kn_core(double e, double theta)
-{
-    const double ratio = compton_ratio(e, theta);
-    const double s = sin(theta);
-    return ratio * ratio * (ratio + 1.0 / ratio - s * s);
-}
-
-struct Ctx {
-    const TransportParams& P;
-    DevStatus* st;
-};
-
-__device__ __forceinline__ Tab mtab(const TransportParams& P, TabDesc d) { return tab_at(P.tabs, d); }
-
-// material.cpp:253-261
-__device__ __forceinline__ double form_S(const TransportParams& P, const MatDesc& m, double q)
-{
-    const Tab t = mtab(P, m.s);
-    if (q >= __ldg(t.x + t.n - 1))
-        return m.z_eff;
-    double y = 0.0;
-    tab_linear(t, q, y);
-    return y;
-}
-
-__device__ __forceinline__ double form_F(const TransportParams& P, const MatDesc& m, double q)
-{
-    return tab_linear_clamped(mtab(P, m.f), q);
-}
-
-__device__ __forceinline__ double loglog_or_fail(const TransportParams& P, TabDesc d, double e,
-                                                 DevStatus* st, int bin)
-{
-    double y = 0.0;
-    if (!tab_loglog(mtab(P, d), e, y))
-        raise(st, XS_E_OUT_OF_RANGE, kErrTableRange, bin, e, 0.0);
-    return y;
-}
-
-// samplers.cpp:56-88
-__device__ __forceinline__ double segment_mass(double q0, double a, double b, double u)
-{
-    const double c0 = a * a, c1 = 2.0 * a * b, c2 = b * b;
-    return 2.0 * (c0 * q0 * u + (c0 + c1 * q0) * u * u / 2.0 + (c1 + c2 * q0) * u * u * u / 3.0 +
-                  c2 * u * u * u * u / 4.0);
-}
-
-__device__ double cumulative_mass(const TransportParams& P, const MatDesc& m, double q)
-{
-    const double* knots = P.tabs + m.f.off;
-    const double* fv = knots + m.f.n;
-    const double* cdf = P.tabs + m.cdf_off;
-    const int n = m.f.n;
-    const double k_last = __ldg(knots + n - 1);
-    if (q >= k_last) {
-        const double f_last = __ldg(fv + n - 1);
-        return __ldg(cdf + n - 1) + f_last * f_last * (q * q - k_last * k_last);
-    }
-    int lo = 0, hi = n - 1;
-    while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (__ldg(knots + mid) <= q)
-            lo = mid;
-        else
-            hi = mid;
-    }
-    const double k0 = __ldg(knots + lo), k1 = __ldg(knots + lo + 1);
-    const double a = __ldg(fv + lo);
-    const double b = (__ldg(fv + lo + 1) - a) / (k1 - k0);
-    return __ldg(cdf + lo) + segment_mass(k0, a, b, q - k0);
-}
-
-__device__ double invert_mass(const TransportParams& P, const MatDesc& m, double target, double q_hi)
-{
-    double lo = 0.0, hi = q_hi;
-    for (int it = 0; it < 64; ++it) {
-        const double mid = 0.5 * (lo + hi);
-        if (cumulative_mass(P, m, mid) < target)
-            lo = mid;
-        else
-            hi = mid;
-    }
-    return 0.5 * (lo + hi);
-}
-
-// ------------------------------------------------------------- mu tables
-// Per-lane table in shared memory, T[k * stride]: for the 4-bit palette the
-// linear attenuation of palette entry k (mass_atten[mat_k] * dens_k, the
-// same product REF MuField::at forms per voxel); for the other formats the
-// mass attenuation of material k (REF MuField, trace.cpp:10-16).
-template <int FMT>
-__device__ __forceinline__ void fill_mu(const TransportParams& P, double* T, int stride,
-                                        double e, DevStatus* st, int bin)
-{
-    if (FMT == kFmtP4) {
-        for (int c = 0; c < P.n_pal; ++c)
-            T[c * stride] = 0.0;
-        for (int m = 1; m < P.n_mats; ++m) {
-            const MatDesc& md = P.mats[m];
-            const double ma = md.has_tables ? loglog_or_fail(P, md.mu, e, st, bin) : 0.0;
-            for (int c = 0; c < P.n_pal; ++c)
-                if (P.pal_mat[c] == m)
-                    T[c * stride] = ma * (double)P.pal_dens[c];
-        }
-    } else {
-        T[0] = 0.0;
-        for (int m = 1; m < P.n_mats; ++m) {
-            const MatDesc& md = P.mats[m];
-            T[m * stride] = md.has_tables ? loglog_or_fail(P, md.mu, e, st, bin) : 0.0;
+    __device__ __noinline__ void fill(const TransportParams& P, double e, DevStatus* st, int bin)
+    {
+        energy = e;
+        if (FMT == kFmtP4) {
+            double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3_ = 0.0;
+            if (!REG)
+                for (int c = 0; c < P.n_pal; ++c)
+                    T[c * kBlock] = 0.0;
+            for (int m = 1; m < P.n_mats; ++m) {
+                const MatDesc& md = P.mats[m];
+                const double ma = md.has_tables ? loglog_or_fail(P, md.mu, e, st, bin) : 0.0;
+                for (int c = 0; c < P.n_pal; ++c)
+                    if (P.pal_mat[c] == m) {
+                        const double mu = ma * (double)P.pal_dens[c];
+                        if (REG) {
+                            if (c == 0)
+                                v0 = mu;
+                            else if (c == 1)
+                                v1 = mu;
+                            else if (c == 2)
+                                v2 = mu;
+                            else
+                                v3_ = mu;
+                        } else {
+                            T[c * kBlock] = mu;
+                        }
+                    }
+            }
+            t0 = v0;
+            t1 = v1;
+            t2 = v2;
+            t3 = v3_;
+        } else {
+            T[0] = 0.0;
+            for (int m = 1; m < P.n_mats; ++m) {
+                const MatDesc& md = P.mats[m];
+                T[m * kBlock] = md.has_tables ? loglog_or_fail(P, md.mu, e, st, bin) : 0.0;
+            }
         }
     }
-}
 
+    __device__ __forceinline__ double mu(const TransportParams& P, int code, float dens) const
+    {
+        if (FMT == kFmtP4) {
+            if (REG) {
+                const double lo = (code & 1) ? t1 : t0;
+                const double hi = (code & 1) ? t3 : t2;
+                return (code & 2) ? hi : lo;
+            }
+            return T[code * kBlock];
+        }
+        if (FMT == kFmtP8)
+            return T[P.pal_mat[code] * kBlock] * (double)P.pal_dens[code];
+        return T[code * kBlock] * (double)dens;
+    }
+};
+
+// Voxel fetch: code (P4/P8 palette index or raw material id) + raw density.
 template <int FMT>
-__device__ __forceinline__ double mu_at(const TransportParams& P, const double* T, int stride,
-                                        uint32_t cell)
+__device__ __forceinline__ void fetch(const Grid& G, int ix, int iy, int iz, int& code, float& dens)
 {
+    const uint32_t c = brick_cell(G, ix, iy, iz);
     if (FMT == kFmtP4) {
-        return T[load_code_p4(P.G, cell) * stride];
+        code = load_code_p4(G, c);
     } else if (FMT == kFmtP8) {
-        const int code = load_code_p8(P.G, cell);
-        return T[P.pal_mat[code] * stride] * (double)P.pal_dens[code];
+        code = load_code_p8(G, c);
     } else {
-        const int id = __ldg(P.G.vox + cell);
-        return T[id * stride] * (double)load_density_raw(P.G, cell);
+        code = __ldg(G.vox + c);
+        dens = load_density_raw(G, c);
     }
 }
 
 template <int FMT>
-__device__ __forceinline__ int material_at(const TransportParams& P, uint32_t cell)
+__device__ __forceinline__ int material_of(const TransportParams& P, int code)
+{
+    return FMT == kFmtRaw ? code : P.pal_mat[code];
+}
+
+// Brick address split into per-axis terms (see brick_cell): cell = ax+ay+az,
+// and a step only recomputes the term of the axis it crosses.
+__device__ __forceinline__ uint32_t term_x(const Grid&, int i) { return ((uint32_t)(i >> 2) << 6) | (uint32_t)(i & 3); }
+__device__ __forceinline__ uint32_t term_y(const Grid& G, int i)
+{
+    return (uint32_t)(i >> 2) * ((uint32_t)G.nbx << 6) + ((uint32_t)(i & 3) << 2);
+}
+__device__ __forceinline__ uint32_t term_z(const Grid& G, int i)
+{
+    return (uint32_t)(i >> 2) * ((uint32_t)G.nbx * (uint32_t)G.nby << 6) + ((uint32_t)(i & 3) << 4);
+}
+
+// Issue the load of a voxel; decoding is deferred to the step that uses it
+// so the load latency overlaps a whole step.
+template <int FMT>
+__device__ __forceinline__ void prefetch(const Grid& G, uint32_t cell, uint32_t& raw, uint32_t& shift,
+                                         float& dens)
+{
+    if (FMT == kFmtP4) {
+        raw = (uint32_t)__ldg(G.vox + (cell >> 1)); // consumed one step later
+        shift = (cell & 1u) << 2;
+    } else {
+        raw = __ldg(G.vox + cell);
+        if (FMT == kFmtRaw)
+            dens = load_density_raw(G, cell);
+    }
+}
+
+template <int FMT>
+__device__ __forceinline__ int decode(uint32_t raw, uint32_t shift)
 {
     if (FMT == kFmtP4)
-        return P.pal_mat[load_code_p4(P.G, cell)];
-    if (FMT == kFmtP8)
-        return P.pal_mat[load_code_p8(P.G, cell)];
-    return __ldg(P.G.vox + cell);
+        return (int)((raw >> shift) & 0xFu);
+    return (int)raw;
 }
 
-// --------------------------------------------------------------- the walker
-// Lane-resident Siddon state (REF trace.cpp:66-103 Walker / start_walk).
+// ------------------------------------------------------------------ walker
 struct Walk {
-    double rx, ry, rz;        // ray direction (origin = photon position)
-    double tnx, tny, tnz;     // next boundary crossing per axis
-    double dtx, dty, dtz;     // per-voxel increments (march: dtx = step length)
+    double ox, oy, oz;    // ray origin
+    double rx, ry, rz;    // ray direction
+    double tnx, tny, tnz; // next boundary crossing per axis
+    double dtx, dty, dtz; // per-voxel increments (march: dtx = step length)
     double t, texit, depth, target;
-    int ix, iy, iz;           // voxel (march: ix = sample j, iy = n samples)
+    int ix, iy, iz;       // current voxel (march: ix = sample j, iy = n samples)
     int sx, sy, sz;
-    int march;                // 0 = exact Siddon, 1 = midpoint march (step_voxels > 1)
-    int hit;                  // free path: interaction inside the grid
+    uint32_t ax, ay, az;  // per-axis brick address terms of the current voxel
+    uint32_t raw;         // prefetched voxel (undecoded) ...
+    uint32_t shift;       // ... and its nibble position (P4)
+    float dens;
+    double mu_hit;        // free path: mu of the voxel it ends in
+    int march;
+    int hit;
 };
 
-// REF clip_to_grid (trace.cpp:29-56); returns false for a miss.
-__device__ __forceinline__ bool clip_to_grid(const Grid& G, V3 o, V3 d, double& t0, double& t1,
-                                             bool& bad)
-{
-    bad = !(isfinite(o.x) && isfinite(o.y) && isfinite(o.z) && isfinite(d.x) && isfinite(d.y) &&
-            isfinite(d.z));
-    if (bad)
-        return false;
-    t0 = 0.0;
-    t1 = CUDART_INF;
-    const double oo[3] = {o.x, o.y, o.z};
-    const double dd[3] = {d.x, d.y, d.z};
-    const double l[3] = {G.ox, G.oy, G.oz};
-    const double h[3] = {G.ux, G.uy, G.uz};
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        if (dd[a] == 0.0) {
-            if (oo[a] < l[a] || oo[a] >= h[a])
-                return false;
-            continue;
-        }
-        double ta = (l[a] - oo[a]) / dd[a];
-        double tb = (h[a] - oo[a]) / dd[a];
-        if (ta > tb) {
-            const double s = ta;
-            ta = tb;
-            tb = s;
-        }
-        t0 = t0 < ta ? ta : t0; // std::max(t0, ta)
-        t1 = tb < t1 ? tb : t1;
-    }
-    return t0 < t1;
-}
-
-__device__ __forceinline__ void start_axis(double p, double o, double d, double org, double hs,
-                                           double inv_h, int n, double t0, int& idx, int& step,
-                                           double& tn, double& dt)
-{
-    idx = voxel_of(p, org, inv_h, n);
-    if (d > 0.0) {
-        step = 1;
-        dt = hs / d;
-        tn = (org + (idx + 1) * hs - o) / d;
-    } else if (d < 0.0) {
-        step = -1;
-        dt = -hs / d;
-        tn = (org + idx * hs - o) / d;
-    } else {
-        step = 0;
-        dt = CUDART_INF;
-        tn = CUDART_INF;
-    }
-    while (tn <= t0 && step != 0) {
-        idx += step;
-        tn += dt;
-    }
-    // REF leaves an out-of-grid index here only in degenerate tangent cases
-    // (it would then read outside the grid); keep the device read in bounds.
-    idx = idx < 0 ? 0 : (idx > n - 1 ? n - 1 : idx);
-}
-
-// Set up the walk of ray (o, d); returns false if the ray misses the grid.
-__device__ __forceinline__ bool walk_begin(const TransportParams& P, Walk& w, V3 o, V3 d,
+template <int FMT>
+__device__ __noinline__ bool walk_begin(const TransportParams& P, Walk& w, V3 o, V3 d,
                                            double target, bool march, DevStatus* st, int bin)
 {
     double t0, t1;
     bool bad;
+    w.ox = o.x;
+    w.oy = o.y;
+    w.oz = o.z;
     w.rx = d.x;
     w.ry = d.y;
     w.rz = d.z;
+    w.hit = 0;
+    w.depth = 0.0;
     if (!clip_to_grid(P.G, o, d, t0, t1, bad)) {
         if (bad)
             raise(st, XS_E_INVALID_ARGUMENT, 0, bin, 0.0, 0.0);
         return false;
     }
-    w.depth = 0.0;
     w.target = target;
-    w.hit = 0;
     w.texit = t1;
     w.t = t0;
     if (march) { // REF trace.cpp:116-134
         w.march = 1;
-        const double len = t1 - t0;
-        int n = (int)ceil(len / P.march_h);
+        const int n = (int)ceil((t1 - t0) / P.march_h);
         w.iy = n < 1 ? 1 : n;
         w.ix = 0;
         w.dtx = P.march_h;
@@ -323,28 +263,35 @@ __device__ __forceinline__ bool walk_begin(const TransportParams& P, Walk& w, V3
     start_axis(p.x, o.x, d.x, G.ox, G.hx, G.ihx, G.nx, t0, w.ix, w.sx, w.tnx, w.dtx);
     start_axis(p.y, o.y, d.y, G.oy, G.hy, G.ihy, G.ny, t0, w.iy, w.sy, w.tny, w.dty);
     start_axis(p.z, o.z, d.z, G.oz, G.hz, G.ihz, G.nz, t0, w.iz, w.sz, w.tnz, w.dtz);
+    w.ax = term_x(G, w.ix);
+    w.ay = term_y(G, w.iy);
+    w.az = term_z(G, w.iz);
+    prefetch<FMT>(G, w.ax + w.ay + w.az, w.raw, w.shift, w.dens);
     return true;
 }
 
-// One voxel of the walk.  Returns true while the walk continues.
-// Siddon: REF trace.cpp:136-155 (attenuation) / :202-228 (free path).
-template <int FMT>
-__device__ __forceinline__ bool walk_step(const TransportParams& P, const double* T, int stride,
-                                          Walk& w, V3 o)
+// One voxel (REF trace.cpp:136-155 / :202-228).  Branch-free axis advance;
+// the next voxel's load is issued before this step's fp64 chain and decoded
+// only in the next step.
+template <int FMT, bool REG>
+__device__ __forceinline__ bool walk_step(const TransportParams& P, const MuTab<FMT, REG>& tab,
+                                          Walk& w)
 {
     const Grid& G = P.G;
-    if (w.march) {
+    if (w.march) { // REF trace.cpp:124-133
         const double ta = w.t + w.ix * w.dtx;
-        const double tb = w.texit < ta + w.dtx ? w.texit : ta + w.dtx; // std::min
+        const double tb = w.texit < ta + w.dtx ? w.texit : ta + w.dtx;
         const double tm = 0.5 * (ta + tb);
-        const V3 p = o + v3(w.rx, w.ry, w.rz) * tm;
-        const int ix = voxel_of(p.x, G.ox, G.ihx, G.nx);
-        const int iy = voxel_of(p.y, G.oy, G.ihy, G.ny);
-        const int iz = voxel_of(p.z, G.oz, G.ihz, G.nz);
-        w.depth += mu_at<FMT>(P, T, stride, brick_cell(G, ix, iy, iz)) * (tb - ta);
+        const double px = w.ox + w.rx * tm, py = w.oy + w.ry * tm, pz = w.oz + w.rz * tm;
+        int code;
+        float dens = 0.f;
+        fetch<FMT>(G, voxel_of(px, G.ox, G.ihx, G.nx), voxel_of(py, G.oy, G.ihy, G.ny),
+                   voxel_of(pz, G.oz, G.ihz, G.nz), code, dens);
+        w.depth += tab.mu(P, code, dens) * (tb - ta);
         return ++w.ix < w.iy;
     }
-    const double mu = mu_at<FMT>(P, T, stride, brick_cell(G, w.ix, w.iy, w.iz));
+    const uint32_t raw = w.raw, shift = w.shift;
+    const float dens = w.dens;
     double tn = w.tnx;
     if (w.tny < tn)
         tn = w.tny;
@@ -352,51 +299,55 @@ __device__ __forceinline__ bool walk_step(const TransportParams& P, const double
         tn = w.tnz;
     if (w.texit < tn)
         tn = w.texit;
+    const bool cx = w.tnx == tn, cy = w.tny == tn, cz = w.tnz == tn;
+    const int nix = cx ? w.ix + w.sx : w.ix;
+    const int niy = cy ? w.iy + w.sy : w.iy;
+    const int niz = cz ? w.iz + w.sz : w.iz;
+    const bool inside = (tn < w.texit) && (uint32_t)nix < (uint32_t)G.nx &&
+                        (uint32_t)niy < (uint32_t)G.ny && (uint32_t)niz < (uint32_t)G.nz;
+    const uint32_t nax = cx ? term_x(G, nix) : w.ax;
+    const uint32_t nay = cy ? term_y(G, niy) : w.ay;
+    const uint32_t naz = cz ? term_z(G, niz) : w.az;
+    if (inside)
+        prefetch<FMT>(G, nax + nay + naz, w.raw, w.shift, w.dens);
+
+    const double mu = tab.mu(P, decode<FMT>(raw, shift), dens);
     const double seg = mu * (tn - w.t);
-    if (w.depth + seg >= w.target) { // free path ends inside this voxel
+    const double nd = w.depth + seg;
+    if (nd >= w.target) { // free path ends inside this voxel; t_hit in hit_t()
         w.hit = 1;
-        w.t = (mu > 0.0) ? w.t + (w.target - w.depth) / mu : tn; // t_hit
+        w.mu_hit = mu;
+        w.texit = tn;
         return false;
     }
-    w.depth += seg;
+    w.depth = nd;
     w.t = tn;
-    if (w.t >= w.texit)
-        return false;
-    if (w.tnx == tn) {
-        w.ix += w.sx;
-        if (w.ix < 0 || w.ix >= G.nx)
-            return false;
-        w.tnx += w.dtx;
-    }
-    if (w.tny == tn) {
-        w.iy += w.sy;
-        if (w.iy < 0 || w.iy >= G.ny)
-            return false;
-        w.tny += w.dty;
-    }
-    if (w.tnz == tn) {
-        w.iz += w.sz;
-        if (w.iz < 0 || w.iz >= G.nz)
-            return false;
-        w.tnz += w.dtz;
-    }
-    return true;
+    w.tnx = cx ? w.tnx + w.dtx : w.tnx;
+    w.tny = cy ? w.tny + w.dty : w.tny;
+    w.tnz = cz ? w.tnz + w.dtz : w.tnz;
+    w.ix = nix;
+    w.iy = niy;
+    w.iz = niz;
+    w.ax = nax;
+    w.ay = nay;
+    w.az = naz;
+    return inside;
+}
+
+// REF trace.cpp:212-213: the interaction point's ray parameter.
+__device__ __forceinline__ double hit_t(const Walk& w)
+{
+    return (w.mu_hit > 0.0) ? w.t + (w.target - w.depth) / w.mu_hit : w.texit;
 }
 
 // ------------------------------------------------------ shared accumulators
-struct SAcc {
-    unsigned long long* bins;   // n_bins * 8
-    unsigned long long* ledger; // 24
-    unsigned long long* diag;   // 8
-};
-
 __device__ __forceinline__ void sadd(unsigned long long* p, uint64_t v)
 {
     if (v)
         atomicAdd(p, (unsigned long long)v);
 }
 
-__device__ __forceinline__ bool tally_shared(unsigned long long* slot, double x, int log2_unit)
+__device__ __forceinline__ bool tally_limbs(unsigned long long* slot, double x, int log2_unit)
 {
     uint64_t l0, l1, l2;
     if (!quantize(ldexp(x, -log2_unit), l0, l1, l2))
@@ -407,620 +358,583 @@ __device__ __forceinline__ bool tally_shared(unsigned long long* slot, double x,
     return true;
 }
 
-__device__ __forceinline__ void ledger_add(const TransportParams& P, const SAcc& S, int k,
+struct Block {
+    unsigned long long* bins;   // n_bins * 8
+    unsigned long long* ledger; // 24
+    unsigned long long* diag;   // 8
+};
+
+__device__ __forceinline__ void ledger_add(const TransportParams& P, const Block& B, int k,
                                            double w, DevStatus* st, int bin)
 {
-    if (w != 0.0 && !tally_shared(S.ledger + 4 * k, w, P.log2_w))
+    if (w != 0.0 && !tally_limbs(B.ledger + 4 * k, w, P.log2_w))
         raise(st, XS_E_RUNTIME, kErrTallyOverflow, bin, 0.0, w);
+}
+
+__device__ __forceinline__ void push(WarpHdr* hdr, uint64_t* q, uint32_t qmask, uint64_t task)
+{
+    const uint32_t i = atomicAdd(&hdr->tail, 1u);
+    q[i & qmask] = task;
+}
+
+__device__ __forceinline__ uint64_t make_task(int type, int slot, uint32_t pixel)
+{
+    return ((uint64_t)pixel << 32) | ((uint64_t)type << 16) | (uint64_t)slot;
+}
+
+// History end (REF run_history :225-241): bin statistics from the exact
+// fixed-point history total, per-pixel grouping for the variance, free slot.
+__device__ __noinline__ void finalize_history(const TransportParams& P, const Block& B, Slot* slots,
+                                              WarpHdr* hdr, int s, uint64_t var_base, DevStatus* st)
+{
+    Slot& S = slots[s];
+    const double t = dequantize(S.T[0], S.T[1], S.T[2], P.log2_img);
+    unsigned long long* bs = B.bins + 8 * S.bin;
+    if (t != 0.0) {
+        if (!tally_limbs(bs, t, P.log2_img) || !tally_limbs(bs + 3, t * t, 2 * P.log2_img))
+            raise(st, XS_E_RUNTIME, kErrTallyOverflow, S.bin, S.E, t);
+    }
+    if (P.track_var) {
+        const uint32_t* vp = P.var_pix + var_base;
+        const double* vv = P.var_val + var_base;
+        const int n = S.n_var < P.var_cap ? S.n_var : P.var_cap;
+        for (int a = 0; a < n; ++a) {
+            const uint32_t pa = vp[a];
+            bool dup = false;
+            for (int b = 0; b < a; ++b)
+                if (vp[b] == pa) {
+                    dup = true;
+                    break;
+                }
+            if (dup)
+                continue;
+            double c = vv[a];
+            for (int b = a + 1; b < n; ++b)
+                if (vp[b] == pa)
+                    c += vv[b];
+            if (!tally_global(P.accum + P.off_var + 4ull * pa, c * c, 2 * P.log2_img))
+                raise(st, XS_E_RUNTIME, kErrTallyOverflow, S.bin, S.E, c);
+        }
+    }
+    sadd(B.diag + 2, 1);
+    atomicOr(&hdr->free_mask, 1ull << s);
+}
+
+__device__ __forceinline__ void end_history(const TransportParams& P, const Block& B, Slot* slots,
+                                            WarpHdr* hdr, int s, uint64_t var_base, DevStatus* st)
+{
+    __threadfence_block(); // this lane's tallies / scratch before the hand-off
+    if (atomicSub(&slots[s].pending, 1) == 1)
+        finalize_history(P, B, slots, hdr, s, var_base, st);
+}
+
+// Free-path completion: the reference's per-history event logic
+// (run_history :141-223) on the history's own Philox stream.
+template <int FMT>
+__device__ __noinline__ void history_event(const TransportParams& P, const Block& B, Slot* slots,
+                                           WarpHdr* hdr, uint64_t* q, uint32_t qmask, int s,
+                                           bool hit, double t_hit, int vix, int viy, int viz,
+                                           uint64_t var_base, DevStatus* st)
+{
+    Slot& S = slots[s];
+    Rng rng = load_rng(S);
+    const int bin = S.bin;
+    const double W = S.W;
+    if (!hit) {
+        ledger_add(P, B, 1, W, st, bin);
+        end_history(P, B, slots, hdr, s, var_base, st);
+        return;
+    }
+    const V3 dir = v3(S.dx, S.dy, S.dz);
+    const V3 pos = v3(S.px, S.py, S.pz) + dir * t_hit;
+    int code;
+    float dens;
+    fetch<FMT>(P.G, vix, viy, viz, code, dens);
+    const int mat = material_of<FMT>(P, code);
+    const MatDesc& md = P.mats[mat];
+    const double E = S.E;
+    // select_interaction (cross_sections.cpp:81-96)
+    const double pe = loglog_or_fail(P, md.pe, E, st, bin);
+    const double incoh = loglog_or_fail(P, md.incoh, E, st, bin);
+    const double coh = loglog_or_fail(P, md.coh, E, st, bin);
+    const double total = pe + incoh + coh;
+    if (!(total > 0.0))
+        raise(st, XS_E_RUNTIME, kErrSigmaAll, bin, E, (double)mat);
+    const double u = rng_uniform(rng, P.k0, P.k1, P.angle) * total;
+    const int kind = u < pe ? K_PE : (u < pe + incoh ? K_COMPTON : K_RAYLEIGH);
+    if (kind == K_PE) {
+        ledger_add(P, B, 2, W, st, bin);
+        store_rng(S, rng);
+        end_history(P, B, slots, hdr, s, var_base, st);
+        return;
+    }
+    S.px = pos.x;
+    S.py = pos.y;
+    S.pz = pos.z;
+    S.ox = pos.x;
+    S.oy = pos.y;
+    S.oz = pos.z;
+    S.ix = dir.x;
+    S.iy = dir.y;
+    S.iz = dir.z;
+    S.e_in = E;
+    S.kind = kind;
+    S.mat = mat;
+    S.w_split = W / P.splitting;
+    atomicAdd(&S.pending, P.splitting);
+    for (int k = 0; k < P.splitting; ++k) { // REF :162-164 pixel draws
+        int iu = (int)(rng_uniform(rng, P.k0, P.k1, P.angle) * P.nu);
+        int iv = (int)(rng_uniform(rng, P.k0, P.k1, P.angle) * P.nv);
+        iu = iu < P.nu - 1 ? iu : P.nu - 1;
+        iv = iv < P.nv - 1 ? iv : P.nv - 1;
+        push(hdr, q, qmask, make_task(T_SCORE, s, (uint32_t)(iv * P.nu + iu)));
+    }
+    // continuation (REF :195-205)
+    V3 ndir;
+    double nE = E;
+    if (kind == K_COMPTON) { // samplers.cpp:32-52
+        const double alpha = E / kMec2;
+        const double q_max = momentum_transfer(E, kPi);
+        const double s_max = form_S(P, md, q_max);
+        double theta = 0.0, ap = 0.0, phi = 0.0;
+        if (!(s_max > 0.0)) {
+            raise(st, XS_E_RUNTIME, kErrComptonS, bin, E, 0.0);
+        } else {
+            for (;;) {
+                const double t = 1.0 + 2.0 * alpha; // kahn_sample_cos_theta, samplers.cpp:12-30
+                double cos_th;
+                for (;;) {
+                    const double r1 = rng_uniform(rng, P.k0, P.k1, P.angle);
+                    const double r2 = rng_uniform(rng, P.k0, P.k1, P.angle);
+                    const double r3 = rng_uniform(rng, P.k0, P.k1, P.angle);
+                    if (r1 <= t / (t + 8.0)) {
+                        const double x = 1.0 + 2.0 * alpha * r2;
+                        if (r3 <= 4.0 * (1.0 / x - 1.0 / (x * x))) {
+                            cos_th = 1.0 - (x - 1.0) / alpha;
+                            break;
+                        }
+                    } else {
+                        const double x = t / (1.0 + 2.0 * alpha * r2);
+                        const double ct = 1.0 - (x - 1.0) / alpha;
+                        if (r3 <= 0.5 * (ct * ct + 1.0 / x)) {
+                            cos_th = ct;
+                            break;
+                        }
+                    }
+                }
+                const double cc = cos_th < -1.0 ? -1.0 : (1.0 < cos_th ? 1.0 : cos_th);
+                theta = nl_acos(cc);
+                const double sv = form_S(P, md, momentum_transfer(E, theta));
+                if (rng_uniform(rng, P.k0, P.k1, P.angle) * s_max <= sv) {
+                    ap = alpha / (1.0 + alpha * (1.0 - nl_cos(theta)));
+                    phi = 2.0 * kPi * rng_uniform(rng, P.k0, P.k1, P.angle);
+                    break;
+                }
+            }
+        }
+        ndir = rotate_direction(dir, theta, phi);
+        nE = ap * kMec2;
+    } else { // samplers.cpp:106-125
+        const double q_max = momentum_transfer(E, kPi);
+        const double tot = cumulative_mass(P, md, q_max);
+        double theta = 0.0, phi = 0.0;
+        if (!(tot > 0.0)) {
+            raise(st, XS_E_RUNTIME, kErrRayleighF, bin, E, 0.0);
+        } else {
+            const double scale = kHc / E;
+            for (;;) {
+                const double qq = invert_mass(P, md, rng_uniform(rng, P.k0, P.k1, P.angle) * tot, q_max);
+                const double sh = 1.0 < qq * scale ? 1.0 : qq * scale;
+                const double cos_th = 1.0 - 2.0 * sh * sh;
+                if (rng_uniform(rng, P.k0, P.k1, P.angle) * 2.0 <= 1.0 + cos_th * cos_th) {
+                    const double cc = cos_th < -1.0 ? -1.0 : (1.0 < cos_th ? 1.0 : cos_th);
+                    theta = nl_acos(cc);
+                    phi = 2.0 * kPi * rng_uniform(rng, P.k0, P.k1, P.angle);
+                    break;
+                }
+            }
+        }
+        ndir = rotate_direction(dir, theta, phi);
+    }
+    S.dx = ndir.x;
+    S.dy = ndir.y;
+    S.dz = ndir.z;
+    S.E = nE;
+    const int gen = ++S.gen;
+    bool alive = true;
+    double Wn = W;
+    if (gen >= P.max_inter) { // REF :207-211
+        ledger_add(P, B, 3, W, st, bin);
+        alive = false;
+    } else if (S.wmin > 0.0 && W < S.wmin) { // REF :213-222
+        if (rng_uniform(rng, P.k0, P.k1, P.angle) < P.survival) {
+            const double boosted = W / P.survival;
+            ledger_add(P, B, 5, boosted - W, st, bin);
+            Wn = boosted;
+        } else {
+            ledger_add(P, B, 4, W, st, bin);
+            alive = false;
+        }
+    }
+    if (alive) {
+        S.W = Wn;
+        S.target = -nl_log(rng_uniform(rng, P.k0, P.k1, P.angle));
+        store_rng(S, rng);
+        push(hdr, q, qmask, make_task(T_FREE, s, 0));
+    } else {
+        store_rng(S, rng);
+        end_history(P, B, slots, hdr, s, var_base, st);
+    }
+}
+
+// History start (REF run_history :120-138, sample_emission :73-87).
+__device__ __noinline__ void history_start(const TransportParams& P, const Block& B, Slot* slots,
+                                           WarpHdr* hdr, uint64_t* q, uint32_t qmask,
+                                           const uint64_t* sstart, int s, uint64_t h, DevStatus* st)
+{
+    Slot& S = slots[s];
+    int lo = 0, hi = P.n_bins; // last bin b with start[b] <= h (skips empty bins)
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (sstart[mid] <= h)
+            lo = mid;
+        else
+            hi = mid;
+    }
+    const int bin = lo;
+    Rng rng;
+    rng_init(rng, (uint32_t)(h - sstart[lo]), (uint32_t)lo);
+    const double u1 = rng_uniform(rng, P.k0, P.k1, P.angle);
+    const double u2 = rng_uniform(rng, P.k0, P.k1, P.angle);
+    const double xu = (u1 - 0.5) * P.nu * P.pitch;
+    const double xv = (u2 - 0.5) * P.nv * P.pitch;
+    const V3 c = v3(P.center[0], P.center[1], P.center[2]);
+    const V3 ua = v3(P.uaxis[0], P.uaxis[1], P.uaxis[2]);
+    const V3 target = (c + ua * xu) + v3(0.0, 0.0, 1.0) * xv;
+    const V3 src = v3(P.src[0], P.src[1], P.src[2]);
+    const V3 delta = target - src;
+    const double d2 = dot(delta, delta);
+    const V3 dir = delta / sqrt(d2);
+    const double cos_psi = -dot(dir, v3(P.normal[0], P.normal[1], P.normal[2]));
+    const double em_weight = P.det_area * cos_psi / d2;
+    const double w0 = __ldg(P.bin_weight + bin) * em_weight / (double)__ldg(P.bin_count + bin);
+    S.px = src.x;
+    S.py = src.y;
+    S.pz = src.z;
+    S.dx = dir.x;
+    S.dy = dir.y;
+    S.dz = dir.z;
+    S.E = __ldg(P.bin_energy + bin);
+    S.W = w0;
+    S.wmin = P.wmin_rel * w0;
+    S.T[0] = S.T[1] = S.T[2] = 0ull;
+    S.bin = bin;
+    S.gen = 0;
+    S.pending = 1;
+    S.n_var = 0;
+    ledger_add(P, B, 0, w0, st, bin);
+    S.target = -nl_log(rng_uniform(rng, P.k0, P.k1, P.angle));
+    store_rng(S, rng);
+    push(hdr, q, qmask, make_task(T_FREE, s, 0));
+    atomicAnd(&hdr->free_mask, ~(1ull << s));
+}
+
+// Scoring-ray set-up (REF run_history :166-183): geometry, p(theta), e_out,
+// response; returns the score prefactor (point_detector_score without exp(-tau)).
+__device__ __noinline__ double score_setup(const TransportParams& P, const Slot& S, uint32_t pix,
+                                              V3& o, V3& to_det, double& e_out, DevStatus* st)
+{
+    const int iu = (int)(pix % (uint32_t)P.nu);
+    const int iv = (int)(pix / (uint32_t)P.nu);
+    const double du = (iu + 0.5 - 0.5 * P.nu) * P.pitch;
+    const double dv = (iv + 0.5 - 0.5 * P.nv) * P.pitch;
+    const V3 c = v3(P.center[0], P.center[1], P.center[2]);
+    const V3 ua = v3(P.uaxis[0], P.uaxis[1], P.uaxis[2]);
+    const V3 px = (c + ua * du) + v3(0.0, 0.0, 1.0) * dv;
+    o = v3(S.ox, S.oy, S.oz);
+    const V3 delta = px - o;
+    const double d2 = dot(delta, delta);
+    to_det = delta / sqrt(d2);
+    double cos_t = dot(v3(S.ix, S.iy, S.iz), to_det);
+    cos_t = cos_t < -1.0 ? -1.0 : (1.0 < cos_t ? 1.0 : cos_t);
+    const double theta = nl_acos(cos_t);
+    const MatDesc& md = P.mats[S.mat];
+    const double E = S.e_in;
+    double p_dir;
+    const double r0 = kR0;
+    if (S.kind == K_COMPTON) { // cross_sections.cpp:56-66
+        const double sigma = loglog_or_fail(P, md.incoh, E, st, S.bin) * kBarn;
+        if (!(sigma > 0.0))
+            raise(st, XS_E_RUNTIME, kErrSigmaIncoh, S.bin, E, 0.0);
+        p_dir = kPi * r0 * r0 / sigma * kn_core(E, theta) * form_S(P, md, momentum_transfer(E, theta));
+        e_out = E * compton_ratio(E, theta);
+    } else { // cross_sections.cpp:68-79
+        const double sigma = loglog_or_fail(P, md.coh, E, st, S.bin) * kBarn;
+        if (!(sigma > 0.0))
+            raise(st, XS_E_RUNTIME, kErrSigmaCoh, S.bin, E, 0.0);
+        const double c2 = nl_cos(theta);
+        const double f = form_F(P, md, momentum_transfer(E, theta));
+        p_dir = kPi * r0 * r0 / sigma * (1.0 + c2 * c2) * f * f;
+        e_out = E;
+    }
+    double dep = 0.0;
+    if (!tab_linear(mtab(P, P.resp_deposit), e_out, dep))
+        raise(st, XS_E_OUT_OF_RANGE, kErrTableRange, S.bin, e_out, 1.0);
+    return dep / e_out * p_dir * S.w_split * P.n_pixels / (2.0 * kPi * d2);
 }
 
 } // namespace
 
 // =================================================================== kernel
-template <int FMT>
-__global__ void __launch_bounds__(256, 2) transport_kernel(const __grid_constant__ TransportParams P)
+template <int FMT, bool REG>
+__global__ void __launch_bounds__(kBlock, 4) transport_kernel(const __grid_constant__ TransportParams P)
 {
     extern __shared__ __align__(16) unsigned char smem[];
-    const int n_tab = FMT == kFmtP4 ? P.n_pal : P.n_mats;
-    const int stride = blockDim.x;
-    double* Tbase = reinterpret_cast<double*>(smem);
-    SAcc S;
-    S.bins = reinterpret_cast<unsigned long long*>(Tbase + (size_t)n_tab * stride);
-    S.ledger = S.bins + 8 * P.n_bins;
-    S.diag = S.ledger + 24;
-    uint64_t* sstart = reinterpret_cast<uint64_t*>(S.diag + 8);
-
-    for (int i = threadIdx.x; i < 8 * P.n_bins + 32; i += blockDim.x)
-        S.bins[i] = 0ull;
-    for (int i = threadIdx.x; i <= P.n_bins; i += blockDim.x)
-        sstart[i] = P.bin_start[i];
-    __syncthreads();
-
-    double* T = Tbase + threadIdx.x;
-    DevStatus* st = P.status;
+    const int H = P.slots_per_warp;
+    const uint32_t qmask = (uint32_t)P.queue_len - 1u; // power of two
+    const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
-    const uint64_t gtid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
 
-    // warp-uniform history queue
-    uint64_t wq_next = 0, wq_end = 0;
+    // ---- carve shared memory
+    Block B;
+    B.bins = reinterpret_cast<unsigned long long*>(smem);
+    B.ledger = B.bins + 8 * P.n_bins;
+    B.diag = B.ledger + 24;
+    uint64_t* sstart = reinterpret_cast<uint64_t*>(B.diag + 8);
+    unsigned char* p = reinterpret_cast<unsigned char*>(sstart + P.n_bins + 1);
+    const size_t warp_bytes = (size_t)H * sizeof(Slot) + sizeof(WarpHdr) + (size_t)P.queue_len * 8;
+    unsigned char* wbase = p + (size_t)warp * warp_bytes;
+    Slot* slots = reinterpret_cast<Slot*>(wbase);
+    WarpHdr* hdr = reinterpret_cast<WarpHdr*>(wbase + (size_t)H * sizeof(Slot));
+    uint64_t* q = reinterpret_cast<uint64_t*>(hdr + 1);
+    MuTab<FMT, REG> tab;
+    tab.T = reinterpret_cast<double*>(p + (size_t)kWarps * warp_bytes) + threadIdx.x;
+    tab.energy = -1.0;
+
+    for (int i = threadIdx.x; i < 8 * P.n_bins + 32; i += blockDim.x)
+        B.bins[i] = 0ull;
+    for (int i = threadIdx.x; i <= P.n_bins; i += blockDim.x)
+        sstart[i] = P.bin_start[i];
+    const unsigned long long all_free = H >= 64 ? ~0ull : ((1ull << H) - 1ull);
+    if (lane == 0) {
+        hdr->tail = 0;
+        hdr->free_mask = all_free;
+    }
+    __syncthreads();
+
+    DevStatus* st = P.status;
+    const uint64_t gwarp = (uint64_t)blockIdx.x * kWarps + warp;
+    const bool march = P.step_voxels > 1;
+
+    uint32_t head = 0;                // warp-uniform queue head
+    uint64_t wq_next = 0, wq_end = 0; // warp-uniform history reservation
     bool pool_empty = false;
 
-    // lane state
-    int state = ST_FETCH;
-    int post = 0; // state to enter when the current walk ends
-    Rng rng;
-    int bin = 0;
-    V3 pos = v3(0, 0, 0), dir = v3(0, 0, 0);
-    double energy = 0.0, weight = 0.0, w_min = 0.0, htotal = 0.0, w_split = 0.0, pre = 0.0;
-    double T_energy = -1.0;
-    int generation = 0, kind = 0, mat = 0, split_left = 0, pixel = 0, n_var = 0;
-    uint32_t fp_steps = 0, sc_steps = 0, n_rays = 0, n_inter = 0;
+    int ttype = T_NONE, tslot = 0;
+    uint32_t tpix = 0;
+    double tpre = 0.0;
+    bool walking = false;
     Walk w;
     w.march = 0;
-
-    const bool march = P.step_voxels > 1;
-    const double n_pixels = P.n_pixels;
+    uint32_t c_fp = 0, c_sc = 0, c_rays = 0, c_int = 0;
 
     for (;;) {
-        // ---------------------------------------------------- fetch phase
-        unsigned need = __ballot_sync(kFull, state == ST_FETCH);
-        while (need) {
-            if (wq_next >= wq_end) {
-                if (pool_empty) {
-                    if (state == ST_FETCH)
-                        state = ST_DONE;
-                    break;
-                }
-                unsigned long long base = 0;
-                if (lane == 0)
-                    base = atomicAdd(P.pool, (unsigned long long)P.grab);
-                base = __shfl_sync(kFull, base, 0);
-                wq_next = P.h_begin + base;
-                wq_end = wq_next + (uint64_t)P.grab;
-                if (wq_end > P.h_end)
-                    wq_end = P.h_end;
-                if (wq_next >= P.h_end) {
-                    pool_empty = true;
-                    continue;
-                }
-            }
-            const uint64_t avail = wq_end - wq_next;
-            const int rank = __popc(need & lt_mask);
-            if (state == ST_FETCH && (uint64_t)rank < avail) {
-                const uint64_t h = wq_next + rank;
-                // bin = last b with start[b] <= h (empty bins are skipped)
-                int lo = 0, hi = P.n_bins;
-                while (hi - lo > 1) {
-                    const int mid = (lo + hi) >> 1;
-                    if (sstart[mid] <= h)
-                        lo = mid;
-                    else
-                        hi = mid;
-                }
-                bin = lo;
-                rng_init(rng, (uint32_t)(h - sstart[lo]), (uint32_t)lo);
-                state = ST_INIT;
-            }
-            const uint64_t used = (uint64_t)__popc(need) < avail ? (uint64_t)__popc(need) : avail;
-            wq_next += used;
-            need = __ballot_sync(kFull, state == ST_FETCH);
-        }
-
-        // ---------------------------------------------------- event phase
-        while (state != ST_WALK && state != ST_DONE && state != ST_FETCH) {
-            switch (state) {
-            case ST_INIT: { // REF run_history :120-138, sample_emission :73-87
-                const double u1 = rng_uniform(rng, P.k0, P.k1, P.angle);
-                const double u2 = rng_uniform(rng, P.k0, P.k1, P.angle);
-                const double xu = (u1 - 0.5) * P.nu * P.pitch;
-                const double xv = (u2 - 0.5) * P.nv * P.pitch;
-                const V3 c = v3(P.center[0], P.center[1], P.center[2]);
-                const V3 ua = v3(P.uaxis[0], P.uaxis[1], P.uaxis[2]);
-                const V3 target = (c + ua * xu) + v3(0.0, 0.0, 1.0) * xv;
-                const V3 src = v3(P.src[0], P.src[1], P.src[2]);
-                const V3 delta = target - src;
-                const double d2 = dot(delta, delta);
-                dir = delta / sqrt(d2);
-                const double cos_psi = -dot(dir, v3(P.normal[0], P.normal[1], P.normal[2]));
-                const double em_weight = P.det_area * cos_psi / d2;
-                const double w0 = __ldg(P.bin_weight + bin) * em_weight / (double)__ldg(P.bin_count + bin);
-                w_min = P.wmin_rel * w0;
-                pos = src;
-                energy = __ldg(P.bin_energy + bin);
-                weight = w0;
-                generation = 0;
-                htotal = 0.0;
-                n_var = 0;
-                ledger_add(P, S, 0, w0, st, bin);
-                if (T_energy != energy) {
-                    fill_mu<FMT>(P, T, stride, energy, st, bin);
-                    T_energy = energy;
-                }
-                state = ST_FREE;
-                break;
-            }
-            case ST_FREE: { // REF trace.cpp:189-230 sample_free_path
-                const double u = rng_uniform(rng, P.k0, P.k1, P.angle);
-                if (T_energy != energy) {
-                    fill_mu<FMT>(P, T, stride, energy, st, bin);
-                    T_energy = energy;
-                }
-                if (walk_begin(P, w, pos, dir, -log(u), false, st, bin)) {
-                    post = ST_AFTER_FREE;
-                    state = ST_WALK;
+        // ------------------------------------------------ 1. completions
+        if (ttype != T_NONE && !walking) {
+            const uint64_t var_base = (gwarp * H + tslot) * (uint64_t)P.var_cap;
+            if (ttype == T_SCORE) { // REF run_history :178-193
+                Slot& S = slots[tslot];
+                const double x = tpre * nl_exp(-w.depth);
+                uint64_t l0 = 0, l1 = 0, l2 = 0;
+                if (!isfinite(x)) {
+                    raise(st, XS_E_RUNTIME, kErrNonFinite, S.bin, S.e_in, x);
+                } else if (!quantize(ldexp(x, -P.log2_img), l0, l1, l2)) {
+                    raise(st, XS_E_RUNTIME, kErrTallyOverflow, S.bin, S.e_in, x);
                 } else {
-                    w.hit = 0;
-                    state = ST_AFTER_FREE;
-                }
-                break;
-            }
-            case ST_AFTER_FREE: { // REF run_history :141-160
-                if (!w.hit) {
-                    ledger_add(P, S, 1, weight, st, bin);
-                    state = ST_END;
-                    break;
-                }
-                const uint32_t cell = brick_cell(P.G, w.ix, w.iy, w.iz);
-                pos = pos + v3(w.rx, w.ry, w.rz) * w.t;
-                mat = material_at<FMT>(P, cell);
-                ++n_inter;
-                const MatDesc& md = P.mats[mat];
-                // select_interaction (cross_sections.cpp:81-96)
-                const double pe = loglog_or_fail(P, md.pe, energy, st, bin);
-                const double incoh = loglog_or_fail(P, md.incoh, energy, st, bin);
-                const double coh = loglog_or_fail(P, md.coh, energy, st, bin);
-                const double total = pe + incoh + coh;
-                if (!(total > 0.0))
-                    raise(st, XS_E_RUNTIME, kErrSigmaAll, bin, energy, (double)mat);
-                const double u = rng_uniform(rng, P.k0, P.k1, P.angle) * total;
-                kind = u < pe ? K_PE : (u < pe + incoh ? K_COMPTON : K_RAYLEIGH);
-                if (kind == K_PE) {
-                    ledger_add(P, S, 2, weight, st, bin);
-                    state = ST_END;
-                    break;
-                }
-                w_split = weight / P.splitting;
-                split_left = P.splitting;
-                state = ST_SCORE;
-                break;
-            }
-            case ST_SCORE: { // REF run_history :162-183
-                int iu = (int)(rng_uniform(rng, P.k0, P.k1, P.angle) * P.nu);
-                int iv = (int)(rng_uniform(rng, P.k0, P.k1, P.angle) * P.nv);
-                iu = iu < P.nu - 1 ? iu : P.nu - 1;
-                iv = iv < P.nv - 1 ? iv : P.nv - 1;
-                const double du = (iu + 0.5 - 0.5 * P.nu) * P.pitch;
-                const double dv = (iv + 0.5 - 0.5 * P.nv) * P.pitch;
-                const V3 c = v3(P.center[0], P.center[1], P.center[2]);
-                const V3 ua = v3(P.uaxis[0], P.uaxis[1], P.uaxis[2]);
-                const V3 pix = (c + ua * du) + v3(0.0, 0.0, 1.0) * dv;
-                const V3 delta = pix - pos;
-                const double d2 = dot(delta, delta);
-                const V3 to_det = delta / sqrt(d2);
-                double cos_t = dot(dir, to_det);
-                cos_t = cos_t < -1.0 ? -1.0 : (1.0 < cos_t ? 1.0 : cos_t);
-                const double theta = acos(cos_t);
-                const MatDesc& md = P.mats[mat];
-                double p_dir, e_out;
-                const double r0 = kR0;
-                if (kind == K_COMPTON) { // cross_sections.cpp:56-66
-                    const double sigma = loglog_or_fail(P, md.incoh, energy, st, bin) * kBarn;
-                    if (!(sigma > 0.0))
-                        raise(st, XS_E_RUNTIME, kErrSigmaIncoh, bin, energy, 0.0);
-                    p_dir = kPi * r0 * r0 / sigma * kn_core(energy, theta) *
-                            form_S(P, md, momentum_transfer(energy, theta));
-                    e_out = energy * compton_ratio(energy, theta);
-                } else { // cross_sections.cpp:68-79
-                    const double sigma = loglog_or_fail(P, md.coh, energy, st, bin) * kBarn;
-                    if (!(sigma > 0.0))
-                        raise(st, XS_E_RUNTIME, kErrSigmaCoh, bin, energy, 0.0);
-                    const double c2 = cos(theta);
-                    const double f = form_F(P, md, momentum_transfer(energy, theta));
-                    p_dir = kPi * r0 * r0 / sigma * (1.0 + c2 * c2) * f * f;
-                    e_out = energy;
-                }
-                double dep = 0.0;
-                if (!tab_linear(mtab(P, P.resp_deposit), e_out, dep))
-                    raise(st, XS_E_OUT_OF_RANGE, kErrTableRange, bin, e_out, 1.0);
-                const double rf = dep / e_out;
-                // REF point_detector_score :66-71 without the exp(-tau) factor
-                pre = rf * p_dir * w_split * n_pixels / (2.0 * kPi * d2);
-                pixel = iv * P.nu + iu;
-                if (T_energy != e_out) { // REF trace_attenuation builds MuField(e_out)
-                    fill_mu<FMT>(P, T, stride, e_out, st, bin);
-                    T_energy = e_out;
-                }
-                ++n_rays;
-                if (walk_begin(P, w, pos, to_det, CUDART_INF, march, st, bin)) {
-                    post = ST_AFTER_SCORE;
-                    state = ST_WALK;
-                } else {
-                    w.depth = 0.0;
-                    state = ST_AFTER_SCORE;
-                }
-                break;
-            }
-            case ST_AFTER_SCORE: { // REF run_history :178-193
-                const double x = pre * exp(-w.depth);
-                if (!isfinite(x))
-                    raise(st, XS_E_RUNTIME, kErrNonFinite, bin, energy, x);
-                else if (!tally_global(P.accum + P.off_image + 4ull * (uint64_t)pixel, x, P.log2_img))
-                    raise(st, XS_E_RUNTIME, kErrTallyOverflow, bin, energy, x);
-                htotal += x;
-                if (P.track_var && n_var < P.var_cap) {
-                    P.var_pix[gtid * P.var_cap + n_var] = (uint32_t)pixel;
-                    P.var_val[gtid * P.var_cap + n_var] = x;
-                    ++n_var;
-                }
-                state = --split_left > 0 ? ST_SCORE : ST_CONT;
-                break;
-            }
-            case ST_CONT: { // REF run_history :195-223
-                const MatDesc& md = P.mats[mat];
-                if (kind == K_COMPTON) { // samplers.cpp:32-52
-                    const double alpha = energy / kMec2;
-                    const double q_max = momentum_transfer(energy, kPi);
-                    const double s_max = form_S(P, md, q_max);
-                    if (!(s_max > 0.0)) {
-                        raise(st, XS_E_RUNTIME, kErrComptonS, bin, energy, 0.0);
-                        state = ST_END;
-                        break;
-                    }
-                    double theta = 0.0, ap = 0.0, phi = 0.0;
-                    for (;;) {
-                        // kahn_sample_cos_theta (samplers.cpp:12-30)
-                        const double t = 1.0 + 2.0 * alpha;
-                        double cos_th;
-                        for (;;) {
-                            const double r1 = rng_uniform(rng, P.k0, P.k1, P.angle);
-                            const double r2 = rng_uniform(rng, P.k0, P.k1, P.angle);
-                            const double r3 = rng_uniform(rng, P.k0, P.k1, P.angle);
-                            if (r1 <= t / (t + 8.0)) {
-                                const double x = 1.0 + 2.0 * alpha * r2;
-                                if (r3 <= 4.0 * (1.0 / x - 1.0 / (x * x))) {
-                                    cos_th = 1.0 - (x - 1.0) / alpha;
-                                    break;
-                                }
-                            } else {
-                                const double x = t / (1.0 + 2.0 * alpha * r2);
-                                const double ct = 1.0 - (x - 1.0) / alpha;
-                                if (r3 <= 0.5 * (ct * ct + 1.0 / x)) {
-                                    cos_th = ct;
-                                    break;
-                                }
-                            }
-                        }
-                        const double cc = cos_th < -1.0 ? -1.0 : (1.0 < cos_th ? 1.0 : cos_th);
-                        theta = acos(cc);
-                        const double s = form_S(P, md, momentum_transfer(energy, theta));
-                        if (rng_uniform(rng, P.k0, P.k1, P.angle) * s_max <= s) {
-                            ap = alpha / (1.0 + alpha * (1.0 - cos(theta)));
-                            phi = 2.0 * kPi * rng_uniform(rng, P.k0, P.k1, P.angle);
-                            break;
-                        }
-                    }
-                    dir = rotate_direction(dir, theta, phi);
-                    energy = ap * kMec2;
-                } else { // samplers.cpp:106-125
-                    const double q_max = momentum_transfer(energy, kPi);
-                    const double total = cumulative_mass(P, md, q_max);
-                    if (!(total > 0.0)) {
-                        raise(st, XS_E_RUNTIME, kErrRayleighF, bin, energy, 0.0);
-                        state = ST_END;
-                        break;
-                    }
-                    const double scale = kHc / energy;
-                    double theta = 0.0, phi = 0.0;
-                    for (;;) {
-                        const double q =
-                            invert_mass(P, md, rng_uniform(rng, P.k0, P.k1, P.angle) * total, q_max);
-                        const double sh = 1.0 < q * scale ? 1.0 : q * scale;
-                        const double cos_th = 1.0 - 2.0 * sh * sh;
-                        if (rng_uniform(rng, P.k0, P.k1, P.angle) * 2.0 <= 1.0 + cos_th * cos_th) {
-                            const double cc = cos_th < -1.0 ? -1.0 : (1.0 < cos_th ? 1.0 : cos_th);
-                            theta = acos(cc);
-                            phi = 2.0 * kPi * rng_uniform(rng, P.k0, P.k1, P.angle);
-                            break;
-                        }
-                    }
-                    dir = rotate_direction(dir, theta, phi);
-                }
-                ++generation;
-                if (generation >= P.max_inter) {
-                    ledger_add(P, S, 3, weight, st, bin);
-                    state = ST_END;
-                    break;
-                }
-                if (w_min > 0.0 && weight < w_min) {
-                    if (rng_uniform(rng, P.k0, P.k1, P.angle) < P.survival) {
-                        const double boosted = weight / P.survival;
-                        ledger_add(P, S, 5, boosted - weight, st, bin);
-                        weight = boosted;
-                    } else {
-                        ledger_add(P, S, 4, weight, st, bin);
-                        state = ST_END;
-                        break;
-                    }
-                }
-                state = ST_FREE;
-                break;
-            }
-            case ST_END: { // REF run_history :225-241
-                unsigned long long* bs = S.bins + 8 * bin;
-                if (htotal != 0.0) {
-                    if (!tally_shared(bs, htotal, P.log2_img) ||
-                        !tally_shared(bs + 3, htotal * htotal, 2 * P.log2_img))
-                        raise(st, XS_E_RUNTIME, kErrTallyOverflow, bin, energy, htotal);
+                    unsigned long long* img = P.accum + P.off_image + 4ull * tpix;
+                    red_add(img + 0, l0);
+                    red_add(img + 1, l1);
+                    red_add(img + 2, l2);
+                    sadd(&S.T[0], l0);
+                    sadd(&S.T[1], l1);
+                    sadd(&S.T[2], l2);
                 }
                 if (P.track_var) {
-                    const uint32_t* vp = P.var_pix + gtid * P.var_cap;
-                    const double* vv = P.var_val + gtid * P.var_cap;
-                    for (int a = 0; a < n_var; ++a) {
-                        const uint32_t pa = vp[a];
-                        bool dup = false;
-                        for (int b2 = 0; b2 < a; ++b2)
-                            if (vp[b2] == pa) {
-                                dup = true;
-                                break;
-                            }
-                        if (dup)
-                            continue;
-                        double c = vv[a];
-                        for (int b2 = a + 1; b2 < n_var; ++b2)
-                            if (vp[b2] == pa)
-                                c += vv[b2];
-                        if (!tally_global(P.accum + P.off_var + 4ull * pa, c * c, 2 * P.log2_img))
-                            raise(st, XS_E_RUNTIME, kErrTallyOverflow, bin, energy, c);
+                    const int k = atomicAdd(&S.n_var, 1);
+                    if (k < P.var_cap) {
+                        P.var_pix[var_base + k] = tpix;
+                        P.var_val[var_base + k] = x;
                     }
                 }
-                sadd(S.diag + 0, fp_steps);
-                sadd(S.diag + 1, sc_steps);
-                sadd(S.diag + 2, 1);
-                sadd(S.diag + 3, n_rays);
-                sadd(S.diag + 4, n_inter);
-                fp_steps = sc_steps = n_rays = n_inter = 0;
-                // abort the launch on the first device error
-                state = *(volatile int32_t*)&st->code != 0 ? ST_DONE : ST_FETCH;
-                break;
+                end_history(P, B, slots, hdr, tslot, var_base, st);
+            } else {
+                if (w.hit)
+                    ++c_int;
+                history_event<FMT>(P, B, slots, hdr, q, qmask, tslot, w.hit != 0, w.hit ? hit_t(w) : 0.0, w.ix, w.iy, w.iz,
+                                   var_base, st);
             }
-            default:
-                state = ST_DONE;
-                break;
+            ttype = T_NONE;
+        }
+        __syncwarp();
+
+        // ------------------------------------------------ 2. admit histories
+        const unsigned long long free_now = hdr->free_mask;
+        if (free_now && !pool_empty) {
+            const int n_free = __popcll(free_now);
+            int n_new = 0;
+            uint64_t first = 0;
+            while (n_new == 0 && !pool_empty) {
+                if (wq_next >= wq_end) {
+                    unsigned long long base = 0;
+                    if (lane == 0)
+                        base = atomicAdd(P.pool, (unsigned long long)P.grab);
+                    base = __shfl_sync(kFull, base, 0);
+                    wq_next = P.h_begin + base;
+                    wq_end = wq_next + (uint64_t)P.grab;
+                    if (wq_end > P.h_end)
+                        wq_end = P.h_end;
+                    if (wq_next >= P.h_end) {
+                        pool_empty = true;
+                        break;
+                    }
+                }
+                const uint64_t avail = wq_end - wq_next;
+                n_new = (uint64_t)n_free < avail ? n_free : (int)avail;
+                if (n_new > 32)
+                    n_new = 32;
+                first = wq_next;
+                wq_next += n_new;
+            }
+            if (lane < n_new) {
+                unsigned long long m = free_now; // lane-th set bit
+                for (int k = 0; k < lane; ++k)
+                    m &= m - 1;
+                const int s = __ffsll((long long)m) - 1;
+                history_start(P, B, slots, hdr, q, qmask, sstart, s, first + lane, st);
             }
         }
+        __syncwarp();
 
-        // ----------------------------------------------------- walk phase
-        unsigned walking = __ballot_sync(kFull, state == ST_WALK);
-        if (!walking) {
-            if (__ballot_sync(kFull, state != ST_DONE) == 0)
+        // ------------------------------------------------ 3. pop + start tasks
+        const uint32_t tail = *(volatile uint32_t*)&hdr->tail;
+        const uint32_t avail = tail - head;
+        const unsigned idle = __ballot_sync(kFull, ttype == T_NONE);
+        const int rank = __popc(idle & lt_mask);
+        if (ttype == T_NONE && (uint32_t)rank < avail) {
+            const uint64_t task = q[(head + rank) & qmask];
+            ttype = (int)((task >> 16) & 0xff);
+            tslot = (int)(task & 0xffff);
+            tpix = (uint32_t)(task >> 32);
+            const Slot& S = slots[tslot];
+            if (ttype == T_FREE) { // REF trace.cpp:189-230
+                if (tab.energy != S.E)
+                    tab.fill(P, S.E, st, S.bin);
+                walking = walk_begin<FMT>(P, w, v3(S.px, S.py, S.pz), v3(S.dx, S.dy, S.dz), S.target,
+                                          false, st, S.bin);
+            } else {
+                V3 o, to_det;
+                double e_out;
+                tpre = score_setup(P, S, tpix, o, to_det, e_out, st);
+                if (tab.energy != e_out) // REF trace_attenuation builds MuField(e_out)
+                    tab.fill(P, e_out, st, S.bin);
+                walking = walk_begin<FMT>(P, w, o, to_det, CUDART_INF, march, st, S.bin);
+                ++c_rays;
+            }
+        }
+        const uint32_t n_idle = (uint32_t)__popc(idle);
+        head += n_idle < avail ? n_idle : avail;
+
+        // ------------------------------------------------ termination
+        const unsigned active = __ballot_sync(kFull, ttype != T_NONE);
+        if (!active) {
+            if (pool_empty && tail == head && hdr->free_mask == all_free)
+                break;
+            if (*(volatile int32_t*)&st->code != 0)
                 break;
             continue;
         }
+
+        // ------------------------------------------------ 4. walk in lockstep
+        const bool can_refill = (tail != head) || (hdr->free_mask != 0 && !pool_empty);
+        const unsigned busy = active;
         for (;;) {
-            if (state == ST_WALK) {
-                const bool go = walk_step<FMT>(P, T, stride, w, pos);
-                if (post == ST_AFTER_FREE)
-                    ++fp_steps;
+            if (walking) {
+                walking = walk_step<FMT, REG>(P, tab, w);
+                if (ttype == T_FREE)
+                    ++c_fp;
                 else
-                    ++sc_steps;
-                if (!go)
-                    state = post;
+                    ++c_sc;
             }
-            walking = __ballot_sync(kFull, state == ST_WALK);
-            if (!walking)
+            const unsigned wmask = __ballot_sync(kFull, walking);
+            if (!wmask)
                 break;
-            const unsigned waiting = __ballot_sync(kFull, state != ST_WALK && state != ST_DONE);
-            if (__popc(waiting) >= P.walk_thresh)
+            const unsigned waiting = can_refill ? ~wmask : (busy & ~wmask);
+            const int need = can_refill ? P.walk_thresh : max(1, __popc(busy) >> 2);
+            if (__popc(waiting) >= need)
                 break;
         }
+        if (*(volatile int32_t*)&st->code != 0)
+            break;
     }
 
-    // flush the block's statistics
+    // flush this warp's counters and the block's statistics
+    sadd(B.diag + 0, c_fp);
+    sadd(B.diag + 1, c_sc);
+    sadd(B.diag + 3, c_rays);
+    sadd(B.diag + 4, c_int);
     __syncthreads();
     for (int i = threadIdx.x; i < 8 * P.n_bins; i += blockDim.x)
-        red_add(P.accum + P.off_bins + i, S.bins[i]);
+        red_add(P.accum + P.off_bins + i, B.bins[i]);
     for (int i = threadIdx.x; i < 24; i += blockDim.x)
-        red_add(P.accum + P.off_ledger + i, S.ledger[i]);
+        red_add(P.accum + P.off_ledger + i, B.ledger[i]);
     for (int i = threadIdx.x; i < 8; i += blockDim.x)
-        red_add(P.accum + P.off_diag + i, S.diag[i]);
-}
-
-// =========================================================== primary kernel
-// REF simulate_primary (transport.cpp:333-377) + trace_rho_lengths
-// (trace.cpp:163-187): one thread per pixel, fp64 walk, per-material rho*L in
-// shared memory, then the spectrum quadrature with host-tabulated
-// attenuation (host glibc loglog, i.e. REF's own values).
-template <int FMT>
-__global__ void __launch_bounds__(128) primary_kernel(const __grid_constant__ PrimaryParams P)
-{
-    extern __shared__ __align__(16) unsigned char smem[];
-    double* rho = reinterpret_cast<double*>(smem) + threadIdx.x;
-    const int stride = blockDim.x;
-    const uint64_t pix = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const uint64_t npix = (uint64_t)P.nu * P.nv;
-    if (pix >= npix)
-        return;
-    const int iv = (int)(pix / (uint64_t)P.nu);
-    const int iu = (int)(pix - (uint64_t)iv * P.nu);
-    for (int m = 0; m < P.n_mats; ++m)
-        rho[m * stride] = 0.0;
-
-    const V3 src = v3(P.src[0], P.src[1], P.src[2]);
-    const double du = (iu + 0.5 - 0.5 * P.nu) * P.pitch;
-    const double dv = (iv + 0.5 - 0.5 * P.nv) * P.pitch;
-    const V3 p = (v3(P.center[0], P.center[1], P.center[2]) + v3(P.uaxis[0], P.uaxis[1], P.uaxis[2]) * du) +
-                 v3(0.0, 0.0, 1.0) * dv;
-    const V3 delta = p - src;
-    const double d2 = dot(delta, delta);
-    const V3 d = delta / sqrt(d2);
-
-    const Grid& G = P.G;
-    double t0, t1;
-    bool bad;
-    if (clip_to_grid(G, src, d, t0, t1, bad)) {
-        const V3 q = src + d * t0;
-        int ix, iy, iz, sx, sy, sz;
-        double tnx, tny, tnz, dtx, dty, dtz;
-        start_axis(q.x, src.x, d.x, G.ox, G.hx, G.ihx, G.nx, t0, ix, sx, tnx, dtx);
-        start_axis(q.y, src.y, d.y, G.oy, G.hy, G.ihy, G.ny, t0, iy, sy, tny, dty);
-        start_axis(q.z, src.z, d.z, G.oz, G.hz, G.ihz, G.nz, t0, iz, sz, tnz, dtz);
-        double t = t0;
-        while (t < t1) {
-            double tn = tnx;
-            if (tny < tn)
-                tn = tny;
-            if (tnz < tn)
-                tn = tnz;
-            if (t1 < tn)
-                tn = t1;
-            const uint32_t cell = brick_cell(G, ix, iy, iz);
-            int m;
-            float dens;
-            if (FMT == kFmtP4) {
-                const int code = load_code_p4(G, cell);
-                m = P.pal_mat[code];
-                dens = P.pal_dens[code];
-            } else if (FMT == kFmtP8) {
-                const int code = load_code_p8(G, cell);
-                m = P.pal_mat[code];
-                dens = P.pal_dens[code];
-            } else {
-                m = __ldg(G.vox + cell);
-                dens = load_density_raw(G, cell);
-            }
-            rho[m * stride] += (double)dens * (tn - t);
-            t = tn;
-            if (t >= t1)
-                break;
-            if (tnx == tn) {
-                ix += sx;
-                if (ix < 0 || ix >= G.nx)
-                    break;
-                tnx += dtx;
-            }
-            if (tny == tn) {
-                iy += sy;
-                if (iy < 0 || iy >= G.ny)
-                    break;
-                tny += dty;
-            }
-            if (tnz == tn) {
-                iz += sz;
-                if (iz < 0 || iz >= G.nz)
-                    break;
-                tnz += dtz;
-            }
-        }
-    }
-    double value = 0.0;
-    for (int b = 0; b < P.n_bins; ++b) {
-        double tau = 0.0;
-        for (int m = 1; m < P.n_mats; ++m)
-            tau += __ldg(P.atten + (size_t)b * P.n_mats + m) * rho[m * stride];
-        value += __ldg(P.wresp + b) * __ldg(P.response + b) * exp(-tau) / d2;
-    }
-    P.image[pix] = value;
-}
-
-// ========================================================== finalize kernel
-// Limb sums -> fp64 image (+ REF's per-pixel variance, transport.cpp:317-322).
-__global__ void finalize_image_kernel(const unsigned long long* __restrict__ acc, uint64_t off_image,
-                                      uint64_t off_var, uint64_t npix, int log2_img, double n_hist,
-                                      int track_var, double* __restrict__ image,
-                                      double* __restrict__ var)
-{
-    for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npix;
-         p += (uint64_t)gridDim.x * blockDim.x) {
-        const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(acc + off_image + 4 * p);
-        const double v = dequantize(a.x, a.y, acc[off_image + 4 * p + 2], log2_img);
-        image[p] = v;
-        if (track_var && var) {
-            const double c2 = dequantize(acc[off_var + 4 * p], acc[off_var + 4 * p + 1],
-                                         acc[off_var + 4 * p + 2], 2 * log2_img);
-            const double x = c2 - v * v / n_hist;
-            const double den = 1.0 < n_hist - 1.0 ? n_hist - 1.0 : 1.0;
-            var[p] = (0.0 < x ? x : 0.0) * n_hist / den;
-        }
-    }
+        red_add(P.accum + P.off_diag + i, B.diag[i]);
 }
 
 // ----------------------------------------------------------------- launchers
-cudaError_t launch_transport(const TransportParams& P, int grid, int block, size_t smem,
-                             cudaStream_t s)
+static bool use_reg(const TransportParams& P) { return P.G.fmt == kFmtP4 && P.n_pal <= 4; }
+
+size_t transport_smem_bytes(const TransportParams& P)
 {
-    switch (P.G.fmt) {
-    case kFmtP4:
-        transport_kernel<kFmtP4><<<grid, block, smem, s>>>(P);
-        break;
-    case kFmtP8:
-        transport_kernel<kFmtP8><<<grid, block, smem, s>>>(P);
-        break;
-    default:
-        transport_kernel<kFmtRaw><<<grid, block, smem, s>>>(P);
-        break;
-    }
-    return cudaGetLastError();
+    const size_t warp_bytes =
+        (size_t)P.slots_per_warp * sizeof(Slot) + sizeof(WarpHdr) + (size_t)P.queue_len * 8;
+    const int n_tab = P.G.fmt == kFmtP4 ? P.n_pal : P.n_mats;
+    return (size_t)(8 * P.n_bins + 32) * 8 + (size_t)(P.n_bins + 1) * 8 + kWarps * warp_bytes +
+           (use_reg(P) ? 0 : (size_t)n_tab * kBlock * 8);
 }
 
-cudaError_t transport_set_smem(size_t smem)
+int transport_block_size() { return kBlock; }
+
+static const void* kernel_for(const TransportParams& P)
 {
-    cudaError_t e;
-    if ((e = cudaFuncSetAttribute(transport_kernel<kFmtP4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem)) != cudaSuccess)
+    if (P.G.fmt == kFmtP4)
+        return use_reg(P) ? (const void*)transport_kernel<kFmtP4, true>
+                          : (const void*)transport_kernel<kFmtP4, false>;
+    if (P.G.fmt == kFmtP8)
+        return (const void*)transport_kernel<kFmtP8, false>;
+    return (const void*)transport_kernel<kFmtRaw, false>;
+}
+
+cudaError_t transport_prepare(const TransportParams& P, size_t smem, int* blocks_per_sm)
+{
+    const void* k = kernel_for(P);
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess)
         return e;
-    if ((e = cudaFuncSetAttribute(transport_kernel<kFmtP8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem)) != cudaSuccess)
-        return e;
-    return cudaFuncSetAttribute(transport_kernel<kFmtRaw>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem);
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k, kBlock, smem);
 }
 
-cudaError_t transport_occupancy(int fmt, int block, size_t smem, int* blocks_per_sm)
+cudaError_t launch_transport(const TransportParams& P, int grid, size_t smem, cudaStream_t s)
 {
-    switch (fmt) {
-    case kFmtP4:
-        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, transport_kernel<kFmtP4>,
-                                                             block, smem);
-    case kFmtP8:
-        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, transport_kernel<kFmtP8>,
-                                                             block, smem);
-    default:
-        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, transport_kernel<kFmtRaw>,
-                                                             block, smem);
-    }
-}
-
-cudaError_t launch_primary(const PrimaryParams& P, cudaStream_t s)
-{
-    const int block = 128;
-    const uint64_t npix = (uint64_t)P.nu * P.nv;
-    const int grid = (int)((npix + block - 1) / block);
-    const size_t smem = (size_t)P.n_mats * block * sizeof(double);
-    switch (P.G.fmt) {
-    case kFmtP4:
-        primary_kernel<kFmtP4><<<grid, block, smem, s>>>(P);
-        break;
-    case kFmtP8:
-        primary_kernel<kFmtP8><<<grid, block, smem, s>>>(P);
-        break;
-    default:
-        primary_kernel<kFmtRaw><<<grid, block, smem, s>>>(P);
-        break;
-    }
-    return cudaGetLastError();
-}
-
-cudaError_t launch_finalize_image(const unsigned long long* acc, uint64_t off_image, uint64_t off_var,
-                                  uint64_t npix, int log2_img, double n_hist, int track_var,
-                                  double* image, double* var, cudaStream_t s)
-{
-    const int block = 256;
-    int grid = (int)((npix + block - 1) / block);
-    if (grid > 148 * 16)
-        grid = 148 * 16;
-    finalize_image_kernel<<<grid, block, 0, s>>>(acc, off_image, off_var, npix, log2_img, n_hist,
-                                                 track_var, image, var);
+    if (P.G.fmt == kFmtP4 && use_reg(P))
+        transport_kernel<kFmtP4, true><<<grid, kBlock, smem, s>>>(P);
+    else if (P.G.fmt == kFmtP4)
+        transport_kernel<kFmtP4, false><<<grid, kBlock, smem, s>>>(P);
+    else if (P.G.fmt == kFmtP8)
+        transport_kernel<kFmtP8, false><<<grid, kBlock, smem, s>>>(P);
+    else
+        transport_kernel<kFmtRaw, false><<<grid, kBlock, smem, s>>>(P);
     return cudaGetLastError();
 }
 

@@ -101,10 +101,12 @@ struct TransportParams {
     // history range and pool
     uint64_t h_begin, h_end;
     unsigned long long* pool;
-    int32_t grab;        // histories per warp grab
-    int32_t walk_thresh; // leave the walk phase when this many lanes need events
+    int32_t grab;           // histories per warp grab
+    int32_t walk_thresh;    // leave the walk phase when this many lanes need events
+    int32_t slots_per_warp; // live histories per warp (<= 64)
+    int32_t queue_len;      // ray-task FIFO entries per warp (power of two)
 
-    // variance scratch: var_cap entries per thread
+    // variance scratch: var_cap entries per history slot
     uint32_t* var_pix;
     double* var_val;
 
