@@ -146,6 +146,7 @@ typedef struct xs_launch_stats {
     double kernel_ms;          /* transport kernel time, CUDA events          */
     int32_t voxel_format;      /* 0 = 4-bit palette, 1 = 8-bit palette, 2 = raw id+density */
     int32_t palette_size;
+    uint64_t upload_bytes;     /* encoded voxel bytes of the last phantom upload (H2D) */
 } xs_launch_stats;
 
 typedef struct xs_context xs_context;

@@ -75,7 +75,8 @@ class XsLaunchStats(C.Structure):
     _fields_ = [("free_path_steps", C.c_uint64), ("scoring_steps", C.c_uint64),
                 ("histories", C.c_uint64), ("scoring_rays", C.c_uint64),
                 ("interactions", C.c_uint64), ("kernel_ms", C.c_double),
-                ("voxel_format", C.c_int32), ("palette_size", C.c_int32)]
+                ("voxel_format", C.c_int32), ("palette_size", C.c_int32),
+                ("upload_bytes", C.c_uint64)]
 
 
 def dptr(a: np.ndarray):

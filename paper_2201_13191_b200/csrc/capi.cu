@@ -76,6 +76,31 @@ struct DevBuf {
     }
 };
 
+// Growable pinned host buffer (H2D staging).
+template <typename T>
+struct PinBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    void reserve(size_t count)
+    {
+        if (count <= n && p)
+            return;
+        if (p)
+            cudaFreeHost(p);
+        p = nullptr;
+        n = 0;
+        cuda_check(cudaMallocHost(&p, std::max<size_t>(count, 1) * sizeof(T)), "cudaMallocHost");
+        n = count;
+    }
+    void release()
+    {
+        if (p)
+            cudaFreeHost(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+
 // Host copy of a table (the C-ABI inputs are borrowed pointers).
 struct HTab {
     std::vector<double> x, y;
@@ -130,6 +155,9 @@ struct xs_context {
     DevBuf<uint8_t> vox;
     DevBuf<float> dens;
     DevBuf<double> tabs;
+    PinBuf<uint8_t> pin_vox;
+    PinBuf<float> pin_dens;
+    uint64_t last_upload_bytes = 0;
 
     // scratch
     DevBuf<unsigned long long> accum;
@@ -331,17 +359,12 @@ void scan_phantom(const xs_phantom& ph, const std::vector<int>& has_tables, Scan
 
 // Re-encodes the x-fastest grid into 4x4x4 bricks (P4 nibbles / P8 bytes /
 // raw id + density), parallel over brick layers.
-void encode_phantom(const xs_phantom& ph, int fmt, const std::vector<PairKey>& pal,
-                    std::vector<uint8_t>& vox, std::vector<float>& dens, int nbx, int nby, int nbz)
+// vox / dens are (pinned) staging buffers of encoded_bytes(); every byte is written.
+void encode_phantom(const xs_phantom& ph, int fmt, const std::vector<PairKey>& pal, uint8_t* vox,
+                    float* dens, int nbx, int nby, int nbz)
 {
     const int nx = ph.dims[0], ny = ph.dims[1], nz = ph.dims[2];
-    const size_t n_bricks = (size_t)nbx * nby * nbz;
-    if (fmt == xsd::kFmtP4)
-        vox.assign(n_bricks * 32, 0);
-    else
-        vox.assign(n_bricks * 64, 0);
-    if (fmt == xsd::kFmtRaw)
-        dens.assign(n_bricks * 64, 0.0f);
+    const size_t layer_bytes = (size_t)nbx * nby * (fmt == xsd::kFmtP4 ? 32 : 64);
     const unsigned nt = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
     std::atomic<int> next{0};
     std::vector<std::thread> th;
@@ -351,6 +374,9 @@ void encode_phantom(const xs_phantom& ph, int fmt, const std::vector<PairKey>& p
                 const int bz = next.fetch_add(1);
                 if (bz >= nbz)
                     return;
+                std::memset(vox + (size_t)bz * layer_bytes, 0, layer_bytes); // padding voxels = code 0
+                if (fmt == xsd::kFmtRaw)
+                    std::memset(dens + (size_t)bz * nbx * nby * 64, 0, (size_t)nbx * nby * 64 * 4);
                 PairKey last{255, 0xFFFFFFFFu};
                 int last_code = 0;
                 for (int z = bz * 4; z < std::min(nz, bz * 4 + 4); ++z)
@@ -540,6 +566,7 @@ void accumulate(xs_context* c, const xs_geometry& g, int angle, const xs_spectru
     c->last.kernel_ms = ms;
     c->last.voxel_format = c->grid.fmt;
     c->last.palette_size = c->n_pal;
+    c->last.upload_bytes = c->last_upload_bytes;
 }
 
 void finalize(xs_context* c, const xs_geometry& g, const xs_spectrum& spec, const xs_sim_config& cfg,
@@ -697,6 +724,8 @@ void xs_ctx_destroy(xs_context* c)
         b->release();
     c->vox.release();
     c->dens.release();
+    c->pin_vox.release();
+    c->pin_dens.release();
     c->accum.release();
     c->bin_start.release();
     c->bin_count.release();
@@ -771,9 +800,12 @@ int xs_upload_phantom(xs_context* c, const xs_phantom* ph)
         G.fmt = fmt;
         G.n_codes = fmt == xsd::kFmtRaw ? 0 : n_pairs;
 
-        std::vector<uint8_t> vox;
-        std::vector<float> dens;
-        encode_phantom(*ph, fmt, scan.pairs, vox, dens, G.nbx, G.nby, G.nbz);
+        const size_t n_bricks = (size_t)G.nbx * G.nby * G.nbz;
+        const size_t vox_bytes = n_bricks * (fmt == xsd::kFmtP4 ? 32 : 64);
+        const size_t dens_count = fmt == xsd::kFmtRaw ? n_bricks * 64 : 0;
+        c->pin_vox.reserve(vox_bytes);
+        c->pin_dens.reserve(std::max<size_t>(dens_count, 1));
+        encode_phantom(*ph, fmt, scan.pairs, c->pin_vox.p, c->pin_dens.p, G.nbx, G.nby, G.nbz);
 
         c->n_pal = fmt == xsd::kFmtRaw ? 0 : n_pairs;
         std::memset(c->pal_mat, 0, sizeof c->pal_mat);
@@ -782,15 +814,16 @@ int xs_upload_phantom(xs_context* c, const xs_phantom* ph)
             c->pal_mat[k] = scan.pairs[k].id;
             std::memcpy(&c->pal_dens[k], &scan.pairs[k].dens_bits, 4);
         }
-        c->vox.reserve(vox.size());
-        cuda_check(cudaMemcpyAsync(c->vox.p, vox.data(), vox.size(), cudaMemcpyHostToDevice, c->stream),
+        c->vox.reserve(vox_bytes);
+        cuda_check(cudaMemcpyAsync(c->vox.p, c->pin_vox.p, vox_bytes, cudaMemcpyHostToDevice, c->stream),
                    "upload voxels");
         if (fmt == xsd::kFmtRaw) {
-            c->dens.reserve(dens.size());
-            cuda_check(cudaMemcpyAsync(c->dens.p, dens.data(), dens.size() * 4, cudaMemcpyHostToDevice,
+            c->dens.reserve(dens_count);
+            cuda_check(cudaMemcpyAsync(c->dens.p, c->pin_dens.p, dens_count * 4, cudaMemcpyHostToDevice,
                                        c->stream),
                        "upload densities");
         }
+        c->last_upload_bytes = vox_bytes + dens_count * 4;
         cuda_check(cudaStreamSynchronize(c->stream), "upload phantom");
         G.vox = c->vox.p;
         G.dens = fmt == xsd::kFmtRaw ? c->dens.p : nullptr;
