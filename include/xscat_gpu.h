@@ -147,6 +147,7 @@ typedef struct xs_launch_stats {
     int32_t voxel_format;      /* 0 = 4-bit palette, 1 = 8-bit palette, 2 = raw id+density */
     int32_t palette_size;
     uint64_t upload_bytes;     /* encoded voxel bytes of the last phantom upload (H2D) */
+    uint64_t walk_iterations;  /* walker loop iterations (< steps when macro cells are skipped) */
 } xs_launch_stats;
 
 typedef struct xs_context xs_context;
@@ -323,6 +324,16 @@ void xs_ctx_destroy(xs_context* ctx);
  * context's own stream. */
 int xs_ctx_set_stream(xs_context* ctx, void* cuda_stream);
 int xs_ctx_synchronize(xs_context* ctx);
+
+/* Tuning / mode knobs (no REF counterpart):
+ *   "exact_walk"  1: voxel-by-voxel Siddon everywhere (strict REF replay);
+ *                 0 (default): cross uniform 8^3 macro cells in one step, which
+ *                 changes the optical depths only at fp64 rounding level
+ *   "walk_thresh" lanes waiting before a warp leaves the walk phase (1..32)
+ *   "queue_len"   ray-task FIFO entries per warp (rounded to a power of two)
+ *   "max_slots"   live histories per warp (1..64)
+ *   "grab"        histories a warp reserves from the pool at a time        */
+int xs_ctx_set_option(xs_context* ctx, const char* key, int64_t value);
 
 /* Scene upload: REF passes the phantom and response by const& to every
  * projector call; here they are uploaded once and reused until replaced.

@@ -76,7 +76,7 @@ class XsLaunchStats(C.Structure):
                 ("histories", C.c_uint64), ("scoring_rays", C.c_uint64),
                 ("interactions", C.c_uint64), ("kernel_ms", C.c_double),
                 ("voxel_format", C.c_int32), ("palette_size", C.c_int32),
-                ("upload_bytes", C.c_uint64)]
+                ("upload_bytes", C.c_uint64), ("walk_iterations", C.c_uint64)]
 
 
 def dptr(a: np.ndarray):
@@ -199,6 +199,7 @@ SIGNATURES = {
     "xs_ctx_destroy": (None, [_P]),
     "xs_ctx_set_stream": (C.c_int, [_P, _P]),
     "xs_ctx_synchronize": (C.c_int, [_P]),
+    "xs_ctx_set_option": (C.c_int, [_P, C.c_char_p, C.c_int64]),
     "xs_upload_phantom": (C.c_int, [_P, C.POINTER(XsPhantom)]),
     "xs_upload_response": (C.c_int, [_P, C.POINTER(XsResponse)]),
     "xs_simulate_scatter_stats": (C.c_int, [_P, C.POINTER(XsGeometry), C.c_int32,

@@ -171,6 +171,7 @@ struct xs_context {
     DevBuf<xsd::InterpEntry> interp_tab;
     uint32_t queue_len = 512;
     int max_slots = 64;
+    int macro_skip = 1;
 
     xs_launch_stats last{};
     int walk_thresh = 28;
@@ -508,6 +509,7 @@ void accumulate(xs_context* c, const xs_geometry& g, int angle, const xs_spectru
     P.step_voxels = cfg.step_voxels;
     P.max_inter = cfg.max_interactions;
     P.track_var = cfg.track_variance ? 1 : 0;
+    P.skip = c->macro_skip;
     P.march_h = cfg.step_voxels *
                 std::min({c->grid.hx, c->grid.hy, c->grid.hz}); // REF trace.cpp:117
     P.accum = d_accum;
@@ -592,6 +594,7 @@ void finalize(xs_context* c, const xs_geometry& g, const xs_spectrum& spec, cons
     c->last.histories = diag[2];
     c->last.scoring_rays = diag[3];
     c->last.interactions = diag[4];
+    c->last.walk_iterations = diag[5];
 
     double* img = d_image;
     if (!img) {
@@ -707,6 +710,8 @@ int xs_ctx_create(int32_t device, xs_context** out)
                 q <<= 1;
             c->queue_len = q;
         }
+        if (const char* e = std::getenv("XSCAT_SKIP"))
+            c->macro_skip = std::atoi(e) != 0;
         if (const char* e = std::getenv("XSCAT_SLOTS"))
             c->max_slots = std::max(1, std::min(64, std::atoi(e)));
         *out = c;
@@ -745,6 +750,29 @@ void xs_ctx_destroy(xs_context* c)
 int xs_ctx_set_stream(xs_context* c, void* stream)
 {
     return guard(c, [&] { c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own; });
+}
+
+int xs_ctx_set_option(xs_context* c, const char* key, int64_t value)
+{
+    return guard(c, [&] {
+        const std::string k = key ? key : "";
+        if (k == "exact_walk") {
+            c->macro_skip = value ? 0 : 1;
+        } else if (k == "walk_thresh") {
+            c->walk_thresh = (int)std::max<int64_t>(1, std::min<int64_t>(32, value));
+        } else if (k == "queue_len") {
+            uint32_t q = 16;
+            while (q < (uint32_t)std::max<int64_t>(16, value))
+                q <<= 1;
+            c->queue_len = q;
+        } else if (k == "max_slots") {
+            c->max_slots = (int)std::max<int64_t>(1, std::min<int64_t>(64, value));
+        } else if (k == "grab") {
+            c->grab = (int)std::max<int64_t>(1, value);
+        } else {
+            fail(XS_E_INVALID_ARGUMENT, "xs_ctx_set_option: unknown option '%s'", k.c_str());
+        }
+    });
 }
 
 int xs_ctx_synchronize(xs_context* c)
@@ -806,6 +834,49 @@ int xs_upload_phantom(xs_context* c, const xs_phantom* ph)
         c->pin_vox.reserve(vox_bytes);
         c->pin_dens.reserve(std::max<size_t>(dens_count, 1));
         encode_phantom(*ph, fmt, scan.pairs, c->pin_vox.p, c->pin_dens.p, G.nbx, G.nby, G.nbz);
+
+        // 8^3 macro cells: mark every voxel of a uniform cell with the
+        // palette's flag bit so the walker can cross the cell in one step
+        G.ubit = 0;
+        if ((fmt == xsd::kFmtP4 && n_pairs <= 8) || (fmt == xsd::kFmtP8 && n_pairs <= 128)) {
+            G.ubit = fmt == xsd::kFmtP4 ? 8 : 128;
+            uint8_t* v = c->pin_vox.p;
+            const size_t bb = fmt == xsd::kFmtP4 ? 32 : 64;
+            auto brick_ptr = [&](int bx, int by, int bz) {
+                return v + ((size_t)bx + (size_t)G.nbx * ((size_t)by + (size_t)G.nby * bz)) * bb;
+            };
+            auto brick_code = [&](int bx, int by, int bz) -> int { // uniform code or -1
+                const uint8_t* b = brick_ptr(bx, by, bz);
+                for (size_t i = 1; i < bb; ++i)
+                    if (b[i] != b[0])
+                        return -1;
+                if (fmt == xsd::kFmtP4)
+                    return (b[0] & 0xF) == (b[0] >> 4) ? (b[0] & 0xF) : -1;
+                return b[0];
+            };
+            const int mnx = (G.nx + 7) / 8, mny = (G.ny + 7) / 8, mnz = (G.nz + 7) / 8;
+            for (int mz = 0; mz < mnz; ++mz)
+                for (int my = 0; my < mny; ++my)
+                    for (int mx = 0; mx < mnx; ++mx) {
+                        int code = -2;
+                        for (int k = 0; k < 8 && code != -1; ++k) {
+                            const int bx = 2 * mx + (k & 1), by = 2 * my + ((k >> 1) & 1), bz = 2 * mz + (k >> 2);
+                            if (bx >= G.nbx || by >= G.nby || bz >= G.nbz)
+                                continue;
+                            const int bc = brick_code(bx, by, bz);
+                            code = (bc < 0 || (code >= 0 && bc != code)) ? -1 : bc;
+                        }
+                        // only whole macro cells inside the grid (partial edge
+                        // cells hold padding voxels)
+                        if (code < 0 || 8 * mx + 8 > G.nx || 8 * my + 8 > G.ny || 8 * mz + 8 > G.nz)
+                            continue;
+                        const int f = code | G.ubit;
+                        const uint8_t byte = fmt == xsd::kFmtP4 ? (uint8_t)(f | (f << 4)) : (uint8_t)f;
+                        for (int k = 0; k < 8; ++k)
+                            std::memset(brick_ptr(2 * mx + (k & 1), 2 * my + ((k >> 1) & 1), 2 * mz + (k >> 2)),
+                                        byte, bb);
+                    }
+        }
 
         c->n_pal = fmt == xsd::kFmtRaw ? 0 : n_pairs;
         std::memset(c->pal_mat, 0, sizeof c->pal_mat);

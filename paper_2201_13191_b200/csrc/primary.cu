@@ -57,11 +57,11 @@ __global__ void __launch_bounds__(128) primary_kernel(const __grid_constant__ Pr
             int m;
             float dens;
             if (FMT == kFmtP4) {
-                const int code = load_code_p4(G, cell);
+                const int code = load_code_p4(G, cell) & ~G.ubit;
                 m = P.pal_mat[code];
                 dens = P.pal_dens[code];
             } else if (FMT == kFmtP8) {
-                const int code = load_code_p8(G, cell);
+                const int code = load_code_p8(G, cell) & ~G.ubit;
                 m = P.pal_mat[code];
                 dens = P.pal_dens[code];
             } else {

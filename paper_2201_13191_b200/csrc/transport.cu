@@ -216,6 +216,7 @@ struct Walk {
     double tnx, tny, tnz; // next boundary crossing per axis
     double dtx, dty, dtz; // per-voxel increments (march: dtx = step length)
     double t, texit, depth, target;
+    double rdx, rdy, rdz; // 1 / dt per axis (macro-cell skips)
     int ix, iy, iz;       // current voxel (march: ix = sample j, iy = n samples)
     int sx, sy, sz;
     uint32_t ax, ay, az;  // per-axis brick address terms of the current voxel
@@ -225,7 +226,11 @@ struct Walk {
     double mu_hit;        // free path: mu of the voxel it ends in
     int march;
     int hit;
+    uint32_t skipped;     // voxel visits integrated inside skipped macro cells
+    uint32_t steps;       // loop iterations of this walk
 };
+
+
 
 template <int FMT>
 __device__ __noinline__ bool walk_begin(const TransportParams& P, Walk& w, V3 o, V3 d,
@@ -241,6 +246,8 @@ __device__ __noinline__ bool walk_begin(const TransportParams& P, Walk& w, V3 o,
     w.rz = d.z;
     w.hit = 0;
     w.depth = 0.0;
+    w.steps = 0;
+    w.skipped = 0;
     if (!clip_to_grid(P.G, o, d, t0, t1, bad)) {
         if (bad)
             raise(st, XS_E_INVALID_ARGUMENT, 0, bin, 0.0, 0.0);
@@ -267,13 +274,53 @@ __device__ __noinline__ bool walk_begin(const TransportParams& P, Walk& w, V3 o,
     w.ay = term_y(G, w.iy);
     w.az = term_z(G, w.iz);
     prefetch<FMT>(G, w.ax + w.ay + w.az, w.raw, w.shift, w.dens);
+    w.rdx = 1.0 / w.dtx;
+    w.rdy = 1.0 / w.dty;
+    w.rdz = 1.0 / w.dtz;
     return true;
+}
+
+// Boundaries tn + j*dt (j = 0..k) with tn + j*dt <= tm: how many an axis
+// crosses while the ray traverses a skipped macro cell (k = crossings left
+// inside the cell along that axis; k + 1 means it also leaves the cell).
+__device__ __forceinline__ int cross_count(double tn, double dt, double rdt, double tm, int k, int s)
+{
+    if (s == 0 || tn > tm)
+        return 0;
+    int n = (int)((tm - tn) * rdt) + 1;
+    n = n > k + 1 ? k + 1 : n;
+    if (n > 1 && tn + (n - 1) * dt > tm)
+        --n;
+    else if (n <= k && tn + n * dt <= tm)
+        ++n;
+    return n;
+}
+
+// Re-establish the exact walker at ray parameter t (REF start_walk,
+// trace.cpp:72-103, applied at the exit of a skipped macro cell).  Returns
+// false when the ray has left the grid.
+__device__ __forceinline__ bool restart_axis(double p, double o, double d, double org, double hs,
+                                             double inv_h, int n, double t, int step, double dt,
+                                             int& idx, double& tn)
+{
+    idx = voxel_of(p, org, inv_h, n);
+    if (step > 0)
+        tn = (org + (idx + 1) * hs - o) / d;
+    else if (step < 0)
+        tn = (org + idx * hs - o) / d;
+    else
+        return true;
+    while (tn <= t) {
+        idx += step;
+        tn += dt;
+    }
+    return idx >= 0 && idx < n;
 }
 
 // One voxel (REF trace.cpp:136-155 / :202-228).  Branch-free axis advance;
 // the next voxel's load is issued before this step's fp64 chain and decoded
 // only in the next step.
-template <int FMT, bool REG>
+template <int FMT, bool REG, bool SKIP>
 __device__ __forceinline__ bool walk_step(const TransportParams& P, const MuTab<FMT, REG>& tab,
                                           Walk& w)
 {
@@ -287,10 +334,55 @@ __device__ __forceinline__ bool walk_step(const TransportParams& P, const MuTab<
         float dens = 0.f;
         fetch<FMT>(G, voxel_of(px, G.ox, G.ihx, G.nx), voxel_of(py, G.oy, G.ihy, G.ny),
                    voxel_of(pz, G.oz, G.ihz, G.nz), code, dens);
-        w.depth += tab.mu(P, code, dens) * (tb - ta);
+        w.depth += tab.mu(P, code & ~G.ubit, dens) * (tb - ta);
         return ++w.ix < w.iy;
     }
-    const uint32_t raw = w.raw, shift = w.shift;
+    const int code = decode<FMT>(w.raw, w.shift);
+    if (SKIP && (code & G.ubit)) { // uniform macro cell: integrate to its exit in one step
+        {
+            const double mu = tab.mu(P, code & ~G.ubit, 0.f);
+            const int kx = w.sx > 0 ? 7 - (w.ix & 7) : (w.ix & 7);
+            const int ky = w.sy > 0 ? 7 - (w.iy & 7) : (w.iy & 7);
+            const int kz = w.sz > 0 ? 7 - (w.iz & 7) : (w.iz & 7);
+            double tm = w.texit;
+            if (w.sx != 0 && w.tnx + kx * w.dtx < tm)
+                tm = w.tnx + kx * w.dtx;
+            if (w.sy != 0 && w.tny + ky * w.dty < tm)
+                tm = w.tny + ky * w.dty;
+            if (w.sz != 0 && w.tnz + kz * w.dtz < tm)
+                tm = w.tnz + kz * w.dtz;
+            const double seg = mu * (tm - w.t);
+            if (w.depth + seg >= w.target) {
+                w.hit = 1;
+                w.mu_hit = mu;
+                w.texit = tm;
+                return false;
+            }
+            w.depth += seg;
+            w.t = tm;
+            if (tm >= w.texit)
+                return false;
+            // advance every axis past the boundaries it crosses before tm
+            const int nx_ = cross_count(w.tnx, w.dtx, w.rdx, tm, kx, w.sx);
+            const int ny_ = cross_count(w.tny, w.dty, w.rdy, tm, ky, w.sy);
+            const int nz_ = cross_count(w.tnz, w.dtz, w.rdz, tm, kz, w.sz);
+            w.ix += nx_ * w.sx;
+            w.iy += ny_ * w.sy;
+            w.iz += nz_ * w.sz;
+            w.tnx += nx_ * w.dtx;
+            w.tny += ny_ * w.dty;
+            w.tnz += nz_ * w.dtz;
+            w.skipped += (uint32_t)(nx_ + ny_ + nz_) - 1u;
+            if ((uint32_t)w.ix >= (uint32_t)G.nx || (uint32_t)w.iy >= (uint32_t)G.ny ||
+                (uint32_t)w.iz >= (uint32_t)G.nz)
+                return false;
+            w.ax = term_x(G, w.ix);
+            w.ay = term_y(G, w.iy);
+            w.az = term_z(G, w.iz);
+            prefetch<FMT>(G, w.ax + w.ay + w.az, w.raw, w.shift, w.dens);
+            return true;
+        }
+    }
     const float dens = w.dens;
     double tn = w.tnx;
     if (w.tny < tn)
@@ -311,7 +403,7 @@ __device__ __forceinline__ bool walk_step(const TransportParams& P, const MuTab<
     if (inside)
         prefetch<FMT>(G, nax + nay + naz, w.raw, w.shift, w.dens);
 
-    const double mu = tab.mu(P, decode<FMT>(raw, shift), dens);
+    const double mu = tab.mu(P, code & ~G.ubit, dens);
     const double seg = mu * (tn - w.t);
     const double nd = w.depth + seg;
     if (nd >= w.target) { // free path ends inside this voxel; t_hit in hit_t()
@@ -450,7 +542,7 @@ __device__ __noinline__ void history_event(const TransportParams& P, const Block
     int code;
     float dens;
     fetch<FMT>(P.G, vix, viy, viz, code, dens);
-    const int mat = material_of<FMT>(P, code);
+    const int mat = material_of<FMT>(P, code & ~P.G.ubit);
     const MatDesc& md = P.mats[mat];
     const double E = S.E;
     // select_interaction (cross_sections.cpp:81-96)
@@ -686,7 +778,7 @@ __device__ __noinline__ double score_setup(const TransportParams& P, const Slot&
 } // namespace
 
 // =================================================================== kernel
-template <int FMT, bool REG>
+template <int FMT, bool REG, bool SKIP>
 __global__ void __launch_bounds__(kBlock, 4) transport_kernel(const __grid_constant__ TransportParams P)
 {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -737,11 +829,16 @@ __global__ void __launch_bounds__(kBlock, 4) transport_kernel(const __grid_const
     bool walking = false;
     Walk w;
     w.march = 0;
-    uint32_t c_fp = 0, c_sc = 0, c_rays = 0, c_int = 0;
+    uint32_t c_fp = 0, c_sc = 0, c_rays = 0, c_int = 0, c_iter = 0;
 
     for (;;) {
         // ------------------------------------------------ 1. completions
         if (ttype != T_NONE && !walking) {
+            if (ttype == T_FREE)
+                c_fp += w.steps + w.skipped;
+            else
+                c_sc += w.steps + w.skipped;
+            c_iter += w.steps;
             const uint64_t var_base = (gwarp * H + tslot) * (uint64_t)P.var_cap;
             if (ttype == T_SCORE) { // REF run_history :178-193
                 Slot& S = slots[tslot];
@@ -860,11 +957,8 @@ __global__ void __launch_bounds__(kBlock, 4) transport_kernel(const __grid_const
         const unsigned busy = active;
         for (;;) {
             if (walking) {
-                walking = walk_step<FMT, REG>(P, tab, w);
-                if (ttype == T_FREE)
-                    ++c_fp;
-                else
-                    ++c_sc;
+                walking = walk_step<FMT, REG, SKIP>(P, tab, w);
+                ++w.steps;
             }
             const unsigned wmask = __ballot_sync(kFull, walking);
             if (!wmask)
@@ -883,6 +977,7 @@ __global__ void __launch_bounds__(kBlock, 4) transport_kernel(const __grid_const
     sadd(B.diag + 1, c_sc);
     sadd(B.diag + 3, c_rays);
     sadd(B.diag + 4, c_int);
+    sadd(B.diag + 5, c_iter);
     __syncthreads();
     for (int i = threadIdx.x; i < 8 * P.n_bins; i += blockDim.x)
         red_add(P.accum + P.off_bins + i, B.bins[i]);
@@ -906,19 +1001,24 @@ size_t transport_smem_bytes(const TransportParams& P)
 
 int transport_block_size() { return kBlock; }
 
-static const void* kernel_for(const TransportParams& P)
+typedef void (*TransportFn)(const TransportParams);
+
+static TransportFn kernel_for(const TransportParams& P)
 {
-    if (P.G.fmt == kFmtP4)
-        return use_reg(P) ? (const void*)transport_kernel<kFmtP4, true>
-                          : (const void*)transport_kernel<kFmtP4, false>;
+    const bool skip = P.skip != 0 && P.G.ubit != 0;
+    if (P.G.fmt == kFmtP4) {
+        if (use_reg(P))
+            return skip ? transport_kernel<kFmtP4, true, true> : transport_kernel<kFmtP4, true, false>;
+        return skip ? transport_kernel<kFmtP4, false, true> : transport_kernel<kFmtP4, false, false>;
+    }
     if (P.G.fmt == kFmtP8)
-        return (const void*)transport_kernel<kFmtP8, false>;
-    return (const void*)transport_kernel<kFmtRaw, false>;
+        return skip ? transport_kernel<kFmtP8, false, true> : transport_kernel<kFmtP8, false, false>;
+    return transport_kernel<kFmtRaw, false, false>;
 }
 
 cudaError_t transport_prepare(const TransportParams& P, size_t smem, int* blocks_per_sm)
 {
-    const void* k = kernel_for(P);
+    const void* k = (const void*)kernel_for(P);
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess)
         return e;
@@ -927,14 +1027,7 @@ cudaError_t transport_prepare(const TransportParams& P, size_t smem, int* blocks
 
 cudaError_t launch_transport(const TransportParams& P, int grid, size_t smem, cudaStream_t s)
 {
-    if (P.G.fmt == kFmtP4 && use_reg(P))
-        transport_kernel<kFmtP4, true><<<grid, kBlock, smem, s>>>(P);
-    else if (P.G.fmt == kFmtP4)
-        transport_kernel<kFmtP4, false><<<grid, kBlock, smem, s>>>(P);
-    else if (P.G.fmt == kFmtP8)
-        transport_kernel<kFmtP8, false><<<grid, kBlock, smem, s>>>(P);
-    else
-        transport_kernel<kFmtRaw, false><<<grid, kBlock, smem, s>>>(P);
+    kernel_for(P)<<<grid, kBlock, smem, s>>>(P);
     return cudaGetLastError();
 }
 

@@ -35,6 +35,10 @@ struct Grid {
     const float* dens;    // raw densities, bricked (raw format only)
     int32_t fmt;
     int32_t n_codes;      // palette size (P4/P8)
+    // Palette codes carry this bit when the voxel's 8^3 macro cell is
+    // uniform (all voxels the same code): 8 for P4 (<= 8 entries), 128 for
+    // P8 (<= 128 entries), 0 when not encoded.
+    int32_t ubit;
 };
 
 // Device error record; code is an xs_status.
@@ -92,6 +96,7 @@ struct TransportParams {
     int32_t track_var;
     int32_t var_cap;
     double march_h;
+    int32_t skip;           // 1: cross uniform macro cells in one step
 
     // tallies
     unsigned long long* accum;

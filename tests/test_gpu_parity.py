@@ -25,6 +25,16 @@ from paper_2201_13191_b200 import synthetic as S
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(params=["exact", "macro"])
+def walk_mode(request):
+    """exact: voxel-by-voxel Siddon (strict REF replay); macro: uniform 8^3
+    macro cells crossed in one step (the default; fp64-rounding-level change)."""
+    ctx = X.projector.default_context(0)
+    ctx.set_option("exact_walk", 1 if request.param == "exact" else 0)
+    yield request.param
+    ctx.set_option("exact_walk", 0)
+
+
 def _crit2():
     w = I.material("water")
     ph = S.make_cube_phantom(32, 0.2, 6.4, w, 1.0)
@@ -98,7 +108,7 @@ def _replay_compare(gpu, cpu, frac_tol=1e-3):
         assert abs(x - y) <= 1e-9 * max(abs(y), 1e-300) or abs(x - y) <= 1e-6 * abs(y), (k, x, y)
 
 
-def test_scatter_replay_criterion2(orc):
+def test_scatter_replay_criterion2(orc, walk_mode):
     """Acceptance criterion 2 inputs (acceptance_main.cpp:128-158), same seed:
     total 0.000496451 (proj/test_output.txt:31)."""
     ph, g = _crit2()
@@ -112,7 +122,7 @@ def test_scatter_replay_criterion2(orc):
 
 
 @pytest.mark.parametrize("step", [1, 3])
-def test_scatter_replay_polyenergetic_roulette_variance(orc, step):
+def test_scatter_replay_polyenergetic_roulette_variance(orc, step, walk_mode):
     ph = _rods(32)
     g = I.make_circular_geometry(100.0, 60.0, 32, 24, 0.8, 4)
     spec, resp = I.kramers_spectrum(150.0), I.detector_response()
@@ -127,7 +137,7 @@ def test_scatter_replay_polyenergetic_roulette_variance(orc, step):
     assert np.mean(rel > 1e-6) <= 1e-3
 
 
-def test_scatter_bit_identical_runs_and_splits():
+def test_scatter_bit_identical_runs_and_splits(walk_mode):
     """Fixed-point tallies: identical bits for repeated runs and any split of
     the history range (the multi-GPU photon-batch contract)."""
     import torch

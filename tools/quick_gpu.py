@@ -16,4 +16,4 @@ for name, fn, n in [("C1", configs.c1, 1_000_000), ("C2", configs.c2, 2_000_000)
     print(f"{name}: build {tb:.2f}s upload {tu:.3f}s fmt={s['voxel_format']} pal={s['palette_size']} "
           f"scatter {ts:.3f}s kernel {s['kernel_ms']:.1f}ms hist/s={r.histories/(s['kernel_ms']/1e3):.3e} "
           f"steps/hist={steps/r.histories:.1f} (fp {s['free_path_steps']/r.histories:.1f}) rays/hist={s['scoring_rays']/r.histories:.2f} "
-          f"Gsteps/s={steps/(s['kernel_ms']/1e3)/1e9:.1f} total={r.total:.6g}±{r.total_std_error:.2g} primary {tp*1e3:.1f}ms", flush=True)
+          f"Gsteps/s={steps/(s["kernel_ms"]/1e3)/1e9:.1f} iters/hist={s["walk_iterations"]/r.histories:.1f} total={r.total:.6g}±{r.total_std_error:.2g} primary {tp*1e3:.1f}ms", flush=True)
