@@ -171,10 +171,12 @@ struct xs_context {
     DevBuf<xsd::InterpEntry> interp_tab;
     uint32_t queue_len = 512;
     int max_slots = 64;
+    int ready_len = 12;
+    int done_len = 64;
     int macro_skip = 1;
 
     xs_launch_stats last{};
-    int walk_thresh = 28;
+    int walk_thresh = 32;
     int grab = 64;
 };
 
@@ -536,6 +538,8 @@ void accumulate(xs_context* c, const xs_geometry& g, int angle, const xs_spectru
     H = std::max(1, std::min(H, std::min(64, c->max_slots)));
     P.slots_per_warp = H;
     P.queue_len = (int32_t)Q;
+    P.ready_len = c->ready_len;
+    P.done_len = std::max(c->done_len, 64);
     const int block = xsd::transport_block_size();
     const size_t smem = xsd::transport_smem_bytes(P);
     int per_sm = 0;
@@ -710,6 +714,8 @@ int xs_ctx_create(int32_t device, xs_context** out)
                 q <<= 1;
             c->queue_len = q;
         }
+        if (const char* e = std::getenv("XSCAT_READY"))
+            c->ready_len = std::max(1, std::min(64, std::atoi(e)));
         if (const char* e = std::getenv("XSCAT_SKIP"))
             c->macro_skip = std::atoi(e) != 0;
         if (const char* e = std::getenv("XSCAT_SLOTS"))
@@ -767,6 +773,10 @@ int xs_ctx_set_option(xs_context* c, const char* key, int64_t value)
             c->queue_len = q;
         } else if (k == "max_slots") {
             c->max_slots = (int)std::max<int64_t>(1, std::min<int64_t>(64, value));
+        } else if (k == "ready_len") {
+            c->ready_len = (int)std::max<int64_t>(1, std::min<int64_t>(64, value));
+        } else if (k == "done_len") {
+            c->done_len = (int)std::max<int64_t>(64, std::min<int64_t>(256, value));
         } else if (k == "grab") {
             c->grab = (int)std::max<int64_t>(1, value);
         } else {
@@ -804,7 +814,7 @@ int xs_upload_phantom(xs_context* c, const xs_phantom* ph)
             fail(XS_E_RUNTIME, "%s", scan.bad_msg.c_str());
 
         const int n_pairs = (int)scan.pairs.size();
-        const int fmt = n_pairs <= 16 ? xsd::kFmtP4 : (n_pairs <= 256 ? xsd::kFmtP8 : xsd::kFmtRaw);
+        const int fmt = n_pairs <= 8 ? xsd::kFmtP4 : (n_pairs <= 255 ? xsd::kFmtP8 : xsd::kFmtRaw);
         xsd::Grid G{};
         G.nx = ph->dims[0];
         G.ny = ph->dims[1];

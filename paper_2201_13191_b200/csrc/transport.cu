@@ -287,6 +287,8 @@ __device__ __forceinline__ int cross_count(double tn, double dt, double rdt, dou
 {
     if (s == 0 || tn > tm)
         return 0;
+    if (k == 0)
+        return 1; // tn == tm: the plain Siddon crossing (REF trace.cpp:146-153)
     int n = (int)((tm - tn) * rdt) + 1;
     n = n > k + 1 ? k + 1 : n;
     if (n > 1 && tn + (n - 1) * dt > tm)
@@ -338,50 +340,61 @@ __device__ __forceinline__ bool walk_step(const TransportParams& P, const MuTab<
         return ++w.ix < w.iy;
     }
     const int code = decode<FMT>(w.raw, w.shift);
-    if (SKIP && (code & G.ubit)) { // uniform macro cell: integrate to its exit in one step
-        {
-            const double mu = tab.mu(P, code & ~G.ubit, 0.f);
-            const int kx = w.sx > 0 ? 7 - (w.ix & 7) : (w.ix & 7);
-            const int ky = w.sy > 0 ? 7 - (w.iy & 7) : (w.iy & 7);
-            const int kz = w.sz > 0 ? 7 - (w.iz & 7) : (w.iz & 7);
-            double tm = w.texit;
-            if (w.sx != 0 && w.tnx + kx * w.dtx < tm)
-                tm = w.tnx + kx * w.dtx;
-            if (w.sy != 0 && w.tny + ky * w.dty < tm)
-                tm = w.tny + ky * w.dty;
-            if (w.sz != 0 && w.tnz + kz * w.dtz < tm)
-                tm = w.tnz + kz * w.dtz;
-            const double seg = mu * (tm - w.t);
-            if (w.depth + seg >= w.target) {
-                w.hit = 1;
-                w.mu_hit = mu;
-                w.texit = tm;
-                return false;
-            }
-            w.depth += seg;
-            w.t = tm;
-            if (tm >= w.texit)
-                return false;
-            // advance every axis past the boundaries it crosses before tm
-            const int nx_ = cross_count(w.tnx, w.dtx, w.rdx, tm, kx, w.sx);
-            const int ny_ = cross_count(w.tny, w.dty, w.rdy, tm, ky, w.sy);
-            const int nz_ = cross_count(w.tnz, w.dtz, w.rdz, tm, kz, w.sz);
-            w.ix += nx_ * w.sx;
-            w.iy += ny_ * w.sy;
-            w.iz += nz_ * w.sz;
-            w.tnx += nx_ * w.dtx;
-            w.tny += ny_ * w.dty;
-            w.tnz += nz_ * w.dtz;
-            w.skipped += (uint32_t)(nx_ + ny_ + nz_) - 1u;
-            if ((uint32_t)w.ix >= (uint32_t)G.nx || (uint32_t)w.iy >= (uint32_t)G.ny ||
-                (uint32_t)w.iz >= (uint32_t)G.nz)
-                return false;
-            w.ax = term_x(G, w.ix);
-            w.ay = term_y(G, w.iy);
-            w.az = term_z(G, w.iz);
-            prefetch<FMT>(G, w.ax + w.ay + w.az, w.raw, w.shift, w.dens);
-            return true;
+    if (SKIP) {
+        // One step = up to the next boundary crossing, or, in a uniform 8^3
+        // macro cell (code flag), up to the cell's exit: k* boundaries of
+        // each axis remain inside the cell (0 outside uniform cells, where
+        // this is exactly REF's voxel step).  Branch-free, so lanes in
+        // uniform and mixed cells do not diverge.
+        const int c = code & ~G.ubit;
+        const bool u = (code & G.ubit) != 0;
+        const int kx = u ? (w.sx > 0 ? 7 - (w.ix & 7) : (w.ix & 7)) : 0;
+        const int ky = u ? (w.sy > 0 ? 7 - (w.iy & 7) : (w.iy & 7)) : 0;
+        const int kz = u ? (w.sz > 0 ? 7 - (w.iz & 7) : (w.iz & 7)) : 0;
+        const double ex = kx ? w.tnx + kx * w.dtx : w.tnx;
+        const double ey = ky ? w.tny + ky * w.dty : w.tny;
+        const double ez = kz ? w.tnz + kz * w.dtz : w.tnz;
+        double tm = ex;
+        if (ey < tm)
+            tm = ey;
+        if (ez < tm)
+            tm = ez;
+        if (w.texit < tm)
+            tm = w.texit;
+        const double mu = tab.mu(P, c, w.dens);
+        const double seg = mu * (tm - w.t);
+        const double nd = w.depth + seg;
+        if (nd >= w.target) { // free path ends in this voxel / cell; t_hit in hit_t()
+            w.hit = 1;
+            w.mu_hit = mu;
+            w.texit = tm;
+            return false;
         }
+        const int nx = cross_count(w.tnx, w.dtx, w.rdx, tm, kx, w.sx);
+        const int ny = cross_count(w.tny, w.dty, w.rdy, tm, ky, w.sy);
+        const int nz = cross_count(w.tnz, w.dtz, w.rdz, tm, kz, w.sz);
+        const int nix = w.ix + nx * w.sx, niy = w.iy + ny * w.sy, niz = w.iz + nz * w.sz;
+        const bool inside = (tm < w.texit) && (uint32_t)nix < (uint32_t)G.nx &&
+                            (uint32_t)niy < (uint32_t)G.ny && (uint32_t)niz < (uint32_t)G.nz;
+        const uint32_t nax = nx ? term_x(G, nix) : w.ax;
+        const uint32_t nay = ny ? term_y(G, niy) : w.ay;
+        const uint32_t naz = nz ? term_z(G, niz) : w.az;
+        if (inside)
+            prefetch<FMT>(G, nax + nay + naz, w.raw, w.shift, w.dens);
+        w.depth = nd;
+        w.t = tm;
+        w.tnx = nx ? w.tnx + nx * w.dtx : w.tnx;
+        w.tny = ny ? w.tny + ny * w.dty : w.tny;
+        w.tnz = nz ? w.tnz + nz * w.dtz : w.tnz;
+        if (u)
+            w.skipped += (uint32_t)(nx + ny + nz) - 1u;
+        w.ix = nix;
+        w.iy = niy;
+        w.iz = niz;
+        w.ax = nax;
+        w.ay = nay;
+        w.az = naz;
+        return inside;
     }
     const float dens = w.dens;
     double tn = w.tnx;

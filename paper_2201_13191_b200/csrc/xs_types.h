@@ -5,7 +5,7 @@
 
 namespace xsd {
 
-constexpr int kMaxMaterials = 16; // incl. vacuum; the REF bundle has 5
+constexpr int kMaxMaterials = 8; // incl. vacuum; the REF bundle has 5
 constexpr int kMaxPalette = 256;
 constexpr int kMaxBins = 1024;
 
@@ -110,6 +110,8 @@ struct TransportParams {
     int32_t walk_thresh;    // leave the walk phase when this many lanes need events
     int32_t slots_per_warp; // live histories per warp (<= 64)
     int32_t queue_len;      // ray-task FIFO entries per warp (power of two)
+    int32_t ready_len;      // set-up rays buffered per warp
+    int32_t done_len;       // finished rays buffered per warp (>= 64)
 
     // variance scratch: var_cap entries per history slot
     uint32_t* var_pix;
