@@ -512,6 +512,20 @@ void accumulate(xs_context* c, const xs_geometry& g, int angle, const xs_spectru
     P.max_inter = cfg.max_interactions;
     P.track_var = cfg.track_variance ? 1 : 0;
     P.skip = c->macro_skip;
+    { // shared energy knots of the mu tables (REF bundle: yes)
+        int first = -1;
+        bool same = true;
+        for (int m = 1; m < c->n_mats; ++m) {
+            if (c->mats[m].t[0].x.empty())
+                continue;
+            if (first < 0)
+                first = m;
+            else if (c->mats[m].t[0].x != c->mats[first].t[0].x)
+                same = false;
+        }
+        P.shared_mu_grid = first > 0 && same;
+        P.grid_mat = first > 0 ? first : 0;
+    }
     P.march_h = cfg.step_voxels *
                 std::min({c->grid.hx, c->grid.hy, c->grid.hz}); // REF trace.cpp:117
     P.accum = d_accum;

@@ -44,6 +44,7 @@ struct __align__(8) Slot {
     double ox, oy, oz;             // last interaction point
     double ix, iy, iz;             // incoming direction at it
     double e_in, w_split;          // energy at it, weight per pseudo-particle
+    double pref;                   // pi r0^2 / sigma(E) of its kind (REF cross_sections.cpp:56-79)
     unsigned long long T[3];       // history total, fixed-point limbs (unit U_img)
     uint32_t r_photon, r_bin, r_block, r_pos, r_b0, r_b1, r_b2, r_b3; // Philox stream
     int32_t bin, gen, kind, mat;
@@ -89,6 +90,47 @@ __device__ __forceinline__ void store_rng(Slot& s, const Rng& r)
 // shared memory: palette entries (P4) or mass attenuation per material
 // (P8 / raw, multiplied by the voxel density at lookup).  Values are the
 // products REF MuField forms (trace.cpp:10-20).
+// Log-log evaluation of several tables at one energy.  When every material's
+// mu table has the same energy knots (true for the reference's bundled data,
+// checked at upload) the knot search and log(e) are shared; the arithmetic
+// is that of tab_loglog (REF table.hpp:57-69), so values are identical.
+struct SharedLog {
+    int i;
+    bool exact, ok;
+    double le;
+    __device__ __forceinline__ void init(const TransportParams& P, double e, DevStatus* st, int bin)
+    {
+        ok = false;
+        if (!P.shared_mu_grid)
+            return;
+        const Tab t = mtab(P, P.mats[P.grid_mat].mu);
+        if (!tab_locate(t, e, i, exact)) {
+            raise(st, XS_E_OUT_OF_RANGE, kErrTableRange, bin, e, 0.0);
+            return;
+        }
+        le = exact ? 0.0 : nl_log(e);
+        ok = true;
+    }
+    __device__ __forceinline__ double eval(const TransportParams& P, TabDesc d, double e, DevStatus* st,
+                                           int bin) const
+    {
+        if (!ok)
+            return loglog_or_fail(P, d, e, st, bin);
+        const Tab t = mtab(P, d);
+        if (exact)
+            return __ldg(t.y + i);
+        const double y0 = __ldg(t.y + i), y1 = __ldg(t.y + i + 1);
+        if (y0 <= 0.0 || y1 <= 0.0) {
+            const double x0 = __ldg(t.x + i), x1 = __ldg(t.x + i + 1);
+            const double u = (e - x0) / (x1 - x0);
+            return y0 + u * (y1 - y0);
+        }
+        const double lx0 = __ldg(t.lx + i), lx1 = __ldg(t.lx + i + 1);
+        const double u = (le - lx0) / (lx1 - lx0);
+        return nl_exp(__ldg(t.ly + i) + u * (__ldg(t.ly + i + 1) - __ldg(t.ly + i)));
+    }
+};
+
 template <int FMT, bool REG>
 struct MuTab {
     double t0, t1, t2, t3;
@@ -103,9 +145,11 @@ struct MuTab {
             if (!REG)
                 for (int c = 0; c < P.n_pal; ++c)
                     T[c * kBlock] = 0.0;
+            SharedLog sl;
+            sl.init(P, e, st, bin);
             for (int m = 1; m < P.n_mats; ++m) {
                 const MatDesc& md = P.mats[m];
-                const double ma = md.has_tables ? loglog_or_fail(P, md.mu, e, st, bin) : 0.0;
+                const double ma = md.has_tables ? sl.eval(P, md.mu, e, st, bin) : 0.0;
                 for (int c = 0; c < P.n_pal; ++c)
                     if (P.pal_mat[c] == m) {
                         const double mu = ma * (double)P.pal_dens[c];
@@ -129,9 +173,11 @@ struct MuTab {
             t3 = v3_;
         } else {
             T[0] = 0.0;
+            SharedLog sl;
+            sl.init(P, e, st, bin);
             for (int m = 1; m < P.n_mats; ++m) {
                 const MatDesc& md = P.mats[m];
-                T[m * kBlock] = md.has_tables ? loglog_or_fail(P, md.mu, e, st, bin) : 0.0;
+                T[m * kBlock] = md.has_tables ? sl.eval(P, md.mu, e, st, bin) : 0.0;
             }
         }
     }
@@ -274,9 +320,10 @@ __device__ __noinline__ bool walk_begin(const TransportParams& P, Walk& w, V3 o,
     w.ay = term_y(G, w.iy);
     w.az = term_z(G, w.iz);
     prefetch<FMT>(G, w.ax + w.ay + w.az, w.raw, w.shift, w.dens);
-    w.rdx = 1.0 / w.dtx;
-    w.rdy = 1.0 / w.dty;
-    w.rdz = 1.0 / w.dtz;
+    // 1/dt estimates for macro-cell skips (cross_count corrects them exactly)
+    w.rdx = fabs(d.x) * G.ihx;
+    w.rdy = fabs(d.y) * G.ihy;
+    w.rdz = fabs(d.z) * G.ihz;
     return true;
 }
 
@@ -586,6 +633,13 @@ __device__ __noinline__ void history_event(const TransportParams& P, const Block
     S.kind = kind;
     S.mat = mat;
     S.w_split = W / P.splitting;
+    { // the cross-section prefactor of p_lambda is the same for all its rays
+        const double sigma = (kind == K_COMPTON ? incoh : coh) * kBarn;
+        if (!(sigma > 0.0))
+            raise(st, XS_E_RUNTIME, kind == K_COMPTON ? kErrSigmaIncoh : kErrSigmaCoh, bin, E, 0.0);
+        const double r0 = kR0;
+        S.pref = kPi * r0 * r0 / sigma;
+    }
     atomicAdd(&S.pending, P.splitting);
     for (int k = 0; k < P.splitting; ++k) { // REF :162-164 pixel draws
         int iu = (int)(rng_uniform(rng, P.k0, P.k1, P.angle) * P.nu);
@@ -766,20 +820,16 @@ __device__ __noinline__ double score_setup(const TransportParams& P, const Slot&
     const MatDesc& md = P.mats[S.mat];
     const double E = S.e_in;
     double p_dir;
-    const double r0 = kR0;
-    if (S.kind == K_COMPTON) { // cross_sections.cpp:56-66
-        const double sigma = loglog_or_fail(P, md.incoh, E, st, S.bin) * kBarn;
-        if (!(sigma > 0.0))
-            raise(st, XS_E_RUNTIME, kErrSigmaIncoh, S.bin, E, 0.0);
-        p_dir = kPi * r0 * r0 / sigma * kn_core(E, theta) * form_S(P, md, momentum_transfer(E, theta));
-        e_out = E * compton_ratio(E, theta);
+    if (S.kind == K_COMPTON) { // cross_sections.cpp:56-66 (ratio shared by kn_core and e_out)
+        const double ratio = compton_ratio(E, theta);
+        const double s = nl_sin(theta);
+        const double kn = ratio * ratio * (ratio + 1.0 / ratio - s * s);
+        p_dir = S.pref * kn * form_S(P, md, momentum_transfer(E, theta));
+        e_out = E * ratio;
     } else { // cross_sections.cpp:68-79
-        const double sigma = loglog_or_fail(P, md.coh, E, st, S.bin) * kBarn;
-        if (!(sigma > 0.0))
-            raise(st, XS_E_RUNTIME, kErrSigmaCoh, S.bin, E, 0.0);
         const double c2 = nl_cos(theta);
         const double f = form_F(P, md, momentum_transfer(E, theta));
-        p_dir = kPi * r0 * r0 / sigma * (1.0 + c2 * c2) * f * f;
+        p_dir = S.pref * (1.0 + c2 * c2) * f * f;
         e_out = E;
     }
     double dep = 0.0;

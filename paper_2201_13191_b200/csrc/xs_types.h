@@ -97,6 +97,8 @@ struct TransportParams {
     int32_t var_cap;
     double march_h;
     int32_t skip;           // 1: cross uniform macro cells in one step
+    int32_t shared_mu_grid; // all materials' mu tables share grid_mat's energy knots
+    int32_t grid_mat;
 
     // tallies
     unsigned long long* accum;
