@@ -885,60 +885,14 @@ __global__ void __launch_bounds__(kBlock, 4) transport_kernel(const __grid_const
     uint32_t head = 0;                // warp-uniform queue head
     uint64_t wq_next = 0, wq_end = 0; // warp-uniform history reservation
     bool pool_empty = false;
-
-    int ttype = T_NONE, tslot = 0;
-    uint32_t tpix = 0;
-    double tpre = 0.0;
-    bool walking = false;
-    Walk w;
-    w.march = 0;
     uint32_t c_fp = 0, c_sc = 0, c_rays = 0, c_int = 0, c_iter = 0;
 
+    // Each iteration: admit histories, set up one ray per lane from the FIFO,
+    // walk until every lane's ray has ended, process the 32 completions.
+    // The walker state is local to an iteration, so nothing of it is live
+    // across the out-of-line event calls (no ABI save/restore traffic).
     for (;;) {
-        // ------------------------------------------------ 1. completions
-        if (ttype != T_NONE && !walking) {
-            if (ttype == T_FREE)
-                c_fp += w.steps + w.skipped;
-            else
-                c_sc += w.steps + w.skipped;
-            c_iter += w.steps;
-            const uint64_t var_base = (gwarp * H + tslot) * (uint64_t)P.var_cap;
-            if (ttype == T_SCORE) { // REF run_history :178-193
-                Slot& S = slots[tslot];
-                const double x = tpre * nl_exp(-w.depth);
-                uint64_t l0 = 0, l1 = 0, l2 = 0;
-                if (!isfinite(x)) {
-                    raise(st, XS_E_RUNTIME, kErrNonFinite, S.bin, S.e_in, x);
-                } else if (!quantize(ldexp(x, -P.log2_img), l0, l1, l2)) {
-                    raise(st, XS_E_RUNTIME, kErrTallyOverflow, S.bin, S.e_in, x);
-                } else {
-                    unsigned long long* img = P.accum + P.off_image + 4ull * tpix;
-                    red_add(img + 0, l0);
-                    red_add(img + 1, l1);
-                    red_add(img + 2, l2);
-                    sadd(&S.T[0], l0);
-                    sadd(&S.T[1], l1);
-                    sadd(&S.T[2], l2);
-                }
-                if (P.track_var) {
-                    const int k = atomicAdd(&S.n_var, 1);
-                    if (k < P.var_cap) {
-                        P.var_pix[var_base + k] = tpix;
-                        P.var_val[var_base + k] = x;
-                    }
-                }
-                end_history(P, B, slots, hdr, tslot, var_base, st);
-            } else {
-                if (w.hit)
-                    ++c_int;
-                history_event<FMT>(P, B, slots, hdr, q, qmask, tslot, w.hit != 0, w.hit ? hit_t(w) : 0.0, w.ix, w.iy, w.iz,
-                                   var_base, st);
-            }
-            ttype = T_NONE;
-        }
-        __syncwarp();
-
-        // ------------------------------------------------ 2. admit histories
+        // ------------------------------------------------ 1. admit histories
         const unsigned long long free_now = hdr->free_mask;
         if (free_now && !pool_empty) {
             const int n_free = __popcll(free_now);
@@ -976,13 +930,21 @@ __global__ void __launch_bounds__(kBlock, 4) transport_kernel(const __grid_const
         }
         __syncwarp();
 
-        // ------------------------------------------------ 3. pop + start tasks
+        // ------------------------------------------------ 2. pop + set up
         const uint32_t tail = *(volatile uint32_t*)&hdr->tail;
         const uint32_t avail = tail - head;
-        const unsigned idle = __ballot_sync(kFull, ttype == T_NONE);
-        const int rank = __popc(idle & lt_mask);
-        if (ttype == T_NONE && (uint32_t)rank < avail) {
-            const uint64_t task = q[(head + rank) & qmask];
+        int ttype = T_NONE, tslot = 0;
+        uint32_t tpix = 0;
+        double tpre = 0.0;
+        bool walking = false;
+        Walk w;
+        w.march = 0;
+        w.hit = 0;
+        w.steps = 0;
+        w.skipped = 0;
+        w.depth = 0.0;
+        if ((uint32_t)lane < avail) {
+            const uint64_t task = q[(head + lane) & qmask];
             ttype = (int)((task >> 16) & 0xff);
             tslot = (int)(task & 0xffff);
             tpix = (uint32_t)(task >> 32);
@@ -1002,12 +964,10 @@ __global__ void __launch_bounds__(kBlock, 4) transport_kernel(const __grid_const
                 ++c_rays;
             }
         }
-        const uint32_t n_idle = (uint32_t)__popc(idle);
-        head += n_idle < avail ? n_idle : avail;
+        head += avail < 32u ? avail : 32u;
 
         // ------------------------------------------------ termination
-        const unsigned active = __ballot_sync(kFull, ttype != T_NONE);
-        if (!active) {
+        if (__ballot_sync(kFull, ttype != T_NONE) == 0) {
             if (pool_empty && tail == head && hdr->free_mask == all_free)
                 break;
             if (*(volatile int32_t*)&st->code != 0)
@@ -1015,22 +975,56 @@ __global__ void __launch_bounds__(kBlock, 4) transport_kernel(const __grid_const
             continue;
         }
 
-        // ------------------------------------------------ 4. walk in lockstep
-        const bool can_refill = (tail != head) || (hdr->free_mask != 0 && !pool_empty);
-        const unsigned busy = active;
-        for (;;) {
+        // ------------------------------------------------ 3. walk in lockstep
+        while (__ballot_sync(kFull, walking)) {
             if (walking) {
                 walking = walk_step<FMT, REG, SKIP>(P, tab, w);
                 ++w.steps;
             }
-            const unsigned wmask = __ballot_sync(kFull, walking);
-            if (!wmask)
-                break;
-            const unsigned waiting = can_refill ? ~wmask : (busy & ~wmask);
-            const int need = can_refill ? P.walk_thresh : max(1, __popc(busy) >> 2);
-            if (__popc(waiting) >= need)
-                break;
         }
+
+        // ------------------------------------------------ 4. completions
+        if (ttype != T_NONE) {
+            if (ttype == T_FREE)
+                c_fp += w.steps + w.skipped;
+            else
+                c_sc += w.steps + w.skipped;
+            c_iter += w.steps;
+            const uint64_t var_base = (gwarp * H + tslot) * (uint64_t)P.var_cap;
+            if (ttype == T_SCORE) { // REF run_history :178-193
+                Slot& S = slots[tslot];
+                const double x = tpre * nl_exp(-w.depth);
+                uint64_t l0 = 0, l1 = 0, l2 = 0;
+                if (!isfinite(x)) {
+                    raise(st, XS_E_RUNTIME, kErrNonFinite, S.bin, S.e_in, x);
+                } else if (!quantize(ldexp(x, -P.log2_img), l0, l1, l2)) {
+                    raise(st, XS_E_RUNTIME, kErrTallyOverflow, S.bin, S.e_in, x);
+                } else {
+                    unsigned long long* img = P.accum + P.off_image + 4ull * tpix;
+                    red_add(img + 0, l0);
+                    red_add(img + 1, l1);
+                    red_add(img + 2, l2);
+                    sadd(&S.T[0], l0);
+                    sadd(&S.T[1], l1);
+                    sadd(&S.T[2], l2);
+                }
+                if (P.track_var) {
+                    const int k = atomicAdd(&S.n_var, 1);
+                    if (k < P.var_cap) {
+                        P.var_pix[var_base + k] = tpix;
+                        P.var_val[var_base + k] = x;
+                    }
+                }
+                end_history(P, B, slots, hdr, tslot, var_base, st);
+            } else {
+                const bool hit = w.hit != 0;
+                if (hit)
+                    ++c_int;
+                history_event<FMT>(P, B, slots, hdr, q, qmask, tslot, hit, hit ? hit_t(w) : 0.0, w.ix,
+                                   w.iy, w.iz, var_base, st);
+            }
+        }
+        __syncwarp();
         if (*(volatile int32_t*)&st->code != 0)
             break;
     }
