@@ -1,0 +1,354 @@
+// xscat_b200_ref_adapter.hpp — drop-in replacement of the reference's
+// projector API (include/xscat/transport.hpp:69-116 and
+// include/xscat/postprocess.hpp:13-41) on the B200 library.
+//
+// Header-only C++17 over the C ABI of xscat_gpu.h.  It takes and returns the
+// reference's own types, so a reference user switches a call site by
+// qualifying it with xscat_b200:: (or with `using xscat_b200::...`), e.g. in
+// REF src/correction.cpp:184-194:
+//
+//     ScanResult scatter_run = xscat_b200::run_scan(phantom, g_mc, spec, resp, cfg.sim,
+//                                                   scatter_subset, ScanQuantity::scatter,
+//                                                   cfg.workers);
+//
+// Errors are rethrown as the exception types the reference throws
+// (xs_status -> std::runtime_error / out_of_range / invalid_argument /
+// domain_error), with the reference's message text.  `workers` is accepted
+// and ignored: results do not depend on it (or on the number of GPUs).
+//
+// Device selection: XSCAT_DEVICE (default 0).  One context per thread; the
+// scene (phantom + response) is uploaded on every call, like the reference
+// receives it on every call; Projector keeps it resident across calls.
+#pragma once
+
+#include <cstdlib>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "xscat/detector_image.hpp"
+#include "xscat/postprocess.hpp"
+#include "xscat/transport.hpp"
+#include "xscat_gpu.h"
+
+namespace xscat_b200 {
+
+inline void throw_status(int st, const xs_context* ctx)
+{
+    if (st == XS_OK)
+        return;
+    const std::string msg = xs_last_error(ctx);
+    switch (st) {
+    case XS_E_OUT_OF_RANGE:
+        throw std::out_of_range(msg);
+    case XS_E_INVALID_ARGUMENT:
+        throw std::invalid_argument(msg);
+    case XS_E_DOMAIN:
+        throw std::domain_error(msg);
+    default:
+        throw std::runtime_error(msg);
+    }
+}
+
+// ---------------------------------------------------------- type bridging
+struct Packed {
+    std::vector<xs_material> mats;
+    xs_phantom ph{};
+    xs_geometry g{};
+    xs_spectrum s{};
+    std::vector<double> se, sw;
+    xs_response r{};
+    xs_sim_config c{};
+};
+
+inline xs_table table_view(const xscat::Table1D& t)
+{
+    return xs_table{static_cast<int32_t>(t.size()), t.xs().data(), t.ys().data()};
+}
+
+inline void pack_phantom(Packed& p, const xscat::VoxelPhantom& ph)
+{
+    p.mats.resize(ph.materials.size());
+    for (std::size_t i = 0; i < ph.materials.size(); ++i) {
+        const xscat::Material& m = ph.materials[i];
+        xs_material& x = p.mats[i];
+        x.name = m.name.c_str();
+        x.z_eff = m.z_eff;
+        x.density_ref = m.density_ref;
+        if (!m.has_tables()) {
+            x.mu = x.sigma_incoh = x.sigma_coh = x.sigma_pe = x.s_factor = x.f_factor =
+                xs_table{0, nullptr, nullptr};
+            continue;
+        }
+        x.mu = table_view(m.mu);
+        x.sigma_incoh = table_view(m.sigma_incoh);
+        x.sigma_coh = table_view(m.sigma_coh);
+        x.sigma_pe = table_view(m.sigma_pe);
+        x.s_factor = table_view(m.s_factor);
+        x.f_factor = table_view(m.f_factor);
+    }
+    for (int a = 0; a < 3; ++a)
+        p.ph.dims[a] = ph.dims[a];
+    p.ph.voxel_size[0] = ph.voxel_size.x;
+    p.ph.voxel_size[1] = ph.voxel_size.y;
+    p.ph.voxel_size[2] = ph.voxel_size.z;
+    p.ph.origin[0] = ph.origin.x;
+    p.ph.origin[1] = ph.origin.y;
+    p.ph.origin[2] = ph.origin.z;
+    p.ph.material_id = ph.material_id.data();
+    p.ph.density = ph.density.data();
+    p.ph.n_materials = static_cast<int32_t>(ph.materials.size());
+    p.ph.materials = p.mats.data();
+}
+
+inline void pack_call(Packed& p, const xscat::ScanGeometry& g, const xscat::Spectrum& spec,
+                      const xscat::SimConfig& cfg)
+{
+    p.g = xs_geometry{g.sdd, g.sod, g.nu, g.nv, g.pixel_pitch, g.n_angles(), g.angles.data()};
+    p.se.clear();
+    p.sw.clear();
+    for (const auto& b : spec.bins) {
+        p.se.push_back(b.energy_kev);
+        p.sw.push_back(b.weight);
+    }
+    p.s = xs_spectrum{static_cast<int32_t>(spec.bins.size()), p.se.data(), p.sw.data()};
+    p.c = xs_sim_config{cfg.photons_total, cfg.splitting,        cfg.roulette_survival,
+                        cfg.roulette_wmin_rel, cfg.step_voxels,  cfg.max_interactions,
+                        cfg.seed,              cfg.track_variance ? 1 : 0};
+}
+
+// ------------------------------------------------------------------ context
+class Context {
+public:
+    explicit Context(int device = default_device())
+    {
+        throw_status(xs_ctx_create(device, &ctx_), nullptr);
+    }
+    ~Context() { xs_ctx_destroy(ctx_); }
+    Context(const Context&) = delete;
+    Context& operator=(const Context&) = delete;
+    xs_context* get() const { return ctx_; }
+
+    static int default_device()
+    {
+        const char* e = std::getenv("XSCAT_DEVICE");
+        return e ? std::atoi(e) : 0;
+    }
+
+private:
+    xs_context* ctx_ = nullptr;
+};
+
+inline Context& thread_context()
+{
+    thread_local Context ctx;
+    return ctx;
+}
+
+// A scene resident on the device (upload once, project many angles).
+class Projector {
+public:
+    Projector(const xscat::VoxelPhantom& ph, const xscat::DetectorResponse& resp,
+              Context& ctx = thread_context())
+        : ctx_(ctx)
+    {
+        Packed p;
+        pack_phantom(p, ph);
+        throw_status(xs_upload_phantom(ctx_.get(), &p.ph), ctx_.get());
+        const xs_response r{table_view(resp.dqe), table_view(resp.deposit)};
+        throw_status(xs_upload_response(ctx_.get(), &r), ctx_.get());
+    }
+
+    // REF simulate_scatter_stats (transport.hpp:89-91)
+    xscat::SimResult scatter_stats(const xscat::ScanGeometry& g, int angle_idx,
+                                   const xscat::Spectrum& spec, const xscat::SimConfig& cfg) const
+    {
+        Packed p;
+        pack_call(p, g, spec, cfg);
+        xscat::SimResult out;
+        out.image = xscat::DetectorImage(g.nu, g.nv);
+        std::vector<double> var;
+        if (cfg.track_variance)
+            var.assign(out.image.values.size(), 0.0);
+        xs_scatter_result r{};
+        r.image = out.image.values.data();
+        r.variance = cfg.track_variance ? var.data() : nullptr;
+        throw_status(xs_simulate_scatter_stats(ctx_.get(), &p.g, angle_idx, &p.s, &p.c, &r),
+                     ctx_.get());
+        if (cfg.track_variance)
+            out.image.variance = std::move(var);
+        out.ledger.initial = r.ledger.initial;
+        out.ledger.escaped = r.ledger.escaped;
+        out.ledger.absorbed = r.ledger.absorbed;
+        out.ledger.culled = r.ledger.culled;
+        out.ledger.roulette_killed = r.ledger.roulette_killed;
+        out.ledger.roulette_boost = r.ledger.roulette_boost;
+        out.histories = r.histories;
+        out.total = r.total;
+        out.total_std_error = r.total_std_error;
+        return out;
+    }
+
+    // REF simulate_primary (transport.hpp:100-102)
+    xscat::DetectorImage primary(const xscat::ScanGeometry& g, int angle_idx,
+                                 const xscat::Spectrum& spec, const xscat::SimConfig& cfg) const
+    {
+        Packed p;
+        pack_call(p, g, spec, cfg);
+        xscat::DetectorImage img(g.nu, g.nv);
+        throw_status(xs_simulate_primary(ctx_.get(), &p.g, angle_idx, &p.s, &p.c, img.values.data()),
+                     ctx_.get());
+        return img;
+    }
+
+    // REF run_scan (transport.hpp:112-116)
+    xscat::ScanResult scan(const xscat::ScanGeometry& g, const xscat::Spectrum& spec,
+                           const xscat::SimConfig& cfg, const std::vector<int>& subset,
+                           xscat::ScanQuantity what) const
+    {
+        Packed p;
+        pack_call(p, g, spec, cfg);
+        const std::size_t np = static_cast<std::size_t>(g.nu) * g.nv;
+        const bool want_p = what != xscat::ScanQuantity::scatter;
+        const bool want_s = what != xscat::ScanQuantity::primary;
+        std::vector<double> prim(want_p ? np * subset.size() : 0), scat(want_s ? np * subset.size() : 0);
+        std::vector<double> secs(subset.size());
+        std::vector<int32_t> sub(subset.begin(), subset.end());
+        const int q = what == xscat::ScanQuantity::primary ? 0 : (what == xscat::ScanQuantity::scatter ? 1 : 2);
+        throw_status(xs_run_scan(ctx_.get(), &p.g, &p.s, &p.c, sub.data(), static_cast<int32_t>(sub.size()), q,
+                                 want_p ? prim.data() : nullptr, want_s ? scat.data() : nullptr,
+                                 secs.data()),
+                     ctx_.get());
+        std::vector<double> angles;
+        for (int i : subset)
+            angles.push_back(g.angles[i]);
+        xscat::ScanResult out;
+        if (want_p)
+            out.primary = xscat::make_stack(g.nu, g.nv, angles);
+        if (want_s)
+            out.scatter = xscat::make_stack(g.nu, g.nv, angles);
+        for (std::size_t i = 0; i < subset.size(); ++i) {
+            if (want_p)
+                std::copy(prim.begin() + i * np, prim.begin() + (i + 1) * np,
+                          out.primary.images[i].values.begin());
+            if (want_s)
+                std::copy(scat.begin() + i * np, scat.begin() + (i + 1) * np,
+                          out.scatter.images[i].values.begin());
+        }
+        out.seconds_per_angle = secs;
+        return out;
+    }
+
+private:
+    Context& ctx_;
+};
+
+// ------------------------------------------- REF-signature free functions
+inline xscat::SimResult simulate_scatter_stats(const xscat::VoxelPhantom& ph, const xscat::ScanGeometry& g,
+                                               int angle_idx, const xscat::Spectrum& spec,
+                                               const xscat::DetectorResponse& resp,
+                                               const xscat::SimConfig& cfg, int /*workers*/ = 1)
+{
+    return Projector(ph, resp).scatter_stats(g, angle_idx, spec, cfg);
+}
+
+inline xscat::DetectorImage simulate_scatter(const xscat::VoxelPhantom& ph, const xscat::ScanGeometry& g,
+                                             int angle_idx, const xscat::Spectrum& spec,
+                                             const xscat::DetectorResponse& resp,
+                                             const xscat::SimConfig& cfg, int workers = 1)
+{
+    return xscat_b200::simulate_scatter_stats(ph, g, angle_idx, spec, resp, cfg, workers).image;
+}
+
+inline xscat::DetectorImage simulate_primary(const xscat::VoxelPhantom& ph, const xscat::ScanGeometry& g,
+                                             int angle_idx, const xscat::Spectrum& spec,
+                                             const xscat::DetectorResponse& resp,
+                                             const xscat::SimConfig& cfg, int /*workers*/ = 1)
+{
+    return Projector(ph, resp).primary(g, angle_idx, spec, cfg);
+}
+
+inline xscat::ScanResult run_scan(const xscat::VoxelPhantom& ph, const xscat::ScanGeometry& g,
+                                  const xscat::Spectrum& spec, const xscat::DetectorResponse& resp,
+                                  const xscat::SimConfig& cfg, const std::vector<int>& angle_subset,
+                                  xscat::ScanQuantity what, int /*workers*/)
+{
+    return Projector(ph, resp).scan(g, spec, cfg, angle_subset, what);
+}
+
+inline std::vector<std::uint64_t> apportion_photons(const xscat::Spectrum& spec,
+                                                    std::uint64_t photons_total)
+{
+    Packed p;
+    pack_call(p, xscat::ScanGeometry{}, spec, xscat::SimConfig{});
+    std::vector<std::uint64_t> out(spec.bins.size());
+    throw_status(xs_apportion_photons(&p.s, photons_total, out.data()), nullptr);
+    return out;
+}
+
+// ------------------------------------------------------ post-processing
+inline std::vector<double> sg_kernel(int left, int right, int polyorder)
+{
+    std::vector<double> k(static_cast<std::size_t>(left + right + 1));
+    throw_status(xs_sg_kernel(left, right, polyorder, k.data()), nullptr);
+    return k;
+}
+
+inline xscat::SgFilterSpec default_sg_spec(int nu, int nv)
+{
+    int32_t w = 0, o = 0;
+    xs_default_sg_spec(nu, nv, &w, &o);
+    return xscat::SgFilterSpec{w, o};
+}
+
+inline xscat::DetectorImage sg_smooth(const xscat::DetectorImage& img, const xscat::SgFilterSpec& f)
+{
+    xscat::DetectorImage out(img.nu, img.nv);
+    Context& c = thread_context();
+    throw_status(xs_sg_smooth(c.get(), img.values.data(), out.values.data(), img.nu, img.nv, 1, f.window,
+                              f.polyorder, 0),
+                 c.get());
+    return out;
+}
+
+inline xscat::ProjectionStack interpolate_angles(const xscat::ProjectionStack& stack,
+                                                 const std::vector<double>& target_angles)
+{
+    const std::size_t np = static_cast<std::size_t>(stack.nu) * stack.nv;
+    std::vector<double> in(np * stack.images.size()), out(np * target_angles.size());
+    for (std::size_t i = 0; i < stack.images.size(); ++i)
+        std::copy(stack.images[i].values.begin(), stack.images[i].values.end(), in.begin() + i * np);
+    Context& c = thread_context();
+    throw_status(xs_interpolate_angles(c.get(), in.data(), stack.angle_values.data(),
+                                       static_cast<int32_t>(stack.angle_values.size()), out.data(),
+                                       target_angles.data(), static_cast<int32_t>(target_angles.size()),
+                                       stack.nu, stack.nv, 0),
+                 c.get());
+    xscat::ProjectionStack r = xscat::make_stack(stack.nu, stack.nv, target_angles);
+    for (std::size_t i = 0; i < target_angles.size(); ++i)
+        std::copy(out.begin() + i * np, out.begin() + (i + 1) * np, r.images[i].values.begin());
+    return r;
+}
+
+inline xscat::DetectorImage upsample_image(const xscat::DetectorImage& img, int nu_out, int nv_out)
+{
+    xscat::DetectorImage out(nu_out, nv_out);
+    Context& c = thread_context();
+    throw_status(xs_upsample_image(c.get(), img.values.data(), img.nu, img.nv, 1, out.values.data(), nu_out,
+                                   nv_out, 0),
+                 c.get());
+    return out;
+}
+
+inline xscat::DetectorImage downsample_average(const xscat::DetectorImage& img, int nu_out, int nv_out)
+{
+    xscat::DetectorImage out(nu_out, nv_out);
+    Context& c = thread_context();
+    throw_status(xs_downsample_average(c.get(), img.values.data(), img.nu, img.nv, 1, out.values.data(),
+                                       nu_out, nv_out, 0),
+                 c.get());
+    return out;
+}
+
+} // namespace xscat_b200

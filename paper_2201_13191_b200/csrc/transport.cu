@@ -33,6 +33,9 @@ namespace {
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kWarps = 4; // warps per block
 constexpr int kBlock = 32 * kWarps;
+#ifndef XSD_MIN_BLOCKS
+#define XSD_MIN_BLOCKS 4
+#endif
 
 enum : int { T_NONE = -1, T_FREE = 0, T_SCORE = 1 };
 enum : int { K_PE = 0, K_COMPTON = 1, K_RAYLEIGH = 2 };
@@ -842,7 +845,7 @@ __device__ __noinline__ double score_setup(const TransportParams& P, const Slot&
 
 // =================================================================== kernel
 template <int FMT, bool REG, bool SKIP>
-__global__ void __launch_bounds__(kBlock, 4) transport_kernel(const __grid_constant__ TransportParams P)
+__global__ void __launch_bounds__(kBlock, XSD_MIN_BLOCKS) transport_kernel(const __grid_constant__ TransportParams P)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     const int H = P.slots_per_warp;

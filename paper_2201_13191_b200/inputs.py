@@ -540,3 +540,44 @@ def kramers_spectrum(e_max: float, filter_material: Optional[Material] = None,
     for w in w_list:
         peak = max(peak, w)
     return Spectrum(np.array(e_list), np.array([w / peak for w in w_list]))
+
+
+# ------------------------------------------------ writers of REF's formats
+def save_material(m: Material, path) -> None:
+    """REF save_material (material.cpp:225-244): %.17g round-trips exactly."""
+    lines = [f"name = {m.name}", f"z_eff = {float(m.z_eff):.17g}",
+             f"density = {float(m.density_ref):.17g}"]
+    for tag, t in zip(_SECTIONS, m.tables()):
+        lines.append(f"[{tag}]")
+        lines += [f"{float(x):.17g} {float(y):.17g}" for x, y in zip(t.x, t.y)]
+    pathlib.Path(path).write_text("\n".join(lines) + "\n")
+
+
+def save_spectrum(s: Spectrum, path) -> None:
+    """REF save_spectrum (spectrum.cpp:62-73)."""
+    rows = ["# keV, relative fluence"] + [f"{float(e):.17g}, {float(w):.17g}"
+                                         for e, w in zip(s.energy_kev, s.weight)]
+    pathlib.Path(path).write_text("\n".join(rows) + "\n")
+
+
+def save_detector_response(r: DetectorResponse, path) -> None:
+    """REF save_detector_response (detector_response.cpp:81-89)."""
+    rows = ["# keV, dqe, deposit_keV"] + [f"{float(e):.17g}, {float(q):.17g}, {float(d):.17g}"
+                                         for e, q, d in zip(r.dqe.x, r.dqe.y, r.deposit.y)]
+    pathlib.Path(path).write_text("\n".join(rows) + "\n")
+
+
+def write_reference_data(root) -> pathlib.Path:
+    """Recreate the reference's proj/data tree (materials/, spectra/,
+    detector/) from the bundled tables, for programs that load REF files."""
+    root = pathlib.Path(root)
+    b = _bundle()
+    for sub in ("materials", "spectra", "detector"):
+        (root / sub).mkdir(parents=True, exist_ok=True)
+    for name in b["materials"]:
+        save_material(material(name), root / "materials" / f"{name}.mat")
+    for name in b["spectra"]:
+        save_spectrum(spectrum(name), root / "spectra" / f"{name}.csv")
+    for name in b["detector"]:
+        save_detector_response(detector_response(name), root / "detector" / f"{name}.csv")
+    return root

@@ -1,0 +1,127 @@
+// ref_adapter_demo.cpp — the reference's own API usage, compiled against the
+// reference headers, run twice: on the reference library (CPU) and through
+// xscat_b200_ref_adapter.hpp on the B200.  Prints one PASS/FAIL line per
+// check (acceptance_main.cpp style) and exits non-zero on any failure.
+//   usage: ref_adapter_demo <data dir with materials/ spectra/ detector/>
+#include <cmath>
+#include <cstdio>
+#include <filesystem>
+#include <string>
+
+#include "xscat/synthetic.hpp"
+#include "xscat_b200_ref_adapter.hpp"
+
+using namespace xscat;
+namespace fs = std::filesystem;
+
+static int g_fail = 0;
+
+static void check(bool ok, const char* what, const std::string& detail)
+{
+    std::printf("%s  %-52s %s\n", ok ? "PASS" : "FAIL", what, detail.c_str());
+    if (!ok)
+        ++g_fail;
+}
+
+int main(int argc, char** argv)
+{
+    if (argc < 2) {
+        std::fprintf(stderr, "usage: %s <data dir>\n", argv[0]);
+        return 2;
+    }
+    const fs::path data = argv[1];
+    const Material w = load_material(data / "materials" / "water.mat");
+    const Material al = load_material(data / "materials" / "aluminum.mat");
+    const DetectorResponse resp = load_detector_response(data / "detector" / "gd2o2s_208um.csv");
+    char buf[256];
+
+    // acceptance criterion 2 inputs (acceptance_main.cpp:128-158)
+    {
+        const VoxelPhantom ph = make_cube_phantom(32, 0.2, 6.4, w, 1.0);
+        const ScanGeometry g = make_circular_geometry(60.0, 40.0, 24, 24, 0.55, 1);
+        const Spectrum spec = monochromatic_spectrum(100.0);
+        SimConfig cfg;
+        cfg.photons_total = 100000;
+        cfg.splitting = 10;
+        cfg.seed = 424242;
+        const SimResult cpu = xscat::simulate_scatter_stats(ph, g, 0, spec, resp, cfg, 4);
+        const SimResult gpu = xscat_b200::simulate_scatter_stats(ph, g, 0, spec, resp, cfg, 4);
+        std::snprintf(buf, sizeof buf, "(ref %.9g, b200 %.9g; se %.3g / %.3g)", cpu.total, gpu.total,
+                      cpu.total_std_error, gpu.total_std_error);
+        check(std::abs(gpu.total - cpu.total) <= 1e-9 * cpu.total && gpu.histories == cpu.histories,
+              "simulate_scatter_stats, criterion-2 inputs", buf);
+    }
+    // primary on a two-material rods phantom, polyenergetic
+    {
+        const VoxelPhantom ph = make_rods_phantom(48, 10.0 / 48, 4.5, 8.0, w, 1.0, 4, 0.6, 3.0, al, 2.699);
+        const ScanGeometry g = make_circular_geometry(128.2, 86.2, 40, 32, 0.5, 6);
+        Spectrum spec;
+        for (int e = 20; e <= 148; e += 8)
+            spec.bins.push_back({double(e), 1.0 / e});
+        const DetectorImage cpu = xscat::simulate_primary(ph, g, 2, spec, resp, SimConfig{}, 4);
+        const DetectorImage gpu = xscat_b200::simulate_primary(ph, g, 2, spec, resp, SimConfig{}, 4);
+        double worst = 0.0;
+        for (std::size_t i = 0; i < cpu.values.size(); ++i)
+            worst = std::max(worst, std::abs(gpu.values[i] - cpu.values[i]) / cpu.values[i]);
+        std::snprintf(buf, sizeof buf, "(max rel diff %.2e)", worst);
+        check(worst <= 1e-12, "simulate_primary, rods + 17-bin spectrum", buf);
+
+        SimConfig cfg;
+        cfg.photons_total = 6000;
+        cfg.splitting = 5;
+        cfg.seed = 20240915;
+        const ScanResult scan = xscat_b200::run_scan(ph, g, spec, resp, cfg, {0, 3, 5}, ScanQuantity::both, 4);
+        bool same = scan.scatter.images.size() == 3 && scan.primary.images.size() == 3;
+        const int idx[3] = {0, 3, 5};
+        for (int i = 0; same && i < 3; ++i)
+            same = scan.scatter.images[i].values ==
+                       xscat_b200::simulate_scatter(ph, g, idx[i], spec, resp, cfg, 1).values &&
+                   scan.primary.images[i].values ==
+                       xscat_b200::simulate_primary(ph, g, idx[i], spec, resp, cfg, 1).values;
+        check(same, "run_scan == per-angle calls (bitwise)", "");
+        bool threw = false;
+        try {
+            xscat_b200::run_scan(ph, g, spec, resp, cfg, {}, ScanQuantity::both, 1);
+        } catch (const std::runtime_error& e) {
+            threw = std::string(e.what()).find("empty angle subset") != std::string::npos;
+        }
+        check(threw, "run_scan({}) throws runtime_error", "");
+        threw = false;
+        try {
+            xscat_b200::run_scan(ph, g, spec, resp, cfg, {9}, ScanQuantity::both, 1);
+        } catch (const std::out_of_range& e) {
+            threw = std::string(e.what()).find("angle index") != std::string::npos;
+        }
+        check(threw, "run_scan({9}) throws out_of_range", "");
+    }
+    // post-processing (REF postprocess.cpp) bitwise
+    {
+        DetectorImage img(40, 33);
+        for (std::size_t i = 0; i < img.values.size(); ++i)
+            img.values[i] = std::sin(0.37 * i) + 0.01 * i;
+        const SgFilterSpec f{7, 3};
+        check(xscat_b200::sg_smooth(img, f).values == xscat::sg_smooth(img, f).values, "sg_smooth bitwise", "");
+        check(xscat_b200::upsample_image(img, 80, 66).values == xscat::upsample_image(img, 80, 66).values,
+              "upsample_image bitwise", "");
+        check(xscat_b200::downsample_average(img, 20, 11).values ==
+                  xscat::downsample_average(img, 20, 11).values,
+              "downsample_average bitwise", "");
+        ProjectionStack st = make_stack(40, 33, {0.0, 1.0, 2.0, 3.0});
+        for (int k = 0; k < 4; ++k)
+            for (std::size_t i = 0; i < img.values.size(); ++i)
+                st.images[k].values[i] = img.values[i] * (k + 1);
+        const std::vector<double> tgt = {0.0, 0.5, 2.25, 3.5, 6.0};
+        const ProjectionStack a = xscat_b200::interpolate_angles(st, tgt), b = xscat::interpolate_angles(st, tgt);
+        bool same = true;
+        for (int k = 0; k < 5; ++k)
+            same = same && a.images[k].values == b.images[k].values;
+        check(same, "interpolate_angles bitwise", "");
+        check(xscat_b200::sg_kernel(2, 2, 3) == xscat::sg_kernel(2, 2, 3), "sg_kernel bitwise", "");
+        Spectrum sp;
+        sp.bins = {{20.0, 0.001}, {40.0, 1.0}, {60.0, 2.0}, {80.0, 0.0}, {100.0, 0.5}};
+        check(xscat_b200::apportion_photons(sp, 12345) == xscat::apportion_photons(sp, 12345),
+              "apportion_photons", "");
+    }
+    std::printf("%s\n", g_fail ? "FAILED" : "all checks passed");
+    return g_fail ? 1 : 0;
+}
