@@ -139,6 +139,10 @@ static __device__ double invert_mass(const TransportParams& P, const MatDesc& m,
 }
 
 // REF clip_to_grid (trace.cpp:29-56); returns false for a miss.
+// FAST: multiply by the reciprocal direction instead of dividing (the
+// macro-cell mode, which already differs from REF at rounding level);
+// otherwise REF's exact divisions.
+template <bool FAST = false>
 __device__ __forceinline__ bool clip_to_grid(const Grid& G, V3 o, V3 d, double& t0, double& t1,
                                              bool& bad)
 {
@@ -159,8 +163,15 @@ __device__ __forceinline__ bool clip_to_grid(const Grid& G, V3 o, V3 d, double& 
                 return false;
             continue;
         }
-        double ta = (l[a] - oo[a]) / dd[a];
-        double tb = (h[a] - oo[a]) / dd[a];
+        double ta, tb;
+        if (FAST) {
+            const double r = 1.0 / dd[a];
+            ta = (l[a] - oo[a]) * r;
+            tb = (h[a] - oo[a]) * r;
+        } else {
+            ta = (l[a] - oo[a]) / dd[a];
+            tb = (h[a] - oo[a]) / dd[a];
+        }
         if (ta > tb) {
             const double s = ta;
             ta = tb;
@@ -172,19 +183,21 @@ __device__ __forceinline__ bool clip_to_grid(const Grid& G, V3 o, V3 d, double& 
     return t0 < t1;
 }
 
+template <bool FAST = false>
 __device__ __forceinline__ void start_axis(double p, double o, double d, double org, double hs,
                                            double inv_h, int n, double t0, int& idx, int& step,
                                            double& tn, double& dt)
 {
     idx = voxel_of(p, org, inv_h, n);
+    const double r = FAST && d != 0.0 ? 1.0 / d : 0.0;
     if (d > 0.0) {
         step = 1;
-        dt = hs / d;
-        tn = (org + (idx + 1) * hs - o) / d;
+        dt = FAST ? hs * r : hs / d;
+        tn = FAST ? (org + (idx + 1) * hs - o) * r : (org + (idx + 1) * hs - o) / d;
     } else if (d < 0.0) {
         step = -1;
-        dt = -hs / d;
-        tn = (org + idx * hs - o) / d;
+        dt = FAST ? -hs * r : -hs / d;
+        tn = FAST ? (org + idx * hs - o) * r : (org + idx * hs - o) / d;
     } else {
         step = 0;
         dt = CUDART_INF;

@@ -281,7 +281,7 @@ struct Walk {
 
 
 
-template <int FMT>
+template <int FMT, bool FAST>
 __device__ __noinline__ bool walk_begin(const TransportParams& P, Walk& w, V3 o, V3 d,
                                            double target, bool march, DevStatus* st, int bin)
 {
@@ -297,7 +297,7 @@ __device__ __noinline__ bool walk_begin(const TransportParams& P, Walk& w, V3 o,
     w.depth = 0.0;
     w.steps = 0;
     w.skipped = 0;
-    if (!clip_to_grid(P.G, o, d, t0, t1, bad)) {
+    if (!clip_to_grid<FAST>(P.G, o, d, t0, t1, bad)) {
         if (bad)
             raise(st, XS_E_INVALID_ARGUMENT, 0, bin, 0.0, 0.0);
         return false;
@@ -316,9 +316,9 @@ __device__ __noinline__ bool walk_begin(const TransportParams& P, Walk& w, V3 o,
     w.march = 0;
     const V3 p = o + d * t0;
     const Grid& G = P.G;
-    start_axis(p.x, o.x, d.x, G.ox, G.hx, G.ihx, G.nx, t0, w.ix, w.sx, w.tnx, w.dtx);
-    start_axis(p.y, o.y, d.y, G.oy, G.hy, G.ihy, G.ny, t0, w.iy, w.sy, w.tny, w.dty);
-    start_axis(p.z, o.z, d.z, G.oz, G.hz, G.ihz, G.nz, t0, w.iz, w.sz, w.tnz, w.dtz);
+    start_axis<FAST>(p.x, o.x, d.x, G.ox, G.hx, G.ihx, G.nx, t0, w.ix, w.sx, w.tnx, w.dtx);
+    start_axis<FAST>(p.y, o.y, d.y, G.oy, G.hy, G.ihy, G.ny, t0, w.iy, w.sy, w.tny, w.dty);
+    start_axis<FAST>(p.z, o.z, d.z, G.oz, G.hz, G.ihz, G.nz, t0, w.iz, w.sz, w.tnz, w.dtz);
     w.ax = term_x(G, w.ix);
     w.ay = term_y(G, w.iy);
     w.az = term_z(G, w.iz);
@@ -955,7 +955,7 @@ __global__ void __launch_bounds__(kBlock, XSD_MIN_BLOCKS) transport_kernel(const
             if (ttype == T_FREE) { // REF trace.cpp:189-230
                 if (tab.energy != S.E)
                     tab.fill(P, S.E, st, S.bin);
-                walking = walk_begin<FMT>(P, w, v3(S.px, S.py, S.pz), v3(S.dx, S.dy, S.dz), S.target,
+                walking = walk_begin<FMT, SKIP>(P, w, v3(S.px, S.py, S.pz), v3(S.dx, S.dy, S.dz), S.target,
                                           false, st, S.bin);
             } else {
                 V3 o, to_det;
@@ -963,7 +963,7 @@ __global__ void __launch_bounds__(kBlock, XSD_MIN_BLOCKS) transport_kernel(const
                 tpre = score_setup(P, S, tpix, o, to_det, e_out, st);
                 if (tab.energy != e_out) // REF trace_attenuation builds MuField(e_out)
                     tab.fill(P, e_out, st, S.bin);
-                walking = walk_begin<FMT>(P, w, o, to_det, CUDART_INF, march, st, S.bin);
+                walking = walk_begin<FMT, SKIP>(P, w, o, to_det, CUDART_INF, march, st, S.bin);
                 ++c_rays;
             }
         }
