@@ -128,6 +128,7 @@ static __device__ double cumulative_mass(const TransportParams& P, const MatDesc
 static __device__ double invert_mass(const TransportParams& P, const MatDesc& m, double target, double q_hi)
 {
     double lo = 0.0, hi = q_hi;
+#pragma unroll 1
     for (int it = 0; it < 64; ++it) {
         const double mid = 0.5 * (lo + hi);
         if (cumulative_mass(P, m, mid) < target)

@@ -61,6 +61,44 @@ struct WarpHdr {
     unsigned long long free_mask;
 };
 
+// One out-of-line Philox draw on a history's stream kept in its slot (REF
+// rng.hpp:29-60).  A single copy of the 10-round refill instead of one per
+// call site keeps the event code small (instruction-cache bound kernel).
+__device__ __noinline__ double slot_uniform(Slot* s, uint32_t k0, uint32_t k1, uint32_t angle)
+{
+    if (s->r_pos == 4) {
+        uint32_t c0 = s->r_block, c1 = s->r_photon, c2 = s->r_bin, c3 = angle;
+#pragma unroll
+        for (int i = 0; i < 10; ++i) {
+            const uint32_t lo0 = 0xD2511F53u * c0, hi0 = __umulhi(0xD2511F53u, c0);
+            const uint32_t lo1 = 0xCD9E8D57u * c2, hi1 = __umulhi(0xCD9E8D57u, c2);
+            c0 = hi1 ^ c1 ^ k0;
+            c1 = lo1;
+            c2 = hi0 ^ c3 ^ k1;
+            c3 = lo0;
+            k0 += 0x9E3779B9u;
+            k1 += 0xBB67AE85u;
+        }
+        s->r_b0 = c0;
+        s->r_b1 = c1;
+        s->r_b2 = c2;
+        s->r_b3 = c3;
+        s->r_pos = 0;
+        ++s->r_block;
+    }
+    uint64_t hi, lo;
+    if (s->r_pos == 0) {
+        hi = s->r_b0;
+        lo = s->r_b1;
+    } else {
+        hi = s->r_b2;
+        lo = s->r_b3;
+    }
+    s->r_pos += 2;
+    const uint64_t bits = ((hi << 32) | lo) >> 11;
+    return ((double)bits + 0.5) * 0x1p-53;
+}
+
 __device__ __forceinline__ Rng load_rng(const Slot& s)
 {
     Rng r;
@@ -592,7 +630,6 @@ __device__ __noinline__ void history_event(const TransportParams& P, const Block
                                            uint64_t var_base, DevStatus* st)
 {
     Slot& S = slots[s];
-    Rng rng = load_rng(S);
     const int bin = S.bin;
     const double W = S.W;
     if (!hit) {
@@ -615,11 +652,10 @@ __device__ __noinline__ void history_event(const TransportParams& P, const Block
     const double total = pe + incoh + coh;
     if (!(total > 0.0))
         raise(st, XS_E_RUNTIME, kErrSigmaAll, bin, E, (double)mat);
-    const double u = rng_uniform(rng, P.k0, P.k1, P.angle) * total;
+    const double u = slot_uniform(&S, P.k0, P.k1, P.angle) * total;
     const int kind = u < pe ? K_PE : (u < pe + incoh ? K_COMPTON : K_RAYLEIGH);
     if (kind == K_PE) {
         ledger_add(P, B, 2, W, st, bin);
-        store_rng(S, rng);
         end_history(P, B, slots, hdr, s, var_base, st);
         return;
     }
@@ -644,9 +680,10 @@ __device__ __noinline__ void history_event(const TransportParams& P, const Block
         S.pref = kPi * r0 * r0 / sigma;
     }
     atomicAdd(&S.pending, P.splitting);
+#pragma unroll 1
     for (int k = 0; k < P.splitting; ++k) { // REF :162-164 pixel draws
-        int iu = (int)(rng_uniform(rng, P.k0, P.k1, P.angle) * P.nu);
-        int iv = (int)(rng_uniform(rng, P.k0, P.k1, P.angle) * P.nv);
+        int iu = (int)(slot_uniform(&S, P.k0, P.k1, P.angle) * P.nu);
+        int iv = (int)(slot_uniform(&S, P.k0, P.k1, P.angle) * P.nv);
         iu = iu < P.nu - 1 ? iu : P.nu - 1;
         iv = iv < P.nv - 1 ? iv : P.nv - 1;
         push(hdr, q, qmask, make_task(T_SCORE, s, (uint32_t)(iv * P.nu + iu)));
@@ -666,9 +703,9 @@ __device__ __noinline__ void history_event(const TransportParams& P, const Block
                 const double t = 1.0 + 2.0 * alpha; // kahn_sample_cos_theta, samplers.cpp:12-30
                 double cos_th;
                 for (;;) {
-                    const double r1 = rng_uniform(rng, P.k0, P.k1, P.angle);
-                    const double r2 = rng_uniform(rng, P.k0, P.k1, P.angle);
-                    const double r3 = rng_uniform(rng, P.k0, P.k1, P.angle);
+                    const double r1 = slot_uniform(&S, P.k0, P.k1, P.angle);
+                    const double r2 = slot_uniform(&S, P.k0, P.k1, P.angle);
+                    const double r3 = slot_uniform(&S, P.k0, P.k1, P.angle);
                     if (r1 <= t / (t + 8.0)) {
                         const double x = 1.0 + 2.0 * alpha * r2;
                         if (r3 <= 4.0 * (1.0 / x - 1.0 / (x * x))) {
@@ -687,9 +724,9 @@ __device__ __noinline__ void history_event(const TransportParams& P, const Block
                 const double cc = cos_th < -1.0 ? -1.0 : (1.0 < cos_th ? 1.0 : cos_th);
                 theta = nl_acos(cc);
                 const double sv = form_S(P, md, momentum_transfer(E, theta));
-                if (rng_uniform(rng, P.k0, P.k1, P.angle) * s_max <= sv) {
+                if (slot_uniform(&S, P.k0, P.k1, P.angle) * s_max <= sv) {
                     ap = alpha / (1.0 + alpha * (1.0 - nl_cos(theta)));
-                    phi = 2.0 * kPi * rng_uniform(rng, P.k0, P.k1, P.angle);
+                    phi = 2.0 * kPi * slot_uniform(&S, P.k0, P.k1, P.angle);
                     break;
                 }
             }
@@ -705,13 +742,13 @@ __device__ __noinline__ void history_event(const TransportParams& P, const Block
         } else {
             const double scale = kHc / E;
             for (;;) {
-                const double qq = invert_mass(P, md, rng_uniform(rng, P.k0, P.k1, P.angle) * tot, q_max);
+                const double qq = invert_mass(P, md, slot_uniform(&S, P.k0, P.k1, P.angle) * tot, q_max);
                 const double sh = 1.0 < qq * scale ? 1.0 : qq * scale;
                 const double cos_th = 1.0 - 2.0 * sh * sh;
-                if (rng_uniform(rng, P.k0, P.k1, P.angle) * 2.0 <= 1.0 + cos_th * cos_th) {
+                if (slot_uniform(&S, P.k0, P.k1, P.angle) * 2.0 <= 1.0 + cos_th * cos_th) {
                     const double cc = cos_th < -1.0 ? -1.0 : (1.0 < cos_th ? 1.0 : cos_th);
                     theta = nl_acos(cc);
-                    phi = 2.0 * kPi * rng_uniform(rng, P.k0, P.k1, P.angle);
+                    phi = 2.0 * kPi * slot_uniform(&S, P.k0, P.k1, P.angle);
                     break;
                 }
             }
@@ -729,7 +766,7 @@ __device__ __noinline__ void history_event(const TransportParams& P, const Block
         ledger_add(P, B, 3, W, st, bin);
         alive = false;
     } else if (S.wmin > 0.0 && W < S.wmin) { // REF :213-222
-        if (rng_uniform(rng, P.k0, P.k1, P.angle) < P.survival) {
+        if (slot_uniform(&S, P.k0, P.k1, P.angle) < P.survival) {
             const double boosted = W / P.survival;
             ledger_add(P, B, 5, boosted - W, st, bin);
             Wn = boosted;
@@ -740,11 +777,9 @@ __device__ __noinline__ void history_event(const TransportParams& P, const Block
     }
     if (alive) {
         S.W = Wn;
-        S.target = -nl_log(rng_uniform(rng, P.k0, P.k1, P.angle));
-        store_rng(S, rng);
+        S.target = -nl_log(slot_uniform(&S, P.k0, P.k1, P.angle));
         push(hdr, q, qmask, make_task(T_FREE, s, 0));
     } else {
-        store_rng(S, rng);
         end_history(P, B, slots, hdr, s, var_base, st);
     }
 }
@@ -764,10 +799,12 @@ __device__ __noinline__ void history_start(const TransportParams& P, const Block
             hi = mid;
     }
     const int bin = lo;
-    Rng rng;
-    rng_init(rng, (uint32_t)(h - sstart[lo]), (uint32_t)lo);
-    const double u1 = rng_uniform(rng, P.k0, P.k1, P.angle);
-    const double u2 = rng_uniform(rng, P.k0, P.k1, P.angle);
+    S.r_photon = (uint32_t)(h - sstart[lo]);
+    S.r_bin = (uint32_t)lo;
+    S.r_block = 0;
+    S.r_pos = 4;
+    const double u1 = slot_uniform(&S, P.k0, P.k1, P.angle);
+    const double u2 = slot_uniform(&S, P.k0, P.k1, P.angle);
     const double xu = (u1 - 0.5) * P.nu * P.pitch;
     const double xv = (u2 - 0.5) * P.nv * P.pitch;
     const V3 c = v3(P.center[0], P.center[1], P.center[2]);
@@ -795,8 +832,7 @@ __device__ __noinline__ void history_start(const TransportParams& P, const Block
     S.pending = 1;
     S.n_var = 0;
     ledger_add(P, B, 0, w0, st, bin);
-    S.target = -nl_log(rng_uniform(rng, P.k0, P.k1, P.angle));
-    store_rng(S, rng);
+    S.target = -nl_log(slot_uniform(&S, P.k0, P.k1, P.angle));
     push(hdr, q, qmask, make_task(T_FREE, s, 0));
     atomicAnd(&hdr->free_mask, ~(1ull << s));
 }
