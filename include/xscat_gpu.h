@@ -329,8 +329,7 @@ int xs_ctx_synchronize(xs_context* ctx);
  *   "exact_walk"  1: voxel-by-voxel Siddon everywhere (strict REF replay);
  *                 0 (default): cross uniform 8^3 macro cells in one step, which
  *                 changes the optical depths only at fp64 rounding level
- *   "walk_thresh" lanes waiting before a warp leaves the walk phase (1..32)
- *   "queue_len"   ray-task FIFO entries per warp (rounded to a power of two)
+ *   "queue_len"   scoring-ray FIFO entries per warp (rounded to a power of two)
  *   "max_slots"   live histories per warp (1..64)
  *   "grab"        histories a warp reserves from the pool at a time        */
 int xs_ctx_set_option(xs_context* ctx, const char* key, int64_t value);

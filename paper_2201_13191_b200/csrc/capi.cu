@@ -171,12 +171,9 @@ struct xs_context {
     DevBuf<xsd::InterpEntry> interp_tab;
     uint32_t queue_len = 512;
     int max_slots = 64;
-    int ready_len = 12;
-    int done_len = 64;
     int macro_skip = 1;
 
     xs_launch_stats last{};
-    int walk_thresh = 32;
     int grab = 64;
 };
 
@@ -540,20 +537,18 @@ void accumulate(xs_context* c, const xs_geometry& g, int angle, const xs_spectru
     P.h_end = h1;
     P.pool = c->pool.p;
     P.grab = c->grab;
-    P.walk_thresh = c->walk_thresh;
     P.status = c->status.p;
 
-    // warp-queue geometry: H live histories per warp, FIFO of Q tasks; the
-    // FIFO never holds more than H * (splitting + 1) tasks (see transport.cu)
+    // warp-queue geometry: H live histories per warp, scoring FIFO of Q
+    // tasks; it never holds more than H * splitting tasks (scoring rays are
+    // popped before any later free path, see transport.cu)
     uint32_t Q = c->queue_len;
-    while (Q < (uint32_t)cfg.splitting + 1)
+    while (Q < (uint32_t)cfg.splitting)
         Q <<= 1;
-    int H = (int)(Q / (uint32_t)(cfg.splitting + 1));
+    int H = (int)(Q / (uint32_t)cfg.splitting);
     H = std::max(1, std::min(H, std::min(64, c->max_slots)));
     P.slots_per_warp = H;
     P.queue_len = (int32_t)Q;
-    P.ready_len = c->ready_len;
-    P.done_len = std::max(c->done_len, 64);
     const int block = xsd::transport_block_size();
     const size_t smem = xsd::transport_smem_bytes(P);
     int per_sm = 0;
@@ -718,8 +713,6 @@ int xs_ctx_create(int32_t device, xs_context** out)
         c->stream = c->own;
         cuda_check(cudaEventCreate(&c->ev0), "event");
         cuda_check(cudaEventCreate(&c->ev1), "event");
-        if (const char* e = std::getenv("XSCAT_WALK_THRESH"))
-            c->walk_thresh = std::max(1, std::min(32, std::atoi(e)));
         if (const char* e = std::getenv("XSCAT_GRAB"))
             c->grab = std::max(1, std::atoi(e));
         if (const char* e = std::getenv("XSCAT_QUEUE")) {
@@ -728,8 +721,6 @@ int xs_ctx_create(int32_t device, xs_context** out)
                 q <<= 1;
             c->queue_len = q;
         }
-        if (const char* e = std::getenv("XSCAT_READY"))
-            c->ready_len = std::max(1, std::min(64, std::atoi(e)));
         if (const char* e = std::getenv("XSCAT_SKIP"))
             c->macro_skip = std::atoi(e) != 0;
         if (const char* e = std::getenv("XSCAT_SLOTS"))
@@ -778,8 +769,6 @@ int xs_ctx_set_option(xs_context* c, const char* key, int64_t value)
         const std::string k = key ? key : "";
         if (k == "exact_walk") {
             c->macro_skip = value ? 0 : 1;
-        } else if (k == "walk_thresh") {
-            c->walk_thresh = (int)std::max<int64_t>(1, std::min<int64_t>(32, value));
         } else if (k == "queue_len") {
             uint32_t q = 16;
             while (q < (uint32_t)std::max<int64_t>(16, value))
@@ -787,10 +776,6 @@ int xs_ctx_set_option(xs_context* c, const char* key, int64_t value)
             c->queue_len = q;
         } else if (k == "max_slots") {
             c->max_slots = (int)std::max<int64_t>(1, std::min<int64_t>(64, value));
-        } else if (k == "ready_len") {
-            c->ready_len = (int)std::max<int64_t>(1, std::min<int64_t>(64, value));
-        } else if (k == "done_len") {
-            c->done_len = (int)std::max<int64_t>(64, std::min<int64_t>(256, value));
         } else if (k == "grab") {
             c->grab = (int)std::max<int64_t>(1, value);
         } else {

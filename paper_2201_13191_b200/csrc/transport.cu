@@ -55,9 +55,16 @@ struct __align__(8) Slot {
     int32_t n_var;                 // variance scratch entries
 };
 
+// Two per-warp FIFOs: scoring rays (H * splitting entries) and free paths
+// (kFreeQ >= H entries, right after the scoring FIFO).  Batches are filled
+// scoring-first, so a batch is mostly one kind of ray (similar lengths, fewer
+// idle lanes in the lockstep walk).  Safety of the record reuse: a free path
+// is only popped once every scoring ray queued before it has been popped,
+// and set-up (which reads the interaction record) precedes any completion.
+constexpr int kFreeQ = 64;
 struct WarpHdr {
-    uint32_t tail;
-    uint32_t pad;
+    uint32_t tail;  // scoring FIFO
+    uint32_t ftail; // free-path FIFO
     unsigned long long free_mask;
 };
 
@@ -564,16 +571,23 @@ __device__ __forceinline__ void ledger_add(const TransportParams& P, const Block
         raise(st, XS_E_RUNTIME, kErrTallyOverflow, bin, 0.0, w);
 }
 
+__device__ __forceinline__ uint64_t make_task(int type, int slot, uint32_t pixel)
+{
+    return ((uint64_t)pixel << 32) | ((uint64_t)type << 16) | (uint64_t)slot;
+}
+
 __device__ __forceinline__ void push(WarpHdr* hdr, uint64_t* q, uint32_t qmask, uint64_t task)
 {
     const uint32_t i = atomicAdd(&hdr->tail, 1u);
     q[i & qmask] = task;
 }
 
-__device__ __forceinline__ uint64_t make_task(int type, int slot, uint32_t pixel)
+__device__ __forceinline__ void push_free(WarpHdr* hdr, uint64_t* q, uint32_t qmask, int s)
 {
-    return ((uint64_t)pixel << 32) | ((uint64_t)type << 16) | (uint64_t)slot;
+    const uint32_t i = atomicAdd(&hdr->ftail, 1u);
+    q[qmask + 1u + (i & (kFreeQ - 1))] = make_task(T_FREE, s, 0);
 }
+
 
 // History end (REF run_history :225-241): bin statistics from the exact
 // fixed-point history total, per-pixel grouping for the variance, free slot.
@@ -778,7 +792,7 @@ __device__ __noinline__ void history_event(const TransportParams& P, const Block
     if (alive) {
         S.W = Wn;
         S.target = -nl_log(slot_uniform(&S, P.k0, P.k1, P.angle));
-        push(hdr, q, qmask, make_task(T_FREE, s, 0));
+        push_free(hdr, q, qmask, s);
     } else {
         end_history(P, B, slots, hdr, s, var_base, st);
     }
@@ -833,7 +847,7 @@ __device__ __noinline__ void history_start(const TransportParams& P, const Block
     S.n_var = 0;
     ledger_add(P, B, 0, w0, st, bin);
     S.target = -nl_log(slot_uniform(&S, P.k0, P.k1, P.angle));
-    push(hdr, q, qmask, make_task(T_FREE, s, 0));
+    push_free(hdr, q, qmask, s);
     atomicAnd(&hdr->free_mask, ~(1ull << s));
 }
 
@@ -897,7 +911,7 @@ __global__ void __launch_bounds__(kBlock, XSD_MIN_BLOCKS) transport_kernel(const
     B.diag = B.ledger + 24;
     uint64_t* sstart = reinterpret_cast<uint64_t*>(B.diag + 8);
     unsigned char* p = reinterpret_cast<unsigned char*>(sstart + P.n_bins + 1);
-    const size_t warp_bytes = (size_t)H * sizeof(Slot) + sizeof(WarpHdr) + (size_t)P.queue_len * 8;
+    const size_t warp_bytes = (size_t)H * sizeof(Slot) + sizeof(WarpHdr) + (size_t)(P.queue_len + kFreeQ) * 8;
     unsigned char* wbase = p + (size_t)warp * warp_bytes;
     Slot* slots = reinterpret_cast<Slot*>(wbase);
     WarpHdr* hdr = reinterpret_cast<WarpHdr*>(wbase + (size_t)H * sizeof(Slot));
@@ -913,6 +927,7 @@ __global__ void __launch_bounds__(kBlock, XSD_MIN_BLOCKS) transport_kernel(const
     const unsigned long long all_free = H >= 64 ? ~0ull : ((1ull << H) - 1ull);
     if (lane == 0) {
         hdr->tail = 0;
+        hdr->ftail = 0;
         hdr->free_mask = all_free;
     }
     __syncthreads();
@@ -921,7 +936,7 @@ __global__ void __launch_bounds__(kBlock, XSD_MIN_BLOCKS) transport_kernel(const
     const uint64_t gwarp = (uint64_t)blockIdx.x * kWarps + warp;
     const bool march = P.step_voxels > 1;
 
-    uint32_t head = 0;                // warp-uniform queue head
+    uint32_t head = 0, fhead = 0;     // warp-uniform FIFO heads
     uint64_t wq_next = 0, wq_end = 0; // warp-uniform history reservation
     bool pool_empty = false;
     uint32_t c_fp = 0, c_sc = 0, c_rays = 0, c_int = 0, c_iter = 0;
@@ -971,7 +986,11 @@ __global__ void __launch_bounds__(kBlock, XSD_MIN_BLOCKS) transport_kernel(const
 
         // ------------------------------------------------ 2. pop + set up
         const uint32_t tail = *(volatile uint32_t*)&hdr->tail;
+        const uint32_t ftail = *(volatile uint32_t*)&hdr->ftail;
         const uint32_t avail = tail - head;
+        const uint32_t n_s = avail < 32u ? avail : 32u;
+        const uint32_t favail = ftail - fhead;
+        const uint32_t n_f = favail < 32u - n_s ? favail : 32u - n_s;
         int ttype = T_NONE, tslot = 0;
         uint32_t tpix = 0;
         double tpre = 0.0;
@@ -982,8 +1001,9 @@ __global__ void __launch_bounds__(kBlock, XSD_MIN_BLOCKS) transport_kernel(const
         w.steps = 0;
         w.skipped = 0;
         w.depth = 0.0;
-        if ((uint32_t)lane < avail) {
-            const uint64_t task = q[(head + lane) & qmask];
+        if ((uint32_t)lane < n_s + n_f) {
+            const uint64_t task = (uint32_t)lane < n_s ? q[(head + lane) & qmask]
+                                                       : q[qmask + 1u + ((fhead + lane - n_s) & (kFreeQ - 1))];
             ttype = (int)((task >> 16) & 0xff);
             tslot = (int)(task & 0xffff);
             tpix = (uint32_t)(task >> 32);
@@ -1003,11 +1023,12 @@ __global__ void __launch_bounds__(kBlock, XSD_MIN_BLOCKS) transport_kernel(const
                 ++c_rays;
             }
         }
-        head += avail < 32u ? avail : 32u;
+        head += n_s;
+        fhead += n_f;
 
         // ------------------------------------------------ termination
         if (__ballot_sync(kFull, ttype != T_NONE) == 0) {
-            if (pool_empty && tail == head && hdr->free_mask == all_free)
+            if (pool_empty && tail == head && ftail == fhead && hdr->free_mask == all_free)
                 break;
             if (*(volatile int32_t*)&st->code != 0)
                 break;
@@ -1089,7 +1110,7 @@ static bool use_reg(const TransportParams& P) { return P.G.fmt == kFmtP4 && P.n_
 size_t transport_smem_bytes(const TransportParams& P)
 {
     const size_t warp_bytes =
-        (size_t)P.slots_per_warp * sizeof(Slot) + sizeof(WarpHdr) + (size_t)P.queue_len * 8;
+        (size_t)P.slots_per_warp * sizeof(Slot) + sizeof(WarpHdr) + (size_t)(P.queue_len + kFreeQ) * 8;
     const int n_tab = P.G.fmt == kFmtP4 ? P.n_pal : P.n_mats;
     return (size_t)(8 * P.n_bins + 32) * 8 + (size_t)(P.n_bins + 1) * 8 + kWarps * warp_bytes +
            (use_reg(P) ? 0 : (size_t)n_tab * kBlock * 8);

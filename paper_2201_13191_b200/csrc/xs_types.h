@@ -109,11 +109,8 @@ struct TransportParams {
     uint64_t h_begin, h_end;
     unsigned long long* pool;
     int32_t grab;           // histories per warp grab
-    int32_t walk_thresh;    // leave the walk phase when this many lanes need events
     int32_t slots_per_warp; // live histories per warp (<= 64)
     int32_t queue_len;      // ray-task FIFO entries per warp (power of two)
-    int32_t ready_len;      // set-up rays buffered per warp
-    int32_t done_len;       // finished rays buffered per warp (>= 64)
 
     // variance scratch: var_cap entries per history slot
     uint32_t* var_pix;

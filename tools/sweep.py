@@ -9,4 +9,4 @@ r = proj.scatter_stats(w.geometry, 0, w.spectrum, configs.c3(photons=200000, pha
 r = proj.scatter_stats(w.geometry, 0, w.spectrum, w.config)
 s = r.stats
 st = s['free_path_steps'] + s['scoring_steps']
-print(f"thresh={os.environ.get('XSCAT_WALK_THRESH','8')} n={n} kernel {s['kernel_ms']:.0f} ms  hist/s {n/(s['kernel_ms']/1e3):.3e}  Gsteps/s {st/(s['kernel_ms']/1e3)/1e9:.1f}", flush=True)
+print(f"n={n} kernel {s['kernel_ms']:.0f} ms  hist/s {n/(s['kernel_ms']/1e3):.3e}  Gsteps/s {st/(s['kernel_ms']/1e3)/1e9:.1f}", flush=True)
