@@ -148,6 +148,11 @@ typedef struct xs_launch_stats {
     int32_t palette_size;
     uint64_t upload_bytes;     /* encoded voxel bytes of the last phantom upload (H2D) */
     uint64_t walk_iterations;  /* walker loop iterations (< steps when macro cells are skipped) */
+    uint64_t walk_lane_slots;  /* 32 x warp-level walker iterations (lane occupancy denominator) */
+    uint32_t blocks_per_sm;    /* resident transport blocks per SM */
+    uint32_t smem_per_block;   /* dynamic shared memory per transport block (bytes) */
+    uint32_t slots_per_warp;   /* live histories per warp */
+    uint32_t reserved;
 } xs_launch_stats;
 
 typedef struct xs_context xs_context;
@@ -329,7 +334,9 @@ int xs_ctx_synchronize(xs_context* ctx);
  *   "exact_walk"  1: voxel-by-voxel Siddon everywhere (strict REF replay);
  *                 0 (default): cross uniform 8^3 macro cells in one step, which
  *                 changes the optical depths only at fp64 rounding level
- *   "queue_len"   scoring-ray FIFO entries per warp (rounded to a power of two)
+ *   "smem_kb"     shared memory per transport block (8..227, default 48:
+ *                 four blocks per SM keep 60 KB of L1); bounds the live
+ *                 histories per warp
  *   "max_slots"   live histories per warp (1..64)
  *   "grab"        histories a warp reserves from the pool at a time        */
 int xs_ctx_set_option(xs_context* ctx, const char* key, int64_t value);

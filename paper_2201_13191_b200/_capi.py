@@ -76,7 +76,10 @@ class XsLaunchStats(C.Structure):
                 ("histories", C.c_uint64), ("scoring_rays", C.c_uint64),
                 ("interactions", C.c_uint64), ("kernel_ms", C.c_double),
                 ("voxel_format", C.c_int32), ("palette_size", C.c_int32),
-                ("upload_bytes", C.c_uint64), ("walk_iterations", C.c_uint64)]
+                ("upload_bytes", C.c_uint64), ("walk_iterations", C.c_uint64),
+                ("walk_lane_slots", C.c_uint64), ("blocks_per_sm", C.c_uint32),
+                ("smem_per_block", C.c_uint32), ("slots_per_warp", C.c_uint32),
+                ("reserved", C.c_uint32)]
 
 
 def dptr(a: np.ndarray):

@@ -22,6 +22,7 @@
 namespace xsd {
 size_t transport_smem_bytes(const TransportParams& P);
 int transport_block_size();
+int transport_pick_slots(TransportParams& P, int max_slots, size_t budget);
 cudaError_t transport_prepare(const TransportParams& P, size_t smem, int* blocks_per_sm);
 cudaError_t launch_transport(const TransportParams& P, int grid, size_t smem, cudaStream_t s);
 cudaError_t launch_primary(const PrimaryParams& P, cudaStream_t s);
@@ -169,7 +170,7 @@ struct xs_context {
     DevBuf<double> var_val;
     DevBuf<double> img, var, pp_a, pp_b, pp_c, pp_k;
     DevBuf<xsd::InterpEntry> interp_tab;
-    uint32_t queue_len = 512;
+    int smem_kb = 48; // per transport block: 4 blocks/SM leave 60 KB of L1
     int max_slots = 64;
     int macro_skip = 1;
 
@@ -539,16 +540,12 @@ void accumulate(xs_context* c, const xs_geometry& g, int angle, const xs_spectru
     P.grab = c->grab;
     P.status = c->status.p;
 
-    // warp-queue geometry: H live histories per warp, scoring FIFO of Q
-    // tasks; it never holds more than H * splitting tasks (scoring rays are
-    // popped before any later free path, see transport.cu)
-    uint32_t Q = c->queue_len;
-    while (Q < (uint32_t)cfg.splitting)
-        Q <<= 1;
-    int H = (int)(Q / (uint32_t)cfg.splitting);
-    H = std::max(1, std::min(H, std::min(64, c->max_slots)));
-    P.slots_per_warp = H;
-    P.queue_len = (int32_t)Q;
+    // warp-queue geometry (transport.cu): H live histories per warp, sized
+    // to the shared-memory budget
+    if ((uint64_t)g.nu * (uint64_t)g.nv >= (1ull << 26))
+        fail(XS_E_UNSUPPORTED, "xscat-gpu: scatter detector with %lld pixels exceeds 2^26",
+             (long long)g.nu * g.nv);
+    const int H = xsd::transport_pick_slots(P, c->max_slots, (size_t)c->smem_kb * 1024);
     const int block = xsd::transport_block_size();
     const size_t smem = xsd::transport_smem_bytes(P);
     int per_sm = 0;
@@ -580,6 +577,9 @@ void accumulate(xs_context* c, const xs_geometry& g, int angle, const xs_spectru
     cuda_check(cudaEventElapsedTime(&ms, c->ev0, c->ev1), "event time");
     c->last.kernel_ms = ms;
     c->last.voxel_format = c->grid.fmt;
+    c->last.blocks_per_sm = (uint32_t)per_sm;
+    c->last.smem_per_block = (uint32_t)smem;
+    c->last.slots_per_warp = (uint32_t)H;
     c->last.palette_size = c->n_pal;
     c->last.upload_bytes = c->last_upload_bytes;
 }
@@ -608,6 +608,7 @@ void finalize(xs_context* c, const xs_geometry& g, const xs_spectrum& spec, cons
     c->last.scoring_rays = diag[3];
     c->last.interactions = diag[4];
     c->last.walk_iterations = diag[5];
+    c->last.walk_lane_slots = diag[6];
 
     double* img = d_image;
     if (!img) {
@@ -715,12 +716,8 @@ int xs_ctx_create(int32_t device, xs_context** out)
         cuda_check(cudaEventCreate(&c->ev1), "event");
         if (const char* e = std::getenv("XSCAT_GRAB"))
             c->grab = std::max(1, std::atoi(e));
-        if (const char* e = std::getenv("XSCAT_QUEUE")) {
-            uint32_t q = 16;
-            while (q < (uint32_t)std::max(16, std::atoi(e)))
-                q <<= 1;
-            c->queue_len = q;
-        }
+        if (const char* e = std::getenv("XSCAT_SMEM_KB"))
+            c->smem_kb = std::max(8, std::min(227, std::atoi(e)));
         if (const char* e = std::getenv("XSCAT_SKIP"))
             c->macro_skip = std::atoi(e) != 0;
         if (const char* e = std::getenv("XSCAT_SLOTS"))
@@ -769,11 +766,8 @@ int xs_ctx_set_option(xs_context* c, const char* key, int64_t value)
         const std::string k = key ? key : "";
         if (k == "exact_walk") {
             c->macro_skip = value ? 0 : 1;
-        } else if (k == "queue_len") {
-            uint32_t q = 16;
-            while (q < (uint32_t)std::max<int64_t>(16, value))
-                q <<= 1;
-            c->queue_len = q;
+        } else if (k == "smem_kb") {
+            c->smem_kb = (int)std::max<int64_t>(8, std::min<int64_t>(227, value));
         } else if (k == "max_slots") {
             c->max_slots = (int)std::max<int64_t>(1, std::min<int64_t>(64, value));
         } else if (k == "grab") {

@@ -42,9 +42,8 @@ enum : int { K_PE = 0, K_COMPTON = 1, K_RAYLEIGH = 2 };
 
 // ------------------------------------------------------------ smem layout
 struct __align__(8) Slot {
-    double px, py, pz, dx, dy, dz; // photon position / direction
+    double px, py, pz, dx, dy, dz; // photon position (= last interaction point) / direction
     double E, W, wmin, target;     // energy, weight, roulette floor, -ln u of the pending free path
-    double ox, oy, oz;             // last interaction point
     double ix, iy, iz;             // incoming direction at it
     double e_in, w_split;          // energy at it, weight per pseudo-particle
     double pref;                   // pi r0^2 / sigma(E) of its kind (REF cross_sections.cpp:56-79)
@@ -571,21 +570,19 @@ __device__ __forceinline__ void ledger_add(const TransportParams& P, const Block
         raise(st, XS_E_RUNTIME, kErrTallyOverflow, bin, 0.0, w);
 }
 
-__device__ __forceinline__ uint64_t make_task(int type, int slot, uint32_t pixel)
+// Scoring task: pixel << 6 | slot (n_pixels < 2^26, checked on the host).
+// The scoring FIFO has qlen = H * splitting + 1 entries and its tail wraps
+// (atomicInc), so it can never fill; the free-path FIFO follows it.
+__device__ __forceinline__ void push_score(WarpHdr* hdr, uint32_t* q, uint32_t qlen, int s, uint32_t pixel)
 {
-    return ((uint64_t)pixel << 32) | ((uint64_t)type << 16) | (uint64_t)slot;
+    const uint32_t i = atomicInc(&hdr->tail, qlen - 1u);
+    q[i] = pixel << 6 | (uint32_t)s;
 }
 
-__device__ __forceinline__ void push(WarpHdr* hdr, uint64_t* q, uint32_t qmask, uint64_t task)
-{
-    const uint32_t i = atomicAdd(&hdr->tail, 1u);
-    q[i & qmask] = task;
-}
-
-__device__ __forceinline__ void push_free(WarpHdr* hdr, uint64_t* q, uint32_t qmask, int s)
+__device__ __forceinline__ void push_free(WarpHdr* hdr, uint32_t* q, uint32_t qlen, int s)
 {
     const uint32_t i = atomicAdd(&hdr->ftail, 1u);
-    q[qmask + 1u + (i & (kFreeQ - 1))] = make_task(T_FREE, s, 0);
+    q[qlen + (i & (kFreeQ - 1))] = (uint32_t)s;
 }
 
 
@@ -639,7 +636,7 @@ __device__ __forceinline__ void end_history(const TransportParams& P, const Bloc
 // (run_history :141-223) on the history's own Philox stream.
 template <int FMT>
 __device__ __noinline__ void history_event(const TransportParams& P, const Block& B, Slot* slots,
-                                           WarpHdr* hdr, uint64_t* q, uint32_t qmask, int s,
+                                           WarpHdr* hdr, uint32_t* q, uint32_t qlen, int s,
                                            bool hit, double t_hit, int vix, int viy, int viz,
                                            uint64_t var_base, DevStatus* st)
 {
@@ -676,9 +673,6 @@ __device__ __noinline__ void history_event(const TransportParams& P, const Block
     S.px = pos.x;
     S.py = pos.y;
     S.pz = pos.z;
-    S.ox = pos.x;
-    S.oy = pos.y;
-    S.oz = pos.z;
     S.ix = dir.x;
     S.iy = dir.y;
     S.iz = dir.z;
@@ -700,7 +694,7 @@ __device__ __noinline__ void history_event(const TransportParams& P, const Block
         int iv = (int)(slot_uniform(&S, P.k0, P.k1, P.angle) * P.nv);
         iu = iu < P.nu - 1 ? iu : P.nu - 1;
         iv = iv < P.nv - 1 ? iv : P.nv - 1;
-        push(hdr, q, qmask, make_task(T_SCORE, s, (uint32_t)(iv * P.nu + iu)));
+        push_score(hdr, q, qlen, s, (uint32_t)(iv * P.nu + iu));
     }
     // continuation (REF :195-205)
     V3 ndir;
@@ -792,7 +786,7 @@ __device__ __noinline__ void history_event(const TransportParams& P, const Block
     if (alive) {
         S.W = Wn;
         S.target = -nl_log(slot_uniform(&S, P.k0, P.k1, P.angle));
-        push_free(hdr, q, qmask, s);
+        push_free(hdr, q, qlen, s);
     } else {
         end_history(P, B, slots, hdr, s, var_base, st);
     }
@@ -800,7 +794,7 @@ __device__ __noinline__ void history_event(const TransportParams& P, const Block
 
 // History start (REF run_history :120-138, sample_emission :73-87).
 __device__ __noinline__ void history_start(const TransportParams& P, const Block& B, Slot* slots,
-                                           WarpHdr* hdr, uint64_t* q, uint32_t qmask,
+                                           WarpHdr* hdr, uint32_t* q, uint32_t qlen,
                                            const uint64_t* sstart, int s, uint64_t h, DevStatus* st)
 {
     Slot& S = slots[s];
@@ -847,7 +841,7 @@ __device__ __noinline__ void history_start(const TransportParams& P, const Block
     S.n_var = 0;
     ledger_add(P, B, 0, w0, st, bin);
     S.target = -nl_log(slot_uniform(&S, P.k0, P.k1, P.angle));
-    push_free(hdr, q, qmask, s);
+    push_free(hdr, q, qlen, s);
     atomicAnd(&hdr->free_mask, ~(1ull << s));
 }
 
@@ -863,7 +857,7 @@ __device__ __noinline__ double score_setup(const TransportParams& P, const Slot&
     const V3 c = v3(P.center[0], P.center[1], P.center[2]);
     const V3 ua = v3(P.uaxis[0], P.uaxis[1], P.uaxis[2]);
     const V3 px = (c + ua * du) + v3(0.0, 0.0, 1.0) * dv;
-    o = v3(S.ox, S.oy, S.oz);
+    o = v3(S.px, S.py, S.pz); // the interaction point until the next free path ends
     const V3 delta = px - o;
     const double d2 = dot(delta, delta);
     to_det = delta / sqrt(d2);
@@ -893,13 +887,19 @@ __device__ __noinline__ double score_setup(const TransportParams& P, const Slot&
 
 } // namespace
 
+// per-warp shared memory: slots, header, scoring + free-path FIFOs (8-aligned)
+__host__ __device__ inline size_t warp_bytes_of(int H, int qlen)
+{
+    return ((size_t)H * sizeof(Slot) + sizeof(WarpHdr) + (size_t)(qlen + kFreeQ) * 4 + 7) & ~(size_t)7;
+}
+
 // =================================================================== kernel
 template <int FMT, bool REG, bool SKIP>
 __global__ void __launch_bounds__(kBlock, XSD_MIN_BLOCKS) transport_kernel(const __grid_constant__ TransportParams P)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     const int H = P.slots_per_warp;
-    const uint32_t qmask = (uint32_t)P.queue_len - 1u; // power of two
+    const uint32_t qlen = (uint32_t)P.queue_len; // H * splitting + 1
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
@@ -911,11 +911,11 @@ __global__ void __launch_bounds__(kBlock, XSD_MIN_BLOCKS) transport_kernel(const
     B.diag = B.ledger + 24;
     uint64_t* sstart = reinterpret_cast<uint64_t*>(B.diag + 8);
     unsigned char* p = reinterpret_cast<unsigned char*>(sstart + P.n_bins + 1);
-    const size_t warp_bytes = (size_t)H * sizeof(Slot) + sizeof(WarpHdr) + (size_t)(P.queue_len + kFreeQ) * 8;
+    const size_t warp_bytes = warp_bytes_of(H, P.queue_len);
     unsigned char* wbase = p + (size_t)warp * warp_bytes;
     Slot* slots = reinterpret_cast<Slot*>(wbase);
     WarpHdr* hdr = reinterpret_cast<WarpHdr*>(wbase + (size_t)H * sizeof(Slot));
-    uint64_t* q = reinterpret_cast<uint64_t*>(hdr + 1);
+    uint32_t* q = reinterpret_cast<uint32_t*>(hdr + 1);
     MuTab<FMT, REG> tab;
     tab.T = reinterpret_cast<double*>(p + (size_t)kWarps * warp_bytes) + threadIdx.x;
     tab.energy = -1.0;
@@ -939,7 +939,7 @@ __global__ void __launch_bounds__(kBlock, XSD_MIN_BLOCKS) transport_kernel(const
     uint32_t head = 0, fhead = 0;     // warp-uniform FIFO heads
     uint64_t wq_next = 0, wq_end = 0; // warp-uniform history reservation
     bool pool_empty = false;
-    uint32_t c_fp = 0, c_sc = 0, c_rays = 0, c_int = 0, c_iter = 0;
+    uint32_t c_fp = 0, c_sc = 0, c_rays = 0, c_int = 0, c_iter = 0, c_wit = 0;
 
     // Each iteration: admit histories, set up one ray per lane from the FIFO,
     // walk until every lane's ray has ended, process the 32 completions.
@@ -979,7 +979,7 @@ __global__ void __launch_bounds__(kBlock, XSD_MIN_BLOCKS) transport_kernel(const
                 for (int k = 0; k < lane; ++k)
                     m &= m - 1;
                 const int s = __ffsll((long long)m) - 1;
-                history_start(P, B, slots, hdr, q, qmask, sstart, s, first + lane, st);
+                history_start(P, B, slots, hdr, q, qlen, sstart, s, first + lane, st);
             }
         }
         __syncwarp();
@@ -987,7 +987,7 @@ __global__ void __launch_bounds__(kBlock, XSD_MIN_BLOCKS) transport_kernel(const
         // ------------------------------------------------ 2. pop + set up
         const uint32_t tail = *(volatile uint32_t*)&hdr->tail;
         const uint32_t ftail = *(volatile uint32_t*)&hdr->ftail;
-        const uint32_t avail = tail - head;
+        const uint32_t avail = tail >= head ? tail - head : tail + qlen - head;
         const uint32_t n_s = avail < 32u ? avail : 32u;
         const uint32_t favail = ftail - fhead;
         const uint32_t n_f = favail < 32u - n_s ? favail : 32u - n_s;
@@ -1002,11 +1002,17 @@ __global__ void __launch_bounds__(kBlock, XSD_MIN_BLOCKS) transport_kernel(const
         w.skipped = 0;
         w.depth = 0.0;
         if ((uint32_t)lane < n_s + n_f) {
-            const uint64_t task = (uint32_t)lane < n_s ? q[(head + lane) & qmask]
-                                                       : q[qmask + 1u + ((fhead + lane - n_s) & (kFreeQ - 1))];
-            ttype = (int)((task >> 16) & 0xff);
-            tslot = (int)(task & 0xffff);
-            tpix = (uint32_t)(task >> 32);
+            uint32_t task;
+            if ((uint32_t)lane < n_s) {
+                uint32_t i = head + lane;
+                task = q[i >= qlen ? i - qlen : i];
+                ttype = T_SCORE;
+            } else {
+                task = q[qlen + ((fhead + lane - n_s) & (kFreeQ - 1))];
+                ttype = T_FREE;
+            }
+            tslot = (int)(task & 63u);
+            tpix = task >> 6;
             const Slot& S = slots[tslot];
             if (ttype == T_FREE) { // REF trace.cpp:189-230
                 if (tab.energy != S.E)
@@ -1024,6 +1030,7 @@ __global__ void __launch_bounds__(kBlock, XSD_MIN_BLOCKS) transport_kernel(const
             }
         }
         head += n_s;
+        head = head >= qlen ? head - qlen : head;
         fhead += n_f;
 
         // ------------------------------------------------ termination
@@ -1037,6 +1044,7 @@ __global__ void __launch_bounds__(kBlock, XSD_MIN_BLOCKS) transport_kernel(const
 
         // ------------------------------------------------ 3. walk in lockstep
         while (__ballot_sync(kFull, walking)) {
+            ++c_wit;
             if (walking) {
                 walking = walk_step<FMT, REG, SKIP>(P, tab, w);
                 ++w.steps;
@@ -1080,7 +1088,7 @@ __global__ void __launch_bounds__(kBlock, XSD_MIN_BLOCKS) transport_kernel(const
                 const bool hit = w.hit != 0;
                 if (hit)
                     ++c_int;
-                history_event<FMT>(P, B, slots, hdr, q, qmask, tslot, hit, hit ? hit_t(w) : 0.0, w.ix,
+                history_event<FMT>(P, B, slots, hdr, q, qlen, tslot, hit, hit ? hit_t(w) : 0.0, w.ix,
                                    w.iy, w.iz, var_base, st);
             }
         }
@@ -1095,6 +1103,8 @@ __global__ void __launch_bounds__(kBlock, XSD_MIN_BLOCKS) transport_kernel(const
     sadd(B.diag + 3, c_rays);
     sadd(B.diag + 4, c_int);
     sadd(B.diag + 5, c_iter);
+    if (lane == 0)
+        sadd(B.diag + 6, 32ull * c_wit);
     __syncthreads();
     for (int i = threadIdx.x; i < 8 * P.n_bins; i += blockDim.x)
         red_add(P.accum + P.off_bins + i, B.bins[i]);
@@ -1109,14 +1119,29 @@ static bool use_reg(const TransportParams& P) { return P.G.fmt == kFmtP4 && P.n_
 
 size_t transport_smem_bytes(const TransportParams& P)
 {
-    const size_t warp_bytes =
-        (size_t)P.slots_per_warp * sizeof(Slot) + sizeof(WarpHdr) + (size_t)(P.queue_len + kFreeQ) * 8;
+    const size_t warp_bytes = warp_bytes_of(P.slots_per_warp, P.queue_len);
     const int n_tab = P.G.fmt == kFmtP4 ? P.n_pal : P.n_mats;
     return (size_t)(8 * P.n_bins + 32) * 8 + (size_t)(P.n_bins + 1) * 8 + kWarps * warp_bytes +
            (use_reg(P) ? 0 : (size_t)n_tab * kBlock * 8);
 }
 
 int transport_block_size() { return kBlock; }
+
+// Live histories per warp: as many as fit a shared-memory budget per block
+// (the rest of the SM's 256 KB stays L1 for the stack frames and voxels).
+int transport_pick_slots(TransportParams& P, int max_slots, size_t budget)
+{
+    int H = max_slots < 64 ? max_slots : 64;
+    for (; H > 1; --H) {
+        P.slots_per_warp = H;
+        P.queue_len = H * P.splitting + 1;
+        if (transport_smem_bytes(P) <= budget)
+            break;
+    }
+    P.slots_per_warp = H;
+    P.queue_len = H * P.splitting + 1;
+    return H;
+}
 
 typedef void (*TransportFn)(const TransportParams);
 

@@ -110,7 +110,7 @@ struct TransportParams {
     unsigned long long* pool;
     int32_t grab;           // histories per warp grab
     int32_t slots_per_warp; // live histories per warp (<= 64)
-    int32_t queue_len;      // ray-task FIFO entries per warp (power of two)
+    int32_t queue_len;      // scoring FIFO entries per warp (H * splitting + 1)
 
     // variance scratch: var_cap entries per history slot
     uint32_t* var_pix;

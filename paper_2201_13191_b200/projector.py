@@ -102,7 +102,7 @@ class Context:
         A.check(st, self.h)
 
     def set_option(self, key: str, value: int):
-        """xs_ctx_set_option: "exact_walk", "queue_len", "max_slots", "grab"."""
+        """xs_ctx_set_option: "exact_walk", "smem_kb", "max_slots", "grab"."""
         self.check(A.lib().xs_ctx_set_option(self.h, key.encode(), int(value)))
 
     def set_stream(self, cuda_stream_ptr: int):
