@@ -379,17 +379,18 @@ __device__ __noinline__ bool walk_begin(const TransportParams& P, Walk& w, V3 o,
 // inside the cell along that axis; k + 1 means it also leaves the cell).
 __device__ __forceinline__ int cross_count(double tn, double dt, double rdt, double tm, int k, int s)
 {
-    if (s == 0 || tn > tm)
-        return 0;
-    if (k == 0)
-        return 1; // tn == tm: the plain Siddon crossing (REF trace.cpp:146-153)
-    int n = (int)((tm - tn) * rdt) + 1;
+    // Boundaries tn + j dt (j = 0..k) at or before tm.  Straight-line code
+    // (estimate, then both one-step corrections evaluated together) so the
+    // three axes overlap instead of running as three divergent branches.
+    // k == 0 gives 1 when tn == tm (the plain Siddon crossing, REF
+    // trace.cpp:146-153); axes without a crossing (s == 0 or tn > tm) give 0.
+    int n = __double2int_rz((tm - tn) * rdt) + 1;
     n = n > k + 1 ? k + 1 : n;
-    if (n > 1 && tn + (n - 1) * dt > tm)
-        --n;
-    else if (n <= k && tn + n * dt <= tm)
-        ++n;
-    return n;
+    n = n < 1 ? 1 : n;
+    const double lo = tn + (double)(n - 1) * dt; // boundary n-1 (must be <= tm)
+    const double hi = tn + (double)n * dt;       // boundary n (must be > tm)
+    n = lo > tm ? n - 1 : ((n <= k && hi <= tm) ? n + 1 : n);
+    return (s != 0 && tn <= tm) ? (n < 1 ? 1 : n) : 0;
 }
 
 // Re-establish the exact walker at ray parameter t (REF start_walk,
@@ -442,12 +443,15 @@ __device__ __forceinline__ bool walk_step(const TransportParams& P, const MuTab<
         // uniform and mixed cells do not diverge.
         const int c = code & ~G.ubit;
         const bool u = (code & G.ubit) != 0;
-        const int kx = u ? (w.sx > 0 ? 7 - (w.ix & 7) : (w.ix & 7)) : 0;
-        const int ky = u ? (w.sy > 0 ? 7 - (w.iy & 7) : (w.iy & 7)) : 0;
-        const int kz = u ? (w.sz > 0 ? 7 - (w.iz & 7) : (w.iz & 7)) : 0;
-        const double ex = kx ? w.tnx + kx * w.dtx : w.tnx;
-        const double ey = ky ? w.tny + ky * w.dty : w.tny;
-        const double ez = kz ? w.tnz + kz * w.dtz : w.tnz;
+        const int um = u ? 7 : 0; // k* = remaining in-cell boundaries, masked to 0 outside uniform cells
+        const int kx = (w.sx > 0 ? ~w.ix : w.ix) & um;
+        const int ky = (w.sy > 0 ? ~w.iy : w.iy) & um;
+        const int kz = (w.sz > 0 ? ~w.iz : w.iz) & um;
+        const double fx = w.tnx + (double)kx * w.dtx, fy = w.tny + (double)ky * w.dty,
+                     fz = w.tnz + (double)kz * w.dtz;
+        const double ex = kx ? fx : w.tnx;
+        const double ey = ky ? fy : w.tny;
+        const double ez = kz ? fz : w.tnz;
         double tm = ex;
         if (ey < tm)
             tm = ey;
