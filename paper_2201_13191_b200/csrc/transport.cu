@@ -377,6 +377,18 @@ __device__ __noinline__ bool walk_begin(const TransportParams& P, Walk& w, V3 o,
 // Boundaries tn + j*dt (j = 0..k) with tn + j*dt <= tm: how many an axis
 // crosses while the ray traverses a skipped macro cell (k = crossings left
 // inside the cell along that axis; k + 1 means it also leaves the cell).
+// Exact small-integer <-> double conversions on the fp64 pipe (fixed
+// latency) instead of I2F/F2I.F64 (variable-latency MIO unit): 2^52 has an
+// ulp of 1, so its bit pattern with k in the low word is 2^52 + k.
+__device__ __forceinline__ double u2d_small(uint32_t k) // exact for any u32
+{
+    return __hiloint2double(0x43300000, (int)k) - 4503599627370496.0;
+}
+__device__ __forceinline__ int d2i_trunc_small(double x) // trunc(x) for 0 <= x < 2^31
+{
+    return __double2loint(__dadd_rz(x, 4503599627370496.0));
+}
+
 __device__ __forceinline__ int cross_count(double tn, double dt, double rdt, double tm, int k, int s)
 {
     // Boundaries tn + j dt (j = 0..k) at or before tm.  Straight-line code
@@ -384,11 +396,11 @@ __device__ __forceinline__ int cross_count(double tn, double dt, double rdt, dou
     // three axes overlap instead of running as three divergent branches.
     // k == 0 gives 1 when tn == tm (the plain Siddon crossing, REF
     // trace.cpp:146-153); axes without a crossing (s == 0 or tn > tm) give 0.
-    int n = __double2int_rz((tm - tn) * rdt) + 1;
+    int n = d2i_trunc_small((tm - tn) * rdt) + 1; // tm >= tn whenever the result is used
     n = n > k + 1 ? k + 1 : n;
     n = n < 1 ? 1 : n;
-    const double lo = tn + (double)(n - 1) * dt; // boundary n-1 (must be <= tm)
-    const double hi = tn + (double)n * dt;       // boundary n (must be > tm)
+    const double lo = tn + u2d_small(n - 1) * dt; // boundary n-1 (must be <= tm)
+    const double hi = tn + u2d_small(n) * dt;     // boundary n (must be > tm)
     n = lo > tm ? n - 1 : ((n <= k && hi <= tm) ? n + 1 : n);
     return (s != 0 && tn <= tm) ? (n < 1 ? 1 : n) : 0;
 }
@@ -447,8 +459,8 @@ __device__ __forceinline__ bool walk_step(const TransportParams& P, const MuTab<
         const int kx = (w.sx > 0 ? ~w.ix : w.ix) & um;
         const int ky = (w.sy > 0 ? ~w.iy : w.iy) & um;
         const int kz = (w.sz > 0 ? ~w.iz : w.iz) & um;
-        const double fx = w.tnx + (double)kx * w.dtx, fy = w.tny + (double)ky * w.dty,
-                     fz = w.tnz + (double)kz * w.dtz;
+        const double fx = w.tnx + u2d_small(kx) * w.dtx, fy = w.tny + u2d_small(ky) * w.dty,
+                     fz = w.tnz + u2d_small(kz) * w.dtz;
         const double ex = kx ? fx : w.tnx;
         const double ey = ky ? fy : w.tny;
         const double ez = kz ? fz : w.tnz;
@@ -481,9 +493,9 @@ __device__ __forceinline__ bool walk_step(const TransportParams& P, const MuTab<
             prefetch<FMT>(G, nax + nay + naz, w.raw, w.shift, w.dens);
         w.depth = nd;
         w.t = tm;
-        w.tnx = nx ? w.tnx + nx * w.dtx : w.tnx;
-        w.tny = ny ? w.tny + ny * w.dty : w.tny;
-        w.tnz = nz ? w.tnz + nz * w.dtz : w.tnz;
+        w.tnx = nx ? w.tnx + u2d_small(nx) * w.dtx : w.tnx;
+        w.tny = ny ? w.tny + u2d_small(ny) * w.dty : w.tny;
+        w.tnz = nz ? w.tnz + u2d_small(nz) * w.dtz : w.tnz;
         if (u)
             w.skipped += (uint32_t)(nx + ny + nz) - 1u;
         w.ix = nix;
