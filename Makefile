@@ -9,7 +9,7 @@ OBJDIR   := $(PKG)/build
 ARCH     := -gencode arch=compute_100a,code=sm_100a
 # -fmad=false: every fp64 add/mul rounds like the reference's x86-64 build
 NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -fmad=false -Xcompiler -fPIC -Xptxas -v \
-            -ccbin $(CXX_HOST) -Iinclude
+            -ccbin $(CXX_HOST) -Iinclude $(NVEXTRA)
 CXXFLAGS := -O2 -std=c++17 -fPIC -ffp-contract=off -Iinclude
 
 CU_SRCS  := $(SRC)/capi.cu $(SRC)/transport.cu $(SRC)/primary.cu $(SRC)/postprocess.cu

@@ -838,11 +838,15 @@ int xs_upload_phantom(xs_context* c, const xs_phantom* ph)
         c->pin_dens.reserve(std::max<size_t>(dens_count, 1));
         encode_phantom(*ph, fmt, scan.pairs, c->pin_vox.p, c->pin_dens.p, G.nbx, G.nby, G.nbz);
 
-        // 8^3 macro cells: mark every voxel of a uniform cell with the
-        // palette's flag bit so the walker can cross the cell in one step
-        G.ubit = 0;
+        // Uniform cells: mark every voxel of a uniform 8^3 macro cell with
+        // u8bit, and every voxel of a uniform 4^3 brick elsewhere with u4bit,
+        // so the walker can cross the cell in one step
+        G.ubit = G.u8bit = G.u4bit = 0;
         if ((fmt == xsd::kFmtP4 && n_pairs <= 8) || (fmt == xsd::kFmtP8 && n_pairs <= 128)) {
-            G.ubit = fmt == xsd::kFmtP4 ? 8 : 128;
+            G.u8bit = fmt == xsd::kFmtP4 ? 8 : 128;
+            if ((fmt == xsd::kFmtP4 && n_pairs <= 4) || (fmt == xsd::kFmtP8 && n_pairs <= 64))
+                G.u4bit = fmt == xsd::kFmtP4 ? 4 : 64;
+            G.ubit = G.u8bit | G.u4bit;
             uint8_t* v = c->pin_vox.p;
             const size_t bb = fmt == xsd::kFmtP4 ? 32 : 64;
             auto brick_ptr = [&](int bx, int by, int bz) {
@@ -857,27 +861,39 @@ int xs_upload_phantom(xs_context* c, const xs_phantom* ph)
                     return (b[0] & 0xF) == (b[0] >> 4) ? (b[0] & 0xF) : -1;
                 return b[0];
             };
+            auto fill_brick = [&](int bx, int by, int bz, int f) {
+                const uint8_t byte = fmt == xsd::kFmtP4 ? (uint8_t)(f | (f << 4)) : (uint8_t)f;
+                std::memset(brick_ptr(bx, by, bz), byte, bb);
+            };
+            // only cells wholly inside the grid (partial edge cells hold padding voxels)
+            auto inside = [&](int x0, int y0, int z0, int n) {
+                return x0 + n <= G.nx && y0 + n <= G.ny && z0 + n <= G.nz;
+            };
             const int mnx = (G.nx + 7) / 8, mny = (G.ny + 7) / 8, mnz = (G.nz + 7) / 8;
             for (int mz = 0; mz < mnz; ++mz)
                 for (int my = 0; my < mny; ++my)
                     for (int mx = 0; mx < mnx; ++mx) {
                         int code = -2;
-                        for (int k = 0; k < 8 && code != -1; ++k) {
+                        int bc[8];
+                        for (int k = 0; k < 8; ++k) {
                             const int bx = 2 * mx + (k & 1), by = 2 * my + ((k >> 1) & 1), bz = 2 * mz + (k >> 2);
-                            if (bx >= G.nbx || by >= G.nby || bz >= G.nbz)
-                                continue;
-                            const int bc = brick_code(bx, by, bz);
-                            code = (bc < 0 || (code >= 0 && bc != code)) ? -1 : bc;
+                            bc[k] = (bx < G.nbx && by < G.nby && bz < G.nbz) ? brick_code(bx, by, bz) : -1;
+                            if (code != -1)
+                                code = (bc[k] < 0 || (code >= 0 && bc[k] != code)) ? -1 : bc[k];
                         }
-                        // only whole macro cells inside the grid (partial edge
-                        // cells hold padding voxels)
-                        if (code < 0 || 8 * mx + 8 > G.nx || 8 * my + 8 > G.ny || 8 * mz + 8 > G.nz)
+                        if (code >= 0 && inside(8 * mx, 8 * my, 8 * mz, 8)) {
+                            for (int k = 0; k < 8; ++k)
+                                fill_brick(2 * mx + (k & 1), 2 * my + ((k >> 1) & 1), 2 * mz + (k >> 2),
+                                           code | G.u8bit);
                             continue;
-                        const int f = code | G.ubit;
-                        const uint8_t byte = fmt == xsd::kFmtP4 ? (uint8_t)(f | (f << 4)) : (uint8_t)f;
-                        for (int k = 0; k < 8; ++k)
-                            std::memset(brick_ptr(2 * mx + (k & 1), 2 * my + ((k >> 1) & 1), 2 * mz + (k >> 2)),
-                                        byte, bb);
+                        }
+                        if (!G.u4bit)
+                            continue;
+                        for (int k = 0; k < 8; ++k) {
+                            const int bx = 2 * mx + (k & 1), by = 2 * my + ((k >> 1) & 1), bz = 2 * mz + (k >> 2);
+                            if (bc[k] >= 0 && inside(4 * bx, 4 * by, 4 * bz, 4))
+                                fill_brick(bx, by, bz, bc[k] | G.u4bit);
+                        }
                     }
         }
 

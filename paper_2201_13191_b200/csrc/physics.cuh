@@ -125,16 +125,59 @@ static __device__ double cumulative_mass(const TransportParams& P, const MatDesc
     return __ldg(cdf + lo) + segment_mass(k0, a, b, q - k0);
 }
 
+// REF's 64-step bisection, bit for bit: every probe evaluates exactly
+// cumulative_mass(mid).  The knot segment of mid lies between those of the
+// bracket ends, so the segment search is confined to that range (empty once
+// the bracket sits in one segment) and a segment's coefficients are loaded
+// (and its slope divided) only when the probe moves to another segment.
 static __device__ double invert_mass(const TransportParams& P, const MatDesc& m, double target, double q_hi)
 {
+    const double* knots = P.tabs + m.f.off;
+    const double* fv = knots + m.f.n;
+    const double* cdf = P.tabs + m.cdf_off;
+    const int n = m.f.n;
+    const double k_last = __ldg(knots + n - 1);
+    const double f_last = __ldg(fv + n - 1);
+    const double c_last = __ldg(cdf + n - 1);
+    int s_lo = 0, s_hi = n - 1; // segments of the bracket ends (n - 1: at/after the last knot)
+    int seg = -1;               // segment whose coefficients are loaded
+    double k0 = 0.0, a = 0.0, b = 0.0, c0 = 0.0;
     double lo = 0.0, hi = q_hi;
 #pragma unroll 1
     for (int it = 0; it < 64; ++it) {
         const double mid = 0.5 * (lo + hi);
-        if (cumulative_mass(P, m, mid) < target)
+        double cm;
+        int s_mid;
+        if (mid >= k_last) {
+            s_mid = n - 1;
+            cm = c_last + f_last * f_last * (mid * mid - k_last * k_last);
+        } else {
+            int l = s_lo, h = s_hi < n - 1 ? s_hi + 1 : n - 1; // knots[l] <= mid < knots[h]
+            while (h - l > 1) {
+                const int md = (l + h) >> 1;
+                if (__ldg(knots + md) <= mid)
+                    l = md;
+                else
+                    h = md;
+            }
+            s_mid = l;
+            if (l != seg) {
+                seg = l;
+                k0 = __ldg(knots + l);
+                const double k1 = __ldg(knots + l + 1);
+                a = __ldg(fv + l);
+                b = (__ldg(fv + l + 1) - a) / (k1 - k0);
+                c0 = __ldg(cdf + l);
+            }
+            cm = c0 + segment_mass(k0, a, b, mid - k0);
+        }
+        if (cm < target) {
             lo = mid;
-        else
+            s_lo = s_mid;
+        } else {
             hi = mid;
+            s_hi = s_mid;
+        }
     }
     return 0.5 * (lo + hi);
 }

@@ -449,13 +449,13 @@ __device__ __forceinline__ bool walk_step(const TransportParams& P, const MuTab<
     const int code = decode<FMT>(w.raw, w.shift);
     if (SKIP) {
         // One step = up to the next boundary crossing, or, in a uniform 8^3
-        // macro cell (code flag), up to the cell's exit: k* boundaries of
+        // macro cell or 4^3 brick (code flags), up to its exit: k* boundaries of
         // each axis remain inside the cell (0 outside uniform cells, where
         // this is exactly REF's voxel step).  Branch-free, so lanes in
         // uniform and mixed cells do not diverge.
         const int c = code & ~G.ubit;
-        const bool u = (code & G.ubit) != 0;
-        const int um = u ? 7 : 0; // k* = remaining in-cell boundaries, masked to 0 outside uniform cells
+        // k* = boundaries left inside the uniform 8^3 cell / 4^3 brick (0 outside)
+        const int um = (code & G.u8bit) ? 7 : ((code & G.u4bit) ? 3 : 0);
         const int kx = (w.sx > 0 ? ~w.ix : w.ix) & um;
         const int ky = (w.sy > 0 ? ~w.iy : w.iy) & um;
         const int kz = (w.sz > 0 ? ~w.iz : w.iz) & um;
@@ -496,7 +496,7 @@ __device__ __forceinline__ bool walk_step(const TransportParams& P, const MuTab<
         w.tnx = nx ? w.tnx + u2d_small(nx) * w.dtx : w.tnx;
         w.tny = ny ? w.tny + u2d_small(ny) * w.dty : w.tny;
         w.tnz = nz ? w.tnz + u2d_small(nz) * w.dtz : w.tnz;
-        if (u)
+        if (um)
             w.skipped += (uint32_t)(nx + ny + nz) - 1u;
         w.ix = nix;
         w.iy = niy;

@@ -35,10 +35,13 @@ struct Grid {
     const float* dens;    // raw densities, bricked (raw format only)
     int32_t fmt;
     int32_t n_codes;      // palette size (P4/P8)
-    // Palette codes carry this bit when the voxel's 8^3 macro cell is
-    // uniform (all voxels the same code): 8 for P4 (<= 8 entries), 128 for
-    // P8 (<= 128 entries), 0 when not encoded.
+    // Uniform-cell flags in the palette codes: u8bit when the voxel's 8^3
+    // macro cell is uniform (all voxels the same code), else u4bit when its
+    // 4^3 brick is.  P4: u8bit 8 (<= 8 entries), u4bit 4 (<= 4 entries);
+    // P8: 128 (<= 128) and 64 (<= 64); 0 when not encoded.  ubit = both.
     int32_t ubit;
+    int32_t u8bit, u4bit;
+    int32_t pad_;
 };
 
 // Device error record; code is an xs_status.
