@@ -151,8 +151,10 @@ typedef struct xs_launch_stats {
     uint64_t walk_lane_slots;  /* 32 x warp-level walker iterations (lane occupancy denominator) */
     uint32_t blocks_per_sm;    /* resident transport blocks per SM */
     uint32_t smem_per_block;   /* dynamic shared memory per transport block (bytes) */
-    uint32_t slots_per_warp;   /* live histories per warp */
-    uint32_t reserved;
+    uint32_t slots_per_warp;   /* live histories per warp (megakernel) */
+    uint32_t engine;           /* 0: persistent megakernel, 1: wavefront pipeline */
+    uint32_t waves;            /* wavefront: pipeline waves run */
+    uint32_t live_histories;   /* histories in flight at once */
 } xs_launch_stats;
 
 typedef struct xs_context xs_context;
@@ -338,7 +340,12 @@ int xs_ctx_synchronize(xs_context* ctx);
  *                 four blocks per SM keep 60 KB of L1); bounds the live
  *                 histories per warp
  *   "max_slots"   live histories per warp (1..64)
- *   "grab"        histories a warp reserves from the pool at a time        */
+ *   "grab"        histories a warp reserves from the pool at a time
+ *   "engine"      1 (default): wavefront pipeline (set-up / walk / event
+ *                 kernels over global queues); 0: persistent megakernel.
+ *                 Both give bit-identical results.  step_voxels > 1
+ *                 (REF's march mode) always runs the megakernel
+ *   "wave_slots"  histories in flight in the wavefront engine (2^20)       */
 int xs_ctx_set_option(xs_context* ctx, const char* key, int64_t value);
 
 /* Scene upload: REF passes the phantom and response by const& to every

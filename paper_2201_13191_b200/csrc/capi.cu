@@ -26,6 +26,11 @@ int transport_pick_slots(TransportParams& P, int max_slots, size_t budget);
 cudaError_t transport_prepare(const TransportParams& P, size_t smem, int* blocks_per_sm);
 cudaError_t launch_transport(const TransportParams& P, int grid, size_t smem, cudaStream_t s);
 cudaError_t launch_primary(const PrimaryParams& P, cudaStream_t s);
+struct WaveEngine;
+WaveEngine* wave_create();
+void wave_destroy(WaveEngine* e);
+cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint32_t n_slots, cudaStream_t s,
+                     WaveInfo* info);
 cudaError_t launch_finalize_image(const unsigned long long* acc, uint64_t off_image, uint64_t off_var,
                                   uint64_t npix, int log2_img, double n_hist, int track_var,
                                   double* image, double* var, cudaStream_t s);
@@ -176,6 +181,9 @@ struct xs_context {
 
     xs_launch_stats last{};
     int grab = 64;
+    int engine = 1;                  // 0: megakernel (transport.cu), 1: wavefront (wavefront.cu)
+    uint32_t wave_slots = 1u << 20;  // live histories of the wavefront engine
+    xsd::WaveEngine* wave = nullptr;
 };
 
 namespace {
@@ -540,6 +548,43 @@ void accumulate(xs_context* c, const xs_geometry& g, int angle, const xs_spectru
     P.grab = c->grab;
     P.status = c->status.p;
 
+    if (c->engine == 1 && cfg.step_voxels <= 1) { // wavefront engine (wavefront.cu)
+        uint32_t n_slots = c->wave_slots;
+        if (cfg.track_variance) {
+            const uint64_t cap = (uint64_t)cfg.splitting * (uint64_t)cfg.max_interactions;
+            if (cap > (1u << 20))
+                fail(XS_E_UNSUPPORTED, "xscat-gpu: splitting*max_interactions too large for variance tracking");
+            P.var_cap = (int32_t)cap;
+            // scratch per live history: keep it near 1 GB
+            n_slots = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(n_slots, (1ull << 30) / (12 * cap)));
+            const uint64_t n_use = std::min<uint64_t>(n_slots, h1 - h0);
+            c->var_pix.reserve(n_use * cap);
+            c->var_val.reserve(n_use * cap);
+            P.var_pix = c->var_pix.p;
+            P.var_val = c->var_val.p;
+        }
+        if (!c->wave)
+            c->wave = xsd::wave_create();
+        xsd::WaveInfo info{};
+        cuda_check(cudaEventRecord(c->ev0, s), "event");
+        cuda_check(xsd::wave_run(c->wave, P, c->sm_count, n_slots, s, &info), "wavefront transport");
+        cuda_check(cudaEventRecord(c->ev1, s), "event");
+        check_status(c, angle, &spec);
+        float ms = 0.f;
+        cuda_check(cudaEventElapsedTime(&ms, c->ev0, c->ev1), "event time");
+        c->last.kernel_ms = ms;
+        c->last.voxel_format = c->grid.fmt;
+        c->last.blocks_per_sm = (uint32_t)info.walk_blocks_per_sm;
+        c->last.smem_per_block = 0;
+        c->last.slots_per_warp = 0;
+        c->last.engine = 1;
+        c->last.waves = info.waves;
+        c->last.live_histories = info.n_slots;
+        c->last.palette_size = c->n_pal;
+        c->last.upload_bytes = c->last_upload_bytes;
+        return;
+    }
+
     // warp-queue geometry (transport.cu): H live histories per warp, sized
     // to the shared-memory budget
     if ((uint64_t)g.nu * (uint64_t)g.nv >= (1ull << 26))
@@ -580,6 +625,9 @@ void accumulate(xs_context* c, const xs_geometry& g, int angle, const xs_spectru
     c->last.blocks_per_sm = (uint32_t)per_sm;
     c->last.smem_per_block = (uint32_t)smem;
     c->last.slots_per_warp = (uint32_t)H;
+    c->last.engine = 0;
+    c->last.waves = 0;
+    c->last.live_histories = (uint32_t)((uint64_t)grid * (block / 32) * H);
     c->last.palette_size = c->n_pal;
     c->last.upload_bytes = c->last_upload_bytes;
 }
@@ -722,6 +770,10 @@ int xs_ctx_create(int32_t device, xs_context** out)
             c->macro_skip = std::atoi(e) != 0;
         if (const char* e = std::getenv("XSCAT_SLOTS"))
             c->max_slots = std::max(1, std::min(64, std::atoi(e)));
+        if (const char* e = std::getenv("XSCAT_ENGINE"))
+            c->engine = std::atoi(e) != 0;
+        if (const char* e = std::getenv("XSCAT_WAVE_SLOTS"))
+            c->wave_slots = (uint32_t)std::max(1, std::atoi(e));
         *out = c;
     });
 }
@@ -746,6 +798,7 @@ void xs_ctx_destroy(xs_context* c)
     c->status.release();
     c->var_pix.release();
     c->interp_tab.release();
+    xsd::wave_destroy(c->wave);
     if (c->ev0)
         cudaEventDestroy(c->ev0);
     if (c->ev1)
@@ -772,6 +825,10 @@ int xs_ctx_set_option(xs_context* c, const char* key, int64_t value)
             c->max_slots = (int)std::max<int64_t>(1, std::min<int64_t>(64, value));
         } else if (k == "grab") {
             c->grab = (int)std::max<int64_t>(1, value);
+        } else if (k == "engine") {
+            c->engine = value != 0;
+        } else if (k == "wave_slots") {
+            c->wave_slots = (uint32_t)std::max<int64_t>(1, std::min<int64_t>(1 << 24, value));
         } else {
             fail(XS_E_INVALID_ARGUMENT, "xs_ctx_set_option: unknown option '%s'", k.c_str());
         }

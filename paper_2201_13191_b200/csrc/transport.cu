@@ -61,7 +61,8 @@ struct WarpQ {
     }
     __device__ __forceinline__ uint32_t* q_() const { return reinterpret_cast<uint32_t*>(hdr_() + 1); }
     __device__ __forceinline__ Slot& slot(int s) const { return slots[s]; }
-    __device__ __forceinline__ void push_score(int s, uint32_t pixel) const
+    __device__ __forceinline__ uint32_t reserve_scores(int) const { return 0; }
+    __device__ __forceinline__ void push_score(uint32_t, int s, uint32_t pixel) const
     {
         const uint32_t i = atomicInc(&hdr_()->tail, qlen - 1u);
         q_()[i] = pixel << 6 | (uint32_t)s;

@@ -5,7 +5,8 @@
 // History state (Slot), the Philox stream, the mu tables, the Siddon walker
 // (REF trace.cpp) and REF's per-history event logic (REF transport.cpp:114-243)
 // live here.  The event logic is templated on a queue policy Q providing
-//   Slot& slot(s); push_score(s, pixel); push_free(s); claim(s); release(s); fence()
+//   Slot& slot(s); reserve_scores(n) -> base; push_score(base + k, s, pixel);
+//   push_free(s); claim(s); release(s); fence()
 // so both engines run the identical arithmetic per history.
 #pragma once
 #include <cmath>
@@ -645,13 +646,14 @@ __device__ __noinline__ void history_event(const TransportParams& P, const Block
         S.pref = kPi * r0 * r0 / sigma;
     }
     atomicAdd(&S.pending, P.splitting);
+    const uint32_t qbase = qs.reserve_scores(P.splitting);
 #pragma unroll 1
     for (int k = 0; k < P.splitting; ++k) { // REF :162-164 pixel draws
         int iu = (int)(slot_uniform(&S, P.k0, P.k1, P.angle) * P.nu);
         int iv = (int)(slot_uniform(&S, P.k0, P.k1, P.angle) * P.nv);
         iu = iu < P.nu - 1 ? iu : P.nu - 1;
         iv = iv < P.nv - 1 ? iv : P.nv - 1;
-        qs.push_score(s, (uint32_t)(iv * P.nu + iu));
+        qs.push_score(qbase + k, s, (uint32_t)(iv * P.nu + iu));
     }
     // continuation (REF :195-205)
     V3 ndir;

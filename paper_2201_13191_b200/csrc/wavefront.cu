@@ -1,0 +1,693 @@
+// wavefront.cu — the scatter transport as a pipeline of small kernels
+// (REF transport.cpp:114-324, same per-history arithmetic as transport.cu).
+//
+// The megakernel (transport.cu) runs set-up, walking and event logic in one
+// persistent kernel.  On B200 it is bound by instruction-cache misses: about
+// 40 KB of set-up code per ray against a 32 KB L1.5 I-cache.  It also idles
+// half its lanes, because a warp walks 32 rays until the longest ends
+// (profiles/r1_bench_kernel_ncu.md).  Here every stage is its own kernel over
+// a global queue, so each kernel's code stays resident and its warps are
+// coherent:
+//
+//   setup    one thread per queued task: scoring geometry + p(theta) + e_out
+//            (REF :166-183) or the free path's start; mu table; Siddon init.
+//            Writes a compact walker state (SoA, coalesced).
+//   walk     persistent; a lane that finishes a ray takes the next state from
+//            the queue (refills batched per warp), so lanes stay busy.  Only
+//            the Siddon loop is resident.
+//   complete one thread per finished ray: scoring tally (REF :178-193) or the
+//            history's event (REF :141-223), which pushes the next wave's
+//            scoring rays and free path.
+//   plan     one thread: admit new histories into released slots.
+//   admit    one thread per admitted history (REF :120-138).
+//
+// Per wave, each live history advances by one free path.  The scoring rays of
+// its last interaction ride in the same wave.  A history's slot is only
+// rewritten by `complete`, after `setup` has copied everything the wave's
+// rays need, so the interaction record needs no double buffering.  Tallies
+// are the same fixed-point integers as the megakernel's, so both engines give
+// bit-identical images and statistics.
+#include <algorithm>
+#include <cstring>
+
+#include "transport_core.cuh"
+
+namespace xsd {
+
+namespace {
+
+constexpr int kRefill = 8; // idle lanes that trigger a warp's refill in the walk kernel
+
+struct WaveQueue {
+    unsigned long long* score; // (slot << 32) | pixel
+    uint32_t* free;            // slot
+    uint32_t n_score, n_free;
+};
+
+struct WaveCtl {
+    WaveQueue q[2];
+    uint32_t* free_stack; // released slots, [0, free_top)
+    int32_t free_top;
+    uint32_t cursor;      // walk kernel work cursor
+    uint32_t n_rays, n_score;
+    uint32_t admit_n, live;
+    unsigned long long next_h, admit_base;
+    uint32_t waves, pad;
+};
+
+// Walker state between the set-up and walk kernels (structure of arrays over
+// the wave's rays, so a warp's loads and stores coalesce).
+struct WaveRays {
+    double *t, *texit, *target, *tn, *dt, *mu; // tn, dt: 3 planes; mu: n_mu planes
+    float* rd;                                 // 3 planes: 1/dt estimates
+    int* vox;                                  // 3 planes: ix, iy, iz
+    uint8_t* flags;                            // (sx+1) | (sy+1) << 2 | (sz+1) << 4 | walking << 6
+    double* pre;                               // scoring prefactor (set-up -> complete)
+    double* res;                               // depth (scoring) / t_hit (free path)
+    int* res_vox;                              // 3 planes: the free path's interaction voxel
+    uint8_t* res_hit;
+    uint32_t cap;
+    int32_t n_mu;
+};
+
+struct WaveArgs {
+    Slot* slots;
+    WaveCtl* ctl;
+    WaveRays R;
+    uint32_t n_slots;
+    int32_t cur; // queue consumed by this wave (the other one is filled)
+};
+
+// Queue policy of the wavefront engine (see transport_core.cuh).
+struct GlobalQ {
+    Slot* slots;
+    WaveCtl* ctl;
+    int out;
+    __device__ __forceinline__ Slot& slot(int s) const { return slots[s]; }
+    __device__ __forceinline__ uint32_t reserve_scores(int n) const
+    {
+        return atomicAdd(&ctl->q[out].n_score, (uint32_t)n); // one atomic per event, not per ray
+    }
+    __device__ __forceinline__ void push_score(uint32_t i, int s, uint32_t pixel) const
+    {
+        ctl->q[out].score[i] = ((unsigned long long)(uint32_t)s << 32) | pixel;
+    }
+    __device__ __forceinline__ void push_free(int s) const
+    {
+        WaveQueue& q = ctl->q[out];
+        const uint32_t i = atomicAdd(&q.n_free, 1u);
+        q.free[i] = (uint32_t)s;
+    }
+    __device__ __forceinline__ void claim(int) const {}
+    __device__ __forceinline__ void release(int s) const
+    {
+        const int i = atomicAdd(&ctl->free_top, 1);
+        ctl->free_stack[i] = (uint32_t)s;
+    }
+    __device__ __forceinline__ void fence() const { __threadfence(); }
+};
+
+__device__ __forceinline__ uint64_t var_base_of(const TransportParams& P, int s)
+{
+    return (uint64_t)s * (uint64_t)P.var_cap;
+}
+
+// Shared-memory statistics of a block (bins, ledger, diagnostics), flushed to
+// the global accumulator when the block ends.
+__device__ __forceinline__ Block block_stats(const TransportParams& P, unsigned long long* smem)
+{
+    Block B;
+    B.bins = smem;
+    B.ledger = B.bins + 8 * P.n_bins;
+    B.diag = B.ledger + 24;
+    for (int i = threadIdx.x; i < 8 * P.n_bins + 32; i += blockDim.x)
+        B.bins[i] = 0ull;
+    __syncthreads();
+    return B;
+}
+
+__device__ __forceinline__ void flush_stats(const TransportParams& P, const Block& B)
+{
+    __syncthreads();
+    for (int i = threadIdx.x; i < 8 * P.n_bins; i += blockDim.x)
+        if (B.bins[i])
+            red_add(P.accum + P.off_bins + i, B.bins[i]);
+    for (int i = threadIdx.x; i < 24; i += blockDim.x)
+        if (B.ledger[i])
+            red_add(P.accum + P.off_ledger + i, B.ledger[i]);
+    for (int i = threadIdx.x; i < 8; i += blockDim.x)
+        if (B.diag[i])
+            red_add(P.accum + P.off_diag + i, B.diag[i]);
+}
+
+template <int FMT, bool REG>
+__device__ __forceinline__ void store_mu(const WaveRays& R, uint32_t i, const MuTab<FMT, REG>& tab)
+{
+    if (REG) {
+        R.mu[i] = tab.t0;
+        R.mu[R.cap + i] = tab.t1;
+        R.mu[2ull * R.cap + i] = tab.t2;
+        R.mu[3ull * R.cap + i] = tab.t3;
+    } else {
+        for (int c = 0; c < R.n_mu; ++c)
+            R.mu[(uint64_t)c * R.cap + i] = tab.T[c * kBlock];
+    }
+}
+
+template <int FMT, bool REG>
+__device__ __forceinline__ void load_mu(const WaveRays& R, uint32_t i, MuTab<FMT, REG>& tab)
+{
+    if (REG) {
+        tab.t0 = R.mu[i];
+        tab.t1 = R.mu[R.cap + i];
+        tab.t2 = R.mu[2ull * R.cap + i];
+        tab.t3 = R.mu[3ull * R.cap + i];
+    } else {
+        for (int c = 0; c < R.n_mu; ++c)
+            tab.T[c * kBlock] = R.mu[(uint64_t)c * R.cap + i];
+    }
+}
+
+// ------------------------------------------------------------------ set-up
+template <int FMT, bool REG, bool SKIP>
+__global__ void __launch_bounds__(kBlock) wave_setup(const __grid_constant__ TransportParams P,
+                                                     const __grid_constant__ WaveArgs A)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    WaveCtl* ctl = A.ctl;
+    const WaveQueue& in = ctl->q[A.cur];
+    const uint32_t n_s = in.n_score, n = n_s + in.n_free;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        ctl->cursor = 0;
+        ctl->n_rays = n;
+        ctl->n_score = n_s;
+        ctl->q[A.cur ^ 1].n_score = 0;
+        ctl->q[A.cur ^ 1].n_free = 0;
+    }
+    MuTab<FMT, REG> tab;
+    tab.T = reinterpret_cast<double*>(smem) + threadIdx.x;
+    tab.energy = -1.0;
+    DevStatus* st = P.status;
+    const WaveRays& R = A.R;
+    uint32_t c_rays = 0;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        Walk w;
+        w.march = 0;
+        bool walking;
+        if (i < n_s) { // REF run_history :166-183
+            const unsigned long long task = in.score[i];
+            const Slot& S = A.slots[(uint32_t)(task >> 32)];
+            V3 o, to_det;
+            double e_out;
+            R.pre[i] = score_setup(P, S, (uint32_t)task, o, to_det, e_out, st);
+            if (tab.energy != e_out) // REF trace_attenuation builds MuField(e_out)
+                tab.fill(P, e_out, st, S.bin);
+            walking = walk_begin<FMT, SKIP>(P, w, o, to_det, CUDART_INF, false, st, S.bin);
+            ++c_rays;
+        } else { // REF trace.cpp:189-230
+            const Slot& S = A.slots[in.free[i - n_s]];
+            if (tab.energy != S.E)
+                tab.fill(P, S.E, st, S.bin);
+            walking = walk_begin<FMT, SKIP>(P, w, v3(S.px, S.py, S.pz), v3(S.dx, S.dy, S.dz), S.target,
+                                            false, st, S.bin);
+        }
+        if (!walking) { // misses the grid: zero depth, no interaction
+            R.flags[i] = 0;
+            R.res[i] = 0.0;
+            R.res_hit[i] = 0;
+            continue;
+        }
+        R.t[i] = w.t;
+        R.texit[i] = w.texit;
+        R.target[i] = w.target;
+        R.tn[i] = w.tnx;
+        R.tn[R.cap + i] = w.tny;
+        R.tn[2ull * R.cap + i] = w.tnz;
+        R.dt[i] = w.dtx;
+        R.dt[R.cap + i] = w.dty;
+        R.dt[2ull * R.cap + i] = w.dtz;
+        R.rd[i] = (float)w.rdx;
+        R.rd[R.cap + i] = (float)w.rdy;
+        R.rd[2ull * R.cap + i] = (float)w.rdz;
+        R.vox[i] = w.ix;
+        R.vox[R.cap + i] = w.iy;
+        R.vox[2ull * R.cap + i] = w.iz;
+        R.flags[i] = (uint8_t)((w.sx + 1) | ((w.sy + 1) << 2) | ((w.sz + 1) << 4) | 64);
+        store_mu(R, i, tab);
+    }
+    c_rays = __reduce_add_sync(kFull, c_rays);
+    if ((threadIdx.x & 31) == 0 && c_rays)
+        red_add(P.accum + P.off_diag + 3, c_rays);
+}
+
+// -------------------------------------------------------------------- walk
+template <int FMT, bool REG, bool SKIP>
+__global__ void __launch_bounds__(kBlock) wave_walk(const __grid_constant__ TransportParams P,
+                                                    const __grid_constant__ WaveArgs A)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    WaveCtl* ctl = A.ctl;
+    const WaveRays& R = A.R;
+    const uint32_t n = ctl->n_rays, n_s = ctl->n_score;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    const Grid& G = P.G;
+    MuTab<FMT, REG> tab;
+    tab.T = reinterpret_cast<double*>(smem) + threadIdx.x;
+    tab.energy = -1.0;
+    Walk w;
+    w.march = 0;
+    bool walking = false, drained = false;
+    uint32_t ray = 0;
+    uint32_t c_fp = 0, c_sc = 0, c_iter = 0, c_wit = 0;
+    for (;;) {
+        const unsigned idle = __ballot_sync(kFull, !walking);
+        if (!drained && (idle == kFull || __popc(idle) >= kRefill)) {
+            uint32_t base = 0;
+            if (lane == 0)
+                base = atomicAdd(&ctl->cursor, (uint32_t)__popc(idle));
+            base = __shfl_sync(kFull, base, 0);
+            drained = base + (uint32_t)__popc(idle) >= n;
+            if (!walking) {
+                const uint32_t r = base + (uint32_t)__popc(idle & lt_mask);
+                if (r < n) {
+                    const uint8_t f = R.flags[r];
+                    if (f & 64) {
+                        ray = r;
+                        w.t = R.t[r];
+                        w.texit = R.texit[r];
+                        w.target = R.target[r];
+                        w.tnx = R.tn[r];
+                        w.tny = R.tn[R.cap + r];
+                        w.tnz = R.tn[2ull * R.cap + r];
+                        w.dtx = R.dt[r];
+                        w.dty = R.dt[R.cap + r];
+                        w.dtz = R.dt[2ull * R.cap + r];
+                        w.rdx = R.rd[r];
+                        w.rdy = R.rd[R.cap + r];
+                        w.rdz = R.rd[2ull * R.cap + r];
+                        w.ix = R.vox[r];
+                        w.iy = R.vox[R.cap + r];
+                        w.iz = R.vox[2ull * R.cap + r];
+                        w.sx = (int)(f & 3) - 1;
+                        w.sy = (int)((f >> 2) & 3) - 1;
+                        w.sz = (int)((f >> 4) & 3) - 1;
+                        w.ax = term_x(G, w.ix);
+                        w.ay = term_y(G, w.iy);
+                        w.az = term_z(G, w.iz);
+                        prefetch<FMT>(G, w.ax + w.ay + w.az, w.raw, w.shift, w.dens);
+                        load_mu(R, r, tab);
+                        w.depth = 0.0;
+                        w.hit = 0;
+                        w.steps = 0;
+                        w.skipped = 0;
+                        walking = true;
+                    }
+                }
+            }
+        }
+        if (__ballot_sync(kFull, walking) == 0) {
+            if (drained)
+                break;
+            continue;
+        }
+        ++c_wit;
+        if (walking) {
+            walking = walk_step<FMT, REG, SKIP>(P, tab, w);
+            ++w.steps;
+            if (!walking) {
+                if (ray < n_s) {
+                    R.res[ray] = w.depth;
+                    c_sc += w.steps + w.skipped;
+                } else {
+                    const bool hit = w.hit != 0;
+                    R.res[ray] = hit ? hit_t(w) : 0.0;
+                    R.res_hit[ray] = hit ? 1 : 0;
+                    R.res_vox[ray] = w.ix;
+                    R.res_vox[R.cap + ray] = w.iy;
+                    R.res_vox[2ull * R.cap + ray] = w.iz;
+                    c_fp += w.steps + w.skipped;
+                }
+                c_iter += w.steps;
+            }
+        }
+    }
+    unsigned long long* diag = P.accum + P.off_diag;
+    c_fp = __reduce_add_sync(kFull, c_fp);
+    c_sc = __reduce_add_sync(kFull, c_sc);
+    c_iter = __reduce_add_sync(kFull, c_iter);
+    if (lane == 0) {
+        red_add(diag + 0, c_fp);
+        red_add(diag + 1, c_sc);
+        red_add(diag + 5, c_iter);
+        red_add(diag + 6, 32ull * c_wit);
+    }
+}
+
+// ---------------------------------------------------------------- complete
+template <int FMT>
+__global__ void __launch_bounds__(kBlock) wave_complete(const __grid_constant__ TransportParams P,
+                                                        const __grid_constant__ WaveArgs A)
+{
+    extern __shared__ __align__(16) unsigned long long acc[];
+    WaveCtl* ctl = A.ctl;
+    const WaveQueue& in = ctl->q[A.cur];
+    const uint32_t n = ctl->n_rays, n_s = ctl->n_score;
+    const Block B = block_stats(P, acc);
+    const GlobalQ qs{A.slots, ctl, A.cur ^ 1};
+    const WaveRays& R = A.R;
+    DevStatus* st = P.status;
+    uint32_t c_int = 0;
+    const int lane = threadIdx.x & 31;
+    const uint32_t n_warps = (gridDim.x * blockDim.x) >> 5;
+    // Warp-sized chunks: a history's scoring rays sit next to each other in
+    // the queue, so a warp folds its lanes' scores per slot (exact integer
+    // limb sums) and touches each slot's total and pending count once.
+    for (uint32_t base = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32u; base < n; base += n_warps * 32u) {
+        const uint32_t i = base + (uint32_t)lane;
+        const bool is_score = i < n_s;
+        if (__any_sync(kFull, is_score)) { // REF run_history :178-193
+            int s = -1;
+            uint64_t l0 = 0, l1 = 0, l2 = 0;
+            if (is_score) {
+                const unsigned long long task = in.score[i];
+                s = (int)(task >> 32);
+                const uint32_t pix = (uint32_t)task;
+                const double x = R.pre[i] * nl_exp(-R.res[i]);
+                if (!isfinite(x)) {
+                    raise(st, XS_E_RUNTIME, kErrNonFinite, A.slots[s].bin, A.slots[s].e_in, x);
+                } else if (!quantize(ldexp(x, -P.log2_img), l0, l1, l2)) {
+                    raise(st, XS_E_RUNTIME, kErrTallyOverflow, A.slots[s].bin, A.slots[s].e_in, x);
+                    l0 = l1 = l2 = 0;
+                } else {
+                    unsigned long long* img = P.accum + P.off_image + 4ull * pix;
+                    red_add(img + 0, l0);
+                    red_add(img + 1, l1);
+                    red_add(img + 2, l2);
+                }
+                if (P.track_var) {
+                    Slot& S = A.slots[s];
+                    const int k = atomicAdd(&S.n_var, 1);
+                    if (k < P.var_cap) {
+                        P.var_pix[var_base_of(P, s) + k] = pix;
+                        P.var_val[var_base_of(P, s) + k] = x;
+                    }
+                }
+            }
+            const unsigned grp = __match_any_sync(kFull, s);
+            // limbs are < 2^32: sum their 16-bit halves exactly in 32 bits
+            const uint32_t a0 = __reduce_add_sync(grp, (uint32_t)(l0 & 0xFFFFu));
+            const uint32_t b0 = __reduce_add_sync(grp, (uint32_t)(l0 >> 16));
+            const uint32_t a1 = __reduce_add_sync(grp, (uint32_t)(l1 & 0xFFFFu));
+            const uint32_t b1 = __reduce_add_sync(grp, (uint32_t)(l1 >> 16));
+            const uint32_t a2 = __reduce_add_sync(grp, (uint32_t)(l2 & 0xFFFFu));
+            const uint32_t b2 = __reduce_add_sync(grp, (uint32_t)(l2 >> 16));
+            if (is_score && lane == __ffs(grp) - 1) {
+                Slot& S = A.slots[s];
+                sadd(&S.T[0], ((uint64_t)b0 << 16) + a0);
+                sadd(&S.T[1], ((uint64_t)b1 << 16) + a1);
+                sadd(&S.T[2], ((uint64_t)b2 << 16) + a2);
+                __threadfence(); // the slot's tallies / scratch before the hand-off
+                const int cnt = __popc(grp);
+                if (atomicSub(&S.pending, cnt) == cnt)
+                    finalize_history(P, B, qs, s, var_base_of(P, s), st);
+            }
+        }
+        if (!is_score && i < n) {
+            const int s = (int)in.free[i - n_s];
+            const bool hit = R.res_hit[i] != 0;
+            c_int += hit;
+            history_event<FMT>(P, B, qs, s, hit, R.res[i], R.res_vox[i], R.res_vox[R.cap + i],
+                               R.res_vox[2ull * R.cap + i], var_base_of(P, s), st);
+        }
+    }
+    if (c_int)
+        atomicAdd(B.diag + 4, (unsigned long long)c_int);
+    flush_stats(P, B);
+}
+
+// ------------------------------------------------------------ admission
+__global__ void wave_plan(const __grid_constant__ TransportParams P, const __grid_constant__ WaveArgs A)
+{
+    WaveCtl* ctl = A.ctl;
+    const unsigned long long left = P.h_end - ctl->next_h;
+    const int32_t top = ctl->free_top;
+    const uint32_t k = (unsigned long long)top < left ? (uint32_t)top : (uint32_t)left;
+    ctl->admit_base = ctl->next_h;
+    ctl->admit_n = k;
+    ctl->free_top = top - (int32_t)k; // admitted slots: free_stack[top - k, top)
+    ctl->next_h += k;
+    ctl->live = A.n_slots - (uint32_t)ctl->free_top;
+    ++ctl->waves;
+}
+
+__global__ void __launch_bounds__(kBlock) wave_admit(const __grid_constant__ TransportParams P,
+                                                     const __grid_constant__ WaveArgs A)
+{
+    extern __shared__ __align__(16) unsigned long long acc[];
+    WaveCtl* ctl = A.ctl;
+    const uint32_t k = ctl->admit_n;
+    if (k == 0)
+        return;
+    const Block B = block_stats(P, acc);
+    const GlobalQ qs{A.slots, ctl, A.cur};
+    const int32_t top = ctl->free_top;
+    const unsigned long long base = ctl->admit_base;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < k; i += gridDim.x * blockDim.x) {
+        const int s = (int)ctl->free_stack[top + i];
+        history_start(P, B, qs, P.bin_start, s, base + i, P.status);
+    }
+    flush_stats(P, B);
+}
+
+__global__ void wave_init(WaveCtl* ctl, uint32_t* stack, uint32_t n_slots, unsigned long long h_begin)
+{
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_slots; i += gridDim.x * blockDim.x)
+        stack[i] = n_slots - 1 - i;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        ctl->free_top = (int32_t)n_slots;
+        ctl->next_h = h_begin;
+        ctl->q[0].n_score = ctl->q[0].n_free = 0;
+        ctl->q[1].n_score = ctl->q[1].n_free = 0;
+        ctl->waves = 0;
+        ctl->live = 0;
+    }
+}
+
+bool use_reg_w(const TransportParams& P) { return P.G.fmt == kFmtP4 && P.n_pal <= 4; }
+
+typedef void (*WaveFn)(const TransportParams, const WaveArgs);
+
+struct WaveSet {
+    WaveFn setup, walk, complete;
+};
+
+template <int FMT, bool REG, bool SKIP>
+WaveSet wave_set()
+{
+    return {wave_setup<FMT, REG, SKIP>, wave_walk<FMT, REG, SKIP>, wave_complete<FMT>};
+}
+
+WaveSet wave_kernels_for(const TransportParams& P)
+{
+    const bool skip = P.skip != 0 && P.G.ubit != 0;
+    if (P.G.fmt == kFmtP4) {
+        if (use_reg_w(P))
+            return skip ? wave_set<kFmtP4, true, true>() : wave_set<kFmtP4, true, false>();
+        return skip ? wave_set<kFmtP4, false, true>() : wave_set<kFmtP4, false, false>();
+    }
+    if (P.G.fmt == kFmtP8)
+        return skip ? wave_set<kFmtP8, false, true>() : wave_set<kFmtP8, false, false>();
+    return wave_set<kFmtRaw, false, false>();
+}
+
+template <class T>
+cudaError_t grow(T*& p, size_t& have, size_t need)
+{
+    if (have >= need)
+        return cudaSuccess;
+    if (p)
+        cudaFree(p);
+    p = nullptr;
+    have = 0;
+    cudaError_t e = cudaMalloc(&p, need * sizeof(T));
+    if (e == cudaSuccess)
+        have = need;
+    return e;
+}
+
+} // namespace
+
+// ------------------------------------------------------------------- host
+struct WaveEngine {
+    Slot* slots = nullptr;
+    size_t n_slots_have = 0;
+    uint32_t* stack = nullptr;
+    size_t stack_have = 0;
+    WaveCtl* ctl = nullptr;
+    size_t ctl_have = 0;
+    unsigned long long* sq[2] = {nullptr, nullptr};
+    size_t sq_have[2] = {0, 0};
+    uint32_t* fq[2] = {nullptr, nullptr};
+    size_t fq_have[2] = {0, 0};
+    double* dbl = nullptr; // t, texit, target, tn x3, dt x3, mu x n_mu, pre, res
+    size_t dbl_have = 0;
+    float* rd = nullptr;
+    size_t rd_have = 0;
+    int* vox = nullptr; // vox x3, res_vox x3
+    size_t vox_have = 0;
+    uint8_t* bytes = nullptr; // flags, res_hit
+    size_t bytes_have = 0;
+    WaveCtl* host_ctl = nullptr; // pinned
+};
+
+WaveEngine* wave_create() { return new WaveEngine(); }
+
+void wave_destroy(WaveEngine* e)
+{
+    if (!e)
+        return;
+    cudaFree(e->slots);
+    cudaFree(e->stack);
+    cudaFree(e->ctl);
+    for (int b = 0; b < 2; ++b) {
+        cudaFree(e->sq[b]);
+        cudaFree(e->fq[b]);
+    }
+    cudaFree(e->dbl);
+    cudaFree(e->rd);
+    cudaFree(e->vox);
+    cudaFree(e->bytes);
+    if (e->host_ctl)
+        cudaFreeHost(e->host_ctl);
+    delete e;
+}
+
+size_t wave_slot_bytes() { return sizeof(Slot); }
+
+cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint32_t n_slots,
+                     cudaStream_t s, WaveInfo* info)
+{
+#define XSW_CHECK(x)                                                                               \
+    do {                                                                                           \
+        cudaError_t err_ = (x);                                                                    \
+        if (err_ != cudaSuccess)                                                                   \
+            return err_;                                                                           \
+    } while (0)
+    const uint64_t n_hist = P.h_end - P.h_begin;
+    if (n_slots > n_hist)
+        n_slots = (uint32_t)n_hist;
+    if (n_slots < 1)
+        n_slots = 1;
+    const uint64_t split = (uint64_t)P.splitting;
+    const uint64_t cap = (uint64_t)n_slots * (split + 1);
+    if (cap >= (1ull << 32))
+        return cudaErrorInvalidValue;
+    const int n_mu = use_reg_w(P) ? 4 : 8;
+    XSW_CHECK(grow(e->slots, e->n_slots_have, n_slots));
+    XSW_CHECK(grow(e->stack, e->stack_have, n_slots));
+    XSW_CHECK(grow(e->ctl, e->ctl_have, 1));
+    for (int b = 0; b < 2; ++b) {
+        XSW_CHECK(grow(e->sq[b], e->sq_have[b], (size_t)n_slots * split));
+        XSW_CHECK(grow(e->fq[b], e->fq_have[b], (size_t)n_slots));
+    }
+    const size_t n_dbl = (size_t)(3 + 3 + 3 + n_mu + 2);
+    XSW_CHECK(grow(e->dbl, e->dbl_have, n_dbl * cap));
+    XSW_CHECK(grow(e->rd, e->rd_have, 3 * cap));
+    XSW_CHECK(grow(e->vox, e->vox_have, 6 * cap));
+    XSW_CHECK(grow(e->bytes, e->bytes_have, 2 * cap));
+    if (!e->host_ctl)
+        XSW_CHECK(cudaHostAlloc(&e->host_ctl, sizeof(WaveCtl), cudaHostAllocDefault));
+
+    WaveArgs A;
+    std::memset(&A, 0, sizeof A);
+    A.slots = e->slots;
+    A.ctl = e->ctl;
+    A.n_slots = n_slots;
+    WaveRays& R = A.R;
+    R.cap = (uint32_t)cap;
+    R.n_mu = n_mu;
+    double* d = e->dbl;
+    R.t = d;
+    R.texit = d + cap;
+    R.target = d + 2 * cap;
+    R.tn = d + 3 * cap;
+    R.dt = d + 6 * cap;
+    R.mu = d + 9 * cap;
+    R.pre = d + (9 + n_mu) * cap;
+    R.res = d + (10 + n_mu) * cap;
+    R.rd = e->rd;
+    R.vox = e->vox;
+    R.res_vox = e->vox + 3 * cap;
+    R.flags = e->bytes;
+    R.res_hit = e->bytes + cap;
+
+    WaveCtl init;
+    std::memset(&init, 0, sizeof init);
+    for (int b = 0; b < 2; ++b) {
+        init.q[b].score = e->sq[b];
+        init.q[b].free = e->fq[b];
+    }
+    init.free_stack = e->stack;
+    XSW_CHECK(cudaMemcpyAsync(e->ctl, &init, sizeof init, cudaMemcpyHostToDevice, s));
+    wave_init<<<sm_count, 256, 0, s>>>(e->ctl, e->stack, n_slots, P.h_begin);
+    XSW_CHECK(cudaGetLastError());
+
+    const WaveSet K = wave_kernels_for(P);
+    const size_t mu_smem = use_reg_w(P) ? 0 : (size_t)8 * kBlock * 8;
+    const size_t stat_smem = (size_t)(8 * P.n_bins + 32) * 8;
+    XSW_CHECK(cudaFuncSetAttribute((const void*)K.setup, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)std::max<size_t>(mu_smem, 1)));
+    XSW_CHECK(cudaFuncSetAttribute((const void*)K.walk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)std::max<size_t>(mu_smem, 1)));
+    XSW_CHECK(cudaFuncSetAttribute((const void*)K.complete, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)stat_smem));
+    XSW_CHECK(cudaFuncSetAttribute((const void*)wave_admit, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)stat_smem));
+    int walk_per_sm = 0;
+    XSW_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&walk_per_sm, K.walk, kBlock, mu_smem));
+    if (walk_per_sm < 1)
+        walk_per_sm = 1;
+    const int g_walk = sm_count * walk_per_sm;
+    const int g_work = sm_count * 8;
+
+    int cur = 0;
+    A.cur = 0;
+    wave_plan<<<1, 1, 0, s>>>(P, A);
+    wave_admit<<<g_work, kBlock, stat_smem, s>>>(P, A);
+    XSW_CHECK(cudaGetLastError());
+    const int check_every = 4;
+    uint32_t waves = 0;
+    for (;;) {
+        for (int k = 0; k < check_every; ++k) {
+            A.cur = cur;
+            K.setup<<<g_work, kBlock, mu_smem, s>>>(P, A);
+            K.walk<<<g_walk, kBlock, mu_smem, s>>>(P, A);
+            K.complete<<<g_work, kBlock, stat_smem, s>>>(P, A);
+            A.cur = cur ^ 1;
+            wave_plan<<<1, 1, 0, s>>>(P, A);
+            wave_admit<<<g_work, kBlock, stat_smem, s>>>(P, A);
+            cur ^= 1;
+            ++waves;
+        }
+        XSW_CHECK(cudaGetLastError());
+        XSW_CHECK(cudaMemcpyAsync(e->host_ctl, e->ctl, sizeof(WaveCtl), cudaMemcpyDeviceToHost, s));
+        DevStatus hs;
+        XSW_CHECK(cudaMemcpyAsync(&hs, P.status, sizeof hs, cudaMemcpyDeviceToHost, s));
+        XSW_CHECK(cudaStreamSynchronize(s));
+        if (hs.code != 0)
+            break;
+        const WaveCtl& h = *e->host_ctl;
+        if (h.live == 0 && h.next_h >= P.h_end && h.q[cur].n_score == 0 && h.q[cur].n_free == 0)
+            break;
+    }
+    if (info) {
+        info->waves = waves;
+        info->n_slots = n_slots;
+        info->walk_blocks_per_sm = walk_per_sm;
+    }
+    return cudaSuccess;
+#undef XSW_CHECK
+}
+
+} // namespace xsd

@@ -122,6 +122,13 @@ struct TransportParams {
     DevStatus* status;
 };
 
+// Wavefront engine run summary (wavefront.cu).
+struct WaveInfo {
+    uint32_t waves;
+    uint32_t n_slots;
+    int32_t walk_blocks_per_sm;
+};
+
 // Angular interpolation plan entry (REF postprocess.cpp:160-192).
 struct InterpEntry {
     int32_t lo, hi, exact;

@@ -1,0 +1,91 @@
+"""The two transport engines against each other and against the oracle on
+every device voxel format.
+
+The wavefront pipeline (wavefront.cu) and the persistent megakernel
+(transport.cu) run the same per-history arithmetic and the same fixed-point
+tallies, so their outputs must be bit-identical (image, variance, totals,
+ledger).  The phantoms cover the four encodings the upload chooses (4-bit
+palette with register mu table, 4-bit palette, 8-bit palette, raw id +
+density) plus both walk modes; each is also replayed against the oracle.
+"""
+import numpy as np
+import pytest
+
+import paper_2201_13191_b200 as X
+from paper_2201_13191_b200 import inputs as I
+from paper_2201_13191_b200 import synthetic as S
+
+from test_gpu_parity import _replay_compare
+
+pytestmark = pytest.mark.gpu
+
+
+def _phantom(kind):
+    water, iron = I.material("water"), I.material("iron")
+    if kind == "p4reg":  # water cube in vacuum: 2 palette entries
+        return S.make_cube_phantom(32, 0.2, 6.4, water, 1.0)
+    if kind == "p4":  # 5..8 (material, density) pairs
+        ph = S.make_rods_phantom(32, 10.0 / 32, 4.5, 8.0, water, 1.0, 4, 0.6, 3.0, iron, 7.874)
+        ph.density[(ph.material_id == 1) & (np.arange(ph.density.size) % 7 == 0)] = 1.05
+        ph.density[(ph.material_id == 1) & (np.arange(ph.density.size) % 11 == 0)] = 0.95
+        ph.density[(ph.material_id == 2) & (np.arange(ph.density.size) % 5 == 0)] = 7.5
+        return ph
+    rng = np.random.default_rng(5)
+    ph = S.make_rods_phantom(32, 10.0 / 32, 4.5, 8.0, water, 1.0, 4, 0.6, 3.0, iron, 7.874)
+    body = ph.material_id == 1
+    levels = 40 if kind == "p8" else 400  # distinct densities -> 8-bit palette / raw
+    ph.density[body] = 0.9 + 0.2 * rng.integers(0, levels, body.sum()) / levels
+    return ph
+
+
+def _format_of(stats):
+    return {0: "p4", 1: "p8", 2: "raw"}.get(stats["voxel_format"], stats["voxel_format"])
+
+
+@pytest.mark.parametrize("kind", ["p4reg", "p4", "p8", "raw"])
+@pytest.mark.parametrize("exact", [0, 1])
+def test_wavefront_equals_megakernel_bitwise(orc, kind, exact):
+    ph = _phantom(kind)
+    g = I.make_circular_geometry(100.0, 60.0, 32, 24, 0.8, 4)
+    spec, resp = I.kramers_spectrum(150.0), I.detector_response()
+    cfg = I.SimConfig(photons_total=20000, splitting=5, seed=31337, roulette_wmin_rel=2.0,
+                      roulette_survival=0.6, track_variance=True)
+    ctx = X.projector.Context(0)
+    ctx.set_option("exact_walk", exact)
+    proj = X.Projector(ph, resp, ctx=ctx)
+    out = {}
+    for engine in (0, 1):
+        ctx.set_option("engine", engine)
+        out[engine] = proj.scatter_stats(g, 1, spec, cfg)
+        assert out[engine].stats["engine"] == engine
+    a, b = out[0], out[1]
+    fmt = _format_of(b.stats)
+    want = {"p4reg": "p4", "p4": "p4", "p8": "p8", "raw": "raw"}[kind]
+    assert fmt == want, (kind, b.stats["voxel_format"], b.stats["palette_size"])
+    assert np.array_equal(a.image, b.image)
+    assert np.array_equal(a.variance, b.variance)
+    assert a.total == b.total and a.total_std_error == b.total_std_error
+    assert a.ledger == b.ledger and a.histories == b.histories
+    for k in ("free_path_steps", "scoring_steps", "histories", "scoring_rays", "interactions"):
+        assert a.stats[k] == b.stats[k], k
+    cpu = orc.simulate_scatter_stats(ph, g, 1, spec, resp, cfg)
+    _replay_compare(b, cpu)
+
+
+def test_wavefront_slot_count_does_not_change_results():
+    """Fewer histories in flight -> more waves, identical bits."""
+    ph = _phantom("p4")
+    g = I.make_circular_geometry(100.0, 60.0, 32, 24, 0.8, 4)
+    spec, resp = I.kramers_spectrum(150.0), I.detector_response()
+    cfg = I.SimConfig(photons_total=20000, splitting=5, seed=4, track_variance=True)
+    ctx = X.projector.Context(0)
+    ctx.set_option("engine", 1)
+    proj = X.Projector(ph, resp, ctx=ctx)
+    ref = proj.scatter_stats(g, 0, spec, cfg)
+    for slots in (3, 64, 1000):
+        ctx.set_option("wave_slots", slots)
+        r = proj.scatter_stats(g, 0, spec, cfg)
+        assert np.array_equal(ref.image, r.image), slots
+        assert np.array_equal(ref.variance, r.variance), slots
+        assert ref.total == r.total and ref.ledger == r.ledger, slots
+        assert r.stats["live_histories"] == slots
