@@ -30,7 +30,7 @@ struct WaveEngine;
 WaveEngine* wave_create();
 void wave_destroy(WaveEngine* e);
 cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint32_t n_slots, cudaStream_t s,
-                     WaveInfo* info);
+                     WaveInfo* info, cudaEvent_t start);
 cudaError_t launch_finalize_image(const unsigned long long* acc, uint64_t off_image, uint64_t off_var,
                                   uint64_t npix, int log2_img, double n_hist, int track_var,
                                   double* image, double* var, cudaStream_t s);
@@ -566,8 +566,7 @@ void accumulate(xs_context* c, const xs_geometry& g, int angle, const xs_spectru
         if (!c->wave)
             c->wave = xsd::wave_create();
         xsd::WaveInfo info{};
-        cuda_check(cudaEventRecord(c->ev0, s), "event");
-        cuda_check(xsd::wave_run(c->wave, P, c->sm_count, n_slots, s, &info), "wavefront transport");
+        cuda_check(xsd::wave_run(c->wave, P, c->sm_count, n_slots, s, &info, c->ev0), "wavefront transport");
         cuda_check(cudaEventRecord(c->ev1, s), "event");
         check_status(c, angle, &spec);
         float ms = 0.f;

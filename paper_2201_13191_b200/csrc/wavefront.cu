@@ -37,6 +37,9 @@ namespace xsd {
 namespace {
 
 constexpr int kRefill = 8; // idle lanes that trigger a warp's refill in the walk kernel
+#ifndef XSW_WALK_BLOCKS
+#define XSW_WALK_BLOCKS 6 // resident walk blocks per SM (<= 80 registers; 7-8 spill or slow the macro walk)
+#endif
 
 struct WaveQueue {
     unsigned long long* score; // (slot << 32) | pixel
@@ -52,7 +55,7 @@ struct WaveCtl {
     uint32_t n_rays, n_score;
     uint32_t admit_n, live;
     unsigned long long next_h, admit_base;
-    uint32_t waves, pad;
+    uint32_t waves, admit_q;
 };
 
 // Walker state between the set-up and walk kernels (structure of arrays over
@@ -78,15 +81,33 @@ struct WaveArgs {
     int32_t cur; // queue consumed by this wave (the other one is filled)
 };
 
+// Warp-aggregated atomicAdd: the converged lanes reserve their entries with
+// one atomic (a handful of queue counters take every push of the wave, so
+// per-lane atomics would serialise at L2).
+template <class T>
+__device__ __forceinline__ T warp_reserve(T* counter, T per_lane)
+{
+    const unsigned m = __activemask();
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(m) - 1;
+    const T rank = (T)__popc(m & ((1u << lane) - 1u));
+    T base = 0;
+    if (lane == leader)
+        base = atomicAdd(counter, per_lane * (T)__popc(m));
+    base = __shfl_sync(m, base, leader);
+    return base + rank * per_lane;
+}
+
 // Queue policy of the wavefront engine (see transport_core.cuh).
 struct GlobalQ {
     Slot* slots;
     WaveCtl* ctl;
     int out;
+    int free_at; // >= 0: this thread's free-path entry is pre-reserved (admission)
     __device__ __forceinline__ Slot& slot(int s) const { return slots[s]; }
     __device__ __forceinline__ uint32_t reserve_scores(int n) const
     {
-        return atomicAdd(&ctl->q[out].n_score, (uint32_t)n); // one atomic per event, not per ray
+        return warp_reserve(&ctl->q[out].n_score, (uint32_t)n);
     }
     __device__ __forceinline__ void push_score(uint32_t i, int s, uint32_t pixel) const
     {
@@ -95,13 +116,13 @@ struct GlobalQ {
     __device__ __forceinline__ void push_free(int s) const
     {
         WaveQueue& q = ctl->q[out];
-        const uint32_t i = atomicAdd(&q.n_free, 1u);
+        const uint32_t i = free_at >= 0 ? (uint32_t)free_at : warp_reserve(&q.n_free, 1u);
         q.free[i] = (uint32_t)s;
     }
     __device__ __forceinline__ void claim(int) const {}
     __device__ __forceinline__ void release(int s) const
     {
-        const int i = atomicAdd(&ctl->free_top, 1);
+        const int i = warp_reserve(&ctl->free_top, 1);
         ctl->free_stack[i] = (uint32_t)s;
     }
     __device__ __forceinline__ void fence() const { __threadfence(); }
@@ -242,7 +263,7 @@ __global__ void __launch_bounds__(kBlock) wave_setup(const __grid_constant__ Tra
 
 // -------------------------------------------------------------------- walk
 template <int FMT, bool REG, bool SKIP>
-__global__ void __launch_bounds__(kBlock) wave_walk(const __grid_constant__ TransportParams P,
+__global__ void __launch_bounds__(kBlock, XSW_WALK_BLOCKS) wave_walk(const __grid_constant__ TransportParams P,
                                                     const __grid_constant__ WaveArgs A)
 {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -354,7 +375,7 @@ __global__ void __launch_bounds__(kBlock) wave_complete(const __grid_constant__ 
     const WaveQueue& in = ctl->q[A.cur];
     const uint32_t n = ctl->n_rays, n_s = ctl->n_score;
     const Block B = block_stats(P, acc);
-    const GlobalQ qs{A.slots, ctl, A.cur ^ 1};
+    const GlobalQ qs{A.slots, ctl, A.cur ^ 1, -1};
     const WaveRays& R = A.R;
     DevStatus* st = P.status;
     uint32_t c_int = 0;
@@ -435,6 +456,8 @@ __global__ void wave_plan(const __grid_constant__ TransportParams P, const __gri
     const uint32_t k = (unsigned long long)top < left ? (uint32_t)top : (uint32_t)left;
     ctl->admit_base = ctl->next_h;
     ctl->admit_n = k;
+    ctl->admit_q = ctl->q[A.cur].n_free; // admitted histories' free paths follow the events'
+    ctl->q[A.cur].n_free += k;
     ctl->free_top = top - (int32_t)k; // admitted slots: free_stack[top - k, top)
     ctl->next_h += k;
     ctl->live = A.n_slots - (uint32_t)ctl->free_top;
@@ -450,11 +473,12 @@ __global__ void __launch_bounds__(kBlock) wave_admit(const __grid_constant__ Tra
     if (k == 0)
         return;
     const Block B = block_stats(P, acc);
-    const GlobalQ qs{A.slots, ctl, A.cur};
     const int32_t top = ctl->free_top;
     const unsigned long long base = ctl->admit_base;
+    const uint32_t qb = ctl->admit_q;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < k; i += gridDim.x * blockDim.x) {
         const int s = (int)ctl->free_stack[top + i];
+        const GlobalQ qs{A.slots, ctl, A.cur, (int)(qb + i)};
         history_start(P, B, qs, P.bin_start, s, base + i, P.status);
     }
     flush_stats(P, B);
@@ -566,7 +590,7 @@ void wave_destroy(WaveEngine* e)
 size_t wave_slot_bytes() { return sizeof(Slot); }
 
 cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint32_t n_slots,
-                     cudaStream_t s, WaveInfo* info)
+                     cudaStream_t s, WaveInfo* info, cudaEvent_t start)
 {
 #define XSW_CHECK(x)                                                                               \
     do {                                                                                           \
@@ -622,6 +646,8 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
     R.flags = e->bytes;
     R.res_hit = e->bytes + cap;
 
+    if (start) // buffers are allocated: the timed region starts here
+        XSW_CHECK(cudaEventRecord(start, s));
     WaveCtl init;
     std::memset(&init, 0, sizeof init);
     for (int b = 0; b < 2; ++b) {
