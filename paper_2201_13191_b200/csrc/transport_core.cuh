@@ -24,6 +24,12 @@ enum : int { T_NONE = -1, T_FREE = 0, T_SCORE = 1 };
 enum : int { K_PE = 0, K_COMPTON = 1, K_RAYLEIGH = 2 };
 
 // ------------------------------------------------------------ smem layout
+// A history's Philox stream (REF rng.hpp:11-67): counter {block, photon, bin,
+// angle}, the current 4-word block and the read position in it.
+struct SlotRng {
+    uint32_t photon, bin, block, pos, b0, b1, b2, b3;
+};
+
 struct __align__(8) Slot {
     double px, py, pz, dx, dy, dz; // photon position (= last interaction point) / direction
     double E, W, wmin, target;     // energy, weight, roulette floor, -ln u of the pending free path
@@ -31,19 +37,20 @@ struct __align__(8) Slot {
     double e_in, w_split;          // energy at it, weight per pseudo-particle
     double pref;                   // pi r0^2 / sigma(E) of its kind (REF cross_sections.cpp:56-79)
     unsigned long long T[3];       // history total, fixed-point limbs (unit U_img)
-    uint32_t r_photon, r_bin, r_block, r_pos, r_b0, r_b1, r_b2, r_b3; // Philox stream
+    SlotRng rng;                   // Philox stream
     int32_t bin, gen, kind, mat;
     int32_t pending;               // queued/in-flight scoring rays + 1 while alive
     int32_t n_var;                 // variance scratch entries
 };
 
-// One out-of-line Philox draw on a history's stream kept in its slot (REF
-// rng.hpp:29-60).  A single copy of the 10-round refill instead of one per
-// call site keeps the event code small (instruction-cache bound kernel).
-__device__ __noinline__ double slot_uniform(Slot* s, uint32_t k0, uint32_t k1, uint32_t angle)
+// One out-of-line Philox draw on a history's stream (REF rng.hpp:29-60).  The
+// event code works on a local copy of the slot's stream (one load and one
+// store per event instead of a slot round trip per draw); a single copy of
+// the 10-round refill keeps the event code small.
+__device__ __noinline__ double slot_uniform(SlotRng* s, uint32_t k0, uint32_t k1, uint32_t angle)
 {
-    if (s->r_pos == 4) {
-        uint32_t c0 = s->r_block, c1 = s->r_photon, c2 = s->r_bin, c3 = angle;
+    if (s->pos == 4) {
+        uint32_t c0 = s->block, c1 = s->photon, c2 = s->bin, c3 = angle;
 #pragma unroll
         for (int i = 0; i < 10; ++i) {
             const uint32_t lo0 = 0xD2511F53u * c0, hi0 = __umulhi(0xD2511F53u, c0);
@@ -55,22 +62,22 @@ __device__ __noinline__ double slot_uniform(Slot* s, uint32_t k0, uint32_t k1, u
             k0 += 0x9E3779B9u;
             k1 += 0xBB67AE85u;
         }
-        s->r_b0 = c0;
-        s->r_b1 = c1;
-        s->r_b2 = c2;
-        s->r_b3 = c3;
-        s->r_pos = 0;
-        ++s->r_block;
+        s->b0 = c0;
+        s->b1 = c1;
+        s->b2 = c2;
+        s->b3 = c3;
+        s->pos = 0;
+        ++s->block;
     }
     uint64_t hi, lo;
-    if (s->r_pos == 0) {
-        hi = s->r_b0;
-        lo = s->r_b1;
+    if (s->pos == 0) {
+        hi = s->b0;
+        lo = s->b1;
     } else {
-        hi = s->r_b2;
-        lo = s->r_b3;
+        hi = s->b2;
+        lo = s->b3;
     }
-    s->r_pos += 2;
+    s->pos += 2;
     const uint64_t bits = ((hi << 32) | lo) >> 11;
     return ((double)bits + 0.5) * 0x1p-53;
 }
@@ -606,6 +613,7 @@ __device__ __noinline__ void history_event(const TransportParams& P, const Block
         end_history(P, B, qs, s, var_base, st);
         return;
     }
+    SlotRng rng = S.rng;
     const V3 dir = v3(S.dx, S.dy, S.dz);
     const V3 pos = v3(S.px, S.py, S.pz) + dir * t_hit;
     int code;
@@ -621,7 +629,7 @@ __device__ __noinline__ void history_event(const TransportParams& P, const Block
     const double total = pe + incoh + coh;
     if (!(total > 0.0))
         raise(st, XS_E_RUNTIME, kErrSigmaAll, bin, E, (double)mat);
-    const double u = slot_uniform(&S, P.k0, P.k1, P.angle) * total;
+    const double u = slot_uniform(&rng, P.k0, P.k1, P.angle) * total;
     const int kind = u < pe ? K_PE : (u < pe + incoh ? K_COMPTON : K_RAYLEIGH);
     if (kind == K_PE) {
         ledger_add(P, B, 2, W, st, bin);
@@ -649,8 +657,8 @@ __device__ __noinline__ void history_event(const TransportParams& P, const Block
     const uint32_t qbase = qs.reserve_scores(P.splitting);
 #pragma unroll 1
     for (int k = 0; k < P.splitting; ++k) { // REF :162-164 pixel draws
-        int iu = (int)(slot_uniform(&S, P.k0, P.k1, P.angle) * P.nu);
-        int iv = (int)(slot_uniform(&S, P.k0, P.k1, P.angle) * P.nv);
+        int iu = (int)(slot_uniform(&rng, P.k0, P.k1, P.angle) * P.nu);
+        int iv = (int)(slot_uniform(&rng, P.k0, P.k1, P.angle) * P.nv);
         iu = iu < P.nu - 1 ? iu : P.nu - 1;
         iv = iv < P.nv - 1 ? iv : P.nv - 1;
         qs.push_score(qbase + k, s, (uint32_t)(iv * P.nu + iu));
@@ -670,9 +678,9 @@ __device__ __noinline__ void history_event(const TransportParams& P, const Block
                 const double t = 1.0 + 2.0 * alpha; // kahn_sample_cos_theta, samplers.cpp:12-30
                 double cos_th;
                 for (;;) {
-                    const double r1 = slot_uniform(&S, P.k0, P.k1, P.angle);
-                    const double r2 = slot_uniform(&S, P.k0, P.k1, P.angle);
-                    const double r3 = slot_uniform(&S, P.k0, P.k1, P.angle);
+                    const double r1 = slot_uniform(&rng, P.k0, P.k1, P.angle);
+                    const double r2 = slot_uniform(&rng, P.k0, P.k1, P.angle);
+                    const double r3 = slot_uniform(&rng, P.k0, P.k1, P.angle);
                     if (r1 <= t / (t + 8.0)) {
                         const double x = 1.0 + 2.0 * alpha * r2;
                         if (r3 <= 4.0 * (1.0 / x - 1.0 / (x * x))) {
@@ -691,9 +699,9 @@ __device__ __noinline__ void history_event(const TransportParams& P, const Block
                 const double cc = cos_th < -1.0 ? -1.0 : (1.0 < cos_th ? 1.0 : cos_th);
                 theta = nl_acos(cc);
                 const double sv = form_S(P, md, momentum_transfer(E, theta));
-                if (slot_uniform(&S, P.k0, P.k1, P.angle) * s_max <= sv) {
+                if (slot_uniform(&rng, P.k0, P.k1, P.angle) * s_max <= sv) {
                     ap = alpha / (1.0 + alpha * (1.0 - nl_cos(theta)));
-                    phi = 2.0 * kPi * slot_uniform(&S, P.k0, P.k1, P.angle);
+                    phi = 2.0 * kPi * slot_uniform(&rng, P.k0, P.k1, P.angle);
                     break;
                 }
             }
@@ -709,13 +717,13 @@ __device__ __noinline__ void history_event(const TransportParams& P, const Block
         } else {
             const double scale = kHc / E;
             for (;;) {
-                const double qq = invert_mass(P, md, slot_uniform(&S, P.k0, P.k1, P.angle) * tot, q_max);
+                const double qq = invert_mass(P, md, slot_uniform(&rng, P.k0, P.k1, P.angle) * tot, q_max);
                 const double sh = 1.0 < qq * scale ? 1.0 : qq * scale;
                 const double cos_th = 1.0 - 2.0 * sh * sh;
-                if (slot_uniform(&S, P.k0, P.k1, P.angle) * 2.0 <= 1.0 + cos_th * cos_th) {
+                if (slot_uniform(&rng, P.k0, P.k1, P.angle) * 2.0 <= 1.0 + cos_th * cos_th) {
                     const double cc = cos_th < -1.0 ? -1.0 : (1.0 < cos_th ? 1.0 : cos_th);
                     theta = nl_acos(cc);
-                    phi = 2.0 * kPi * slot_uniform(&S, P.k0, P.k1, P.angle);
+                    phi = 2.0 * kPi * slot_uniform(&rng, P.k0, P.k1, P.angle);
                     break;
                 }
             }
@@ -733,7 +741,7 @@ __device__ __noinline__ void history_event(const TransportParams& P, const Block
         ledger_add(P, B, 3, W, st, bin);
         alive = false;
     } else if (S.wmin > 0.0 && W < S.wmin) { // REF :213-222
-        if (slot_uniform(&S, P.k0, P.k1, P.angle) < P.survival) {
+        if (slot_uniform(&rng, P.k0, P.k1, P.angle) < P.survival) {
             const double boosted = W / P.survival;
             ledger_add(P, B, 5, boosted - W, st, bin);
             Wn = boosted;
@@ -744,7 +752,8 @@ __device__ __noinline__ void history_event(const TransportParams& P, const Block
     }
     if (alive) {
         S.W = Wn;
-        S.target = -nl_log(slot_uniform(&S, P.k0, P.k1, P.angle));
+        S.target = -nl_log(slot_uniform(&rng, P.k0, P.k1, P.angle));
+        S.rng = rng;
         qs.push_free(s);
     } else {
         end_history(P, B, qs, s, var_base, st);
@@ -766,12 +775,13 @@ __device__ __noinline__ void history_start(const TransportParams& P, const Block
             hi = mid;
     }
     const int bin = lo;
-    S.r_photon = (uint32_t)(h - sstart[lo]);
-    S.r_bin = (uint32_t)lo;
-    S.r_block = 0;
-    S.r_pos = 4;
-    const double u1 = slot_uniform(&S, P.k0, P.k1, P.angle);
-    const double u2 = slot_uniform(&S, P.k0, P.k1, P.angle);
+    SlotRng rng;
+    rng.photon = (uint32_t)(h - sstart[lo]);
+    rng.bin = (uint32_t)lo;
+    rng.block = 0;
+    rng.pos = 4;
+    const double u1 = slot_uniform(&rng, P.k0, P.k1, P.angle);
+    const double u2 = slot_uniform(&rng, P.k0, P.k1, P.angle);
     const double xu = (u1 - 0.5) * P.nu * P.pitch;
     const double xv = (u2 - 0.5) * P.nv * P.pitch;
     const V3 c = v3(P.center[0], P.center[1], P.center[2]);
@@ -799,7 +809,8 @@ __device__ __noinline__ void history_start(const TransportParams& P, const Block
     S.pending = 1;
     S.n_var = 0;
     ledger_add(P, B, 0, w0, st, bin);
-    S.target = -nl_log(slot_uniform(&S, P.k0, P.k1, P.angle));
+    S.target = -nl_log(slot_uniform(&rng, P.k0, P.k1, P.angle));
+    S.rng = rng;
     qs.push_free(s);
     qs.claim(s);
 }

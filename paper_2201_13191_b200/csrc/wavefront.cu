@@ -675,7 +675,7 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
     if (walk_per_sm < 1)
         walk_per_sm = 1;
     const int g_walk = sm_count * walk_per_sm;
-    const int g_work = sm_count * 8;
+    const int g_work = sm_count * 4;
 
     int cur = 0;
     A.cur = 0;
