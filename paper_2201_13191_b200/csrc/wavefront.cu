@@ -366,9 +366,81 @@ __global__ void __launch_bounds__(kBlock, XSW_WALK_BLOCKS) wave_walk(const __gri
 }
 
 // ---------------------------------------------------------------- complete
+// Scoring rays (REF run_history :178-193).  Warp-sized chunks: a history's
+// scoring rays sit next to each other in the queue, so a warp folds its
+// lanes' scores per slot (exact integer limb sums) and touches each slot's
+// total and pending count once.
+__global__ void __launch_bounds__(kBlock) wave_score(const __grid_constant__ TransportParams P,
+                                                     const __grid_constant__ WaveArgs A)
+{
+    extern __shared__ __align__(16) unsigned long long acc[];
+    WaveCtl* ctl = A.ctl;
+    const WaveQueue& in = ctl->q[A.cur];
+    const uint32_t n_s = ctl->n_score;
+    const Block B = block_stats(P, acc);
+    const GlobalQ qs{A.slots, ctl, A.cur ^ 1, -1};
+    const WaveRays& R = A.R;
+    DevStatus* st = P.status;
+    const int lane = threadIdx.x & 31;
+    const uint32_t n_warps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t base = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32u; base < n_s;
+         base += n_warps * 32u) {
+        const uint32_t i = base + (uint32_t)lane;
+        const bool is_score = i < n_s;
+        int s = -1;
+        uint64_t l0 = 0, l1 = 0, l2 = 0;
+        if (is_score) {
+            const unsigned long long task = in.score[i];
+            s = (int)(task >> 32);
+            const uint32_t pix = (uint32_t)task;
+            const double x = R.pre[i] * nl_exp(-R.res[i]);
+            if (!isfinite(x)) {
+                raise(st, XS_E_RUNTIME, kErrNonFinite, A.slots[s].bin, A.slots[s].e_in, x);
+            } else if (!quantize(ldexp(x, -P.log2_img), l0, l1, l2)) {
+                raise(st, XS_E_RUNTIME, kErrTallyOverflow, A.slots[s].bin, A.slots[s].e_in, x);
+                l0 = l1 = l2 = 0;
+            } else {
+                unsigned long long* img = P.accum + P.off_image + 4ull * pix;
+                red_add(img + 0, l0);
+                red_add(img + 1, l1);
+                red_add(img + 2, l2);
+            }
+            if (P.track_var) {
+                Slot& S = A.slots[s];
+                const int k = atomicAdd(&S.n_var, 1);
+                if (k < P.var_cap) {
+                    P.var_pix[var_base_of(P, s) + k] = pix;
+                    P.var_val[var_base_of(P, s) + k] = x;
+                }
+            }
+        }
+        const unsigned grp = __match_any_sync(kFull, s);
+        // limbs are < 2^32: sum their 16-bit halves exactly in 32 bits
+        const uint32_t a0 = __reduce_add_sync(grp, (uint32_t)(l0 & 0xFFFFu));
+        const uint32_t b0 = __reduce_add_sync(grp, (uint32_t)(l0 >> 16));
+        const uint32_t a1 = __reduce_add_sync(grp, (uint32_t)(l1 & 0xFFFFu));
+        const uint32_t b1 = __reduce_add_sync(grp, (uint32_t)(l1 >> 16));
+        const uint32_t a2 = __reduce_add_sync(grp, (uint32_t)(l2 & 0xFFFFu));
+        const uint32_t b2 = __reduce_add_sync(grp, (uint32_t)(l2 >> 16));
+        if (is_score && lane == __ffs(grp) - 1) {
+            Slot& S = A.slots[s];
+            sadd(&S.T[0], ((uint64_t)b0 << 16) + a0);
+            sadd(&S.T[1], ((uint64_t)b1 << 16) + a1);
+            sadd(&S.T[2], ((uint64_t)b2 << 16) + a2);
+            __threadfence(); // the slot's tallies / scratch before the hand-off
+            const int cnt = __popc(grp);
+            if (atomicSub(&S.pending, cnt) == cnt)
+                finalize_history(P, B, qs, s, var_base_of(P, s), st);
+        }
+    }
+    flush_stats(P, B);
+}
+
+// Free paths: the history's event (REF run_history :141-223), which pushes
+// the next wave's scoring rays and free path.
 template <int FMT>
-__global__ void __launch_bounds__(kBlock) wave_complete(const __grid_constant__ TransportParams P,
-                                                        const __grid_constant__ WaveArgs A)
+__global__ void __launch_bounds__(kBlock) wave_event(const __grid_constant__ TransportParams P,
+                                                     const __grid_constant__ WaveArgs A)
 {
     extern __shared__ __align__(16) unsigned long long acc[];
     WaveCtl* ctl = A.ctl;
@@ -377,70 +449,13 @@ __global__ void __launch_bounds__(kBlock) wave_complete(const __grid_constant__ 
     const Block B = block_stats(P, acc);
     const GlobalQ qs{A.slots, ctl, A.cur ^ 1, -1};
     const WaveRays& R = A.R;
-    DevStatus* st = P.status;
     uint32_t c_int = 0;
-    const int lane = threadIdx.x & 31;
-    const uint32_t n_warps = (gridDim.x * blockDim.x) >> 5;
-    // Warp-sized chunks: a history's scoring rays sit next to each other in
-    // the queue, so a warp folds its lanes' scores per slot (exact integer
-    // limb sums) and touches each slot's total and pending count once.
-    for (uint32_t base = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32u; base < n; base += n_warps * 32u) {
-        const uint32_t i = base + (uint32_t)lane;
-        const bool is_score = i < n_s;
-        if (__any_sync(kFull, is_score)) { // REF run_history :178-193
-            int s = -1;
-            uint64_t l0 = 0, l1 = 0, l2 = 0;
-            if (is_score) {
-                const unsigned long long task = in.score[i];
-                s = (int)(task >> 32);
-                const uint32_t pix = (uint32_t)task;
-                const double x = R.pre[i] * nl_exp(-R.res[i]);
-                if (!isfinite(x)) {
-                    raise(st, XS_E_RUNTIME, kErrNonFinite, A.slots[s].bin, A.slots[s].e_in, x);
-                } else if (!quantize(ldexp(x, -P.log2_img), l0, l1, l2)) {
-                    raise(st, XS_E_RUNTIME, kErrTallyOverflow, A.slots[s].bin, A.slots[s].e_in, x);
-                    l0 = l1 = l2 = 0;
-                } else {
-                    unsigned long long* img = P.accum + P.off_image + 4ull * pix;
-                    red_add(img + 0, l0);
-                    red_add(img + 1, l1);
-                    red_add(img + 2, l2);
-                }
-                if (P.track_var) {
-                    Slot& S = A.slots[s];
-                    const int k = atomicAdd(&S.n_var, 1);
-                    if (k < P.var_cap) {
-                        P.var_pix[var_base_of(P, s) + k] = pix;
-                        P.var_val[var_base_of(P, s) + k] = x;
-                    }
-                }
-            }
-            const unsigned grp = __match_any_sync(kFull, s);
-            // limbs are < 2^32: sum their 16-bit halves exactly in 32 bits
-            const uint32_t a0 = __reduce_add_sync(grp, (uint32_t)(l0 & 0xFFFFu));
-            const uint32_t b0 = __reduce_add_sync(grp, (uint32_t)(l0 >> 16));
-            const uint32_t a1 = __reduce_add_sync(grp, (uint32_t)(l1 & 0xFFFFu));
-            const uint32_t b1 = __reduce_add_sync(grp, (uint32_t)(l1 >> 16));
-            const uint32_t a2 = __reduce_add_sync(grp, (uint32_t)(l2 & 0xFFFFu));
-            const uint32_t b2 = __reduce_add_sync(grp, (uint32_t)(l2 >> 16));
-            if (is_score && lane == __ffs(grp) - 1) {
-                Slot& S = A.slots[s];
-                sadd(&S.T[0], ((uint64_t)b0 << 16) + a0);
-                sadd(&S.T[1], ((uint64_t)b1 << 16) + a1);
-                sadd(&S.T[2], ((uint64_t)b2 << 16) + a2);
-                __threadfence(); // the slot's tallies / scratch before the hand-off
-                const int cnt = __popc(grp);
-                if (atomicSub(&S.pending, cnt) == cnt)
-                    finalize_history(P, B, qs, s, var_base_of(P, s), st);
-            }
-        }
-        if (!is_score && i < n) {
-            const int s = (int)in.free[i - n_s];
-            const bool hit = R.res_hit[i] != 0;
-            c_int += hit;
-            history_event<FMT>(P, B, qs, s, hit, R.res[i], R.res_vox[i], R.res_vox[R.cap + i],
-                               R.res_vox[2ull * R.cap + i], var_base_of(P, s), st);
-        }
+    for (uint32_t i = n_s + blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int s = (int)in.free[i - n_s];
+        const bool hit = R.res_hit[i] != 0;
+        c_int += hit;
+        history_event<FMT>(P, B, qs, s, hit, R.res[i], R.res_vox[i], R.res_vox[R.cap + i],
+                           R.res_vox[2ull * R.cap + i], var_base_of(P, s), P.status);
     }
     if (c_int)
         atomicAdd(B.diag + 4, (unsigned long long)c_int);
@@ -503,13 +518,13 @@ bool use_reg_w(const TransportParams& P) { return P.G.fmt == kFmtP4 && P.n_pal <
 typedef void (*WaveFn)(const TransportParams, const WaveArgs);
 
 struct WaveSet {
-    WaveFn setup, walk, complete;
+    WaveFn setup, walk, event;
 };
 
 template <int FMT, bool REG, bool SKIP>
 WaveSet wave_set()
 {
-    return {wave_setup<FMT, REG, SKIP>, wave_walk<FMT, REG, SKIP>, wave_complete<FMT>};
+    return {wave_setup<FMT, REG, SKIP>, wave_walk<FMT, REG, SKIP>, wave_event<FMT>};
 }
 
 WaveSet wave_kernels_for(const TransportParams& P)
@@ -666,7 +681,9 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
                                    (int)std::max<size_t>(mu_smem, 1)));
     XSW_CHECK(cudaFuncSetAttribute((const void*)K.walk, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)std::max<size_t>(mu_smem, 1)));
-    XSW_CHECK(cudaFuncSetAttribute((const void*)K.complete, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    XSW_CHECK(cudaFuncSetAttribute((const void*)K.event, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)stat_smem));
+    XSW_CHECK(cudaFuncSetAttribute((const void*)wave_score, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)stat_smem));
     XSW_CHECK(cudaFuncSetAttribute((const void*)wave_admit, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)stat_smem));
@@ -675,7 +692,9 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
     if (walk_per_sm < 1)
         walk_per_sm = 1;
     const int g_walk = sm_count * walk_per_sm;
-    const int g_work = sm_count * 4;
+    const int g_work = sm_count * 4;  // admission / events (~120 registers)
+    const int g_setup = sm_count * 8; // <= 64 registers
+    const int g_score = sm_count * 8;
 
     int cur = 0;
     A.cur = 0;
@@ -687,9 +706,10 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
     for (;;) {
         for (int k = 0; k < check_every; ++k) {
             A.cur = cur;
-            K.setup<<<g_work, kBlock, mu_smem, s>>>(P, A);
+            K.setup<<<g_setup, kBlock, mu_smem, s>>>(P, A);
             K.walk<<<g_walk, kBlock, mu_smem, s>>>(P, A);
-            K.complete<<<g_work, kBlock, stat_smem, s>>>(P, A);
+            wave_score<<<g_score, kBlock, stat_smem, s>>>(P, A);
+            K.event<<<g_work, kBlock, stat_smem, s>>>(P, A);
             A.cur = cur ^ 1;
             wave_plan<<<1, 1, 0, s>>>(P, A);
             wave_admit<<<g_work, kBlock, stat_smem, s>>>(P, A);
