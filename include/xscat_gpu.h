@@ -155,6 +155,7 @@ typedef struct xs_launch_stats {
     uint32_t engine;           /* 0: persistent megakernel, 1: wavefront pipeline */
     uint32_t waves;            /* wavefront: pipeline waves run */
     uint32_t live_histories;   /* histories in flight at once */
+    uint64_t uniform_iterations; /* walker iterations that crossed a uniform cell / brick */
 } xs_launch_stats;
 
 typedef struct xs_context xs_context;

@@ -182,6 +182,8 @@ struct xs_context {
     xs_launch_stats last{};
     int grab = 64;
     int engine = 1;                  // 0: megakernel (transport.cu), 1: wavefront (wavefront.cu)
+    std::vector<int> lvl_edges2{4, 8, 32}; // uniform-block edges with two level bits (C3 sweep: best of 7 sets)
+    int lvl_edge1 = 8;                      // ... with one level bit
     uint32_t wave_slots = 1u << 20;  // live histories of the wavefront engine
     xsd::WaveEngine* wave = nullptr;
 };
@@ -422,6 +424,90 @@ void encode_phantom(const xs_phantom& ph, int fmt, const std::vector<PairKey>& p
         t.join();
 }
 
+// Level marking for uniform blocks (see Grid::lvl_masks).  Bottom-up
+// uniformity over aligned blocks of each edge in `edges` (ascending powers of
+// two >= 4), then every brick of a uniform block (largest level first) is
+// rewritten with code | level << lvl_shift.
+void mark_uniform_blocks(const xsd::Grid& G, int fmt, uint8_t* vox, const std::vector<int>& edges)
+{
+    const size_t bb = fmt == xsd::kFmtP4 ? 32 : 64;
+    const int nbx = G.nbx, nby = G.nby, nbz = G.nbz;
+    auto brick_ptr = [&](size_t bx, size_t by, size_t bz) {
+        return vox + (bx + (size_t)nbx * (by + (size_t)nby * bz)) * bb;
+    };
+    // uniform code of every brick (4^3, wholly inside the grid) or -1
+    std::vector<int16_t> cur((size_t)nbx * nby * nbz);
+    for (int bz = 0; bz < nbz; ++bz)
+        for (int by = 0; by < nby; ++by)
+            for (int bx = 0; bx < nbx; ++bx) {
+                const uint8_t* b = brick_ptr(bx, by, bz);
+                int code = -1;
+                if (4 * bx + 4 <= G.nx && 4 * by + 4 <= G.ny && 4 * bz + 4 <= G.nz) {
+                    bool same = true;
+                    for (size_t i = 1; i < bb && same; ++i)
+                        same = b[i] == b[0];
+                    if (same)
+                        code = fmt == xsd::kFmtP4 ? ((b[0] & 0xF) == (b[0] >> 4) ? (b[0] & 0xF) : -1) : b[0];
+                }
+                cur[bx + (size_t)nbx * (by + (size_t)nby * bz)] = (int16_t)code;
+            }
+    // per level: uniform code of each aligned block of that edge (in bricks)
+    std::vector<std::vector<int16_t>> lv(edges.size());
+    std::vector<int> nb(edges.size() * 3);
+    int prev_edge = 4;
+    std::vector<int16_t> prev = cur;
+    int pnx = nbx, pny = nby, pnz = nbz;
+    for (size_t l = 0; l < edges.size(); ++l) {
+        const int f = edges[l] / prev_edge; // children per axis
+        const int qx = (pnx + f - 1) / f, qy = (pny + f - 1) / f, qz = (pnz + f - 1) / f;
+        std::vector<int16_t> nxt((size_t)qx * qy * qz, (int16_t)-1);
+        for (int z = 0; z < qz; ++z)
+            for (int y = 0; y < qy; ++y)
+                for (int x = 0; x < qx; ++x) {
+                    int code = -2;
+                    for (int k = 0; k < f * f * f && code != -1; ++k) {
+                        const int cx = x * f + k % f, cy = y * f + (k / f) % f, cz = z * f + k / (f * f);
+                        const int cc = (cx < pnx && cy < pny && cz < pnz)
+                                           ? prev[cx + (size_t)pnx * (cy + (size_t)pny * cz)]
+                                           : -1;
+                        code = (cc < 0 || (code >= 0 && cc != code)) ? -1 : cc;
+                    }
+                    nxt[x + (size_t)qx * (y + (size_t)qy * z)] = (int16_t)(code < 0 ? -1 : code);
+                }
+        if (f == 1)
+            nxt = prev;
+        lv[l] = nxt;
+        nb[3 * l] = qx;
+        nb[3 * l + 1] = qy;
+        nb[3 * l + 2] = qz;
+        prev = nxt;
+        pnx = qx;
+        pny = qy;
+        pnz = qz;
+        prev_edge = edges[l];
+    }
+    // rewrite bricks: each brick takes the largest uniform level containing it
+    for (int bz = 0; bz < nbz; ++bz)
+        for (int by = 0; by < nby; ++by)
+            for (int bx = 0; bx < nbx; ++bx) {
+                int level = 0, code = -1;
+                for (int l = (int)edges.size() - 1; l >= 0 && level == 0; --l) {
+                    const int e = edges[l] / 4; // edge in bricks
+                    const int x = bx / e, y = by / e, z = bz / e;
+                    const int cc = lv[l][x + (size_t)nb[3 * l] * (y + (size_t)nb[3 * l + 1] * z)];
+                    if (cc >= 0) {
+                        level = l + 1;
+                        code = cc;
+                    }
+                }
+                if (!level)
+                    continue;
+                const int f = code | (level << G.lvl_shift);
+                const uint8_t byte = fmt == xsd::kFmtP4 ? (uint8_t)(f | (f << 4)) : (uint8_t)f;
+                std::memset(brick_ptr(bx, by, bz), byte, bb);
+            }
+}
+
 // --------------------------------------------------------- scatter launch
 struct Plan {
     std::vector<uint64_t> counts, start;
@@ -656,6 +742,7 @@ void finalize(xs_context* c, const xs_geometry& g, const xs_spectrum& spec, cons
     c->last.interactions = diag[4];
     c->last.walk_iterations = diag[5];
     c->last.walk_lane_slots = diag[6];
+    c->last.uniform_iterations = diag[7];
 
     double* img = d_image;
     if (!img) {
@@ -769,6 +856,20 @@ int xs_ctx_create(int32_t device, xs_context** out)
             c->macro_skip = std::atoi(e) != 0;
         if (const char* e = std::getenv("XSCAT_SLOTS"))
             c->max_slots = std::max(1, std::min(64, std::atoi(e)));
+        if (const char* e = std::getenv("XSCAT_LEVELS")) { // e.g. "4,16,64"
+            std::vector<int> v;
+            for (const char* q = e; *q;) {
+                const int x = std::atoi(q);
+                if (x >= 4 && x <= 128 && (x & (x - 1)) == 0)
+                    v.push_back(x);
+                while (*q && *q != ',')
+                    ++q;
+                if (*q == ',')
+                    ++q;
+            }
+            if (!v.empty() && v.size() <= 3)
+                c->lvl_edges2 = v;
+        }
         if (const char* e = std::getenv("XSCAT_ENGINE"))
             c->engine = std::atoi(e) != 0;
         if (const char* e = std::getenv("XSCAT_WAVE_SLOTS"))
@@ -894,63 +995,29 @@ int xs_upload_phantom(xs_context* c, const xs_phantom* ph)
         c->pin_dens.reserve(std::max<size_t>(dens_count, 1));
         encode_phantom(*ph, fmt, scan.pairs, c->pin_vox.p, c->pin_dens.p, G.nbx, G.nby, G.nbz);
 
-        // Uniform cells: mark every voxel of a uniform 8^3 macro cell with
-        // u8bit, and every voxel of a uniform 4^3 brick elsewhere with u4bit,
-        // so the walker can cross the cell in one step
-        G.ubit = G.u8bit = G.u4bit = 0;
-        if ((fmt == xsd::kFmtP4 && n_pairs <= 8) || (fmt == xsd::kFmtP8 && n_pairs <= 128)) {
-            G.u8bit = fmt == xsd::kFmtP4 ? 8 : 128;
+        // Uniform blocks: every voxel of an aligned uniform block (all voxels
+        // the same code, wholly inside the grid) carries the level of the
+        // largest such block holding it, so the walker crosses the block in
+        // one step.  Block edges: 4 (a brick) and up, powers of two.
+        G.ubit = 0;
+        G.lvl_shift = 0;
+        G.lvl_masks = 0;
+        {
+            int lvl_bits = 0;
             if ((fmt == xsd::kFmtP4 && n_pairs <= 4) || (fmt == xsd::kFmtP8 && n_pairs <= 64))
-                G.u4bit = fmt == xsd::kFmtP4 ? 4 : 64;
-            G.ubit = G.u8bit | G.u4bit;
-            uint8_t* v = c->pin_vox.p;
-            const size_t bb = fmt == xsd::kFmtP4 ? 32 : 64;
-            auto brick_ptr = [&](int bx, int by, int bz) {
-                return v + ((size_t)bx + (size_t)G.nbx * ((size_t)by + (size_t)G.nby * bz)) * bb;
-            };
-            auto brick_code = [&](int bx, int by, int bz) -> int { // uniform code or -1
-                const uint8_t* b = brick_ptr(bx, by, bz);
-                for (size_t i = 1; i < bb; ++i)
-                    if (b[i] != b[0])
-                        return -1;
-                if (fmt == xsd::kFmtP4)
-                    return (b[0] & 0xF) == (b[0] >> 4) ? (b[0] & 0xF) : -1;
-                return b[0];
-            };
-            auto fill_brick = [&](int bx, int by, int bz, int f) {
-                const uint8_t byte = fmt == xsd::kFmtP4 ? (uint8_t)(f | (f << 4)) : (uint8_t)f;
-                std::memset(brick_ptr(bx, by, bz), byte, bb);
-            };
-            // only cells wholly inside the grid (partial edge cells hold padding voxels)
-            auto inside = [&](int x0, int y0, int z0, int n) {
-                return x0 + n <= G.nx && y0 + n <= G.ny && z0 + n <= G.nz;
-            };
-            const int mnx = (G.nx + 7) / 8, mny = (G.ny + 7) / 8, mnz = (G.nz + 7) / 8;
-            for (int mz = 0; mz < mnz; ++mz)
-                for (int my = 0; my < mny; ++my)
-                    for (int mx = 0; mx < mnx; ++mx) {
-                        int code = -2;
-                        int bc[8];
-                        for (int k = 0; k < 8; ++k) {
-                            const int bx = 2 * mx + (k & 1), by = 2 * my + ((k >> 1) & 1), bz = 2 * mz + (k >> 2);
-                            bc[k] = (bx < G.nbx && by < G.nby && bz < G.nbz) ? brick_code(bx, by, bz) : -1;
-                            if (code != -1)
-                                code = (bc[k] < 0 || (code >= 0 && bc[k] != code)) ? -1 : bc[k];
-                        }
-                        if (code >= 0 && inside(8 * mx, 8 * my, 8 * mz, 8)) {
-                            for (int k = 0; k < 8; ++k)
-                                fill_brick(2 * mx + (k & 1), 2 * my + ((k >> 1) & 1), 2 * mz + (k >> 2),
-                                           code | G.u8bit);
-                            continue;
-                        }
-                        if (!G.u4bit)
-                            continue;
-                        for (int k = 0; k < 8; ++k) {
-                            const int bx = 2 * mx + (k & 1), by = 2 * my + ((k >> 1) & 1), bz = 2 * mz + (k >> 2);
-                            if (bc[k] >= 0 && inside(4 * bx, 4 * by, 4 * bz, 4))
-                                fill_brick(bx, by, bz, bc[k] | G.u4bit);
-                        }
-                    }
+                lvl_bits = 2;
+            else if ((fmt == xsd::kFmtP4 && n_pairs <= 8) || (fmt == xsd::kFmtP8 && n_pairs <= 128))
+                lvl_bits = 1;
+            std::vector<int> edges = lvl_bits == 2 ? c->lvl_edges2 : std::vector<int>{c->lvl_edge1};
+            if (lvl_bits == 0)
+                edges.clear();
+            const int code_bits = fmt == xsd::kFmtP4 ? 4 - lvl_bits : 8 - lvl_bits;
+            G.lvl_shift = code_bits;
+            G.ubit = lvl_bits ? (((1 << lvl_bits) - 1) << code_bits) : 0;
+            for (size_t l = 0; l < edges.size(); ++l)
+                G.lvl_masks |= (uint32_t)(edges[l] - 1) << (8 * (l + 1));
+            if (!edges.empty())
+                mark_uniform_blocks(G, fmt, c->pin_vox.p, edges);
         }
 
         c->n_pal = fmt == xsd::kFmtRaw ? 0 : n_pairs;

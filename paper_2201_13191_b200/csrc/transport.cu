@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(kBlock, XSD_MIN_BLOCKS) transport_kernel(const
     uint32_t head = 0, fhead = 0;     // warp-uniform FIFO heads
     uint64_t wq_next = 0, wq_end = 0; // warp-uniform history reservation
     bool pool_empty = false;
-    uint32_t c_fp = 0, c_sc = 0, c_rays = 0, c_int = 0, c_iter = 0, c_wit = 0;
+    uint32_t c_fp = 0, c_sc = 0, c_rays = 0, c_int = 0, c_iter = 0, c_wit = 0, c_uni = 0;
 
     // Each iteration: admit histories, set up one ray per lane from the FIFO,
     // walk until every lane's ray has ended, process the 32 completions.
@@ -193,6 +193,7 @@ __global__ void __launch_bounds__(kBlock, XSD_MIN_BLOCKS) transport_kernel(const
         w.hit = 0;
         w.steps = 0;
         w.skipped = 0;
+        w.ucells = 0;
         w.depth = 0.0;
         if ((uint32_t)lane < n_s + n_f) {
             uint32_t task;
@@ -251,6 +252,7 @@ __global__ void __launch_bounds__(kBlock, XSD_MIN_BLOCKS) transport_kernel(const
             else
                 c_sc += w.steps + w.skipped;
             c_iter += w.steps;
+            c_uni += w.ucells;
             const uint64_t var_base = (gwarp * H + tslot) * (uint64_t)P.var_cap;
             if (ttype == T_SCORE) { // REF run_history :178-193
                 score_complete(P, B, qs, tslot, tpix, tpre, w.depth, var_base, st);
@@ -273,6 +275,7 @@ __global__ void __launch_bounds__(kBlock, XSD_MIN_BLOCKS) transport_kernel(const
     sadd(B.diag + 3, c_rays);
     sadd(B.diag + 4, c_int);
     sadd(B.diag + 5, c_iter);
+    sadd(B.diag + 7, c_uni);
     if (lane == 0)
         sadd(B.diag + 6, 32ull * c_wit);
     __syncthreads();

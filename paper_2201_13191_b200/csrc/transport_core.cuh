@@ -272,6 +272,7 @@ struct Walk {
     int hit;
     uint32_t skipped;     // voxel visits integrated inside skipped macro cells
     uint32_t steps;       // loop iterations of this walk
+    uint32_t ucells;      // ... of which crossed a uniform cell / brick
 };
 
 
@@ -292,6 +293,7 @@ __device__ __noinline__ bool walk_begin(const TransportParams& P, Walk& w, V3 o,
     w.depth = 0.0;
     w.steps = 0;
     w.skipped = 0;
+    w.ucells = 0;
     if (!clip_to_grid<FAST>(P.G, o, d, t0, t1, bad)) {
         if (bad)
             raise(st, XS_E_INVALID_ARGUMENT, 0, bin, 0.0, 0.0);
@@ -378,14 +380,14 @@ __device__ __forceinline__ bool walk_step(const TransportParams& P, const MuTab<
     }
     const int code = decode<FMT>(w.raw, w.shift);
     if (SKIP) {
-        // One step = up to the next boundary crossing, or, in a uniform 8^3
-        // macro cell or 4^3 brick (code flags), up to its exit: k* boundaries of
+        // One step = up to the next boundary crossing, or, in an aligned
+        // uniform block (level field of the code), up to its exit: k* boundaries of
         // each axis remain inside the cell (0 outside uniform cells, where
         // this is exactly REF's voxel step).  Branch-free, so lanes in
         // uniform and mixed cells do not diverge.
         const int c = code & ~G.ubit;
-        // k* = boundaries left inside the uniform 8^3 cell / 4^3 brick (0 outside)
-        const int um = (code & G.u8bit) ? 7 : ((code & G.u4bit) ? 3 : 0);
+        // k* = boundaries left inside the voxel's uniform block (0 outside)
+        const int um = (int)((G.lvl_masks >> (((uint32_t)code >> G.lvl_shift) << 3)) & 0xFFu);
         const int kx = (w.sx > 0 ? ~w.ix : w.ix) & um;
         const int ky = (w.sy > 0 ? ~w.iy : w.iy) & um;
         const int kz = (w.sz > 0 ? ~w.iz : w.iz) & um;
@@ -426,8 +428,10 @@ __device__ __forceinline__ bool walk_step(const TransportParams& P, const MuTab<
         w.tnx = nx ? w.tnx + u2d_small(nx) * w.dtx : w.tnx;
         w.tny = ny ? w.tny + u2d_small(ny) * w.dty : w.tny;
         w.tnz = nz ? w.tnz + u2d_small(nz) * w.dtz : w.tnz;
-        if (um)
+        if (um) {
             w.skipped += (uint32_t)(nx + ny + nz) - 1u;
+            ++w.ucells;
+        }
         w.ix = nix;
         w.iy = niy;
         w.iz = niz;

@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(kBlock, XSW_WALK_BLOCKS) wave_walk(const __gri
     w.march = 0;
     bool walking = false, drained = false;
     uint32_t ray = 0;
-    uint32_t c_fp = 0, c_sc = 0, c_iter = 0, c_wit = 0;
+    uint32_t c_fp = 0, c_sc = 0, c_iter = 0, c_wit = 0, c_uni = 0;
     for (;;) {
         const unsigned idle = __ballot_sync(kFull, !walking);
         if (!drained && (idle == kFull || __popc(idle) >= kRefill)) {
@@ -322,6 +322,7 @@ __global__ void __launch_bounds__(kBlock, XSW_WALK_BLOCKS) wave_walk(const __gri
                         w.hit = 0;
                         w.steps = 0;
                         w.skipped = 0;
+                        w.ucells = 0;
                         walking = true;
                     }
                 }
@@ -350,6 +351,7 @@ __global__ void __launch_bounds__(kBlock, XSW_WALK_BLOCKS) wave_walk(const __gri
                     c_fp += w.steps + w.skipped;
                 }
                 c_iter += w.steps;
+                c_uni += w.ucells;
             }
         }
     }
@@ -357,7 +359,9 @@ __global__ void __launch_bounds__(kBlock, XSW_WALK_BLOCKS) wave_walk(const __gri
     c_fp = __reduce_add_sync(kFull, c_fp);
     c_sc = __reduce_add_sync(kFull, c_sc);
     c_iter = __reduce_add_sync(kFull, c_iter);
+    c_uni = __reduce_add_sync(kFull, c_uni);
     if (lane == 0) {
+        red_add(diag + 7, c_uni);
         red_add(diag + 0, c_fp);
         red_add(diag + 1, c_sc);
         red_add(diag + 5, c_iter);

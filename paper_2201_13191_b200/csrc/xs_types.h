@@ -35,12 +35,15 @@ struct Grid {
     const float* dens;    // raw densities, bricked (raw format only)
     int32_t fmt;
     int32_t n_codes;      // palette size (P4/P8)
-    // Uniform-cell flags in the palette codes: u8bit when the voxel's 8^3
-    // macro cell is uniform (all voxels the same code), else u4bit when its
-    // 4^3 brick is.  P4: u8bit 8 (<= 8 entries), u4bit 4 (<= 4 entries);
-    // P8: 128 (<= 128) and 64 (<= 64); 0 when not encoded.  ubit = both.
+    // Uniform-block level in the palette codes: the bits above the palette
+    // index (ubit = their mask, lvl_shift = their position) give the level of
+    // the largest aligned uniform block (all voxels the same code) holding the
+    // voxel; byte l of lvl_masks is that block's edge - 1 (0: not uniform).
+    // P4 <= 4 entries / P8 <= 64: two level bits; P4 <= 8 / P8 <= 128: one;
+    // otherwise none (ubit = 0).
     int32_t ubit;
-    int32_t u8bit, u4bit;
+    int32_t lvl_shift;
+    uint32_t lvl_masks;
     int32_t pad_;
 };
 

@@ -11,3 +11,5 @@ r = proj.scatter_stats(w.geometry, 0, w.spectrum, w.config)
 s = r.stats
 print(f"n={n} kernel {s['kernel_ms']:.1f} ms hist/s {n/(s['kernel_ms']/1e3):.3e} lane-occ {s['walk_iterations']/max(1,s['walk_lane_slots']):.3f} "
       f"walk-blk/SM {s['blocks_per_sm']} waves {s['waves']}", flush=True)
+print(f"  walk_iterations {s['walk_iterations']:.3e} uniform {s['uniform_iterations']:.3e} ({s['uniform_iterations']/max(1,s['walk_iterations']):.3f}) "
+      f"REF visits {s['free_path_steps']+s['scoring_steps']:.3e}")
