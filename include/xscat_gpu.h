@@ -156,6 +156,8 @@ typedef struct xs_launch_stats {
     uint32_t waves;            /* wavefront: pipeline waves run */
     uint32_t live_histories;   /* histories in flight at once */
     uint64_t uniform_iterations; /* walker iterations that crossed a uniform cell / brick */
+    float walk_ms;             /* device time of the walk kernel(s) (the whole kernel for the megakernel) */
+    uint32_t launches;         /* kernels launched by the scatter call */
 } xs_launch_stats;
 
 typedef struct xs_context xs_context;

@@ -665,6 +665,8 @@ void accumulate(xs_context* c, const xs_geometry& g, int angle, const xs_spectru
         c->last.engine = 1;
         c->last.waves = info.waves;
         c->last.live_histories = info.n_slots;
+        c->last.walk_ms = info.walk_ms;
+        c->last.launches = info.launches;
         c->last.palette_size = c->n_pal;
         c->last.upload_bytes = c->last_upload_bytes;
         return;
@@ -713,6 +715,8 @@ void accumulate(xs_context* c, const xs_geometry& g, int angle, const xs_spectru
     c->last.engine = 0;
     c->last.waves = 0;
     c->last.live_histories = (uint32_t)((uint64_t)grid * (block / 32) * H);
+    c->last.walk_ms = ms;
+    c->last.launches = 1;
     c->last.palette_size = c->n_pal;
     c->last.upload_bytes = c->last_upload_bytes;
 }

@@ -29,6 +29,7 @@
 // bit-identical images and statistics.
 #include <algorithm>
 #include <cstring>
+#include <vector>
 
 #include "transport_core.cuh"
 
@@ -582,6 +583,7 @@ struct WaveEngine {
     uint8_t* bytes = nullptr; // flags, res_hit
     size_t bytes_have = 0;
     WaveCtl* host_ctl = nullptr; // pinned
+    std::vector<cudaEvent_t> ev;  // walk-kernel timing, a pair per wave
 };
 
 WaveEngine* wave_create() { return new WaveEngine(); }
@@ -603,6 +605,8 @@ void wave_destroy(WaveEngine* e)
     cudaFree(e->bytes);
     if (e->host_ctl)
         cudaFreeHost(e->host_ctl);
+    for (cudaEvent_t v : e->ev)
+        cudaEventDestroy(v);
     delete e;
 }
 
@@ -706,12 +710,19 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
     wave_admit<<<g_work, kBlock, stat_smem, s>>>(P, A);
     XSW_CHECK(cudaGetLastError());
     const int check_every = 4;
-    uint32_t waves = 0;
+    uint32_t waves = 0, launches = 3;
     for (;;) {
         for (int k = 0; k < check_every; ++k) {
             A.cur = cur;
+            while (e->ev.size() < 2 * (size_t)(waves + 1)) {
+                cudaEvent_t v;
+                XSW_CHECK(cudaEventCreate(&v));
+                e->ev.push_back(v);
+            }
             K.setup<<<g_setup, kBlock, mu_smem, s>>>(P, A);
+            XSW_CHECK(cudaEventRecord(e->ev[2 * waves], s));
             K.walk<<<g_walk, kBlock, mu_smem, s>>>(P, A);
+            XSW_CHECK(cudaEventRecord(e->ev[2 * waves + 1], s));
             wave_score<<<g_score, kBlock, stat_smem, s>>>(P, A);
             K.event<<<g_work, kBlock, stat_smem, s>>>(P, A);
             A.cur = cur ^ 1;
@@ -719,6 +730,7 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
             wave_admit<<<g_work, kBlock, stat_smem, s>>>(P, A);
             cur ^= 1;
             ++waves;
+            launches += 6;
         }
         XSW_CHECK(cudaGetLastError());
         XSW_CHECK(cudaMemcpyAsync(e->host_ctl, e->ctl, sizeof(WaveCtl), cudaMemcpyDeviceToHost, s));
@@ -735,6 +747,14 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
         info->waves = waves;
         info->n_slots = n_slots;
         info->walk_blocks_per_sm = walk_per_sm;
+        info->launches = launches;
+        float walk = 0.f;
+        for (uint32_t w = 0; w < waves; ++w) {
+            float ms = 0.f;
+            XSW_CHECK(cudaEventElapsedTime(&ms, e->ev[2 * w], e->ev[2 * w + 1]));
+            walk += ms;
+        }
+        info->walk_ms = walk;
     }
     return cudaSuccess;
 #undef XSW_CHECK

@@ -130,6 +130,8 @@ struct WaveInfo {
     uint32_t waves;
     uint32_t n_slots;
     int32_t walk_blocks_per_sm;
+    uint32_t launches;
+    float walk_ms; // summed device time of the walk kernels
 };
 
 // Angular interpolation plan entry (REF postprocess.cpp:160-192).
