@@ -53,6 +53,8 @@ struct WaveCtl {
     uint32_t* free_stack; // released slots, [0, free_top)
     int32_t free_top;
     uint32_t cursor;      // walk kernel work cursor
+    uint32_t ev_cursor;   // event kernel work cursor
+    uint32_t setup_cursor; // set-up kernel work cursor (reset by wave_plan)
     uint32_t n_rays, n_score;
     uint32_t admit_n, live;
     unsigned long long next_h, admit_base;
@@ -201,6 +203,7 @@ __global__ void __launch_bounds__(kBlock) wave_setup(const __grid_constant__ Tra
     const uint32_t n_s = in.n_score, n = n_s + in.n_free;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         ctl->cursor = 0;
+        ctl->ev_cursor = 0;
         ctl->n_rays = n;
         ctl->n_score = n_s;
         ctl->q[A.cur ^ 1].n_score = 0;
@@ -212,7 +215,17 @@ __global__ void __launch_bounds__(kBlock) wave_setup(const __grid_constant__ Tra
     DevStatus* st = P.status;
     const WaveRays& R = A.R;
     uint32_t c_rays = 0;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    for (;;) { // 32 tasks per warp fetch (scoring and free-path set-ups differ in cost)
+        uint32_t base = 0;
+        if (lane == 0)
+            base = atomicAdd(&ctl->setup_cursor, 32u);
+        base = __shfl_sync(kFull, base, 0);
+        if (base >= n)
+            break;
+        const uint32_t i = base + (uint32_t)lane;
+        if (i >= n)
+            continue;
         Walk w;
         w.march = 0;
         bool walking;
@@ -455,12 +468,24 @@ __global__ void __launch_bounds__(kBlock) wave_event(const __grid_constant__ Tra
     const GlobalQ qs{A.slots, ctl, A.cur ^ 1, -1};
     const WaveRays& R = A.R;
     uint32_t c_int = 0;
-    for (uint32_t i = n_s + blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const int s = (int)in.free[i - n_s];
-        const bool hit = R.res_hit[i] != 0;
-        c_int += hit;
-        history_event<FMT>(P, B, qs, s, hit, R.res[i], R.res_vox[i], R.res_vox[R.cap + i],
-                           R.res_vox[2ull * R.cap + i], var_base_of(P, s), P.status);
+    const int lane = threadIdx.x & 31;
+    // events differ a lot in cost (escape vs. Compton / Rayleigh sampling):
+    // warps fetch 32 at a time from a counter instead of a fixed stride
+    for (;;) {
+        uint32_t base = 0;
+        if (lane == 0)
+            base = atomicAdd(&ctl->ev_cursor, 32u);
+        base = __shfl_sync(kFull, base, 0) + n_s;
+        if (base >= n)
+            break;
+        const uint32_t i = base + (uint32_t)lane;
+        if (i < n) {
+            const int s = (int)in.free[i - n_s];
+            const bool hit = R.res_hit[i] != 0;
+            c_int += hit;
+            history_event<FMT>(P, B, qs, s, hit, R.res[i], R.res_vox[i], R.res_vox[R.cap + i],
+                               R.res_vox[2ull * R.cap + i], var_base_of(P, s), P.status);
+        }
     }
     if (c_int)
         atomicAdd(B.diag + 4, (unsigned long long)c_int);
@@ -481,6 +506,7 @@ __global__ void wave_plan(const __grid_constant__ TransportParams P, const __gri
     ctl->free_top = top - (int32_t)k; // admitted slots: free_stack[top - k, top)
     ctl->next_h += k;
     ctl->live = A.n_slots - (uint32_t)ctl->free_top;
+    ctl->setup_cursor = 0;
     ++ctl->waves;
 }
 
