@@ -30,7 +30,7 @@ struct WaveEngine;
 WaveEngine* wave_create();
 void wave_destroy(WaveEngine* e);
 cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint32_t n_slots, cudaStream_t s,
-                     WaveInfo* info, cudaEvent_t start);
+                     WaveInfo* info, cudaEvent_t start, int n_pipes);
 cudaError_t launch_finalize_image(const unsigned long long* acc, uint64_t off_image, uint64_t off_var,
                                   uint64_t npix, int log2_img, double n_hist, int track_var,
                                   double* image, double* var, cudaStream_t s);
@@ -185,6 +185,7 @@ struct xs_context {
     std::vector<int> lvl_edges2{4, 8, 32}; // uniform-block edges with two level bits (C3 sweep: best of 7 sets)
     int lvl_edge1 = 8;                      // ... with one level bit
     uint32_t wave_slots = 1u << 20;  // live histories of the wavefront engine
+    int wave_pipes = 2;              // concurrent wavefront pipelines (streams)
     xsd::WaveEngine* wave = nullptr;
 };
 
@@ -652,7 +653,8 @@ void accumulate(xs_context* c, const xs_geometry& g, int angle, const xs_spectru
         if (!c->wave)
             c->wave = xsd::wave_create();
         xsd::WaveInfo info{};
-        cuda_check(xsd::wave_run(c->wave, P, c->sm_count, n_slots, s, &info, c->ev0), "wavefront transport");
+        cuda_check(xsd::wave_run(c->wave, P, c->sm_count, n_slots, s, &info, c->ev0, c->wave_pipes),
+                   "wavefront transport");
         cuda_check(cudaEventRecord(c->ev1, s), "event");
         check_status(c, angle, &spec);
         float ms = 0.f;
@@ -876,6 +878,8 @@ int xs_ctx_create(int32_t device, xs_context** out)
         }
         if (const char* e = std::getenv("XSCAT_ENGINE"))
             c->engine = std::atoi(e) != 0;
+        if (const char* e = std::getenv("XSCAT_WAVE_PIPES"))
+            c->wave_pipes = std::max(1, std::min(2, std::atoi(e)));
         if (const char* e = std::getenv("XSCAT_WAVE_SLOTS"))
             c->wave_slots = (uint32_t)std::max(1, std::atoi(e));
         *out = c;
@@ -931,6 +935,8 @@ int xs_ctx_set_option(xs_context* c, const char* key, int64_t value)
             c->grab = (int)std::max<int64_t>(1, value);
         } else if (k == "engine") {
             c->engine = value != 0;
+        } else if (k == "wave_pipes") {
+            c->wave_pipes = (int)std::max<int64_t>(1, std::min<int64_t>(2, value));
         } else if (k == "wave_slots") {
             c->wave_slots = (uint32_t)std::max<int64_t>(1, std::min<int64_t>(1 << 24, value));
         } else {

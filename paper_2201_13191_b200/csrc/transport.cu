@@ -52,6 +52,7 @@ struct WarpHdr {
 // The scoring FIFO has qlen = H * splitting + 1 entries and its tail wraps
 // (atomicInc), so it can never fill; the free-path FIFO follows it.
 struct WarpQ {
+    static constexpr bool kBatchScores = false;
     Slot* slots;   // H slots, then the WarpHdr, then the FIFOs
     uint32_t hoff; // byte offset of the WarpHdr
     uint32_t qlen;

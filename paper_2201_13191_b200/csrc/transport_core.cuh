@@ -43,6 +43,37 @@ struct __align__(8) Slot {
     int32_t n_var;                 // variance scratch entries
 };
 
+// Philox4x32-10 block for counter {block, photon, bin, angle} and key
+// {k0, k1} (REF rng.hpp:29-60).
+__device__ __forceinline__ void philox_block(uint32_t block, uint32_t photon, uint32_t bin, uint32_t angle,
+                                             uint32_t k0, uint32_t k1, uint32_t& o0, uint32_t& o1,
+                                             uint32_t& o2, uint32_t& o3)
+{
+    uint32_t c0 = block, c1 = photon, c2 = bin, c3 = angle;
+#pragma unroll
+    for (int i = 0; i < 10; ++i) {
+        const uint32_t lo0 = 0xD2511F53u * c0, hi0 = __umulhi(0xD2511F53u, c0);
+        const uint32_t lo1 = 0xCD9E8D57u * c2, hi1 = __umulhi(0xCD9E8D57u, c2);
+        c0 = hi1 ^ c1 ^ k0;
+        c1 = lo1;
+        c2 = hi0 ^ c3 ^ k1;
+        c3 = lo0;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    o0 = c0;
+    o1 = c1;
+    o2 = c2;
+    o3 = c3;
+}
+
+// REF Rng::uniform: the top 53 bits of a 64-bit word pair, centred.
+__device__ __forceinline__ double words_to_uniform(uint32_t hi, uint32_t lo)
+{
+    const uint64_t bits = (((uint64_t)hi << 32) | lo) >> 11;
+    return ((double)bits + 0.5) * 0x1p-53;
+}
+
 // One out-of-line Philox draw on a history's stream (REF rng.hpp:29-60).  The
 // event code works on a local copy of the slot's stream (one load and one
 // store per event instead of a slot round trip per draw); a single copy of
@@ -50,36 +81,45 @@ struct __align__(8) Slot {
 __device__ __noinline__ double slot_uniform(SlotRng* s, uint32_t k0, uint32_t k1, uint32_t angle)
 {
     if (s->pos == 4) {
-        uint32_t c0 = s->block, c1 = s->photon, c2 = s->bin, c3 = angle;
-#pragma unroll
-        for (int i = 0; i < 10; ++i) {
-            const uint32_t lo0 = 0xD2511F53u * c0, hi0 = __umulhi(0xD2511F53u, c0);
-            const uint32_t lo1 = 0xCD9E8D57u * c2, hi1 = __umulhi(0xCD9E8D57u, c2);
-            c0 = hi1 ^ c1 ^ k0;
-            c1 = lo1;
-            c2 = hi0 ^ c3 ^ k1;
-            c3 = lo0;
-            k0 += 0x9E3779B9u;
-            k1 += 0xBB67AE85u;
-        }
-        s->b0 = c0;
-        s->b1 = c1;
-        s->b2 = c2;
-        s->b3 = c3;
+        philox_block(s->block, s->photon, s->bin, angle, k0, k1, s->b0, s->b1, s->b2, s->b3);
         s->pos = 0;
         ++s->block;
     }
-    uint64_t hi, lo;
-    if (s->pos == 0) {
-        hi = s->b0;
-        lo = s->b1;
-    } else {
-        hi = s->b2;
-        lo = s->b3;
-    }
+    const uint32_t hi = s->pos == 0 ? s->b0 : s->b2;
+    const uint32_t lo = s->pos == 0 ? s->b1 : s->b3;
     s->pos += 2;
-    const uint64_t bits = ((hi << 32) | lo) >> 11;
-    return ((double)bits + 0.5) * 0x1p-53;
+    return words_to_uniform(hi, lo);
+}
+
+// The j-th draw after stream state `r` without drawing the ones before it
+// (Philox is counter-based): the wavefront engine draws a history's scoring
+// pixels in parallel, one thread per ray, bit for bit REF's sequential order.
+__device__ __forceinline__ double rng_uniform_at(const SlotRng& r, uint32_t j, uint32_t k0, uint32_t k1,
+                                                 uint32_t angle)
+{
+    const uint32_t m0 = (4u - r.pos) >> 1; // draws left in the buffered block
+    if (j < m0) {
+        const uint32_t q = r.pos + 2 * j;
+        return words_to_uniform(q == 0 ? r.b0 : r.b2, q == 0 ? r.b1 : r.b3);
+    }
+    const uint32_t k = j - m0;
+    uint32_t o0, o1, o2, o3;
+    philox_block(r.block + (k >> 1), r.photon, r.bin, angle, k0, k1, o0, o1, o2, o3);
+    return (k & 1) ? words_to_uniform(o2, o3) : words_to_uniform(o0, o1);
+}
+
+// Advance the stream past n draws (the state slot_uniform would leave).
+__device__ __forceinline__ void rng_skip(SlotRng& r, uint32_t n, uint32_t k0, uint32_t k1, uint32_t angle)
+{
+    const uint32_t m0 = (4u - r.pos) >> 1;
+    if (n <= m0) {
+        r.pos += 2 * n;
+        return;
+    }
+    const uint32_t rem = n - m0, nb = (rem + 1) >> 1;
+    philox_block(r.block + nb - 1, r.photon, r.bin, angle, k0, k1, r.b0, r.b1, r.b2, r.b3);
+    r.block += nb;
+    r.pos = (rem & 1) ? 2 : 4;
 }
 
 // ----------------------------------------------------------------- mu table
@@ -602,6 +642,16 @@ __device__ __forceinline__ void score_complete(const TransportParams& P, const B
     end_history(P, B, qs, s, var_base, st);
 }
 
+// REF run_history :162-164: the scoring pixel of one (u, v) draw pair.
+__device__ __forceinline__ uint32_t score_pixel(const TransportParams& P, double uu, double uv)
+{
+    int iu = (int)(uu * P.nu);
+    int iv = (int)(uv * P.nv);
+    iu = iu < P.nu - 1 ? iu : P.nu - 1;
+    iv = iv < P.nv - 1 ? iv : P.nv - 1;
+    return (uint32_t)(iv * P.nu + iu);
+}
+
 // Free-path completion: the reference's per-history event logic
 // (run_history :141-223) on the history's own Philox stream.
 template <int FMT, class Q>
@@ -658,14 +708,18 @@ __device__ __noinline__ void history_event(const TransportParams& P, const Block
         S.pref = kPi * r0 * r0 / sigma;
     }
     atomicAdd(&S.pending, P.splitting);
-    const uint32_t qbase = qs.reserve_scores(P.splitting);
+    if constexpr (Q::kBatchScores) {
+        // one batch entry; the set-up kernel draws its pixels in parallel
+        qs.push_score_batch(s, rng);
+        rng_skip(rng, 2u * (uint32_t)P.splitting, P.k0, P.k1, P.angle);
+    } else {
+        const uint32_t qbase = qs.reserve_scores(P.splitting);
 #pragma unroll 1
-    for (int k = 0; k < P.splitting; ++k) { // REF :162-164 pixel draws
-        int iu = (int)(slot_uniform(&rng, P.k0, P.k1, P.angle) * P.nu);
-        int iv = (int)(slot_uniform(&rng, P.k0, P.k1, P.angle) * P.nv);
-        iu = iu < P.nu - 1 ? iu : P.nu - 1;
-        iv = iv < P.nv - 1 ? iv : P.nv - 1;
-        qs.push_score(qbase + k, s, (uint32_t)(iv * P.nu + iu));
+        for (int k = 0; k < P.splitting; ++k) { // REF :162-164 pixel draws
+            const double uu = slot_uniform(&rng, P.k0, P.k1, P.angle); // u first, then v
+            const double uv = slot_uniform(&rng, P.k0, P.k1, P.angle);
+            qs.push_score(qbase + k, s, score_pixel(P, uu, uv));
+        }
     }
     // continuation (REF :195-205)
     V3 ndir;

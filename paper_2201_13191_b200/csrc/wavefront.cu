@@ -28,6 +28,7 @@
 // are the same fixed-point integers as the megakernel's, so both engines give
 // bit-identical images and statistics.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -42,10 +43,18 @@ constexpr int kRefill = 8; // idle lanes that trigger a warp's refill in the wal
 #define XSW_WALK_BLOCKS 6 // resident walk blocks per SM (<= 80 registers; 7-8 spill or slow the macro walk)
 #endif
 
+// A history's scoring rays of one interaction: the slot and its Philox
+// stream at the first pixel draw (the set-up kernel draws pixel k from
+// draws 2k, 2k+1, REF run_history :162-164).
+struct ScoreBatch {
+    uint32_t slot;
+    SlotRng rng;
+};
+
 struct WaveQueue {
-    unsigned long long* score; // (slot << 32) | pixel
-    uint32_t* free;            // slot
-    uint32_t n_score, n_free;
+    ScoreBatch* batch; // one per interaction, splitting rays each
+    uint32_t* free;    // slot
+    uint32_t n_batch, n_free;
 };
 
 struct WaveCtl {
@@ -69,6 +78,7 @@ struct WaveRays {
     int* vox;                                  // 3 planes: ix, iy, iz
     uint8_t* flags;                            // (sx+1) | (sy+1) << 2 | (sz+1) << 4 | walking << 6
     double* pre;                               // scoring prefactor (set-up -> complete)
+    uint32_t* pix;                             // scoring pixel (set-up -> complete)
     double* res;                               // depth (scoring) / t_hit (free path)
     int* res_vox;                              // 3 planes: the free path's interaction voxel
     uint8_t* res_hit;
@@ -80,6 +90,7 @@ struct WaveArgs {
     Slot* slots;
     WaveCtl* ctl;
     WaveRays R;
+    unsigned long long* next_h; // next history to admit, shared by the pipelines
     uint32_t n_slots;
     int32_t cur; // queue consumed by this wave (the other one is filled)
 };
@@ -108,14 +119,17 @@ struct GlobalQ {
     int out;
     int free_at; // >= 0: this thread's free-path entry is pre-reserved (admission)
     __device__ __forceinline__ Slot& slot(int s) const { return slots[s]; }
-    __device__ __forceinline__ uint32_t reserve_scores(int n) const
+    static constexpr bool kBatchScores = true;
+    __device__ __forceinline__ void push_score_batch(int s, const SlotRng& r) const
     {
-        return warp_reserve(&ctl->q[out].n_score, (uint32_t)n);
+        WaveQueue& q = ctl->q[out];
+        const uint32_t i = warp_reserve(&q.n_batch, 1u);
+        q.batch[i].slot = (uint32_t)s;
+        q.batch[i].rng = r;
     }
-    __device__ __forceinline__ void push_score(uint32_t i, int s, uint32_t pixel) const
-    {
-        ctl->q[out].score[i] = ((unsigned long long)(uint32_t)s << 32) | pixel;
-    }
+    // (per-ray pushes: megakernel only)
+    __device__ __forceinline__ uint32_t reserve_scores(int) const { return 0; }
+    __device__ __forceinline__ void push_score(uint32_t, int, uint32_t) const {}
     __device__ __forceinline__ void push_free(int s) const
     {
         WaveQueue& q = ctl->q[out];
@@ -200,13 +214,13 @@ __global__ void __launch_bounds__(kBlock) wave_setup(const __grid_constant__ Tra
     extern __shared__ __align__(16) unsigned char smem[];
     WaveCtl* ctl = A.ctl;
     const WaveQueue& in = ctl->q[A.cur];
-    const uint32_t n_s = in.n_score, n = n_s + in.n_free;
+    const uint32_t n_s = in.n_batch * (uint32_t)P.splitting, n = n_s + in.n_free;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         ctl->cursor = 0;
         ctl->ev_cursor = 0;
         ctl->n_rays = n;
         ctl->n_score = n_s;
-        ctl->q[A.cur ^ 1].n_score = 0;
+        ctl->q[A.cur ^ 1].n_batch = 0;
         ctl->q[A.cur ^ 1].n_free = 0;
     }
     MuTab<FMT, REG> tab;
@@ -229,12 +243,16 @@ __global__ void __launch_bounds__(kBlock) wave_setup(const __grid_constant__ Tra
         Walk w;
         w.march = 0;
         bool walking;
-        if (i < n_s) { // REF run_history :166-183
-            const unsigned long long task = in.score[i];
-            const Slot& S = A.slots[(uint32_t)(task >> 32)];
+        if (i < n_s) { // REF run_history :162-183
+            const uint32_t b = i / (uint32_t)P.splitting, k = i - b * (uint32_t)P.splitting;
+            const ScoreBatch& sb = in.batch[b];
+            const Slot& S = A.slots[sb.slot];
+            const uint32_t pix = score_pixel(P, rng_uniform_at(sb.rng, 2 * k, P.k0, P.k1, P.angle),
+                                             rng_uniform_at(sb.rng, 2 * k + 1, P.k0, P.k1, P.angle));
+            R.pix[i] = pix;
             V3 o, to_det;
             double e_out;
-            R.pre[i] = score_setup(P, S, (uint32_t)task, o, to_det, e_out, st);
+            R.pre[i] = score_setup(P, S, pix, o, to_det, e_out, st);
             if (tab.energy != e_out) // REF trace_attenuation builds MuField(e_out)
                 tab.fill(P, e_out, st, S.bin);
             walking = walk_begin<FMT, SKIP>(P, w, o, to_det, CUDART_INF, false, st, S.bin);
@@ -408,9 +426,8 @@ __global__ void __launch_bounds__(kBlock) wave_score(const __grid_constant__ Tra
         int s = -1;
         uint64_t l0 = 0, l1 = 0, l2 = 0;
         if (is_score) {
-            const unsigned long long task = in.score[i];
-            s = (int)(task >> 32);
-            const uint32_t pix = (uint32_t)task;
+            s = (int)in.batch[i / (uint32_t)P.splitting].slot;
+            const uint32_t pix = R.pix[i];
             const double x = R.pre[i] * nl_exp(-R.res[i]);
             if (!isfinite(x)) {
                 raise(st, XS_E_RUNTIME, kErrNonFinite, A.slots[s].bin, A.slots[s].e_in, x);
@@ -496,15 +513,18 @@ __global__ void __launch_bounds__(kBlock) wave_event(const __grid_constant__ Tra
 __global__ void wave_plan(const __grid_constant__ TransportParams P, const __grid_constant__ WaveArgs A)
 {
     WaveCtl* ctl = A.ctl;
-    const unsigned long long left = P.h_end - ctl->next_h;
     const int32_t top = ctl->free_top;
+    // claim up to one history per free slot from the shared counter (several
+    // pipelines admit concurrently; claims past h_end are simply empty)
+    const unsigned long long base = top > 0 ? atomicAdd(A.next_h, (unsigned long long)top) : *A.next_h;
+    const unsigned long long left = base < P.h_end ? P.h_end - base : 0ull;
     const uint32_t k = (unsigned long long)top < left ? (uint32_t)top : (uint32_t)left;
-    ctl->admit_base = ctl->next_h;
+    ctl->admit_base = base;
     ctl->admit_n = k;
+    ctl->next_h = base + (unsigned long long)top;
     ctl->admit_q = ctl->q[A.cur].n_free; // admitted histories' free paths follow the events'
     ctl->q[A.cur].n_free += k;
     ctl->free_top = top - (int32_t)k; // admitted slots: free_stack[top - k, top)
-    ctl->next_h += k;
     ctl->live = A.n_slots - (uint32_t)ctl->free_top;
     ctl->setup_cursor = 0;
     ++ctl->waves;
@@ -536,9 +556,9 @@ __global__ void wave_init(WaveCtl* ctl, uint32_t* stack, uint32_t n_slots, unsig
         stack[i] = n_slots - 1 - i;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         ctl->free_top = (int32_t)n_slots;
-        ctl->next_h = h_begin;
-        ctl->q[0].n_score = ctl->q[0].n_free = 0;
-        ctl->q[1].n_score = ctl->q[1].n_free = 0;
+        ctl->next_h = h_begin; // this pipeline's last view of the shared counter
+        ctl->q[0].n_batch = ctl->q[0].n_free = 0;
+        ctl->q[1].n_batch = ctl->q[1].n_free = 0;
         ctl->waves = 0;
         ctl->live = 0;
     }
@@ -589,14 +609,18 @@ cudaError_t grow(T*& p, size_t& have, size_t need)
 } // namespace
 
 // ------------------------------------------------------------------- host
-struct WaveEngine {
+// One pipeline: its histories (slots), queues, ray arrays and stream.  Two
+// pipelines run on two streams and share the history counter, so one's
+// latency-bound event/set-up kernels overlap the other's issue-bound walk and
+// each kernel's tail is filled by the other pipeline's work.
+struct WavePipe {
     Slot* slots = nullptr;
     size_t n_slots_have = 0;
     uint32_t* stack = nullptr;
     size_t stack_have = 0;
     WaveCtl* ctl = nullptr;
     size_t ctl_have = 0;
-    unsigned long long* sq[2] = {nullptr, nullptr};
+    ScoreBatch* sq[2] = {nullptr, nullptr};
     size_t sq_have[2] = {0, 0};
     uint32_t* fq[2] = {nullptr, nullptr};
     size_t fq_have[2] = {0, 0};
@@ -604,12 +628,49 @@ struct WaveEngine {
     size_t dbl_have = 0;
     float* rd = nullptr;
     size_t rd_have = 0;
-    int* vox = nullptr; // vox x3, res_vox x3
+    int* vox = nullptr; // vox x3, res_vox x3, pix
     size_t vox_have = 0;
     uint8_t* bytes = nullptr; // flags, res_hit
     size_t bytes_have = 0;
     WaveCtl* host_ctl = nullptr; // pinned
-    std::vector<cudaEvent_t> ev;  // walk-kernel timing, a pair per wave
+    cudaStream_t stream = nullptr;
+    cudaEvent_t join = nullptr;
+    std::vector<cudaEvent_t> ev; // walk-kernel timing, a pair per wave
+    // per run
+    WaveArgs A;
+    TransportParams P;
+    int cur = 0;
+    uint32_t waves = 0;
+    bool done = false;
+
+    void release()
+    {
+        cudaFree(slots);
+        cudaFree(stack);
+        cudaFree(ctl);
+        for (int b = 0; b < 2; ++b) {
+            cudaFree(sq[b]);
+            cudaFree(fq[b]);
+        }
+        cudaFree(dbl);
+        cudaFree(rd);
+        cudaFree(vox);
+        cudaFree(bytes);
+        if (host_ctl)
+            cudaFreeHost(host_ctl);
+        for (cudaEvent_t v : ev)
+            cudaEventDestroy(v);
+        if (join)
+            cudaEventDestroy(join);
+        if (stream)
+            cudaStreamDestroy(stream);
+    }
+};
+
+struct WaveEngine {
+    WavePipe pipe[2];
+    unsigned long long* next_h = nullptr;
+    cudaEvent_t fork = nullptr;
 };
 
 WaveEngine* wave_create() { return new WaveEngine(); }
@@ -618,69 +679,57 @@ void wave_destroy(WaveEngine* e)
 {
     if (!e)
         return;
-    cudaFree(e->slots);
-    cudaFree(e->stack);
-    cudaFree(e->ctl);
-    for (int b = 0; b < 2; ++b) {
-        cudaFree(e->sq[b]);
-        cudaFree(e->fq[b]);
-    }
-    cudaFree(e->dbl);
-    cudaFree(e->rd);
-    cudaFree(e->vox);
-    cudaFree(e->bytes);
-    if (e->host_ctl)
-        cudaFreeHost(e->host_ctl);
-    for (cudaEvent_t v : e->ev)
-        cudaEventDestroy(v);
+    for (WavePipe& p : e->pipe)
+        p.release();
+    cudaFree(e->next_h);
+    if (e->fork)
+        cudaEventDestroy(e->fork);
     delete e;
 }
 
 size_t wave_slot_bytes() { return sizeof(Slot); }
 
-cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint32_t n_slots,
-                     cudaStream_t s, WaveInfo* info, cudaEvent_t start)
-{
 #define XSW_CHECK(x)                                                                               \
     do {                                                                                           \
         cudaError_t err_ = (x);                                                                    \
         if (err_ != cudaSuccess)                                                                   \
             return err_;                                                                           \
     } while (0)
-    const uint64_t n_hist = P.h_end - P.h_begin;
-    if (n_slots > n_hist)
-        n_slots = (uint32_t)n_hist;
-    if (n_slots < 1)
-        n_slots = 1;
+
+static cudaError_t pipe_prepare(WavePipe& w, const TransportParams& P, uint32_t n_slots, int n_mu)
+{
     const uint64_t split = (uint64_t)P.splitting;
     const uint64_t cap = (uint64_t)n_slots * (split + 1);
     if (cap >= (1ull << 32))
         return cudaErrorInvalidValue;
-    const int n_mu = use_reg_w(P) ? 4 : 8;
-    XSW_CHECK(grow(e->slots, e->n_slots_have, n_slots));
-    XSW_CHECK(grow(e->stack, e->stack_have, n_slots));
-    XSW_CHECK(grow(e->ctl, e->ctl_have, 1));
+    XSW_CHECK(grow(w.slots, w.n_slots_have, n_slots));
+    XSW_CHECK(grow(w.stack, w.stack_have, n_slots));
+    XSW_CHECK(grow(w.ctl, w.ctl_have, 1));
     for (int b = 0; b < 2; ++b) {
-        XSW_CHECK(grow(e->sq[b], e->sq_have[b], (size_t)n_slots * split));
-        XSW_CHECK(grow(e->fq[b], e->fq_have[b], (size_t)n_slots));
+        XSW_CHECK(grow(w.sq[b], w.sq_have[b], (size_t)n_slots));
+        XSW_CHECK(grow(w.fq[b], w.fq_have[b], (size_t)n_slots));
     }
     const size_t n_dbl = (size_t)(3 + 3 + 3 + n_mu + 2);
-    XSW_CHECK(grow(e->dbl, e->dbl_have, n_dbl * cap));
-    XSW_CHECK(grow(e->rd, e->rd_have, 3 * cap));
-    XSW_CHECK(grow(e->vox, e->vox_have, 6 * cap));
-    XSW_CHECK(grow(e->bytes, e->bytes_have, 2 * cap));
-    if (!e->host_ctl)
-        XSW_CHECK(cudaHostAlloc(&e->host_ctl, sizeof(WaveCtl), cudaHostAllocDefault));
+    XSW_CHECK(grow(w.dbl, w.dbl_have, n_dbl * cap));
+    XSW_CHECK(grow(w.rd, w.rd_have, 3 * cap));
+    XSW_CHECK(grow(w.vox, w.vox_have, 7 * cap));
+    XSW_CHECK(grow(w.bytes, w.bytes_have, 2 * cap));
+    if (!w.host_ctl)
+        XSW_CHECK(cudaHostAlloc(&w.host_ctl, sizeof(WaveCtl), cudaHostAllocDefault));
+    if (!w.stream)
+        XSW_CHECK(cudaStreamCreateWithFlags(&w.stream, cudaStreamNonBlocking));
+    if (!w.join)
+        XSW_CHECK(cudaEventCreateWithFlags(&w.join, cudaEventDisableTiming));
 
-    WaveArgs A;
+    WaveArgs& A = w.A;
     std::memset(&A, 0, sizeof A);
-    A.slots = e->slots;
-    A.ctl = e->ctl;
+    A.slots = w.slots;
+    A.ctl = w.ctl;
     A.n_slots = n_slots;
     WaveRays& R = A.R;
     R.cap = (uint32_t)cap;
     R.n_mu = n_mu;
-    double* d = e->dbl;
+    double* d = w.dbl;
     R.t = d;
     R.texit = d + cap;
     R.target = d + 2 * cap;
@@ -689,24 +738,41 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
     R.mu = d + 9 * cap;
     R.pre = d + (9 + n_mu) * cap;
     R.res = d + (10 + n_mu) * cap;
-    R.rd = e->rd;
-    R.vox = e->vox;
-    R.res_vox = e->vox + 3 * cap;
-    R.flags = e->bytes;
-    R.res_hit = e->bytes + cap;
+    R.rd = w.rd;
+    R.vox = w.vox;
+    R.res_vox = w.vox + 3 * cap;
+    R.pix = reinterpret_cast<uint32_t*>(w.vox + 6 * cap);
+    R.flags = w.bytes;
+    R.res_hit = w.bytes + cap;
+    return cudaSuccess;
+}
 
-    if (start) // buffers are allocated: the timed region starts here
-        XSW_CHECK(cudaEventRecord(start, s));
-    WaveCtl init;
-    std::memset(&init, 0, sizeof init);
-    for (int b = 0; b < 2; ++b) {
-        init.q[b].score = e->sq[b];
-        init.q[b].free = e->fq[b];
+cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint32_t n_slots,
+                     cudaStream_t s, WaveInfo* info, cudaEvent_t start, int n_pipes)
+{
+    const uint64_t n_hist = P.h_end - P.h_begin;
+    if (n_slots > n_hist)
+        n_slots = (uint32_t)n_hist;
+    if (n_slots < 1)
+        n_slots = 1;
+    n_pipes = n_pipes < 1 ? 1 : (n_pipes > 2 ? 2 : n_pipes);
+    if (n_slots < 2)
+        n_pipes = 1;
+    const uint32_t per = (n_slots + n_pipes - 1) / n_pipes;
+    const int n_mu = use_reg_w(P) ? 4 : 8;
+    for (int p = 0; p < n_pipes; ++p) {
+        WavePipe& w = e->pipe[p];
+        XSW_CHECK(pipe_prepare(w, P, per, n_mu));
+        w.P = P;
+        if (P.track_var) { // scratch: var_cap entries per slot, pipelines side by side
+            w.P.var_pix = P.var_pix + (size_t)p * per * P.var_cap;
+            w.P.var_val = P.var_val + (size_t)p * per * P.var_cap;
+        }
     }
-    init.free_stack = e->stack;
-    XSW_CHECK(cudaMemcpyAsync(e->ctl, &init, sizeof init, cudaMemcpyHostToDevice, s));
-    wave_init<<<sm_count, 256, 0, s>>>(e->ctl, e->stack, n_slots, P.h_begin);
-    XSW_CHECK(cudaGetLastError());
+    if (!e->next_h)
+        XSW_CHECK(cudaMalloc(&e->next_h, sizeof(unsigned long long)));
+    if (!e->fork)
+        XSW_CHECK(cudaEventCreateWithFlags(&e->fork, cudaEventDisableTiming));
 
     const WaveSet K = wave_kernels_for(P);
     const size_t mu_smem = use_reg_w(P) ? 0 : (size_t)8 * kBlock * 8;
@@ -725,65 +791,116 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
     XSW_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&walk_per_sm, K.walk, kBlock, mu_smem));
     if (walk_per_sm < 1)
         walk_per_sm = 1;
-    const int g_walk = sm_count * walk_per_sm;
+    int walk_use = walk_per_sm;
+    if (const char* v = std::getenv("XSCAT_WALK_BPS")) // experiment: walk blocks per SM actually launched
+        walk_use = std::max(1, std::min(walk_per_sm, std::atoi(v)));
+    const int g_walk = sm_count * walk_use;
     const int g_work = sm_count * 4;  // admission / events (~120 registers)
     const int g_setup = sm_count * 8; // <= 64 registers
     const int g_score = sm_count * 8;
 
-    int cur = 0;
-    A.cur = 0;
-    wave_plan<<<1, 1, 0, s>>>(P, A);
-    wave_admit<<<g_work, kBlock, stat_smem, s>>>(P, A);
-    XSW_CHECK(cudaGetLastError());
-    const int check_every = 4;
-    uint32_t waves = 0, launches = 3;
-    for (;;) {
-        for (int k = 0; k < check_every; ++k) {
-            A.cur = cur;
-            while (e->ev.size() < 2 * (size_t)(waves + 1)) {
-                cudaEvent_t v;
-                XSW_CHECK(cudaEventCreate(&v));
-                e->ev.push_back(v);
-            }
-            K.setup<<<g_setup, kBlock, mu_smem, s>>>(P, A);
-            XSW_CHECK(cudaEventRecord(e->ev[2 * waves], s));
-            K.walk<<<g_walk, kBlock, mu_smem, s>>>(P, A);
-            XSW_CHECK(cudaEventRecord(e->ev[2 * waves + 1], s));
-            wave_score<<<g_score, kBlock, stat_smem, s>>>(P, A);
-            K.event<<<g_work, kBlock, stat_smem, s>>>(P, A);
-            A.cur = cur ^ 1;
-            wave_plan<<<1, 1, 0, s>>>(P, A);
-            wave_admit<<<g_work, kBlock, stat_smem, s>>>(P, A);
-            cur ^= 1;
-            ++waves;
-            launches += 6;
+    if (start) // buffers are allocated: the timed region starts here
+        XSW_CHECK(cudaEventRecord(start, s));
+    XSW_CHECK(cudaMemcpyAsync(e->next_h, &P.h_begin, sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
+    XSW_CHECK(cudaEventRecord(e->fork, s));
+    uint32_t launches = 0;
+    for (int p = 0; p < n_pipes; ++p) {
+        WavePipe& w = e->pipe[p];
+        cudaStream_t ps = w.stream;
+        XSW_CHECK(cudaStreamWaitEvent(ps, e->fork, 0));
+        WaveCtl init;
+        std::memset(&init, 0, sizeof init);
+        for (int b = 0; b < 2; ++b) {
+            init.q[b].batch = w.sq[b];
+            init.q[b].free = w.fq[b];
         }
+        init.free_stack = w.stack;
+        XSW_CHECK(cudaMemcpyAsync(w.ctl, &init, sizeof init, cudaMemcpyHostToDevice, ps));
+        wave_init<<<sm_count, 256, 0, ps>>>(w.ctl, w.stack, per, P.h_begin);
+        w.A.next_h = e->next_h;
+        w.cur = 0;
+        w.waves = 0;
+        w.done = false;
+        w.A.cur = 0;
+        wave_plan<<<1, 1, 0, ps>>>(w.P, w.A);
+        wave_admit<<<g_work, kBlock, stat_smem, ps>>>(w.P, w.A);
         XSW_CHECK(cudaGetLastError());
-        XSW_CHECK(cudaMemcpyAsync(e->host_ctl, e->ctl, sizeof(WaveCtl), cudaMemcpyDeviceToHost, s));
+        launches += 3;
+    }
+    const int check_every = 4;
+    for (;;) {
+        for (int k = 0; k < check_every; ++k)
+            for (int p = 0; p < n_pipes; ++p) {
+                WavePipe& w = e->pipe[p];
+                if (w.done)
+                    continue;
+                cudaStream_t ps = w.stream;
+                WaveArgs& A = w.A;
+                while (w.ev.size() < 2 * (size_t)(w.waves + 1)) {
+                    cudaEvent_t v;
+                    XSW_CHECK(cudaEventCreate(&v));
+                    w.ev.push_back(v);
+                }
+                A.cur = w.cur;
+                K.setup<<<g_setup, kBlock, mu_smem, ps>>>(w.P, A);
+                XSW_CHECK(cudaEventRecord(w.ev[2 * w.waves], ps));
+                K.walk<<<g_walk, kBlock, mu_smem, ps>>>(w.P, A);
+                XSW_CHECK(cudaEventRecord(w.ev[2 * w.waves + 1], ps));
+                wave_score<<<g_score, kBlock, stat_smem, ps>>>(w.P, A);
+                K.event<<<g_work, kBlock, stat_smem, ps>>>(w.P, A);
+                A.cur = w.cur ^ 1;
+                wave_plan<<<1, 1, 0, ps>>>(w.P, A);
+                wave_admit<<<g_work, kBlock, stat_smem, ps>>>(w.P, A);
+                w.cur ^= 1;
+                ++w.waves;
+                launches += 6;
+            }
+        XSW_CHECK(cudaGetLastError());
+        for (int p = 0; p < n_pipes; ++p) {
+            WavePipe& w = e->pipe[p];
+            if (!w.done)
+                XSW_CHECK(cudaMemcpyAsync(w.host_ctl, w.ctl, sizeof(WaveCtl), cudaMemcpyDeviceToHost, w.stream));
+        }
         DevStatus hs;
-        XSW_CHECK(cudaMemcpyAsync(&hs, P.status, sizeof hs, cudaMemcpyDeviceToHost, s));
-        XSW_CHECK(cudaStreamSynchronize(s));
-        if (hs.code != 0)
+        XSW_CHECK(cudaMemcpyAsync(&hs, P.status, sizeof hs, cudaMemcpyDeviceToHost, e->pipe[0].stream));
+        bool all_done = true;
+        for (int p = 0; p < n_pipes; ++p) {
+            WavePipe& w = e->pipe[p];
+            if (w.done)
+                continue;
+            XSW_CHECK(cudaStreamSynchronize(w.stream));
+            const WaveCtl& h = *w.host_ctl;
+            // nothing left to admit (the shared counter, as this pipeline last saw it,
+            // is past the end) and no history in flight
+            w.done = h.live == 0 && h.next_h >= P.h_end && h.q[w.cur].n_batch == 0 && h.q[w.cur].n_free == 0;
+            all_done = all_done && w.done;
+        }
+        if (hs.code != 0 || all_done)
             break;
-        const WaveCtl& h = *e->host_ctl;
-        if (h.live == 0 && h.next_h >= P.h_end && h.q[cur].n_score == 0 && h.q[cur].n_free == 0)
-            break;
+    }
+    uint32_t waves = 0;
+    float walk = 0.f;
+    for (int p = 0; p < n_pipes; ++p) {
+        WavePipe& w = e->pipe[p];
+        XSW_CHECK(cudaEventRecord(w.join, w.stream));
+        XSW_CHECK(cudaStreamWaitEvent(s, w.join, 0));
+        XSW_CHECK(cudaStreamSynchronize(w.stream));
+        for (uint32_t i = 0; i < w.waves; ++i) {
+            float ms = 0.f;
+            XSW_CHECK(cudaEventElapsedTime(&ms, w.ev[2 * i], w.ev[2 * i + 1]));
+            walk += ms;
+        }
+        waves = std::max(waves, w.waves);
     }
     if (info) {
         info->waves = waves;
-        info->n_slots = n_slots;
+        info->n_slots = per * n_pipes;
         info->walk_blocks_per_sm = walk_per_sm;
         info->launches = launches;
-        float walk = 0.f;
-        for (uint32_t w = 0; w < waves; ++w) {
-            float ms = 0.f;
-            XSW_CHECK(cudaEventElapsedTime(&ms, e->ev[2 * w], e->ev[2 * w + 1]));
-            walk += ms;
-        }
         info->walk_ms = walk;
     }
     return cudaSuccess;
-#undef XSW_CHECK
 }
+#undef XSW_CHECK
 
 } // namespace xsd
