@@ -486,8 +486,18 @@ __global__ void __launch_bounds__(kBlock) wave_event(const __grid_constant__ Tra
     const WaveRays& R = A.R;
     uint32_t c_int = 0;
     const int lane = threadIdx.x & 31;
-    // events differ a lot in cost (escape vs. Compton / Rayleigh sampling):
-    // warps fetch 32 at a time from a counter instead of a fixed stride
+    const unsigned lt_mask = (1u << lane) - 1u;
+    // Escapes (no interaction) are cheap and run where they are found; the
+    // interactions are gathered per warp and run 32 at a time, so the long
+    // sampling code executes with full warps.
+    __shared__ uint32_t hits[kBlock / 32][64];
+    uint32_t* hb = hits[threadIdx.x >> 5];
+    uint32_t nb = 0; // warp-uniform
+    auto interact = [&](uint32_t i) {
+        const int s = (int)in.free[i - n_s];
+        history_event<FMT>(P, B, qs, s, true, R.res[i], R.res_vox[i], R.res_vox[R.cap + i],
+                           R.res_vox[2ull * R.cap + i], var_base_of(P, s), P.status);
+    };
     for (;;) {
         uint32_t base = 0;
         if (lane == 0)
@@ -496,14 +506,28 @@ __global__ void __launch_bounds__(kBlock) wave_event(const __grid_constant__ Tra
         if (base >= n)
             break;
         const uint32_t i = base + (uint32_t)lane;
-        if (i < n) {
+        const bool valid = i < n;
+        const bool hit = valid && R.res_hit[i] != 0;
+        if (valid && !hit) {
             const int s = (int)in.free[i - n_s];
-            const bool hit = R.res_hit[i] != 0;
-            c_int += hit;
-            history_event<FMT>(P, B, qs, s, hit, R.res[i], R.res_vox[i], R.res_vox[R.cap + i],
-                               R.res_vox[2ull * R.cap + i], var_base_of(P, s), P.status);
+            history_event<FMT>(P, B, qs, s, false, 0.0, 0, 0, 0, var_base_of(P, s), P.status);
         }
+        const unsigned hm = __ballot_sync(kFull, hit);
+        if (hit)
+            hb[nb + __popc(hm & lt_mask)] = i;
+        nb += __popc(hm);
+        c_int += hit;
+        __syncwarp();
+        if (nb >= 32) {
+            const uint32_t j = hb[nb - 32 + lane];
+            __syncwarp();
+            nb -= 32;
+            interact(j);
+        }
+        __syncwarp();
     }
+    if ((uint32_t)lane < nb)
+        interact(hb[lane]);
     if (c_int)
         atomicAdd(B.diag + 4, (unsigned long long)c_int);
     flush_stats(P, B);
