@@ -348,7 +348,12 @@ int xs_ctx_synchronize(xs_context* ctx);
  *                 kernels over global queues); 0: persistent megakernel.
  *                 Both give bit-identical results.  step_voxels > 1
  *                 (REF's march mode) always runs the megakernel
- *   "wave_slots"  histories in flight in the wavefront engine (2^20)       */
+ *   "wave_slots"  histories in flight in the wavefront engine (2^20)
+ *   "wave_pipes"  concurrent wavefront pipelines on their own streams (2)
+ *   "compact_palette" 1: 4-bit voxel palette for <= 8 (material, density)
+ *                 pairs (half the bytes); 0 (default): 8-bit palette, which
+ *                 leaves room for more uniform-block levels.  Applies to the
+ *                 next xs_upload_phantom                                     */
 int xs_ctx_set_option(xs_context* ctx, const char* key, int64_t value);
 
 /* Scene upload: REF passes the phantom and response by const& to every

@@ -184,6 +184,8 @@ struct xs_context {
     int engine = 1;                  // 0: megakernel (transport.cu), 1: wavefront (wavefront.cu)
     std::vector<int> lvl_edges2{4, 8, 32}; // uniform-block edges with two level bits (C3 sweep: best of 7 sets)
     int lvl_edge1 = 8;                      // ... with one level bit
+    std::vector<int> lvl_edges3{4, 8, 16, 32, 64, 128, 256}; // ... with three (8-bit palette)
+    bool compact_palette = false;           // 4-bit palette for <= 8 pairs (half the bytes, fewer level bits)
     uint32_t wave_slots = 1u << 20;  // live histories of the wavefront engine
     int wave_pipes = 2;              // concurrent wavefront pipelines (streams)
     xsd::WaveEngine* wave = nullptr;
@@ -425,7 +427,7 @@ void encode_phantom(const xs_phantom& ph, int fmt, const std::vector<PairKey>& p
         t.join();
 }
 
-// Level marking for uniform blocks (see Grid::lvl_masks).  Bottom-up
+// Level marking for uniform blocks (see Grid::lvl_log2).  Bottom-up
 // uniformity over aligned blocks of each edge in `edges` (ascending powers of
 // two >= 4), then every brick of a uniform block (largest level first) is
 // rewritten with code | level << lvl_shift.
@@ -876,6 +878,8 @@ int xs_ctx_create(int32_t device, xs_context** out)
             if (!v.empty() && v.size() <= 3)
                 c->lvl_edges2 = v;
         }
+        if (const char* e = std::getenv("XSCAT_P4"))
+            c->compact_palette = std::atoi(e) != 0;
         if (const char* e = std::getenv("XSCAT_ENGINE"))
             c->engine = std::atoi(e) != 0;
         if (const char* e = std::getenv("XSCAT_WAVE_PIPES"))
@@ -935,6 +939,8 @@ int xs_ctx_set_option(xs_context* c, const char* key, int64_t value)
             c->grab = (int)std::max<int64_t>(1, value);
         } else if (k == "engine") {
             c->engine = value != 0;
+        } else if (k == "compact_palette") {
+            c->compact_palette = value != 0;
         } else if (k == "wave_pipes") {
             c->wave_pipes = (int)std::max<int64_t>(1, std::min<int64_t>(2, value));
         } else if (k == "wave_slots") {
@@ -974,7 +980,10 @@ int xs_upload_phantom(xs_context* c, const xs_phantom* ph)
             fail(XS_E_RUNTIME, "%s", scan.bad_msg.c_str());
 
         const int n_pairs = (int)scan.pairs.size();
-        const int fmt = n_pairs <= 8 ? xsd::kFmtP4 : (n_pairs <= 255 ? xsd::kFmtP8 : xsd::kFmtRaw);
+        // 8-bit palette by default: room for three uniform-block level bits
+        // (C3: -11% walker iterations, +6% throughput against the 4-bit one)
+        const int fmt = (n_pairs <= 8 && c->compact_palette) ? xsd::kFmtP4
+                                                              : (n_pairs <= 255 ? xsd::kFmtP8 : xsd::kFmtRaw);
         xsd::Grid G{};
         G.nx = ph->dims[0];
         G.ny = ph->dims[1];
@@ -1011,21 +1020,29 @@ int xs_upload_phantom(xs_context* c, const xs_phantom* ph)
         // one step.  Block edges: 4 (a brick) and up, powers of two.
         G.ubit = 0;
         G.lvl_shift = 0;
-        G.lvl_masks = 0;
+        G.lvl_log2 = 0;
         {
-            int lvl_bits = 0;
-            if ((fmt == xsd::kFmtP4 && n_pairs <= 4) || (fmt == xsd::kFmtP8 && n_pairs <= 64))
-                lvl_bits = 2;
-            else if ((fmt == xsd::kFmtP4 && n_pairs <= 8) || (fmt == xsd::kFmtP8 && n_pairs <= 128))
-                lvl_bits = 1;
-            std::vector<int> edges = lvl_bits == 2 ? c->lvl_edges2 : std::vector<int>{c->lvl_edge1};
-            if (lvl_bits == 0)
-                edges.clear();
-            const int code_bits = fmt == xsd::kFmtP4 ? 4 - lvl_bits : 8 - lvl_bits;
+            int need = 0; // bits of the palette index
+            while ((1 << need) < n_pairs)
+                ++need;
+            const int width = fmt == xsd::kFmtP4 ? 4 : (fmt == xsd::kFmtP8 ? 8 : 0);
+            const int lvl_bits = std::max(0, std::min(3, width - need));
+            std::vector<int> edges;
+            if (lvl_bits == 1)
+                edges = {c->lvl_edge1};
+            else if (lvl_bits == 2)
+                edges = c->lvl_edges2;
+            else if (lvl_bits == 3)
+                edges = c->lvl_edges3;
+            const int code_bits = width - lvl_bits;
             G.lvl_shift = code_bits;
             G.ubit = lvl_bits ? (((1 << lvl_bits) - 1) << code_bits) : 0;
-            for (size_t l = 0; l < edges.size(); ++l)
-                G.lvl_masks |= (uint32_t)(edges[l] - 1) << (8 * (l + 1));
+            for (size_t l = 0; l < edges.size(); ++l) {
+                int lg = 0;
+                while ((1 << lg) < edges[l])
+                    ++lg;
+                G.lvl_log2 |= (uint32_t)lg << (4 * (l + 1));
+            }
             if (!edges.empty())
                 mark_uniform_blocks(G, fmt, c->pin_vox.p, edges);
         }

@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(kBlock, XSD_MIN_BLOCKS) transport_kernel(const
 }
 
 // ----------------------------------------------------------------- launchers
-static bool use_reg(const TransportParams& P) { return P.G.fmt == kFmtP4 && P.n_pal <= 4; }
+static bool use_reg(const TransportParams& P) { return (P.G.fmt == kFmtP4 || P.G.fmt == kFmtP8) && P.n_pal <= 4; }
 
 size_t transport_smem_bytes(const TransportParams& P)
 {
@@ -327,8 +327,11 @@ static TransportFn kernel_for(const TransportParams& P)
             return skip ? transport_kernel<kFmtP4, true, true> : transport_kernel<kFmtP4, true, false>;
         return skip ? transport_kernel<kFmtP4, false, true> : transport_kernel<kFmtP4, false, false>;
     }
-    if (P.G.fmt == kFmtP8)
+    if (P.G.fmt == kFmtP8) {
+        if (use_reg(P))
+            return skip ? transport_kernel<kFmtP8, true, true> : transport_kernel<kFmtP8, true, false>;
         return skip ? transport_kernel<kFmtP8, false, true> : transport_kernel<kFmtP8, false, false>;
+    }
     return transport_kernel<kFmtRaw, false, false>;
 }
 

@@ -124,7 +124,7 @@ __device__ __forceinline__ void rng_skip(SlotRng& r, uint32_t n, uint32_t k0, ui
 
 // ----------------------------------------------------------------- mu table
 // Linear attenuation lookup for the current ray's energy.  REG: <= 4 palette
-// entries held in registers (4-bit palette); otherwise a per-lane table in
+// entries held in registers (4- or 8-bit palette); otherwise a per-lane table in
 // shared memory: palette entries (P4) or mass attenuation per material
 // (P8 / raw, multiplied by the voxel density at lookup).  Values are the
 // products REF MuField forms (trace.cpp:10-20).
@@ -178,7 +178,7 @@ struct MuTab {
     __device__ __noinline__ void fill(const TransportParams& P, double e, DevStatus* st, int bin)
     {
         energy = e;
-        if (FMT == kFmtP4) {
+        if (FMT == kFmtP4 || REG) { // per palette entry (REG: <= 4 entries, either palette width)
             double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3_ = 0.0;
             if (!REG)
                 for (int c = 0; c < P.n_pal; ++c)
@@ -222,14 +222,13 @@ struct MuTab {
 
     __device__ __forceinline__ double mu(const TransportParams& P, int code, float dens) const
     {
-        if (FMT == kFmtP4) {
-            if (REG) {
-                const double lo = (code & 1) ? t1 : t0;
-                const double hi = (code & 1) ? t3 : t2;
-                return (code & 2) ? hi : lo;
-            }
-            return T[code * kBlock];
+        if (REG) {
+            const double lo = (code & 1) ? t1 : t0;
+            const double hi = (code & 1) ? t3 : t2;
+            return (code & 2) ? hi : lo;
         }
+        if (FMT == kFmtP4)
+            return T[code * kBlock];
         if (FMT == kFmtP8)
             return T[P.pal_mat[code] * kBlock] * (double)P.pal_dens[code];
         return T[code * kBlock] * (double)dens;
@@ -427,7 +426,7 @@ __device__ __forceinline__ bool walk_step(const TransportParams& P, const MuTab<
         // uniform and mixed cells do not diverge.
         const int c = code & ~G.ubit;
         // k* = boundaries left inside the voxel's uniform block (0 outside)
-        const int um = (int)((G.lvl_masks >> (((uint32_t)code >> G.lvl_shift) << 3)) & 0xFFu);
+        const int um = (1 << ((G.lvl_log2 >> (((uint32_t)code >> G.lvl_shift) << 2)) & 0xFu)) - 1;
         const int kx = (w.sx > 0 ? ~w.ix : w.ix) & um;
         const int ky = (w.sy > 0 ? ~w.iy : w.iy) & um;
         const int kz = (w.sz > 0 ? ~w.iz : w.iz) & um;

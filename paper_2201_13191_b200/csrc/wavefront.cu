@@ -588,7 +588,7 @@ __global__ void wave_init(WaveCtl* ctl, uint32_t* stack, uint32_t n_slots, unsig
     }
 }
 
-bool use_reg_w(const TransportParams& P) { return P.G.fmt == kFmtP4 && P.n_pal <= 4; }
+bool use_reg_w(const TransportParams& P) { return (P.G.fmt == kFmtP4 || P.G.fmt == kFmtP8) && P.n_pal <= 4; }
 
 typedef void (*WaveFn)(const TransportParams, const WaveArgs);
 
@@ -610,8 +610,11 @@ WaveSet wave_kernels_for(const TransportParams& P)
             return skip ? wave_set<kFmtP4, true, true>() : wave_set<kFmtP4, true, false>();
         return skip ? wave_set<kFmtP4, false, true>() : wave_set<kFmtP4, false, false>();
     }
-    if (P.G.fmt == kFmtP8)
+    if (P.G.fmt == kFmtP8) {
+        if (use_reg_w(P))
+            return skip ? wave_set<kFmtP8, true, true>() : wave_set<kFmtP8, true, false>();
         return skip ? wave_set<kFmtP8, false, true>() : wave_set<kFmtP8, false, false>();
+    }
     return wave_set<kFmtRaw, false, false>();
 }
 

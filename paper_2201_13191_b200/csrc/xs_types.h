@@ -36,14 +36,13 @@ struct Grid {
     int32_t fmt;
     int32_t n_codes;      // palette size (P4/P8)
     // Uniform-block level in the palette codes: the bits above the palette
-    // index (ubit = their mask, lvl_shift = their position) give the level of
-    // the largest aligned uniform block (all voxels the same code) holding the
-    // voxel; byte l of lvl_masks is that block's edge - 1 (0: not uniform).
-    // P4 <= 4 entries / P8 <= 64: two level bits; P4 <= 8 / P8 <= 128: one;
-    // otherwise none (ubit = 0).
+    // index (ubit = their mask, lvl_shift = their position; up to three)
+    // give the level of the largest aligned uniform block (all voxels the
+    // same code) holding the voxel; nibble l of lvl_log2 is log2 of that
+    // block's edge (level 0: not uniform, edge 1).
     int32_t ubit;
     int32_t lvl_shift;
-    uint32_t lvl_masks;
+    uint32_t lvl_log2;
     int32_t pad_;
 };
 

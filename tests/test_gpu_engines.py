@@ -42,16 +42,17 @@ def _format_of(stats):
     return {0: "p4", 1: "p8", 2: "raw"}.get(stats["voxel_format"], stats["voxel_format"])
 
 
-@pytest.mark.parametrize("kind", ["p4reg", "p4", "p8", "raw"])
+@pytest.mark.parametrize("kind", ["p4reg", "p4", "p8reg", "p8", "raw"])
 @pytest.mark.parametrize("exact", [0, 1])
 def test_wavefront_equals_megakernel_bitwise(orc, kind, exact):
-    ph = _phantom(kind)
+    ph = _phantom(kind.replace("p8reg", "p4reg"))
     g = I.make_circular_geometry(100.0, 60.0, 32, 24, 0.8, 4)
     spec, resp = I.kramers_spectrum(150.0), I.detector_response()
     cfg = I.SimConfig(photons_total=20000, splitting=5, seed=31337, roulette_wmin_rel=2.0,
                       roulette_survival=0.6, track_variance=True)
     ctx = X.projector.Context(0)
     ctx.set_option("exact_walk", exact)
+    ctx.set_option("compact_palette", 1 if kind.startswith("p4") else 0)
     proj = X.Projector(ph, resp, ctx=ctx)
     out = {}
     for engine in (0, 1):
@@ -60,7 +61,7 @@ def test_wavefront_equals_megakernel_bitwise(orc, kind, exact):
         assert out[engine].stats["engine"] == engine
     a, b = out[0], out[1]
     fmt = _format_of(b.stats)
-    want = {"p4reg": "p4", "p4": "p4", "p8": "p8", "raw": "raw"}[kind]
+    want = {"p4reg": "p4", "p4": "p4", "p8reg": "p8", "p8": "p8", "raw": "raw"}[kind]
     assert fmt == want, (kind, b.stats["voxel_format"], b.stats["palette_size"])
     assert np.array_equal(a.image, b.image)
     assert np.array_equal(a.variance, b.variance)
