@@ -26,6 +26,9 @@ int transport_pick_slots(TransportParams& P, int max_slots, size_t budget);
 cudaError_t transport_prepare(const TransportParams& P, size_t smem, int* blocks_per_sm);
 cudaError_t launch_transport(const TransportParams& P, int grid, size_t smem, cudaStream_t s);
 cudaError_t launch_primary(const PrimaryParams& P, cudaStream_t s);
+size_t levels_scratch_bytes(const Grid& G, const int* edges, int n_levels);
+cudaError_t launch_mark_levels(uint8_t* vox, const Grid& G, int fmt, const int* edges, int n_levels,
+                               void* scratch, int sm_count, cudaStream_t s);
 struct WaveEngine;
 WaveEngine* wave_create();
 void wave_destroy(WaveEngine* e);
@@ -175,6 +178,7 @@ struct xs_context {
     DevBuf<double> var_val;
     DevBuf<double> img, var, pp_a, pp_b, pp_c, pp_k;
     DevBuf<xsd::InterpEntry> interp_tab;
+    DevBuf<uint8_t> lvl_scratch;
     int smem_kb = 48; // per transport block: 4 blocks/SM leave 60 KB of L1
     int max_slots = 64;
     int macro_skip = 1;
@@ -425,90 +429,6 @@ void encode_phantom(const xs_phantom& ph, int fmt, const std::vector<PairKey>& p
         });
     for (auto& t : th)
         t.join();
-}
-
-// Level marking for uniform blocks (see Grid::lvl_log2).  Bottom-up
-// uniformity over aligned blocks of each edge in `edges` (ascending powers of
-// two >= 4), then every brick of a uniform block (largest level first) is
-// rewritten with code | level << lvl_shift.
-void mark_uniform_blocks(const xsd::Grid& G, int fmt, uint8_t* vox, const std::vector<int>& edges)
-{
-    const size_t bb = fmt == xsd::kFmtP4 ? 32 : 64;
-    const int nbx = G.nbx, nby = G.nby, nbz = G.nbz;
-    auto brick_ptr = [&](size_t bx, size_t by, size_t bz) {
-        return vox + (bx + (size_t)nbx * (by + (size_t)nby * bz)) * bb;
-    };
-    // uniform code of every brick (4^3, wholly inside the grid) or -1
-    std::vector<int16_t> cur((size_t)nbx * nby * nbz);
-    for (int bz = 0; bz < nbz; ++bz)
-        for (int by = 0; by < nby; ++by)
-            for (int bx = 0; bx < nbx; ++bx) {
-                const uint8_t* b = brick_ptr(bx, by, bz);
-                int code = -1;
-                if (4 * bx + 4 <= G.nx && 4 * by + 4 <= G.ny && 4 * bz + 4 <= G.nz) {
-                    bool same = true;
-                    for (size_t i = 1; i < bb && same; ++i)
-                        same = b[i] == b[0];
-                    if (same)
-                        code = fmt == xsd::kFmtP4 ? ((b[0] & 0xF) == (b[0] >> 4) ? (b[0] & 0xF) : -1) : b[0];
-                }
-                cur[bx + (size_t)nbx * (by + (size_t)nby * bz)] = (int16_t)code;
-            }
-    // per level: uniform code of each aligned block of that edge (in bricks)
-    std::vector<std::vector<int16_t>> lv(edges.size());
-    std::vector<int> nb(edges.size() * 3);
-    int prev_edge = 4;
-    std::vector<int16_t> prev = cur;
-    int pnx = nbx, pny = nby, pnz = nbz;
-    for (size_t l = 0; l < edges.size(); ++l) {
-        const int f = edges[l] / prev_edge; // children per axis
-        const int qx = (pnx + f - 1) / f, qy = (pny + f - 1) / f, qz = (pnz + f - 1) / f;
-        std::vector<int16_t> nxt((size_t)qx * qy * qz, (int16_t)-1);
-        for (int z = 0; z < qz; ++z)
-            for (int y = 0; y < qy; ++y)
-                for (int x = 0; x < qx; ++x) {
-                    int code = -2;
-                    for (int k = 0; k < f * f * f && code != -1; ++k) {
-                        const int cx = x * f + k % f, cy = y * f + (k / f) % f, cz = z * f + k / (f * f);
-                        const int cc = (cx < pnx && cy < pny && cz < pnz)
-                                           ? prev[cx + (size_t)pnx * (cy + (size_t)pny * cz)]
-                                           : -1;
-                        code = (cc < 0 || (code >= 0 && cc != code)) ? -1 : cc;
-                    }
-                    nxt[x + (size_t)qx * (y + (size_t)qy * z)] = (int16_t)(code < 0 ? -1 : code);
-                }
-        if (f == 1)
-            nxt = prev;
-        lv[l] = nxt;
-        nb[3 * l] = qx;
-        nb[3 * l + 1] = qy;
-        nb[3 * l + 2] = qz;
-        prev = nxt;
-        pnx = qx;
-        pny = qy;
-        pnz = qz;
-        prev_edge = edges[l];
-    }
-    // rewrite bricks: each brick takes the largest uniform level containing it
-    for (int bz = 0; bz < nbz; ++bz)
-        for (int by = 0; by < nby; ++by)
-            for (int bx = 0; bx < nbx; ++bx) {
-                int level = 0, code = -1;
-                for (int l = (int)edges.size() - 1; l >= 0 && level == 0; --l) {
-                    const int e = edges[l] / 4; // edge in bricks
-                    const int x = bx / e, y = by / e, z = bz / e;
-                    const int cc = lv[l][x + (size_t)nb[3 * l] * (y + (size_t)nb[3 * l + 1] * z)];
-                    if (cc >= 0) {
-                        level = l + 1;
-                        code = cc;
-                    }
-                }
-                if (!level)
-                    continue;
-                const int f = code | (level << G.lvl_shift);
-                const uint8_t byte = fmt == xsd::kFmtP4 ? (uint8_t)(f | (f << 4)) : (uint8_t)f;
-                std::memset(brick_ptr(bx, by, bz), byte, bb);
-            }
 }
 
 // --------------------------------------------------------- scatter launch
@@ -910,6 +830,7 @@ void xs_ctx_destroy(xs_context* c)
     c->status.release();
     c->var_pix.release();
     c->interp_tab.release();
+    c->lvl_scratch.release();
     xsd::wave_destroy(c->wave);
     if (c->ev0)
         cudaEventDestroy(c->ev0);
@@ -975,7 +896,12 @@ int xs_upload_phantom(xs_context* c, const xs_phantom* ph)
         for (int m = 1; m < ph->n_materials; ++m)
             has_tables[m] = ph->materials[m].mu.n > 0;
         ScanResult scan;
+        const bool timing = std::getenv("XSCAT_TIMING") != nullptr;
+        auto now = [] { return std::chrono::steady_clock::now(); };
+        auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+        const auto t0 = now();
         scan_phantom(*ph, has_tables, scan);
+        const auto t1 = now();
         if (scan.first_bad != SIZE_MAX)
             fail(XS_E_RUNTIME, "%s", scan.bad_msg.c_str());
 
@@ -1013,6 +939,7 @@ int xs_upload_phantom(xs_context* c, const xs_phantom* ph)
         c->pin_vox.reserve(vox_bytes);
         c->pin_dens.reserve(std::max<size_t>(dens_count, 1));
         encode_phantom(*ph, fmt, scan.pairs, c->pin_vox.p, c->pin_dens.p, G.nbx, G.nby, G.nbz);
+        const auto t2 = now();
 
         // Uniform blocks: every voxel of an aligned uniform block (all voxels
         // the same code, wholly inside the grid) carries the level of the
@@ -1021,6 +948,7 @@ int xs_upload_phantom(xs_context* c, const xs_phantom* ph)
         G.ubit = 0;
         G.lvl_shift = 0;
         G.lvl_log2 = 0;
+        std::vector<int> lvl_edges;
         {
             int need = 0; // bits of the palette index
             while ((1 << need) < n_pairs)
@@ -1043,8 +971,7 @@ int xs_upload_phantom(xs_context* c, const xs_phantom* ph)
                     ++lg;
                 G.lvl_log2 |= (uint32_t)lg << (4 * (l + 1));
             }
-            if (!edges.empty())
-                mark_uniform_blocks(G, fmt, c->pin_vox.p, edges);
+            lvl_edges = edges;
         }
 
         c->n_pal = fmt == xsd::kFmtRaw ? 0 : n_pairs;
@@ -1063,8 +990,17 @@ int xs_upload_phantom(xs_context* c, const xs_phantom* ph)
                                        c->stream),
                        "upload densities");
         }
+        if (!lvl_edges.empty()) { // uniform-block levels, on the device (levels.cu)
+            c->lvl_scratch.reserve(xsd::levels_scratch_bytes(G, lvl_edges.data(), (int)lvl_edges.size()));
+            cuda_check(xsd::launch_mark_levels(c->vox.p, G, fmt, lvl_edges.data(), (int)lvl_edges.size(),
+                                               c->lvl_scratch.p, c->sm_count, c->stream),
+                       "uniform-block levels");
+        }
         c->last_upload_bytes = vox_bytes + dens_count * 4;
         cuda_check(cudaStreamSynchronize(c->stream), "upload phantom");
+        if (timing)
+            std::fprintf(stderr, "[xscat] upload: scan %.1f ms, encode %.1f ms, levels+H2D %.1f ms\n", ms(t0, t1),
+                         ms(t1, t2), ms(t2, now()));
         G.vox = c->vox.p;
         G.dens = fmt == xsd::kFmtRaw ? c->dens.p : nullptr;
         c->grid = G;

@@ -1,0 +1,144 @@
+// levels.cu — uniform-block levels of the device voxel grid (see
+// Grid::lvl_log2 in xs_types.h), computed on the device right after the
+// encoded grid is uploaded.
+//
+// A voxel carries the level of the largest aligned block (edges `edges[l]`,
+// powers of two >= 4 voxels = one brick) that lies wholly inside the grid and
+// holds a single palette code.  Three passes, all over bricks or blocks, not
+// voxels: brick codes, block codes per level (bottom-up), then every brick of
+// a uniform block is rewritten with code | level << lvl_shift.  The result is
+// byte-identical to the host marking it replaces (capi.cu keeps that one as
+// the documented reference of the encoding).
+#include <cstdint>
+
+#include "xs_types.h"
+
+namespace xsd {
+
+namespace {
+
+// uniform code of a brick wholly inside the grid, else -1
+__global__ void brick_codes(const uint8_t* __restrict__ vox, Grid G, int bb, int16_t* __restrict__ out)
+{
+    const uint64_t n = (uint64_t)G.nbx * G.nby * G.nbz;
+    for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < n; b += (uint64_t)gridDim.x * blockDim.x) {
+        const int bx = (int)(b % G.nbx), by = (int)((b / G.nbx) % G.nby), bz = (int)(b / ((uint64_t)G.nbx * G.nby));
+        int code = -1;
+        if (4 * bx + 4 <= G.nx && 4 * by + 4 <= G.ny && 4 * bz + 4 <= G.nz) {
+            const uint32_t* w = reinterpret_cast<const uint32_t*>(vox + b * bb);
+            const uint32_t w0 = w[0];
+            bool same = true;
+            for (int i = 1; i < bb / 4; ++i)
+                same &= w[i] == w0;
+            same &= (w0 & 0xFFu) == ((w0 >> 8) & 0xFFu) && (w0 & 0xFFu) == ((w0 >> 16) & 0xFFu) &&
+                    (w0 & 0xFFu) == (w0 >> 24);
+            const int b0 = (int)(w0 & 0xFFu);
+            if (same)
+                code = bb == 32 ? ((b0 & 0xF) == (b0 >> 4) ? (b0 & 0xF) : -1) : b0;
+        }
+        out[b] = (int16_t)code;
+    }
+}
+
+// uniform code of each block of f^3 children (or -1)
+__global__ void block_codes(const int16_t* __restrict__ child, int cnx, int cny, int cnz, int f,
+                            int16_t* __restrict__ out, int qx, int qy, int qz)
+{
+    const uint64_t n = (uint64_t)qx * qy * qz;
+    for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < n; q += (uint64_t)gridDim.x * blockDim.x) {
+        const int x = (int)(q % qx), y = (int)((q / qx) % qy), z = (int)(q / ((uint64_t)qx * qy));
+        int code = -2;
+        for (int k = 0; k < f * f * f && code != -1; ++k) {
+            const int cx = x * f + k % f, cy = y * f + (k / f) % f, cz = z * f + k / (f * f);
+            const int cc = (cx < cnx && cy < cny && cz < cnz) ? child[cx + (size_t)cnx * (cy + (size_t)cny * cz)] : -1;
+            code = (cc < 0 || (code >= 0 && cc != code)) ? -1 : cc;
+        }
+        out[q] = (int16_t)(code < 0 ? -1 : code);
+    }
+}
+
+struct LevelTabs {
+    const int16_t* code[8];
+    int nx[8], ny[8];
+    int edge_b[8]; // block edge in bricks
+    int n;
+};
+
+__global__ void rewrite_bricks(uint8_t* __restrict__ vox, Grid G, int bb, LevelTabs L)
+{
+    const uint64_t n = (uint64_t)G.nbx * G.nby * G.nbz;
+    for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < n; b += (uint64_t)gridDim.x * blockDim.x) {
+        const int bx = (int)(b % G.nbx), by = (int)((b / G.nbx) % G.nby), bz = (int)(b / ((uint64_t)G.nbx * G.nby));
+        int level = 0, code = -1;
+        for (int l = L.n - 1; l >= 0 && level == 0; --l) {
+            const int e = L.edge_b[l];
+            const int cc = L.code[l][bx / e + (size_t)L.nx[l] * (by / e + (size_t)L.ny[l] * (bz / e))];
+            if (cc >= 0) {
+                level = l + 1;
+                code = cc;
+            }
+        }
+        if (!level)
+            continue;
+        const int f = code | (level << G.lvl_shift);
+        const uint32_t byte = bb == 32 ? (uint32_t)((f | (f << 4)) & 0xFF) : (uint32_t)(f & 0xFF);
+        const uint32_t word = byte * 0x01010101u;
+        uint32_t* w = reinterpret_cast<uint32_t*>(vox + b * bb);
+        for (int i = 0; i < bb / 4; ++i)
+            w[i] = word;
+    }
+}
+
+} // namespace
+
+// scratch: int16 per brick plus the (smaller) level tables; returns the
+// bytes needed when scratch == nullptr
+size_t levels_scratch_bytes(const Grid& G, const int* edges, int n_levels)
+{
+    size_t total = (size_t)G.nbx * G.nby * G.nbz;
+    int px = G.nbx, py = G.nby, pz = G.nbz, prev = 4;
+    for (int l = 0; l < n_levels; ++l) {
+        const int f = edges[l] / prev;
+        px = (px + f - 1) / f;
+        py = (py + f - 1) / f;
+        pz = (pz + f - 1) / f;
+        total += (size_t)px * py * pz;
+        prev = edges[l];
+    }
+    return total * sizeof(int16_t) + 256;
+}
+
+cudaError_t launch_mark_levels(uint8_t* vox, const Grid& G, int fmt, const int* edges, int n_levels,
+                               void* scratch, int sm_count, cudaStream_t s)
+{
+    if (n_levels <= 0)
+        return cudaSuccess;
+    const int bb = fmt == kFmtP4 ? 32 : 64;
+    const int grid = sm_count * 8, block = 256;
+    int16_t* bricks = static_cast<int16_t*>(scratch);
+    brick_codes<<<grid, block, 0, s>>>(vox, G, bb, bricks);
+    LevelTabs L{};
+    L.n = n_levels;
+    const int16_t* prev = bricks;
+    int px = G.nbx, py = G.nby, pz = G.nbz, pe = 4;
+    int16_t* next = bricks + (size_t)G.nbx * G.nby * G.nbz;
+    for (int l = 0; l < n_levels; ++l) {
+        const int f = edges[l] / pe;
+        const int qx = (px + f - 1) / f, qy = (py + f - 1) / f, qz = (pz + f - 1) / f;
+        block_codes<<<grid, block, 0, s>>>(prev, px, py, pz, f, next, qx, qy, qz);
+        L.code[l] = next;
+        L.nx[l] = qx;
+        L.ny[l] = qy;
+        L.edge_b[l] = edges[l] / 4;
+        prev = next;
+        next += (size_t)qx * qy * qz;
+        px = qx;
+        py = qy;
+        pz = qz;
+        pe = edges[l];
+    }
+    rewrite_bricks<<<grid, block, 0, s>>>(vox, G, bb, L);
+    return cudaGetLastError();
+}
+
+} // namespace xsd
