@@ -188,7 +188,7 @@ struct xs_context {
     int engine = 1;                  // 0: megakernel (transport.cu), 1: wavefront (wavefront.cu)
     std::vector<int> lvl_edges2{4, 8, 32}; // uniform-block edges with two level bits (C3 sweep: best of 7 sets)
     int lvl_edge1 = 8;                      // ... with one level bit
-    std::vector<int> lvl_edges3{4, 8, 16, 32, 64, 128, 256}; // ... with three (8-bit palette)
+    std::vector<int> lvl_edges3{2, 4, 8, 16, 32, 64, 128}; // ... with three (8-bit palette; edge 2 = 2^3 sub-blocks of mixed bricks)
     bool compact_palette = false;           // 4-bit palette for <= 8 pairs (half the bytes, fewer level bits)
     uint32_t wave_slots = 1u << 20;  // live histories of the wavefront engine
     int wave_pipes = 2;              // concurrent wavefront pipelines (streams)
@@ -788,7 +788,7 @@ int xs_ctx_create(int32_t device, xs_context** out)
             std::vector<int> v;
             for (const char* q = e; *q;) {
                 const int x = std::atoi(q);
-                if (x >= 4 && x <= 128 && (x & (x - 1)) == 0)
+                if (x >= 2 && x <= 256 && (x & (x - 1)) == 0)
                     v.push_back(x);
                 while (*q && *q != ',')
                     ++q;
@@ -797,6 +797,8 @@ int xs_ctx_create(int32_t device, xs_context** out)
             }
             if (!v.empty() && v.size() <= 3)
                 c->lvl_edges2 = v;
+            else if (v.size() <= 7)
+                c->lvl_edges3 = v;
         }
         if (const char* e = std::getenv("XSCAT_P4"))
             c->compact_palette = std::atoi(e) != 0;

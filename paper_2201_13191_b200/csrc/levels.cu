@@ -3,12 +3,11 @@
 // encoded grid is uploaded.
 //
 // A voxel carries the level of the largest aligned block (edges `edges[l]`,
-// powers of two >= 4 voxels = one brick) that lies wholly inside the grid and
-// holds a single palette code.  Three passes, all over bricks or blocks, not
-// voxels: brick codes, block codes per level (bottom-up), then every brick of
-// a uniform block is rewritten with code | level << lvl_shift.  The result is
-// byte-identical to the host marking it replaces (capi.cu keeps that one as
-// the documented reference of the encoding).
+// powers of two) that lies wholly inside the grid and holds a single palette
+// code.  Passes over bricks or blocks, not voxels: brick codes, block codes
+// per level (bottom-up), then every brick of a uniform block is rewritten
+// with code | level << lvl_shift; an edge-2 level, if requested, marks the
+// uniform 2x2x2 sub-blocks of the remaining (mixed) bricks.
 #include <cstdint>
 
 #include "xs_types.h"
@@ -62,6 +61,7 @@ struct LevelTabs {
     int nx[8], ny[8];
     int edge_b[8]; // block edge in bricks
     int n;
+    int lvl0; // level number of edges[0] is lvl0 + 1
 };
 
 __global__ void rewrite_bricks(uint8_t* __restrict__ vox, Grid G, int bb, LevelTabs L)
@@ -74,7 +74,7 @@ __global__ void rewrite_bricks(uint8_t* __restrict__ vox, Grid G, int bb, LevelT
             const int e = L.edge_b[l];
             const int cc = L.code[l][bx / e + (size_t)L.nx[l] * (by / e + (size_t)L.ny[l] * (bz / e))];
             if (cc >= 0) {
-                level = l + 1;
+                level = l + 1 + L.lvl0;
                 code = cc;
             }
         }
@@ -89,12 +89,56 @@ __global__ void rewrite_bricks(uint8_t* __restrict__ vox, Grid G, int bb, LevelT
     }
 }
 
+// Edge-2 level inside mixed bricks: each uniform 2x2x2 sub-block of a brick
+// that carries no larger level gets level `lvl` (voxel granularity; cell
+// index inside a brick = x | y << 2 | z << 4).
+__global__ void mark_subbricks(uint8_t* __restrict__ vox, Grid G, int bb, int lvl)
+{
+    const uint64_t n = (uint64_t)G.nbx * G.nby * G.nbz;
+    const uint32_t lmask = (uint32_t)G.ubit;
+    for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < n; b += (uint64_t)gridDim.x * blockDim.x) {
+        const int bx = (int)(b % G.nbx), by = (int)((b / G.nbx) % G.nby), bz = (int)(b / ((uint64_t)G.nbx * G.nby));
+        uint8_t* p = vox + b * bb;
+        auto get = [&](int c) -> uint32_t {
+            return bb == 32 ? (uint32_t)((p[c >> 1] >> ((c & 1) * 4)) & 0xF) : (uint32_t)p[c];
+        };
+        if (get(0) & lmask) // the brick is inside a larger uniform block
+            continue;
+        for (int sb = 0; sb < 8; ++sb) {
+            const int x0 = 2 * (sb & 1), y0 = 2 * ((sb >> 1) & 1), z0 = 2 * (sb >> 2);
+            if (4 * bx + x0 + 2 > G.nx || 4 * by + y0 + 2 > G.ny || 4 * bz + z0 + 2 > G.nz)
+                continue; // padding voxels beyond the grid
+            const int c0 = x0 | (y0 << 2) | (z0 << 4);
+            const uint32_t code = get(c0);
+            bool same = true;
+            for (int k = 1; k < 8 && same; ++k)
+                same = get(c0 + (k & 1) + ((k >> 1) & 1) * 4 + (k >> 2) * 16) == code;
+            if (!same)
+                continue;
+            const uint32_t f = code | ((uint32_t)lvl << G.lvl_shift);
+            for (int k = 0; k < 8; ++k) {
+                const int c = c0 + (k & 1) + ((k >> 1) & 1) * 4 + (k >> 2) * 16;
+                if (bb == 32) {
+                    const int sh = (c & 1) * 4;
+                    p[c >> 1] = (uint8_t)((p[c >> 1] & ~(0xF << sh)) | (f << sh));
+                } else {
+                    p[c] = (uint8_t)f;
+                }
+            }
+        }
+    }
+}
+
 } // namespace
 
 // scratch: int16 per brick plus the (smaller) level tables; returns the
 // bytes needed when scratch == nullptr
 size_t levels_scratch_bytes(const Grid& G, const int* edges, int n_levels)
 {
+    if (n_levels > 0 && edges[0] == 2) {
+        ++edges;
+        --n_levels;
+    }
     size_t total = (size_t)G.nbx * G.nby * G.nbz;
     int px = G.nbx, py = G.nby, pz = G.nbz, prev = 4;
     for (int l = 0; l < n_levels; ++l) {
@@ -114,6 +158,9 @@ cudaError_t launch_mark_levels(uint8_t* vox, const Grid& G, int fmt, const int* 
     if (n_levels <= 0)
         return cudaSuccess;
     const int bb = fmt == kFmtP4 ? 32 : 64;
+    const int sub = edges[0] == 2 ? 1 : 0; // level 1 = 2x2x2 sub-blocks of mixed bricks
+    edges += sub;
+    n_levels -= sub;
     const int grid = sm_count * 8, block = 256;
     int16_t* bricks = static_cast<int16_t*>(scratch);
     brick_codes<<<grid, block, 0, s>>>(vox, G, bb, bricks);
@@ -130,6 +177,7 @@ cudaError_t launch_mark_levels(uint8_t* vox, const Grid& G, int fmt, const int* 
         L.nx[l] = qx;
         L.ny[l] = qy;
         L.edge_b[l] = edges[l] / 4;
+        L.lvl0 = sub;
         prev = next;
         next += (size_t)qx * qy * qz;
         px = qx;
@@ -137,7 +185,10 @@ cudaError_t launch_mark_levels(uint8_t* vox, const Grid& G, int fmt, const int* 
         pz = qz;
         pe = edges[l];
     }
-    rewrite_bricks<<<grid, block, 0, s>>>(vox, G, bb, L);
+    if (n_levels > 0)
+        rewrite_bricks<<<grid, block, 0, s>>>(vox, G, bb, L);
+    if (sub)
+        mark_subbricks<<<grid, block, 0, s>>>(vox, G, bb, 1);
     return cudaGetLastError();
 }
 

@@ -229,17 +229,7 @@ __global__ void __launch_bounds__(kBlock) wave_setup(const __grid_constant__ Tra
     DevStatus* st = P.status;
     const WaveRays& R = A.R;
     uint32_t c_rays = 0;
-    const int lane = threadIdx.x & 31;
-    for (;;) { // 32 tasks per warp fetch (scoring and free-path set-ups differ in cost)
-        uint32_t base = 0;
-        if (lane == 0)
-            base = atomicAdd(&ctl->setup_cursor, 32u);
-        base = __shfl_sync(kFull, base, 0);
-        if (base >= n)
-            break;
-        const uint32_t i = base + (uint32_t)lane;
-        if (i >= n)
-            continue;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         Walk w;
         w.march = 0;
         bool walking;
