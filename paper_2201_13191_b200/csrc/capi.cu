@@ -186,7 +186,7 @@ struct xs_context {
     xs_launch_stats last{};
     int grab = 64;
     int engine = 1;                  // 0: megakernel (transport.cu), 1: wavefront (wavefront.cu)
-    std::vector<int> lvl_edges2{4, 8, 32}; // uniform-block edges with two level bits (C3 sweep: best of 7 sets)
+    std::vector<int> lvl_edges2{2, 8, 32}; // uniform-block edges with two level bits (C3 sweeps)
     int lvl_edge1 = 8;                      // ... with one level bit
     std::vector<int> lvl_edges3{2, 4, 8, 16, 32, 64, 128}; // ... with three (8-bit palette; edge 2 = 2^3 sub-blocks of mixed bricks)
     bool compact_palette = false;           // 4-bit palette for <= 8 pairs (half the bytes, fewer level bits)
