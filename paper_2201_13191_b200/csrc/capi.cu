@@ -540,6 +540,13 @@ void accumulate(xs_context* c, const xs_geometry& g, int angle, const xs_spectru
         }
         P.shared_mu_grid = first > 0 && same;
         P.grid_mat = first > 0 ? first : 0;
+        // ... and of every energy table (mu, sigma_incoh, sigma_coh, sigma_pe)
+        bool all = P.shared_mu_grid != 0;
+        for (int m = 1; m < c->n_mats && all; ++m)
+            if (!c->mats[m].t[0].x.empty())
+                for (int k = 1; k < 4; ++k)
+                    all = all && c->mats[m].t[k].x == c->mats[first].t[0].x;
+        P.shared_e_grid = all;
     }
     P.march_h = cfg.step_voxels *
                 std::min({c->grid.hx, c->grid.hy, c->grid.hz}); // REF trace.cpp:117

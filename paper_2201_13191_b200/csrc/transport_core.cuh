@@ -136,10 +136,11 @@ struct SharedLog {
     int i;
     bool exact, ok;
     double le;
-    __device__ __forceinline__ void init(const TransportParams& P, double e, DevStatus* st, int bin)
+    __device__ __forceinline__ void init(const TransportParams& P, double e, DevStatus* st, int bin,
+                                         bool enabled = true)
     {
         ok = false;
-        if (!P.shared_mu_grid)
+        if (!P.shared_mu_grid || !enabled)
             return;
         const Tab t = mtab(P, P.mats[P.grid_mat].mu);
         if (!tab_locate(t, e, i, exact)) {
@@ -675,10 +676,13 @@ __device__ __noinline__ void history_event(const TransportParams& P, const Block
     const int mat = material_of<FMT>(P, code & ~P.G.ubit);
     const MatDesc& md = P.mats[mat];
     const double E = S.E;
-    // select_interaction (cross_sections.cpp:81-96)
-    const double pe = loglog_or_fail(P, md.pe, E, st, bin);
-    const double incoh = loglog_or_fail(P, md.incoh, E, st, bin);
-    const double coh = loglog_or_fail(P, md.coh, E, st, bin);
+    // select_interaction (cross_sections.cpp:81-96); one knot search and one
+    // log(E) for the three tables when they share the energy knots
+    SharedLog sl;
+    sl.init(P, E, st, bin, P.shared_e_grid != 0);
+    const double pe = sl.eval(P, md.pe, E, st, bin);
+    const double incoh = sl.eval(P, md.incoh, E, st, bin);
+    const double coh = sl.eval(P, md.coh, E, st, bin);
     const double total = pe + incoh + coh;
     if (!(total > 0.0))
         raise(st, XS_E_RUNTIME, kErrSigmaAll, bin, E, (double)mat);

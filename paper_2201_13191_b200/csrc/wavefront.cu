@@ -812,9 +812,18 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
     if (const char* v = std::getenv("XSCAT_WALK_BPS")) // experiment: walk blocks per SM actually launched
         walk_use = std::max(1, std::min(walk_per_sm, std::atoi(v)));
     const int g_walk = sm_count * walk_use;
-    const int g_work = sm_count * 4;  // admission / events (~120 registers)
-    const int g_setup = sm_count * 8; // <= 64 registers
-    const int g_score = sm_count * 8;
+    // grid-stride kernels: as many resident blocks as fit (they are latency-bound)
+    auto resident = [&](const void* k, size_t smem, int* out) -> cudaError_t {
+        int per = 0;
+        cudaError_t err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, kBlock, smem);
+        *out = sm_count * (per < 1 ? 1 : per);
+        return err;
+    };
+    int g_work = 0, g_setup = 0, g_score = 0, g_admit = 0;
+    XSW_CHECK(resident((const void*)K.event, stat_smem, &g_work));
+    XSW_CHECK(resident((const void*)K.setup, mu_smem, &g_setup));
+    XSW_CHECK(resident((const void*)wave_score, stat_smem, &g_score));
+    XSW_CHECK(resident((const void*)wave_admit, stat_smem, &g_admit));
 
     if (start) // buffers are allocated: the timed region starts here
         XSW_CHECK(cudaEventRecord(start, s));
@@ -840,7 +849,7 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
         w.done = false;
         w.A.cur = 0;
         wave_plan<<<1, 1, 0, ps>>>(w.P, w.A);
-        wave_admit<<<g_work, kBlock, stat_smem, ps>>>(w.P, w.A);
+        wave_admit<<<g_admit, kBlock, stat_smem, ps>>>(w.P, w.A);
         XSW_CHECK(cudaGetLastError());
         launches += 3;
     }
@@ -867,7 +876,7 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
                 K.event<<<g_work, kBlock, stat_smem, ps>>>(w.P, A);
                 A.cur = w.cur ^ 1;
                 wave_plan<<<1, 1, 0, ps>>>(w.P, A);
-                wave_admit<<<g_work, kBlock, stat_smem, ps>>>(w.P, A);
+                wave_admit<<<g_admit, kBlock, stat_smem, ps>>>(w.P, A);
                 w.cur ^= 1;
                 ++w.waves;
                 launches += 6;

@@ -103,6 +103,7 @@ struct TransportParams {
     double march_h;
     int32_t skip;           // 1: cross uniform macro cells in one step
     int32_t shared_mu_grid; // all materials' mu tables share grid_mat's energy knots
+    int32_t shared_e_grid;  // ... and so do their sigma_incoh / sigma_coh / sigma_pe tables
     int32_t grid_mat;
 
     // tallies
