@@ -267,6 +267,20 @@ def gpu_arm(args):
     ms_per_step = total_ms / args.steps
     value = n_hist / (ms_per_step / 1e3)
 
+    # ---------------- primary image of the same projection (reported beside the scatter
+    # metric: "Primary is timed and reported separately")
+    primary_ms = None
+    if rank == 0:
+        proj.primary(g, 0, spec, cfg)  # warm
+        torch.cuda.synchronize()
+        pa, pb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        pa.record(stream)
+        for _ in range(3):
+            proj.primary(g, 0, spec, cfg)
+        pb.record(stream)
+        torch.cuda.synchronize()
+        primary_ms = pa.elapsed_time(pb) / 3
+
     # ---------------- e2e: C ABI with host buffers (phantom upload + image D2H each step)
     e2e = None
     if not args.no_e2e:
@@ -339,6 +353,7 @@ def gpu_arm(args):
                        "parallelism": f"photon batches x{ws} + NCCL reduce" if ws > 1 else "1 GPU",
                        "l2": "flushed between timed steps (256 MiB write)"},
             "sec_per_projection": ms_per_step / 1e3,
+            "primary_ms": primary_ms,
             "e2e": e2e,
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
