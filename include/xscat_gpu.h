@@ -430,6 +430,36 @@ int xs_downsample_average(xs_context* ctx, const double* in, int32_t nu, int32_t
                           int32_t n_images, double* out, int32_t nu_out, int32_t nv_out,
                           int32_t device_ptrs);
 
+/* ------------------------------------------------ correction-loop stages
+ * (the elementwise stages that follow the projector
+ * in REF's iterative correction).  Stacks are n_images row-major images;
+ * device_ptrs as above.  Errors carry REF's messages (runtime_error). */
+
+/* REF intensity_to_attenuation (recon.cpp:324-348): a = ln(flat / I). */
+int xs_intensity_to_attenuation(xs_context* ctx, const double* intensity, const double* flatfield,
+                                int32_t nu, int32_t nv, int32_t n_images, double* out,
+                                int32_t device_ptrs);
+
+/* REF correct_projections (correction.cpp:58-86), Eq. 8:
+ * c = a - ln(Ip / (Ip + max(Is, 0))); *clamped = negative-scatter pixels. */
+int xs_correct_projections(xs_context* ctx, const double* a, const double* primary,
+                           const double* scatter, int32_t nu, int32_t nv, int32_t n_images,
+                           double* out, uint64_t* clamped, int32_t device_ptrs);
+
+/* The loop's tail after the Monte Carlo runs (REF correction.cpp:199-246):
+ * SG-smooth the n_sub scatter images (MC resolution nu x nv), interpolate
+ * them to the n_full angles, up-sample scatter and primary (n_full images at
+ * nu x nv) to nu_out x nv_out, floor each primary view at 1e-12 of its peak,
+ * and apply Eq. 8 to `a` (n_full images at nu_out x nv_out).  The scatter
+ * up-sampling is fused with the correction, so the full-resolution scatter
+ * stack is never stored.  Returns the corrected stack, the mean scatter
+ * fraction Is / (Ip + Is) and the clamped count. */
+int xs_correction_tail(xs_context* ctx, const double* scatter_sub, const double* sub_angles,
+                       int32_t n_sub, const double* primary_mc, const double* full_angles,
+                       int32_t n_full, int32_t nu, int32_t nv, int32_t sg_window, int32_t sg_order,
+                       const double* a, int32_t nu_out, int32_t nv_out, double* corrected,
+                       double* mean_scatter_fraction, uint64_t* clamped, int32_t device_ptrs);
+
 #ifdef __cplusplus
 }
 #endif

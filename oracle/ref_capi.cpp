@@ -15,7 +15,9 @@
 
 #include "../include/xscat_gpu.h"
 #include "support/oracles.hpp" // reference tests/support (analog oracle)
+#include "xscat/correction.hpp"
 #include "xscat/cross_sections.hpp"
+#include "xscat/recon.hpp"
 #include "xscat/material.hpp"
 #include "xscat/postprocess.hpp"
 #include "xscat/samplers.hpp"
@@ -442,6 +444,103 @@ int xr_downsample_average(const double* in, int32_t nu, int32_t nv, double* out,
     return guarded([&] {
         const DetectorImage r = downsample_average(image_from(in, nu, nv), nu_out, nv_out);
         std::memcpy(out, r.values.data(), r.values.size() * sizeof(double));
+    });
+}
+
+static ProjectionStack stack_from(const double* in, int32_t nu, int32_t nv, int32_t n)
+{
+    ProjectionStack s = make_stack(nu, nv, std::vector<double>(static_cast<std::size_t>(n), 0.0));
+    const std::size_t np = static_cast<std::size_t>(nu) * nv;
+    for (int i = 0; i < n; ++i)
+        s.images[i] = image_from(in + i * np, nu, nv);
+    return s;
+}
+
+static void stack_to(const ProjectionStack& s, double* out)
+{
+    const std::size_t np = static_cast<std::size_t>(s.nu) * s.nv;
+    for (int i = 0; i < s.n_angles(); ++i)
+        std::memcpy(out + i * np, s.images[i].values.data(), np * sizeof(double));
+}
+
+// correction.cpp:58-86 (Eq. 8)
+int xr_correct_projections(const double* a, const double* primary, const double* scatter, int32_t nu,
+                           int32_t nv, int32_t n, double* out, uint64_t* clamped)
+{
+    return guarded([&] {
+        std::size_t cl = 0;
+        const ProjectionStack c = correct_projections(stack_from(a, nu, nv, n), stack_from(primary, nu, nv, n),
+                                                      stack_from(scatter, nu, nv, n), &cl);
+        stack_to(c, out);
+        *clamped = cl;
+    });
+}
+
+// recon.cpp:324-348
+int xr_intensity_to_attenuation(const double* intensity, const double* flat, int32_t nu, int32_t nv,
+                                int32_t n, double* out)
+{
+    return guarded([&] {
+        const ProjectionStack a = intensity_to_attenuation(stack_from(intensity, nu, nv, n), image_from(flat, nu, nv));
+        stack_to(a, out);
+    });
+}
+
+// correction.cpp:199-246: the loop's tail after the Monte Carlo runs, composed
+// of REF's own functions in REF's order (SG on every scatter image, angle
+// interpolation, up-sampling of both stacks, primary floor, mean scatter
+// fraction, Eq. 8).
+int xr_correction_tail(const double* scatter_sub, const double* sub_angles, int32_t n_sub,
+                       const double* primary_mc, const double* full_angles, int32_t n_full, int32_t nu,
+                       int32_t nv, int32_t sg_window, int32_t sg_order, const double* a, int32_t nu_out,
+                       int32_t nv_out, double* corrected, double* mean_fraction, uint64_t* clamped)
+{
+    return guarded([&] {
+        const SgFilterSpec sg{sg_window, sg_order};
+        ProjectionStack scat = make_stack(nu, nv, std::vector<double>(sub_angles, sub_angles + n_sub));
+        const std::size_t np = static_cast<std::size_t>(nu) * nv;
+        for (int i = 0; i < n_sub; ++i)
+            scat.images[i] = image_from(scatter_sub + i * np, nu, nv);
+        const std::vector<double> full(full_angles, full_angles + n_full);
+        ProjectionStack scatter_hi = make_stack(nu_out, nv_out, full);
+        ProjectionStack primary_hi = make_stack(nu_out, nv_out, full);
+        for (auto& img : scat.images)
+            img = sg_smooth(img, sg);
+        const ProjectionStack scatter_full = interpolate_angles(scat, full);
+        for (int i = 0; i < n_full; ++i) {
+            scatter_hi.images[i] = upsample_image(scatter_full.images[i], nu_out, nv_out);
+            primary_hi.images[i] = upsample_image(image_from(primary_mc + i * np, nu, nv), nu_out, nv_out);
+        }
+        for (auto& img : primary_hi.images) {
+            double peak = 0.0;
+            for (double v : img.values)
+                peak = std::max(peak, v);
+            const double floor_val = 1e-12 * peak;
+            for (auto& v : img.values)
+                v = std::max(v, floor_val);
+        }
+        double frac_sum = 0.0;
+        std::size_t frac_n = 0;
+        for (int i = 0; i < n_full; ++i) {
+            const auto& pv = primary_hi.images[i].values;
+            const auto& sv = scatter_hi.images[i].values;
+            for (std::size_t p = 0; p < pv.size(); ++p) {
+                const double is = std::max(0.0, sv[p]);
+                if (pv[p] + is > 0.0) {
+                    frac_sum += is / (pv[p] + is);
+                    ++frac_n;
+                }
+            }
+        }
+        *mean_fraction = frac_n ? frac_sum / frac_n : 0.0;
+        std::size_t cl = 0;
+        ProjectionStack a_stack = make_stack(nu_out, nv_out, full);
+        const std::size_t npo = static_cast<std::size_t>(nu_out) * nv_out;
+        for (int i = 0; i < n_full; ++i)
+            a_stack.images[i] = image_from(a + i * npo, nu_out, nv_out);
+        const ProjectionStack c = correct_projections(a_stack, primary_hi, scatter_hi, &cl);
+        stack_to(c, corrected);
+        *clamped = cl;
     });
 }
 

@@ -2030,3 +2030,108 @@ int xo_downsample_average(const double* in, int32_t nu, int32_t nv, double* out,
     }
     return XS_OK;
 }
+
+/* ------------------------------------------------ correction-loop stages */
+
+/* REF intensity_to_attenuation (recon.cpp:324-348). */
+int xo_intensity_to_attenuation(const double* intensity, const double* flat, int32_t nu, int32_t nv,
+                                int32_t n, double* out)
+{
+    const size_t np = (size_t)nu * nv;
+    size_t bad = 0, p;
+    int i;
+    for (p = 0; p < np; ++p)
+        if (!(flat[p] > 0.0))
+            ++bad;
+    for (i = 0; i < n; ++i)
+        for (p = 0; p < np; ++p) {
+            const double v = intensity[(size_t)i * np + p];
+            if (!(v > 0.0)) {
+                ++bad;
+                out[(size_t)i * np + p] = 0.0;
+                continue;
+            }
+            out[(size_t)i * np + p] = log(flat[p] / v);
+        }
+    if (bad > 0) {
+        snprintf(tl_last, sizeof tl_last,
+                 "intensity_to_attenuation: %zu non-positive pixels (underexposed or invalid data)", bad);
+        return XS_E_RUNTIME;
+    }
+    return XS_OK;
+}
+
+/* REF correct_projections (correction.cpp:58-86), Eq. 8. */
+int xo_correct_projections(const double* a, const double* primary, const double* scatter, int32_t nu,
+                           int32_t nv, int32_t n, double* out, uint64_t* clamped)
+{
+    const size_t total = (size_t)nu * nv * n;
+    size_t k, cl = 0;
+    for (k = 0; k < total; ++k) {
+        double is = scatter[k];
+        if (!(primary[k] > 0.0)) {
+            snprintf(tl_last, sizeof tl_last, "correct_projections: non-positive primary pixel");
+            return XS_E_RUNTIME;
+        }
+        if (is < 0.0) {
+            is = 0.0;
+            ++cl;
+        }
+        out[k] = a[k] - log(primary[k] / (primary[k] + is));
+    }
+    *clamped = cl;
+    return XS_OK;
+}
+
+/* REF correction.cpp:199-246, the loop's tail after the Monte Carlo runs:
+ * SG per scatter image, angle interpolation, up-sampling of both stacks,
+ * primary floor at 1e-12 of each view's peak, mean scatter fraction, Eq. 8. */
+int xo_correction_tail(const double* scatter_sub, const double* sub_angles, int32_t n_sub,
+                       const double* primary_mc, const double* full_angles, int32_t n_full, int32_t nu,
+                       int32_t nv, int32_t sg_window, int32_t sg_order, const double* a, int32_t nu_out,
+                       int32_t nv_out, double* corrected, double* mean_fraction, uint64_t* clamped)
+{
+    const size_t np = (size_t)nu * nv, npo = (size_t)nu_out * nv_out;
+    double *sg = (double*)malloc(np * (n_sub ? n_sub : 1) * sizeof(double));
+    double *full = (double*)malloc(np * (n_full ? n_full : 1) * sizeof(double));
+    double *s_hi = (double*)malloc(npo * (n_full ? n_full : 1) * sizeof(double));
+    double *p_hi = (double*)malloc(npo * (n_full ? n_full : 1) * sizeof(double));
+    double frac_sum = 0.0;
+    size_t frac_n = 0, p;
+    int i, rc = XS_OK;
+    for (i = 0; i < n_sub && rc == XS_OK; ++i)
+        rc = xo_sg_smooth(scatter_sub + i * np, sg + i * np, nu, nv, sg_window, sg_order);
+    if (rc == XS_OK)
+        rc = xo_interpolate_angles(sg, sub_angles, n_sub, full, full_angles, n_full, nu, nv);
+    for (i = 0; i < n_full && rc == XS_OK; ++i) {
+        rc = xo_upsample_image(full + i * np, nu, nv, s_hi + i * npo, nu_out, nv_out);
+        if (rc == XS_OK)
+            rc = xo_upsample_image(primary_mc + i * np, nu, nv, p_hi + i * npo, nu_out, nv_out);
+    }
+    for (i = 0; i < n_full && rc == XS_OK; ++i) { /* correction.cpp:212-221 */
+        double peak = 0.0, floor_val;
+        double* img = p_hi + i * npo;
+        for (p = 0; p < npo; ++p)
+            peak = img[p] > peak ? img[p] : peak;
+        floor_val = 1e-12 * peak;
+        for (p = 0; p < npo; ++p)
+            img[p] = img[p] > floor_val ? img[p] : floor_val;
+    }
+    if (rc == XS_OK) { /* correction.cpp:226-239 */
+        for (p = 0; p < npo * n_full; ++p) {
+            const double is = s_hi[p] > 0.0 ? s_hi[p] : 0.0;
+            if (p_hi[p] + is > 0.0) {
+                frac_sum += is / (p_hi[p] + is);
+                ++frac_n;
+            }
+        }
+        *mean_fraction = frac_n ? frac_sum / frac_n : 0.0;
+        rc = xo_correct_projections(a, p_hi, s_hi, nu_out, nv_out, n_full, corrected, clamped);
+    }
+    free(sg);
+    free(full);
+    free(s_hi);
+    free(p_hi);
+    return rc;
+}
+

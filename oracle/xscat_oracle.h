@@ -95,6 +95,16 @@ int xo_upsample_image(const double* in, int32_t nu, int32_t nv, double* out, int
 int xo_downsample_average(const double* in, int32_t nu, int32_t nv, double* out,
                           int32_t nu_out, int32_t nv_out);
 
+/* Correction-loop stages (REF recon.cpp:324-348, correction.cpp:58-86, :199-246). */
+int xo_intensity_to_attenuation(const double* intensity, const double* flat, int32_t nu, int32_t nv,
+                                int32_t n, double* out);
+int xo_correct_projections(const double* a, const double* primary, const double* scatter, int32_t nu,
+                           int32_t nv, int32_t n, double* out, uint64_t* clamped);
+int xo_correction_tail(const double* scatter_sub, const double* sub_angles, int32_t n_sub,
+                       const double* primary_mc, const double* full_angles, int32_t n_full, int32_t nu,
+                       int32_t nv, int32_t sg_window, int32_t sg_order, const double* a, int32_t nu_out,
+                       int32_t nv_out, double* corrected, double* mean_fraction, uint64_t* clamped);
+
 #ifdef __cplusplus
 }
 #endif

@@ -14,7 +14,8 @@ from .inputs import (DetectorResponse, Material, ScanGeometry, SimConfig, Spectr
                      material, monochromatic_spectrum, spectrum)
 from .projector import (BOTH, PRIMARY, SCATTER, Context, ProjectionStack, Projector,  # noqa: F401
                         ScanResult, SgFilterSpec, SimResult, WeightLedger, apportion_photons,
-                        default_sg_spec, device_count, downsample_average, finalize_host,
+                        correct_projections, correction_tail, default_sg_spec, device_count,
+                        downsample_average, finalize_host, intensity_to_attenuation,
                         history_count, interpolate_angles, point_detector_score, run_scan,
                         sg_kernel, sg_smooth, simulate_primary, simulate_scatter,
                         simulate_scatter_stats, upsample_image)

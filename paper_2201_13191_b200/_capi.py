@@ -232,6 +232,13 @@ SIGNATURES = {
                                     C.c_int32, C.c_int32]),
     "xs_downsample_average": (C.c_int, [_P, _P, C.c_int32, C.c_int32, C.c_int32, _P,
                                         C.c_int32, C.c_int32, C.c_int32]),
+    "xs_intensity_to_attenuation": (C.c_int, [_P, _P, _P, C.c_int32, C.c_int32, C.c_int32, _P,
+                                              C.c_int32]),
+    "xs_correct_projections": (C.c_int, [_P, _P, _P, _P, C.c_int32, C.c_int32, C.c_int32, _P,
+                                         C.POINTER(C.c_uint64), C.c_int32]),
+    "xs_correction_tail": (C.c_int, [_P, _P, _P, C.c_int32, _P, _P, C.c_int32, C.c_int32,
+                                     C.c_int32, C.c_int32, C.c_int32, _P, C.c_int32, C.c_int32,
+                                     _P, C.POINTER(C.c_double), C.POINTER(C.c_uint64), C.c_int32]),
 }
 
 

@@ -27,6 +27,14 @@ cudaError_t transport_prepare(const TransportParams& P, size_t smem, int* blocks
 cudaError_t launch_transport(const TransportParams& P, int grid, size_t smem, cudaStream_t s);
 cudaError_t launch_primary(const PrimaryParams& P, cudaStream_t s);
 size_t levels_scratch_bytes(const Grid& G, const int* edges, int n_levels);
+size_t correct_stats_bytes(int n_views);
+cudaError_t launch_i2a(const double* in, const double* flat, double* out, size_t npix, int n_img, void* stats,
+                       int sm_count, cudaStream_t s);
+cudaError_t launch_correct(const double* a, const double* ip, const double* is, double* out, size_t n, void* stats,
+                           int sm_count, cudaStream_t s);
+cudaError_t launch_correction_tail(const double* primary, const double* scatter, const double* a, double* tmp,
+                                   double* p_hi, double* out, int nu, int nv, int n_views, int nu_out, int nv_out,
+                                   void* stats, cudaStream_t s);
 cudaError_t launch_mark_levels(uint8_t* vox, const Grid& G, int fmt, const int* edges, int n_levels,
                                void* scratch, int sm_count, cudaStream_t s);
 struct WaveEngine;
@@ -179,6 +187,8 @@ struct xs_context {
     DevBuf<double> img, var, pp_a, pp_b, pp_c, pp_k;
     DevBuf<xsd::InterpEntry> interp_tab;
     DevBuf<uint8_t> lvl_scratch;
+    DevBuf<double> cc_in[3], cc_out, cc_tmp, cc_phi, cc_sg, cc_full;
+    DevBuf<unsigned long long> cc_stats;
     int smem_kb = 48; // per transport block: 4 blocks/SM leave 60 KB of L1
     int max_slots = 64;
     int macro_skip = 1;
@@ -840,6 +850,11 @@ void xs_ctx_destroy(xs_context* c)
     c->var_pix.release();
     c->interp_tab.release();
     c->lvl_scratch.release();
+    for (auto& b : c->cc_in)
+        b.release();
+    for (auto* b : {&c->cc_out, &c->cc_tmp, &c->cc_phi, &c->cc_sg, &c->cc_full})
+        b->release();
+    c->cc_stats.release();
     xsd::wave_destroy(c->wave);
     if (c->ev0)
         cudaEventDestroy(c->ev0);
@@ -1160,6 +1175,72 @@ int xs_last_launch_stats(const xs_context* c, xs_launch_stats* out)
 
 // ------------------------------------------------------------ postprocess
 namespace {
+// REF sg_smooth set-up (postprocess.cpp:124-145): validation and the
+// (half+1)^2 truncated kernels (host-solved by REF's normal equations).
+int upload_sg_kernels(xs_context* c, int nu, int nv, int window, int polyorder)
+{
+    xsh::validate_sg(window, polyorder);
+    if (nu < window || nv < window)
+        fail(XS_E_RUNTIME, "sg_smooth: image dims smaller than filter window");
+    const int half = window / 2, W = 2 * half + 1;
+    std::vector<double> K((size_t)(half + 1) * (half + 1) * W, 0.0);
+    for (int l = 0; l <= half; ++l)
+        for (int r = 0; r <= half; ++r) {
+            const auto k = xsh::sg_kernel(l, r, polyorder);
+            std::copy(k.begin(), k.end(), K.begin() + (size_t)(l * (half + 1) + r) * W);
+        }
+    c->pp_k.reserve(K.size());
+    cuda_check(cudaMemcpyAsync(c->pp_k.p, K.data(), K.size() * 8, cudaMemcpyHostToDevice, c->stream), "H2D");
+    return half;
+}
+
+// REF interpolate_angles bracket selection (postprocess.cpp:147-196), on the
+// host; the per-pixel lerp runs on the device.
+void upload_interp_plan(xs_context* c, const double* src, int n_src, const double* tgt, int n_tgt)
+{
+    for (int i = 1; i < n_src; ++i)
+        if (!(src[i] > src[i - 1]))
+            fail(XS_E_RUNTIME, "interpolate_angles: source angles not sorted");
+    for (int i = 1; i < n_tgt; ++i)
+        if (!(tgt[i] > tgt[i - 1]))
+            fail(XS_E_RUNTIME, "interpolate_angles: target angles not sorted");
+    std::vector<xsd::InterpEntry> tab(n_tgt);
+    const double period = 2.0 * kPi;
+    for (int t = 0; t < n_tgt; ++t) {
+        const double b = tgt[t];
+        const double* lb = std::lower_bound(src, src + n_src, b);
+        if (lb != src + n_src && *lb == b) {
+            tab[t] = {(int)(lb - src), (int)(lb - src), 1, 0.0};
+            continue;
+        }
+        if (n_src < 2)
+            fail(XS_E_RUNTIME, "interpolate_angles: missing bracket for angle %f", b);
+        int hi = (int)(lb - src), lo;
+        double a_lo, a_hi;
+        if (hi == 0) {
+            lo = n_src - 1;
+            a_lo = src[lo] - period;
+            a_hi = src[0];
+        } else if (hi == n_src) {
+            lo = n_src - 1;
+            hi = 0;
+            a_lo = src[lo];
+            a_hi = src[0] + period;
+        } else {
+            lo = hi - 1;
+            a_lo = src[lo];
+            a_hi = src[hi];
+        }
+        tab[t] = {lo, hi, 0, (b - a_lo) / (a_hi - a_lo)};
+    }
+    if (n_tgt == 0)
+        return;
+    c->interp_tab.reserve(n_tgt);
+    cuda_check(cudaMemcpyAsync(c->interp_tab.p, tab.data(), n_tgt * sizeof(xsd::InterpEntry),
+                               cudaMemcpyHostToDevice, c->stream),
+               "H2D");
+}
+
 struct Staged {
     const double* in;
     double* out;
@@ -1188,18 +1269,7 @@ int xs_sg_smooth(xs_context* c, const double* in, double* out, int32_t nu, int32
                  int32_t window, int32_t polyorder, int32_t device_ptrs)
 {
     return guard(c, [&] {
-        xsh::validate_sg(window, polyorder);
-        if (nu < window || nv < window)
-            fail(XS_E_RUNTIME, "sg_smooth: image dims smaller than filter window");
-        const int half = window / 2, W = 2 * half + 1;
-        std::vector<double> K((size_t)(half + 1) * (half + 1) * W, 0.0);
-        for (int l = 0; l <= half; ++l)
-            for (int r = 0; r <= half; ++r) {
-                const auto k = xsh::sg_kernel(l, r, polyorder);
-                std::copy(k.begin(), k.end(), K.begin() + (size_t)(l * (half + 1) + r) * W);
-            }
-        c->pp_k.reserve(K.size());
-        cuda_check(cudaMemcpyAsync(c->pp_k.p, K.data(), K.size() * 8, cudaMemcpyHostToDevice, c->stream), "H2D");
+        const int half = upload_sg_kernels(c, nu, nv, window, polyorder);
         const size_t n = (size_t)nu * nv * n_images;
         const Staged s = stage(c, in, n, out, n, device_ptrs != 0);
         c->pp_c.reserve(n);
@@ -1212,48 +1282,9 @@ int xs_interpolate_angles(xs_context* c, const double* in, const double* src, in
                           const double* tgt, int32_t n_tgt, int32_t nu, int32_t nv, int32_t device_ptrs)
 {
     return guard(c, [&] {
-        for (int i = 1; i < n_src; ++i)
-            if (!(src[i] > src[i - 1]))
-                fail(XS_E_RUNTIME, "interpolate_angles: source angles not sorted");
-        for (int i = 1; i < n_tgt; ++i)
-            if (!(tgt[i] > tgt[i - 1]))
-                fail(XS_E_RUNTIME, "interpolate_angles: target angles not sorted");
-        // REF postprocess.cpp:160-192 bracket selection on the host
-        std::vector<xsd::InterpEntry> tab(n_tgt);
-        const double period = 2.0 * kPi;
-        for (int t = 0; t < n_tgt; ++t) {
-            const double b = tgt[t];
-            const double* lb = std::lower_bound(src, src + n_src, b);
-            if (lb != src + n_src && *lb == b) {
-                tab[t] = {(int)(lb - src), (int)(lb - src), 1, 0.0};
-                continue;
-            }
-            if (n_src < 2)
-                fail(XS_E_RUNTIME, "interpolate_angles: missing bracket for angle %f", b);
-            int hi = (int)(lb - src), lo;
-            double a_lo, a_hi;
-            if (hi == 0) {
-                lo = n_src - 1;
-                a_lo = src[lo] - period;
-                a_hi = src[0];
-            } else if (hi == n_src) {
-                lo = n_src - 1;
-                hi = 0;
-                a_lo = src[lo];
-                a_hi = src[0] + period;
-            } else {
-                lo = hi - 1;
-                a_lo = src[lo];
-                a_hi = src[hi];
-            }
-            tab[t] = {lo, hi, 0, (b - a_lo) / (a_hi - a_lo)};
-        }
+        upload_interp_plan(c, src, n_src, tgt, n_tgt);
         if (n_tgt == 0)
             return;
-        c->interp_tab.reserve(n_tgt);
-        cuda_check(cudaMemcpyAsync(c->interp_tab.p, tab.data(), n_tgt * sizeof(xsd::InterpEntry),
-                                   cudaMemcpyHostToDevice, c->stream),
-                   "H2D");
         const size_t np = (size_t)nu * nv;
         const Staged s = stage(c, in, np * n_src, out, np * n_tgt, device_ptrs != 0);
         cuda_check(xsd::launch_interp(s.in, s.out, c->interp_tab.p, n_tgt, np, c->stream), "interp");
@@ -1289,6 +1320,141 @@ int xs_downsample_average(xs_context* c, const double* in, int32_t nu, int32_t n
         cuda_check(xsd::launch_downsample(s.in, s.out, nu, nv, n_images, nu_out, nv_out, c->stream),
                    "downsample");
         unstage(c, s, out, n_out, device_ptrs != 0);
+    });
+}
+
+// ------------------------------------------------- correction-loop stages
+namespace {
+// host -> device staging of one input (device_ptrs: used in place)
+const double* cc_input(xs_context* c, int k, const double* p, size_t n, bool device)
+{
+    if (device)
+        return p;
+    c->cc_in[k].reserve(n);
+    cuda_check(cudaMemcpyAsync(c->cc_in[k].p, p, n * 8, cudaMemcpyHostToDevice, c->stream), "H2D");
+    return c->cc_in[k].p;
+}
+
+unsigned long long* cc_stats(xs_context* c, int n_views)
+{
+    const size_t words = (xsd::correct_stats_bytes(n_views) + 7) / 8;
+    c->cc_stats.reserve(words);
+    cuda_check(cudaMemsetAsync(c->cc_stats.p, 0, words * 8, c->stream), "memset");
+    return c->cc_stats.p;
+}
+
+void cc_read_stats(xs_context* c, uint64_t out[5])
+{
+    cuda_check(cudaMemcpyAsync(out, c->cc_stats.p, 5 * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    cuda_check(cudaStreamSynchronize(c->stream), "correction");
+}
+} // namespace
+
+int xs_intensity_to_attenuation(xs_context* c, const double* intensity, const double* flatfield, int32_t nu,
+                                int32_t nv, int32_t n_images, double* out, int32_t device_ptrs)
+{
+    return guard(c, [&] {
+        const bool dev = device_ptrs != 0;
+        const size_t np = (size_t)nu * nv, n = np * n_images;
+        const double* in = cc_input(c, 0, intensity, n, dev);
+        const double* flat = cc_input(c, 1, flatfield, np, dev);
+        double* o = out;
+        if (!dev) {
+            c->cc_out.reserve(n);
+            o = c->cc_out.p;
+        }
+        unsigned long long* st = cc_stats(c, 1);
+        cuda_check(xsd::launch_i2a(in, flat, o, np, n_images, st, c->sm_count, c->stream), "intensity_to_attenuation");
+        uint64_t h[5];
+        cc_read_stats(c, h);
+        if (h[1] > 0) // recon.cpp:343-345
+            fail(XS_E_RUNTIME, "intensity_to_attenuation: %llu non-positive pixels (underexposed or invalid data)",
+                 (unsigned long long)h[1]);
+        if (!dev) {
+            cuda_check(cudaMemcpyAsync(out, o, n * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+            cuda_check(cudaStreamSynchronize(c->stream), "D2H");
+        }
+    });
+}
+
+int xs_correct_projections(xs_context* c, const double* a, const double* primary, const double* scatter,
+                           int32_t nu, int32_t nv, int32_t n_images, double* out, uint64_t* clamped,
+                           int32_t device_ptrs)
+{
+    return guard(c, [&] {
+        const bool dev = device_ptrs != 0;
+        const size_t n = (size_t)nu * nv * n_images;
+        const double* da = cc_input(c, 0, a, n, dev);
+        const double* dp = cc_input(c, 1, primary, n, dev);
+        const double* ds = cc_input(c, 2, scatter, n, dev);
+        double* o = out;
+        if (!dev) {
+            c->cc_out.reserve(n);
+            o = c->cc_out.p;
+        }
+        unsigned long long* st = cc_stats(c, 1);
+        cuda_check(xsd::launch_correct(da, dp, ds, o, n, st, c->sm_count, c->stream), "correct_projections");
+        uint64_t h[5];
+        cc_read_stats(c, h);
+        if (h[1] > 0) // correction.cpp:72-73
+            fail(XS_E_RUNTIME, "correct_projections: non-positive primary pixel");
+        if (clamped)
+            *clamped = h[0];
+        if (!dev) {
+            cuda_check(cudaMemcpyAsync(out, o, n * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+            cuda_check(cudaStreamSynchronize(c->stream), "D2H");
+        }
+    });
+}
+
+int xs_correction_tail(xs_context* c, const double* scatter_sub, const double* sub_angles, int32_t n_sub,
+                       const double* primary_mc, const double* full_angles, int32_t n_full, int32_t nu, int32_t nv,
+                       int32_t sg_window, int32_t sg_order, const double* a, int32_t nu_out, int32_t nv_out,
+                       double* corrected, double* mean_scatter_fraction, uint64_t* clamped, int32_t device_ptrs)
+{
+    return guard(c, [&] {
+        if (nu_out < nu || nv_out < nv)
+            fail(XS_E_RUNTIME, "upsample_image: target dims must be >= source dims");
+        const bool dev = device_ptrs != 0;
+        const size_t np = (size_t)nu * nv, npo = (size_t)nu_out * nv_out;
+        // REF correction.cpp:199-205: SG on every scatter image, then angles
+        const int half = upload_sg_kernels(c, nu, nv, sg_window, sg_order);
+        upload_interp_plan(c, sub_angles, n_sub, full_angles, n_full);
+        if (n_full == 0)
+            return;
+        const double* ds = cc_input(c, 0, scatter_sub, np * n_sub, dev);
+        const double* dp = cc_input(c, 1, primary_mc, np * n_full, dev);
+        const double* da = cc_input(c, 2, a, npo * n_full, dev);
+        c->cc_sg.reserve(np * n_sub);
+        c->pp_c.reserve(np * n_sub);
+        cuda_check(xsd::launch_sg(ds, c->pp_c.p, c->cc_sg.p, nu, nv, n_sub, half, c->pp_k.p, c->stream), "sg");
+        c->cc_full.reserve(np * n_full);
+        cuda_check(xsd::launch_interp(c->cc_sg.p, c->cc_full.p, c->interp_tab.p, n_full, np, c->stream), "interp");
+        // correction.cpp:206-246, fused (correct.cu)
+        double* o = corrected;
+        if (!dev) {
+            c->cc_out.reserve(npo * n_full);
+            o = c->cc_out.p;
+        }
+        c->cc_tmp.reserve(2 * (size_t)n_full * nv * nu_out);
+        c->cc_phi.reserve(npo * n_full);
+        unsigned long long* st = cc_stats(c, n_full);
+        cuda_check(xsd::launch_correction_tail(dp, c->cc_full.p, da, c->cc_tmp.p, c->cc_phi.p, o, nu, nv, n_full,
+                                               nu_out, nv_out, st, c->stream),
+                   "correction tail");
+        uint64_t h[5];
+        cc_read_stats(c, h);
+        if (h[1] > 0)
+            fail(XS_E_RUNTIME, "correct_projections: non-positive primary pixel");
+        if (clamped)
+            *clamped = h[0];
+        if (mean_scatter_fraction) // fixed-point sum of the fractions / count
+            *mean_scatter_fraction =
+                h[4] ? (std::ldexp((double)h[2], -32) + std::ldexp((double)h[3], -64)) / (double)h[4] : 0.0;
+        if (!dev) {
+            cuda_check(cudaMemcpyAsync(corrected, o, npo * n_full * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+            cuda_check(cudaStreamSynchronize(c->stream), "D2H");
+        }
     });
 }
 

@@ -337,3 +337,63 @@ def downsample_average(img, nu_out: int, nv_out: int, ctx: Optional[Context] = N
     ctx.check(A.lib().xs_downsample_average(ctx.h, a.ctypes.data, a.shape[2], a.shape[1],
                                             a.shape[0], out.ctypes.data, nu_out, nv_out, 0))
     return out[0] if single else out
+
+
+# ------------------------------------------------------ correction-loop stages
+def intensity_to_attenuation(intensity, flatfield, ctx: Optional[Context] = None) -> np.ndarray:
+    """REF intensity_to_attenuation (recon.cpp:324-348): a = ln(flat / I) per pixel.
+    ``intensity``: (n, nv, nu) stack (or one image); ``flatfield``: (nv, nu)."""
+    ctx = ctx or default_context()
+    a, single = _as_stack(intensity)
+    flat = np.ascontiguousarray(flatfield, dtype=np.float64)
+    if flat.shape != a.shape[1:]:
+        raise I.XscatError("intensity_to_attenuation: flatfield dims mismatch")
+    out = np.empty_like(a)
+    ctx.check(A.lib().xs_intensity_to_attenuation(ctx.h, a.ctypes.data, flat.ctypes.data, a.shape[2],
+                                                  a.shape[1], a.shape[0], out.ctypes.data, 0))
+    return out[0] if single else out
+
+
+def correct_projections(a, primary, scatter, ctx: Optional[Context] = None):
+    """REF correct_projections (correction.cpp:58-86), Eq. 8:
+    c = a - ln(Ip / (Ip + max(Is, 0))).  Returns (corrected, clamped_count)."""
+    ctx = ctx or default_context()
+    sa, single = _as_stack(a)
+    sp, _ = _as_stack(primary)
+    ss, _ = _as_stack(scatter)
+    if sa.shape != sp.shape or sa.shape != ss.shape:
+        raise I.XscatError("correct_projections: stack dims mismatch")
+    out = np.empty_like(sa)
+    clamped = C.c_uint64(0)
+    ctx.check(A.lib().xs_correct_projections(ctx.h, sa.ctypes.data, sp.ctypes.data, ss.ctypes.data,
+                                             sa.shape[2], sa.shape[1], sa.shape[0], out.ctypes.data,
+                                             C.byref(clamped), 0))
+    return (out[0] if single else out), int(clamped.value)
+
+
+def correction_tail(scatter_sub, sub_angles, primary_mc, full_angles, f: SgFilterSpec, a,
+                    ctx: Optional[Context] = None):
+    """The correction loop's tail after the Monte Carlo runs (REF
+    correction.cpp:199-246), fused on the device: SG on the scatter images,
+    angle interpolation, Catmull-Rom up-sampling of scatter and primary to the
+    size of ``a``, primary floor at 1e-12 of each view's peak, Eq. 8.
+    Returns (corrected stack, mean scatter fraction, clamped count)."""
+    ctx = ctx or default_context()
+    s = np.ascontiguousarray(scatter_sub, dtype=np.float64)
+    p = np.ascontiguousarray(primary_mc, dtype=np.float64)
+    aa = np.ascontiguousarray(a, dtype=np.float64)
+    sa = np.ascontiguousarray(sub_angles, dtype=np.float64)
+    fa = np.ascontiguousarray(full_angles, dtype=np.float64)
+    n_sub, nv, nu = s.shape
+    n_full, nv_out, nu_out = aa.shape
+    if p.shape != (n_full, nv, nu) or sa.size != n_sub or fa.size != n_full:
+        raise I.XscatError("correction_tail: stack dims mismatch")
+    out = np.empty_like(aa)
+    frac = C.c_double(0.0)
+    clamped = C.c_uint64(0)
+    ctx.check(A.lib().xs_correction_tail(ctx.h, s.ctypes.data, sa.ctypes.data, n_sub, p.ctypes.data,
+                                         fa.ctypes.data, n_full, nu, nv, f.window, f.polyorder,
+                                         aa.ctypes.data, nu_out, nv_out, out.ctypes.data,
+                                         C.byref(frac), C.byref(clamped), 0))
+    return out, float(frac.value), int(clamped.value)
+

@@ -57,6 +57,12 @@ def _sig(L, prefix):
         f"{p}_upsample_image": (C.c_int, [_dp, C.c_int32, C.c_int32, _dp, C.c_int32, C.c_int32]),
         f"{p}_downsample_average": (C.c_int, [_dp, C.c_int32, C.c_int32, _dp, C.c_int32,
                                               C.c_int32]),
+        f"{p}_intensity_to_attenuation": (C.c_int, [_dp, _dp, C.c_int32, C.c_int32, C.c_int32, _dp]),
+        f"{p}_correct_projections": (C.c_int, [_dp, _dp, _dp, C.c_int32, C.c_int32, C.c_int32, _dp,
+                                               A.c_u64_p]),
+        f"{p}_correction_tail": (C.c_int, [_dp, _dp, C.c_int32, _dp, _dp, C.c_int32, C.c_int32,
+                                           C.c_int32, C.c_int32, C.c_int32, _dp, C.c_int32,
+                                           C.c_int32, _dp, _dp, A.c_u64_p]),
         f"{p}_last_error": (C.c_char_p, []),
     }
     if prefix == "xo":
@@ -239,6 +245,43 @@ class Oracle:
         self.check(self.fn("downsample_average")(A.dptr(img), nu, nv, A.dptr(out), nu_out,
                                                  nv_out))
         return out
+
+
+    # correction-loop stages (REF recon.cpp:324-348, correction.cpp:58-86, :199-246)
+    def intensity_to_attenuation(self, intensity, flat):
+        x = np.ascontiguousarray(intensity, np.float64)
+        f = np.ascontiguousarray(flat, np.float64)
+        n, nv, nu = x.shape
+        out = np.zeros_like(x)
+        self.check(self.fn("intensity_to_attenuation")(A.dptr(x), A.dptr(f), nu, nv, n, A.dptr(out)))
+        return out
+
+    def correct_projections(self, a, primary, scatter):
+        a = np.ascontiguousarray(a, np.float64)
+        p = np.ascontiguousarray(primary, np.float64)
+        s = np.ascontiguousarray(scatter, np.float64)
+        n, nv, nu = a.shape
+        out = np.zeros_like(a)
+        cl = C.c_uint64(0)
+        self.check(self.fn("correct_projections")(A.dptr(a), A.dptr(p), A.dptr(s), nu, nv, n, A.dptr(out),
+                                                  C.byref(cl)))
+        return out, int(cl.value)
+
+    def correction_tail(self, scatter_sub, sub_angles, primary_mc, full_angles, window, order, a):
+        s = np.ascontiguousarray(scatter_sub, np.float64)
+        p = np.ascontiguousarray(primary_mc, np.float64)
+        a = np.ascontiguousarray(a, np.float64)
+        sa = np.ascontiguousarray(sub_angles, np.float64)
+        fa = np.ascontiguousarray(full_angles, np.float64)
+        n_sub, nv, nu = s.shape
+        n_full, nv_out, nu_out = a.shape
+        out = np.zeros_like(a)
+        frac = C.c_double(0.0)
+        cl = C.c_uint64(0)
+        self.check(self.fn("correction_tail")(A.dptr(s), A.dptr(sa), n_sub, A.dptr(p), A.dptr(fa), n_full, nu,
+                                              nv, window, order, A.dptr(a), nu_out, nv_out, A.dptr(out),
+                                              C.byref(frac), C.byref(cl)))
+        return out, float(frac.value), int(cl.value)
 
 
 _oracle = None
