@@ -27,8 +27,10 @@
 #include <string>
 #include <vector>
 
+#include "xscat/correction.hpp"
 #include "xscat/detector_image.hpp"
 #include "xscat/postprocess.hpp"
+#include "xscat/recon.hpp"
 #include "xscat/transport.hpp"
 #include "xscat_gpu.h"
 
@@ -349,6 +351,90 @@ inline xscat::DetectorImage downsample_average(const xscat::DetectorImage& img, 
                                        nu_out, nv_out, 0),
                  c.get());
     return out;
+}
+
+// ------------------------------------------------ correction-loop stages
+namespace detail {
+inline std::vector<double> flatten(const xscat::ProjectionStack& s)
+{
+    const std::size_t np = static_cast<std::size_t>(s.nu) * s.nv;
+    std::vector<double> v(np * s.images.size());
+    for (std::size_t i = 0; i < s.images.size(); ++i)
+        std::copy(s.images[i].values.begin(), s.images[i].values.end(), v.begin() + i * np);
+    return v;
+}
+
+inline xscat::ProjectionStack unflatten(const std::vector<double>& v, int nu, int nv,
+                                        const std::vector<double>& angles)
+{
+    xscat::ProjectionStack r = xscat::make_stack(nu, nv, angles);
+    const std::size_t np = static_cast<std::size_t>(nu) * nv;
+    for (std::size_t i = 0; i < r.images.size(); ++i)
+        std::copy(v.begin() + i * np, v.begin() + (i + 1) * np, r.images[i].values.begin());
+    return r;
+}
+} // namespace detail
+
+// REF recon.hpp intensity_to_attenuation (recon.cpp:324-348)
+inline xscat::ProjectionStack intensity_to_attenuation(const xscat::ProjectionStack& intensity,
+                                                       const xscat::DetectorImage& flatfield)
+{
+    if (flatfield.nu != intensity.nu || flatfield.nv != intensity.nv)
+        throw std::runtime_error("intensity_to_attenuation: flatfield dims mismatch");
+    const std::vector<double> in = detail::flatten(intensity);
+    std::vector<double> out(in.size());
+    Context& c = thread_context();
+    throw_status(xs_intensity_to_attenuation(c.get(), in.data(), flatfield.values.data(), intensity.nu,
+                                             intensity.nv, intensity.n_angles(), out.data(), 0),
+                 c.get());
+    return detail::unflatten(out, intensity.nu, intensity.nv, intensity.angle_values);
+}
+
+// REF correction.hpp correct_projections (correction.cpp:58-86), Eq. 8
+inline xscat::ProjectionStack correct_projections(const xscat::ProjectionStack& a, const xscat::ProjectionStack& primary,
+                                                  const xscat::ProjectionStack& scatter,
+                                                  std::size_t* clamped_count = nullptr)
+{
+    if (a.nu != primary.nu || a.nv != primary.nv || a.nu != scatter.nu || a.nv != scatter.nv ||
+        a.n_angles() != primary.n_angles() || a.n_angles() != scatter.n_angles())
+        throw std::runtime_error("correct_projections: stack dims mismatch");
+    const std::vector<double> va = detail::flatten(a), vp = detail::flatten(primary), vs = detail::flatten(scatter);
+    std::vector<double> out(va.size());
+    uint64_t clamped = 0;
+    Context& c = thread_context();
+    throw_status(xs_correct_projections(c.get(), va.data(), vp.data(), vs.data(), a.nu, a.nv, a.n_angles(),
+                                        out.data(), &clamped, 0),
+                 c.get());
+    if (clamped_count)
+        *clamped_count = static_cast<std::size_t>(clamped);
+    return detail::unflatten(out, a.nu, a.nv, a.angle_values);
+}
+
+// The loop's tail after the Monte Carlo runs (REF correction.cpp:199-246) in
+// one device call: `scatter_run` = run_scan(..., scatter) on the angle subset
+// (MC resolution), `primary_run` = the primary on every angle (MC
+// resolution), `a` = the attenuation stack at full resolution.
+inline xscat::ProjectionStack correction_tail(const xscat::ProjectionStack& scatter_run,
+                                              const xscat::ProjectionStack& primary_run,
+                                              const xscat::SgFilterSpec& sg, const xscat::ProjectionStack& a,
+                                              double* mean_scatter_fraction = nullptr,
+                                              std::size_t* clamped_count = nullptr)
+{
+    const std::vector<double> vs = detail::flatten(scatter_run), vp = detail::flatten(primary_run),
+                              va = detail::flatten(a);
+    std::vector<double> out(va.size());
+    double frac = 0.0;
+    uint64_t clamped = 0;
+    Context& c = thread_context();
+    throw_status(xs_correction_tail(c.get(), vs.data(), scatter_run.angle_values.data(), scatter_run.n_angles(),
+                                    vp.data(), a.angle_values.data(), a.n_angles(), scatter_run.nu, scatter_run.nv,
+                                    sg.window, sg.polyorder, va.data(), a.nu, a.nv, out.data(), &frac, &clamped, 0),
+                 c.get());
+    if (mean_scatter_fraction)
+        *mean_scatter_fraction = frac;
+    if (clamped_count)
+        *clamped_count = static_cast<std::size_t>(clamped);
+    return detail::unflatten(out, a.nu, a.nv, a.angle_values);
 }
 
 } // namespace xscat_b200

@@ -122,6 +122,43 @@ int main(int argc, char** argv)
         check(xscat_b200::apportion_photons(sp, 12345) == xscat::apportion_photons(sp, 12345),
               "apportion_photons", "");
     }
+    { // correction-loop stages: REF correct_projections / intensity_to_attenuation
+        const int nu = 37, nv = 29, n = 3;
+        ProjectionStack a = make_stack(nu, nv, {0.0, 1.0, 2.0}), p = a, sc = a, inten = a;
+        DetectorImage flat(nu, nv);
+        for (int i = 0; i < n; ++i)
+            for (std::size_t k = 0; k < a.images[i].values.size(); ++k) {
+                const double x = 0.001 * (double)(k + 97 * i);
+                a.images[i].values[k] = 1.0 + std::sin(x);
+                p.images[i].values[k] = 0.5 + 0.4 * std::cos(3 * x);
+                sc.images[i].values[k] = 0.1 * std::sin(7 * x); // some negative: clamped
+                inten.images[i].values[k] = 0.2 + 0.1 * std::cos(x);
+                flat.values[k] = 1.5;
+            }
+        std::size_t cr = 0, cg = 0;
+        const ProjectionStack r = xscat::correct_projections(a, p, sc, &cr);
+        const ProjectionStack g = xscat_b200::correct_projections(a, p, sc, &cg);
+        double md = 0.0;
+        for (int i = 0; i < n; ++i)
+            for (std::size_t k = 0; k < r.images[i].values.size(); ++k)
+                md = std::max(md, std::fabs(r.images[i].values[k] - g.images[i].values[k]));
+        check(cr == cg && md <= 1e-14, "correct_projections (Eq. 8)", "max |diff| " + std::to_string(md));
+        const ProjectionStack ar = xscat::intensity_to_attenuation(inten, flat);
+        const ProjectionStack ag = xscat_b200::intensity_to_attenuation(inten, flat);
+        md = 0.0;
+        for (int i = 0; i < n; ++i)
+            for (std::size_t k = 0; k < ar.images[i].values.size(); ++k)
+                md = std::max(md, std::fabs(ar.images[i].values[k] - ag.images[i].values[k]));
+        check(md <= 1e-14, "intensity_to_attenuation", "max |diff| " + std::to_string(md));
+        p.images[1].values[5] = 0.0;
+        bool threw = false;
+        try {
+            xscat_b200::correct_projections(a, p, sc);
+        } catch (const std::runtime_error& e) {
+            threw = std::string(e.what()).find("non-positive primary pixel") != std::string::npos;
+        }
+        check(threw, "correct_projections throws runtime_error", "");
+    }
     std::printf("%s\n", g_fail ? "FAILED" : "all checks passed");
     return g_fail ? 1 : 0;
 }
