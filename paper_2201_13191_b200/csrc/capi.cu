@@ -33,8 +33,8 @@ cudaError_t launch_i2a(const double* in, const double* flat, double* out, size_t
 cudaError_t launch_correct(const double* a, const double* ip, const double* is, double* out, size_t n, void* stats,
                            int sm_count, cudaStream_t s);
 cudaError_t launch_correction_tail(const double* primary, const double* scatter, const double* a, double* tmp,
-                                   double* p_hi, double* out, int nu, int nv, int n_views, int nu_out, int nv_out,
-                                   void* stats, cudaStream_t s);
+                                   double* out, int nu, int nv, int n_views, int nu_out, int nv_out, void* stats,
+                                   cudaStream_t s);
 cudaError_t launch_mark_levels(uint8_t* vox, const Grid& G, int fmt, const int* edges, int n_levels,
                                void* scratch, int sm_count, cudaStream_t s);
 struct WaveEngine;
@@ -187,7 +187,7 @@ struct xs_context {
     DevBuf<double> img, var, pp_a, pp_b, pp_c, pp_k;
     DevBuf<xsd::InterpEntry> interp_tab;
     DevBuf<uint8_t> lvl_scratch;
-    DevBuf<double> cc_in[3], cc_out, cc_tmp, cc_phi, cc_sg, cc_full;
+    DevBuf<double> cc_in[3], cc_out, cc_tmp, cc_sg, cc_full;
     DevBuf<unsigned long long> cc_stats;
     int smem_kb = 48; // per transport block: 4 blocks/SM leave 60 KB of L1
     int max_slots = 64;
@@ -852,7 +852,7 @@ void xs_ctx_destroy(xs_context* c)
     c->lvl_scratch.release();
     for (auto& b : c->cc_in)
         b.release();
-    for (auto* b : {&c->cc_out, &c->cc_tmp, &c->cc_phi, &c->cc_sg, &c->cc_full})
+    for (auto* b : {&c->cc_out, &c->cc_tmp, &c->cc_sg, &c->cc_full})
         b->release();
     c->cc_stats.release();
     xsd::wave_destroy(c->wave);
@@ -1437,10 +1437,9 @@ int xs_correction_tail(xs_context* c, const double* scatter_sub, const double* s
             o = c->cc_out.p;
         }
         c->cc_tmp.reserve(2 * (size_t)n_full * nv * nu_out);
-        c->cc_phi.reserve(npo * n_full);
         unsigned long long* st = cc_stats(c, n_full);
-        cuda_check(xsd::launch_correction_tail(dp, c->cc_full.p, da, c->cc_tmp.p, c->cc_phi.p, o, nu, nv, n_full,
-                                               nu_out, nv_out, st, c->stream),
+        cuda_check(xsd::launch_correction_tail(dp, c->cc_full.p, da, c->cc_tmp.p, o, nu, nv, n_full, nu_out,
+                                               nv_out, st, c->stream),
                    "correction tail");
         uint64_t h[5];
         cc_read_stats(c, h);

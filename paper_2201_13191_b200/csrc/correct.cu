@@ -6,9 +6,10 @@
 // The tail is fused: the scatter stack's column up-sampling pass (the last
 // Catmull-Rom pass, REF postprocess.cpp:235-252) computes each full-resolution
 // scatter pixel in registers and applies the primary floor, the scatter-
-// fraction statistic and Eq. 8 right there, so the up-sampled scatter stack
-// (720 x 2048^2 x 8 B = 24 GB in REF's C5 loop) is never written.  The
-// primary's column pass records each view's peak for the floor.
+// fraction statistic and Eq. 8 right there; the primary's column pass runs
+// twice (once for each view's peak, once inside the correction), so neither
+// up-sampled stack (720 x 2048^2 x 8 B = 24 GB each in REF's C5 loop) is
+// ever written.
 //
 // Counts (clamped negative scatter, bad pixels) are integers and the mean
 // scatter fraction is summed as 2 x 32-bit fixed-point limbs per pixel, so
@@ -143,54 +144,107 @@ __device__ __forceinline__ double cr_sample_c(const double* line, int n_in, int 
            w2 * cr_fetch_c(line, n_in, stride, base + 1) + w3 * cr_fetch_c(line, n_in, stride, base + 2);
 }
 
-// primary column pass: out = up-sampled primary, peak[view] = max(0, max over the view)
-__global__ void cr_cols_peak_kernel(const double* __restrict__ tmp, double* __restrict__ out, int nu_out,
-                                    int nv, int nv_out, CorrectStats* st)
+// Column passes loop over rows (blockIdx.y strides by gridDim.y) so that the
+// statistics are reduced in registers and then once per block: per-warp
+// atomics on a handful of addresses would serialise at L2 (94M of them for a
+// 720 x 2048^2 stack).
+constexpr int kRowGroups = 16; // row chunks per column (contiguous rows: the 4 taps are reused)
+
+__device__ __forceinline__ unsigned long long block_sum(unsigned long long v, unsigned long long* sh)
 {
+    v = warp_sum(v);
+    const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0)
+        sh[w] = v;
+    __syncthreads();
+    unsigned long long t = 0;
+    for (int i = 0; i < nw; ++i)
+        t += sh[i];
+    return t;
+}
+
+// primary column pass, statistics only: peak[view] = max(0, max of the
+// up-sampled view).  The correction pass recomputes the primary pixels in
+// registers, so the full-resolution primary stack is never stored either.
+__global__ void cr_cols_peak_kernel(const double* __restrict__ tmp, int nu_out, int nv, int nv_out,
+                                    CorrectStats* st)
+{
+    __shared__ double shm[32];
     const int iu = blockIdx.x * blockDim.x + threadIdx.x;
-    const int j = blockIdx.y;
-    double v = 0.0;
+    const int chunk = (nv_out + gridDim.y - 1) / gridDim.y;
+    const int j0 = blockIdx.y * chunk, j1 = j0 + chunk < nv_out ? j0 + chunk : nv_out;
+    double m = 0.0;
     if (iu < nu_out) {
         const double* line = tmp + (size_t)blockIdx.z * nu_out * nv + iu;
-        v = cr_sample_c(line, nv, nv_out, (size_t)nu_out, j);
-        out[(size_t)blockIdx.z * nu_out * nv_out + (size_t)j * nu_out + iu] = v;
+        for (int j = j0; j < j1; ++j) {
+            const double v = cr_sample_c(line, nv, nv_out, (size_t)nu_out, j);
+            m = v > m ? v : m;
+        }
     }
-    double m = v > 0.0 ? v : 0.0;
 #pragma unroll
     for (int o = 16; o; o >>= 1)
         m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0 && m > 0.0) // non-negative doubles order like their bits
-        atomicMax(&st->peak[blockIdx.z], (unsigned long long)__double_as_longlong(m));
+    if ((threadIdx.x & 31) == 0)
+        shm[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < (int)(blockDim.x >> 5); ++i)
+            m = fmax(m, shm[i]);
+        if (m > 0.0) // non-negative doubles order like their bits
+            atomicMax(&st->peak[blockIdx.z], (unsigned long long)__double_as_longlong(m));
+    }
 }
 
-// scatter column pass fused with the primary floor, the mean-scatter-fraction
-// sums and Eq. 8 (REF correction.cpp:212-246)
-__global__ void cr_cols_correct_kernel(const double* __restrict__ tmp_s, const double* __restrict__ p_hi,
+// column passes of both stacks fused with the primary floor, the mean-
+// scatter-fraction sums and Eq. 8 (REF correction.cpp:206-246)
+__global__ void cr_cols_correct_kernel(const double* __restrict__ tmp_p, const double* __restrict__ tmp_s,
                                        const double* __restrict__ a, double* __restrict__ out, int nu_out,
                                        int nv, int nv_out, CorrectStats* st)
 {
+    __shared__ unsigned long long sh[32];
     const int iu = blockIdx.x * blockDim.x + threadIdx.x;
-    const int j = blockIdx.y;
+    const int chunk = (nv_out + gridDim.y - 1) / gridDim.y;
+    const int j0 = blockIdx.y * chunk, j1 = j0 + chunk < nv_out ? j0 + chunk : nv_out;
     unsigned long long clamped = 0, bad = 0, fh = 0, fl = 0, fn = 0;
     if (iu < nu_out) {
-        const double* line = tmp_s + (size_t)blockIdx.z * nu_out * nv + iu;
-        const double s = cr_sample_c(line, nv, nv_out, (size_t)nu_out, j);
-        const size_t o = (size_t)blockIdx.z * nu_out * nv_out + (size_t)j * nu_out + iu;
+        const size_t col = (size_t)blockIdx.z * nu_out * nv + iu;
         const double peak = __longlong_as_double((long long)st->peak[blockIdx.z]);
         const double floor_val = 1e-12 * peak;
-        const double ip = p_hi[o] > floor_val ? p_hi[o] : floor_val; // std::max(v, floor_val)
-        const double isc = s > 0.0 ? s : 0.0;                          // std::max(0.0, s)
-        if (ip + isc > 0.0) {
-            const double f = isc / (ip + isc); // in [0, 1]
-            const double f32 = f * 4294967296.0;
-            const double h = floor(f32);
-            fh = (unsigned long long)h;
-            fl = (unsigned long long)floor((f32 - h) * 4294967296.0);
-            fn = 1;
+        for (int j = j0; j < j1; ++j) {
+            const double pv = cr_sample_c(tmp_p + col, nv, nv_out, (size_t)nu_out, j);
+            const double s = cr_sample_c(tmp_s + col, nv, nv_out, (size_t)nu_out, j);
+            const size_t o = (size_t)blockIdx.z * nu_out * nv_out + (size_t)j * nu_out + iu;
+            const double ip = pv > floor_val ? pv : floor_val; // std::max(v, floor_val)
+            const double isc = s > 0.0 ? s : 0.0;              // std::max(0.0, s)
+            if (ip + isc > 0.0) {
+                const double f = isc / (ip + isc); // in [0, 1]
+                const double f32 = f * 4294967296.0;
+                const double h = floor(f32);
+                fh += (unsigned long long)h;
+                fl += (unsigned long long)floor((f32 - h) * 4294967296.0);
+                ++fn;
+            }
+            out[o] = eq8(a[o], ip, s, clamped, bad);
         }
-        out[o] = eq8(a[o], ip, s, clamped, bad);
     }
-    add_stats(st, clamped, bad, fh, fl, fn);
+    clamped = block_sum(clamped, sh);
+    bad = block_sum(bad, sh);
+    fh = block_sum(fh, sh);
+    fl = block_sum(fl, sh);
+    fn = block_sum(fn, sh);
+    if (threadIdx.x == 0) {
+        if (clamped)
+            atomicAdd(&st->clamped, clamped);
+        if (bad)
+            atomicAdd(&st->bad, bad);
+        if (fh)
+            atomicAdd(&st->frac_hi, fh);
+        if (fl)
+            atomicAdd(&st->frac_lo, fl);
+        if (fn)
+            atomicAdd(&st->frac_n, fn);
+    }
 }
 
 // rows: in (nv x nu) -> tmp (nv x nu_out)
@@ -222,20 +276,20 @@ cudaError_t launch_correct(const double* a, const double* ip, const double* is, 
 }
 
 // in: primary (nv x nu per view) and the angle-interpolated scatter stack at
-// the Monte Carlo resolution; tmp: 2 x n_views x nv x nu_out; p_hi: the
-// up-sampled, un-floored primary (n_views x nv_out x nu_out)
+// the Monte Carlo resolution; tmp: 2 x n_views x nv x nu_out (the row passes)
 cudaError_t launch_correction_tail(const double* primary, const double* scatter, const double* a, double* tmp,
-                                   double* p_hi, double* out, int nu, int nv, int n_views, int nu_out,
-                                   int nv_out, void* stats, cudaStream_t s)
+                                   double* out, int nu, int nv, int n_views, int nu_out, int nv_out, void* stats,
+                                   cudaStream_t s)
 {
     CorrectStats* st = static_cast<CorrectStats*>(stats);
     double* tmp_p = tmp;
     double* tmp_s = tmp + (size_t)n_views * nv * nu_out;
-    const dim3 rows((nu_out + 127) / 128, nv, n_views), cols((nu_out + 127) / 128, nv_out, n_views);
+    const dim3 rows((nu_out + 127) / 128, nv, n_views),
+        cols((nu_out + 127) / 128, nv_out < kRowGroups ? nv_out : kRowGroups, n_views);
     cr_rows_c<<<rows, 128, 0, s>>>(primary, tmp_p, nu, nv, nu_out);
     cr_rows_c<<<rows, 128, 0, s>>>(scatter, tmp_s, nu, nv, nu_out);
-    cr_cols_peak_kernel<<<cols, 128, 0, s>>>(tmp_p, p_hi, nu_out, nv, nv_out, st);
-    cr_cols_correct_kernel<<<cols, 128, 0, s>>>(tmp_s, p_hi, a, out, nu_out, nv, nv_out, st);
+    cr_cols_peak_kernel<<<cols, 128, 0, s>>>(tmp_p, nu_out, nv, nv_out, st);
+    cr_cols_correct_kernel<<<cols, 128, 0, s>>>(tmp_p, tmp_s, a, out, nu_out, nv, nv_out, st);
     return cudaGetLastError();
 }
 
