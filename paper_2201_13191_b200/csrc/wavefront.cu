@@ -40,7 +40,8 @@ namespace {
 
 constexpr int kRefill = 8; // idle lanes that trigger a warp's refill in the walk kernel
 #ifndef XSW_WALK_BLOCKS
-#define XSW_WALK_BLOCKS 6 // resident walk blocks per SM (<= 80 registers; 7-8 spill or slow the macro walk)
+#define XSW_WALK_BLOCKS 6 // resident walk blocks per SM (<= 80 registers; 7-8 spill or slow the macro walk;
+                          // the exact walk is lighter and runs one more)
 #endif
 
 // A history's scoring rays of one interaction: the slot and its Philox
@@ -285,7 +286,7 @@ __global__ void __launch_bounds__(kBlock) wave_setup(const __grid_constant__ Tra
 
 // -------------------------------------------------------------------- walk
 template <int FMT, bool REG, bool SKIP>
-__global__ void __launch_bounds__(kBlock, XSW_WALK_BLOCKS) wave_walk(const __grid_constant__ TransportParams P,
+__global__ void __launch_bounds__(kBlock, SKIP ? XSW_WALK_BLOCKS : XSW_WALK_BLOCKS + 1) wave_walk(const __grid_constant__ TransportParams P,
                                                     const __grid_constant__ WaveArgs A)
 {
     extern __shared__ __align__(16) unsigned char smem[];
