@@ -21,7 +21,7 @@ constexpr int kBlock = 128; // threads per block of every transport kernel (mu-t
 
 constexpr unsigned kFull = 0xffffffffu;
 enum : int { T_NONE = -1, T_FREE = 0, T_SCORE = 1 };
-enum : int { K_PE = 0, K_COMPTON = 1, K_RAYLEIGH = 2 };
+enum : int { K_NONE = -1, K_PE = 0, K_COMPTON = 1, K_RAYLEIGH = 2 };
 
 // ------------------------------------------------------------ smem layout
 // A history's Philox stream (REF rng.hpp:11-67): counter {block, photon, bin,
@@ -653,11 +653,16 @@ __device__ __forceinline__ uint32_t score_pixel(const TransportParams& P, double
 }
 
 // Free-path completion: the reference's per-history event logic
-// (run_history :141-223) on the history's own Philox stream.
+// (run_history :141-223) on the history's own Philox stream, in two phases:
+// event_select (escape / interaction choice / the scoring rays, REF
+// :141-194) returns the interaction kind, and event_continue (the scattered
+// photon, cap and roulette, REF :195-223) follows for Compton and Rayleigh.
+// The stream is handed over in the slot, so the wavefront engine can run the
+// two phases for different lanes (continuations gathered by kind).
 template <int FMT, class Q>
-__device__ __noinline__ void history_event(const TransportParams& P, const Block& B, const Q qs, int s,
-                                           bool hit, double t_hit, int vix, int viy, int viz,
-                                           uint64_t var_base, DevStatus* st)
+__device__ __noinline__ int event_select(const TransportParams& P, const Block& B, const Q qs, int s,
+                                         bool hit, double t_hit, int vix, int viy, int viz,
+                                         uint64_t var_base, DevStatus* st)
 {
     Slot& S = qs.slot(s);
     const int bin = S.bin;
@@ -665,7 +670,7 @@ __device__ __noinline__ void history_event(const TransportParams& P, const Block
     if (!hit) {
         ledger_add(P, B, 1, W, st, bin);
         end_history(P, B, qs, s, var_base, st);
-        return;
+        return K_NONE;
     }
     SlotRng rng = S.rng;
     const V3 dir = v3(S.dx, S.dy, S.dz);
@@ -691,7 +696,7 @@ __device__ __noinline__ void history_event(const TransportParams& P, const Block
     if (kind == K_PE) {
         ledger_add(P, B, 2, W, st, bin);
         end_history(P, B, qs, s, var_base, st);
-        return;
+        return K_PE;
     }
     S.px = pos.x;
     S.py = pos.y;
@@ -724,6 +729,22 @@ __device__ __noinline__ void history_event(const TransportParams& P, const Block
             qs.push_score(qbase + k, s, score_pixel(P, uu, uv));
         }
     }
+    S.rng = rng;
+    return kind;
+}
+
+template <class Q>
+__device__ __noinline__ void event_continue(const TransportParams& P, const Block& B, const Q qs, int s,
+                                            uint64_t var_base, DevStatus* st)
+{
+    Slot& S = qs.slot(s);
+    SlotRng rng = S.rng;
+    const int bin = S.bin;
+    const double W = S.W;
+    const double E = S.e_in;
+    const int kind = S.kind;
+    const V3 dir = v3(S.ix, S.iy, S.iz);
+    const MatDesc& md = P.mats[S.mat];
     // continuation (REF :195-205)
     V3 ndir;
     double nE = E;
@@ -819,6 +840,16 @@ __device__ __noinline__ void history_event(const TransportParams& P, const Block
     } else {
         end_history(P, B, qs, s, var_base, st);
     }
+}
+
+template <int FMT, class Q>
+__device__ __forceinline__ void history_event(const TransportParams& P, const Block& B, const Q qs, int s,
+                                              bool hit, double t_hit, int vix, int viy, int viz,
+                                              uint64_t var_base, DevStatus* st)
+{
+    const int kind = event_select<FMT>(P, B, qs, s, hit, t_hit, vix, viy, viz, var_base, st);
+    if (kind == K_COMPTON || kind == K_RAYLEIGH)
+        event_continue(P, B, qs, s, var_base, st);
 }
 
 // History start (REF run_history :120-138, sample_emission :73-87).

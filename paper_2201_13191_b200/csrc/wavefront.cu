@@ -478,16 +478,44 @@ __global__ void __launch_bounds__(kBlock) wave_event(const __grid_constant__ Tra
     uint32_t c_int = 0;
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
-    // Escapes (no interaction) are cheap and run where they are found; the
-    // interactions are gathered per warp and run 32 at a time, so the long
-    // sampling code executes with full warps.
-    __shared__ uint32_t hits[kBlock / 32][64];
-    uint32_t* hb = hits[threadIdx.x >> 5];
-    uint32_t nb = 0; // warp-uniform
-    auto interact = [&](uint32_t i) {
-        const int s = (int)in.free[i - n_s];
-        history_event<FMT>(P, B, qs, s, true, R.res[i], R.res_vox[i], R.res_vox[R.cap + i],
-                           R.res_vox[2ull * R.cap + i], var_base_of(P, s), P.status);
+    // Escapes (no interaction) are cheap and run where they are found.  The
+    // interactions are gathered per warp and their selection phase (event_select)
+    // runs 32 at a time; its Compton and Rayleigh continuations are gathered
+    // again by kind, so each sampler runs with full warps of its own kind.
+    __shared__ uint32_t bufs[kBlock / 32][3][64]; // hits (ray index), Compton, Rayleigh (slot)
+    uint32_t* hb = bufs[threadIdx.x >> 5][0];
+    uint32_t* cb = bufs[threadIdx.x >> 5][1];
+    uint32_t* rb = bufs[threadIdx.x >> 5][2];
+    uint32_t nb = 0, nc = 0, nr = 0; // warp-uniform fill levels
+    auto cont = [&](uint32_t* q, uint32_t& n, bool all) { // run 32 (or, at the end, all) continuations
+        if (all ? n == 0 : n < 32)
+            return;
+        const uint32_t take = n < 32 ? n : 32;
+        const uint32_t sl = (uint32_t)lane < take ? q[n - take + lane] : 0u;
+        __syncwarp();
+        n -= take;
+        if ((uint32_t)lane < take)
+            event_continue(P, B, qs, (int)sl, var_base_of(P, (int)sl), P.status);
+        __syncwarp();
+    };
+    auto select = [&](bool active, uint32_t i) { // selection phase for the lanes with `active`
+        int kind = K_NONE, s = 0;
+        if (active) {
+            s = (int)in.free[i - n_s];
+            kind = event_select<FMT>(P, B, qs, s, true, R.res[i], R.res_vox[i], R.res_vox[R.cap + i],
+                                     R.res_vox[2ull * R.cap + i], var_base_of(P, s), P.status);
+        }
+        const unsigned mc = __ballot_sync(kFull, kind == K_COMPTON);
+        const unsigned mr = __ballot_sync(kFull, kind == K_RAYLEIGH);
+        if (kind == K_COMPTON)
+            cb[nc + __popc(mc & lt_mask)] = (uint32_t)s;
+        if (kind == K_RAYLEIGH)
+            rb[nr + __popc(mr & lt_mask)] = (uint32_t)s;
+        nc += __popc(mc);
+        nr += __popc(mr);
+        __syncwarp();
+        cont(cb, nc, false);
+        cont(rb, nr, false);
     };
     for (;;) {
         uint32_t base = 0;
@@ -513,12 +541,19 @@ __global__ void __launch_bounds__(kBlock) wave_event(const __grid_constant__ Tra
             const uint32_t j = hb[nb - 32 + lane];
             __syncwarp();
             nb -= 32;
-            interact(j);
+            select(true, j);
         }
         __syncwarp();
     }
-    if ((uint32_t)lane < nb)
-        interact(hb[lane]);
+    if (nb > 0) {
+        const uint32_t j = (uint32_t)lane < nb ? hb[lane] : 0u;
+        const bool act = (uint32_t)lane < nb;
+        __syncwarp();
+        nb = 0;
+        select(act, j);
+    }
+    cont(cb, nc, true);
+    cont(rb, nr, true);
     if (c_int)
         atomicAdd(B.diag + 4, (unsigned long long)c_int);
     flush_stats(P, B);
