@@ -588,14 +588,19 @@ __global__ void __launch_bounds__(kBlock) wave_admit(const __grid_constant__ Tra
     const uint32_t k = ctl->admit_n;
     if (k == 0)
         return;
-    const Block B = block_stats(P, acc);
+    // the bin search of history_start runs on a shared-memory copy of the
+    // bin offsets (after the block statistics)
+    uint64_t* sstart = reinterpret_cast<uint64_t*>(acc + 8 * P.n_bins + 32);
+    for (int i = threadIdx.x; i <= P.n_bins; i += blockDim.x)
+        sstart[i] = P.bin_start[i];
+    const Block B = block_stats(P, acc); // (synchronises)
     const int32_t top = ctl->free_top;
     const unsigned long long base = ctl->admit_base;
     const uint32_t qb = ctl->admit_q;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < k; i += gridDim.x * blockDim.x) {
         const int s = (int)ctl->free_stack[top + i];
         const GlobalQ qs{A.slots, ctl, A.cur, (int)(qb + i)};
-        history_start(P, B, qs, P.bin_start, s, base + i, P.status);
+        history_start(P, B, qs, sstart, s, base + i, P.status);
     }
     flush_stats(P, B);
 }
@@ -838,8 +843,9 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
                                    (int)stat_smem));
     XSW_CHECK(cudaFuncSetAttribute((const void*)wave_score, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)stat_smem));
+    const size_t admit_smem = stat_smem + (size_t)(P.n_bins + 1) * 8;
     XSW_CHECK(cudaFuncSetAttribute((const void*)wave_admit, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)stat_smem));
+                                   (int)admit_smem));
     int walk_per_sm = 0;
     XSW_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&walk_per_sm, K.walk, kBlock, mu_smem));
     if (walk_per_sm < 1)
@@ -859,7 +865,7 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
     XSW_CHECK(resident((const void*)K.event, stat_smem, &g_work));
     XSW_CHECK(resident((const void*)K.setup, mu_smem, &g_setup));
     XSW_CHECK(resident((const void*)wave_score, stat_smem, &g_score));
-    XSW_CHECK(resident((const void*)wave_admit, stat_smem, &g_admit));
+    XSW_CHECK(resident((const void*)wave_admit, admit_smem, &g_admit));
 
     if (start) // buffers are allocated: the timed region starts here
         XSW_CHECK(cudaEventRecord(start, s));
@@ -885,7 +891,7 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
         w.done = false;
         w.A.cur = 0;
         wave_plan<<<1, 1, 0, ps>>>(w.P, w.A);
-        wave_admit<<<g_admit, kBlock, stat_smem, ps>>>(w.P, w.A);
+        wave_admit<<<g_admit, kBlock, admit_smem, ps>>>(w.P, w.A);
         XSW_CHECK(cudaGetLastError());
         launches += 3;
     }
@@ -912,7 +918,7 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
                 K.event<<<g_work, kBlock, stat_smem, ps>>>(w.P, A);
                 A.cur = w.cur ^ 1;
                 wave_plan<<<1, 1, 0, ps>>>(w.P, A);
-                wave_admit<<<g_admit, kBlock, stat_smem, ps>>>(w.P, A);
+                wave_admit<<<g_admit, kBlock, admit_smem, ps>>>(w.P, A);
                 w.cur ^= 1;
                 ++w.waves;
                 launches += 6;
