@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <functional>
 #include <string>
 #include <thread>
 #include <vector>
@@ -187,6 +188,10 @@ struct xs_context {
     DevBuf<double> img, var, pp_a, pp_b, pp_c, pp_k;
     DevBuf<xsd::InterpEntry> interp_tab;
     DevBuf<uint8_t> lvl_scratch;
+    DevBuf<double> scan_img[2]; // run_scan: double-buffered scatter images ...
+    PinBuf<double> scan_pin[2]; // ... and their pinned staging
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t scan_ev[2] = {nullptr, nullptr}, scan_done[2] = {nullptr, nullptr};
     DevBuf<double> cc_in[3], cc_out, cc_tmp, cc_sg, cc_full;
     DevBuf<unsigned long long> cc_stats;
     int smem_kb = 48; // per transport block: 4 blocks/SM leave 60 KB of L1
@@ -850,6 +855,16 @@ void xs_ctx_destroy(xs_context* c)
     c->var_pix.release();
     c->interp_tab.release();
     c->lvl_scratch.release();
+    for (int b = 0; b < 2; ++b) {
+        c->scan_img[b].release();
+        c->scan_pin[b].release();
+        if (c->scan_ev[b])
+            cudaEventDestroy(c->scan_ev[b]);
+        if (c->scan_done[b])
+            cudaEventDestroy(c->scan_done[b]);
+    }
+    if (c->copy_stream)
+        cudaStreamDestroy(c->copy_stream);
     for (auto& b : c->cc_in)
         b.release();
     for (auto* b : {&c->cc_out, &c->cc_tmp, &c->cc_sg, &c->cc_full})
@@ -1135,18 +1150,61 @@ int xs_run_scan(xs_context* c, const xs_geometry* g, const xs_spectrum* spec, co
                 fail(XS_E_OUT_OF_RANGE, "run_scan: angle index %d out of range", subset[i]);
         const bool want_primary = what != 1, want_scatter = what != 0;
         const size_t np = (size_t)g->nu * g->nv;
+        // Scatter images leave through a copy stream and pinned staging (double
+        // buffered): the D2H and the host copy of angle i overlap the
+        // transport of angle i + 1.
+        if (!c->copy_stream)
+            cuda_check(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking), "stream");
+        for (int b = 0; b < 2; ++b) {
+            if (!c->scan_ev[b])
+                cuda_check(cudaEventCreateWithFlags(&c->scan_ev[b], cudaEventDisableTiming), "event");
+            if (!c->scan_done[b])
+                cuda_check(cudaEventCreateWithFlags(&c->scan_done[b], cudaEventDisableTiming), "event");
+        }
+        std::thread copier[2];
+        auto drain = [&](int b) {
+            if (copier[b].joinable())
+                copier[b].join();
+        };
+        struct Joiner {
+            std::function<void()> f;
+            ~Joiner() { f(); }
+        } join_all{[&] {
+            drain(0);
+            drain(1);
+        }};
         for (int i = 0; i < n_subset; ++i) {
             const auto t0 = std::chrono::steady_clock::now();
             try {
                 if (want_scatter) {
                     validate_call(*g, subset[i], *spec, *cfg, "simulate_scatter");
                     const Plan plan = make_plan(*g, *spec, *cfg);
+                    const int b = i & 1;
+                    drain(b); // angle i - 2's copy out of this buffer pair
                     c->accum.reserve(plan.layout.words);
                     cuda_check(cudaMemsetAsync(c->accum.p, 0, plan.layout.words * 8, c->stream), "memset");
                     accumulate(c, *g, subset[i], *spec, *cfg, 0, plan.n_hist, c->accum.p);
                     xs_scatter_result r{};
-                    r.image = scatter_out ? scatter_out + (size_t)i * np : nullptr;
-                    finalize(c, *g, *spec, *cfg, c->accum.p, 0, plan.n_hist, &r, nullptr);
+                    c->scan_img[b].reserve(np);
+                    finalize(c, *g, *spec, *cfg, c->accum.p, 0, plan.n_hist, &r, c->scan_img[b].p);
+                    if (scatter_out) {
+                        c->scan_pin[b].reserve(np);
+                        cuda_check(cudaEventRecord(c->scan_ev[b], c->stream), "event");
+                        cuda_check(cudaStreamWaitEvent(c->copy_stream, c->scan_ev[b], 0), "wait");
+                        cuda_check(cudaMemcpyAsync(c->scan_pin[b].p, c->scan_img[b].p, np * 8, cudaMemcpyDeviceToHost,
+                                                   c->copy_stream),
+                                   "D2H image");
+                        cuda_check(cudaEventRecord(c->scan_done[b], c->copy_stream), "event");
+                        double* dst = scatter_out + (size_t)i * np;
+                        const double* src = c->scan_pin[b].p;
+                        cudaEvent_t done = c->scan_done[b];
+                        copier[b] = std::thread([dst, src, np, done] {
+                            cudaEventSynchronize(done);
+                            std::memcpy(dst, src, np * 8);
+                        });
+                    }
+                    // the next angle's transport overwrites only the accumulator, and
+                    // its finalize writes the other image buffer
                 }
                 if (want_primary) {
                     validate_call(*g, subset[i], *spec, *cfg, "simulate_primary");
