@@ -460,6 +460,19 @@ int xs_correction_tail(xs_context* ctx, const double* scatter_sub, const double*
                        const double* a, int32_t nu_out, int32_t nv_out, double* corrected,
                        double* mean_scatter_fraction, uint64_t* clamped, int32_t device_ptrs);
 
+/* FDK reconstruction (REF fbp_reconstruct, recon.cpp:58-157; SURVEY.md §8(f)
+ * rank 2): cosine weighting, row ramp filter (hann = 1: Hann window, 0:
+ * Ram-Lak), distance-weighted bilinear backprojection.  `stack` holds
+ * n_views images (nv x nu, row-major) at `angles` (ascending); the volume is
+ * dims[0] x dims[1] x dims[2] floats (x fastest) in 1/m, centred on the
+ * isocenter.  Same arithmetic and order as REF: bit-identical volume.
+ * Errors as REF: empty stack, insufficient angular coverage (runtime_error). */
+int xs_fbp_reconstruct(xs_context* ctx, const double* stack, const double* angles, int32_t n_views,
+                       int32_t nu, int32_t nv, const xs_geometry* g, const int32_t dims[3],
+                       const double voxel[3], int32_t hann, float* volume, int32_t device_ptrs);
+/* REF default_voxel_size (recon.cpp:13-18). */
+void xs_default_voxel_size(const xs_geometry* g, const int32_t dims[3], double out[3]);
+
 #ifdef __cplusplus
 }
 #endif

@@ -544,6 +544,23 @@ int xr_correction_tail(const double* scatter_sub, const double* sub_angles, int3
     });
 }
 
+// recon.cpp:58-157
+int xr_fbp_reconstruct(const double* stack, const double* angles, int32_t n_views, int32_t nu, int32_t nv,
+                       const xs_geometry* g, const int32_t dims[3], const double voxel[3], int32_t hann,
+                       float* volume)
+{
+    return guarded([&] {
+        ProjectionStack s = make_stack(nu, nv, std::vector<double>(angles, angles + n_views));
+        const std::size_t np = static_cast<std::size_t>(nu) * nv;
+        for (int i = 0; i < n_views; ++i)
+            s.images[i] = image_from(stack + i * np, nu, nv);
+        const Volume v = fbp_reconstruct(s, geometry(*g), {dims[0], dims[1], dims[2]},
+                                         Vec3{voxel[0], voxel[1], voxel[2]},
+                                         hann ? RampWindow::hann : RampWindow::ramlak, 1);
+        std::memcpy(volume, v.values.data(), v.values.size() * sizeof(float));
+    });
+}
+
 // synthetic.cpp:101-178: phantom generators, to pin the host-side fixtures.
 // kind 0 cube(edge), 1 cylinder(radius, height), 2 rods(body_r, height,
 // n_rods, rod_r, ring_r, rod_density), 3 cylinder_head(insert_density).

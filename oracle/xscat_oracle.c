@@ -2135,3 +2135,128 @@ int xo_correction_tail(const double* scatter_sub, const double* sub_angles, int3
     return rc;
 }
 
+/* ------------------------------------------------------------------ FDK */
+/* REF fbp_reconstruct (recon.cpp:58-157): cosine weighting, direct row
+ * convolution with the ramp kernel (recon.cpp:23-43), distance-weighted
+ * bilinear backprojection accumulated in float in view order, x 100. */
+static double xo_ramlak(int k, double du)
+{
+    const double pi = 3.14159265358979323846;
+    if (k == 0)
+        return 1.0 / (8.0 * du * du);
+    if (k % 2 == 0)
+        return 0.0;
+    return -1.0 / (2.0 * pi * pi * k * k * du * du);
+}
+
+int xo_fbp_reconstruct(const double* stack, const double* angles, int32_t n_views, int32_t nu, int32_t nv,
+                       const xs_geometry* g, const int32_t dims[3], const double voxel[3], int32_t hann,
+                       float* volume)
+{
+    const double pi = 3.14159265358979323846;
+    const double fan = 2.0 * atan(0.5 * g->nu * g->pixel_pitch / g->sdd);
+    double span = 0.0, R, D, du, dv, x0, y0, z0;
+    double *kern, *dbeta, *q, *w;
+    size_t np = (size_t)nu * nv, nvox = (size_t)dims[0] * dims[1] * dims[2], p;
+    int i, k, iv, iu, j, view, ix, iy, iz;
+    if (n_views <= 0) {
+        snprintf(tl_last, sizeof tl_last, "fbp: empty projection stack");
+        return XS_E_RUNTIME;
+    }
+    if (n_views >= 2) {
+        double max_gap = 2.0 * pi + angles[0] - angles[n_views - 1];
+        for (i = 1; i < n_views; ++i)
+            if (angles[i] - angles[i - 1] > max_gap)
+                max_gap = angles[i] - angles[i - 1];
+        span = 2.0 * pi - max_gap;
+    }
+    if (n_views < 2 || span + 1e-9 < pi + fan) {
+        snprintf(tl_last, sizeof tl_last, "fbp: insufficient angular coverage (need >= 180 deg + fan)");
+        return XS_E_RUNTIME;
+    }
+    R = g->sod;
+    D = g->sdd;
+    du = g->pixel_pitch * R / D;
+    dv = du;
+    dbeta = (double*)malloc(sizeof(double) * n_views);
+    for (i = 0; i < n_views; ++i) {
+        const double prev = (i == 0) ? angles[n_views - 1] - 2.0 * pi : angles[i - 1];
+        const double next = (i == n_views - 1) ? angles[0] + 2.0 * pi : angles[i + 1];
+        dbeta[i] = 0.5 * (next - prev);
+    }
+    kern = (double*)malloc(sizeof(double) * (2 * (size_t)nu - 1));
+    for (k = -(nu - 1); k <= nu - 1; ++k) {
+        double v = xo_ramlak(k, du);
+        if (hann)
+            v = 0.5 * xo_ramlak(k, du) + 0.25 * (xo_ramlak(k - 1, du) + xo_ramlak(k + 1, du));
+        kern[k + nu - 1] = v;
+    }
+    q = (double*)malloc(sizeof(double) * np * n_views);
+    w = (double*)malloc(sizeof(double) * np);
+    for (view = 0; view < n_views; ++view) {
+        const double* img = stack + (size_t)view * np;
+        for (iv = 0; iv < nv; ++iv) {
+            const double vv = (iv + 0.5 - 0.5 * nv) * dv;
+            for (iu = 0; iu < nu; ++iu) {
+                const double uu = (iu + 0.5 - 0.5 * nu) * du;
+                w[(size_t)iv * nu + iu] = img[(size_t)iv * nu + iu] * R / sqrt(R * R + uu * uu + vv * vv);
+            }
+        }
+        for (iv = 0; iv < nv; ++iv) {
+            const double* row = w + (size_t)iv * nu;
+            double* out = q + (size_t)view * np + (size_t)iv * nu;
+            for (i = 0; i < nu; ++i) {
+                double s = 0.0;
+                for (j = 0; j < nu; ++j)
+                    s += row[j] * kern[i - j + nu - 1];
+                out[i] = s * du;
+            }
+        }
+    }
+    for (p = 0; p < nvox; ++p)
+        volume[p] = 0.0f;
+    x0 = -0.5 * dims[0] * voxel[0];
+    y0 = -0.5 * dims[1] * voxel[1];
+    z0 = -0.5 * dims[2] * voxel[2];
+    for (iz = 0; iz < dims[2]; ++iz) {
+        const double z = z0 + (iz + 0.5) * voxel[2];
+        for (view = 0; view < n_views; ++view) {
+            const double beta = angles[view];
+            const double cb = cos(beta), sb = sin(beta);
+            const double* qv = q + (size_t)view * np;
+            for (iy = 0; iy < dims[1]; ++iy) {
+                const double y = y0 + (iy + 0.5) * voxel[1];
+                for (ix = 0; ix < dims[0]; ++ix) {
+                    const double x = x0 + (ix + 0.5) * voxel[0];
+                    const double s_comp = x * cb + y * sb;
+                    const double t_comp = -x * sb + y * cb;
+                    const double L = R - s_comp;
+                    double pu, pv, fu, fv, val;
+                    int u0, v0;
+                    if (L <= 1e-9)
+                        continue;
+                    pu = (R * t_comp / L) / du + 0.5 * nu - 0.5;
+                    pv = (R * z / L) / dv + 0.5 * nv - 0.5;
+                    if (pu < 0.0 || pu > nu - 1 || pv < 0.0 || pv > nv - 1)
+                        continue;
+                    u0 = (int)pu < nu - 2 ? (int)pu : nu - 2;
+                    v0 = (int)pv < nv - 2 ? (int)pv : nv - 2;
+                    fu = pu - u0;
+                    fv = pv - v0;
+                    val = (1 - fu) * (1 - fv) * qv[(size_t)v0 * nu + u0] + fu * (1 - fv) * qv[(size_t)v0 * nu + u0 + 1] +
+                          (1 - fu) * fv * qv[(size_t)(v0 + 1) * nu + u0] + fu * fv * qv[(size_t)(v0 + 1) * nu + u0 + 1];
+                    volume[(size_t)ix + (size_t)dims[0] * ((size_t)iy + (size_t)dims[1] * iz)] +=
+                        (float)(dbeta[view] * R * R / (L * L) * val);
+                }
+            }
+        }
+    }
+    for (p = 0; p < nvox; ++p)
+        volume[p] *= 100.0f;
+    free(dbeta);
+    free(kern);
+    free(q);
+    free(w);
+    return XS_OK;
+}
+

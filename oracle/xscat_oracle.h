@@ -105,6 +105,11 @@ int xo_correction_tail(const double* scatter_sub, const double* sub_angles, int3
                        int32_t nv, int32_t sg_window, int32_t sg_order, const double* a, int32_t nu_out,
                        int32_t nv_out, double* corrected, double* mean_fraction, uint64_t* clamped);
 
+/* FDK (REF recon.cpp:58-157). */
+int xo_fbp_reconstruct(const double* stack, const double* angles, int32_t n_views, int32_t nu, int32_t nv,
+                       const xs_geometry* g, const int32_t dims[3], const double voxel[3], int32_t hann,
+                       float* volume);
+
 #ifdef __cplusplus
 }
 #endif

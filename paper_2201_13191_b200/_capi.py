@@ -232,6 +232,10 @@ SIGNATURES = {
                                     C.c_int32, C.c_int32]),
     "xs_downsample_average": (C.c_int, [_P, _P, C.c_int32, C.c_int32, C.c_int32, _P,
                                         C.c_int32, C.c_int32, C.c_int32]),
+    "xs_fbp_reconstruct": (C.c_int, [_P, _P, _P, C.c_int32, C.c_int32, C.c_int32,
+                                     C.POINTER(XsGeometry), C.POINTER(C.c_int32), _P, C.c_int32, _P,
+                                     C.c_int32]),
+    "xs_default_voxel_size": (None, [C.POINTER(XsGeometry), C.POINTER(C.c_int32), _P]),
     "xs_intensity_to_attenuation": (C.c_int, [_P, _P, _P, C.c_int32, C.c_int32, C.c_int32, _P,
                                               C.c_int32]),
     "xs_correct_projections": (C.c_int, [_P, _P, _P, _P, C.c_int32, C.c_int32, C.c_int32, _P,

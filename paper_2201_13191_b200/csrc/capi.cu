@@ -29,6 +29,12 @@ cudaError_t launch_transport(const TransportParams& P, int grid, size_t smem, cu
 cudaError_t launch_primary(const PrimaryParams& P, cudaStream_t s);
 size_t levels_scratch_bytes(const Grid& G, const int* edges, int n_levels);
 size_t correct_stats_bytes(int n_views);
+size_t fbp_filter_smem(int nu);
+cudaError_t launch_fbp_filter(const double* in, double* out, const double* kern, int nu, int nv, int n_views,
+                              double R, double du, double dv, cudaStream_t s);
+cudaError_t launch_fbp_backproject(const double* q, const void* views, int n_views, int nu, int nv,
+                                   const int dims[3], const double voxel[3], double R, double du, double dv,
+                                   float* vol, cudaStream_t s);
 cudaError_t launch_i2a(const double* in, const double* flat, double* out, size_t npix, int n_img, void* stats,
                        int sm_count, cudaStream_t s);
 cudaError_t launch_correct(const double* a, const double* ip, const double* is, double* out, size_t n, void* stats,
@@ -194,6 +200,8 @@ struct xs_context {
     cudaEvent_t scan_ev[2] = {nullptr, nullptr}, scan_done[2] = {nullptr, nullptr};
     DevBuf<double> cc_in[3], cc_out, cc_tmp, cc_sg, cc_full;
     DevBuf<unsigned long long> cc_stats;
+    DevBuf<double> fbp_in, fbp_q, fbp_k, fbp_views;
+    DevBuf<float> fbp_vol;
     int smem_kb = 48; // per transport block: 4 blocks/SM leave 60 KB of L1
     int max_slots = 64;
     int macro_skip = 1;
@@ -870,6 +878,9 @@ void xs_ctx_destroy(xs_context* c)
     for (auto* b : {&c->cc_out, &c->cc_tmp, &c->cc_sg, &c->cc_full})
         b->release();
     c->cc_stats.release();
+    for (auto* b : {&c->fbp_in, &c->fbp_q, &c->fbp_k, &c->fbp_views})
+        b->release();
+    c->fbp_vol.release();
     xsd::wave_destroy(c->wave);
     if (c->ev0)
         cudaEventDestroy(c->ev0);
@@ -1512,6 +1523,94 @@ int xs_correction_tail(xs_context* c, const double* scatter_sub, const double* s
             cuda_check(cudaMemcpyAsync(corrected, o, npo * n_full * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
             cuda_check(cudaStreamSynchronize(c->stream), "D2H");
         }
+    });
+}
+
+// ------------------------------------------------------------------- FDK
+void xs_default_voxel_size(const xs_geometry* g, const int32_t dims[3], double out[3])
+{
+    // REF recon.cpp:13-18
+    const double fov = g->nu * g->pixel_pitch * g->sod / g->sdd;
+    const double h = fov / std::max({dims[0], dims[1], dims[2]});
+    out[0] = out[1] = out[2] = h;
+}
+
+int xs_fbp_reconstruct(xs_context* c, const double* stack, const double* angles, int32_t n_views, int32_t nu,
+                       int32_t nv, const xs_geometry* g, const int32_t dims[3], const double voxel[3],
+                       int32_t hann, float* volume, int32_t device_ptrs)
+{
+    return guard(c, [&] {
+        if (n_views <= 0)
+            fail(XS_E_RUNTIME, "fbp: empty projection stack");
+        // REF recon.cpp:62-67: coverage >= 180 deg + fan, span = 2 pi - largest circular gap
+        const double pi = kPi;
+        const double fan = 2.0 * std::atan(0.5 * g->nu * g->pixel_pitch / g->sdd);
+        double span = 0.0;
+        if (n_views >= 2) {
+            double max_gap = 2.0 * pi + angles[0] - angles[n_views - 1];
+            for (int i = 1; i < n_views; ++i)
+                max_gap = std::max(max_gap, angles[i] - angles[i - 1]);
+            span = 2.0 * pi - max_gap;
+        }
+        if (n_views < 2 || span + 1e-9 < pi + fan)
+            fail(XS_E_RUNTIME, "fbp: insufficient angular coverage (need >= 180 deg + fan)");
+        if (dims[0] <= 0 || dims[1] <= 0 || dims[2] <= 0 || nu < 2 || nv < 2)
+            fail(XS_E_RUNTIME, "fbp: degenerate dimensions");
+        const double R = g->sod, D = g->sdd;
+        const double du = g->pixel_pitch * R / D, dv = du;
+        // REF recon.cpp:23-43 ramp kernel (Hann = (1/4, 1/2, 1/4) smoothing of Ram-Lak)
+        auto ramlak = [&](int k) -> double {
+            if (k == 0)
+                return 1.0 / (8.0 * du * du);
+            if (k % 2 == 0)
+                return 0.0;
+            return -1.0 / (2.0 * pi * pi * k * k * du * du);
+        };
+        std::vector<double> kern(2 * (size_t)nu - 1);
+        for (int k = -(nu - 1); k <= nu - 1; ++k) {
+            double v = ramlak(k);
+            if (hann)
+                v = 0.5 * ramlak(k) + 0.25 * (ramlak(k - 1) + ramlak(k + 1));
+            kern[k + nu - 1] = v;
+        }
+        // REF :76-82 per-view angular weights; cos / sin of the view angles (glibc)
+        std::vector<double> views(3 * (size_t)n_views);
+        for (int i = 0; i < n_views; ++i) {
+            const double prev = (i == 0) ? angles[n_views - 1] - 2.0 * pi : angles[i - 1];
+            const double next = (i == n_views - 1) ? angles[0] + 2.0 * pi : angles[i + 1];
+            views[3 * i + 0] = std::cos(angles[i]);
+            views[3 * i + 1] = std::sin(angles[i]);
+            views[3 * i + 2] = 0.5 * (next - prev);
+        }
+        cudaStream_t st = c->stream;
+        const size_t np = (size_t)nu * nv * n_views, nvox = (size_t)dims[0] * dims[1] * dims[2];
+        const double* in = stack;
+        if (!device_ptrs) {
+            c->fbp_in.reserve(np);
+            cuda_check(cudaMemcpyAsync(c->fbp_in.p, stack, np * 8, cudaMemcpyHostToDevice, st), "H2D");
+            in = c->fbp_in.p;
+        }
+        c->fbp_q.reserve(np);
+        c->fbp_k.reserve(kern.size());
+        c->fbp_views.reserve(views.size());
+        cuda_check(cudaMemcpyAsync(c->fbp_k.p, kern.data(), kern.size() * 8, cudaMemcpyHostToDevice, st), "H2D");
+        cuda_check(cudaMemcpyAsync(c->fbp_views.p, views.data(), views.size() * 8, cudaMemcpyHostToDevice, st),
+                   "H2D");
+        if (xsd::fbp_filter_smem(nu) > 227 * 1024)
+            fail(XS_E_UNSUPPORTED, "fbp: detector rows of %d pixels exceed the shared-memory filter", nu);
+        cuda_check(xsd::launch_fbp_filter(in, c->fbp_q.p, c->fbp_k.p, nu, nv, n_views, R, du, dv, st), "fbp filter");
+        float* vol = volume;
+        if (!device_ptrs) {
+            c->fbp_vol.reserve(nvox);
+            vol = c->fbp_vol.p;
+        }
+        const int d3[3] = {dims[0], dims[1], dims[2]};
+        cuda_check(xsd::launch_fbp_backproject(c->fbp_q.p, c->fbp_views.p, n_views, nu, nv, d3, voxel, R, du, dv,
+                                               vol, st),
+                   "fbp backprojection");
+        if (!device_ptrs)
+            cuda_check(cudaMemcpyAsync(volume, vol, nvox * 4, cudaMemcpyDeviceToHost, st), "D2H");
+        cuda_check(cudaStreamSynchronize(st), "fbp");
     });
 }
 

@@ -397,3 +397,35 @@ def correction_tail(scatter_sub, sub_angles, primary_mc, full_angles, f: SgFilte
                                          C.byref(frac), C.byref(clamped), 0))
     return out, float(frac.value), int(clamped.value)
 
+
+# -------------------------------------------------------------------- FDK
+RAMLAK, HANN = 0, 1
+
+
+def default_voxel_size(g: I.ScanGeometry, dims) -> np.ndarray:
+    """REF default_voxel_size (recon.cpp:13-18)."""
+    pk = A.Packed()
+    d = (C.c_int32 * 3)(*dims)
+    out = np.zeros(3)
+    A.lib().xs_default_voxel_size(C.byref(pk.geometry(g)), d, A.dptr(out))
+    return out
+
+
+def fbp_reconstruct(stack: ProjectionStack, g: I.ScanGeometry, dims, voxel_size=None, window: int = HANN,
+                    ctx: Optional[Context] = None) -> np.ndarray:
+    """REF fbp_reconstruct (recon.cpp:58-157): FDK of an attenuation stack;
+    returns the float32 volume (dims[2], dims[1], dims[0]) in 1/m."""
+    ctx = ctx or default_context()
+    imgs = np.ascontiguousarray(stack.images, dtype=np.float64)
+    ang = np.ascontiguousarray(stack.angle_values, dtype=np.float64)
+    n, nv, nu = imgs.shape
+    vx = np.ascontiguousarray(default_voxel_size(g, dims) if voxel_size is None else voxel_size,
+                              dtype=np.float64)
+    out = np.empty((dims[2], dims[1], dims[0]), np.float32)
+    pk = A.Packed()
+    d = (C.c_int32 * 3)(*dims)
+    ctx.check(A.lib().xs_fbp_reconstruct(ctx.h, imgs.ctypes.data, A.dptr(ang), n, nu, nv,
+                                         C.byref(pk.geometry(g)), d, A.dptr(vx), int(window),
+                                         out.ctypes.data, 0))
+    return out
+

@@ -63,6 +63,8 @@ def _sig(L, prefix):
         f"{p}_correction_tail": (C.c_int, [_dp, _dp, C.c_int32, _dp, _dp, C.c_int32, C.c_int32,
                                            C.c_int32, C.c_int32, C.c_int32, _dp, C.c_int32,
                                            C.c_int32, _dp, _dp, A.c_u64_p]),
+        f"{p}_fbp_reconstruct": (C.c_int, [_dp, _dp, C.c_int32, C.c_int32, C.c_int32, _g,
+                                           C.POINTER(C.c_int32), _dp, C.c_int32, C.c_void_p]),
         f"{p}_last_error": (C.c_char_p, []),
     }
     if prefix == "xo":
@@ -282,6 +284,20 @@ class Oracle:
                                               nv, window, order, A.dptr(a), nu_out, nv_out, A.dptr(out),
                                               C.byref(frac), C.byref(cl)))
         return out, float(frac.value), int(cl.value)
+
+
+    def fbp_reconstruct(self, stack, angles, g, dims, voxel, hann=True):
+        from paper_2201_13191_b200 import _capi as A_
+        st = np.ascontiguousarray(stack, np.float64)
+        an = np.ascontiguousarray(angles, np.float64)
+        n, nv, nu = st.shape
+        d = (C.c_int32 * 3)(*dims)
+        vx = np.ascontiguousarray(voxel, np.float64)
+        out = np.zeros((dims[2], dims[1], dims[0]), np.float32)
+        pk = A_.Packed()
+        self.check(self.fn("fbp_reconstruct")(A.dptr(st), A.dptr(an), n, nu, nv, C.byref(pk.geometry(g)), d,
+                                              A.dptr(vx), 1 if hann else 0, out.ctypes.data))
+        return out
 
 
 _oracle = None
