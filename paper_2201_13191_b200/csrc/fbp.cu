@@ -7,8 +7,9 @@
 //     (Hann-windowed) ramp kernel, each output summed over j = 0..nu-1 in
 //     order, times du.  Register tiling: a thread owns T outputs and walks j
 //     in steps of T with the 2T-1 kernel taps of the step in registers, so
-//     one T x T tile costs 3T - 1 shared-memory loads for T^2 fp64 MACs
-//     (the convolution is fp64-pipe bound, not shared-memory bound).
+//     one T x T tile costs 3T - 1 shared-memory loads for T^2 fp64 MACs; the
+//     kernel taps are stored with a one-word skew per 8 so the loads are free
+//     of bank conflicts.
 //   * backprojection: one thread per voxel, views in REF's order, each view's
 //     contribution formed in fp64 and added to a float accumulator exactly
 //     like REF's `vol.at(...) += static_cast<float>(...)`.
@@ -32,12 +33,15 @@ __global__ void __launch_bounds__(kFiltThr) fbp_filter_kernel(const double* __re
                                                                int rows_per_block, double R, double du, double dv)
 {
     extern __shared__ double sm[];
-    double* K = sm;                       // K[m + kT - 1] = kernel[m], zero padding on both sides
-    double* row = sm + 2 * nu - 1 + 2 * (kT - 1); // nu entries + kT zero tail
+    // logical K[k] = kernel[k - (kT - 1)] (zero outside), stored at k + k / 8:
+    // a thread reads taps 8 apart from its neighbour, and the one-word skew
+    // per 8 spreads a half-warp's 64-bit loads over all banks (stride 9)
+    double* K = sm;
     const int nk = 2 * nu - 1 + 2 * (kT - 1);
+    double* row = sm + nk + nk / 8 + 1; // nu entries + kT zero tail
     for (int m = threadIdx.x; m < nk; m += blockDim.x) {
         const int src = m - (kT - 1);
-        K[m] = (src >= 0 && src < 2 * nu - 1) ? kern[src] : 0.0;
+        K[m + (m >> 3)] = (src >= 0 && src < 2 * nu - 1) ? kern[src] : 0.0;
     }
     const int view = blockIdx.x;
     const double* img = in + (size_t)view * nu * nv;
@@ -60,13 +64,16 @@ __global__ void __launch_bounds__(kFiltThr) fbp_filter_kernel(const double* __re
 #pragma unroll
             for (int t = 0; t < kT; ++t)
                 s[t] = 0.0;
-            // output i = i0 + t, tap j: kernel[i - j + nu - 1] = K[i - j + nu - 1 + kT - 1]
-            const int base = i0 + nu - 1 + (kT - 1);
+            // output i = i0 + t, tap j: kernel[i - j + nu - 1] = K[i - j + nu - 1 + kT - 1];
+            // tile (i0 + t, j0 + u) uses kk[t - u + kT - 1] = K[kb + m], kb = i0 - j0 + nu - 1
+            const int r = (nu - 1) & 7; // kb mod 8 (i0, j0 are multiples of kT = 8)
             for (int j0 = 0; j0 < nu; j0 += kT) {
-                double kk[2 * kT - 1]; // kk[m] = K[base - j0 - (kT - 1) + m]
+                const int kb = i0 - j0 + nu - 1;
+                const double* kp = K + kb + (kb >> 3);
+                double kk[2 * kT - 1]; // kk[m] = K[kb + m] at kb + m + (kb + m) / 8
 #pragma unroll
                 for (int m = 0; m < 2 * kT - 1; ++m)
-                    kk[m] = K[base - j0 - (kT - 1) + m];
+                    kk[m] = kp[m + ((r + m) >> 3)];
                 if (j0 + kT <= nu) {
 #pragma unroll
                     for (int u = 0; u < kT; ++u) {
@@ -143,7 +150,11 @@ __global__ void fbp_backproject_kernel(const double* __restrict__ q, const BpVie
 
 } // namespace
 
-size_t fbp_filter_smem(int nu) { return (size_t)(2 * nu - 1 + 2 * (kT - 1) + nu + kT) * sizeof(double); }
+size_t fbp_filter_smem(int nu)
+{
+    const int nk = 2 * nu - 1 + 2 * (kT - 1);
+    return (size_t)(nk + nk / 8 + 1 + nu + kT) * sizeof(double);
+}
 
 cudaError_t launch_fbp_filter(const double* in, double* out, const double* kern, int nu, int nv, int n_views,
                               double R, double du, double dv, cudaStream_t s)
