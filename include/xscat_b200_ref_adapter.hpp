@@ -21,6 +21,8 @@
 // receives it on every call; Projector keeps it resident across calls.
 #pragma once
 
+#include <algorithm>
+#include <array>
 #include <cstdlib>
 #include <memory>
 #include <stdexcept>
@@ -435,6 +437,43 @@ inline xscat::ProjectionStack correction_tail(const xscat::ProjectionStack& scat
     if (clamped_count)
         *clamped_count = static_cast<std::size_t>(clamped);
     return detail::unflatten(out, a.nu, a.nv, a.angle_values);
+}
+
+// REF recon.hpp default_voxel_size (recon.cpp:13-18)
+inline xscat::Vec3 default_voxel_size(const xscat::ScanGeometry& g, const std::array<int, 3>& out_dims)
+{
+    const double fov = g.nu * g.pixel_pitch * g.sod / g.sdd;
+    const double h = fov / std::max({out_dims[0], out_dims[1], out_dims[2]});
+    return {h, h, h};
+}
+
+// REF recon.hpp fbp_reconstruct (recon.cpp:58-157) on the device; `workers`
+// is accepted and ignored (the result does not depend on it).
+inline xscat::Volume fbp_reconstruct(const xscat::ProjectionStack& stack, const xscat::ScanGeometry& g,
+                                     const std::array<int, 3>& out_dims, const xscat::Vec3& voxel_size,
+                                     xscat::RampWindow window = xscat::RampWindow::hann, int workers = 1)
+{
+    (void)workers;
+    if (stack.images.empty())
+        throw std::runtime_error("fbp: empty projection stack");
+    const std::vector<double> v = detail::flatten(stack);
+    xs_geometry xg{};
+    xg.sdd = g.sdd;
+    xg.sod = g.sod;
+    xg.nu = g.nu;
+    xg.nv = g.nv;
+    xg.pixel_pitch = g.pixel_pitch;
+    xg.angles = g.angles.data();
+    xg.n_angles = static_cast<int32_t>(g.angles.size());
+    const int32_t dims[3] = {out_dims[0], out_dims[1], out_dims[2]};
+    const double vox[3] = {voxel_size.x, voxel_size.y, voxel_size.z};
+    xscat::Volume vol = xscat::make_volume(out_dims[0], out_dims[1], out_dims[2], voxel_size);
+    Context& c = thread_context();
+    throw_status(xs_fbp_reconstruct(c.get(), v.data(), stack.angle_values.data(), stack.n_angles(), stack.nu,
+                                    stack.nv, &xg, dims, vox, window == xscat::RampWindow::hann ? 1 : 0,
+                                    vol.values.data(), 0),
+                 c.get());
+    return vol;
 }
 
 } // namespace xscat_b200

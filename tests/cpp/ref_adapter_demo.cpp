@@ -159,6 +159,22 @@ int main(int argc, char** argv)
         }
         check(threw, "correct_projections throws runtime_error", "");
     }
+    { // FDK: REF fbp_reconstruct vs the device, bit for bit
+        const int nu = 24, nv = 16, n = 48;
+        ScanGeometry g = make_circular_geometry(60.0, 40.0, nu, nv, 0.5, n);
+        ProjectionStack st = make_stack(nu, nv, g.angles);
+        for (int i = 0; i < n; ++i)
+            for (int iv = 0; iv < nv; ++iv)
+                for (int iu = 0; iu < nu; ++iu)
+                    st.images[i].values[(size_t)iv * nu + iu] =
+                        std::exp(-((iu - 12.0) * (iu - 12.0) / 30.0 + (iv - 8.0) * (iv - 8.0) / 20.0)) *
+                        (1.0 + 0.1 * std::sin((double)i));
+        const std::array<int, 3> dims{12, 10, 8};
+        const Vec3 vx = xscat::default_voxel_size(g, dims);
+        const Volume a = xscat::fbp_reconstruct(st, g, dims, vx);
+        const Volume b = xscat_b200::fbp_reconstruct(st, g, dims, xscat_b200::default_voxel_size(g, dims));
+        check(a.values == b.values, "fbp_reconstruct bitwise", "");
+    }
     std::printf("%s\n", g_fail ? "FAILED" : "all checks passed");
     return g_fail ? 1 : 0;
 }
