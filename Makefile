@@ -12,7 +12,7 @@ NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -fmad=false -Xcompiler -fPIC -Xptxa
             -ccbin $(CXX_HOST) -Iinclude $(NVEXTRA)
 CXXFLAGS := -O2 -std=c++17 -fPIC -ffp-contract=off -Iinclude
 
-CU_SRCS  := $(SRC)/capi.cu $(SRC)/transport.cu $(SRC)/wavefront.cu $(SRC)/levels.cu $(SRC)/correct.cu $(SRC)/fbp.cu $(SRC)/primary.cu $(SRC)/postprocess.cu
+CU_SRCS  := $(SRC)/capi.cu $(SRC)/transport.cu $(SRC)/wavefront.cu $(SRC)/levels.cu $(SRC)/correct.cu $(SRC)/fbp.cu $(SRC)/segment.cu $(SRC)/primary.cu $(SRC)/postprocess.cu
 CU_OBJS  := $(patsubst $(SRC)/%.cu,$(OBJDIR)/%.o,$(CU_SRCS))
 CPP_OBJS := $(OBJDIR)/host_common.o
 HDRS     := $(wildcard $(SRC)/*.h $(SRC)/*.cuh) include/xscat_gpu.h

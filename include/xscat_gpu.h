@@ -473,6 +473,51 @@ int xs_fbp_reconstruct(xs_context* ctx, const double* stack, const double* angle
 /* REF default_voxel_size (recon.cpp:13-18). */
 void xs_default_voxel_size(const xs_geometry* g, const int32_t dims[3], double out[3]);
 
+/* ----------------------------------------------------------- segmentation
+ * the loop's segmentation stage (REF recon.cpp:159-322,
+ * correction.cpp:167-172) on the device.  Bit-identical to REF. */
+
+/* REF ClassSpec (recon.hpp:32-35). */
+typedef struct xs_class_spec {
+    int32_t material_id; /* 0 = vacuum */
+    double density;      /* g/cm^3 */
+} xs_class_spec;
+
+/* REF otsu_thresholds (recon.hpp:27-29, recon.cpp:159-240): n_classes - 1
+ * ascending thresholds (host array) of a dims[0] x dims[1] x dims[2] float
+ * volume (x fastest).  Errors as REF: invalid_argument for n_classes outside
+ * [2,4] or histogram_bins < n_classes; runtime_error "degenerate histogram". */
+int xs_otsu_thresholds(xs_context* ctx, const float* volume, const int32_t dims[3], int32_t n_classes,
+                       int32_t histogram_bins, double* thresholds, int32_t device_ptrs);
+
+/* REF segment_volume (recon.hpp:43-44, recon.cpp:242-262): labels[i] = number
+ * of leading thresholds <= volume[i].  n_class_map = REF class_map.size()
+ * (checked like REF).  thresholds are host doubles. */
+int xs_segment_volume(xs_context* ctx, const float* volume, uint64_t n_voxels, const double* thresholds,
+                      int32_t n_thresholds, int32_t n_class_map, uint8_t* labels, int32_t device_ptrs);
+
+/* REF to_density_phantom (recon.hpp:50-53, recon.cpp:264-322): block mode of
+ * the labels (ties to the higher label) and block mean of the class
+ * densities onto target_dims; then REF validate_phantom against `materials`
+ * (n_materials incl. vacuum; NULL skips it).  Errors: "unmapped label N". */
+int xs_to_density_phantom(xs_context* ctx, const uint8_t* labels, const int32_t src_dims[3],
+                          const xs_class_spec* class_map, int32_t n_classes, const int32_t target_dims[3],
+                          int32_t n_materials, const xs_material* materials, uint8_t* material_id,
+                          float* density, int32_t device_ptrs);
+
+/* The loop's segmentation stage fused (REF correction.cpp:168-171): Otsu
+ * with REF's default 1024 bins (or histogram_bins) -> labels -> density
+ * phantom on target_dims, which becomes the context's scene (as if passed
+ * to xs_upload_phantom) without leaving the device.  Thresholds out (host). */
+int xs_segment_to_scene(xs_context* ctx, const float* volume, const int32_t dims[3], const double voxel_size[3],
+                        int32_t n_classes, int32_t histogram_bins, const xs_class_spec* class_map,
+                        const int32_t target_dims[3], int32_t n_materials, const xs_material* materials,
+                        double* thresholds, int32_t device_ptrs);
+
+/* xs_upload_phantom for a phantom whose material_id / density arrays are
+ * device pointers (same validation, errors and device grid). */
+int xs_upload_phantom_device(xs_context* ctx, const xs_phantom* ph);
+
 #ifdef __cplusplus
 }
 #endif

@@ -597,4 +597,54 @@ int xr_make_phantom(int32_t kind, int32_t n, double voxel_cm, const double* para
     });
 }
 
+// recon.cpp:159-322: otsu_thresholds, segment_volume, to_density_phantom
+static Volume volume_from(const float* v, const int32_t dims[3])
+{
+    Volume vol = make_volume(dims[0], dims[1], dims[2], Vec3{0.1, 0.1, 0.1});
+    std::memcpy(vol.values.data(), v, vol.values.size() * sizeof(float));
+    return vol;
+}
+
+int xr_otsu_thresholds(const float* vol, const int32_t dims[3], int32_t n_classes, int32_t bins,
+                       double* thresholds)
+{
+    return guarded([&] {
+        const std::vector<double> th = otsu_thresholds(volume_from(vol, dims), n_classes, bins);
+        std::copy(th.begin(), th.end(), thresholds);
+    });
+}
+
+int xr_segment_volume(const float* v, uint64_t n, const double* thr, int32_t n_thr, int32_t n_class_map,
+                      uint8_t* labels)
+{
+    return guarded([&] {
+        Volume vol;
+        vol.dims = {static_cast<int>(n), 1, 1};
+        vol.voxel_size = Vec3{0.1, 0.1, 0.1};
+        vol.values.assign(v, v + n);
+        const SegmentationResult seg =
+            segment_volume(vol, std::vector<double>(thr, thr + n_thr), std::vector<ClassSpec>(n_class_map));
+        std::memcpy(labels, seg.labels.data(), n);
+    });
+}
+
+int xr_to_density_phantom(const uint8_t* labels, const int32_t src[3], const xs_class_spec* cls,
+                          int32_t n_classes, const int32_t tgt[3], int32_t n_materials,
+                          const xs_material* materials, uint8_t* ids, float* dens)
+{
+    return guarded([&] {
+        Volume vol = make_volume(src[0], src[1], src[2], Vec3{0.1, 0.1, 0.1});
+        SegmentationResult seg;
+        seg.labels.assign(labels, labels + vol.voxel_count());
+        for (int l = 0; l < n_classes; ++l)
+            seg.class_map.push_back(ClassSpec{cls[l].material_id, cls[l].density});
+        std::vector<Material> mats;
+        for (int m = 1; m < n_materials; ++m)
+            mats.push_back(material(materials[m]));
+        const VoxelPhantom ph = to_density_phantom(vol, seg, {tgt[0], tgt[1], tgt[2]}, mats);
+        std::memcpy(ids, ph.material_id.data(), ph.voxel_count());
+        std::memcpy(dens, ph.density.data(), ph.voxel_count() * sizeof(float));
+    });
+}
+
 } // extern "C"

@@ -2260,3 +2260,194 @@ int xo_fbp_reconstruct(const double* stack, const double* angles, int32_t n_view
     return XS_OK;
 }
 
+
+/* ---------------------------------------------------------- segmentation
+ * recon.cpp:159-322. */
+
+/* recon.cpp:159-240 */
+int xo_otsu_thresholds(const float* vol, const int32_t dims[3], int32_t n_classes, int32_t bins,
+                       double* thresholds)
+{
+    const int mx = dims[0] / 20 > 0 ? dims[0] / 20 : 0, my = dims[1] / 20 > 0 ? dims[1] / 20 : 0,
+              mz = dims[2] / 20 > 0 ? dims[2] / 20 : 0;
+    double lo = INFINITY, hi = -INFINITY, scale, *count, *pc, *ps, *best;
+    int *arg, ix, iy, iz, b, k, m, cuts[4], W = bins + 1;
+    const double neg_inf = -INFINITY;
+    if (n_classes < 2 || n_classes > 4) {
+        snprintf(tl_last, sizeof tl_last, "otsu: n_classes must be in [2,4]");
+        return XS_E_INVALID_ARGUMENT;
+    }
+    if (bins < n_classes) {
+        snprintf(tl_last, sizeof tl_last, "otsu: too few histogram bins");
+        return XS_E_INVALID_ARGUMENT;
+    }
+#define XO_AT(x, y, z) vol[(size_t)(x) + (size_t)dims[0] * ((size_t)(y) + (size_t)dims[1] * (size_t)(z))]
+    for (iz = mz; iz < dims[2] - mz; ++iz)
+        for (iy = my; iy < dims[1] - my; ++iy)
+            for (ix = mx; ix < dims[0] - mx; ++ix) {
+                const double v = XO_AT(ix, iy, iz);
+                lo = (v < lo) ? v : lo; /* std::min(lo, v) */
+                hi = (hi < v) ? v : hi; /* std::max(hi, v) */
+            }
+    if (!(hi > lo)) {
+        snprintf(tl_last, sizeof tl_last, "otsu: degenerate histogram");
+        return XS_E_RUNTIME;
+    }
+    count = (double*)calloc((size_t)bins, sizeof(double));
+    scale = bins / (hi - lo);
+    for (iz = mz; iz < dims[2] - mz; ++iz)
+        for (iy = my; iy < dims[1] - my; ++iy)
+            for (ix = mx; ix < dims[0] - mx; ++ix) {
+                const double t = (XO_AT(ix, iy, iz) - lo) * scale;
+                /* static_cast<int>; out-of-range / NaN convert to INT_MIN on x86-64 */
+                b = (t == t && t > -2147483649.0 && t < 2147483648.0) ? (int)t : (-2147483647 - 1);
+                b = b < 0 ? 0 : (b > bins - 1 ? bins - 1 : b);
+                count[b] += 1.0;
+            }
+#undef XO_AT
+    pc = (double*)calloc((size_t)W, sizeof(double));
+    ps = (double*)calloc((size_t)W, sizeof(double));
+    for (b = 0; b < bins; ++b) {
+        pc[b + 1] = pc[b] + count[b];
+        ps[b + 1] = ps[b] + count[b] * (b + 0.5);
+    }
+    best = (double*)malloc(sizeof(double) * (size_t)(n_classes + 1) * W);
+    arg = (int*)malloc(sizeof(int) * (size_t)(n_classes + 1) * W);
+    for (b = 0; b < (n_classes + 1) * W; ++b) {
+        best[b] = neg_inf;
+        arg[b] = -1;
+    }
+    best[0] = 0.0;
+    for (k = 1; k <= n_classes; ++k)
+        for (b = k; b <= bins; ++b)
+            for (m = k - 1; m < b; ++m) {
+                double sc, cand, n;
+                if (best[(k - 1) * W + m] == neg_inf)
+                    continue;
+                n = pc[b] - pc[m];
+                if (n <= 0.0) {
+                    sc = neg_inf;
+                } else {
+                    const double s = ps[b] - ps[m];
+                    sc = s * s / n;
+                }
+                cand = best[(k - 1) * W + m] + sc;
+                if (cand > best[k * W + b]) {
+                    best[k * W + b] = cand;
+                    arg[k * W + b] = m;
+                }
+            }
+    if (best[n_classes * W + bins] == neg_inf) {
+        free(count), free(pc), free(ps), free(best), free(arg);
+        snprintf(tl_last, sizeof tl_last, "otsu: degenerate histogram");
+        return XS_E_RUNTIME;
+    }
+    /* backtrack; the cuts come out descending, the last one (0) is dropped */
+    b = bins;
+    for (k = n_classes; k >= 1; --k) {
+        cuts[k - 1] = arg[k * W + b];
+        b = arg[k * W + b];
+    }
+    for (k = 1; k < n_classes; ++k)
+        thresholds[k - 1] = lo + cuts[k] / scale;
+    free(count), free(pc), free(ps), free(best), free(arg);
+    return XS_OK;
+}
+
+/* recon.cpp:242-262 */
+int xo_segment_volume(const float* vol, uint64_t n, const double* thr, int32_t n_thr, int32_t n_class_map,
+                      uint8_t* labels)
+{
+    uint64_t i;
+    int t;
+    for (t = 1; t < n_thr; ++t)
+        if (!(thr[t] > thr[t - 1])) {
+            snprintf(tl_last, sizeof tl_last, "segment_volume: thresholds must be strictly increasing");
+            return XS_E_RUNTIME;
+        }
+    if (n_class_map != n_thr + 1) {
+        snprintf(tl_last, sizeof tl_last, "segment_volume: class_map must cover all %d classes", n_thr + 1);
+        return XS_E_RUNTIME;
+    }
+    for (i = 0; i < n; ++i) {
+        const double v = vol[i];
+        uint8_t label = 0;
+        while (label < n_thr && v >= thr[label])
+            ++label;
+        labels[i] = label;
+    }
+    return XS_OK;
+}
+
+/* recon.cpp:264-322, then validate_phantom (phantom.cpp:33-56) */
+int xo_to_density_phantom(const uint8_t* labels, const int32_t src[3], const xs_class_spec* cls,
+                          int32_t n_classes, const int32_t tgt[3], int32_t n_materials,
+                          const xs_material* materials, uint8_t* ids, float* dens)
+{
+    const uint64_t n_src = (uint64_t)src[0] * src[1] * src[2];
+    uint64_t i, votes[256];
+    int ox, oy, oz, ix, iy, iz, l;
+    for (i = 0; i < n_src; ++i)
+        if (labels[i] >= n_classes) {
+            snprintf(tl_last, sizeof tl_last, "to_density_phantom: unmapped label %d", (int)labels[i]);
+            return XS_E_RUNTIME;
+        }
+    for (oz = 0; oz < tgt[2]; ++oz) {
+        const int z0 = oz * src[2] / tgt[2], z1 = (oz + 1) * src[2] / tgt[2];
+        for (oy = 0; oy < tgt[1]; ++oy) {
+            const int y0 = oy * src[1] / tgt[1], y1 = (oy + 1) * src[1] / tgt[1];
+            for (ox = 0; ox < tgt[0]; ++ox) {
+                const int x0 = ox * src[0] / tgt[0], x1 = (ox + 1) * src[0] / tgt[0];
+                const size_t cell = (size_t)ox + (size_t)tgt[0] * ((size_t)oy + (size_t)tgt[1] * oz);
+                double rho_sum = 0.0;
+                uint64_t cnt = 0;
+                int mode = 0;
+                for (l = 0; l < n_classes; ++l)
+                    votes[l] = 0;
+                for (iz = z0; iz < z1; ++iz)
+                    for (iy = y0; iy < y1; ++iy)
+                        for (ix = x0; ix < x1; ++ix) {
+                            const uint8_t label =
+                                labels[(size_t)ix + (size_t)src[0] * ((size_t)iy + (size_t)src[1] * iz)];
+                            ++votes[label];
+                            rho_sum += cls[label].density;
+                            ++cnt;
+                        }
+                for (l = 1; l < n_classes; ++l)
+                    if (votes[l] >= votes[mode])
+                        mode = l;
+                if (cls[mode].material_id == 0) {
+                    ids[cell] = 0;
+                    dens[cell] = 0.0f;
+                } else {
+                    ids[cell] = (uint8_t)cls[mode].material_id;
+                    dens[cell] = (float)(rho_sum / (double)cnt);
+                }
+            }
+        }
+    }
+    if (materials) {
+        const uint64_t n_out = (uint64_t)tgt[0] * tgt[1] * tgt[2];
+        for (i = 0; i < n_out; ++i) {
+            const int id = ids[i];
+            if (id >= n_materials) {
+                snprintf(tl_last, sizeof tl_last, "phantom: material id %d has no loaded material", id);
+                return XS_E_RUNTIME;
+            }
+            if (id != 0 && materials[id].mu.n <= 0) {
+                snprintf(tl_last, sizeof tl_last, "phantom: material id %d (%s) has no tables", id,
+                         materials[id].name ? materials[id].name : "?");
+                return XS_E_RUNTIME;
+            }
+            if (!(dens[i] >= 0.0f)) {
+                snprintf(tl_last, sizeof tl_last, "phantom: negative density");
+                return XS_E_RUNTIME;
+            }
+            if (id == 0 && dens[i] != 0.0f) {
+                snprintf(tl_last, sizeof tl_last, "phantom: vacuum voxel with nonzero density");
+                return XS_E_RUNTIME;
+            }
+        }
+    }
+    return XS_OK;
+}

@@ -110,6 +110,15 @@ int xo_fbp_reconstruct(const double* stack, const double* angles, int32_t n_view
                        const xs_geometry* g, const int32_t dims[3], const double voxel[3], int32_t hann,
                        float* volume);
 
+/* Segmentation (REF recon.cpp:159-322). */
+int xo_otsu_thresholds(const float* vol, const int32_t dims[3], int32_t n_classes, int32_t bins,
+                       double* thresholds);
+int xo_segment_volume(const float* vol, uint64_t n, const double* thr, int32_t n_thr, int32_t n_class_map,
+                      uint8_t* labels);
+int xo_to_density_phantom(const uint8_t* labels, const int32_t src[3], const xs_class_spec* cls,
+                          int32_t n_classes, const int32_t tgt[3], int32_t n_materials,
+                          const xs_material* materials, uint8_t* ids, float* dens);
+
 #ifdef __cplusplus
 }
 #endif

@@ -60,6 +60,10 @@ class XsSimConfig(C.Structure):
                 ("seed", C.c_uint64), ("track_variance", C.c_int32)]
 
 
+class XsClassSpec(C.Structure):
+    _fields_ = [("material_id", C.c_int32), ("density", C.c_double)]
+
+
 class XsLedger(C.Structure):
     _fields_ = [(k, C.c_double) for k in ("initial", "escaped", "absorbed", "culled",
                                           "roulette_killed", "roulette_boost")]
@@ -123,6 +127,20 @@ class Packed:
         out.sigma_pe = self.table(m.sigma_pe)
         out.s_factor = self.table(m.s_factor)
         out.f_factor = self.table(m.f_factor)
+
+    def materials(self, mats) -> "C.Array":
+        """xs_material array of a REF material list (index 0 = vacuum sentinel)."""
+        arr = (XsMaterial * len(mats))()
+        for i, m in enumerate(mats):
+            self.material(m, arr[i])
+        return self.keep(arr)
+
+    def class_map(self, cmap) -> "C.Array":
+        arr = (XsClassSpec * max(1, len(cmap)))()
+        for i, c in enumerate(cmap):
+            arr[i].material_id = int(c.material_id)
+            arr[i].density = float(c.density)
+        return self.keep(arr)
 
     def phantom(self, ph: I.VoxelPhantom) -> XsPhantom:
         mats = (XsMaterial * len(ph.materials))()
@@ -243,6 +261,16 @@ SIGNATURES = {
     "xs_correction_tail": (C.c_int, [_P, _P, _P, C.c_int32, _P, _P, C.c_int32, C.c_int32,
                                      C.c_int32, C.c_int32, C.c_int32, _P, C.c_int32, C.c_int32,
                                      _P, C.POINTER(C.c_double), C.POINTER(C.c_uint64), C.c_int32]),
+    "xs_otsu_thresholds": (C.c_int, [_P, _P, C.POINTER(C.c_int32), C.c_int32, C.c_int32, _P,
+                                     C.c_int32]),
+    "xs_segment_volume": (C.c_int, [_P, _P, C.c_uint64, _P, C.c_int32, C.c_int32, _P, C.c_int32]),
+    "xs_to_density_phantom": (C.c_int, [_P, _P, C.POINTER(C.c_int32), C.POINTER(XsClassSpec),
+                                        C.c_int32, C.POINTER(C.c_int32), C.c_int32,
+                                        C.POINTER(XsMaterial), _P, _P, C.c_int32]),
+    "xs_segment_to_scene": (C.c_int, [_P, _P, C.POINTER(C.c_int32), _P, C.c_int32, C.c_int32,
+                                      C.POINTER(XsClassSpec), C.POINTER(C.c_int32), C.c_int32,
+                                      C.POINTER(XsMaterial), _P, C.c_int32]),
+    "xs_upload_phantom_device": (C.c_int, [_P, C.POINTER(XsPhantom)]),
 }
 
 

@@ -44,6 +44,21 @@ cudaError_t launch_correction_tail(const double* primary, const double* scatter,
                                    cudaStream_t s);
 cudaError_t launch_mark_levels(uint8_t* vox, const Grid& G, int fmt, const int* edges, int n_levels,
                                void* scratch, int sm_count, cudaStream_t s);
+size_t seg_ctl_bytes();
+size_t otsu_scratch_bytes(int bins, int n_classes);
+cudaError_t launch_seg_reset(void* ctl, cudaStream_t s);
+cudaError_t launch_otsu(const float* vol, const int dims[3], int n_classes, int bins, void* ctl, void* scratch,
+                        double* thr, int sm_count, cudaStream_t s);
+cudaError_t launch_segment_labels(const float* vol, uint64_t n, const double* thr, int n_thr, uint8_t* labels,
+                                  int sm_count, cudaStream_t s);
+cudaError_t launch_density_phantom(const uint8_t* labels, const float* vol, const int src[3], const int tgt[3],
+                                   const int* cls_mat, const double* cls_dens, int n_labels, const double* thr,
+                                   int n_thr, uint8_t* id_out, float* dens_out, void* ctl, int sm_count,
+                                   cudaStream_t s);
+cudaError_t launch_phantom_scan(const uint8_t* ids, const float* dens, uint64_t n, int n_materials,
+                                uint32_t has_tables, void* ctl, int sm_count, cudaStream_t s);
+cudaError_t launch_phantom_encode(const uint8_t* ids, const float* dens, const unsigned long long* pal, int n_pal,
+                                  const Grid& G, int fmt, uint8_t* vox, float* vdens, int sm_count, cudaStream_t s);
 struct WaveEngine;
 WaveEngine* wave_create();
 void wave_destroy(WaveEngine* e);
@@ -202,6 +217,11 @@ struct xs_context {
     DevBuf<unsigned long long> cc_stats;
     DevBuf<double> fbp_in, fbp_q, fbp_k, fbp_views;
     DevBuf<float> fbp_vol;
+    DevBuf<unsigned char> seg_ctl, seg_scratch; // segmentation stage (segment.cu)
+    DevBuf<double> seg_thr;
+    DevBuf<uint8_t> seg_ids, seg_labels;
+    DevBuf<float> seg_dens, seg_vol;
+    DevBuf<unsigned long long> seg_pal;
     int smem_kb = 48; // per transport block: 4 blocks/SM leave 60 KB of L1
     int max_slots = 64;
     int macro_skip = 1;
@@ -332,6 +352,22 @@ struct ScanResult {
     std::vector<PairKey> pairs; // up to 257 distinct
 };
 
+// REF validate_phantom's per-voxel checks (phantom.cpp:42-54), in its order;
+// empty when the voxel is valid.
+std::string voxel_error(const xs_phantom& ph, const std::vector<int>& has_tables, uint8_t id, float d)
+{
+    if (id >= ph.n_materials)
+        return "phantom: material id " + std::to_string(id) + " has no loaded material";
+    if (id != 0 && !has_tables[id])
+        return "phantom: material id " + std::to_string(id) + " (" +
+               std::string(ph.materials[id].name ? ph.materials[id].name : "?") + ") has no tables";
+    if (!(d >= 0.0f))
+        return "phantom: negative density";
+    if (id == 0 && d != 0.0f)
+        return "phantom: vacuum voxel with nonzero density";
+    return std::string();
+}
+
 // REF validate_phantom (phantom.cpp:33-56) fused with palette discovery.
 void scan_phantom(const xs_phantom& ph, const std::vector<int>& has_tables, ScanResult& out)
 {
@@ -453,6 +489,39 @@ void encode_phantom(const xs_phantom& ph, int fmt, const std::vector<PairKey>& p
     for (auto& t : th)
         t.join();
 }
+
+// Host view of the device SegCtl record (segment.cu): first_bad at byte 8,
+// n_pairs / overflow at 16 / 20, the pair set at 56.
+struct SegCtlView {
+    const unsigned char* p;
+    explicit SegCtlView(const unsigned char* b) : p(b) {}
+    template <typename T>
+    T at(size_t off) const
+    {
+        T v;
+        std::memcpy(&v, p + off, sizeof v);
+        return v;
+    }
+    unsigned long long first_bad() const { return at<unsigned long long>(8); }
+    uint32_t n_pairs() const { return at<uint32_t>(16); }
+    uint32_t overflow() const { return at<uint32_t>(20); }
+    int32_t status() const { return at<int32_t>(24); }
+    // distinct pairs, sorted; more than kMaxPalette entries = the raw format
+    void pairs(std::vector<PairKey>& out) const
+    {
+        out.clear();
+        if (overflow() || n_pairs() > (uint32_t)xsd::kMaxPalette) {
+            out.resize(xsd::kMaxPalette + 1);
+            return;
+        }
+        for (int i = 0; i < 1024; ++i) {
+            const unsigned long long k = at<unsigned long long>(56 + 8 * (size_t)i);
+            if (k != ~0ull)
+                out.push_back(PairKey{(uint8_t)(k >> 32), (uint32_t)k});
+        }
+        std::sort(out.begin(), out.end());
+    }
+};
 
 // --------------------------------------------------------- scatter launch
 struct Plan {
@@ -881,6 +950,14 @@ void xs_ctx_destroy(xs_context* c)
     for (auto* b : {&c->fbp_in, &c->fbp_q, &c->fbp_k, &c->fbp_views})
         b->release();
     c->fbp_vol.release();
+    c->seg_ctl.release();
+    c->seg_scratch.release();
+    c->seg_thr.release();
+    c->seg_ids.release();
+    c->seg_labels.release();
+    c->seg_dens.release();
+    c->seg_vol.release();
+    c->seg_pal.release();
     xsd::wave_destroy(c->wave);
     if (c->ev0)
         cudaEventDestroy(c->ev0);
@@ -927,9 +1004,13 @@ int xs_ctx_synchronize(xs_context* c)
     return guard(c, [&] { cuda_check(cudaStreamSynchronize(c->stream), "synchronize"); });
 }
 
-int xs_upload_phantom(xs_context* c, const xs_phantom* ph)
+// REF validate_phantom + the device encoding of the grid.  on_device: the
+// phantom's id / density arrays are device pointers (the segmentation stage
+// builds them in HBM): validation, palette discovery and encoding run on the
+// device (segment.cu) and give the same grid as the host path.
+static void upload_phantom_impl(xs_context* c, const xs_phantom* ph, bool on_device)
 {
-    return guard(c, [&] {
+    {
         if (ph->dims[0] <= 0 || ph->dims[1] <= 0 || ph->dims[2] <= 0)
             fail(XS_E_RUNTIME, "phantom: dims must be positive");
         if (!(ph->voxel_size[0] > 0.0 && ph->voxel_size[1] > 0.0 && ph->voxel_size[2] > 0.0))
@@ -950,7 +1031,31 @@ int xs_upload_phantom(xs_context* c, const xs_phantom* ph)
         auto now = [] { return std::chrono::steady_clock::now(); };
         auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
         const auto t0 = now();
-        scan_phantom(*ph, has_tables, scan);
+        if (on_device) {
+            uint32_t tab_bits = 0;
+            for (int m = 1; m < ph->n_materials; ++m)
+                tab_bits |= has_tables[m] ? (1u << m) : 0u;
+            c->seg_ctl.reserve(xsd::seg_ctl_bytes());
+            cuda_check(xsd::launch_seg_reset(c->seg_ctl.p, c->stream), "phantom scan");
+            cuda_check(xsd::launch_phantom_scan(ph->material_id, ph->density, nvox, ph->n_materials, tab_bits,
+                                                c->seg_ctl.p, c->sm_count, c->stream),
+                       "phantom scan");
+            std::vector<unsigned char> ctl(xsd::seg_ctl_bytes());
+            cuda_check(cudaMemcpyAsync(ctl.data(), c->seg_ctl.p, ctl.size(), cudaMemcpyDeviceToHost, c->stream),
+                       "phantom scan");
+            cuda_check(cudaStreamSynchronize(c->stream), "phantom scan");
+            SegCtlView v(ctl.data());
+            if (v.first_bad() != ~0ull) {
+                uint8_t id = 0;
+                float d = 0.f;
+                cuda_check(cudaMemcpy(&id, ph->material_id + v.first_bad(), 1, cudaMemcpyDeviceToHost), "D2H");
+                cuda_check(cudaMemcpy(&d, ph->density + v.first_bad(), 4, cudaMemcpyDeviceToHost), "D2H");
+                fail(XS_E_RUNTIME, "%s", voxel_error(*ph, has_tables, id, d).c_str());
+            }
+            v.pairs(scan.pairs);
+        } else {
+            scan_phantom(*ph, has_tables, scan);
+        }
         const auto t1 = now();
         if (scan.first_bad != SIZE_MAX)
             fail(XS_E_RUNTIME, "%s", scan.bad_msg.c_str());
@@ -986,9 +1091,11 @@ int xs_upload_phantom(xs_context* c, const xs_phantom* ph)
         const size_t n_bricks = (size_t)G.nbx * G.nby * G.nbz;
         const size_t vox_bytes = n_bricks * (fmt == xsd::kFmtP4 ? 32 : 64);
         const size_t dens_count = fmt == xsd::kFmtRaw ? n_bricks * 64 : 0;
-        c->pin_vox.reserve(vox_bytes);
-        c->pin_dens.reserve(std::max<size_t>(dens_count, 1));
-        encode_phantom(*ph, fmt, scan.pairs, c->pin_vox.p, c->pin_dens.p, G.nbx, G.nby, G.nbz);
+        if (!on_device) {
+            c->pin_vox.reserve(vox_bytes);
+            c->pin_dens.reserve(std::max<size_t>(dens_count, 1));
+            encode_phantom(*ph, fmt, scan.pairs, c->pin_vox.p, c->pin_dens.p, G.nbx, G.nby, G.nbz);
+        }
         const auto t2 = now();
 
         // Uniform blocks: every voxel of an aligned uniform block (all voxels
@@ -1032,13 +1139,27 @@ int xs_upload_phantom(xs_context* c, const xs_phantom* ph)
             std::memcpy(&c->pal_dens[k], &scan.pairs[k].dens_bits, 4);
         }
         c->vox.reserve(vox_bytes);
-        cuda_check(cudaMemcpyAsync(c->vox.p, c->pin_vox.p, vox_bytes, cudaMemcpyHostToDevice, c->stream),
-                   "upload voxels");
-        if (fmt == xsd::kFmtRaw) {
+        if (fmt == xsd::kFmtRaw)
             c->dens.reserve(dens_count);
-            cuda_check(cudaMemcpyAsync(c->dens.p, c->pin_dens.p, dens_count * 4, cudaMemcpyHostToDevice,
-                                       c->stream),
-                       "upload densities");
+        if (on_device) {
+            std::vector<unsigned long long> keys(scan.pairs.size());
+            for (size_t k = 0; k < keys.size(); ++k)
+                keys[k] = ((unsigned long long)scan.pairs[k].id << 32) | scan.pairs[k].dens_bits;
+            const int n_keys = fmt == xsd::kFmtRaw ? 0 : (int)keys.size();
+            c->seg_pal.reserve(std::max(n_keys, 1));
+            if (n_keys)
+                cuda_check(cudaMemcpyAsync(c->seg_pal.p, keys.data(), n_keys * 8, cudaMemcpyHostToDevice, c->stream),
+                           "palette");
+            cuda_check(xsd::launch_phantom_encode(ph->material_id, ph->density, c->seg_pal.p, n_keys, G, fmt, c->vox.p,
+                                                  fmt == xsd::kFmtRaw ? c->dens.p : nullptr, c->sm_count, c->stream),
+                       "encode phantom");
+        } else {
+            cuda_check(cudaMemcpyAsync(c->vox.p, c->pin_vox.p, vox_bytes, cudaMemcpyHostToDevice, c->stream),
+                       "upload voxels");
+            if (fmt == xsd::kFmtRaw)
+                cuda_check(cudaMemcpyAsync(c->dens.p, c->pin_dens.p, dens_count * 4, cudaMemcpyHostToDevice,
+                                           c->stream),
+                           "upload densities");
         }
         if (!lvl_edges.empty()) { // uniform-block levels, on the device (levels.cu)
             c->lvl_scratch.reserve(xsd::levels_scratch_bytes(G, lvl_edges.data(), (int)lvl_edges.size()));
@@ -1046,7 +1167,7 @@ int xs_upload_phantom(xs_context* c, const xs_phantom* ph)
                                                c->lvl_scratch.p, c->sm_count, c->stream),
                        "uniform-block levels");
         }
-        c->last_upload_bytes = vox_bytes + dens_count * 4;
+        c->last_upload_bytes = on_device ? 0 : vox_bytes + dens_count * 4;
         cuda_check(cudaStreamSynchronize(c->stream), "upload phantom");
         if (timing)
             std::fprintf(stderr, "[xscat] upload: scan %.1f ms, encode %.1f ms, levels+H2D %.1f ms\n", ms(t0, t1),
@@ -1073,7 +1194,17 @@ int xs_upload_phantom(xs_context* c, const xs_phantom* ph)
         }
         rebuild_tables(c);
         c->have_phantom = true;
-    });
+    }
+}
+
+int xs_upload_phantom(xs_context* c, const xs_phantom* ph)
+{
+    return guard(c, [&] { upload_phantom_impl(c, ph, false); });
+}
+
+int xs_upload_phantom_device(xs_context* c, const xs_phantom* ph)
+{
+    return guard(c, [&] { upload_phantom_impl(c, ph, true); });
 }
 
 int xs_upload_response(xs_context* c, const xs_response* r)
@@ -1611,6 +1742,236 @@ int xs_fbp_reconstruct(xs_context* c, const double* stack, const double* angles,
         if (!device_ptrs)
             cuda_check(cudaMemcpyAsync(volume, vol, nvox * 4, cudaMemcpyDeviceToHost, st), "D2H");
         cuda_check(cudaStreamSynchronize(st), "fbp");
+    });
+}
+
+// ---------------------------------------------------------- segmentation
+// REF otsu_thresholds / segment_volume / to_density_phantom (recon.cpp:159-322)
+// and the loop's fused segmentation stage (correction.cpp:167-172) on the
+// device (segment.cu); SURVEY.md §8(f) rank 3.
+static const float* seg_volume_in(xs_context* c, const float* volume, size_t nvox, int32_t device_ptrs)
+{
+    if (device_ptrs)
+        return volume;
+    c->seg_vol.reserve(nvox);
+    cuda_check(cudaMemcpyAsync(c->seg_vol.p, volume, nvox * 4, cudaMemcpyHostToDevice, c->stream), "H2D");
+    return c->seg_vol.p;
+}
+
+static void seg_otsu(xs_context* c, const float* vol, const int32_t dims[3], int n_classes, int bins,
+                     double* thresholds)
+{
+    if (n_classes < 2 || n_classes > 4)
+        fail(XS_E_INVALID_ARGUMENT, "otsu: n_classes must be in [2,4]");
+    if (bins < n_classes)
+        fail(XS_E_INVALID_ARGUMENT, "otsu: too few histogram bins");
+    if (dims[0] <= 0 || dims[1] <= 0 || dims[2] <= 0)
+        fail(XS_E_RUNTIME, "otsu: degenerate histogram");
+    c->seg_ctl.reserve(xsd::seg_ctl_bytes());
+    c->seg_scratch.reserve(xsd::otsu_scratch_bytes(bins, n_classes));
+    c->seg_thr.reserve(16);
+    cuda_check(xsd::launch_seg_reset(c->seg_ctl.p, c->stream), "otsu");
+    const int d[3] = {dims[0], dims[1], dims[2]};
+    cuda_check(xsd::launch_otsu(vol, d, n_classes, bins, c->seg_ctl.p, c->seg_scratch.p, c->seg_thr.p, c->sm_count,
+                                c->stream),
+               "otsu");
+    unsigned char ctl[64];
+    cuda_check(cudaMemcpyAsync(ctl, c->seg_ctl.p, sizeof ctl, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    cuda_check(cudaMemcpyAsync(thresholds, c->seg_thr.p, (n_classes - 1) * sizeof(double), cudaMemcpyDeviceToHost,
+                               c->stream),
+               "D2H");
+    cuda_check(cudaStreamSynchronize(c->stream), "otsu");
+    if (SegCtlView(ctl).status() != 0)
+        fail(XS_E_RUNTIME, "otsu: degenerate histogram");
+}
+
+static void check_thresholds(const double* thr, int n_thr, int n_class_map)
+{
+    for (int i = 1; i < n_thr; ++i)
+        if (!(thr[i] > thr[i - 1]))
+            fail(XS_E_RUNTIME, "segment_volume: thresholds must be strictly increasing");
+    if (n_class_map != n_thr + 1)
+        fail(XS_E_RUNTIME, "segment_volume: class_map must cover all %d classes", n_thr + 1);
+    if (n_thr > 15)
+        fail(XS_E_UNSUPPORTED, "xscat-gpu: at most 16 segmentation classes supported");
+}
+
+static void check_density_phantom_args(const xs_class_spec* cls, int n_classes, const int32_t tgt[3],
+                                       int n_materials)
+{
+    if (n_classes <= 0 || n_classes > 16)
+        fail(XS_E_UNSUPPORTED, "xscat-gpu: 1..16 segmentation classes supported");
+    if (tgt[0] <= 0 || tgt[1] <= 0 || tgt[2] <= 0)
+        fail(XS_E_RUNTIME, "phantom: dims must be positive");
+    if (n_materials <= 0)
+        fail(XS_E_RUNTIME, "phantom: no material table");
+    for (int l = 0; l < n_classes; ++l)
+        if (cls[l].material_id < 0 || cls[l].material_id > 255)
+            fail(XS_E_RUNTIME, "to_density_phantom: class material id out of range");
+}
+
+int xs_otsu_thresholds(xs_context* c, const float* volume, const int32_t dims[3], int32_t n_classes,
+                       int32_t histogram_bins, double* thresholds, int32_t device_ptrs)
+{
+    return guard(c, [&] {
+        const size_t nvox = (size_t)std::max(dims[0], 0) * std::max(dims[1], 0) * std::max(dims[2], 0);
+        const float* vol = (n_classes >= 2 && n_classes <= 4 && histogram_bins >= n_classes && nvox)
+                               ? seg_volume_in(c, volume, nvox, device_ptrs)
+                               : volume;
+        seg_otsu(c, vol, dims, n_classes, histogram_bins, thresholds);
+    });
+}
+
+int xs_segment_volume(xs_context* c, const float* volume, uint64_t n_voxels, const double* thresholds,
+                      int32_t n_thresholds, int32_t n_class_map, uint8_t* labels, int32_t device_ptrs)
+{
+    return guard(c, [&] {
+        check_thresholds(thresholds, n_thresholds, n_class_map);
+        if (!n_voxels)
+            return;
+        const float* vol = seg_volume_in(c, volume, n_voxels, device_ptrs);
+        c->seg_thr.reserve(16);
+        if (n_thresholds)
+            cuda_check(cudaMemcpyAsync(c->seg_thr.p, thresholds, n_thresholds * sizeof(double),
+                                       cudaMemcpyHostToDevice, c->stream),
+                       "H2D");
+        uint8_t* out = labels;
+        if (!device_ptrs) {
+            c->seg_labels.reserve(n_voxels);
+            out = c->seg_labels.p;
+        }
+        cuda_check(xsd::launch_segment_labels(vol, n_voxels, c->seg_thr.p, n_thresholds, out, c->sm_count, c->stream),
+                   "segment");
+        if (!device_ptrs)
+            cuda_check(cudaMemcpyAsync(labels, out, n_voxels, cudaMemcpyDeviceToHost, c->stream), "D2H");
+        cuda_check(cudaStreamSynchronize(c->stream), "segment");
+    });
+}
+
+// REF to_density_phantom's label check, then the phantom's validation
+// (validate_phantom at recon.cpp:320) on the device outputs.
+static void density_checks(xs_context* c, const uint8_t* labels_dev, const uint8_t* ids, const float* dens,
+                           uint64_t n_out, int n_materials, const xs_material* materials)
+{
+    unsigned char ctl[64];
+    cuda_check(cudaMemcpyAsync(ctl, c->seg_ctl.p, sizeof ctl, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    cuda_check(cudaStreamSynchronize(c->stream), "to_density_phantom");
+    const unsigned long long bad = SegCtlView(ctl).first_bad();
+    if (bad != ~0ull) {
+        uint8_t l = 0;
+        cuda_check(cudaMemcpy(&l, labels_dev + bad, 1, cudaMemcpyDeviceToHost), "D2H");
+        fail(XS_E_RUNTIME, "to_density_phantom: unmapped label %d", (int)l);
+    }
+    if (!materials)
+        return;
+    xs_phantom ph{};
+    ph.n_materials = n_materials;
+    ph.materials = materials;
+    std::vector<int> has_tables(n_materials, 0);
+    uint32_t tab_bits = 0;
+    for (int m = 1; m < n_materials && m < 32; ++m) {
+        has_tables[m] = materials[m].mu.n > 0;
+        tab_bits |= has_tables[m] ? (1u << m) : 0u;
+    }
+    cuda_check(xsd::launch_seg_reset(c->seg_ctl.p, c->stream), "validate");
+    cuda_check(xsd::launch_phantom_scan(ids, dens, n_out, n_materials, tab_bits, c->seg_ctl.p, c->sm_count, c->stream),
+               "validate");
+    cuda_check(cudaMemcpyAsync(ctl, c->seg_ctl.p, sizeof ctl, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    cuda_check(cudaStreamSynchronize(c->stream), "validate");
+    const unsigned long long vb = SegCtlView(ctl).first_bad();
+    if (vb != ~0ull) {
+        uint8_t id = 0;
+        float d = 0.f;
+        cuda_check(cudaMemcpy(&id, ids + vb, 1, cudaMemcpyDeviceToHost), "D2H");
+        cuda_check(cudaMemcpy(&d, dens + vb, 4, cudaMemcpyDeviceToHost), "D2H");
+        fail(XS_E_RUNTIME, "%s", voxel_error(ph, has_tables, id, d).c_str());
+    }
+}
+
+int xs_to_density_phantom(xs_context* c, const uint8_t* labels, const int32_t src_dims[3],
+                          const xs_class_spec* class_map, int32_t n_classes, const int32_t target_dims[3],
+                          int32_t n_materials, const xs_material* materials, uint8_t* material_id, float* density,
+                          int32_t device_ptrs)
+{
+    return guard(c, [&] {
+        check_density_phantom_args(class_map, n_classes, target_dims, n_materials);
+        const uint64_t n_src = (uint64_t)src_dims[0] * src_dims[1] * src_dims[2];
+        const uint64_t n_out = (uint64_t)target_dims[0] * target_dims[1] * target_dims[2];
+        const uint8_t* lab = labels;
+        if (!device_ptrs) {
+            c->seg_labels.reserve(n_src);
+            cuda_check(cudaMemcpyAsync(c->seg_labels.p, labels, n_src, cudaMemcpyHostToDevice, c->stream), "H2D");
+            lab = c->seg_labels.p;
+        }
+        uint8_t* ids = material_id;
+        float* dens = density;
+        if (!device_ptrs) {
+            c->seg_ids.reserve(n_out);
+            c->seg_dens.reserve(n_out);
+            ids = c->seg_ids.p;
+            dens = c->seg_dens.p;
+        }
+        int mat[16];
+        double rho[16];
+        for (int l = 0; l < n_classes; ++l) {
+            mat[l] = class_map[l].material_id;
+            rho[l] = class_map[l].density;
+        }
+        const int s3[3] = {src_dims[0], src_dims[1], src_dims[2]}, t3[3] = {target_dims[0], target_dims[1], target_dims[2]};
+        c->seg_ctl.reserve(xsd::seg_ctl_bytes());
+        cuda_check(xsd::launch_seg_reset(c->seg_ctl.p, c->stream), "to_density_phantom");
+        cuda_check(xsd::launch_density_phantom(lab, nullptr, s3, t3, mat, rho, n_classes, nullptr, 0, ids, dens,
+                                               c->seg_ctl.p, c->sm_count, c->stream),
+                   "to_density_phantom");
+        density_checks(c, lab, ids, dens, n_out, n_materials, materials);
+        if (!device_ptrs) {
+            cuda_check(cudaMemcpyAsync(material_id, ids, n_out, cudaMemcpyDeviceToHost, c->stream), "D2H");
+            cuda_check(cudaMemcpyAsync(density, dens, n_out * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+            cuda_check(cudaStreamSynchronize(c->stream), "D2H");
+        }
+    });
+}
+
+int xs_segment_to_scene(xs_context* c, const float* volume, const int32_t dims[3], const double voxel_size[3],
+                        int32_t n_classes, int32_t histogram_bins, const xs_class_spec* class_map,
+                        const int32_t target_dims[3], int32_t n_materials, const xs_material* materials,
+                        double* thresholds, int32_t device_ptrs)
+{
+    return guard(c, [&] {
+        const size_t nvox = (size_t)std::max(dims[0], 0) * std::max(dims[1], 0) * std::max(dims[2], 0);
+        const float* vol = (n_classes >= 2 && n_classes <= 4 && histogram_bins >= n_classes && nvox)
+                               ? seg_volume_in(c, volume, nvox, device_ptrs)
+                               : volume;
+        // REF correction.cpp:168-171: otsu -> segment_volume -> to_density_phantom
+        seg_otsu(c, vol, dims, n_classes, histogram_bins, thresholds);
+        check_thresholds(thresholds, n_classes - 1, n_classes);
+        check_density_phantom_args(class_map, n_classes, target_dims, n_materials);
+        const uint64_t n_out = (uint64_t)target_dims[0] * target_dims[1] * target_dims[2];
+        c->seg_ids.reserve(n_out);
+        c->seg_dens.reserve(n_out);
+        int mat[16];
+        double rho[16];
+        for (int l = 0; l < n_classes; ++l) {
+            mat[l] = class_map[l].material_id;
+            rho[l] = class_map[l].density;
+        }
+        const int s3[3] = {dims[0], dims[1], dims[2]}, t3[3] = {target_dims[0], target_dims[1], target_dims[2]};
+        cuda_check(xsd::launch_seg_reset(c->seg_ctl.p, c->stream), "segmentation");
+        cuda_check(xsd::launch_density_phantom(nullptr, vol, s3, t3, mat, rho, n_classes, thresholds, n_classes - 1,
+                                               c->seg_ids.p, c->seg_dens.p, c->seg_ctl.p, c->sm_count, c->stream),
+                   "segmentation");
+        // REF to_density_phantom: voxel size = vol voxel * dims / target, centred grid
+        xs_phantom ph{};
+        for (int a = 0; a < 3; ++a) {
+            ph.dims[a] = target_dims[a];
+            ph.voxel_size[a] = voxel_size[a] * dims[a] / target_dims[a];
+            ph.origin[a] = (-target_dims[a] * ph.voxel_size[a]) * 0.5;
+        }
+        ph.material_id = c->seg_ids.p;
+        ph.density = c->seg_dens.p;
+        ph.n_materials = n_materials;
+        ph.materials = materials;
+        upload_phantom_impl(c, &ph, true);
     });
 }
 

@@ -429,3 +429,96 @@ def fbp_reconstruct(stack: ProjectionStack, g: I.ScanGeometry, dims, voxel_size=
                                          out.ctypes.data, 0))
     return out
 
+
+
+# ----------------------------------------------------------- segmentation
+# REF recon.hpp:27-53 / recon.cpp:159-322 on the device.
+@dataclasses.dataclass
+class ClassSpec:
+    """REF ClassSpec (recon.hpp:32-35)."""
+    material_id: int = 0
+    density: float = 0.0
+
+
+@dataclasses.dataclass
+class SegmentationResult:
+    """REF SegmentationResult (recon.hpp:37-41); labels shaped like the volume."""
+    thresholds: List[float]
+    labels: np.ndarray
+    class_map: List[ClassSpec]
+
+
+def _volume(vol) -> np.ndarray:
+    v = np.ascontiguousarray(vol, dtype=np.float32)
+    if v.ndim != 3:
+        raise I.XscatError("volume: expected a (nz, ny, nx) array")
+    return v
+
+
+def otsu_thresholds(vol, n_classes: int, histogram_bins: int = 1024,
+                    ctx: Optional[Context] = None) -> List[float]:
+    """REF otsu_thresholds (recon.cpp:159-240) of a (nz, ny, nx) float volume."""
+    ctx = ctx or default_context()
+    v = _volume(vol)
+    d = (C.c_int32 * 3)(v.shape[2], v.shape[1], v.shape[0])
+    out = np.zeros(max(0, min(int(n_classes), 4) - 1) + 1)
+    ctx.check(A.lib().xs_otsu_thresholds(ctx.h, v.ctypes.data, d, int(n_classes), int(histogram_bins),
+                                         out.ctypes.data, 0))
+    return [float(x) for x in out[:int(n_classes) - 1]]
+
+
+def segment_volume(vol, thresholds, class_map, ctx: Optional[Context] = None) -> SegmentationResult:
+    """REF segment_volume (recon.cpp:242-262)."""
+    ctx = ctx or default_context()
+    v = _volume(vol)
+    thr = np.ascontiguousarray(thresholds, dtype=np.float64).reshape(-1)
+    labels = np.empty(v.shape, np.uint8)
+    ctx.check(A.lib().xs_segment_volume(ctx.h, v.ctypes.data, v.size, A.dptr(thr), thr.size,
+                                        len(class_map), labels.ctypes.data, 0))
+    return SegmentationResult([float(x) for x in thr], labels, list(class_map))
+
+
+def to_density_phantom(vol, voxel_size, seg: SegmentationResult, target_dims, materials,
+                       ctx: Optional[Context] = None) -> I.VoxelPhantom:
+    """REF to_density_phantom (recon.cpp:264-322): `vol` gives the source
+    dims (nz, ny, nx) and `voxel_size` its voxel size (REF Volume); `materials`
+    is REF's list without the vacuum entry, which is prepended like REF
+    make_empty_phantom does."""
+    ctx = ctx or default_context()
+    shape = np.shape(vol)
+    src = (C.c_int32 * 3)(shape[2], shape[1], shape[0])
+    tgt = (C.c_int32 * 3)(*target_dims)
+    mats = [None] + [m for m in materials if m is not None]
+    pk = A.Packed()
+    labels = np.ascontiguousarray(seg.labels, dtype=np.uint8)
+    n_out = int(target_dims[0]) * int(target_dims[1]) * int(target_dims[2])
+    ids = np.empty(n_out, np.uint8)
+    dens = np.empty(n_out, np.float32)
+    ctx.check(A.lib().xs_to_density_phantom(ctx.h, labels.ctypes.data, src, pk.class_map(seg.class_map),
+                                            len(seg.class_map), tgt, len(mats), pk.materials(mats),
+                                            ids.ctypes.data, dens.ctypes.data, 0))
+    vs = [float(voxel_size[a]) * shape[2 - a] / int(target_dims[a]) for a in range(3)]
+    origin = [(-int(target_dims[a]) * vs[a]) * 0.5 for a in range(3)]
+    return I.VoxelPhantom(tuple(target_dims), tuple(vs), tuple(origin), ids, dens, mats)
+
+
+def segment_to_scene(vol, voxel_size, n_classes: int, class_map, target_dims, materials,
+                     response: Optional[I.DetectorResponse] = None, histogram_bins: int = 1024,
+                     ctx: Optional[Context] = None) -> List[float]:
+    """The loop's segmentation stage (REF correction.cpp:168-171) fused on the
+    device: Otsu -> labels -> density phantom, which becomes ctx's scene.
+    Returns the thresholds."""
+    ctx = ctx or default_context()
+    v = _volume(vol)
+    d = (C.c_int32 * 3)(v.shape[2], v.shape[1], v.shape[0])
+    vs = np.ascontiguousarray(voxel_size, dtype=np.float64)
+    tgt = (C.c_int32 * 3)(*target_dims)
+    mats = [None] + [m for m in materials if m is not None]
+    pk = A.Packed()
+    thr = np.zeros(5)
+    ctx.check(A.lib().xs_segment_to_scene(ctx.h, v.ctypes.data, d, A.dptr(vs), int(n_classes),
+                                          int(histogram_bins), pk.class_map(class_map), tgt, len(mats),
+                                          pk.materials(mats), thr.ctypes.data, 0))
+    if response is not None:
+        ctx.check(A.lib().xs_upload_response(ctx.h, C.byref(pk.response(response))))
+    return [float(x) for x in thr[:int(n_classes) - 1]]

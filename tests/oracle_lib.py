@@ -65,6 +65,14 @@ def _sig(L, prefix):
                                            C.c_int32, _dp, _dp, A.c_u64_p]),
         f"{p}_fbp_reconstruct": (C.c_int, [_dp, _dp, C.c_int32, C.c_int32, C.c_int32, _g,
                                            C.POINTER(C.c_int32), _dp, C.c_int32, C.c_void_p]),
+        f"{p}_otsu_thresholds": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.c_int32, C.c_int32,
+                                           _dp]),
+        f"{p}_segment_volume": (C.c_int, [C.c_void_p, C.c_uint64, _dp, C.c_int32, C.c_int32,
+                                          C.c_void_p]),
+        f"{p}_to_density_phantom": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32),
+                                              C.POINTER(A.XsClassSpec), C.c_int32,
+                                              C.POINTER(C.c_int32), C.c_int32, _m, C.c_void_p,
+                                              C.c_void_p]),
         f"{p}_last_error": (C.c_char_p, []),
     }
     if prefix == "xo":
@@ -298,6 +306,38 @@ class Oracle:
         self.check(self.fn("fbp_reconstruct")(A.dptr(st), A.dptr(an), n, nu, nv, C.byref(pk.geometry(g)), d,
                                               A.dptr(vx), 1 if hann else 0, out.ctypes.data))
         return out
+
+
+    # ------------------------------------------------------- segmentation
+    def otsu_thresholds(self, vol, n_classes, bins=1024):
+        v = np.ascontiguousarray(vol, np.float32)
+        d = (C.c_int32 * 3)(v.shape[2], v.shape[1], v.shape[0])
+        out = np.zeros(4)
+        self.check(self.fn("otsu_thresholds")(v.ctypes.data, d, n_classes, bins, A.dptr(out)))
+        return [float(x) for x in out[:n_classes - 1]]
+
+    def segment_volume(self, vol, thresholds, n_class_map):
+        v = np.ascontiguousarray(vol, np.float32)
+        thr = np.ascontiguousarray(thresholds, np.float64).reshape(-1)
+        labels = np.empty(v.shape, np.uint8)
+        self.check(self.fn("segment_volume")(v.ctypes.data, v.size, A.dptr(thr), thr.size, n_class_map,
+                                             labels.ctypes.data))
+        return labels
+
+    def to_density_phantom(self, labels, class_map, target_dims, materials):
+        """materials: REF list without vacuum (None entries dropped)."""
+        lab = np.ascontiguousarray(labels, np.uint8)
+        src = (C.c_int32 * 3)(lab.shape[2], lab.shape[1], lab.shape[0])
+        tgt = (C.c_int32 * 3)(*target_dims)
+        mats = [None] + [m for m in materials if m is not None]
+        pk = A.Packed()
+        n = int(np.prod(target_dims))
+        ids = np.empty(n, np.uint8)
+        dens = np.empty(n, np.float32)
+        self.check(self.fn("to_density_phantom")(lab.ctypes.data, src, pk.class_map(class_map),
+                                                 len(class_map), tgt, len(mats), pk.materials(mats),
+                                                 ids.ctypes.data, dens.ctypes.data))
+        return ids, dens
 
 
 _oracle = None
