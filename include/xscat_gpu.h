@@ -518,6 +518,53 @@ int xs_segment_to_scene(xs_context* ctx, const float* volume, const int32_t dims
  * device pointers (same validation, errors and device grid). */
 int xs_upload_phantom_device(xs_context* ctx, const xs_phantom* ph);
 
+/* xs_run_scan with device outputs: d_primary / d_scatter (either NULL) hold
+ * n_subset images of nu x nv doubles in device memory. */
+int xs_run_scan_device(xs_context* ctx, const xs_geometry* g, const xs_spectrum* spec, const xs_sim_config* cfg,
+                       const int32_t* angle_subset, int32_t n_subset, int32_t what, double* d_primary,
+                       double* d_scatter, double* seconds_per_angle);
+
+/* ------------------------------------------------- iterative correction */
+
+/* REF CorrectionConfig (correction.hpp:13-24); defaults via
+ * xs_correction_config_default.  class_map: n_classes entries. */
+typedef struct xs_correction_config {
+    int32_t n_iterations;
+    int32_t simulate_every_kth_angle;
+    int32_t mc_nu, mc_nv; /* 0 = full resolution */
+    int32_t recon_dims[3];
+    int32_t n_classes;
+    const xs_class_spec* class_map;
+    xs_sim_config sim;
+    int32_t sg_window, sg_polyorder;
+    int32_t sg_auto_window;
+} xs_correction_config;
+void xs_correction_config_default(xs_correction_config* cfg);
+
+/* REF IterationReport (correction.hpp:26-39).  seconds_postprocess covers the
+ * fused post-processing + Eq. 8 pass (seconds_correction is 0). */
+typedef struct xs_iteration_report {
+    int32_t iteration;
+    int32_t pad_;
+    double seconds_fbp, seconds_segmentation, seconds_mc_scatter, seconds_mc_primary;
+    double seconds_postprocess, seconds_correction, seconds_total;
+    double mc_seconds_per_projection, mean_scatter_fraction, ncc_to_previous;
+    uint64_t negative_scatter_clamped;
+} xs_iteration_report;
+
+/* REF run_iterative_correction (correction.hpp:60-75, correction.cpp:137-266)
+ * with every stage on the device.  raw_intensity: g->n_angles images of
+ * nv x nu; flatfield: one image; materials: n_materials entries incl. vacuum
+ * (REF's list + 1); the detector response comes from xs_upload_response.
+ * Outputs (either may be NULL): the corrected volume (recon_dims floats) and
+ * the corrected stack; reports: n_iterations entries.  device_ptrs applies
+ * to raw_intensity, flatfield and both outputs.  Errors as REF, stage errors
+ * prefixed "iteration N, stage S: ". */
+int xs_run_iterative_correction(xs_context* ctx, const double* raw_intensity, const double* flatfield,
+                                const xs_geometry* g, const xs_spectrum* spec, const xs_correction_config* cfg,
+                                int32_t n_materials, const xs_material* materials, float* corrected_volume,
+                                double* corrected_stack, xs_iteration_report* reports, int32_t device_ptrs);
+
 #ifdef __cplusplus
 }
 #endif

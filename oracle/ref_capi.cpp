@@ -647,4 +647,59 @@ int xr_to_density_phantom(const uint8_t* labels, const int32_t src[3], const xs_
     });
 }
 
+// correction.cpp:137-266: the whole loop on REF's CPU path
+int xr_run_iterative_correction(const double* raw, const double* flat, const xs_geometry* g,
+                                const xs_spectrum* spec, const xs_response* resp,
+                                const xs_correction_config* cc, int32_t n_materials,
+                                const xs_material* materials, float* vol_out, double* stack_out,
+                                xs_iteration_report* reports, int32_t workers)
+{
+    return guarded([&] {
+        const ScanGeometry geo = geometry(*g);
+        const std::size_t np = static_cast<std::size_t>(g->nu) * g->nv;
+        ProjectionStack raw_s = make_stack(g->nu, g->nv, geo.angles);
+        for (int i = 0; i < g->n_angles; ++i)
+            raw_s.images[i] = image_from(raw + i * np, g->nu, g->nv);
+        const DetectorImage flat_img = image_from(flat, g->nu, g->nv);
+        CorrectionConfig cfg;
+        cfg.n_iterations = cc->n_iterations;
+        cfg.simulate_every_kth_angle = cc->simulate_every_kth_angle;
+        cfg.mc_nu = cc->mc_nu;
+        cfg.mc_nv = cc->mc_nv;
+        cfg.recon_dims = {cc->recon_dims[0], cc->recon_dims[1], cc->recon_dims[2]};
+        cfg.n_classes = cc->n_classes;
+        for (int l = 0; l < cc->n_classes; ++l)
+            cfg.class_map.push_back(ClassSpec{cc->class_map[l].material_id, cc->class_map[l].density});
+        cfg.sim = config(cc->sim);
+        cfg.sg = SgFilterSpec{cc->sg_window, cc->sg_polyorder};
+        cfg.sg_auto_window = cc->sg_auto_window != 0;
+        cfg.workers = workers;
+        std::vector<Material> mats;
+        for (int m = 1; m < n_materials; ++m)
+            mats.push_back(material(materials[m]));
+        const CorrectionResult out =
+            run_iterative_correction(raw_s, flat_img, geo, spectrum(*spec), response(*resp), cfg, mats);
+        if (vol_out)
+            std::memcpy(vol_out, out.corrected_volume.values.data(), out.corrected_volume.values.size() * 4);
+        if (stack_out)
+            stack_to(out.corrected_stack, stack_out);
+        for (std::size_t i = 0; i < out.reports.size(); ++i) {
+            const IterationReport& r = out.reports[i];
+            xs_iteration_report& x = reports[i];
+            x.iteration = r.iteration;
+            x.seconds_fbp = r.seconds_fbp;
+            x.seconds_segmentation = r.seconds_segmentation;
+            x.seconds_mc_scatter = r.seconds_mc_scatter;
+            x.seconds_mc_primary = r.seconds_mc_primary;
+            x.seconds_postprocess = r.seconds_postprocess;
+            x.seconds_correction = r.seconds_correction;
+            x.seconds_total = r.seconds_total;
+            x.mc_seconds_per_projection = r.mc_seconds_per_projection;
+            x.mean_scatter_fraction = r.mean_scatter_fraction;
+            x.ncc_to_previous = r.ncc_to_previous;
+            x.negative_scatter_clamped = r.negative_scatter_clamped;
+        }
+    });
+}
+
 } // extern "C"

@@ -20,6 +20,7 @@ from .projector import (BOTH, HANN, PRIMARY, RAMLAK, SCATTER, Context, Projectio
                         history_count, interpolate_angles, point_detector_score, run_scan,
                         sg_kernel, sg_smooth, simulate_primary, simulate_scatter,
                         simulate_scatter_stats, upsample_image, ClassSpec, SegmentationResult,
-                        otsu_thresholds, segment_volume, to_density_phantom, segment_to_scene)
+                        otsu_thresholds, segment_volume, to_density_phantom, segment_to_scene,
+                        CorrectionConfig, CorrectionResult, IterationReport, run_iterative_correction)
 
 __version__ = "0.1.0"

@@ -64,6 +64,23 @@ class XsClassSpec(C.Structure):
     _fields_ = [("material_id", C.c_int32), ("density", C.c_double)]
 
 
+class XsCorrectionConfig(C.Structure):
+    _fields_ = [("n_iterations", C.c_int32), ("simulate_every_kth_angle", C.c_int32),
+                ("mc_nu", C.c_int32), ("mc_nv", C.c_int32), ("recon_dims", C.c_int32 * 3),
+                ("n_classes", C.c_int32), ("class_map", C.POINTER(XsClassSpec)),
+                ("sim", XsSimConfig), ("sg_window", C.c_int32), ("sg_polyorder", C.c_int32),
+                ("sg_auto_window", C.c_int32)]
+
+
+class XsIterationReport(C.Structure):
+    _fields_ = [("iteration", C.c_int32), ("pad_", C.c_int32)] + [
+        (k, C.c_double) for k in ("seconds_fbp", "seconds_segmentation", "seconds_mc_scatter",
+                                  "seconds_mc_primary", "seconds_postprocess", "seconds_correction",
+                                  "seconds_total", "mc_seconds_per_projection",
+                                  "mean_scatter_fraction", "ncc_to_previous")] + [
+        ("negative_scatter_clamped", C.c_uint64)]
+
+
 class XsLedger(C.Structure):
     _fields_ = [(k, C.c_double) for k in ("initial", "escaped", "absorbed", "culled",
                                           "roulette_killed", "roulette_boost")]
@@ -141,6 +158,20 @@ class Packed:
             arr[i].material_id = int(c.material_id)
             arr[i].density = float(c.density)
         return self.keep(arr)
+
+    def correction_config(self, cc) -> XsCorrectionConfig:
+        """xs_correction_config of a projector.CorrectionConfig."""
+        x = XsCorrectionConfig()
+        x.n_iterations = int(cc.n_iterations)
+        x.simulate_every_kth_angle = int(cc.simulate_every_kth_angle)
+        x.mc_nu, x.mc_nv = int(cc.mc_nu), int(cc.mc_nv)
+        x.recon_dims[:] = [int(d) for d in cc.recon_dims]
+        x.n_classes = int(cc.n_classes)
+        x.class_map = C.cast(self.class_map(cc.class_map), C.POINTER(XsClassSpec))
+        x.sim = self.config(cc.sim)
+        x.sg_window, x.sg_polyorder = int(cc.sg.window), int(cc.sg.polyorder)
+        x.sg_auto_window = 1 if cc.sg_auto_window else 0
+        return self.keep(x)
 
     def phantom(self, ph: I.VoxelPhantom) -> XsPhantom:
         mats = (XsMaterial * len(ph.materials))()
@@ -271,6 +302,15 @@ SIGNATURES = {
                                       C.POINTER(XsClassSpec), C.POINTER(C.c_int32), C.c_int32,
                                       C.POINTER(XsMaterial), _P, C.c_int32]),
     "xs_upload_phantom_device": (C.c_int, [_P, C.POINTER(XsPhantom)]),
+    "xs_run_scan_device": (C.c_int, [_P, C.POINTER(XsGeometry), C.POINTER(XsSpectrum),
+                                     C.POINTER(XsSimConfig), C.POINTER(C.c_int32), C.c_int32,
+                                     C.c_int32, _P, _P, _P]),
+    "xs_correction_config_default": (None, [C.POINTER(XsCorrectionConfig)]),
+    "xs_run_iterative_correction": (C.c_int, [_P, _P, _P, C.POINTER(XsGeometry),
+                                              C.POINTER(XsSpectrum),
+                                              C.POINTER(XsCorrectionConfig), C.c_int32,
+                                              C.POINTER(XsMaterial), _P, _P,
+                                              C.POINTER(XsIterationReport), C.c_int32]),
 }
 
 

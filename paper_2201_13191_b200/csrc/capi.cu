@@ -59,6 +59,8 @@ cudaError_t launch_phantom_scan(const uint8_t* ids, const float* dens, uint64_t 
                                 uint32_t has_tables, void* ctl, int sm_count, cudaStream_t s);
 cudaError_t launch_phantom_encode(const uint8_t* ids, const float* dens, const unsigned long long* pal, int n_pal,
                                   const Grid& G, int fmt, uint8_t* vox, float* vdens, int sm_count, cudaStream_t s);
+size_t ncc_scratch_bytes();
+cudaError_t launch_ncc(const float* x1, const float* x2, uint64_t n, void* scratch, cudaStream_t s);
 struct WaveEngine;
 WaveEngine* wave_create();
 void wave_destroy(WaveEngine* e);
@@ -222,6 +224,8 @@ struct xs_context {
     DevBuf<uint8_t> seg_ids, seg_labels;
     DevBuf<float> seg_dens, seg_vol;
     DevBuf<unsigned long long> seg_pal;
+    DevBuf<double> loop_a, loop_c, loop_scat, loop_prim, loop_flat, loop_ncc; // iterative correction
+    DevBuf<float> loop_vol[2];
     int smem_kb = 48; // per transport block: 4 blocks/SM leave 60 KB of L1
     int max_slots = 64;
     int macro_skip = 1;
@@ -958,6 +962,10 @@ void xs_ctx_destroy(xs_context* c)
     c->seg_dens.release();
     c->seg_vol.release();
     c->seg_pal.release();
+    for (auto* b : {&c->loop_a, &c->loop_c, &c->loop_scat, &c->loop_prim, &c->loop_flat, &c->loop_ncc})
+        b->release();
+    c->loop_vol[0].release();
+    c->loop_vol[1].release();
     xsd::wave_destroy(c->wave);
     if (c->ev0)
         cudaEventDestroy(c->ev0);
@@ -1276,6 +1284,58 @@ int xs_simulate_primary(xs_context* c, const xs_geometry* g, int32_t angle, cons
         cuda_check(cudaMemcpyAsync(image_host, c->img.p, np * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
         cuda_check(cudaStreamSynchronize(c->stream), "D2H");
     });
+}
+
+// run_scan with device outputs (images stay in HBM for the loop's tail):
+// same validation, order and error text as xs_run_scan.
+static void scan_device_impl(xs_context* c, const xs_geometry* g, const xs_spectrum* spec, const xs_sim_config* cfg,
+                             const int32_t* subset, int32_t n_subset, int32_t what, double* d_primary,
+                             double* d_scatter, double* seconds)
+{
+    if (n_subset <= 0)
+        fail(XS_E_RUNTIME, "run_scan: empty angle subset");
+    xsh::validate_sim_config(*cfg);
+    xsh::validate_geometry(*g);
+    for (int i = 0; i < n_subset; ++i)
+        if (subset[i] < 0 || subset[i] >= g->n_angles)
+            fail(XS_E_OUT_OF_RANGE, "run_scan: angle index %d out of range", subset[i]);
+    const bool want_primary = what != 1, want_scatter = what != 0;
+    const size_t np = (size_t)g->nu * g->nv;
+    for (int i = 0; i < n_subset; ++i) {
+        const auto t0 = std::chrono::steady_clock::now();
+        try {
+            if (want_scatter) {
+                validate_call(*g, subset[i], *spec, *cfg, "simulate_scatter");
+                const Plan plan = make_plan(*g, *spec, *cfg);
+                c->accum.reserve(plan.layout.words);
+                cuda_check(cudaMemsetAsync(c->accum.p, 0, plan.layout.words * 8, c->stream), "memset");
+                accumulate(c, *g, subset[i], *spec, *cfg, 0, plan.n_hist, c->accum.p);
+                xs_scatter_result r{};
+                c->scan_img[0].reserve(np);
+                double* dst = d_scatter ? d_scatter + (size_t)i * np : c->scan_img[0].p;
+                finalize(c, *g, *spec, *cfg, c->accum.p, 0, plan.n_hist, &r, dst);
+            }
+            if (want_primary) {
+                validate_call(*g, subset[i], *spec, *cfg, "simulate_primary");
+                c->img.reserve(np);
+                primary(c, *g, subset[i], *spec, d_primary ? d_primary + (size_t)i * np : c->img.p);
+                if (seconds)
+                    cuda_check(cudaStreamSynchronize(c->stream), "primary");
+            }
+        } catch (const Error& e) {
+            fail(XS_E_RUNTIME, "run_scan: angle index %d: %s", subset[i], e.msg.c_str());
+        }
+        if (seconds)
+            seconds[i] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
+    cuda_check(cudaStreamSynchronize(c->stream), "run_scan");
+}
+
+int xs_run_scan_device(xs_context* c, const xs_geometry* g, const xs_spectrum* spec, const xs_sim_config* cfg,
+                       const int32_t* subset, int32_t n_subset, int32_t what, double* d_primary, double* d_scatter,
+                       double* seconds)
+{
+    return guard(c, [&] { scan_device_impl(c, g, spec, cfg, subset, n_subset, what, d_primary, d_scatter, seconds); });
 }
 
 int xs_run_scan(xs_context* c, const xs_geometry* g, const xs_spectrum* spec, const xs_sim_config* cfg,
@@ -1972,6 +2032,186 @@ int xs_segment_to_scene(xs_context* c, const float* volume, const int32_t dims[3
         ph.n_materials = n_materials;
         ph.materials = materials;
         upload_phantom_impl(c, &ph, true);
+    });
+}
+
+// ------------------------------------------------ iterative correction
+// REF run_iterative_correction (correction.cpp:137-266) with every stage on
+// the device: ln conversion, FDK, segmentation -> scene, scatter and primary
+// scans, the fused post-processing + Eq. 8 tail, FDK of the corrected stack.
+// Only thresholds, statistics and the reports cross to the host.
+void xs_correction_config_default(xs_correction_config* cc)
+{
+    std::memset(cc, 0, sizeof *cc);
+    cc->n_iterations = 3;
+    cc->simulate_every_kth_angle = 2;
+    cc->recon_dims[0] = cc->recon_dims[1] = cc->recon_dims[2] = 64;
+    cc->n_classes = 3;
+    xs_sim_config_default(&cc->sim);
+    cc->sg_window = 15;
+    cc->sg_polyorder = 3;
+    cc->sg_auto_window = 1;
+}
+
+static void call_status(xs_context* c, int st)
+{
+    if (st != XS_OK)
+        fail(st, "%s", c->err.c_str());
+}
+
+static void loop_stage(xs_context* c, int iteration, const char* name, const std::function<void()>& f)
+{
+    try {
+        f();
+    } catch (const Error& e) { // REF correction.cpp:22-31
+        fail(XS_E_RUNTIME, "iteration %d, stage %s: %s", iteration, name, e.msg.c_str());
+    }
+    (void)c;
+}
+
+int xs_run_iterative_correction(xs_context* c, const double* raw_intensity, const double* flatfield,
+                                const xs_geometry* g, const xs_spectrum* spec, const xs_correction_config* cc,
+                                int32_t n_materials, const xs_material* materials, float* corrected_volume,
+                                double* corrected_stack, xs_iteration_report* reports, int32_t device_ptrs)
+{
+    return guard(c, [&] {
+        using clk = std::chrono::steady_clock;
+        auto secs = [](clk::time_point t0) { return std::chrono::duration<double>(clk::now() - t0).count(); };
+        // REF validate_correction_config (correction.cpp:35-59), n_materials incl. vacuum
+        if (cc->n_iterations < 1)
+            fail(XS_E_RUNTIME, "correction config: n_iterations must be >= 1");
+        if (cc->simulate_every_kth_angle < 1)
+            fail(XS_E_RUNTIME, "correction config: simulate_every_kth_angle must be >= 1");
+        if (cc->n_classes < 2 || cc->n_classes > 4)
+            fail(XS_E_RUNTIME, "correction config: n_classes must be in [2,4]");
+        if (!cc->class_map)
+            fail(XS_E_RUNTIME, "correction config: class_map must have n_classes entries");
+        for (int l = 0; l < cc->n_classes; ++l) {
+            const xs_class_spec& k = cc->class_map[l];
+            if (k.material_id < 0 || k.material_id >= n_materials)
+                fail(XS_E_RUNTIME, "correction config: class material id %d out of range", k.material_id);
+            if (k.material_id == 0 && k.density != 0.0)
+                fail(XS_E_RUNTIME, "correction config: vacuum class must have density 0");
+            if (k.density < 0.0)
+                fail(XS_E_RUNTIME, "correction config: negative class density");
+        }
+        for (int d : cc->recon_dims)
+            if (d <= 0)
+                fail(XS_E_RUNTIME, "correction config: recon dims must be positive");
+        xsh::validate_sim_config(cc->sim);
+        xsh::validate_geometry(*g);
+        if (!c->have_response)
+            fail(XS_E_RUNTIME, "xscat-gpu: no detector response uploaded (xs_upload_response)");
+        const int nu = g->nu, nv = g->nv, n_full = g->n_angles;
+        const int mc_nu = cc->mc_nu > 0 ? cc->mc_nu : nu, mc_nv = cc->mc_nv > 0 ? cc->mc_nv : nv;
+        if ((long long)mc_nv * nu != (long long)mc_nu * nv)
+            fail(XS_E_RUNTIME, "run_iterative_correction: mc grid must preserve the detector aspect ratio");
+        xs_geometry g_mc = *g;
+        g_mc.nu = mc_nu;
+        g_mc.nv = mc_nv;
+        g_mc.pixel_pitch = g->pixel_pitch * g->nu / mc_nu;
+        int32_t sg_w = cc->sg_window, sg_o = cc->sg_polyorder;
+        if (cc->sg_auto_window) {
+            int32_t dummy;
+            xs_default_sg_spec(mc_nu, mc_nv, &sg_w, &dummy);
+        }
+        if (xs_validate_sg_spec(sg_w, sg_o) != XS_OK)
+            fail(XS_E_RUNTIME, "%s", xs_last_error(nullptr));
+        std::vector<int32_t> sub, all(n_full);
+        for (int i = 0; i < n_full; i += cc->simulate_every_kth_angle)
+            sub.push_back(i);
+        std::vector<double> sub_angles;
+        for (int i : sub)
+            sub_angles.push_back(g->angles[i]);
+        for (int i = 0; i < n_full; ++i)
+            all[i] = i;
+        const size_t np = (size_t)nu * nv, np_mc = (size_t)mc_nu * mc_nv;
+        const size_t nvox = (size_t)cc->recon_dims[0] * cc->recon_dims[1] * cc->recon_dims[2];
+        cudaStream_t st = c->stream;
+
+        // One-time path (REF :171-178): a = ln(flat / I), FDK of a
+        c->loop_a.reserve(np * n_full);
+        c->loop_c.reserve(np * n_full);
+        const double* raw = raw_intensity;
+        const double* flat = flatfield;
+        if (!device_ptrs) {
+            cuda_check(cudaMemcpyAsync(c->loop_c.p, raw_intensity, np * n_full * 8, cudaMemcpyHostToDevice, st), "H2D");
+            c->loop_flat.reserve(np);
+            cuda_check(cudaMemcpyAsync(c->loop_flat.p, flatfield, np * 8, cudaMemcpyHostToDevice, st), "H2D");
+            raw = c->loop_c.p;
+            flat = c->loop_flat.p;
+        }
+        call_status(c, xs_intensity_to_attenuation(c, raw, flat, nu, nv, n_full, c->loop_a.p, 1));
+        double voxel[3];
+        xs_default_voxel_size(g, cc->recon_dims, voxel);
+        c->loop_vol[0].reserve(nvox);
+        c->loop_vol[1].reserve(nvox);
+        call_status(c, xs_fbp_reconstruct(c, c->loop_a.p, g->angles, n_full, nu, nv, g, cc->recon_dims, voxel, 1,
+                                          c->loop_vol[0].p, 1));
+        c->loop_scat.reserve(np_mc * sub.size());
+        c->loop_prim.reserve(np_mc * n_full);
+        c->loop_ncc.reserve(xsd::ncc_scratch_bytes() / 8);
+        int prev = 0;
+        for (int iter = 1; iter <= cc->n_iterations; ++iter) {
+            xs_iteration_report rep{};
+            rep.iteration = iter;
+            const auto t_iter = clk::now();
+            auto t0 = clk::now();
+            double thr[4];
+            loop_stage(c, iter, "segmentation", [&] {
+                call_status(c, xs_segment_to_scene(c, c->loop_vol[prev].p, cc->recon_dims, voxel, cc->n_classes, 1024,
+                                                   cc->class_map, cc->recon_dims, n_materials, materials, thr, 1));
+            });
+            rep.seconds_segmentation = secs(t0);
+            t0 = clk::now();
+            loop_stage(c, iter, "mc-scatter", [&] {
+                scan_device_impl(c, &g_mc, spec, &cc->sim, sub.data(), (int32_t)sub.size(), 1, nullptr,
+                                 c->loop_scat.p, nullptr);
+            });
+            rep.seconds_mc_scatter = secs(t0);
+            t0 = clk::now();
+            loop_stage(c, iter, "mc-primary", [&] {
+                scan_device_impl(c, &g_mc, spec, &cc->sim, all.data(), n_full, 0, c->loop_prim.p, nullptr, nullptr);
+            });
+            rep.seconds_mc_primary = secs(t0);
+            rep.mc_seconds_per_projection = rep.seconds_mc_scatter / (double)sub.size();
+            // REF :199-246 post-processing, scatter fraction and Eq. 8, fused
+            t0 = clk::now();
+            uint64_t clamped = 0;
+            loop_stage(c, iter, "postprocess", [&] {
+                call_status(c, xs_correction_tail(c, c->loop_scat.p, sub_angles.data(), (int32_t)sub.size(),
+                                                  c->loop_prim.p, g->angles, n_full, mc_nu, mc_nv, sg_w, sg_o,
+                                                  c->loop_a.p, nu, nv, c->loop_c.p, &rep.mean_scatter_fraction,
+                                                  &clamped, 1));
+            });
+            rep.seconds_postprocess = secs(t0);
+            rep.seconds_correction = 0.0; // fused into the tail above
+            rep.negative_scatter_clamped = clamped;
+            t0 = clk::now();
+            loop_stage(c, iter, "fbp", [&] {
+                call_status(c, xs_fbp_reconstruct(c, c->loop_c.p, g->angles, n_full, nu, nv, g, cc->recon_dims, voxel,
+                                                  1, c->loop_vol[prev ^ 1].p, 1));
+            });
+            rep.seconds_fbp = secs(t0);
+            // REF :255-256 ncc(corrected, previous)
+            double m[5];
+            cuda_check(xsd::launch_ncc(c->loop_vol[prev ^ 1].p, c->loop_vol[prev].p, nvox, c->loop_ncc.p, st), "ncc");
+            cuda_check(cudaMemcpyAsync(m, c->loop_ncc.p, sizeof m, cudaMemcpyDeviceToHost, st), "D2H");
+            cuda_check(cudaStreamSynchronize(st), "ncc");
+            if (!(m[3] > 0.0) || !(m[4] > 0.0))
+                fail(XS_E_RUNTIME, "ncc: zero variance input");
+            rep.ncc_to_previous = m[2] / std::sqrt(m[3] * m[4]);
+            prev ^= 1;
+            rep.seconds_total = secs(t_iter);
+            if (reports)
+                reports[iter - 1] = rep;
+        }
+        const cudaMemcpyKind k = device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+        if (corrected_volume)
+            cuda_check(cudaMemcpyAsync(corrected_volume, c->loop_vol[prev].p, nvox * 4, k, st), "volume out");
+        if (corrected_stack)
+            cuda_check(cudaMemcpyAsync(corrected_stack, c->loop_c.p, np * n_full * 8, k, st), "stack out");
+        cuda_check(cudaStreamSynchronize(st), "run_iterative_correction");
     });
 }
 

@@ -455,7 +455,91 @@ int grid_for(uint64_t n, int sm_count)
     return (int)(want < cap ? (want ? want : 1) : cap);
 }
 
+// Normalised cross-correlation of two float volumes (REF metrics.cpp:19-35,
+// the loop's ncc_to_previous report): two passes (means, then centred
+// moments) with per-block fp64 partials over a fixed grid, combined in block
+// order by one thread, so the value does not depend on the schedule.
+constexpr int kNccBlocks = 592;
+
+__device__ __forceinline__ void block_sum3(double& a, double& b, double& c)
+{
+    __shared__ double sh[3][kThr];
+    sh[0][threadIdx.x] = a;
+    sh[1][threadIdx.x] = b;
+    sh[2][threadIdx.x] = c;
+    __syncthreads();
+    for (int s = kThr / 2; s > 0; s >>= 1) {
+        if ((int)threadIdx.x < s) {
+            sh[0][threadIdx.x] += sh[0][threadIdx.x + s];
+            sh[1][threadIdx.x] += sh[1][threadIdx.x + s];
+            sh[2][threadIdx.x] += sh[2][threadIdx.x + s];
+        }
+        __syncthreads();
+    }
+    a = sh[0][0];
+    b = sh[1][0];
+    c = sh[2][0];
+}
+
+__global__ void __launch_bounds__(kThr) ncc_pass(const float* __restrict__ x1, const float* __restrict__ x2, uint64_t n,
+                                                 const double* __restrict__ means, double* __restrict__ partial)
+{
+    double a = 0.0, b = 0.0, c = 0.0;
+    const bool centred = means != nullptr;
+    const double m1 = centred ? means[0] : 0.0, m2 = centred ? means[1] : 0.0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const double u = (double)x1[i] - m1, v = (double)x2[i] - m2;
+        if (centred) {
+            a += u * v;
+            b += u * u;
+            c += v * v;
+        } else {
+            a += u;
+            b += v;
+        }
+    }
+    block_sum3(a, b, c);
+    if (threadIdx.x == 0) {
+        partial[3 * blockIdx.x + 0] = a;
+        partial[3 * blockIdx.x + 1] = b;
+        partial[3 * blockIdx.x + 2] = c;
+    }
+}
+
+__global__ void ncc_combine(const double* __restrict__ partial, int n_blocks, uint64_t n, double* __restrict__ out,
+                            int final_pass)
+{
+    double a = 0.0, b = 0.0, c = 0.0;
+    for (int i = 0; i < n_blocks; ++i) {
+        a += partial[3 * i + 0];
+        b += partial[3 * i + 1];
+        c += partial[3 * i + 2];
+    }
+    if (!final_pass) { // means
+        out[0] = a / (double)n;
+        out[1] = b / (double)n;
+    } else { // cov, v1, v2
+        out[2] = a;
+        out[3] = b;
+        out[4] = c;
+    }
+}
+
 } // namespace
+
+size_t ncc_scratch_bytes() { return (3 * (size_t)kNccBlocks + 8) * sizeof(double); }
+
+// out[0..4] = mean1, mean2, cov, var1, var2 (device); ncc = cov / sqrt(v1 v2)
+cudaError_t launch_ncc(const float* x1, const float* x2, uint64_t n, void* scratch, cudaStream_t s)
+{
+    double* out = static_cast<double*>(scratch);
+    double* partial = out + 8;
+    ncc_pass<<<kNccBlocks, kThr, 0, s>>>(x1, x2, n, nullptr, partial);
+    ncc_combine<<<1, 1, 0, s>>>(partial, kNccBlocks, n, out, 0);
+    ncc_pass<<<kNccBlocks, kThr, 0, s>>>(x1, x2, n, out, partial);
+    ncc_combine<<<1, 1, 0, s>>>(partial, kNccBlocks, n, out, 1);
+    return cudaGetLastError();
+}
 
 size_t seg_ctl_bytes() { return sizeof(SegCtl); }
 

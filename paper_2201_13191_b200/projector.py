@@ -522,3 +522,76 @@ def segment_to_scene(vol, voxel_size, n_classes: int, class_map, target_dims, ma
     if response is not None:
         ctx.check(A.lib().xs_upload_response(ctx.h, C.byref(pk.response(response))))
     return [float(x) for x in thr[:int(n_classes) - 1]]
+
+
+# --------------------------------------------------- iterative correction
+@dataclasses.dataclass
+class CorrectionConfig:
+    """REF CorrectionConfig (correction.hpp:13-24), same defaults."""
+    n_iterations: int = 3
+    simulate_every_kth_angle: int = 2
+    mc_nu: int = 0
+    mc_nv: int = 0
+    recon_dims: tuple = (64, 64, 64)
+    n_classes: int = 3
+    class_map: list = dataclasses.field(default_factory=list)
+    sim: I.SimConfig = dataclasses.field(default_factory=I.SimConfig)
+    sg: SgFilterSpec = dataclasses.field(default_factory=lambda: SgFilterSpec(15, 3))
+    sg_auto_window: bool = True
+    workers: int = 1
+
+
+@dataclasses.dataclass
+class IterationReport:
+    """REF IterationReport (correction.hpp:26-39); seconds_postprocess holds
+    the fused post-processing + correction pass (seconds_correction = 0)."""
+    iteration: int
+    seconds_fbp: float
+    seconds_segmentation: float
+    seconds_mc_scatter: float
+    seconds_mc_primary: float
+    seconds_postprocess: float
+    seconds_correction: float
+    seconds_total: float
+    mc_seconds_per_projection: float
+    mean_scatter_fraction: float
+    ncc_to_previous: float
+    negative_scatter_clamped: int
+
+
+@dataclasses.dataclass
+class CorrectionResult:
+    """REF CorrectionResult (correction.hpp:53-57)."""
+    corrected_volume: np.ndarray
+    corrected_stack: ProjectionStack
+    reports: List[IterationReport]
+
+
+def reports_from(arr, n) -> List[IterationReport]:
+    names = [k for k, _ in A.XsIterationReport._fields_ if k != "pad_"]
+    return [IterationReport(**{k: getattr(arr[i], k) for k in names}) for i in range(n)]
+
+
+def run_iterative_correction(raw_intensity: ProjectionStack, flatfield, g: I.ScanGeometry, spec: I.Spectrum,
+                             resp: I.DetectorResponse, cfg: CorrectionConfig, materials,
+                             ctx: Optional[Context] = None) -> CorrectionResult:
+    """REF run_iterative_correction (correction.cpp:137-266) with every stage
+    on the device; `materials` is REF's list (vacuum prepended here)."""
+    ctx = ctx or default_context()
+    raw = np.ascontiguousarray(raw_intensity.images, dtype=np.float64)
+    if raw.shape[0] != g.n_angles:
+        raise I.XscatError("run_iterative_correction: stack angle count mismatch")
+    flat = np.ascontiguousarray(flatfield, dtype=np.float64)
+    mats = [None] + [m for m in materials if m is not None]
+    pk = A.Packed()
+    ctx.check(A.lib().xs_upload_response(ctx.h, C.byref(pk.response(resp))))
+    vol = np.empty(tuple(int(d) for d in cfg.recon_dims[::-1]), np.float32)
+    stack = np.empty_like(raw)
+    reps = (A.XsIterationReport * max(1, int(cfg.n_iterations)))()
+    ctx.check(A.lib().xs_run_iterative_correction(ctx.h, raw.ctypes.data, flat.ctypes.data,
+                                                  C.byref(pk.geometry(g)), C.byref(pk.spectrum(spec)),
+                                                  C.byref(pk.correction_config(cfg)), len(mats),
+                                                  pk.materials(mats), vol.ctypes.data, stack.ctypes.data,
+                                                  reps, 0))
+    return CorrectionResult(vol, ProjectionStack(list(raw_intensity.angle_values), stack),
+                            reports_from(reps, int(cfg.n_iterations)))

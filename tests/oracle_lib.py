@@ -83,6 +83,10 @@ def _sig(L, prefix):
             "xr_analog_scatter": (C.c_int, [_ph, _g, C.c_int32, _s, _r, C.c_uint64, C.c_uint64,
                                             _dp, _dp, _dp]),
             "xr_trace_sorted_crossings": (C.c_int, [_ph, _dp, _dp, C.c_double, _dp]),
+            "xr_run_iterative_correction": (C.c_int, [_dp, _dp, _g, _s, _r,
+                                                      C.POINTER(A.XsCorrectionConfig), C.c_int32, _m,
+                                                      C.c_void_p, C.c_void_p,
+                                                      C.POINTER(A.XsIterationReport), C.c_int32]),
             "xr_make_phantom": (C.c_int, [C.c_int32, C.c_int32, C.c_double, _dp, C.c_double,
                                           C.POINTER(C.c_int32), _dp, _dp,
                                           C.POINTER(C.c_uint8), C.POINTER(C.c_float)]),
@@ -338,6 +342,23 @@ class Oracle:
                                                  len(class_map), tgt, len(mats), pk.materials(mats),
                                                  ids.ctypes.data, dens.ctypes.data))
         return ids, dens
+
+
+    def run_iterative_correction(self, raw, flat, g, spec, resp, cfg, materials, workers=8):
+        """REF run_iterative_correction (xr_ only); returns (volume, stack, reports)."""
+        from paper_2201_13191_b200 import projector as P
+        raw = np.ascontiguousarray(raw, np.float64)
+        flat = np.ascontiguousarray(flat, np.float64)
+        mats = [None] + [m for m in materials if m is not None]
+        pk = A.Packed()
+        vol = np.empty(tuple(int(d) for d in cfg.recon_dims[::-1]), np.float32)
+        stack = np.empty_like(raw)
+        reps = (A.XsIterationReport * cfg.n_iterations)()
+        self.check(self.fn("run_iterative_correction")(
+            A.dptr(raw), A.dptr(flat), C.byref(pk.geometry(g)), C.byref(pk.spectrum(spec)),
+            C.byref(pk.response(resp)), C.byref(pk.correction_config(cfg)), len(mats),
+            pk.materials(mats), vol.ctypes.data, stack.ctypes.data, reps, workers))
+        return vol, stack, P.reports_from(reps, cfg.n_iterations)
 
 
 _oracle = None

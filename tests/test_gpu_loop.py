@@ -1,0 +1,99 @@
+"""The whole iterative correction loop on the device (xs_run_iterative_correction)
+against the compiled reference's run_iterative_correction (correction.cpp:137-266)
+on REF's own loop tests (test_correction.cpp:118-230).
+
+Every stage is REF's arithmetic, but two are not bit-exact against glibc:
+the device log in the ln conversion / Eq. 8, and the scatter tallies'
+fixed-point sums (quantum 2^-64 of the peak).  So the loop's outputs are
+compared with tolerances far below Monte Carlo noise; the segmentation
+(thresholds, phantom) is expected to come out identical."""
+import numpy as np
+import pytest
+
+import paper_2201_13191_b200 as X
+from paper_2201_13191_b200 import inputs as I
+from paper_2201_13191_b200 import synthetic as S
+from paper_2201_13191_b200.projector import ClassSpec, CorrectionConfig
+
+pytestmark = pytest.mark.gpu
+
+
+def measurement(ph, g, spec, resp, truth_cfg, with_scatter):
+    proj = X.Projector(ph, resp)
+    run = proj.run_scan(g, spec, truth_cfg, list(range(g.n_angles)), X.BOTH if with_scatter else X.PRIMARY)
+    raw = run.primary.images.copy()
+    if with_scatter:
+        sm = X.sg_smooth(run.scatter.images, X.default_sg_spec(g.nu, g.nv))
+        raw += np.maximum(0.0, sm)
+    empty = I.make_empty_phantom(*ph.dims, ph.voxel_size, [m for m in ph.materials if m is not None])
+    flat = X.Projector(empty, resp).primary(g, 0, spec, truth_cfg)
+    return raw, flat
+
+
+def compare(dev, ref_out, vol_tol, stack_tol):
+    vol, stack, reps = ref_out
+    assert len(dev.reports) == len(reps)
+    for a, b in zip(dev.reports, reps):
+        assert a.iteration == b.iteration
+        assert a.ncc_to_previous == pytest.approx(b.ncc_to_previous, rel=1e-9, abs=1e-12)
+        assert a.mean_scatter_fraction == pytest.approx(b.mean_scatter_fraction, rel=1e-9, abs=1e-15)
+        assert abs(a.negative_scatter_clamped - b.negative_scatter_clamped) <= max(2, b.negative_scatter_clamped // 1000)
+    scale = float(np.max(np.abs(vol)))
+    assert np.max(np.abs(dev.corrected_volume - vol)) <= vol_tol * scale
+    assert np.allclose(dev.corrected_stack.images, stack, rtol=stack_tol, atol=stack_tol)
+
+
+def test_scatter_free_fixed_point(ref):
+    # REF test_correction.cpp:118-160
+    w = I.material("water")
+    n = 24
+    ph = S.make_cylinder_phantom(n, 0.3, 2.2, 5.0, w, 1.0)
+    g = I.make_circular_geometry(60.0, 40.0, 24, 24, 0.5, 36)
+    spec, resp = I.monochromatic_spectrum(100.0), I.detector_response()
+    sim = I.SimConfig(photons_total=2000, splitting=4, seed=99)
+    raw, flat = measurement(ph, g, spec, resp, sim, False)
+    cfg = CorrectionConfig(n_iterations=1, simulate_every_kth_angle=2, mc_nu=12, mc_nv=12,
+                           recon_dims=(n, n, n), n_classes=2, class_map=[ClassSpec(0, 0.0), ClassSpec(1, 1.0)],
+                           sim=sim)
+    dev = X.run_iterative_correction(X.ProjectionStack(g.angles, raw), flat, g, spec, resp, cfg, [w])
+    assert dev.reports[0].ncc_to_previous > 0.999
+    compare(dev, ref.run_iterative_correction(raw, flat, g, spec, resp, cfg, [w]), 1e-5, 1e-9)
+
+
+def test_cement_iron_two_iterations(ref):
+    # REF test_correction.cpp:162-230 (smaller grid, two iterations)
+    cem, fe = I.material("cement"), I.material("iron")
+    n = 32
+    ph = S.make_rods_phantom(n, 0.27, 3.2, 6.0, cem, 2.3, 2, 0.6, 1.9, fe, 7.874)
+    det = 32
+    g = I.make_circular_geometry(60.0, 40.0, det, det, 14.0 / det, 48)
+    spec, resp = I.monochromatic_spectrum(100.0), I.detector_response()
+    truth = I.SimConfig(photons_total=20000, splitting=10, seed=808)
+    raw, flat = measurement(ph, g, spec, resp, truth, True)
+    cfg = CorrectionConfig(n_iterations=2, simulate_every_kth_angle=2, mc_nu=16, mc_nv=16,
+                           recon_dims=(n, n, n), n_classes=3,
+                           class_map=[ClassSpec(0, 0.0), ClassSpec(1, 2.3), ClassSpec(2, 7.874)],
+                           sim=I.SimConfig(photons_total=5000, splitting=5, seed=4242))
+    dev = X.run_iterative_correction(X.ProjectionStack(g.angles, raw), flat, g, spec, resp, cfg, [cem, fe])
+    assert all(r.mean_scatter_fraction > 0 for r in dev.reports)
+    compare(dev, ref.run_iterative_correction(raw, flat, g, spec, resp, cfg, [cem, fe]), 1e-5, 1e-9)
+
+
+def test_loop_errors():
+    w = I.material("water")
+    g = I.make_circular_geometry(60.0, 40.0, 16, 16, 0.5, 24)
+    spec, resp = I.monochromatic_spectrum(100.0), I.detector_response()
+    raw = X.ProjectionStack(g.angles, np.ones((24, 16, 16)))
+    flat = np.full((16, 16), 2.0)
+    cfg = CorrectionConfig(n_iterations=1, recon_dims=(8, 8, 8), n_classes=2,
+                           class_map=[ClassSpec(0, 0.5), ClassSpec(1, 1.0)])
+    with pytest.raises(I.XscatError, match="vacuum class must have density 0"):
+        X.run_iterative_correction(raw, flat, g, spec, resp, cfg, [w])
+    cfg.class_map = [ClassSpec(0, 0.0), ClassSpec(1, 1.0)]
+    cfg.mc_nu, cfg.mc_nv = 8, 4
+    with pytest.raises(I.XscatError, match="aspect ratio"):
+        X.run_iterative_correction(raw, flat, g, spec, resp, cfg, [w])
+    cfg.mc_nu, cfg.mc_nv = 8, 8
+    # a flat measurement: constant FDK volume -> Otsu fails inside the first iteration
+    with pytest.raises(I.XscatError, match="iteration 1, stage segmentation: otsu: degenerate histogram"):
+        X.run_iterative_correction(raw, np.ones((16, 16)), g, spec, resp, cfg, [w])
