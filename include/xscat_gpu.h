@@ -158,6 +158,7 @@ typedef struct xs_launch_stats {
     uint64_t uniform_iterations; /* walker iterations that crossed a uniform cell / brick */
     float walk_ms;             /* device time of the walk kernel(s) (the whole kernel for the megakernel) */
     uint32_t launches;         /* kernels launched by the scatter call */
+    uint32_t block_walk;       /* 1: the walk crossed uniform blocks (walk_mode, per-phantom probe) */
 } xs_launch_stats;
 
 typedef struct xs_context xs_context;

@@ -101,7 +101,8 @@ class XsLaunchStats(C.Structure):
                 ("walk_lane_slots", C.c_uint64), ("blocks_per_sm", C.c_uint32),
                 ("smem_per_block", C.c_uint32), ("slots_per_warp", C.c_uint32),
                 ("engine", C.c_uint32), ("waves", C.c_uint32), ("live_histories", C.c_uint32),
-                ("uniform_iterations", C.c_uint64), ("walk_ms", C.c_float), ("launches", C.c_uint32)]
+                ("uniform_iterations", C.c_uint64), ("walk_ms", C.c_float), ("launches", C.c_uint32),
+                ("block_walk", C.c_uint32)]
 
 
 def dptr(a: np.ndarray):

@@ -42,6 +42,7 @@ cudaError_t launch_correct(const double* a, const double* ip, const double* is, 
 cudaError_t launch_correction_tail(const double* primary, const double* scatter, const double* a, double* tmp,
                                    double* out, int nu, int nv, int n_views, int nu_out, int nv_out, void* stats,
                                    cudaStream_t s);
+cudaError_t launch_walk_probe(const TransportParams& P, unsigned long long* iters, cudaStream_t s);
 cudaError_t launch_mark_levels(uint8_t* vox, const Grid& G, int fmt, const int* edges, int n_levels,
                                void* scratch, int sm_count, cudaStream_t s);
 size_t seg_ctl_bytes();
@@ -228,7 +229,10 @@ struct xs_context {
     DevBuf<float> loop_vol[2];
     int smem_kb = 48; // per transport block: 4 blocks/SM leave 60 KB of L1
     int max_slots = 64;
-    int macro_skip = 1;
+    int macro_skip = 2;  // 0: voxel walk, 1: cross uniform blocks, 2: decided per phantom at upload
+    bool skip_pays = true; // walk probe of the uploaded phantom (launch_walk_probe)
+    unsigned long long probe_iters[2] = {0, 0};
+    DevBuf<unsigned long long> probe;
 
     xs_launch_stats last{};
     int grab = 64;
@@ -328,6 +332,8 @@ void check_status(xs_context* c, int angle_idx, const xs_spectrum* spec)
     }
     case xsd::kErrComptonS:
         fail(XS_E_RUNTIME, "sample_compton: S vanishes over the kinematic range at %f keV", e);
+    case xsd::kErrStuck:
+        fail(XS_E_RUNTIME, "simulate_scatter: transport did not terminate (E %f keV, site %g) - corrupt state", e, s.value);
     case xsd::kErrRayleighF:
         fail(XS_E_RUNTIME, "sample_rayleigh: F vanishes over the kinematic range at %f keV", e);
     default:
@@ -622,7 +628,7 @@ void accumulate(xs_context* c, const xs_geometry& g, int angle, const xs_spectru
     P.step_voxels = cfg.step_voxels;
     P.max_inter = cfg.max_interactions;
     P.track_var = cfg.track_variance ? 1 : 0;
-    P.skip = c->macro_skip;
+    P.skip = c->macro_skip == 2 ? (c->skip_pays ? 1 : 0) : c->macro_skip;
     { // shared energy knots of the mu tables (REF bundle: yes)
         int first = -1;
         bool same = true;
@@ -696,6 +702,7 @@ void accumulate(xs_context* c, const xs_geometry& g, int angle, const xs_spectru
         c->last.launches = info.launches;
         c->last.palette_size = c->n_pal;
         c->last.upload_bytes = c->last_upload_bytes;
+        c->last.block_walk = P.skip && c->grid.ubit ? 1u : 0u;
         return;
     }
 
@@ -746,6 +753,7 @@ void accumulate(xs_context* c, const xs_geometry& g, int angle, const xs_spectru
     c->last.launches = 1;
     c->last.palette_size = c->n_pal;
     c->last.upload_bytes = c->last_upload_bytes;
+    c->last.block_walk = P.skip && c->grid.ubit ? 1u : 0u;
 }
 
 void finalize(xs_context* c, const xs_geometry& g, const xs_spectrum& spec, const xs_sim_config& cfg,
@@ -870,6 +878,8 @@ int xs_ctx_create(int32_t device, xs_context** out)
         if (device < 0 || device >= n)
             fail(XS_E_OUT_OF_RANGE, "xs_ctx_create: device %d out of range (%d devices)", device, n);
         cuda_check(cudaSetDevice(device), "cudaSetDevice");
+        if (const char* e = std::getenv("XSCAT_STACK"))
+            cuda_check(cudaDeviceSetLimit(cudaLimitStackSize, (size_t)std::atoi(e)), "stack limit");
         auto* c = new xs_context();
         c->device = device;
         cudaDeviceProp prop;
@@ -884,7 +894,7 @@ int xs_ctx_create(int32_t device, xs_context** out)
         if (const char* e = std::getenv("XSCAT_SMEM_KB"))
             c->smem_kb = std::max(8, std::min(227, std::atoi(e)));
         if (const char* e = std::getenv("XSCAT_SKIP"))
-            c->macro_skip = std::atoi(e) != 0;
+            c->macro_skip = std::max(0, std::min(2, std::atoi(e)));
         if (const char* e = std::getenv("XSCAT_SLOTS"))
             c->max_slots = std::max(1, std::min(64, std::atoi(e)));
         if (const char* e = std::getenv("XSCAT_LEVELS")) { // e.g. "4,16,64"
@@ -962,6 +972,7 @@ void xs_ctx_destroy(xs_context* c)
     c->seg_dens.release();
     c->seg_vol.release();
     c->seg_pal.release();
+    c->probe.release();
     for (auto* b : {&c->loop_a, &c->loop_c, &c->loop_scat, &c->loop_prim, &c->loop_flat, &c->loop_ncc})
         b->release();
     c->loop_vol[0].release();
@@ -987,6 +998,8 @@ int xs_ctx_set_option(xs_context* c, const char* key, int64_t value)
         const std::string k = key ? key : "";
         if (k == "exact_walk") {
             c->macro_skip = value ? 0 : 1;
+        } else if (k == "walk_mode") { // 0 voxel walk, 1 block walk, 2 per phantom (default)
+            c->macro_skip = (int)std::max<int64_t>(0, std::min<int64_t>(2, value));
         } else if (k == "smem_kb") {
             c->smem_kb = (int)std::max<int64_t>(8, std::min<int64_t>(227, value));
         } else if (k == "max_slots") {
@@ -1183,6 +1196,21 @@ static void upload_phantom_impl(xs_context* c, const xs_phantom* ph, bool on_dev
         G.vox = c->vox.p;
         G.dens = fmt == xsd::kFmtRaw ? c->dens.p : nullptr;
         c->grid = G;
+        c->skip_pays = false;
+        if (fmt != xsd::kFmtRaw && G.ubit) { // does crossing uniform blocks pay on this grid?
+            xsd::TransportParams P{};
+            P.G = G;
+            for (int k = 0; k < n_pairs && k < xsd::kMaxPalette; ++k)
+                P.pal_mat[k] = scan.pairs[k].id;
+            c->probe.reserve(2);
+            cuda_check(xsd::launch_walk_probe(P, c->probe.p, c->stream), "walk probe");
+            unsigned long long it[2];
+            cuda_check(cudaMemcpyAsync(it, c->probe.p, sizeof it, cudaMemcpyDeviceToHost, c->stream), "D2H");
+            cuda_check(cudaStreamSynchronize(c->stream), "walk probe");
+            c->skip_pays = (double)it[1] < 0.6 * (double)it[0]; // a block step costs ~1.7 voxel steps
+            c->probe_iters[0] = it[0];
+            c->probe_iters[1] = it[1];
+        }
         c->n_mats = ph->n_materials;
         c->mats.assign(ph->n_materials, HMat{});
         for (int m = 0; m < ph->n_materials; ++m) {

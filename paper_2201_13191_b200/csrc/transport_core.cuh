@@ -579,6 +579,10 @@ __device__ __noinline__ void finalize_history(const TransportParams& P, const Bl
         const int n = S.n_var < P.var_cap ? S.n_var : P.var_cap;
         for (int a = 0; a < n; ++a) {
             const uint32_t pa = vp[a];
+            if (pa >= (uint32_t)P.nu * (uint32_t)P.nv) { // corrupt scratch: report, never write out of bounds
+                raise(st, XS_E_RUNTIME, kErrStuck, S.bin, S.E, 14.0);
+                continue;
+            }
             bool dup = false;
             for (int b = 0; b < a; ++b)
                 if (vp[b] == pa) {
@@ -679,6 +683,11 @@ __device__ __noinline__ int event_select(const TransportParams& P, const Block& 
     float dens;
     fetch<FMT>(P.G, vix, viy, viz, code, dens);
     const int mat = material_of<FMT>(P, code & ~P.G.ubit);
+    if (mat <= 0 || mat >= P.n_mats) { // an interaction needs matter: corrupt state
+        raise(st, XS_E_RUNTIME, kErrStuck, bin, S.E, 15.0);
+        end_history(P, B, qs, s, var_base, st);
+        return K_NONE;
+    }
     const MatDesc& md = P.mats[mat];
     const double E = S.E;
     // select_interaction (cross_sections.cpp:81-96); one knot search and one
@@ -756,10 +765,18 @@ __device__ __noinline__ void event_continue(const TransportParams& P, const Bloc
         if (!(s_max > 0.0)) {
             raise(st, XS_E_RUNTIME, kErrComptonS, bin, E, 0.0);
         } else {
+            // trials are bounded (2^24 draws) so corrupt state raises instead of hanging
+            uint32_t trials = 0;
             for (;;) {
+                if (trials > (1u << 24)) {
+                    raise(st, XS_E_RUNTIME, kErrStuck, bin, E, 1.0 + S.mat);
+                    break;
+                }
                 const double t = 1.0 + 2.0 * alpha; // kahn_sample_cos_theta, samplers.cpp:12-30
-                double cos_th;
-                for (;;) {
+                double cos_th = 1.0;
+                for (;; ++trials) {
+                    if (trials > (1u << 24))
+                        break;
                     const double r1 = slot_uniform(&rng, P.k0, P.k1, P.angle);
                     const double r2 = slot_uniform(&rng, P.k0, P.k1, P.angle);
                     const double r3 = slot_uniform(&rng, P.k0, P.k1, P.angle);
@@ -798,7 +815,11 @@ __device__ __noinline__ void event_continue(const TransportParams& P, const Bloc
             raise(st, XS_E_RUNTIME, kErrRayleighF, bin, E, 0.0);
         } else {
             const double scale = kHc / E;
-            for (;;) {
+            for (uint32_t trials = 0;; ++trials) {
+                if (trials > (1u << 24)) {
+                    raise(st, XS_E_RUNTIME, kErrStuck, bin, E, 200.0 + S.mat);
+                    break;
+                }
                 const double qq = invert_mass(P, md, slot_uniform(&rng, P.k0, P.k1, P.angle) * tot, q_max);
                 const double sh = 1.0 < qq * scale ? 1.0 : qq * scale;
                 const double cos_th = 1.0 - 2.0 * sh * sh;

@@ -28,6 +28,8 @@
 // are the same fixed-point integers as the megakernel's, so both engines give
 // bit-identical images and statistics.
 #include <algorithm>
+#include <cstdio>
+#include <unistd.h>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -35,6 +37,11 @@
 #include "transport_core.cuh"
 
 namespace xsd {
+
+// Data-driven indices are validated before use: a violation (which would
+// mean corrupt pipeline state) raises a device error naming the site instead
+// of touching memory out of bounds.
+#define XS_GUARD(cond, st, site) (__builtin_expect(!!(cond), 1) ? true : (raise((st), XS_E_RUNTIME, kErrStuck, 0, 0.0, (site)), false))
 
 namespace {
 
@@ -96,35 +103,35 @@ struct WaveArgs {
     int32_t cur; // queue consumed by this wave (the other one is filled)
 };
 
-// Warp-aggregated atomicAdd: the converged lanes reserve their entries with
-// one atomic (a handful of queue counters take every push of the wave, so
-// per-lane atomics would serialise at L2).
-template <class T>
-__device__ __forceinline__ T warp_reserve(T* counter, T per_lane)
-{
-    const unsigned m = __activemask();
-    const int lane = threadIdx.x & 31;
-    const int leader = __ffs(m) - 1;
-    const T rank = (T)__popc(m & ((1u << lane) - 1u));
-    T base = 0;
-    if (lane == leader)
-        base = atomicAdd(counter, per_lane * (T)__popc(m));
-    base = __shfl_sync(m, base, leader);
-    return base + rank * per_lane;
-}
+// Queue pushes of the event code, deferred to a point where the warp has
+// reconverged.  The event functions run in deeply divergent code (rejection
+// loops of different lengths, __noinline__ calls); warp-aggregated
+// reservations there (__activemask + __shfl_sync) hung the event kernel on
+// some inputs.  Each lane records at most one push of each kind per window
+// and the kernel flushes them with full-warp ballots (flush_deferred).
+struct Deferred {
+    int32_t batch_slot, free_slot, rel_slot;
+    SlotRng rng;
+};
 
 // Queue policy of the wavefront engine (see transport_core.cuh).
 struct GlobalQ {
     Slot* slots;
     WaveCtl* ctl;
     int out;
-    int free_at; // >= 0: this thread's free-path entry is pre-reserved (admission)
+    int free_at;    // >= 0: this thread's free-path entry is pre-reserved (admission)
+    Deferred* def;  // this lane's deferred pushes
     __device__ __forceinline__ Slot& slot(int s) const { return slots[s]; }
     static constexpr bool kBatchScores = true;
     __device__ __forceinline__ void push_score_batch(int s, const SlotRng& r) const
     {
-        WaveQueue& q = ctl->q[out];
-        const uint32_t i = warp_reserve(&q.n_batch, 1u);
+        if (def->batch_slot < 0) {
+            def->batch_slot = s;
+            def->rng = r;
+            return;
+        }
+        WaveQueue& q = ctl->q[out]; // (a second push in one window: not aggregated)
+        const uint32_t i = atomicAdd(&q.n_batch, 1u);
         q.batch[i].slot = (uint32_t)s;
         q.batch[i].rng = r;
     }
@@ -134,17 +141,74 @@ struct GlobalQ {
     __device__ __forceinline__ void push_free(int s) const
     {
         WaveQueue& q = ctl->q[out];
-        const uint32_t i = free_at >= 0 ? (uint32_t)free_at : warp_reserve(&q.n_free, 1u);
-        q.free[i] = (uint32_t)s;
+        if (free_at >= 0)
+            q.free[free_at] = (uint32_t)s;
+        else if (def->free_slot < 0)
+            def->free_slot = s;
+        else
+            q.free[atomicAdd(&q.n_free, 1u)] = (uint32_t)s;
     }
     __device__ __forceinline__ void claim(int) const {}
     __device__ __forceinline__ void release(int s) const
     {
-        const int i = warp_reserve(&ctl->free_top, 1);
-        ctl->free_stack[i] = (uint32_t)s;
+        if (def->rel_slot < 0) {
+            def->rel_slot = s;
+            return;
+        }
+        ctl->free_stack[atomicAdd(&ctl->free_top, 1)] = (uint32_t)s;
     }
     __device__ __forceinline__ void fence() const { __threadfence(); }
 };
+
+__device__ __forceinline__ void deferred_reset(Deferred& d)
+{
+    d.batch_slot = d.free_slot = d.rel_slot = -1;
+}
+
+// All 32 lanes, converged: one reservation per queue for the warp's pushes.
+__device__ __forceinline__ void flush_deferred(WaveCtl* ctl, int out, Deferred& d, uint32_t n_slots, DevStatus* st)
+{
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    WaveQueue& q = ctl->q[out];
+    const unsigned mb = __ballot_sync(kFull, d.batch_slot >= 0);
+    if (mb) {
+        uint32_t base = 0;
+        if (lane == 0)
+            base = atomicAdd(&q.n_batch, (uint32_t)__popc(mb));
+        base = __shfl_sync(kFull, base, 0);
+        if (d.batch_slot >= 0) {
+            const uint32_t i = base + (uint32_t)__popc(mb & lt);
+            if (XS_GUARD(i < n_slots, st, 16.0)) {
+                q.batch[i].slot = (uint32_t)d.batch_slot;
+                q.batch[i].rng = d.rng;
+            }
+        }
+    }
+    const unsigned mf = __ballot_sync(kFull, d.free_slot >= 0);
+    if (mf) {
+        uint32_t base = 0;
+        if (lane == 0)
+            base = atomicAdd(&q.n_free, (uint32_t)__popc(mf));
+        base = __shfl_sync(kFull, base, 0);
+        if (d.free_slot >= 0) {
+            if (XS_GUARD(base + (uint32_t)__popc(mf & lt) < n_slots, st, 17.0))
+                q.free[base + (uint32_t)__popc(mf & lt)] = (uint32_t)d.free_slot;
+        }
+    }
+    const unsigned mr = __ballot_sync(kFull, d.rel_slot >= 0);
+    if (mr) {
+        int32_t base = 0;
+        if (lane == 0)
+            base = atomicAdd(&ctl->free_top, (int32_t)__popc(mr));
+        base = __shfl_sync(kFull, base, 0);
+        if (d.rel_slot >= 0) {
+            if (XS_GUARD((uint32_t)(base + __popc(mr & lt)) < n_slots, st, 18.0))
+                ctl->free_stack[base + __popc(mr & lt)] = (uint32_t)d.rel_slot;
+        }
+    }
+    deferred_reset(d);
+}
 
 __device__ __forceinline__ uint64_t var_base_of(const TransportParams& P, int s)
 {
@@ -358,8 +422,22 @@ __global__ void __launch_bounds__(kBlock, SKIP ? XSW_WALK_BLOCKS : XSW_WALK_BLOC
         }
         ++c_wit;
         if (walking) {
+#ifdef XSW_DEBUG_STUCK
+            const double t_prev = w.t, tnx0 = w.tnx, tny0 = w.tny, tnz0 = w.tnz;
+            const int ix0 = w.ix, iy0 = w.iy, iz0 = w.iz;
+            const uint32_t raw0 = w.raw;
+#endif
             walking = walk_step<FMT, REG, SKIP>(P, tab, w);
             ++w.steps;
+#ifdef XSW_DEBUG_STUCK
+            if (walking && w.steps > 100000u) {
+                printf("STUCK ray %u t %.17g->%.17g tn %.17g %.17g %.17g -> %.17g %.17g %.17g dt %.17g %.17g %.17g "
+                       "rd %.9g %.9g %.9g vox %d %d %d -> %d %d %d s %d %d %d raw %u texit %.17g\n",
+                       ray, t_prev, w.t, tnx0, tny0, tnz0, w.tnx, w.tny, w.tnz, w.dtx, w.dty, w.dtz, w.rdx, w.rdy,
+                       w.rdz, ix0, iy0, iz0, w.ix, w.iy, w.iz, w.sx, w.sy, w.sz, raw0, w.texit);
+                walking = false;
+            }
+#endif
             if (!walking) {
                 if (ray < n_s) {
                     R.res[ray] = w.depth;
@@ -397,6 +475,7 @@ __global__ void __launch_bounds__(kBlock, SKIP ? XSW_WALK_BLOCKS : XSW_WALK_BLOC
 // scoring rays sit next to each other in the queue, so a warp folds its
 // lanes' scores per slot (exact integer limb sums) and touches each slot's
 // total and pending count once.
+
 __global__ void __launch_bounds__(kBlock) wave_score(const __grid_constant__ TransportParams P,
                                                      const __grid_constant__ WaveArgs A)
 {
@@ -405,7 +484,9 @@ __global__ void __launch_bounds__(kBlock) wave_score(const __grid_constant__ Tra
     const WaveQueue& in = ctl->q[A.cur];
     const uint32_t n_s = ctl->n_score;
     const Block B = block_stats(P, acc);
-    const GlobalQ qs{A.slots, ctl, A.cur ^ 1, -1};
+    Deferred def;
+    deferred_reset(def);
+    const GlobalQ qs{A.slots, ctl, A.cur ^ 1, -1, &def};
     const WaveRays& R = A.R;
     DevStatus* st = P.status;
     const int lane = threadIdx.x & 31;
@@ -413,9 +494,9 @@ __global__ void __launch_bounds__(kBlock) wave_score(const __grid_constant__ Tra
     for (uint32_t base = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32u; base < n_s;
          base += n_warps * 32u) {
         const uint32_t i = base + (uint32_t)lane;
-        const bool is_score = i < n_s;
         int s = -1;
         uint64_t l0 = 0, l1 = 0, l2 = 0;
+        const bool is_score = i < n_s && XS_GUARD(in.batch[i / (uint32_t)P.splitting].slot < A.n_slots, st, 13.0);
         if (is_score) {
             s = (int)in.batch[i / (uint32_t)P.splitting].slot;
             const uint32_t pix = R.pix[i];
@@ -458,6 +539,8 @@ __global__ void __launch_bounds__(kBlock) wave_score(const __grid_constant__ Tra
             if (atomicSub(&S.pending, cnt) == cnt)
                 finalize_history(P, B, qs, s, var_base_of(P, s), st);
         }
+        __syncwarp();
+        flush_deferred(ctl, A.cur ^ 1, def, A.n_slots, P.status);
     }
     flush_stats(P, B);
 }
@@ -473,7 +556,9 @@ __global__ void __launch_bounds__(kBlock) wave_event(const __grid_constant__ Tra
     const WaveQueue& in = ctl->q[A.cur];
     const uint32_t n = ctl->n_rays, n_s = ctl->n_score;
     const Block B = block_stats(P, acc);
-    const GlobalQ qs{A.slots, ctl, A.cur ^ 1, -1};
+    Deferred def;
+    deferred_reset(def);
+    const GlobalQ qs{A.slots, ctl, A.cur ^ 1, -1, &def};
     const WaveRays& R = A.R;
     uint32_t c_int = 0;
     const int lane = threadIdx.x & 31;
@@ -497,14 +582,20 @@ __global__ void __launch_bounds__(kBlock) wave_event(const __grid_constant__ Tra
         if ((uint32_t)lane < take)
             event_continue(P, B, qs, (int)sl, var_base_of(P, (int)sl), P.status);
         __syncwarp();
+        flush_deferred(ctl, A.cur ^ 1, def, A.n_slots, P.status);
     };
     auto select = [&](bool active, uint32_t i) { // selection phase for the lanes with `active`
         int kind = K_NONE, s = 0;
         if (active) {
             s = (int)in.free[i - n_s];
-            kind = event_select<FMT>(P, B, qs, s, true, R.res[i], R.res_vox[i], R.res_vox[R.cap + i],
-                                     R.res_vox[2ull * R.cap + i], var_base_of(P, s), P.status);
+            const int vx = R.res_vox[i], vy = R.res_vox[R.cap + i], vz = R.res_vox[2ull * R.cap + i];
+            if (XS_GUARD((uint32_t)s < A.n_slots && (uint32_t)vx < (uint32_t)P.G.nx && (uint32_t)vy < (uint32_t)P.G.ny &&
+                             (uint32_t)vz < (uint32_t)P.G.nz,
+                         P.status, 11.0))
+                kind = event_select<FMT>(P, B, qs, s, true, R.res[i], vx, vy, vz, var_base_of(P, s), P.status);
         }
+        __syncwarp();
+        flush_deferred(ctl, A.cur ^ 1, def, A.n_slots, P.status);
         const unsigned mc = __ballot_sync(kFull, kind == K_COMPTON);
         const unsigned mr = __ballot_sync(kFull, kind == K_RAYLEIGH);
         if (kind == K_COMPTON)
@@ -529,8 +620,11 @@ __global__ void __launch_bounds__(kBlock) wave_event(const __grid_constant__ Tra
         const bool hit = valid && R.res_hit[i] != 0;
         if (valid && !hit) {
             const int s = (int)in.free[i - n_s];
-            history_event<FMT>(P, B, qs, s, false, 0.0, 0, 0, 0, var_base_of(P, s), P.status);
+            if (XS_GUARD((uint32_t)s < A.n_slots, P.status, 12.0))
+                history_event<FMT>(P, B, qs, s, false, 0.0, 0, 0, 0, var_base_of(P, s), P.status);
         }
+        __syncwarp(); // reconverge before the warp-synchronous gather
+        flush_deferred(ctl, A.cur ^ 1, def, A.n_slots, P.status);
         const unsigned hm = __ballot_sync(kFull, hit);
         if (hit)
             hb[nb + __popc(hm & lt_mask)] = i;
@@ -597,10 +691,18 @@ __global__ void __launch_bounds__(kBlock) wave_admit(const __grid_constant__ Tra
     const int32_t top = ctl->free_top;
     const unsigned long long base = ctl->admit_base;
     const uint32_t qb = ctl->admit_q;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < k; i += gridDim.x * blockDim.x) {
-        const int s = (int)ctl->free_stack[top + i];
-        const GlobalQ qs{A.slots, ctl, A.cur, (int)(qb + i)};
-        history_start(P, B, qs, sstart, s, base + i, P.status);
+    Deferred def;
+    deferred_reset(def);
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t i0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); i0 < k; i0 += stride) {
+        const uint32_t i = i0 + (threadIdx.x & 31u);
+        if (i < k) {
+            const int s = (int)ctl->free_stack[top + i];
+            const GlobalQ qs{A.slots, ctl, A.cur, (int)(qb + i), &def};
+            history_start(P, B, qs, sstart, s, base + i, P.status);
+        }
+        __syncwarp();
+        flush_deferred(ctl, A.cur, def, A.n_slots, P.status);
     }
     flush_stats(P, B);
 }
@@ -731,6 +833,88 @@ struct WaveEngine {
     cudaEvent_t fork = nullptr;
 };
 
+namespace {
+
+// ---------------------------------------------------------- walk probe
+// Does crossing uniform blocks pay on this phantom?  A block step costs about
+// 1.7x a voxel step, so on speckled grids (segmented reconstructions: few
+// uniform blocks along the rays) the plain voxel walk is faster.  At upload,
+// a fixed set of rays (start points in non-vacuum voxels, isotropic
+// directions, a counter hash of the ray index: deterministic per phantom) is
+// walked to the grid exit in both modes, counting loop iterations.
+__device__ __forceinline__ uint32_t probe_hash(uint32_t x)
+{
+    x ^= x >> 16;
+    x *= 0x7FEB352Du;
+    x ^= x >> 15;
+    x *= 0x846CA68Bu;
+    x ^= x >> 16;
+    return x;
+}
+__device__ __forceinline__ double probe_u(uint32_t i, uint32_t k)
+{
+    return (probe_hash(i * 0x9E3779B9u + k * 0x85EBCA6Bu + 0x1234567u) >> 8) * (1.0 / 16777216.0) + 0.5 / 16777216.0;
+}
+
+template <int FMT, bool SKIP>
+__global__ void __launch_bounds__(kBlock) walk_probe(const __grid_constant__ TransportParams P, int n_rays,
+                                                     unsigned long long* iters)
+{
+    const Grid& G = P.G;
+    MuTab<FMT, true> tab;
+    tab.t0 = tab.t1 = tab.t2 = tab.t3 = 1.0;
+    tab.T = nullptr;
+    tab.energy = 0.0;
+    unsigned long long n_it = 0;
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n_rays; r += gridDim.x * blockDim.x) {
+        V3 o = v3(0.0, 0.0, 0.0);
+        for (int k = 0; k < 8; ++k) { // a point in matter (last try kept)
+            o = v3(G.ox + probe_u(r, 3 * k) * (G.ux - G.ox), G.oy + probe_u(r, 3 * k + 1) * (G.uy - G.oy),
+                   G.oz + probe_u(r, 3 * k + 2) * (G.uz - G.oz));
+            int code;
+            float dens = 0.f;
+            fetch<FMT>(G, voxel_of(o.x, G.ox, G.ihx, G.nx), voxel_of(o.y, G.oy, G.ihy, G.ny),
+                       voxel_of(o.z, G.oz, G.ihz, G.nz), code, dens);
+            if (P.pal_mat[(code & ~G.ubit) & (kMaxPalette - 1)] != 0)
+                break;
+        }
+        const double cz = 2.0 * probe_u(r, 40) - 1.0, ph = 6.283185307179586 * probe_u(r, 41);
+        const double sz = sqrt(fmax(0.0, 1.0 - cz * cz));
+        const V3 d = v3(sz * cos(ph), sz * sin(ph), cz);
+        Walk w;
+        w.march = 0;
+        if (!walk_begin<FMT, SKIP>(P, w, o, d, CUDART_INF, false, nullptr, 0))
+            continue;
+        bool walking = true;
+        while (walking) {
+            walking = walk_step<FMT, true, SKIP>(P, tab, w);
+            ++n_it;
+        }
+    }
+    n_it = __reduce_add_sync(kFull, (unsigned)n_it);
+    if ((threadIdx.x & 31) == 0)
+        atomicAdd(iters, n_it);
+}
+
+} // namespace
+
+// iters[0]: voxel-walk iterations, iters[1]: block-walk iterations (device, zeroed here)
+cudaError_t launch_walk_probe(const TransportParams& P, unsigned long long* iters, cudaStream_t s)
+{
+    cudaError_t e = cudaMemsetAsync(iters, 0, 2 * sizeof(unsigned long long), s);
+    if (e != cudaSuccess)
+        return e;
+    const int n = 8192, grid = (n + kBlock - 1) / kBlock;
+    if (P.G.fmt == kFmtP4) {
+        walk_probe<kFmtP4, false><<<grid, kBlock, 0, s>>>(P, n, iters);
+        walk_probe<kFmtP4, true><<<grid, kBlock, 0, s>>>(P, n, iters + 1);
+    } else {
+        walk_probe<kFmtP8, false><<<grid, kBlock, 0, s>>>(P, n, iters);
+        walk_probe<kFmtP8, true><<<grid, kBlock, 0, s>>>(P, n, iters + 1);
+    }
+    return cudaGetLastError();
+}
+
 WaveEngine* wave_create() { return new WaveEngine(); }
 
 void wave_destroy(WaveEngine* e)
@@ -747,12 +931,24 @@ void wave_destroy(WaveEngine* e)
 
 size_t wave_slot_bytes() { return sizeof(Slot); }
 
+#ifdef XSW_DEBUG_SYNC
+#define XSW_CHECK(x)                                                                               \
+    do {                                                                                           \
+        cudaError_t err_ = (x);                                                                    \
+        if (err_ != cudaSuccess) {                                                                 \
+            std::fprintf(stderr, "XSW_CHECK failed at wavefront.cu:%d: %s\n", __LINE__,           \
+                         cudaGetErrorString(err_));                                                \
+            return err_;                                                                           \
+        }                                                                                          \
+    } while (0)
+#else
 #define XSW_CHECK(x)                                                                               \
     do {                                                                                           \
         cudaError_t err_ = (x);                                                                    \
         if (err_ != cudaSuccess)                                                                   \
             return err_;                                                                           \
     } while (0)
+#endif
 
 static cudaError_t pipe_prepare(WavePipe& w, const TransportParams& P, uint32_t n_slots, int n_mu)
 {
@@ -910,15 +1106,87 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
                     w.ev.push_back(v);
                 }
                 A.cur = w.cur;
+#ifdef XSW_DEBUG_SYNC
+                auto dbg_wait = [&](const char* what) {
+                    const cudaError_t err = cudaStreamSynchronize(ps);
+                    if (err != cudaSuccess) {
+                        std::fprintf(stderr, "FAULT in %s, pipe %d wave %u: %s\n", what, p, w.waves, cudaGetErrorString(err));
+                        std::fflush(stderr);
+                        _exit(3);
+                    }
+                };
+#else
+                auto dbg_wait = [](const char*) {};
+#endif
+#ifdef XSW_DEBUG_POISON
+                if (w.waves == 0 && w.P.track_var)
+                    XSW_CHECK(cudaMemsetAsync(w.P.var_pix, 0x7F, (size_t)A.n_slots * w.P.var_cap * 4, ps));
+                // poison the per-ray results: a ray the walk does not finish reads as a hit
+                // at a voxel far outside the grid
+                XSW_CHECK(cudaMemsetAsync(A.R.res_hit, 1, A.R.cap, ps));
+                XSW_CHECK(cudaMemsetAsync(A.R.res_vox, 0x7F, 3ull * A.R.cap * sizeof(int), ps));
+#endif
                 K.setup<<<g_setup, kBlock, mu_smem, ps>>>(w.P, A);
+                dbg_wait("setup");
                 XSW_CHECK(cudaEventRecord(w.ev[2 * w.waves], ps));
                 K.walk<<<g_walk, kBlock, mu_smem, ps>>>(w.P, A);
+                dbg_wait("walk");
+#ifdef XSW_DEBUG_POISON
+                {
+                    WaveCtl hc;
+                    XSW_CHECK(cudaMemcpy(&hc, w.ctl, sizeof hc, cudaMemcpyDeviceToHost));
+                    const uint32_t nn = hc.n_rays, ns = hc.n_score;
+                    std::vector<uint8_t> hit(nn), fl(nn);
+                    std::vector<int> vx(nn);
+                    XSW_CHECK(cudaMemcpy(hit.data(), A.R.res_hit, nn, cudaMemcpyDeviceToHost));
+                    XSW_CHECK(cudaMemcpy(fl.data(), A.R.flags, nn, cudaMemcpyDeviceToHost));
+                    XSW_CHECK(cudaMemcpy(vx.data(), A.R.res_vox, nn * 4, cudaMemcpyDeviceToHost));
+                    int bad = 0;
+                    for (uint32_t i = ns; i < nn; ++i)
+                        if (hit[i] && (uint32_t)vx[i] >= (uint32_t)P.G.nx) {
+                            if (bad < 5)
+                                std::fprintf(stderr, "wave %u ray %u (n_s %u n %u): hit %d flags %d vox %d\n", w.waves, i, ns,
+                                             nn, hit[i], fl[i], vx[i]);
+                            ++bad;
+                        }
+                    if (bad)
+                        std::fprintf(stderr, "wave %u: %d unwritten hit rays of %u free\n", w.waves, bad, nn - ns);
+                }
+#endif
                 XSW_CHECK(cudaEventRecord(w.ev[2 * w.waves + 1], ps));
                 wave_score<<<g_score, kBlock, stat_smem, ps>>>(w.P, A);
+                dbg_wait("score");
+#ifdef XSW_DEBUG_POISON
+                if (w.P.track_var) {
+                    std::vector<Slot> hs(A.n_slots);
+                    XSW_CHECK(cudaMemcpy(hs.data(), A.slots, hs.size() * sizeof(Slot), cudaMemcpyDeviceToHost));
+                    const size_t cap = (size_t)w.P.var_cap;
+                    std::vector<uint32_t> vp(hs.size() * cap);
+                    XSW_CHECK(cudaMemcpy(vp.data(), w.P.var_pix, vp.size() * 4, cudaMemcpyDeviceToHost));
+                    int bad = 0;
+                    for (size_t q = 0; q < hs.size(); ++q) {
+                        const Slot& S = hs[q];
+                        if (S.pending <= 0)
+                            continue;
+                        const int nv = S.n_var < (int)cap ? S.n_var : (int)cap;
+                        for (int a = 0; a < nv; ++a)
+                            if (vp[q * cap + a] >= (uint32_t)(w.P.nu * w.P.nv)) {
+                                if (bad < 5)
+                                    std::fprintf(stderr, "wave %u slot %zu: n_var %d entry %d pix %u pending %d gen %d\n",
+                                                 w.waves, q, S.n_var, a, vp[q * cap + a], S.pending, S.gen);
+                                ++bad;
+                                break;
+                            }
+                    }
+                    std::fprintf(stderr, "wave %u after score: %d slots with bad var entries\n", w.waves, bad);
+                }
+#endif
                 K.event<<<g_work, kBlock, stat_smem, ps>>>(w.P, A);
+                dbg_wait("event");
                 A.cur = w.cur ^ 1;
                 wave_plan<<<1, 1, 0, ps>>>(w.P, A);
                 wave_admit<<<g_admit, kBlock, admit_smem, ps>>>(w.P, A);
+                dbg_wait("admit");
                 w.cur ^= 1;
                 ++w.waves;
                 launches += 6;
@@ -942,9 +1210,29 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
             // is past the end) and no history in flight
             w.done = h.live == 0 && h.next_h >= P.h_end && h.q[w.cur].n_batch == 0 && h.q[w.cur].n_free == 0;
             all_done = all_done && w.done;
+#ifdef XSW_DEBUG_STUCK
+            if (w.waves % 512 == 0)
+                std::fprintf(stderr, "pipe %d wave %u live %u next_h %llu/%llu batch %u free %u rays %u\n", p, w.waves,
+                             h.live, (unsigned long long)h.next_h, (unsigned long long)P.h_end, h.q[w.cur].n_batch,
+                             h.q[w.cur].n_free, h.n_rays);
+#endif
         }
         if (hs.code != 0 || all_done)
             break;
+        // every wave advances each live history by one free path: a history
+        // needs at most max_interactions + 1 of them, so the run cannot need
+        // more waves than this unless the pipeline state is corrupt
+        uint32_t max_w = 0;
+        for (int p = 0; p < n_pipes; ++p)
+            max_w = std::max(max_w, e->pipe[p].waves);
+        const uint64_t bound = 4ull * ((n_hist + n_slots - 1) / n_slots + 1) * (uint64_t)(P.max_inter + 2) + 64;
+        if (max_w > bound) {
+            DevStatus bad{};
+            bad.code = XS_E_RUNTIME;
+            bad.what = kErrStuck;
+            XSW_CHECK(cudaMemcpyAsync(P.status, &bad, sizeof bad, cudaMemcpyHostToDevice, e->pipe[0].stream));
+            break;
+        }
     }
     uint32_t waves = 0;
     float walk = 0.f;

@@ -66,6 +66,7 @@ enum ErrWhat : int32_t {
     kErrComptonS = 7,
     kErrRayleighF = 8,
     kErrTheta = 9,
+    kErrStuck = 10,
 };
 
 struct TransportParams {

@@ -27,16 +27,16 @@ pytestmark = pytest.mark.gpu
 
 @pytest.fixture(params=["exact-wave", "macro-wave", "exact-mega", "macro-mega"])
 def walk_mode(request):
-    """exact: voxel-by-voxel Siddon (strict REF replay); macro: uniform 8^3
-    cells / 4^3 bricks crossed in one step (the default; fp64-rounding-level
-    change).  wave: the wavefront engine (default); mega: the persistent
+    """exact: voxel-by-voxel Siddon (strict REF replay); macro: uniform
+    blocks crossed in one step (fp64-rounding-level change; the default
+    walk_mode 2 picks one of the two per phantom).  wave: the wavefront engine (default); mega: the persistent
     megakernel."""
     mode, engine = request.param.split("-")
     ctx = X.projector.default_context(0)
     ctx.set_option("exact_walk", 1 if mode == "exact" else 0)
     ctx.set_option("engine", 1 if engine == "wave" else 0)
     yield request.param
-    ctx.set_option("exact_walk", 0)
+    ctx.set_option("walk_mode", 2)
     ctx.set_option("engine", 1)
 
 

@@ -153,3 +153,25 @@ def test_segment_to_scene_matches_host_chain(orc):
     assert dev[1] > 0 and np.array_equal(dev[0], host[0]) and dev[1] == host[1]
     ctx.close()
     ctx2.close()
+
+
+def test_walk_mode_is_chosen_per_phantom():
+    """walk_mode 2 (default): the upload probe keeps the block walk on a
+    blocky phantom and the voxel walk on a speckled one; each choice gives the
+    same image as forcing that mode."""
+    ph, g, angle, spec, resp, cfg = poly()
+    rng = np.random.default_rng(9)
+    speckled = I.VoxelPhantom(ph.dims, ph.voxel_size, ph.origin, ph.material_id.copy(), ph.density.copy(),
+                              ph.materials)
+    flip = (rng.uniform(size=ph.material_id.size) < 0.3) & (ph.material_id > 0)
+    speckled.material_id[flip] = 2
+    speckled.density[flip] = 7.874
+    for phantom, want in ((ph, 1), (speckled, 0)):
+        ctx = X.Context(0)
+        ctx.upload(phantom, resp)
+        auto = _scatter(ctx, g, angle, spec, cfg)
+        assert ctx.launch_stats()["block_walk"] == want
+        ctx.set_option("walk_mode", want)
+        forced = _scatter(ctx, g, angle, spec, cfg)
+        assert np.array_equal(auto[0], forced[0])
+        ctx.close()
