@@ -476,4 +476,163 @@ inline xscat::Volume fbp_reconstruct(const xscat::ProjectionStack& stack, const 
     return vol;
 }
 
+// ------------------------------------------------------------ segmentation
+namespace detail {
+inline std::vector<xs_class_spec> class_specs(const std::vector<xscat::ClassSpec>& m)
+{
+    std::vector<xs_class_spec> out;
+    for (const auto& c : m)
+        out.push_back(xs_class_spec{c.material_id, c.density});
+    return out;
+}
+
+// REF material list (without vacuum) -> xs_material array with vacuum at 0
+struct MaterialList {
+    std::vector<xscat::Material> keep;
+    std::vector<xs_material> xs;
+    explicit MaterialList(const std::vector<xscat::Material>& mats)
+    {
+        keep.push_back(xscat::vacuum_material());
+        for (const auto& m : mats)
+            if (m.name != "vacuum")
+                keep.push_back(m);
+        xs.resize(keep.size());
+        for (std::size_t i = 0; i < keep.size(); ++i) {
+            const xscat::Material& m = keep[i];
+            xs_material& x = xs[i];
+            x.name = m.name.c_str();
+            x.z_eff = m.z_eff;
+            x.density_ref = m.density_ref;
+            if (!m.has_tables()) {
+                x.mu = x.sigma_incoh = x.sigma_coh = x.sigma_pe = x.s_factor = x.f_factor =
+                    xs_table{0, nullptr, nullptr};
+                continue;
+            }
+            x.mu = table_view(m.mu);
+            x.sigma_incoh = table_view(m.sigma_incoh);
+            x.sigma_coh = table_view(m.sigma_coh);
+            x.sigma_pe = table_view(m.sigma_pe);
+            x.s_factor = table_view(m.s_factor);
+            x.f_factor = table_view(m.f_factor);
+        }
+    }
+};
+} // namespace detail
+
+// REF recon.hpp otsu_thresholds (recon.cpp:159-240) on the device
+inline std::vector<double> otsu_thresholds(const xscat::Volume& vol, int n_classes, int histogram_bins = 1024)
+{
+    Context& c = thread_context();
+    const int32_t dims[3] = {vol.dims[0], vol.dims[1], vol.dims[2]};
+    double thr[4] = {0, 0, 0, 0};
+    throw_status(xs_otsu_thresholds(c.get(), vol.values.data(), dims, n_classes, histogram_bins, thr, 0), c.get());
+    return std::vector<double>(thr, thr + std::max(0, n_classes - 1));
+}
+
+// REF recon.hpp segment_volume (recon.cpp:242-262)
+inline xscat::SegmentationResult segment_volume(const xscat::Volume& vol, const std::vector<double>& thresholds,
+                                                std::vector<xscat::ClassSpec> class_map)
+{
+    Context& c = thread_context();
+    xscat::SegmentationResult seg;
+    seg.labels.resize(vol.voxel_count());
+    throw_status(xs_segment_volume(c.get(), vol.values.data(), vol.voxel_count(), thresholds.data(),
+                                   static_cast<int32_t>(thresholds.size()), static_cast<int32_t>(class_map.size()),
+                                   seg.labels.data(), 0),
+                 c.get());
+    seg.thresholds = thresholds;
+    seg.class_map = std::move(class_map);
+    return seg;
+}
+
+// REF recon.hpp to_density_phantom (recon.cpp:264-322)
+inline xscat::VoxelPhantom to_density_phantom(const xscat::Volume& vol, const xscat::SegmentationResult& seg,
+                                              const std::array<int, 3>& target_dims,
+                                              std::vector<xscat::Material> materials)
+{
+    if (seg.labels.size() != vol.voxel_count())
+        throw std::runtime_error("to_density_phantom: segmentation size mismatch");
+    const xscat::Vec3 vs{vol.voxel_size.x * vol.dims[0] / target_dims[0],
+                         vol.voxel_size.y * vol.dims[1] / target_dims[1],
+                         vol.voxel_size.z * vol.dims[2] / target_dims[2]};
+    xscat::VoxelPhantom ph = xscat::make_empty_phantom(target_dims[0], target_dims[1], target_dims[2], vs,
+                                                       std::move(materials));
+    detail::MaterialList ml(std::vector<xscat::Material>(ph.materials.begin() + 1, ph.materials.end()));
+    const auto cls = detail::class_specs(seg.class_map);
+    const int32_t src[3] = {vol.dims[0], vol.dims[1], vol.dims[2]};
+    const int32_t tgt[3] = {target_dims[0], target_dims[1], target_dims[2]};
+    Context& c = thread_context();
+    throw_status(xs_to_density_phantom(c.get(), seg.labels.data(), src, cls.data(), static_cast<int32_t>(cls.size()),
+                                       tgt, static_cast<int32_t>(ml.xs.size()), ml.xs.data(), ph.material_id.data(),
+                                       ph.density.data(), 0),
+                 c.get());
+    return ph;
+}
+
+// REF correction.hpp run_iterative_correction (correction.cpp:137-266), every
+// stage on the device; `workers` is ignored.  seconds_postprocess holds the
+// fused post-processing + correction pass (seconds_correction is 0).
+inline xscat::CorrectionResult run_iterative_correction(const xscat::ProjectionStack& raw_intensity,
+                                                        const xscat::DetectorImage& flatfield,
+                                                        const xscat::ScanGeometry& g, const xscat::Spectrum& spec,
+                                                        const xscat::DetectorResponse& resp,
+                                                        const xscat::CorrectionConfig& cfg,
+                                                        const std::vector<xscat::Material>& materials)
+{
+    if (raw_intensity.n_angles() != g.n_angles())
+        throw std::runtime_error("run_iterative_correction: stack angle count mismatch");
+    Context& c = thread_context();
+    const xs_response r{table_view(resp.dqe), table_view(resp.deposit)};
+    throw_status(xs_upload_response(c.get(), &r), c.get());
+    Packed p;
+    pack_call(p, g, spec, cfg.sim);
+    detail::MaterialList ml(materials);
+    const auto cls = detail::class_specs(cfg.class_map);
+    xs_correction_config cc;
+    xs_correction_config_default(&cc);
+    cc.n_iterations = cfg.n_iterations;
+    cc.simulate_every_kth_angle = cfg.simulate_every_kth_angle;
+    cc.mc_nu = cfg.mc_nu;
+    cc.mc_nv = cfg.mc_nv;
+    for (int a = 0; a < 3; ++a)
+        cc.recon_dims[a] = cfg.recon_dims[a];
+    cc.n_classes = cfg.n_classes;
+    cc.class_map = cls.empty() ? nullptr : cls.data();
+    cc.sim = p.c;
+    cc.sg_window = cfg.sg.window;
+    cc.sg_polyorder = cfg.sg.polyorder;
+    cc.sg_auto_window = cfg.sg_auto_window ? 1 : 0;
+    if (static_cast<int>(cfg.class_map.size()) != cfg.n_classes && cfg.n_classes >= 2 && cfg.n_classes <= 4)
+        throw std::runtime_error("correction config: class_map must have n_classes entries");
+    const std::vector<double> raw = detail::flatten(raw_intensity);
+    xscat::CorrectionResult out;
+    out.corrected_volume = xscat::make_volume(cfg.recon_dims[0], cfg.recon_dims[1], cfg.recon_dims[2],
+                                              xscat::default_voxel_size(g, cfg.recon_dims));
+    std::vector<double> stack(raw.size());
+    std::vector<xs_iteration_report> reps(std::max(1, cfg.n_iterations));
+    throw_status(xs_run_iterative_correction(c.get(), raw.data(), flatfield.values.data(), &p.g, &p.s, &cc,
+                                             static_cast<int32_t>(ml.xs.size()), ml.xs.data(),
+                                             out.corrected_volume.values.data(), stack.data(), reps.data(), 0),
+                 c.get());
+    out.corrected_stack = detail::unflatten(stack, raw_intensity.nu, raw_intensity.nv, raw_intensity.angle_values);
+    for (int i = 0; i < cfg.n_iterations; ++i) {
+        const xs_iteration_report& x = reps[i];
+        xscat::IterationReport rep;
+        rep.iteration = x.iteration;
+        rep.seconds_fbp = x.seconds_fbp;
+        rep.seconds_segmentation = x.seconds_segmentation;
+        rep.seconds_mc_scatter = x.seconds_mc_scatter;
+        rep.seconds_mc_primary = x.seconds_mc_primary;
+        rep.seconds_postprocess = x.seconds_postprocess;
+        rep.seconds_correction = x.seconds_correction;
+        rep.seconds_total = x.seconds_total;
+        rep.mc_seconds_per_projection = x.mc_seconds_per_projection;
+        rep.mean_scatter_fraction = x.mean_scatter_fraction;
+        rep.ncc_to_previous = x.ncc_to_previous;
+        rep.negative_scatter_clamped = x.negative_scatter_clamped;
+        out.reports.push_back(rep);
+    }
+    return out;
+}
+
 } // namespace xscat_b200

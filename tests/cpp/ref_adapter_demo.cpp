@@ -8,6 +8,7 @@
 #include <filesystem>
 #include <string>
 
+#include "xscat/rng.hpp"
 #include "xscat/synthetic.hpp"
 #include "xscat_b200_ref_adapter.hpp"
 
@@ -174,6 +175,60 @@ int main(int argc, char** argv)
         const Volume a = xscat::fbp_reconstruct(st, g, dims, vx);
         const Volume b = xscat_b200::fbp_reconstruct(st, g, dims, xscat_b200::default_voxel_size(g, dims));
         check(a.values == b.values, "fbp_reconstruct bitwise", "");
+    }
+    { // segmentation (recon.cpp:159-322): REF vs the device, bit for bit
+        Volume vol = make_volume(20, 21, 22, {0.1, 0.1, 0.1});
+        CounterRng rng(29);
+        for (auto& v : vol.values) {
+            const double pick = rng.uniform();
+            v = static_cast<float>(pick < 0.3 ? 10.0 + 3.0 * rng.uniform()
+                                  : pick < 0.7 ? 25.0 + 4.0 * rng.uniform() : 45.0 + 5.0 * rng.uniform());
+        }
+        const auto ta = xscat::otsu_thresholds(vol, 3, 1024);
+        const auto tb = xscat_b200::otsu_thresholds(vol, 3, 1024);
+        check(ta == tb, "otsu_thresholds bitwise", "");
+        const std::vector<ClassSpec> cmap{{0, 0.0}, {1, 1.0}, {2, 2.699}};
+        const auto sa = xscat::segment_volume(vol, ta, cmap);
+        const auto sb = xscat_b200::segment_volume(vol, tb, cmap);
+        check(sa.labels == sb.labels, "segment_volume bitwise", "");
+        const VoxelPhantom pa = xscat::to_density_phantom(vol, sa, {10, 7, 11}, {w, al});
+        const VoxelPhantom pb = xscat_b200::to_density_phantom(vol, sb, {10, 7, 11}, {w, al});
+        check(pa.material_id == pb.material_id && pa.density == pb.density && pa.voxel_size.x == pb.voxel_size.x &&
+                  pa.origin.z == pb.origin.z,
+              "to_density_phantom bitwise", "");
+    }
+    { // the whole loop (correction.cpp:137-266): REF's scatter-free fixed-point case
+        const VoxelPhantom ph = make_cylinder_phantom(24, 0.3, 2.2, 5.0, w, 1.0);
+        const ScanGeometry g = make_circular_geometry(60.0, 40.0, 24, 24, 0.5, 36);
+        const Spectrum spec = monochromatic_spectrum(100.0);
+        SimConfig sim;
+        sim.photons_total = 2000;
+        sim.splitting = 4;
+        sim.seed = 99;
+        std::vector<int> all(g.n_angles());
+        for (int i = 0; i < g.n_angles(); ++i)
+            all[i] = i;
+        const ScanResult primary = xscat::run_scan(ph, g, spec, resp, sim, all, ScanQuantity::primary, 2);
+        VoxelPhantom empty = make_empty_phantom(24, 24, 24, ph.voxel_size, ph.materials);
+        const DetectorImage flat = xscat::simulate_primary(empty, g, 0, spec, resp, sim);
+        CorrectionConfig cfg;
+        cfg.n_iterations = 1;
+        cfg.mc_nu = cfg.mc_nv = 12;
+        cfg.recon_dims = {24, 24, 24};
+        cfg.n_classes = 2;
+        cfg.class_map = {ClassSpec{0, 0.0}, ClassSpec{1, 1.0}};
+        cfg.sim = sim;
+        const CorrectionResult a = xscat::run_iterative_correction(primary.primary, flat, g, spec, resp, cfg, {w});
+        const CorrectionResult b = xscat_b200::run_iterative_correction(primary.primary, flat, g, spec, resp, cfg, {w});
+        double md = 0.0, peak = 0.0;
+        for (std::size_t i = 0; i < a.corrected_volume.values.size(); ++i) {
+            md = std::max(md, (double)std::abs(a.corrected_volume.values[i] - b.corrected_volume.values[i]));
+            peak = std::max(peak, (double)std::abs(a.corrected_volume.values[i]));
+        }
+        std::snprintf(buf, sizeof buf, "(ncc %.9f / %.9f, max |dvol| %.2g of %.3g)", a.reports[0].ncc_to_previous,
+                      b.reports[0].ncc_to_previous, md, peak);
+        check(std::abs(a.reports[0].ncc_to_previous - b.reports[0].ncc_to_previous) < 1e-9 && md <= 1e-5 * peak,
+              "run_iterative_correction vs REF", buf);
     }
     std::printf("%s\n", g_fail ? "FAILED" : "all checks passed");
     return g_fail ? 1 : 0;
