@@ -178,6 +178,10 @@ struct MuTab {
 
     __device__ __noinline__ void fill(const TransportParams& P, double e, DevStatus* st, int bin)
     {
+        fill_impl(P, e, st, bin);
+    }
+    __device__ __forceinline__ void fill_impl(const TransportParams& P, double e, DevStatus* st, int bin)
+    {
         energy = e;
         if (FMT == kFmtP4 || REG) { // per palette entry (REG: <= 4 entries, either palette width)
             double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3_ = 0.0;
@@ -318,8 +322,8 @@ struct Walk {
 
 
 template <int FMT, bool FAST>
-__device__ __noinline__ bool walk_begin(const TransportParams& P, Walk& w, V3 o, V3 d,
-                                           double target, bool march, DevStatus* st, int bin)
+__device__ __forceinline__ bool walk_begin_impl(const TransportParams& P, Walk& w, V3 o, V3 d,
+                                                double target, bool march, DevStatus* st, int bin)
 {
     double t0, t1;
     bool bad;
@@ -365,6 +369,16 @@ __device__ __noinline__ bool walk_begin(const TransportParams& P, Walk& w, V3 o,
     w.rdy = fabs(d.y) * G.ihy;
     w.rdz = fabs(d.z) * G.ihz;
     return true;
+}
+
+// Out-of-line copy (the megakernel keeps its instruction footprint small);
+// the wavefront set-up kernel inlines walk_begin_impl so the walker state
+// stays in registers instead of a local-memory frame.
+template <int FMT, bool FAST>
+__device__ __noinline__ bool walk_begin(const TransportParams& P, Walk& w, V3 o, V3 d, double target, bool march,
+                                        DevStatus* st, int bin)
+{
+    return walk_begin_impl<FMT, FAST>(P, w, o, d, target, march, st, bin);
 }
 
 // Boundaries tn + j*dt (j = 0..k) with tn + j*dt <= tm: how many an axis
@@ -930,7 +944,7 @@ __device__ __noinline__ void history_start(const TransportParams& P, const Block
 
 // Scoring-ray set-up (REF run_history :166-183): geometry, p(theta), e_out,
 // response; returns the score prefactor (point_detector_score without exp(-tau)).
-__device__ __noinline__ double score_setup(const TransportParams& P, const Slot& S, uint32_t pix,
+__device__ __forceinline__ double score_setup(const TransportParams& P, const Slot& S, uint32_t pix,
                                               V3& o, V3& to_det, double& e_out, DevStatus* st)
 {
     const int iu = (int)(pix % (uint32_t)P.nu);

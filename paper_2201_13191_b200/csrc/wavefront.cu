@@ -309,14 +309,14 @@ __global__ void __launch_bounds__(kBlock) wave_setup(const __grid_constant__ Tra
             double e_out;
             R.pre[i] = score_setup(P, S, pix, o, to_det, e_out, st);
             if (tab.energy != e_out) // REF trace_attenuation builds MuField(e_out)
-                tab.fill(P, e_out, st, S.bin);
-            walking = walk_begin<FMT, SKIP>(P, w, o, to_det, CUDART_INF, false, st, S.bin);
+                tab.fill_impl(P, e_out, st, S.bin);
+            walking = walk_begin_impl<FMT, SKIP>(P, w, o, to_det, CUDART_INF, false, st, S.bin);
             ++c_rays;
         } else { // REF trace.cpp:189-230
             const Slot& S = A.slots[in.free[i - n_s]];
             if (tab.energy != S.E)
-                tab.fill(P, S.E, st, S.bin);
-            walking = walk_begin<FMT, SKIP>(P, w, v3(S.px, S.py, S.pz), v3(S.dx, S.dy, S.dz), S.target,
+                tab.fill_impl(P, S.E, st, S.bin);
+            walking = walk_begin_impl<FMT, SKIP>(P, w, v3(S.px, S.py, S.pz), v3(S.dx, S.dy, S.dz), S.target,
                                             false, st, S.bin);
         }
         if (!walking) { // misses the grid: zero depth, no interaction
