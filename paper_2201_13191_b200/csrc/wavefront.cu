@@ -247,10 +247,10 @@ template <int FMT, bool REG>
 __device__ __forceinline__ void store_mu(const WaveRays& R, uint32_t i, const MuTab<FMT, REG>& tab)
 {
     if (REG) {
-        R.mu[i] = tab.t0;
-        R.mu[R.cap + i] = tab.t1;
-        R.mu[2ull * R.cap + i] = tab.t2;
-        R.mu[3ull * R.cap + i] = tab.t3;
+        __stcs(&R.mu[i], tab.t0);
+        __stcs(&R.mu[R.cap + i], tab.t1);
+        __stcs(&R.mu[2ull * R.cap + i], tab.t2);
+        __stcs(&R.mu[3ull * R.cap + i], tab.t3);
     } else {
         for (int c = 0; c < R.n_mu; ++c)
             R.mu[(uint64_t)c * R.cap + i] = tab.T[c * kBlock];
@@ -261,10 +261,10 @@ template <int FMT, bool REG>
 __device__ __forceinline__ void load_mu(const WaveRays& R, uint32_t i, MuTab<FMT, REG>& tab)
 {
     if (REG) {
-        tab.t0 = R.mu[i];
-        tab.t1 = R.mu[R.cap + i];
-        tab.t2 = R.mu[2ull * R.cap + i];
-        tab.t3 = R.mu[3ull * R.cap + i];
+        tab.t0 = __ldcs(&R.mu[i]);
+        tab.t1 = __ldcs(&R.mu[R.cap + i]);
+        tab.t2 = __ldcs(&R.mu[2ull * R.cap + i]);
+        tab.t3 = __ldcs(&R.mu[3ull * R.cap + i]);
     } else {
         for (int c = 0; c < R.n_mu; ++c)
             tab.T[c * kBlock] = R.mu[(uint64_t)c * R.cap + i];
@@ -325,21 +325,21 @@ __global__ void __launch_bounds__(kBlock) wave_setup(const __grid_constant__ Tra
             R.res_hit[i] = 0;
             continue;
         }
-        R.t[i] = w.t;
-        R.texit[i] = w.texit;
-        R.target[i] = w.target;
-        R.tn[i] = w.tnx;
-        R.tn[R.cap + i] = w.tny;
-        R.tn[2ull * R.cap + i] = w.tnz;
-        R.dt[i] = w.dtx;
-        R.dt[R.cap + i] = w.dty;
-        R.dt[2ull * R.cap + i] = w.dtz;
-        R.rd[i] = (float)w.rdx;
-        R.rd[R.cap + i] = (float)w.rdy;
-        R.rd[2ull * R.cap + i] = (float)w.rdz;
-        R.vox[i] = w.ix;
-        R.vox[R.cap + i] = w.iy;
-        R.vox[2ull * R.cap + i] = w.iz;
+        __stcs(&R.t[i], w.t);
+        __stcs(&R.texit[i], w.texit);
+        __stcs(&R.target[i], w.target);
+        __stcs(&R.tn[i], w.tnx);
+        __stcs(&R.tn[R.cap + i], w.tny);
+        __stcs(&R.tn[2ull * R.cap + i], w.tnz);
+        __stcs(&R.dt[i], w.dtx);
+        __stcs(&R.dt[R.cap + i], w.dty);
+        __stcs(&R.dt[2ull * R.cap + i], w.dtz);
+        __stcs(&R.rd[i], (float)w.rdx);
+        __stcs(&R.rd[R.cap + i], (float)w.rdy);
+        __stcs(&R.rd[2ull * R.cap + i], (float)w.rdz);
+        __stcs(&R.vox[i], w.ix);
+        __stcs(&R.vox[R.cap + i], w.iy);
+        __stcs(&R.vox[2ull * R.cap + i], w.iz);
         R.flags[i] = (uint8_t)((w.sx + 1) | ((w.sy + 1) << 2) | ((w.sz + 1) << 4) | 64);
         store_mu(R, i, tab);
     }
@@ -382,21 +382,21 @@ __global__ void __launch_bounds__(kBlock, SKIP ? XSW_WALK_BLOCKS : XSW_WALK_BLOC
                     const uint8_t f = R.flags[r];
                     if (f & 64) {
                         ray = r;
-                        w.t = R.t[r];
-                        w.texit = R.texit[r];
-                        w.target = R.target[r];
-                        w.tnx = R.tn[r];
-                        w.tny = R.tn[R.cap + r];
-                        w.tnz = R.tn[2ull * R.cap + r];
-                        w.dtx = R.dt[r];
-                        w.dty = R.dt[R.cap + r];
-                        w.dtz = R.dt[2ull * R.cap + r];
-                        w.rdx = R.rd[r];
-                        w.rdy = R.rd[R.cap + r];
-                        w.rdz = R.rd[2ull * R.cap + r];
-                        w.ix = R.vox[r];
-                        w.iy = R.vox[R.cap + r];
-                        w.iz = R.vox[2ull * R.cap + r];
+                        w.t = __ldcs(&R.t[r]);
+                        w.texit = __ldcs(&R.texit[r]);
+                        w.target = __ldcs(&R.target[r]);
+                        w.tnx = __ldcs(&R.tn[r]);
+                        w.tny = __ldcs(&R.tn[R.cap + r]);
+                        w.tnz = __ldcs(&R.tn[2ull * R.cap + r]);
+                        w.dtx = __ldcs(&R.dt[r]);
+                        w.dty = __ldcs(&R.dt[R.cap + r]);
+                        w.dtz = __ldcs(&R.dt[2ull * R.cap + r]);
+                        w.rdx = __ldcs(&R.rd[r]);
+                        w.rdy = __ldcs(&R.rd[R.cap + r]);
+                        w.rdz = __ldcs(&R.rd[2ull * R.cap + r]);
+                        w.ix = __ldcs(&R.vox[r]);
+                        w.iy = __ldcs(&R.vox[R.cap + r]);
+                        w.iz = __ldcs(&R.vox[2ull * R.cap + r]);
                         w.sx = (int)(f & 3) - 1;
                         w.sy = (int)((f >> 2) & 3) - 1;
                         w.sz = (int)((f >> 4) & 3) - 1;
