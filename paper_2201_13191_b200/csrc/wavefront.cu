@@ -304,10 +304,10 @@ __global__ void __launch_bounds__(kBlock) wave_setup(const __grid_constant__ Tra
             const Slot& S = A.slots[sb.slot];
             const uint32_t pix = score_pixel(P, rng_uniform_at(sb.rng, 2 * k, P.k0, P.k1, P.angle),
                                              rng_uniform_at(sb.rng, 2 * k + 1, P.k0, P.k1, P.angle));
-            R.pix[i] = pix;
+            __stcs(&R.pix[i], pix);
             V3 o, to_det;
             double e_out;
-            R.pre[i] = score_setup(P, S, pix, o, to_det, e_out, st);
+            __stcs(&R.pre[i], score_setup(P, S, pix, o, to_det, e_out, st));
             if (tab.energy != e_out) // REF trace_attenuation builds MuField(e_out)
                 tab.fill_impl(P, e_out, st, S.bin);
             walking = walk_begin_impl<FMT, SKIP>(P, w, o, to_det, CUDART_INF, false, st, S.bin);
@@ -440,15 +440,15 @@ __global__ void __launch_bounds__(kBlock, SKIP ? XSW_WALK_BLOCKS : XSW_WALK_BLOC
 #endif
             if (!walking) {
                 if (ray < n_s) {
-                    R.res[ray] = w.depth;
+                    __stcs(&R.res[ray], w.depth);
                     c_sc += w.steps + w.skipped;
                 } else {
                     const bool hit = w.hit != 0;
-                    R.res[ray] = hit ? hit_t(w) : 0.0;
+                    __stcs(&R.res[ray], hit ? hit_t(w) : 0.0);
                     R.res_hit[ray] = hit ? 1 : 0;
-                    R.res_vox[ray] = w.ix;
-                    R.res_vox[R.cap + ray] = w.iy;
-                    R.res_vox[2ull * R.cap + ray] = w.iz;
+                    __stcs(&R.res_vox[ray], w.ix);
+                    __stcs(&R.res_vox[R.cap + ray], w.iy);
+                    __stcs(&R.res_vox[2ull * R.cap + ray], w.iz);
                     c_fp += w.steps + w.skipped;
                 }
                 c_iter += w.steps;
@@ -499,8 +499,8 @@ __global__ void __launch_bounds__(kBlock) wave_score(const __grid_constant__ Tra
         const bool is_score = i < n_s && XS_GUARD(in.batch[i / (uint32_t)P.splitting].slot < A.n_slots, st, 13.0);
         if (is_score) {
             s = (int)in.batch[i / (uint32_t)P.splitting].slot;
-            const uint32_t pix = R.pix[i];
-            const double x = R.pre[i] * nl_exp(-R.res[i]);
+            const uint32_t pix = __ldcs(&R.pix[i]);
+            const double x = __ldcs(&R.pre[i]) * nl_exp(-__ldcs(&R.res[i]));
             if (!isfinite(x)) {
                 raise(st, XS_E_RUNTIME, kErrNonFinite, A.slots[s].bin, A.slots[s].e_in, x);
             } else if (!quantize(ldexp(x, -P.log2_img), l0, l1, l2)) {
@@ -588,11 +588,12 @@ __global__ void __launch_bounds__(kBlock) wave_event(const __grid_constant__ Tra
         int kind = K_NONE, s = 0;
         if (active) {
             s = (int)in.free[i - n_s];
-            const int vx = R.res_vox[i], vy = R.res_vox[R.cap + i], vz = R.res_vox[2ull * R.cap + i];
+            const int vx = __ldcs(&R.res_vox[i]), vy = __ldcs(&R.res_vox[R.cap + i]),
+                      vz = __ldcs(&R.res_vox[2ull * R.cap + i]);
             if (XS_GUARD((uint32_t)s < A.n_slots && (uint32_t)vx < (uint32_t)P.G.nx && (uint32_t)vy < (uint32_t)P.G.ny &&
                              (uint32_t)vz < (uint32_t)P.G.nz,
                          P.status, 11.0))
-                kind = event_select<FMT>(P, B, qs, s, true, R.res[i], vx, vy, vz, var_base_of(P, s), P.status);
+                kind = event_select<FMT>(P, B, qs, s, true, __ldcs(&R.res[i]), vx, vy, vz, var_base_of(P, s), P.status);
         }
         __syncwarp();
         flush_deferred(ctl, A.cur ^ 1, def, A.n_slots, P.status);
