@@ -365,7 +365,7 @@ def gpu_arm(args):
                          "walk_ms": walk_ms_max, "transport_ms": kernel_ms_max,
                          "note": "5 B per REF voxel visit (u8 id + f32 density) / walk-kernel "
                                  "time; traffic = ncu DRAM bytes of the same walk launches. The "
-                                 "device grid is a 4-bit palette (0.5 B/voxel) with uniform "
+                                 "device grid is an 8-bit palette (1 B/voxel) with uniform "
                                  "blocks crossed without loads, so the walk is issue-bound"},
             "cpu_baseline": cpu,
             "clocks": clocks,
