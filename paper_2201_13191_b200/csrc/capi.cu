@@ -1211,6 +1211,29 @@ static void upload_phantom_impl(xs_context* c, const xs_phantom* ph, bool on_dev
             c->probe_iters[0] = it[0];
             c->probe_iters[1] = it[1];
         }
+        const bool block_walk = c->macro_skip == 1 || (c->macro_skip == 2 && c->skip_pays);
+        if (!block_walk && fmt == xsd::kFmtP8 && n_pairs <= 16) {
+            // The voxel walk never reads level bits: re-encode as 4-bit codes.
+            // Half the bytes keeps the grid L2-resident for the random voxel
+            // reads of speckled phantoms (same palette indices: same results).
+            G.fmt = xsd::kFmtP4;
+            G.ubit = 0;
+            G.lvl_shift = 4;
+            G.lvl_log2 = 0;
+            const size_t vb4 = n_bricks * 32;
+            if (on_device) {
+                cuda_check(xsd::launch_phantom_encode(ph->material_id, ph->density, c->seg_pal.p, n_pairs, G,
+                                                      xsd::kFmtP4, c->vox.p, nullptr, c->sm_count, c->stream),
+                           "encode phantom");
+            } else {
+                encode_phantom(*ph, xsd::kFmtP4, scan.pairs, c->pin_vox.p, c->pin_dens.p, G.nbx, G.nby, G.nbz);
+                cuda_check(cudaMemcpyAsync(c->vox.p, c->pin_vox.p, vb4, cudaMemcpyHostToDevice, c->stream),
+                           "upload voxels");
+                c->last_upload_bytes += vb4;
+            }
+            cuda_check(cudaStreamSynchronize(c->stream), "upload phantom");
+            c->grid = G;
+        }
         c->n_mats = ph->n_materials;
         c->mats.assign(ph->n_materials, HMat{});
         for (int m = 0; m < ph->n_materials; ++m) {
