@@ -1207,7 +1207,7 @@ static void upload_phantom_impl(xs_context* c, const xs_phantom* ph, bool on_dev
             unsigned long long it[2];
             cuda_check(cudaMemcpyAsync(it, c->probe.p, sizeof it, cudaMemcpyDeviceToHost, c->stream), "D2H");
             cuda_check(cudaStreamSynchronize(c->stream), "walk probe");
-            c->skip_pays = (double)it[1] < 0.6 * (double)it[0]; // a block step costs ~1.7 voxel steps
+            c->skip_pays = (double)it[1] < 0.5 * (double)it[0]; // a block step costs ~2 (4-bit) voxel steps
             c->probe_iters[0] = it[0];
             c->probe_iters[1] = it[1];
         }
