@@ -422,22 +422,8 @@ __global__ void __launch_bounds__(kBlock, SKIP ? XSW_WALK_BLOCKS : XSW_WALK_BLOC
         }
         ++c_wit;
         if (walking) {
-#ifdef XSW_DEBUG_STUCK
-            const double t_prev = w.t, tnx0 = w.tnx, tny0 = w.tny, tnz0 = w.tnz;
-            const int ix0 = w.ix, iy0 = w.iy, iz0 = w.iz;
-            const uint32_t raw0 = w.raw;
-#endif
             walking = walk_step<FMT, REG, SKIP>(P, tab, w);
             ++w.steps;
-#ifdef XSW_DEBUG_STUCK
-            if (walking && w.steps > 100000u) {
-                printf("STUCK ray %u t %.17g->%.17g tn %.17g %.17g %.17g -> %.17g %.17g %.17g dt %.17g %.17g %.17g "
-                       "rd %.9g %.9g %.9g vox %d %d %d -> %d %d %d s %d %d %d raw %u texit %.17g\n",
-                       ray, t_prev, w.t, tnx0, tny0, tnz0, w.tnx, w.tny, w.tnz, w.dtx, w.dty, w.dtz, w.rdx, w.rdy,
-                       w.rdz, ix0, iy0, iz0, w.ix, w.iy, w.iz, w.sx, w.sy, w.sz, raw0, w.texit);
-                walking = false;
-            }
-#endif
             if (!walking) {
                 if (ray < n_s) {
                     __stcs(&R.res[ray], w.depth);
@@ -1107,7 +1093,7 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
                     w.ev.push_back(v);
                 }
                 A.cur = w.cur;
-#ifdef XSW_DEBUG_SYNC
+#ifdef XSW_DEBUG_SYNC // debugging aid: name the kernel that faults (host-side only)
                 auto dbg_wait = [&](const char* what) {
                     const cudaError_t err = cudaStreamSynchronize(ps);
                     if (err != cudaSuccess) {
@@ -1119,69 +1105,14 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
 #else
                 auto dbg_wait = [](const char*) {};
 #endif
-#ifdef XSW_DEBUG_POISON
-                if (w.waves == 0 && w.P.track_var)
-                    XSW_CHECK(cudaMemsetAsync(w.P.var_pix, 0x7F, (size_t)A.n_slots * w.P.var_cap * 4, ps));
-                // poison the per-ray results: a ray the walk does not finish reads as a hit
-                // at a voxel far outside the grid
-                XSW_CHECK(cudaMemsetAsync(A.R.res_hit, 1, A.R.cap, ps));
-                XSW_CHECK(cudaMemsetAsync(A.R.res_vox, 0x7F, 3ull * A.R.cap * sizeof(int), ps));
-#endif
                 K.setup<<<g_setup, kBlock, mu_smem, ps>>>(w.P, A);
                 dbg_wait("setup");
                 XSW_CHECK(cudaEventRecord(w.ev[2 * w.waves], ps));
                 K.walk<<<g_walk, kBlock, mu_smem, ps>>>(w.P, A);
                 dbg_wait("walk");
-#ifdef XSW_DEBUG_POISON
-                {
-                    WaveCtl hc;
-                    XSW_CHECK(cudaMemcpy(&hc, w.ctl, sizeof hc, cudaMemcpyDeviceToHost));
-                    const uint32_t nn = hc.n_rays, ns = hc.n_score;
-                    std::vector<uint8_t> hit(nn), fl(nn);
-                    std::vector<int> vx(nn);
-                    XSW_CHECK(cudaMemcpy(hit.data(), A.R.res_hit, nn, cudaMemcpyDeviceToHost));
-                    XSW_CHECK(cudaMemcpy(fl.data(), A.R.flags, nn, cudaMemcpyDeviceToHost));
-                    XSW_CHECK(cudaMemcpy(vx.data(), A.R.res_vox, nn * 4, cudaMemcpyDeviceToHost));
-                    int bad = 0;
-                    for (uint32_t i = ns; i < nn; ++i)
-                        if (hit[i] && (uint32_t)vx[i] >= (uint32_t)P.G.nx) {
-                            if (bad < 5)
-                                std::fprintf(stderr, "wave %u ray %u (n_s %u n %u): hit %d flags %d vox %d\n", w.waves, i, ns,
-                                             nn, hit[i], fl[i], vx[i]);
-                            ++bad;
-                        }
-                    if (bad)
-                        std::fprintf(stderr, "wave %u: %d unwritten hit rays of %u free\n", w.waves, bad, nn - ns);
-                }
-#endif
                 XSW_CHECK(cudaEventRecord(w.ev[2 * w.waves + 1], ps));
                 wave_score<<<g_score, kBlock, stat_smem, ps>>>(w.P, A);
                 dbg_wait("score");
-#ifdef XSW_DEBUG_POISON
-                if (w.P.track_var) {
-                    std::vector<Slot> hs(A.n_slots);
-                    XSW_CHECK(cudaMemcpy(hs.data(), A.slots, hs.size() * sizeof(Slot), cudaMemcpyDeviceToHost));
-                    const size_t cap = (size_t)w.P.var_cap;
-                    std::vector<uint32_t> vp(hs.size() * cap);
-                    XSW_CHECK(cudaMemcpy(vp.data(), w.P.var_pix, vp.size() * 4, cudaMemcpyDeviceToHost));
-                    int bad = 0;
-                    for (size_t q = 0; q < hs.size(); ++q) {
-                        const Slot& S = hs[q];
-                        if (S.pending <= 0)
-                            continue;
-                        const int nv = S.n_var < (int)cap ? S.n_var : (int)cap;
-                        for (int a = 0; a < nv; ++a)
-                            if (vp[q * cap + a] >= (uint32_t)(w.P.nu * w.P.nv)) {
-                                if (bad < 5)
-                                    std::fprintf(stderr, "wave %u slot %zu: n_var %d entry %d pix %u pending %d gen %d\n",
-                                                 w.waves, q, S.n_var, a, vp[q * cap + a], S.pending, S.gen);
-                                ++bad;
-                                break;
-                            }
-                    }
-                    std::fprintf(stderr, "wave %u after score: %d slots with bad var entries\n", w.waves, bad);
-                }
-#endif
                 K.event<<<g_work, kBlock, stat_smem, ps>>>(w.P, A);
                 dbg_wait("event");
                 A.cur = w.cur ^ 1;
@@ -1211,12 +1142,6 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
             // is past the end) and no history in flight
             w.done = h.live == 0 && h.next_h >= P.h_end && h.q[w.cur].n_batch == 0 && h.q[w.cur].n_free == 0;
             all_done = all_done && w.done;
-#ifdef XSW_DEBUG_STUCK
-            if (w.waves % 512 == 0)
-                std::fprintf(stderr, "pipe %d wave %u live %u next_h %llu/%llu batch %u free %u rays %u\n", p, w.waves,
-                             h.live, (unsigned long long)h.next_h, (unsigned long long)P.h_end, h.q[w.cur].n_batch,
-                             h.q[w.cur].n_free, h.n_rays);
-#endif
         }
         if (hs.code != 0 || all_done)
             break;
