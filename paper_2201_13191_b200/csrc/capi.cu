@@ -675,7 +675,8 @@ void accumulate(xs_context* c, const xs_geometry& g, int angle, const xs_spectru
             P.var_cap = (int32_t)cap;
             // scratch per live history: keep it near 1 GB
             n_slots = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(n_slots, (1ull << 30) / (12 * cap)));
-            const uint64_t n_use = std::min<uint64_t>(n_slots, h1 - h0);
+            // wave_run gives each of its pipelines ceil(n / pipes) slots, side by side
+            const uint64_t n_use = std::min<uint64_t>(n_slots, h1 - h0) + (uint64_t)c->wave_pipes;
             c->var_pix.reserve(n_use * cap);
             c->var_val.reserve(n_use * cap);
             P.var_pix = c->var_pix.p;
