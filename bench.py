@@ -320,7 +320,8 @@ def gpu_arm(args):
                "d2h_bytes_per_step": int(img_h.nbytes) if rank == 0 else 0,
                "steps": n_e2e,
                "note": "per step: xs_upload_phantom of the host u8 id + f32 density grid "
-                       "(validate, palette-encode, H2D), transport, reduce, finalize, image D2H"}
+                       "(pinned staging, H2D, device validation + palette encode), transport, "
+                       "reduce, finalize, image D2H"}
 
     if rank == 0:
         hbm, kind = peaks()

@@ -99,6 +99,7 @@ def test_device_upload_matches_host_upload(kind):
         ph.density = ph.density * (1.0 + 1e-3 * (np.arange(ph.density.size) % 300)).astype(np.float32)
         ph.density[ph.material_id == 0] = 0.0
     ctx = X.Context(0)
+    ctx.set_option("upload_path", 0)  # the host encoder
     ctx.upload(ph, resp)
     a = _scatter(ctx, g, angle, spec, cfg)
     host_fmt = ctx.launch_stats()["voxel_format"]
@@ -149,6 +150,7 @@ def test_segment_to_scene_matches_host_chain(orc):
     ph = I.VoxelPhantom((nx, ny, nz), vs, tuple(-n * v * 0.5 for n, v in zip((nx, ny, nz), vs)), ids, dens,
                         [None] + mats)
     ctx2 = X.Context(0)
+    ctx2.set_option("upload_path", 0)
     ctx2.upload(ph, resp)
     host = _scatter(ctx2, g, angle, spec, cfg)
     assert dev[1] > 0 and np.array_equal(dev[0], host[0]) and dev[1] == host[1]
@@ -176,3 +178,25 @@ def test_walk_mode_is_chosen_per_phantom():
         forced = _scatter(ctx, g, angle, spec, cfg)
         assert np.array_equal(auto[0], forced[0])
         ctx.close()
+
+
+@pytest.mark.parametrize("kind", ["palette", "raw"])
+def test_staged_upload_matches_host_encoder(kind):
+    """xs_upload_phantom's default path (pinned staging + device encode) gives
+    the host encoder's grid: identical scatter images; same validation errors."""
+    ph, g, angle, spec, resp, cfg = poly()
+    if kind == "raw":
+        ph.density = ph.density * (1.0 + 1e-3 * (np.arange(ph.density.size) % 300)).astype(np.float32)
+        ph.density[ph.material_id == 0] = 0.0
+    out = []
+    for path in (0, 1):
+        ctx = X.Context(0)
+        ctx.set_option("upload_path", path)
+        ctx.upload(ph, resp)
+        out.append(_scatter(ctx, g, angle, spec, cfg))
+        bad = rods(16)
+        bad.density[100], bad.material_id[100] = 0.5, 0
+        with pytest.raises(I.XscatError, match="vacuum voxel with nonzero density"):
+            ctx.upload(bad, resp)
+        ctx.close()
+    assert np.array_equal(out[0][0], out[1][0]) and out[0][1] == out[1][1]
