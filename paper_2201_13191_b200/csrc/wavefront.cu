@@ -45,6 +45,12 @@ namespace xsd {
 
 namespace {
 
+#ifndef XSW_REFILL_EXACT
+#define XSW_REFILL_EXACT 4 // the voxel walk refills sooner (its steps are short): -3%
+#endif
+#ifndef XSW_EXACT_BLOCKS
+#define XSW_EXACT_BLOCKS (XSW_WALK_BLOCKS + 1)
+#endif
 constexpr int kRefill = 8; // idle lanes that trigger a warp's refill in the walk kernel
 
 #ifndef XSW_WALK_BLOCKS
@@ -351,7 +357,7 @@ __global__ void __launch_bounds__(kBlock) wave_setup(const __grid_constant__ Tra
 
 // -------------------------------------------------------------------- walk
 template <int FMT, bool REG, bool SKIP>
-__global__ void __launch_bounds__(kBlock, SKIP ? XSW_WALK_BLOCKS : XSW_WALK_BLOCKS + 1) wave_walk(const __grid_constant__ TransportParams P,
+__global__ void __launch_bounds__(kBlock, SKIP ? XSW_WALK_BLOCKS : XSW_EXACT_BLOCKS) wave_walk(const __grid_constant__ TransportParams P,
                                                     const __grid_constant__ WaveArgs A)
 {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -371,7 +377,7 @@ __global__ void __launch_bounds__(kBlock, SKIP ? XSW_WALK_BLOCKS : XSW_WALK_BLOC
     uint32_t c_fp = 0, c_sc = 0, c_iter = 0, c_wit = 0, c_uni = 0;
     for (;;) {
         const unsigned idle = __ballot_sync(kFull, !walking);
-        if (!drained && (idle == kFull || __popc(idle) >= kRefill)) {
+        if (!drained && (idle == kFull || __popc(idle) >= (SKIP ? kRefill : XSW_REFILL_EXACT))) {
             uint32_t base = 0;
             if (lane == 0)
                 base = atomicAdd(&ctl->cursor, (uint32_t)__popc(idle));
