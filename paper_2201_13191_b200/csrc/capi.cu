@@ -233,7 +233,6 @@ struct xs_context {
     int max_slots = 64;
     int macro_skip = 2;  // 0: voxel walk, 1: cross uniform blocks, 2: decided per phantom at upload
     bool skip_pays = true; // walk probe of the uploaded phantom (launch_walk_probe)
-    unsigned long long probe_iters[2] = {0, 0};
     DevBuf<unsigned long long> probe;
 
     xs_launch_stats last{};
@@ -1214,8 +1213,6 @@ static void upload_phantom_impl(xs_context* c, const xs_phantom* ph, bool on_dev
             cuda_check(cudaMemcpyAsync(it, c->probe.p, sizeof it, cudaMemcpyDeviceToHost, c->stream), "D2H");
             cuda_check(cudaStreamSynchronize(c->stream), "walk probe");
             c->skip_pays = (double)it[1] < 0.5 * (double)it[0]; // a block step costs ~2 (4-bit) voxel steps
-            c->probe_iters[0] = it[0];
-            c->probe_iters[1] = it[1];
         }
         const bool block_walk = c->macro_skip == 1 || (c->macro_skip == 2 && c->skip_pays);
         if (!block_walk && fmt == xsd::kFmtP8 && n_pairs <= 16) {
