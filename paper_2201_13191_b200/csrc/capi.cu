@@ -242,7 +242,7 @@ struct xs_context {
     int lvl_edge1 = 8;                      // ... with one level bit
     std::vector<int> lvl_edges3{2, 4, 8, 16, 32, 64, 128}; // ... with three (8-bit palette; edge 2 = 2^3 sub-blocks of mixed bricks)
     bool compact_palette = false;           // 4-bit palette for <= 8 pairs (half the bytes, fewer level bits)
-    uint32_t wave_slots = 1u << 20;  // live histories of the wavefront engine
+    uint32_t wave_slots = 1u << 22;  // live histories of the wavefront engine (2^20 -> 2^22: +6% on C3)
     int wave_pipes = 2;              // concurrent wavefront pipelines (streams)
     xsd::WaveEngine* wave = nullptr;
 };
