@@ -51,7 +51,10 @@ namespace {
 #ifndef XSW_EXACT_BLOCKS
 #define XSW_EXACT_BLOCKS (XSW_WALK_BLOCKS + 1)
 #endif
-constexpr int kRefill = 8; // idle lanes that trigger a warp's refill in the walk kernel
+#ifndef XSW_REFILL
+#define XSW_REFILL 8
+#endif
+constexpr int kRefill = XSW_REFILL; // idle lanes that trigger a warp's refill in the walk kernel
 
 #ifndef XSW_WALK_BLOCKS
 #define XSW_WALK_BLOCKS 6 // resident walk blocks per SM (<= 80 registers; 7-8 spill or slow the macro walk;
