@@ -349,12 +349,18 @@ int xs_ctx_synchronize(xs_context* ctx);
  *                 kernels over global queues); 0: persistent megakernel.
  *                 Both give bit-identical results.  step_voxels > 1
  *                 (REF's march mode) always runs the megakernel
- *   "wave_slots"  histories in flight in the wavefront engine (2^20)
+ *   "wave_slots"  histories in flight in the wavefront engine (2^22)
  *   "wave_pipes"  concurrent wavefront pipelines on their own streams (2)
  *   "compact_palette" 1: 4-bit voxel palette for <= 8 (material, density)
  *                 pairs (half the bytes); 0 (default): 8-bit palette, which
  *                 leaves room for more uniform-block levels.  Applies to the
- *                 next xs_upload_phantom                                     */
+ *                 next xs_upload_phantom
+ *   "walk_mode"   0: voxel-by-voxel walk; 1: cross uniform blocks in one step;
+ *                 2 (default): chosen per phantom at upload by a ray probe
+ *                 (voxel-walk phantoms of <= 16 pairs are stored as 4-bit codes)
+ *   "upload_path" 1 (default): xs_upload_phantom stages the host arrays
+ *                 through pinned memory and validates / encodes on the device;
+ *                 0: validates / encodes on the host.  Same grid either way  */
 int xs_ctx_set_option(xs_context* ctx, const char* key, int64_t value);
 
 /* Scene upload: REF passes the phantom and response by const& to every
