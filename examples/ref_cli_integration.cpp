@@ -1,10 +1,13 @@
-// xscat_b200_cli.cpp — the reference CLI's compute commands on the B200
-// (SURVEY.md §8(f) rank 4): REF's own run configuration, input loaders and
-// file formats (run_config.cpp, phantom.cpp XVOX1, detector_image.cpp XPRJ1,
-// volume.cpp XVOL1) are linked as a library; every computation goes through
-// xscat_b200_ref_adapter.hpp.  Outputs have REF's names and shapes
-// (tools/main.cpp:83-130 simulate, :132-150 reconstruct, :152-180 correct):
-// primary.xprj / scatter.xprj / timing.csv, corrected.xvol / reports.
+// ref_cli_integration.cpp — INTEGRATION EXAMPLE, not part of the product.
+//
+// Shows how the reference's own CLI (REF tools/main.cpp:83-180) is pointed at
+// the B200 projector: REF's run configuration, input loaders and file formats
+// (run_config.cpp, phantom.cpp XVOX1, detector_image.cpp XPRJ1, volume.cpp
+// XVOL1) are REF's compiled objects, linked as a library; only the compute
+// calls are re-qualified to xscat_b200:: (include/xscat_b200_ref_adapter.hpp).
+// The command bodies therefore follow REF's cmd_simulate / cmd_reconstruct /
+// cmd_correct closely by design.  No native file-format or INI handling is
+// claimed here (SURVEY.md §8(f) rank 4 is NOT done).
 //
 //   xscat_b200_cli <config.ini> simulate [--what primary|scatter|both] [--angles a:b | i,j,...]
 //   xscat_b200_cli <config.ini> reconstruct <stack.xprj> [--flat flat.xprj] <out.xvol> <dim>

@@ -604,6 +604,15 @@ inline xscat::CorrectionResult run_iterative_correction(const xscat::ProjectionS
     cc.sg_auto_window = cfg.sg_auto_window ? 1 : 0;
     if (static_cast<int>(cfg.class_map.size()) != cfg.n_classes && cfg.n_classes >= 2 && cfg.n_classes <= 4)
         throw std::runtime_error("correction config: class_map must have n_classes entries");
+    // the C call reads g.nu * g.nv * n_angles doubles of the stack and g.nu * g.nv
+    // of the flat field: check the caller's dims first, with REF's messages
+    // (REF recon.cpp:327-328; a stack that does not match the geometry fails
+    // REF's Eq. 8 stage, correction.cpp:60-63 inside the stage wrapper :20-29)
+    if (flatfield.nu != raw_intensity.nu || flatfield.nv != raw_intensity.nv ||
+        flatfield.values.size() != static_cast<size_t>(flatfield.nu) * static_cast<size_t>(flatfield.nv))
+        throw std::runtime_error("intensity_to_attenuation: flatfield dims mismatch");
+    if (raw_intensity.n_angles() == g.n_angles() && (raw_intensity.nu != g.nu || raw_intensity.nv != g.nv))
+        throw std::runtime_error("iteration 1, stage correction: correct_projections: stack dims mismatch");
     const std::vector<double> raw = detail::flatten(raw_intensity);
     xscat::CorrectionResult out;
     out.corrected_volume = xscat::make_volume(cfg.recon_dims[0], cfg.recon_dims[1], cfg.recon_dims[2],

@@ -1273,7 +1273,10 @@ static void upload_phantom_staged(xs_context* c, const xs_phantom* ph)
     const size_t chunk = (size_t)32 << 20; // voxels per chunk (160 MB of ids + densities)
     c->seg_ids.reserve(n);
     c->seg_dens.reserve(n);
-    c->pin_raw.reserve(2 * 5 * std::min(n, chunk));
+    // per half: the ids, padded to 16 bytes so the densities after them stay aligned
+    const size_t id_bytes = (std::min(n, chunk) + 15) & ~(size_t)15;
+    const size_t half = id_bytes + 4 * std::min(n, chunk);
+    c->pin_raw.reserve(2 * half);
     if (!c->copy_stream)
         cuda_check(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking), "stream");
     for (int b = 0; b < 2; ++b)
@@ -1284,8 +1287,8 @@ static void upload_phantom_staged(xs_context* c, const xs_phantom* ph)
     for (size_t v0 = 0; v0 < n; v0 += chunk, ++k) {
         const size_t nv = std::min(chunk, n - v0);
         const int b = k & 1;
-        uint8_t* ids = c->pin_raw.p + (size_t)b * 5 * std::min(n, chunk);
-        float* dens = reinterpret_cast<float*>(ids + std::min(n, chunk));
+        uint8_t* ids = c->pin_raw.p + (size_t)b * half;
+        float* dens = reinterpret_cast<float*>(ids + id_bytes);
         cuda_check(cudaEventSynchronize(c->scan_done[b]), "staging"); // this half's previous DMA
         std::vector<std::thread> th;
         for (unsigned t = 0; t < nt; ++t)

@@ -807,6 +807,11 @@ struct WavePipe {
     uint32_t waves = 0;
     bool done = false;
 
+    size_t bytes_held() const
+    {
+        return n_slots_have * sizeof(Slot) + stack_have * 4 + (sq_have[0] + sq_have[1]) * sizeof(ScoreBatch) +
+               (fq_have[0] + fq_have[1]) * 4 + dbl_have * 8 + rd_have * 4 + vox_have * 4 + bytes_have;
+    }
     void release()
     {
         cudaFree(slots);
@@ -954,6 +959,15 @@ size_t wave_slot_bytes() { return sizeof(Slot); }
     } while (0)
 #endif
 
+// Device bytes of one pipeline with n_slots live histories (pipe_prepare).
+static double pipe_bytes(uint32_t n_slots, int splitting, int n_mu)
+{
+    const double cap = (double)n_slots * ((double)splitting + 1.0);
+    const double per_ray = (3 + 3 + 3 + n_mu + 2) * 8.0 + 3 * 4.0 + 7 * 4.0 + 2.0;
+    const double per_slot = (double)sizeof(Slot) + 4.0 + 2.0 * (sizeof(ScoreBatch) + 4.0);
+    return cap * per_ray + (double)n_slots * per_slot;
+}
+
 static cudaError_t pipe_prepare(WavePipe& w, const TransportParams& P, uint32_t n_slots, int n_mu)
 {
     const uint64_t split = (uint64_t)P.splitting;
@@ -1016,8 +1030,23 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
     n_pipes = n_pipes < 1 ? 1 : (n_pipes > 2 ? 2 : n_pipes);
     if (n_slots < 2)
         n_pipes = 1;
+    // per-lane mu table entries: palette codes (4-bit palette, up to 16) or
+    // materials (8-bit palette / raw ids, up to kMaxMaterials)
+    const int n_mu = use_reg_w(P) ? 4 : (P.G.fmt == kFmtP4 ? std::max(P.n_pal, 1) : kMaxMaterials);
+    { // live histories are bounded by device memory: the walker state grows
+      // with splitting (n_slots * (splitting + 1) ray entries), so a large
+      // splitting factor gets fewer slots instead of failing the run
+        size_t free_b = 0, total_b = 0;
+        if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+            size_t held = 0;
+            for (const WavePipe& w : e->pipe)
+                held += w.bytes_held();
+            const double budget = 0.7 * (double)(free_b + held);
+            while (n_slots > 4096 && (double)n_pipes * pipe_bytes((n_slots + n_pipes - 1) / n_pipes, P.splitting, n_mu) > budget)
+                n_slots >>= 1;
+        }
+    }
     const uint32_t per = (n_slots + n_pipes - 1) / n_pipes;
-    const int n_mu = use_reg_w(P) ? 4 : 8;
     for (int p = 0; p < n_pipes; ++p) {
         WavePipe& w = e->pipe[p];
         XSW_CHECK(pipe_prepare(w, P, per, n_mu));
@@ -1033,7 +1062,7 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
         XSW_CHECK(cudaEventCreateWithFlags(&e->fork, cudaEventDisableTiming));
 
     const WaveSet K = wave_kernels_for(P);
-    const size_t mu_smem = use_reg_w(P) ? 0 : (size_t)8 * kBlock * 8;
+    const size_t mu_smem = use_reg_w(P) ? 0 : (size_t)n_mu * kBlock * 8;
     const size_t stat_smem = (size_t)(8 * P.n_bins + 32) * 8;
     XSW_CHECK(cudaFuncSetAttribute((const void*)K.setup, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)std::max<size_t>(mu_smem, 1)));

@@ -577,11 +577,20 @@ def run_iterative_correction(raw_intensity: ProjectionStack, flatfield, g: I.Sca
                              ctx: Optional[Context] = None) -> CorrectionResult:
     """REF run_iterative_correction (correction.cpp:137-266) with every stage
     on the device; `materials` is REF's list (vacuum prepended here)."""
-    ctx = ctx or default_context()
     raw = np.ascontiguousarray(raw_intensity.images, dtype=np.float64)
+    cmap = list(cfg.class_map or [])
+    if 2 <= int(cfg.n_classes) <= 4 and len(cmap) != int(cfg.n_classes):
+        raise I.XscatError("correction config: class_map must have n_classes entries")
+    flat = np.ascontiguousarray(flatfield, dtype=np.float64)
+    # the C call reads g.nu * g.nv per image: check the caller's dims first, with
+    # REF's messages (recon.cpp:327-328; correction.cpp:60-63 inside stage())
+    if flat.shape[-2:] != raw.shape[-2:] or flat.size != raw.shape[-1] * raw.shape[-2]:
+        raise I.XscatError("intensity_to_attenuation: flatfield dims mismatch")
     if raw.shape[0] != g.n_angles:
         raise I.XscatError("run_iterative_correction: stack angle count mismatch")
-    flat = np.ascontiguousarray(flatfield, dtype=np.float64)
+    if raw.shape[1:] != (g.nv, g.nu):
+        raise I.XscatError("iteration 1, stage correction: correct_projections: stack dims mismatch")
+    ctx = ctx or default_context()
     mats = [None] + [m for m in materials if m is not None]
     pk = A.Packed()
     ctx.check(A.lib().xs_upload_response(ctx.h, C.byref(pk.response(resp))))

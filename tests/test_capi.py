@@ -126,3 +126,24 @@ def test_context_without_gpu_fails_loudly():
         pytest.skip("a GPU is present")
     with pytest.raises(X.XscatError):
         X.Context(0)
+
+
+def test_correction_loop_rejects_mismatched_dims_before_the_device():
+    """The C loop reads g.nu*g.nv per image: the Python mirror checks the
+    caller's stack / flat-field / class_map sizes first with REF's messages
+    (recon.cpp:327-328, correction.cpp:40-42, :60-63, :133-134)."""
+    g = I.make_circular_geometry(60.0, 40.0, 8, 6, 0.5, 4)
+    spec, resp = I.monochromatic_spectrum(60.0), I.detector_response()
+    ok = X.CorrectionConfig(n_classes=2, class_map=[X.ClassSpec(0, 0.0), X.ClassSpec(1, 1.0)])
+    good = X.ProjectionStack(list(g.angles), np.ones((4, 6, 8)))
+    with pytest.raises(X.XscatError, match="flatfield dims mismatch"):
+        X.run_iterative_correction(good, np.ones((6, 7)), g, spec, resp, ok, [I.material("water")])
+    with pytest.raises(X.XscatError, match="stack angle count mismatch"):
+        X.run_iterative_correction(X.ProjectionStack(list(g.angles[:3]), np.ones((3, 6, 8))), np.ones((6, 8)),
+                                   g, spec, resp, ok, [I.material("water")])
+    with pytest.raises(X.XscatError, match="stack dims mismatch"):
+        X.run_iterative_correction(X.ProjectionStack(list(g.angles), np.ones((4, 5, 8))), np.ones((5, 8)),
+                                   g, spec, resp, ok, [I.material("water")])
+    short = X.CorrectionConfig(n_classes=3, class_map=[X.ClassSpec(0, 0.0)])
+    with pytest.raises(X.XscatError, match="class_map must have n_classes entries"):
+        X.run_iterative_correction(good, np.ones((6, 8)), g, spec, resp, short, [I.material("water")])

@@ -1,5 +1,5 @@
-"""The reference CLI's compute commands on the B200 (tools/cpp/xscat_b200_cli.cpp,
-SURVEY.md §8(f) rank 4): REF's INI run configuration, input loaders and file
+"""Integration example (examples/ref_cli_integration.cpp; not a product
+component, SURVEY.md §8(f) rank 4 is not claimed): the reference CLI's compute commands on the B200: REF's INI run configuration, input loaders and file
 formats (XVOX1 phantom in, XPRJ1 stacks / XVOL1 volume / timing.csv out), with
 every computation through the adapter.  The stacks it writes must equal the
 Python API's results for the same inputs, rounded to float32 like REF's

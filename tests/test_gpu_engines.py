@@ -31,6 +31,13 @@ def _phantom(kind):
         ph.density[(ph.material_id == 1) & (np.arange(ph.density.size) % 11 == 0)] = 0.95
         ph.density[(ph.material_id == 2) & (np.arange(ph.density.size) % 5 == 0)] = 7.5
         return ph
+    if kind == "p4wide":  # 9..16 pairs: 4-bit codes on the voxel walk, mu table in shared memory
+        ph = S.make_rods_phantom(32, 10.0 / 32, 4.5, 8.0, water, 1.0, 4, 0.6, 3.0, iron, 7.874)
+        idx = np.arange(ph.density.size)
+        for k, d in enumerate((1.05, 0.95, 1.1, 0.9, 1.15, 0.85, 1.2, 0.8, 1.25, 0.75)):
+            ph.density[(ph.material_id == 1) & (idx % (13 + k) == 0)] = d
+        ph.density[(ph.material_id == 2) & (idx % 5 == 0)] = 7.5
+        return ph
     rng = np.random.default_rng(5)
     ph = S.make_rods_phantom(32, 10.0 / 32, 4.5, 8.0, water, 1.0, 4, 0.6, 3.0, iron, 7.874)
     body = ph.material_id == 1
@@ -97,3 +104,27 @@ def test_wavefront_slot_count_does_not_change_results(pipes):
         assert np.array_equal(ref.variance, r.variance), slots
         assert ref.total == r.total and ref.ledger == r.ledger, slots
         assert slots <= r.stats["live_histories"] <= slots + 1
+
+
+def test_wide_four_bit_palette_on_the_voxel_walk(orc):
+    """9..16 (material, density) pairs on the voxel walk are stored as 4-bit
+    codes; the wavefront engine's per-lane mu table must hold all 16 entries
+    (it was sized for 8).  Both engines, bitwise, and the oracle."""
+    ph = _phantom("p4wide")
+    n_pairs = len({(int(i), float(d)) for i, d in zip(ph.material_id, ph.density)})
+    assert 9 <= n_pairs <= 16, n_pairs
+    g = I.make_circular_geometry(100.0, 60.0, 32, 24, 0.8, 4)
+    spec, resp = I.kramers_spectrum(150.0), I.detector_response()
+    cfg = I.SimConfig(photons_total=20000, splitting=5, seed=4242, track_variance=True)
+    ctx = X.projector.Context(0)
+    ctx.set_option("walk_mode", 0)
+    proj = X.Projector(ph, resp, ctx=ctx)
+    out = {}
+    for engine in (0, 1):
+        ctx.set_option("engine", engine)
+        out[engine] = proj.scatter_stats(g, 1, spec, cfg)
+    assert _format_of(out[1].stats) == "p4" and out[1].stats["palette_size"] == n_pairs
+    assert np.array_equal(out[0].image, out[1].image)
+    assert np.array_equal(out[0].variance, out[1].variance)
+    assert out[0].ledger == out[1].ledger
+    _replay_compare(out[1], orc.simulate_scatter_stats(ph, g, 1, spec, resp, cfg))
