@@ -99,15 +99,31 @@ def test_primary_beer_lambert_criterion3():
     assert worst < 1e-6, worst
 
 
-def _replay_compare(gpu, cpu, frac_tol=1e-3):
+def tally_quantum(g, spec):
+    """Resolution of the device's fixed-point image tallies: 2^-64 U_img,
+    U_img = 2^floor(log2(sum_b w_b / sdd^2)) (include/xscat_gpu.h
+    xs_accum_units_make); each score rounds to it (limb0 round-half-even)."""
+    import math
+    return math.ldexp(1.0, math.frexp(float(np.sum(spec.weight)) / g.sdd ** 2)[1] - 1 - 64)
+
+
+def _replay_compare(gpu, cpu, frac_tol=1e-3, quantum=0.0):
+    """Same-seed replay: per pixel |gpu - cpu| <= 1e-9 |cpu| + atol, where
+    atol = 1024 tally quanta (2^-64 U_img, ~5e-17 of the flat field per
+    pixel; pass `quantum` = tally_quantum(g, spec)).  Scores far below the
+    quantum (rays through centimetres of iron, exp(-tau) < 1e-20) cannot be
+    represented by the fixed-point tally, so such pixels are compared in
+    absolute terms.  At most frac_tol of the pixels may exceed the bound (a
+    last-ulp libm difference can flip a branch of one history)."""
     a, b = gpu.image, cpu["image"]
     assert gpu.histories == cpu["histories"]
     assert abs(gpu.total - cpu["total"]) <= 1e-11 * abs(cpu["total"]) + 1e-300 or \
         abs(gpu.total - cpu["total"]) <= 1e-6 * abs(cpu["total"])
+    atol = 1024.0 * quantum
     nz = b > 0
-    rel = np.abs(a[nz] - b[nz]) / b[nz]
-    assert np.mean(rel > 1e-9) <= frac_tol, (np.mean(rel > 1e-9), rel.max())
-    assert np.all(a[~nz] == 0.0)
+    bad = np.abs(a[nz] - b[nz]) > 1e-9 * b[nz] + atol
+    assert np.mean(bad) <= frac_tol, (np.mean(bad), (np.abs(a[nz] - b[nz]) / b[nz]).max())
+    assert np.all(np.abs(a[~nz]) <= atol)
     for k in ("initial", "escaped", "absorbed", "culled", "roulette_killed", "roulette_boost"):
         x, y = getattr(gpu.ledger, k), cpu["ledger"][k]
         assert abs(x - y) <= 1e-9 * max(abs(y), 1e-300) or abs(x - y) <= 1e-6 * abs(y), (k, x, y)
