@@ -12,7 +12,7 @@ NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -fmad=false -Xcompiler -fPIC -Xptxa
             -ccbin $(CXX_HOST) -Iinclude $(NVEXTRA)
 CXXFLAGS := -O2 -std=c++17 -fPIC -ffp-contract=off -Iinclude
 
-CU_SRCS  := $(SRC)/capi.cu $(SRC)/transport.cu $(SRC)/wavefront.cu $(SRC)/levels.cu $(SRC)/correct.cu $(SRC)/fbp.cu $(SRC)/segment.cu $(SRC)/primary.cu $(SRC)/postprocess.cu
+CU_SRCS  := $(SRC)/capi.cu $(SRC)/transport.cu $(SRC)/wavefront.cu $(SRC)/levels.cu $(SRC)/correct.cu $(SRC)/fbp.cu $(SRC)/segment.cu $(SRC)/primary.cu $(SRC)/postprocess.cu $(SRC)/multi.cu
 CU_OBJS  := $(patsubst $(SRC)/%.cu,$(OBJDIR)/%.o,$(CU_SRCS))
 CPP_OBJS := $(OBJDIR)/host_common.o
 HDRS     := $(wildcard $(SRC)/*.h $(SRC)/*.cuh) include/xscat_gpu.h
@@ -32,7 +32,7 @@ $(OBJDIR)/host_common.o: $(SRC)/host_common.cpp $(HDRS)
 
 $(LIBDIR)/libxscatgpu.so: $(CU_OBJS) $(CPP_OBJS)
 	@mkdir -p $(LIBDIR)
-	$(NVCC) $(ARCH) -shared -ccbin $(CXX_HOST) -o $@ $^ -lpthread
+	$(NVCC) $(ARCH) -shared -ccbin $(CXX_HOST) -o $@ $^ -lnccl -lpthread
 
 oracle:
 	$(MAKE) -C oracle

@@ -410,6 +410,12 @@ int xs_scatter_finalize_device(xs_context* ctx, const xs_geometry* g, const xs_s
 int xs_primary_device(xs_context* ctx, const xs_geometry* g, int32_t angle_idx,
                       const xs_spectrum* spec, const xs_sim_config* cfg, double* d_image);
 
+/* Replicates ctx src's uploaded scene (encoded voxel grid, materials,
+ * detector response) into ctx dst, device to device (NVLink peer copy when
+ * the devices differ), without re-validating or re-encoding.  Used to give
+ * every GPU of a group the phantom that was uploaded (or segmented) on one. */
+int xs_ctx_copy_scene(xs_context* dst, const xs_context* src);
+
 /* Counters of the last scatter launch. */
 int xs_last_launch_stats(const xs_context* ctx, xs_launch_stats* out);
 
@@ -571,6 +577,83 @@ int xs_run_iterative_correction(xs_context* ctx, const double* raw_intensity, co
                                 const xs_geometry* g, const xs_spectrum* spec, const xs_correction_config* cfg,
                                 int32_t n_materials, const xs_material* materials, float* corrected_volume,
                                 double* corrected_stack, xs_iteration_report* reports, int32_t device_ptrs);
+
+/* ------------------------------------------------------------- multi-GPU
+ * SURVEY.md §8(e).  A history is a pure function of (seed, angle, bin,
+ * photon) (REF rng.hpp:13-17, transport.cpp:122-123) and the tallies are
+ * integers, so one projection's history range is split into contiguous
+ * photon batches, one per GPU (REF's chunk rule transport.cpp:274-275 with one
+ * chunk per GPU), and the accumulators are summed: the image is bit-identical
+ * for any GPU count.  Scans are split into contiguous angle ranges (REF
+ * run_scan's angle loop transport.cpp:405-420).
+ *
+ * Multi-process (one process per GPU, e.g. torchrun): rank 0 calls
+ * xs_comm_unique_id and sends the id to every rank by any channel; every rank
+ * calls xs_ctx_comm_init on its context.  The context then owns an NCCL
+ * communicator: accumulators are combined with ncclReduce(ncclUint64, ncclSum)
+ * and scan images gathered with ncclSend/ncclRecv, on the context's stream.
+ * Every rank calls the *_mgpu functions with identical arguments; if any rank
+ * fails, all ranks fail (the failing rank with its own REF message). */
+typedef struct xs_comm_id {
+    char internal[128];
+} xs_comm_id;
+int xs_comm_unique_id(xs_comm_id* out);
+int xs_ctx_comm_init(xs_context* ctx, int32_t n_ranks, int32_t rank, const xs_comm_id* id);
+int xs_ctx_comm_size(const xs_context* ctx, int32_t* n_ranks, int32_t* rank);
+
+/* REF simulate_scatter_stats (transport.cpp:246-324) over the communicator:
+ * rank r runs histories [n r / N, n (r + 1) / N) of the bin-major order, the
+ * accumulators are reduced onto `root`, which finalizes into *out (image and
+ * variance as in xs_simulate_scatter_stats; out->image may be NULL) and, if
+ * d_image is not NULL, into that device buffer.  Other ranks get
+ * out->histories = their share and nothing else. */
+int xs_simulate_scatter_stats_mgpu(xs_context* ctx, const xs_geometry* g, int32_t angle_idx,
+                                   const xs_spectrum* spec, const xs_sim_config* cfg, int32_t root,
+                                   xs_scatter_result* out, double* d_image);
+
+/* REF run_scan (transport.cpp:379-422) over the communicator: rank r runs the
+ * contiguous share [n r / N, n (r + 1) / N) of angle_subset and writes those
+ * angles' images (and seconds) into its own outputs, laid out as for
+ * xs_run_scan (n_subset images, angle-major; NULL outputs are skipped).  With
+ * gather != 0 the root's outputs also receive every other rank's images. */
+int xs_run_scan_mgpu(xs_context* ctx, const xs_geometry* g, const xs_spectrum* spec, const xs_sim_config* cfg,
+                     const int32_t* angle_subset, int32_t n_subset, int32_t what, int32_t gather, int32_t root,
+                     double* primary_out, double* scatter_out, double* seconds_per_angle);
+
+/* One process, several GPUs: a group of contexts, one per listed device (a
+ * device may repeat; its contexts then share it).  Group calls run the members
+ * concurrently, one host thread each.  The photon batches of one projection
+ * are combined by the root's (member 0) finalize kernel, which reads every
+ * member's accumulator over NVLink peer memory and sums the limbs as it
+ * dequantizes (reduce + finalize in one pass).  The phantom is uploaded once
+ * and replicated device to device (xs_ctx_copy_scene). */
+typedef struct xs_group xs_group;
+int xs_group_create(const int32_t* devices, int32_t n_devices, xs_group** out);
+void xs_group_destroy(xs_group* grp);
+int32_t xs_group_size(const xs_group* grp);
+xs_context* xs_group_context(xs_group* grp, int32_t member); /* owned by the group */
+const char* xs_group_last_error(const xs_group* grp);
+int xs_group_set_option(xs_group* grp, const char* key, int64_t value);
+int xs_group_upload_phantom(xs_group* grp, const xs_phantom* ph);
+int xs_group_upload_response(xs_group* grp, const xs_response* resp);
+/* REF simulate_scatter_stats, photon batches over the members. */
+int xs_group_simulate_scatter_stats(xs_group* grp, const xs_geometry* g, int32_t angle_idx,
+                                    const xs_spectrum* spec, const xs_sim_config* cfg,
+                                    xs_scatter_result* out);
+/* REF run_scan, angle ranges over the members (outputs as xs_run_scan). */
+int xs_group_run_scan(xs_group* grp, const xs_geometry* g, const xs_spectrum* spec, const xs_sim_config* cfg,
+                      const int32_t* angle_subset, int32_t n_subset, int32_t what, double* primary_out,
+                      double* scatter_out, double* seconds_per_angle);
+/* REF run_iterative_correction (as xs_run_iterative_correction on member 0)
+ * with the loop's scatter and primary scans sharded by angle over the group:
+ * each iteration's segmented phantom is replicated to the members device to
+ * device, and their images return into member 0's stacks over NVLink. */
+int xs_group_run_iterative_correction(xs_group* grp, const double* raw_intensity, const double* flatfield,
+                                      const xs_geometry* g, const xs_spectrum* spec,
+                                      const xs_correction_config* cfg, int32_t n_materials,
+                                      const xs_material* materials, float* corrected_volume,
+                                      double* corrected_stack, xs_iteration_report* reports,
+                                      int32_t device_ptrs);
 
 #ifdef __cplusplus
 }

@@ -12,7 +12,7 @@ from .inputs import (DetectorResponse, Material, ScanGeometry, SimConfig, Spectr
                      XscatOutOfRange, detector_response, kramers_spectrum, load_detector_response,
                      load_material, load_spectrum, make_circular_geometry, make_empty_phantom,
                      material, monochromatic_spectrum, spectrum)
-from .projector import (BOTH, HANN, PRIMARY, RAMLAK, SCATTER, Context, ProjectionStack, Projector,  # noqa: F401
+from .projector import (BOTH, HANN, PRIMARY, RAMLAK, SCATTER, Context, Group, ProjectionStack, Projector,  # noqa: F401
                         ScanResult, SgFilterSpec, SimResult, WeightLedger, apportion_photons,
                         correct_projections, correction_tail, default_sg_spec, default_voxel_size,
                         device_count, fbp_reconstruct,

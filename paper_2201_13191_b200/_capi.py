@@ -212,6 +212,11 @@ class Packed:
                                      1 if c.track_variance else 0))
 
 
+class XsCommId(C.Structure):
+    """include/xscat_gpu.h xs_comm_id (an NCCL unique id, 128 bytes)."""
+    _fields_ = [("internal", C.c_char * 128)]
+
+
 # ------------------------------------------------------ accumulator layout
 def accum_layout(nu: int, nv: int, n_bins: int, track_variance: bool) -> dict:
     """include/xscat_gpu.h xs_accum_layout_make."""
@@ -306,6 +311,36 @@ SIGNATURES = {
     "xs_run_scan_device": (C.c_int, [_P, C.POINTER(XsGeometry), C.POINTER(XsSpectrum),
                                      C.POINTER(XsSimConfig), C.POINTER(C.c_int32), C.c_int32,
                                      C.c_int32, _P, _P, _P]),
+    "xs_ctx_copy_scene": (C.c_int, [_P, _P]),
+    "xs_comm_unique_id": (C.c_int, [C.POINTER(XsCommId)]),
+    "xs_ctx_comm_init": (C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(XsCommId)]),
+    "xs_ctx_comm_size": (C.c_int, [_P, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    "xs_simulate_scatter_stats_mgpu": (C.c_int, [_P, C.POINTER(XsGeometry), C.c_int32,
+                                                 C.POINTER(XsSpectrum), C.POINTER(XsSimConfig),
+                                                 C.c_int32, C.POINTER(XsScatterResult), _P]),
+    "xs_run_scan_mgpu": (C.c_int, [_P, C.POINTER(XsGeometry), C.POINTER(XsSpectrum),
+                                   C.POINTER(XsSimConfig), C.POINTER(C.c_int32), C.c_int32,
+                                   C.c_int32, C.c_int32, C.c_int32, c_double_p, c_double_p,
+                                   c_double_p]),
+    "xs_group_create": (C.c_int, [C.POINTER(C.c_int32), C.c_int32, C.POINTER(_P)]),
+    "xs_group_destroy": (None, [_P]),
+    "xs_group_size": (C.c_int32, [_P]),
+    "xs_group_context": (_P, [_P, C.c_int32]),
+    "xs_group_last_error": (C.c_char_p, [_P]),
+    "xs_group_set_option": (C.c_int, [_P, C.c_char_p, C.c_int64]),
+    "xs_group_upload_phantom": (C.c_int, [_P, C.POINTER(XsPhantom)]),
+    "xs_group_upload_response": (C.c_int, [_P, C.POINTER(XsResponse)]),
+    "xs_group_simulate_scatter_stats": (C.c_int, [_P, C.POINTER(XsGeometry), C.c_int32,
+                                                  C.POINTER(XsSpectrum), C.POINTER(XsSimConfig),
+                                                  C.POINTER(XsScatterResult)]),
+    "xs_group_run_scan": (C.c_int, [_P, C.POINTER(XsGeometry), C.POINTER(XsSpectrum),
+                                    C.POINTER(XsSimConfig), C.POINTER(C.c_int32), C.c_int32,
+                                    C.c_int32, c_double_p, c_double_p, c_double_p]),
+    "xs_group_run_iterative_correction": (C.c_int, [_P, _P, _P, C.POINTER(XsGeometry),
+                                                    C.POINTER(XsSpectrum),
+                                                    C.POINTER(XsCorrectionConfig), C.c_int32,
+                                                    C.POINTER(XsMaterial), _P, _P,
+                                                    C.POINTER(XsIterationReport), C.c_int32]),
     "xs_correction_config_default": (None, [C.POINTER(XsCorrectionConfig)]),
     "xs_run_iterative_correction": (C.c_int, [_P, _P, _P, C.POINTER(XsGeometry),
                                               C.POINTER(XsSpectrum),

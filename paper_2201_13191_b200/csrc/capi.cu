@@ -17,6 +17,7 @@
 #include <thread>
 #include <vector>
 
+#include "capi_internal.h"
 #include "host_common.h"
 #include "xs_types.h"
 
@@ -67,8 +68,8 @@ WaveEngine* wave_create();
 void wave_destroy(WaveEngine* e);
 cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint32_t n_slots, cudaStream_t s,
                      WaveInfo* info, cudaEvent_t start, int n_pipes);
-cudaError_t launch_finalize_image(const unsigned long long* acc, uint64_t off_image, uint64_t off_var,
-                                  uint64_t npix, int log2_img, double n_hist, int track_var,
+cudaError_t launch_finalize_image(const unsigned long long* const* srcs, int n_src, uint64_t off_image,
+                                  uint64_t off_var, uint64_t npix, int log2_img, double n_hist, int track_var,
                                   double* image, double* var, cudaStream_t s);
 cudaError_t launch_sg(const double* in, double* tmp, double* out, int nu, int nv, int n_images,
                       int half, const double* K, cudaStream_t s);
@@ -245,6 +246,12 @@ struct xs_context {
     uint32_t wave_slots = 1u << 22;  // live histories of the wavefront engine (2^20 -> 2^22: +6% on C3)
     int wave_pipes = 2;              // concurrent wavefront pipelines (streams)
     xsd::WaveEngine* wave = nullptr;
+
+    // multi-GPU (multi.cu): the NCCL communicator of xs_ctx_comm_init, and
+    // the scan delegate a group installs on its root so the correction
+    // loop's scans are sharded by angle over the group's devices
+    void* mgpu = nullptr;
+    xsi::ScanHook scan_hook;
 };
 
 namespace {
@@ -758,21 +765,28 @@ void accumulate(xs_context* c, const xs_geometry& g, int angle, const xs_spectru
     c->last.block_walk = P.skip && c->grid.ubit ? 1u : 0u;
 }
 
+// SimResult from n_src accumulators (their sum: one per GPU / context of a
+// photon-batch split; device pointers readable from c's device, i.e. local
+// or peer memory).  The statistics words are summed on the host, the image
+// words by the finalize kernel as it dequantizes (reduce and finalize fused).
 void finalize(xs_context* c, const xs_geometry& g, const xs_spectrum& spec, const xs_sim_config& cfg,
-              const unsigned long long* d_accum, uint64_t h0, uint64_t h1, xs_scatter_result* out,
-              double* d_image)
+              const unsigned long long* const* srcs, int n_src, uint64_t h0, uint64_t h1,
+              xs_scatter_result* out, double* d_image)
 {
     const Plan plan = make_plan(g, spec, cfg);
     if (h1 > plan.n_hist)
         h1 = plan.n_hist;
     const xs_accum_layout& L = plan.layout;
     cudaStream_t s = c->stream;
-    // statistics words (bins, ledger, diag) -> host
+    // statistics words (bins, ledger, diag) -> host, summed over the sources
     const size_t tail = L.words - L.off_bins;
-    std::vector<uint64_t> stats(tail);
-    cuda_check(cudaMemcpyAsync(stats.data(), d_accum + L.off_bins, tail * 8, cudaMemcpyDeviceToHost, s),
-               "D2H stats");
-    cuda_check(cudaStreamSynchronize(s), "D2H stats");
+    std::vector<uint64_t> stats(tail, 0), part(tail);
+    for (int k = 0; k < n_src; ++k) {
+        cuda_check(cudaMemcpyAsync(part.data(), srcs[k] + L.off_bins, tail * 8, cudaMemcpyDefault, s), "D2H stats");
+        cuda_check(cudaStreamSynchronize(s), "D2H stats");
+        for (size_t i = 0; i < tail; ++i)
+            stats[i] += part[i];
+    }
     xsh::finalize_stats(spec, plan.counts, h0, h1, stats.data(), stats.data() + (L.off_ledger - L.off_bins),
                         plan.units, out);
     const uint64_t* diag = stats.data() + (L.off_diag - L.off_bins);
@@ -795,7 +809,7 @@ void finalize(xs_context* c, const xs_geometry& g, const xs_spectrum& spec, cons
         c->var.reserve(L.n_pixels);
         var = c->var.p;
     }
-    cuda_check(xsd::launch_finalize_image(d_accum, L.off_image, L.off_variance, L.n_pixels,
+    cuda_check(xsd::launch_finalize_image(srcs, n_src, L.off_image, L.off_variance, L.n_pixels,
                                           plan.units.log2_img, static_cast<double>(out->histories),
                                           cfg.track_variance, img, var, s),
                "finalize launch");
@@ -805,6 +819,13 @@ void finalize(xs_context* c, const xs_geometry& g, const xs_spectrum& spec, cons
         cuda_check(cudaMemcpyAsync(out->variance, var, L.n_pixels * 8, cudaMemcpyDeviceToHost, s),
                    "D2H variance");
     cuda_check(cudaStreamSynchronize(s), "finalize");
+}
+
+void finalize(xs_context* c, const xs_geometry& g, const xs_spectrum& spec, const xs_sim_config& cfg,
+              const unsigned long long* d_accum, uint64_t h0, uint64_t h1, xs_scatter_result* out,
+              double* d_image)
+{
+    finalize(c, g, spec, cfg, &d_accum, 1, h0, h1, out, d_image);
 }
 
 void primary(xs_context* c, const xs_geometry& g, int angle, const xs_spectrum& spec, double* d_image)
@@ -980,6 +1001,7 @@ void xs_ctx_destroy(xs_context* c)
         b->release();
     c->loop_vol[0].release();
     c->loop_vol[1].release();
+    xsi::mgpu_release(c);
     xsd::wave_destroy(c->wave);
     if (c->ev0)
         cudaEventDestroy(c->ev0);
@@ -1335,6 +1357,50 @@ int xs_upload_response(xs_context* c, const xs_response* r)
         c->resp_dep.set(r->deposit);
         c->have_response = true;
         rebuild_tables(c);
+    });
+}
+
+int xs_ctx_copy_scene(xs_context* dst, const xs_context* src)
+{
+    return guard(dst, [&] {
+        if (!src || !src->have_phantom)
+            fail(XS_E_RUNTIME, "xscat-gpu: no phantom uploaded (xs_upload_phantom)");
+        if (dst == src)
+            return;
+        const xsd::Grid& G = src->grid;
+        const size_t n_bricks = (size_t)G.nbx * G.nby * G.nbz;
+        const size_t vox_bytes = n_bricks * (G.fmt == xsd::kFmtP4 ? 32 : 64);
+        const size_t dens_count = G.fmt == xsd::kFmtRaw ? n_bricks * 64 : 0;
+        // the source's device work (upload, encode, levels) must be complete
+        cuda_check(cudaSetDevice(src->device), "cudaSetDevice");
+        cuda_check(cudaStreamSynchronize(src->stream), "copy scene");
+        cuda_check(cudaSetDevice(dst->device), "cudaSetDevice");
+        dst->vox.reserve(vox_bytes);
+        cuda_check(cudaMemcpyPeerAsync(dst->vox.p, dst->device, src->vox.p, src->device, vox_bytes, dst->stream),
+                   "copy scene");
+        if (dens_count) {
+            dst->dens.reserve(dens_count);
+            cuda_check(cudaMemcpyPeerAsync(dst->dens.p, dst->device, src->dens.p, src->device, dens_count * 4,
+                                           dst->stream),
+                       "copy scene");
+        }
+        dst->grid = G;
+        dst->grid.vox = dst->vox.p;
+        dst->grid.dens = dens_count ? dst->dens.p : nullptr;
+        dst->n_mats = src->n_mats;
+        dst->mats = src->mats;
+        dst->n_pal = src->n_pal;
+        std::memcpy(dst->pal_mat, src->pal_mat, sizeof dst->pal_mat);
+        std::memcpy(dst->pal_dens, src->pal_dens, sizeof dst->pal_dens);
+        dst->skip_pays = src->skip_pays;
+        dst->last_upload_bytes = 0;
+        dst->have_phantom = true;
+        if (src->have_response) {
+            dst->resp_dqe = src->resp_dqe;
+            dst->resp_dep = src->resp_dep;
+            dst->have_response = true;
+        }
+        rebuild_tables(dst); // (synchronises dst's stream)
     });
 }
 
@@ -2164,6 +2230,17 @@ void xs_correction_config_default(xs_correction_config* cc)
     cc->sg_auto_window = 1;
 }
 
+// The loop's scans: on this context, or sharded by angle over a group's
+// devices when a group installed its delegate (xs_group_run_iterative_correction).
+static void loop_scan(xs_context* c, const xs_geometry* g, const xs_spectrum* spec, const xs_sim_config* cfg,
+                      const int32_t* subset, int32_t n, int32_t what, double* d_primary, double* d_scatter)
+{
+    if (c->scan_hook)
+        c->scan_hook(g, spec, cfg, subset, n, what, d_primary, d_scatter);
+    else
+        scan_device_impl(c, g, spec, cfg, subset, n, what, d_primary, d_scatter, nullptr);
+}
+
 static void call_status(xs_context* c, int st)
 {
     if (st != XS_OK)
@@ -2276,13 +2353,12 @@ int xs_run_iterative_correction(xs_context* c, const double* raw_intensity, cons
             rep.seconds_segmentation = secs(t0);
             t0 = clk::now();
             loop_stage(c, iter, "mc-scatter", [&] {
-                scan_device_impl(c, &g_mc, spec, &cc->sim, sub.data(), (int32_t)sub.size(), 1, nullptr,
-                                 c->loop_scat.p, nullptr);
+                loop_scan(c, &g_mc, spec, &cc->sim, sub.data(), (int32_t)sub.size(), 1, nullptr, c->loop_scat.p);
             });
             rep.seconds_mc_scatter = secs(t0);
             t0 = clk::now();
             loop_stage(c, iter, "mc-primary", [&] {
-                scan_device_impl(c, &g_mc, spec, &cc->sim, all.data(), n_full, 0, c->loop_prim.p, nullptr, nullptr);
+                loop_scan(c, &g_mc, spec, &cc->sim, all.data(), n_full, 0, c->loop_prim.p, nullptr);
             });
             rep.seconds_mc_primary = secs(t0);
             rep.mc_seconds_per_projection = rep.seconds_mc_scatter / (double)sub.size();
@@ -2327,3 +2403,68 @@ int xs_run_iterative_correction(xs_context* c, const double* raw_intensity, cons
 }
 
 } // extern "C"
+
+// ================================================ internal API (multi.cu)
+namespace xsi {
+
+int run(xs_context* c, const std::function<void()>& f)
+{
+    return guard(c, f);
+}
+
+int device(const xs_context* c) { return c->device; }
+cudaStream_t stream(const xs_context* c) { return c->stream; }
+void*& mgpu_slot(xs_context* c) { return c->mgpu; }
+void set_scan_hook(xs_context* c, ScanHook h) { c->scan_hook = std::move(h); }
+
+uint64_t history_count(const xs_geometry& g, const xs_spectrum& spec, const xs_sim_config& cfg)
+{
+    return make_plan(g, spec, cfg).n_hist;
+}
+
+xs_accum_layout layout(const xs_geometry& g, const xs_spectrum& spec, const xs_sim_config& cfg)
+{
+    return make_plan(g, spec, cfg).layout;
+}
+
+unsigned long long* own_accum(xs_context* c, size_t words)
+{
+    c->accum.reserve(words);
+    return c->accum.p;
+}
+
+void accumulate(xs_context* c, const xs_geometry& g, int angle, const xs_spectrum& spec, const xs_sim_config& cfg,
+                uint64_t h0, uint64_t h1, unsigned long long* d_accum)
+{
+    validate_call(g, angle, spec, cfg, "simulate_scatter");
+    ::accumulate(c, g, angle, spec, cfg, h0, h1, d_accum);
+}
+
+void finalize(xs_context* c, const xs_geometry& g, const xs_spectrum& spec, const xs_sim_config& cfg,
+              const unsigned long long* const* srcs, int n_src, uint64_t h0, uint64_t h1, xs_scatter_result* out,
+              double* d_image)
+{
+    ::finalize(c, g, spec, cfg, srcs, n_src, h0, h1, out, d_image);
+}
+
+void scan_device(xs_context* c, const xs_geometry* g, const xs_spectrum* spec, const xs_sim_config* cfg,
+                 const int32_t* subset, int32_t n, int32_t what, double* d_primary, double* d_scatter,
+                 double* seconds)
+{
+    scan_device_impl(c, g, spec, cfg, subset, n, what, d_primary, d_scatter, seconds);
+}
+
+void check_scan_args(const xs_geometry* g, const xs_sim_config* cfg, const int32_t* subset, int32_t n)
+{
+    if (n <= 0)
+        fail(XS_E_RUNTIME, "run_scan: empty angle subset");
+    xsh::validate_sim_config(*cfg);
+    xsh::validate_geometry(*g);
+    for (int i = 0; i < n; ++i)
+        if (subset[i] < 0 || subset[i] >= g->n_angles)
+            fail(XS_E_OUT_OF_RANGE, "run_scan: angle index %d out of range", subset[i]);
+}
+
+void cuda(cudaError_t e, const char* what) { cuda_check(e, what); }
+
+} // namespace xsi

@@ -104,19 +104,40 @@ __global__ void __launch_bounds__(128) primary_kernel(const __grid_constant__ Pr
 
 // ========================================================== finalize kernel
 // Limb sums -> fp64 image (+ REF's per-pixel variance, transport.cpp:317-322).
-__global__ void finalize_image_kernel(const unsigned long long* __restrict__ acc, uint64_t off_image,
-                                      uint64_t off_var, uint64_t npix, int log2_img, double n_hist,
-                                      int track_var, double* __restrict__ image,
-                                      double* __restrict__ var)
+// The accumulator may come in several parts (one per GPU or context of a
+// photon-batch split, in local or NVLink peer memory): the kernel sums the
+// parts' limbs as it reads them, so the reduce and the finalize are one pass.
+constexpr int kMaxSrc = 16;
+struct AccSrcs {
+    const unsigned long long* p[kMaxSrc];
+    int n;
+};
+
+__device__ __forceinline__ void load_limbs(const AccSrcs& S, uint64_t off, unsigned long long& l0,
+                                           unsigned long long& l1, unsigned long long& l2)
+{
+    l0 = l1 = l2 = 0ull;
+    for (int k = 0; k < S.n; ++k) {
+        const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(S.p[k] + off);
+        l0 += a.x;
+        l1 += a.y;
+        l2 += S.p[k][off + 2];
+    }
+}
+
+__global__ void finalize_image_kernel(const __grid_constant__ AccSrcs S, uint64_t off_image, uint64_t off_var,
+                                      uint64_t npix, int log2_img, double n_hist, int track_var,
+                                      double* __restrict__ image, double* __restrict__ var)
 {
     for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npix;
          p += (uint64_t)gridDim.x * blockDim.x) {
-        const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(acc + off_image + 4 * p);
-        const double v = dequantize(a.x, a.y, acc[off_image + 4 * p + 2], log2_img);
+        unsigned long long l0, l1, l2;
+        load_limbs(S, off_image + 4 * p, l0, l1, l2);
+        const double v = dequantize(l0, l1, l2, log2_img);
         image[p] = v;
         if (track_var && var) {
-            const double c2 = dequantize(acc[off_var + 4 * p], acc[off_var + 4 * p + 1],
-                                         acc[off_var + 4 * p + 2], 2 * log2_img);
+            load_limbs(S, off_var + 4 * p, l0, l1, l2);
+            const double c2 = dequantize(l0, l1, l2, 2 * log2_img);
             const double x = c2 - v * v / n_hist;
             const double den = 1.0 < n_hist - 1.0 ? n_hist - 1.0 : 1.0;
             var[p] = (0.0 < x ? x : 0.0) * n_hist / den;
@@ -144,16 +165,22 @@ cudaError_t launch_primary(const PrimaryParams& P, cudaStream_t s)
     return cudaGetLastError();
 }
 
-cudaError_t launch_finalize_image(const unsigned long long* acc, uint64_t off_image, uint64_t off_var,
-                                  uint64_t npix, int log2_img, double n_hist, int track_var,
+cudaError_t launch_finalize_image(const unsigned long long* const* srcs, int n_src, uint64_t off_image,
+                                  uint64_t off_var, uint64_t npix, int log2_img, double n_hist, int track_var,
                                   double* image, double* var, cudaStream_t s)
 {
+    if (n_src < 1 || n_src > kMaxSrc)
+        return cudaErrorInvalidValue;
+    AccSrcs S{};
+    S.n = n_src;
+    for (int k = 0; k < n_src; ++k)
+        S.p[k] = srcs[k];
     const int block = 256;
     int grid = (int)((npix + block - 1) / block);
     if (grid > 148 * 16)
         grid = 148 * 16;
-    finalize_image_kernel<<<grid, block, 0, s>>>(acc, off_image, off_var, npix, log2_img, n_hist,
-                                                 track_var, image, var);
+    finalize_image_kernel<<<grid, block, 0, s>>>(S, off_image, off_var, npix, log2_img, n_hist, track_var, image,
+                                                 var);
     return cudaGetLastError();
 }
 

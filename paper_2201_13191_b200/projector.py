@@ -113,6 +113,25 @@ class Context:
         self.check(A.lib().xs_upload_phantom(self.h, C.byref(pk.phantom(ph))))
         self.check(A.lib().xs_upload_response(self.h, C.byref(pk.response(resp))))
 
+    # multi-process (one process per GPU): an NCCL communicator in the library
+    @staticmethod
+    def comm_unique_id() -> bytes:
+        """xs_comm_unique_id on the rank that creates the communicator; send
+        the 128 bytes to every rank (e.g. torch.distributed.broadcast)."""
+        cid = A.XsCommId()
+        A.check(A.lib().xs_comm_unique_id(C.byref(cid)))
+        return C.string_at(C.addressof(cid), 128)
+
+    def comm_init(self, n_ranks: int, rank: int, unique_id: bytes):
+        cid = A.XsCommId()
+        C.memmove(C.addressof(cid), bytes(unique_id), min(len(unique_id), 128))
+        self.check(A.lib().xs_ctx_comm_init(self.h, int(n_ranks), int(rank), C.byref(cid)))
+
+    def comm_size(self):
+        n, r = C.c_int32(), C.c_int32()
+        self.check(A.lib().xs_ctx_comm_size(self.h, C.byref(n), C.byref(r)))
+        return n.value, r.value
+
     def launch_stats(self) -> Dict[str, float]:
         s = A.XsLaunchStats()
         self.check(A.lib().xs_last_launch_stats(self.h, C.byref(s)))
@@ -188,6 +207,48 @@ class Projector:
                           None if scat is None else ProjectionStack(angles, scat[:n]),
                           list(secs[:n]))
 
+    # photon batches / angle ranges over the context's NCCL communicator
+    def scatter_stats_mgpu(self, g: I.ScanGeometry, angle_idx: int, spec: I.Spectrum,
+                           cfg: I.SimConfig, root: int = 0, d_image_ptr: int = 0,
+                           host_image: bool = True) -> SimResult:
+        """xs_simulate_scatter_stats_mgpu: every rank calls it; the root's
+        result holds the whole projection, the others only `histories`."""
+        pk = A.Packed()
+        img = np.empty(g.nu * g.nv) if host_image else None
+        var = np.empty(g.nu * g.nv) if cfg.track_variance and host_image else None
+        res = A.XsScatterResult()
+        res.image = A.dptr(img) if img is not None else None
+        res.variance = A.dptr(var) if var is not None else None
+        self.ctx.check(A.lib().xs_simulate_scatter_stats_mgpu(
+            self.ctx.h, C.byref(pk.geometry(g)), angle_idx, C.byref(pk.spectrum(spec)),
+            C.byref(pk.config(cfg)), int(root), C.byref(res),
+            C.c_void_p(d_image_ptr) if d_image_ptr else None))
+        if img is None:
+            img = np.zeros(g.nu * g.nv)
+        return _result(img, var, res, g, self.ctx.launch_stats())
+
+    def run_scan_mgpu(self, g: I.ScanGeometry, spec: I.Spectrum, cfg: I.SimConfig,
+                      angle_subset: Sequence[int], what: int = BOTH, gather: bool = True,
+                      root: int = 0) -> ScanResult:
+        """xs_run_scan_mgpu: this rank's angle range (all of them on the root
+        with gather)."""
+        pk = A.Packed()
+        sub = np.ascontiguousarray(np.asarray(angle_subset, dtype=np.int32))
+        n = int(sub.size)
+        prim = np.zeros((max(n, 1), g.nv, g.nu)) if what != SCATTER else None
+        scat = np.zeros((max(n, 1), g.nv, g.nu)) if what != PRIMARY else None
+        secs = np.zeros(max(n, 1))
+        self.ctx.check(A.lib().xs_run_scan_mgpu(
+            self.ctx.h, C.byref(pk.geometry(g)), C.byref(pk.spectrum(spec)),
+            C.byref(pk.config(cfg)), sub.ctypes.data_as(C.POINTER(C.c_int32)), n, what,
+            1 if gather else 0, int(root),
+            A.dptr(prim) if prim is not None else None,
+            A.dptr(scat) if scat is not None else None, A.dptr(secs)))
+        angles = g.angles[sub] if n else np.zeros(0)
+        return ScanResult(None if prim is None else ProjectionStack(angles, prim[:n]),
+                          None if scat is None else ProjectionStack(angles, scat[:n]),
+                          list(secs[:n]))
+
     # device-level split (photon batches across GPUs)
     def accumulate(self, g, angle_idx, spec, cfg, hist_begin, hist_end, d_accum_ptr: int):
         pk = A.Packed()
@@ -207,6 +268,89 @@ class Projector:
             C.byref(pk.config(cfg)), C.c_void_p(d_accum_ptr), hist_begin, hist_end,
             C.byref(res), None))
         return _result(img, var, res, g, self.ctx.launch_stats())
+
+
+class Group:
+    """One process, several GPUs (an ``xs_group``): a scene replicated on every
+    member; scatter projections split into photon batches over the members
+    (their accumulators summed by the root's finalize kernel over NVLink peer
+    memory), scans and the correction loop's scans split by angle.  A device
+    may be listed more than once."""
+
+    def __init__(self, devices: Sequence[int], phantom: Optional[I.VoxelPhantom] = None,
+                 response: Optional[I.DetectorResponse] = None):
+        L = A.lib()
+        devs = (C.c_int32 * len(devices))(*[int(d) for d in devices])
+        h = C.c_void_p()
+        A.check(L.xs_group_create(devs, len(devices), C.byref(h)))
+        self.h = h
+        self.devices = list(devices)
+        if phantom is not None:
+            self.upload(phantom, response)
+
+    def close(self):
+        if self.h:
+            A.lib().xs_group_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def check(self, st):
+        if st != 0:
+            msg = A.lib().xs_group_last_error(self.h)
+            raise A._STATUS_EXC.get(st, I.XscatError)((msg or b"").decode(errors="replace"))
+
+    def __len__(self):
+        return int(A.lib().xs_group_size(self.h))
+
+    def set_option(self, key: str, value: int):
+        self.check(A.lib().xs_group_set_option(self.h, key.encode(), int(value)))
+
+    def upload(self, ph: I.VoxelPhantom, resp: Optional[I.DetectorResponse]):
+        pk = A.Packed()
+        if resp is not None:
+            self.check(A.lib().xs_group_upload_response(self.h, C.byref(pk.response(resp))))
+        self.check(A.lib().xs_group_upload_phantom(self.h, C.byref(pk.phantom(ph))))
+
+    def launch_stats(self, member: int = 0) -> Dict[str, float]:
+        s = A.XsLaunchStats()
+        A.check(A.lib().xs_last_launch_stats(A.lib().xs_group_context(self.h, member), C.byref(s)))
+        return {k: getattr(s, k) for k, _ in A.XsLaunchStats._fields_}
+
+    def scatter_stats(self, g: I.ScanGeometry, angle_idx: int, spec: I.Spectrum,
+                      cfg: I.SimConfig) -> SimResult:
+        pk = A.Packed()
+        img = np.empty(g.nu * g.nv)
+        var = np.empty(g.nu * g.nv) if cfg.track_variance else None
+        res = A.XsScatterResult()
+        res.image = A.dptr(img)
+        res.variance = A.dptr(var) if var is not None else None
+        self.check(A.lib().xs_group_simulate_scatter_stats(
+            self.h, C.byref(pk.geometry(g)), angle_idx, C.byref(pk.spectrum(spec)),
+            C.byref(pk.config(cfg)), C.byref(res)))
+        return _result(img, var, res, g, self.launch_stats())
+
+    def run_scan(self, g: I.ScanGeometry, spec: I.Spectrum, cfg: I.SimConfig,
+                 angle_subset: Sequence[int], what: int = BOTH) -> ScanResult:
+        pk = A.Packed()
+        sub = np.ascontiguousarray(np.asarray(angle_subset, dtype=np.int32))
+        n = int(sub.size)
+        prim = np.empty((max(n, 1), g.nv, g.nu)) if what != SCATTER else None
+        scat = np.empty((max(n, 1), g.nv, g.nu)) if what != PRIMARY else None
+        secs = np.zeros(max(n, 1))
+        self.check(A.lib().xs_group_run_scan(
+            self.h, C.byref(pk.geometry(g)), C.byref(pk.spectrum(spec)), C.byref(pk.config(cfg)),
+            sub.ctypes.data_as(C.POINTER(C.c_int32)), n, what,
+            A.dptr(prim) if prim is not None else None,
+            A.dptr(scat) if scat is not None else None, A.dptr(secs)))
+        angles = g.angles[sub] if n else np.zeros(0)
+        return ScanResult(None if prim is None else ProjectionStack(angles, prim[:n]),
+                          None if scat is None else ProjectionStack(angles, scat[:n]),
+                          list(secs[:n]))
 
 
 # ------------------------------------------------ REF-signature free functions
@@ -574,7 +718,7 @@ def reports_from(arr, n) -> List[IterationReport]:
 
 def run_iterative_correction(raw_intensity: ProjectionStack, flatfield, g: I.ScanGeometry, spec: I.Spectrum,
                              resp: I.DetectorResponse, cfg: CorrectionConfig, materials,
-                             ctx: Optional[Context] = None) -> CorrectionResult:
+                             ctx: Optional[Context] = None, group: Optional["Group"] = None) -> CorrectionResult:
     """REF run_iterative_correction (correction.cpp:137-266) with every stage
     on the device; `materials` is REF's list (vacuum prepended here)."""
     raw = np.ascontiguousarray(raw_intensity.images, dtype=np.float64)
@@ -590,17 +734,20 @@ def run_iterative_correction(raw_intensity: ProjectionStack, flatfield, g: I.Sca
         raise I.XscatError("run_iterative_correction: stack angle count mismatch")
     if raw.shape[1:] != (g.nv, g.nu):
         raise I.XscatError("iteration 1, stage correction: correct_projections: stack dims mismatch")
-    ctx = ctx or default_context()
     mats = [None] + [m for m in materials if m is not None]
     pk = A.Packed()
-    ctx.check(A.lib().xs_upload_response(ctx.h, C.byref(pk.response(resp))))
     vol = np.empty(tuple(int(d) for d in cfg.recon_dims[::-1]), np.float32)
     stack = np.empty_like(raw)
     reps = (A.XsIterationReport * max(1, int(cfg.n_iterations)))()
-    ctx.check(A.lib().xs_run_iterative_correction(ctx.h, raw.ctypes.data, flat.ctypes.data,
-                                                  C.byref(pk.geometry(g)), C.byref(pk.spectrum(spec)),
-                                                  C.byref(pk.correction_config(cfg)), len(mats),
-                                                  pk.materials(mats), vol.ctypes.data, stack.ctypes.data,
-                                                  reps, 0))
+    args = (raw.ctypes.data, flat.ctypes.data, C.byref(pk.geometry(g)), C.byref(pk.spectrum(spec)),
+            C.byref(pk.correction_config(cfg)), len(mats), pk.materials(mats), vol.ctypes.data,
+            stack.ctypes.data, reps, 0)
+    if group is not None:  # the loop's scans sharded by angle over the group's GPUs
+        group.check(A.lib().xs_group_upload_response(group.h, C.byref(pk.response(resp))))
+        group.check(A.lib().xs_group_run_iterative_correction(group.h, *args))
+    else:
+        ctx = ctx or default_context()
+        ctx.check(A.lib().xs_upload_response(ctx.h, C.byref(pk.response(resp))))
+        ctx.check(A.lib().xs_run_iterative_correction(ctx.h, *args))
     return CorrectionResult(vol, ProjectionStack(list(raw_intensity.angle_values), stack),
                             reports_from(reps, int(cfg.n_iterations)))

@@ -19,7 +19,7 @@ ROOT = pathlib.Path(__file__).resolve().parents[1]
 
 def test_library_exports_every_declared_symbol():
     header = (ROOT / "include" / "xscat_gpu.h").read_text()
-    declared = set(re.findall(r"^\s*(?:int|void|double|const char\*)\s+(xs_\w+)\(", header, re.M))
+    declared = set(re.findall(r"^\s*(?:int|int32_t|void|double|const char\*|xs_context\*)\s+(xs_\w+)\(", header, re.M))
     assert len(declared) >= 30
     L = A.lib()
     missing = [s for s in sorted(declared) if not hasattr(L, s)]
