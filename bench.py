@@ -3,10 +3,13 @@
 One step = one projection of BASELINE config C3: 150 kVp, 512^3 Al/Fe
 "cylinder head" phantom, 2048x2048 flat panel, 1e8 photon histories,
 splitting 20 (BASELINE.json metric "photon histories/sec and sec/projection
-(1e8 photons)").  With N GPUs the projection's history range is split into N
-contiguous photon batches (one per rank) whose fixed-point tallies are summed
-by an NCCL reduce to rank 0, which finalizes the image (strong scaling: total
-work fixed).  Results are bit-identical for every N.
+(1e8 photons)").  Every step goes through the library's multi-GPU entry
+point xs_simulate_scatter_stats_mgpu: with N GPUs (torchrun, one process per
+GPU) the projection's history range is split into N contiguous photon batches
+(one per rank) whose fixed-point tallies are summed by an ncclReduce inside
+libxscatgpu (its own communicator, xs_ctx_comm_init) onto rank 0, which
+finalizes the image (strong scaling: total work fixed).  Results are
+bit-identical for every N.
 
   value : histories/s with the scene resident on the device (kernel path)
   e2e   : the same through the C ABI with host buffers: phantom upload
@@ -201,31 +204,30 @@ def gpu_arm(args):
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
     proj = X.Projector(w.phantom, resp, ctx=ctx)
-    L = A.accum_layout(g.nu, g.nv, spec.n_bins, cfg.track_variance)
+    # the library's own NCCL communicator (xs_ctx_comm_init): rank 0 makes the
+    # id, torch.distributed only carries its 128 bytes to the other ranks
+    uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+    if rank == 0:
+        uid.copy_(torch.frombuffer(bytearray(X.Context.comm_unique_id()), dtype=torch.uint8))
+    if ws > 1:
+        dist.broadcast(uid, src=0)
+    ctx.comm_init(ws, rank, bytes(uid.cpu().numpy().tobytes()))
     n_hist = X.history_count(spec, cfg.photons_total)
-    h0, h1 = n_hist * rank // ws, n_hist * (rank + 1) // ws
-    accum = torch.zeros(L["words"], dtype=torch.int64, device="cuda")
     image = torch.empty(g.nu * g.nv, dtype=torch.float64, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
 
     def step():
-        accum.zero_()
-        proj.accumulate(g, 0, spec, cfg, h0, h1, accum.data_ptr())
-        ls = ctx.launch_stats()
+        # xs_simulate_scatter_stats_mgpu: this rank's photon batch, ncclReduce of the
+        # fixed-point accumulators onto rank 0, finalize into a device image there
+        r = proj.scatter_stats_mgpu(g, 0, spec, cfg, root=0, d_image_ptr=image.data_ptr(),
+                                    host_image=False)
+        ls = r.stats
         kms = (ls["kernel_ms"], ls["walk_ms"], ls["launches"] + 1)  # + the finalize kernel
         stats = None
-        if ws > 1:
-            dist.reduce(accum, dst=0)
         if rank == 0:
-            res = A.XsScatterResult()
-            pk = A.Packed()
-            A.check(A.lib().xs_scatter_finalize_device(
-                ctx.h, A.C.byref(pk.geometry(g)), A.C.byref(pk.spectrum(spec)),
-                A.C.byref(pk.config(cfg)), A.C.c_void_p(accum.data_ptr()), 0, n_hist,
-                A.C.byref(res), A.C.c_void_p(image.data_ptr())), ctx.h)
-            stats = ctx.launch_stats()
-            stats["total"] = res.total
-            stats["total_std_error"] = res.total_std_error
+            stats = dict(ls)
+            stats["total"] = r.total
+            stats["total_std_error"] = r.total_std_error
         return kms, stats
 
     for _ in range(args.warmup):
@@ -290,17 +292,9 @@ def gpu_arm(args):
         def e2e_step():
             pk = A.Packed()
             A.check(A.lib().xs_upload_phantom(ctx.h, A.C.byref(pk.phantom(w.phantom))), ctx.h)
-            accum.zero_()
-            proj.accumulate(g, 0, spec, cfg, h0, h1, accum.data_ptr())
-            if ws > 1:
-                dist.reduce(accum, dst=0)
+            r = proj.scatter_stats_mgpu(g, 0, spec, cfg, root=0, host_image=rank == 0)
             if rank == 0:
-                res = A.XsScatterResult()
-                res.image = A.dptr(img_h)
-                A.check(A.lib().xs_scatter_finalize_device(
-                    ctx.h, A.C.byref(pk.geometry(g)), A.C.byref(pk.spectrum(spec)),
-                    A.C.byref(pk.config(cfg)), A.C.c_void_p(accum.data_ptr()), 0, n_hist,
-                    A.C.byref(res), None), ctx.h)
+                img_h[:] = r.image.ravel()
             torch.cuda.synchronize()
 
         e2e_step()
@@ -320,8 +314,9 @@ def gpu_arm(args):
                "d2h_bytes_per_step": int(img_h.nbytes) if rank == 0 else 0,
                "steps": n_e2e,
                "note": "per step: xs_upload_phantom of the host u8 id + f32 density grid "
-                       "(pinned staging, H2D, device validation + palette encode), transport, "
-                       "reduce, finalize, image D2H"}
+                       "(pinned staging, H2D, device validation + palette encode), then "
+                       "xs_simulate_scatter_stats_mgpu with a host image: this rank's photon "
+                       "batch, ncclReduce, finalize, image D2H on rank 0"}
 
     if rank == 0:
         hbm, kind = peaks()
@@ -351,7 +346,9 @@ def gpu_arm(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": WORKLOAD, "histories": n_hist, "splitting": cfg.splitting,
                        "detector": [g.nu, g.nv], "phantom": list(w.phantom.dims),
-                       "parallelism": f"photon batches x{ws} + NCCL reduce" if ws > 1 else "1 GPU",
+                       "parallelism": (f"photon batches x{ws}, ncclReduce of the fixed-point tallies "
+                                       "inside libxscatgpu (xs_simulate_scatter_stats_mgpu)") if ws > 1
+                       else "1 GPU (xs_simulate_scatter_stats_mgpu, 1 rank)",
                        "l2": "flushed between timed steps (256 MiB write)"},
             "sec_per_projection": ms_per_step / 1e3,
             "primary_ms": primary_ms,
@@ -403,6 +400,12 @@ def c4_arm(args):
     mine = list(range(n_ang * rank // ws, n_ang * (rank + 1) // ws))
     ctx = X.Context(local)
     proj = X.Projector(w.phantom, w.response, ctx=ctx)
+    uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+    if rank == 0:
+        uid.copy_(torch.frombuffer(bytearray(X.Context.comm_unique_id()), dtype=torch.uint8))
+    if ws > 1:
+        dist.broadcast(uid, src=0)
+    ctx.comm_init(ws, rank, bytes(uid.cpu().numpy().tobytes()))
     for _ in range(args.warmup):
         proj.run_scan(g, w.spectrum, w.config, mine[:1], X.SCATTER)
     torch.cuda.synchronize()
@@ -412,7 +415,8 @@ def c4_arm(args):
     sampler.start()
     t = time.perf_counter()
     for _ in range(args.steps):
-        proj.run_scan(g, w.spectrum, w.config, mine, X.SCATTER)
+        # xs_run_scan_mgpu: this rank's contiguous angle range, images to its host memory
+        proj.run_scan_mgpu(g, w.spectrum, w.config, list(range(n_ang)), X.SCATTER, gather=False)
     torch.cuda.synchronize()
     dt = torch.tensor([(time.perf_counter() - t) / args.steps], dtype=torch.float64, device="cuda")
     if ws > 1:
@@ -431,7 +435,8 @@ def c4_arm(args):
             "sec_per_projection": sec / n_ang * ws,
             "e2e": {"value": n_hist / sec, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 8 * 2048 * 2048 * len(mine),
-                    "note": "run_scan through the C ABI, scatter images copied to host memory every angle"},
+                    "note": "xs_run_scan_mgpu through the C ABI (angle-sharded, no gather), scatter "
+                            "images copied to each rank's host memory every angle"},
             "clocks": clocks}), flush=True)
     if ws > 1:
         dist.destroy_process_group()
