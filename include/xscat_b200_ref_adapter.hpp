@@ -19,6 +19,10 @@
 // Device selection: XSCAT_DEVICE (default 0).  One context per thread; the
 // scene (phantom + response) is uploaded on every call, like the reference
 // receives it on every call; Projector keeps it resident across calls.
+// Several GPUs: XSCAT_DEVICES="0,1,2,3" (two or more entries) makes the
+// projector calls and the correction loop run on an xs_group of those devices
+// (photon batches for one projection, angle ranges for scans and the loop's
+// scans; bit-identical results for any device list, REF PAPER.md:215).
 #pragma once
 
 #include <algorithm>
@@ -150,18 +154,96 @@ inline Context& thread_context()
     return ctx;
 }
 
+inline void throw_group(int st, const xs_group* grp)
+{
+    if (st == XS_OK)
+        return;
+    const std::string msg = xs_group_last_error(grp);
+    switch (st) {
+    case XS_E_OUT_OF_RANGE:
+        throw std::out_of_range(msg);
+    case XS_E_INVALID_ARGUMENT:
+        throw std::invalid_argument(msg);
+    case XS_E_DOMAIN:
+        throw std::domain_error(msg);
+    default:
+        throw std::runtime_error(msg);
+    }
+}
+
+// A group of GPUs in this process (xs_group): one context per device.
+class Group {
+public:
+    explicit Group(const std::vector<int>& devices)
+    {
+        std::vector<int32_t> d(devices.begin(), devices.end());
+        throw_status(xs_group_create(d.data(), static_cast<int32_t>(d.size()), &grp_), nullptr);
+    }
+    ~Group() { xs_group_destroy(grp_); }
+    Group(const Group&) = delete;
+    Group& operator=(const Group&) = delete;
+    xs_group* get() const { return grp_; }
+
+    // XSCAT_DEVICES="0,1,...": the devices, or empty when unset / one entry
+    static std::vector<int> devices_from_env()
+    {
+        std::vector<int> out;
+        const char* e = std::getenv("XSCAT_DEVICES");
+        if (!e)
+            return out;
+        for (const char* q = e; *q;) {
+            out.push_back(std::atoi(q));
+            while (*q && *q != ',')
+                ++q;
+            if (*q == ',')
+                ++q;
+        }
+        if (out.size() < 2)
+            out.clear();
+        return out;
+    }
+
+private:
+    xs_group* grp_ = nullptr;
+};
+
+// This thread's group when XSCAT_DEVICES names two or more devices, else null.
+inline Group* thread_group()
+{
+    thread_local std::unique_ptr<Group> grp = [] {
+        const std::vector<int> d = Group::devices_from_env();
+        return d.empty() ? std::unique_ptr<Group>() : std::unique_ptr<Group>(new Group(d));
+    }();
+    return grp.get();
+}
+
 // A scene resident on the device (upload once, project many angles).
 class Projector {
 public:
     Projector(const xscat::VoxelPhantom& ph, const xscat::DetectorResponse& resp,
               Context& ctx = thread_context())
-        : ctx_(ctx)
+        : ctx_(ctx), grp_(thread_group())
     {
         Packed p;
         pack_phantom(p, ph);
-        throw_status(xs_upload_phantom(ctx_.get(), &p.ph), ctx_.get());
         const xs_response r{table_view(resp.dqe), table_view(resp.deposit)};
+        if (grp_) { // the scene on every device of the group (one upload, device-to-device copies)
+            throw_group(xs_group_upload_response(grp_->get(), &r), grp_->get());
+            throw_group(xs_group_upload_phantom(grp_->get(), &p.ph), grp_->get());
+            return;
+        }
+        throw_status(xs_upload_phantom(ctx_.get(), &p.ph), ctx_.get());
         throw_status(xs_upload_response(ctx_.get(), &r), ctx_.get());
+    }
+    // Explicit group (overrides XSCAT_DEVICES).
+    Projector(const xscat::VoxelPhantom& ph, const xscat::DetectorResponse& resp, Group& grp)
+        : ctx_(thread_context()), grp_(&grp)
+    {
+        Packed p;
+        pack_phantom(p, ph);
+        const xs_response r{table_view(resp.dqe), table_view(resp.deposit)};
+        throw_group(xs_group_upload_response(grp_->get(), &r), grp_->get());
+        throw_group(xs_group_upload_phantom(grp_->get(), &p.ph), grp_->get());
     }
 
     // REF simulate_scatter_stats (transport.hpp:89-91)
@@ -178,8 +260,10 @@ public:
         xs_scatter_result r{};
         r.image = out.image.values.data();
         r.variance = cfg.track_variance ? var.data() : nullptr;
-        throw_status(xs_simulate_scatter_stats(ctx_.get(), &p.g, angle_idx, &p.s, &p.c, &r),
-                     ctx_.get());
+        if (grp_)
+            throw_group(xs_group_simulate_scatter_stats(grp_->get(), &p.g, angle_idx, &p.s, &p.c, &r), grp_->get());
+        else
+            throw_status(xs_simulate_scatter_stats(ctx_.get(), &p.g, angle_idx, &p.s, &p.c, &r), ctx_.get());
         if (cfg.track_variance)
             out.image.variance = std::move(var);
         out.ledger.initial = r.ledger.initial;
@@ -201,8 +285,8 @@ public:
         Packed p;
         pack_call(p, g, spec, cfg);
         xscat::DetectorImage img(g.nu, g.nv);
-        throw_status(xs_simulate_primary(ctx_.get(), &p.g, angle_idx, &p.s, &p.c, img.values.data()),
-                     ctx_.get());
+        xs_context* c = grp_ ? xs_group_context(grp_->get(), 0) : ctx_.get();
+        throw_status(xs_simulate_primary(c, &p.g, angle_idx, &p.s, &p.c, img.values.data()), c);
         return img;
     }
 
@@ -220,10 +304,16 @@ public:
         std::vector<double> secs(subset.size());
         std::vector<int32_t> sub(subset.begin(), subset.end());
         const int q = what == xscat::ScanQuantity::primary ? 0 : (what == xscat::ScanQuantity::scatter ? 1 : 2);
-        throw_status(xs_run_scan(ctx_.get(), &p.g, &p.s, &p.c, sub.data(), static_cast<int32_t>(sub.size()), q,
-                                 want_p ? prim.data() : nullptr, want_s ? scat.data() : nullptr,
-                                 secs.data()),
-                     ctx_.get());
+        if (grp_)
+            throw_group(xs_group_run_scan(grp_->get(), &p.g, &p.s, &p.c, sub.data(), static_cast<int32_t>(sub.size()),
+                                          q, want_p ? prim.data() : nullptr, want_s ? scat.data() : nullptr,
+                                          secs.data()),
+                        grp_->get());
+        else
+            throw_status(xs_run_scan(ctx_.get(), &p.g, &p.s, &p.c, sub.data(), static_cast<int32_t>(sub.size()), q,
+                                     want_p ? prim.data() : nullptr, want_s ? scat.data() : nullptr,
+                                     secs.data()),
+                         ctx_.get());
         std::vector<double> angles;
         for (int i : subset)
             angles.push_back(g.angles[i]);
@@ -246,6 +336,7 @@ public:
 
 private:
     Context& ctx_;
+    Group* grp_ = nullptr;
 };
 
 // ------------------------------------------- REF-signature free functions
@@ -582,8 +673,12 @@ inline xscat::CorrectionResult run_iterative_correction(const xscat::ProjectionS
     if (raw_intensity.n_angles() != g.n_angles())
         throw std::runtime_error("run_iterative_correction: stack angle count mismatch");
     Context& c = thread_context();
+    Group* grp = thread_group(); // XSCAT_DEVICES: the loop's scans sharded over the group
     const xs_response r{table_view(resp.dqe), table_view(resp.deposit)};
-    throw_status(xs_upload_response(c.get(), &r), c.get());
+    if (grp)
+        throw_group(xs_group_upload_response(grp->get(), &r), grp->get());
+    else
+        throw_status(xs_upload_response(c.get(), &r), c.get());
     Packed p;
     pack_call(p, g, spec, cfg.sim);
     detail::MaterialList ml(materials);
@@ -619,10 +714,17 @@ inline xscat::CorrectionResult run_iterative_correction(const xscat::ProjectionS
                                               xscat::default_voxel_size(g, cfg.recon_dims));
     std::vector<double> stack(raw.size());
     std::vector<xs_iteration_report> reps(std::max(1, cfg.n_iterations));
-    throw_status(xs_run_iterative_correction(c.get(), raw.data(), flatfield.values.data(), &p.g, &p.s, &cc,
-                                             static_cast<int32_t>(ml.xs.size()), ml.xs.data(),
-                                             out.corrected_volume.values.data(), stack.data(), reps.data(), 0),
-                 c.get());
+    if (grp)
+        throw_group(xs_group_run_iterative_correction(grp->get(), raw.data(), flatfield.values.data(), &p.g, &p.s,
+                                                      &cc, static_cast<int32_t>(ml.xs.size()), ml.xs.data(),
+                                                      out.corrected_volume.values.data(), stack.data(), reps.data(),
+                                                      0),
+                    grp->get());
+    else
+        throw_status(xs_run_iterative_correction(c.get(), raw.data(), flatfield.values.data(), &p.g, &p.s, &cc,
+                                                 static_cast<int32_t>(ml.xs.size()), ml.xs.data(),
+                                                 out.corrected_volume.values.data(), stack.data(), reps.data(), 0),
+                     c.get());
     out.corrected_stack = detail::unflatten(stack, raw_intensity.nu, raw_intensity.nv, raw_intensity.angle_values);
     for (int i = 0; i < cfg.n_iterations; ++i) {
         const xs_iteration_report& x = reps[i];

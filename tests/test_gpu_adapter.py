@@ -14,11 +14,18 @@ DEMO = ROOT / "oracle" / "_ref" / "ref_adapter_demo"
 
 
 @pytest.mark.gpu
-def test_reference_api_program_on_b200(tmp_path):
+@pytest.mark.parametrize("devices", [None, "0,0"])
+def test_reference_api_program_on_b200(tmp_path, devices):
+    """devices "0,0": XSCAT_DEVICES makes the adapter run on an xs_group (two
+    contexts on the test box's one GPU): the same checks must pass."""
+    import os
     if not DEMO.exists():
         pytest.skip("oracle/_ref/ref_adapter_demo not built (needs /root/reference at build time)")
     data = I.write_reference_data(tmp_path / "data")
-    r = subprocess.run([str(DEMO), str(data)], capture_output=True, text=True, timeout=600)
+    env = dict(os.environ)
+    if devices:
+        env["XSCAT_DEVICES"] = devices
+    r = subprocess.run([str(DEMO), str(data)], capture_output=True, text=True, timeout=600, env=env)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "all checks passed" in r.stdout
