@@ -242,10 +242,10 @@ __device__ __forceinline__ void start_axis(double p, double o, double d, double 
         step = -1;
         dt = FAST ? -hs * r : -hs / d;
         tn = FAST ? (org + idx * hs - o) * r : (org + idx * hs - o) / d;
-    } else {
+    } else { // (FAST, the block walk: finite sentinels, see cross_n)
         step = 0;
-        dt = CUDART_INF;
-        tn = CUDART_INF;
+        dt = FAST ? 1e300 : CUDART_INF;
+        tn = FAST ? 1e300 : CUDART_INF;
     }
     while (tn <= t0 && step != 0) {
         idx += step;

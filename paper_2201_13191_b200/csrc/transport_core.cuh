@@ -364,10 +364,11 @@ __device__ __forceinline__ bool walk_begin_impl(const TransportParams& P, Walk& 
     w.ay = term_y(G, w.iy);
     w.az = term_z(G, w.iz);
     prefetch<FMT>(G, w.ax + w.ay + w.az, w.raw, w.shift, w.dens);
-    // 1/dt estimates for macro-cell skips (cross_count corrects them exactly)
-    w.rdx = fabs(d.x) * G.ihx;
-    w.rdy = fabs(d.y) * G.ihy;
-    w.rdz = fabs(d.z) * G.ihz;
+    // 1/dt for the block walk's crossing counts (cross_n); axes that do not
+    // move get the sentinel of start_axis<true>
+    w.rdx = d.x != 0.0 ? fabs(d.x) * G.ihx : 1e-300;
+    w.rdy = d.y != 0.0 ? fabs(d.y) * G.ihy : 1e-300;
+    w.rdz = d.z != 0.0 ? fabs(d.z) * G.ihz : 1e-300;
     return true;
 }
 
@@ -396,20 +397,25 @@ __device__ __forceinline__ int d2i_trunc_small(double x) // trunc(x) for 0 <= x 
     return __double2loint(__dadd_rz(x, 4503599627370496.0));
 }
 
-__device__ __forceinline__ int cross_count(double tn, double dt, double rdt, double tm, int k, int s)
+// Boundaries of one axis crossed by a step that ends at tm.  e = tn + k dt
+// is the axis' last boundary inside the current block (k = boundaries left
+// in it, 0 outside uniform blocks).  An axis whose block face is the step's
+// exit (e <= tm, i.e. e == tm) crosses all k + 1; any other axis crosses the
+// boundaries at or before tm, counted as trunc((tm - tn) / dt + 1) with the
+// fp64 reciprocal (rd = |d| / h) and clamped to [0, k].  The count can be off
+// by one only for a boundary within rounding of tm, which moves the depth by
+// rounding-level amounts: the block walk already differs from REF at that
+// level.  Outside uniform blocks (k = 0) this is exactly REF's step: the
+// axes with tn == tm cross (trace.cpp:146-153).  Axes that do not move carry
+// finite sentinels (tn = dt = 1e300, rd = 1e-300; start_axis<true>) so the
+// estimate is 0 and tn + 0 * dt stays tn.
+__device__ __forceinline__ int cross_n(double tn, double e, double rd, double tm, int k)
 {
-    // Boundaries tn + j dt (j = 0..k) at or before tm.  Straight-line code
-    // (estimate, then both one-step corrections evaluated together) so the
-    // three axes overlap instead of running as three divergent branches.
-    // k == 0 gives 1 when tn == tm (the plain Siddon crossing, REF
-    // trace.cpp:146-153); axes without a crossing (s == 0 or tn > tm) give 0.
-    int n = d2i_trunc_small((tm - tn) * rdt) + 1; // tm >= tn whenever the result is used
-    n = n > k + 1 ? k + 1 : n;
-    n = n < 1 ? 1 : n;
-    const double lo = tn + u2d_small(n - 1) * dt; // boundary n-1 (must be <= tm)
-    const double hi = tn + u2d_small(n) * dt;     // boundary n (must be > tm)
-    n = lo > tm ? n - 1 : ((n <= k && hi <= tm) ? n + 1 : n);
-    return (s != 0 && tn <= tm) ? (n < 1 ? 1 : n) : 0;
+    // 2^52 + 1 + q rounded toward zero: its low word is trunc(q + 1) for q >= -1,
+    // and negative (0xFFFFFFFx) just below, which the clamp turns into 0
+    const int est = __double2loint(__dadd_rz((tm - tn) * rd, 4503599627370497.0));
+    const int n = est < 0 ? 0 : (est > k ? k : est);
+    return e <= tm ? k + 1 : n;
 }
 
 // One voxel (REF trace.cpp:136-155 / :202-228).  Branch-free axis advance;
@@ -435,21 +441,19 @@ __device__ __forceinline__ bool walk_step(const TransportParams& P, const MuTab<
     const int code = decode<FMT>(w.raw, w.shift);
     if (SKIP) {
         // One step = up to the next boundary crossing, or, in an aligned
-        // uniform block (level field of the code), up to its exit: k* boundaries of
-        // each axis remain inside the cell (0 outside uniform cells, where
+        // uniform block (level field of the code), up to its exit: k* boundaries
+        // of each axis remain inside the block (0 outside uniform blocks, where
         // this is exactly REF's voxel step).  Branch-free, so lanes in
         // uniform and mixed cells do not diverge.
         const int c = code & ~G.ubit;
-        // k* = boundaries left inside the voxel's uniform block (0 outside)
         const int um = (1 << ((G.lvl_log2 >> (((uint32_t)code >> G.lvl_shift) << 2)) & 0xFu)) - 1;
         const int kx = (w.sx > 0 ? ~w.ix : w.ix) & um;
         const int ky = (w.sy > 0 ? ~w.iy : w.iy) & um;
         const int kz = (w.sz > 0 ? ~w.iz : w.iz) & um;
-        const double fx = w.tnx + u2d_small(kx) * w.dtx, fy = w.tny + u2d_small(ky) * w.dty,
-                     fz = w.tnz + u2d_small(kz) * w.dtz;
-        const double ex = kx ? fx : w.tnx;
-        const double ey = ky ? fy : w.tny;
-        const double ez = kz ? fz : w.tnz;
+        // the block's exit face per axis (k = 0: the next boundary, tn itself)
+        const double ex = w.tnx + u2d_small(kx) * w.dtx;
+        const double ey = w.tny + u2d_small(ky) * w.dty;
+        const double ez = w.tnz + u2d_small(kz) * w.dtz;
         double tm = ex;
         if (ey < tm)
             tm = ey;
@@ -460,28 +464,28 @@ __device__ __forceinline__ bool walk_step(const TransportParams& P, const MuTab<
         const double mu = tab.mu(P, c, w.dens);
         const double seg = mu * (tm - w.t);
         const double nd = w.depth + seg;
-        if (nd >= w.target) { // free path ends in this voxel / cell; t_hit in hit_t()
+        if (nd >= w.target) { // free path ends in this voxel / block; t_hit in hit_t()
             w.hit = 1;
             w.mu_hit = mu;
             w.texit = tm;
             return false;
         }
-        const int nx = cross_count(w.tnx, w.dtx, w.rdx, tm, kx, w.sx);
-        const int ny = cross_count(w.tny, w.dty, w.rdy, tm, ky, w.sy);
-        const int nz = cross_count(w.tnz, w.dtz, w.rdz, tm, kz, w.sz);
+        const int nx = cross_n(w.tnx, ex, w.rdx, tm, kx);
+        const int ny = cross_n(w.tny, ey, w.rdy, tm, ky);
+        const int nz = cross_n(w.tnz, ez, w.rdz, tm, kz);
         const int nix = w.ix + nx * w.sx, niy = w.iy + ny * w.sy, niz = w.iz + nz * w.sz;
         const bool inside = (tm < w.texit) && (uint32_t)nix < (uint32_t)G.nx &&
                             (uint32_t)niy < (uint32_t)G.ny && (uint32_t)niz < (uint32_t)G.nz;
-        const uint32_t nax = nx ? term_x(G, nix) : w.ax;
-        const uint32_t nay = ny ? term_y(G, niy) : w.ay;
-        const uint32_t naz = nz ? term_z(G, niz) : w.az;
+        // (an axis that does not cross keeps its term: term_x(nix) == ax)
+        const uint32_t nax = term_x(G, nix), nay = term_y(G, niy), naz = term_z(G, niz);
         if (inside)
             prefetch<FMT>(G, nax + nay + naz, w.raw, w.shift, w.dens);
         w.depth = nd;
         w.t = tm;
-        w.tnx = nx ? w.tnx + u2d_small(nx) * w.dtx : w.tnx;
-        w.tny = ny ? w.tny + u2d_small(ny) * w.dty : w.tny;
-        w.tnz = nz ? w.tnz + u2d_small(nz) * w.dtz : w.tnz;
+        // (n = 0: tn + 0 * dt == tn, dt finite)
+        w.tnx = w.tnx + u2d_small(nx) * w.dtx;
+        w.tny = w.tny + u2d_small(ny) * w.dty;
+        w.tnz = w.tnz + u2d_small(nz) * w.dtz;
         if (um) {
             w.skipped += (uint32_t)(nx + ny + nz) - 1u;
             ++w.ucells;

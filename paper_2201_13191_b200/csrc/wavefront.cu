@@ -92,7 +92,7 @@ struct WaveCtl {
 // the wave's rays, so a warp's loads and stores coalesce).
 struct WaveRays {
     double *t, *texit, *target, *tn, *dt, *mu; // tn, dt: 3 planes; mu: n_mu planes
-    float* rd;                                 // 3 planes: 1/dt estimates
+    double* rd;                                // 3 planes: 1/dt (block walk crossing counts)
     int* vox;                                  // 3 planes: ix, iy, iz
     uint8_t* flags;                            // (sx+1) | (sy+1) << 2 | (sz+1) << 4 | walking << 6
     double* pre;                               // scoring prefactor (set-up -> complete)
@@ -344,9 +344,11 @@ __global__ void __launch_bounds__(kBlock) wave_setup(const __grid_constant__ Tra
         __stcs(&R.dt[i], w.dtx);
         __stcs(&R.dt[R.cap + i], w.dty);
         __stcs(&R.dt[2ull * R.cap + i], w.dtz);
-        __stcs(&R.rd[i], (float)w.rdx);
-        __stcs(&R.rd[R.cap + i], (float)w.rdy);
-        __stcs(&R.rd[2ull * R.cap + i], (float)w.rdz);
+        if (SKIP) {
+            __stcs(&R.rd[i], w.rdx);
+            __stcs(&R.rd[R.cap + i], w.rdy);
+            __stcs(&R.rd[2ull * R.cap + i], w.rdz);
+        }
         __stcs(&R.vox[i], w.ix);
         __stcs(&R.vox[R.cap + i], w.iy);
         __stcs(&R.vox[2ull * R.cap + i], w.iz);
@@ -401,9 +403,11 @@ __global__ void __launch_bounds__(kBlock, SKIP ? XSW_WALK_BLOCKS : XSW_EXACT_BLO
                         w.dtx = __ldcs(&R.dt[r]);
                         w.dty = __ldcs(&R.dt[R.cap + r]);
                         w.dtz = __ldcs(&R.dt[2ull * R.cap + r]);
-                        w.rdx = __ldcs(&R.rd[r]);
-                        w.rdy = __ldcs(&R.rd[R.cap + r]);
-                        w.rdz = __ldcs(&R.rd[2ull * R.cap + r]);
+                        if (SKIP) {
+                            w.rdx = __ldcs(&R.rd[r]);
+                            w.rdy = __ldcs(&R.rd[R.cap + r]);
+                            w.rdz = __ldcs(&R.rd[2ull * R.cap + r]);
+                        }
                         w.ix = __ldcs(&R.vox[r]);
                         w.iy = __ldcs(&R.vox[R.cap + r]);
                         w.iz = __ldcs(&R.vox[2ull * R.cap + r]);
@@ -790,7 +794,7 @@ struct WavePipe {
     size_t fq_have[2] = {0, 0};
     double* dbl = nullptr; // t, texit, target, tn x3, dt x3, mu x n_mu, pre, res
     size_t dbl_have = 0;
-    float* rd = nullptr;
+    double* rd = nullptr;
     size_t rd_have = 0;
     int* vox = nullptr; // vox x3, res_vox x3, pix
     size_t vox_have = 0;
@@ -810,7 +814,7 @@ struct WavePipe {
     size_t bytes_held() const
     {
         return n_slots_have * sizeof(Slot) + stack_have * 4 + (sq_have[0] + sq_have[1]) * sizeof(ScoreBatch) +
-               (fq_have[0] + fq_have[1]) * 4 + dbl_have * 8 + rd_have * 4 + vox_have * 4 + bytes_have;
+               (fq_have[0] + fq_have[1]) * 4 + dbl_have * 8 + rd_have * 8 + vox_have * 4 + bytes_have;
     }
     void release()
     {
@@ -963,7 +967,7 @@ size_t wave_slot_bytes() { return sizeof(Slot); }
 static double pipe_bytes(uint32_t n_slots, int splitting, int n_mu)
 {
     const double cap = (double)n_slots * ((double)splitting + 1.0);
-    const double per_ray = (3 + 3 + 3 + n_mu + 2) * 8.0 + 3 * 4.0 + 7 * 4.0 + 2.0;
+    const double per_ray = (3 + 3 + 3 + n_mu + 2) * 8.0 + 3 * 8.0 + 7 * 4.0 + 2.0;
     const double per_slot = (double)sizeof(Slot) + 4.0 + 2.0 * (sizeof(ScoreBatch) + 4.0);
     return cap * per_ray + (double)n_slots * per_slot;
 }
