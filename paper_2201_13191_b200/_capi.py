@@ -9,6 +9,7 @@ or calls anything under ``oracle/``.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import pathlib
 from typing import List, Optional
 
@@ -17,7 +18,9 @@ import numpy as np
 from . import inputs as I
 
 PKG = pathlib.Path(__file__).resolve().parent
-LIB_PATH = PKG / "lib" / "libxscatgpu.so"
+# XSCAT_LIB: an alternative build of the library (A/B experiments, tools/ab.sh);
+# the product path is the in-tree lib/libxscatgpu.so
+LIB_PATH = pathlib.Path(os.environ["XSCAT_LIB"]) if os.environ.get("XSCAT_LIB") else PKG / "lib" / "libxscatgpu.so"
 
 c_double_p = C.POINTER(C.c_double)
 c_u64_p = C.POINTER(C.c_uint64)

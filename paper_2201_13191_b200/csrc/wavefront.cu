@@ -54,6 +54,9 @@ namespace {
 #ifndef XSW_REFILL
 #define XSW_REFILL 8
 #endif
+#ifndef XSW_BLOCK_UNROLL
+#define XSW_BLOCK_UNROLL 0 // two block steps per loop trip
+#endif
 constexpr int kRefill = XSW_REFILL; // idle lanes that trigger a warp's refill in the walk kernel
 
 #ifndef XSW_WALK_BLOCKS
@@ -379,7 +382,14 @@ __global__ void __launch_bounds__(kBlock, SKIP ? XSW_WALK_BLOCKS : XSW_EXACT_BLO
     w.march = 0;
     bool walking = false, drained = false;
     uint32_t ray = 0;
-    uint32_t c_fp = 0, c_sc = 0, c_iter = 0, c_wit = 0, c_uni = 0;
+    // launch counters (free-path / scoring visits, iterations, uniform-block
+    // iterations) in shared memory, added when a ray ends: per-lane counter
+    // registers would push the loop past the 80-register budget
+    __shared__ unsigned int cnt[4];
+    if (threadIdx.x < 4)
+        cnt[threadIdx.x] = 0u;
+    __syncthreads();
+    uint32_t c_wit = 0;
     for (;;) {
         const unsigned idle = __ballot_sync(kFull, !walking);
         if (!drained && (idle == kFull || __popc(idle) >= (SKIP ? kRefill : XSW_REFILL_EXACT))) {
@@ -439,16 +449,15 @@ __global__ void __launch_bounds__(kBlock, SKIP ? XSW_WALK_BLOCKS : XSW_EXACT_BLO
             walking = walk_step<FMT, REG, SKIP>(P, tab, w);
             ++w.steps;
             // the voxel walk takes a second step per loop trip (halves the per-step
-            // loop overhead: -21% walk time on speckled phantoms); the block
-            // walk's larger step would spill
-            if (!SKIP && walking) {
+            // loop overhead: -21% walk time on speckled phantoms)
+            if ((!SKIP || XSW_BLOCK_UNROLL) && walking) {
                 walking = walk_step<FMT, REG, SKIP>(P, tab, w);
                 ++w.steps;
             }
             if (!walking) {
-                if (ray < n_s) {
+                const bool score = ray < n_s;
+                if (score) {
                     __stcs(&R.res[ray], w.depth);
-                    c_sc += w.steps + w.skipped;
                 } else {
                     const bool hit = w.hit != 0;
                     __stcs(&R.res[ray], hit ? hit_t(w) : 0.0);
@@ -456,24 +465,21 @@ __global__ void __launch_bounds__(kBlock, SKIP ? XSW_WALK_BLOCKS : XSW_EXACT_BLO
                     __stcs(&R.res_vox[ray], w.ix);
                     __stcs(&R.res_vox[R.cap + ray], w.iy);
                     __stcs(&R.res_vox[2ull * R.cap + ray], w.iz);
-                    c_fp += w.steps + w.skipped;
                 }
-                c_iter += w.steps;
-                c_uni += w.ucells;
+                atomicAdd(&cnt[score ? 1 : 0], w.steps + w.skipped);
+                atomicAdd(&cnt[2], w.steps);
+                if (w.ucells)
+                    atomicAdd(&cnt[3], w.ucells);
             }
         }
     }
     unsigned long long* diag = P.accum + P.off_diag;
-    c_fp = __reduce_add_sync(kFull, c_fp);
-    c_sc = __reduce_add_sync(kFull, c_sc);
-    c_iter = __reduce_add_sync(kFull, c_iter);
-    c_uni = __reduce_add_sync(kFull, c_uni);
-    if (lane == 0) {
-        red_add(diag + 7, c_uni);
-        red_add(diag + 0, c_fp);
-        red_add(diag + 1, c_sc);
-        red_add(diag + 5, c_iter);
+    if (lane == 0)
         red_add(diag + 6, 32ull * c_wit);
+    __syncthreads();
+    if (threadIdx.x < 4) { // free-path visits, scoring visits, iterations, uniform iterations
+        const int slot[4] = {0, 1, 5, 7};
+        red_add(diag + slot[threadIdx.x], cnt[threadIdx.x]);
     }
 }
 
