@@ -159,6 +159,9 @@ typedef struct xs_launch_stats {
     float walk_ms;             /* device time of the walk kernel(s) (the whole kernel for the megakernel) */
     uint32_t launches;         /* kernels launched by the scatter call */
     uint32_t block_walk;       /* 1: the walk crossed uniform blocks (walk_mode, per-phantom probe) */
+    /* environment XSCAT_KTIME=1 (wavefront engine): summed device time of the
+     * other kernels of every wave, CUDA events on the pipeline streams */
+    float setup_ms, score_ms, event_ms, admit_ms;
 } xs_launch_stats;
 
 typedef struct xs_context xs_context;

@@ -105,7 +105,8 @@ class XsLaunchStats(C.Structure):
                 ("smem_per_block", C.c_uint32), ("slots_per_warp", C.c_uint32),
                 ("engine", C.c_uint32), ("waves", C.c_uint32), ("live_histories", C.c_uint32),
                 ("uniform_iterations", C.c_uint64), ("walk_ms", C.c_float), ("launches", C.c_uint32),
-                ("block_walk", C.c_uint32)]
+                ("block_walk", C.c_uint32), ("setup_ms", C.c_float), ("score_ms", C.c_float),
+                ("event_ms", C.c_float), ("admit_ms", C.c_float)]
 
 
 def dptr(a: np.ndarray):

@@ -708,6 +708,10 @@ void accumulate(xs_context* c, const xs_geometry& g, int angle, const xs_spectru
         c->last.waves = info.waves;
         c->last.live_histories = info.n_slots;
         c->last.walk_ms = info.walk_ms;
+        c->last.setup_ms = info.setup_ms;
+        c->last.score_ms = info.score_ms;
+        c->last.event_ms = info.event_ms;
+        c->last.admit_ms = info.admit_ms;
         c->last.launches = info.launches;
         c->last.palette_size = c->n_pal;
         c->last.upload_bytes = c->last_upload_bytes;

@@ -76,6 +76,18 @@ struct WarpQ {
     __device__ __forceinline__ void claim(int s) const { atomicAnd(&hdr_()->free_mask, ~(1ull << s)); }
     __device__ __forceinline__ void release(int s) const { atomicOr(&hdr_()->free_mask, 1ull << s); }
     __device__ __forceinline__ void fence() const { __threadfence_block(); }
+    // statistics straight into the block's shared accumulators
+    __device__ __forceinline__ void ledger(const TransportParams& P, const Block& B, int k, double w,
+                                           DevStatus* st, int bin) const
+    {
+        ledger_add(P, B, k, w, st, bin);
+    }
+    __device__ __forceinline__ void bin_total(const TransportParams& P, const Block& B, int bin, double t,
+                                              DevStatus* st) const
+    {
+        bin_total_add(P, B, bin, t, st);
+    }
+    __device__ __forceinline__ void history_done(const Block& B) const { sadd(B.diag + 2, 1); }
 };
 
 } // namespace

@@ -74,14 +74,28 @@ __device__ __forceinline__ double words_to_uniform(uint32_t hi, uint32_t lo)
     return ((double)bits + 0.5) * 0x1p-53;
 }
 
-// One out-of-line Philox draw on a history's stream (REF rng.hpp:29-60).  The
-// event code works on a local copy of the slot's stream (one load and one
-// store per event instead of a slot round trip per draw); a single copy of
-// the 10-round refill keeps the event code small.
-__device__ __noinline__ double slot_uniform(SlotRng* s, uint32_t k0, uint32_t k1, uint32_t angle)
+// The 10-round Philox block, out of line with scalar arguments and a uint4
+// result (registers only): one copy serves every draw site of the event
+// code, and the caller's stream state stays in registers.
+__device__ __noinline__ uint4 philox_out(uint32_t block, uint32_t photon, uint32_t bin, uint32_t angle, uint32_t k0,
+                                         uint32_t k1)
+{
+    uint4 o;
+    philox_block(block, photon, bin, angle, k0, k1, o.x, o.y, o.z, o.w);
+    return o;
+}
+
+// One Philox draw on a history's stream (REF rng.hpp:29-60).  The event code
+// works on a local copy of the slot's stream (one load and one store per
+// event instead of a slot round trip per draw).
+__device__ __forceinline__ double slot_uniform(SlotRng* s, uint32_t k0, uint32_t k1, uint32_t angle)
 {
     if (s->pos == 4) {
-        philox_block(s->block, s->photon, s->bin, angle, k0, k1, s->b0, s->b1, s->b2, s->b3);
+        const uint4 o = philox_out(s->block, s->photon, s->bin, angle, k0, k1);
+        s->b0 = o.x;
+        s->b1 = o.y;
+        s->b2 = o.z;
+        s->b3 = o.w;
         s->pos = 0;
         ++s->block;
     }
@@ -578,6 +592,17 @@ __device__ __forceinline__ void ledger_add(const TransportParams& P, const Block
         raise(st, XS_E_RUNTIME, kErrTallyOverflow, bin, 0.0, w);
 }
 
+// A history's total into its bin's Sum t and Sum t^2 (REF run_history :225-228).
+__device__ __forceinline__ void bin_total_add(const TransportParams& P, const Block& B, int bin, double t,
+                                              DevStatus* st)
+{
+    if (t != 0.0) {
+        unsigned long long* bs = B.bins + 8 * bin;
+        if (!tally_limbs(bs, t, P.log2_img) || !tally_limbs(bs + 3, t * t, 2 * P.log2_img))
+            raise(st, XS_E_RUNTIME, kErrTallyOverflow, bin, 0.0, t);
+    }
+}
+
 // History end (REF run_history :225-241): bin statistics from the exact
 // fixed-point history total, per-pixel grouping for the variance, free slot.
 template <class Q>
@@ -586,11 +611,7 @@ __device__ __noinline__ void finalize_history(const TransportParams& P, const Bl
 {
     Slot& S = qs.slot(s);
     const double t = dequantize(S.T[0], S.T[1], S.T[2], P.log2_img);
-    unsigned long long* bs = B.bins + 8 * S.bin;
-    if (t != 0.0) {
-        if (!tally_limbs(bs, t, P.log2_img) || !tally_limbs(bs + 3, t * t, 2 * P.log2_img))
-            raise(st, XS_E_RUNTIME, kErrTallyOverflow, S.bin, S.E, t);
-    }
+    qs.bin_total(P, B, S.bin, t, st);
     if (P.track_var) {
         const uint32_t* vp = P.var_pix + var_base;
         const double* vv = P.var_val + var_base;
@@ -617,7 +638,7 @@ __device__ __noinline__ void finalize_history(const TransportParams& P, const Bl
                 raise(st, XS_E_RUNTIME, kErrTallyOverflow, S.bin, S.E, c);
         }
     }
-    sadd(B.diag + 2, 1);
+    qs.history_done(B);
     qs.release(s);
 }
 
@@ -690,7 +711,7 @@ __device__ __noinline__ int event_select(const TransportParams& P, const Block& 
     const int bin = S.bin;
     const double W = S.W;
     if (!hit) {
-        ledger_add(P, B, 1, W, st, bin);
+        qs.ledger(P, B, 1, W, st, bin);
         end_history(P, B, qs, s, var_base, st);
         return K_NONE;
     }
@@ -721,7 +742,7 @@ __device__ __noinline__ int event_select(const TransportParams& P, const Block& 
     const double u = slot_uniform(&rng, P.k0, P.k1, P.angle) * total;
     const int kind = u < pe ? K_PE : (u < pe + incoh ? K_COMPTON : K_RAYLEIGH);
     if (kind == K_PE) {
-        ledger_add(P, B, 2, W, st, bin);
+        qs.ledger(P, B, 2, W, st, bin);
         end_history(P, B, qs, s, var_base, st);
         return K_PE;
     }
@@ -859,15 +880,15 @@ __device__ __noinline__ void event_continue(const TransportParams& P, const Bloc
     bool alive = true;
     double Wn = W;
     if (gen >= P.max_inter) { // REF :207-211
-        ledger_add(P, B, 3, W, st, bin);
+        qs.ledger(P, B, 3, W, st, bin);
         alive = false;
     } else if (S.wmin > 0.0 && W < S.wmin) { // REF :213-222
         if (slot_uniform(&rng, P.k0, P.k1, P.angle) < P.survival) {
             const double boosted = W / P.survival;
-            ledger_add(P, B, 5, boosted - W, st, bin);
+            qs.ledger(P, B, 5, boosted - W, st, bin);
             Wn = boosted;
         } else {
-            ledger_add(P, B, 4, W, st, bin);
+            qs.ledger(P, B, 4, W, st, bin);
             alive = false;
         }
     }
@@ -892,9 +913,13 @@ __device__ __forceinline__ void history_event(const TransportParams& P, const Bl
 }
 
 // History start (REF run_history :120-138, sample_emission :73-87).
+// Returns the history's initial weight w0; tally_w0 = false leaves its ledger
+// entry ("initial") to the caller (the wavefront admission sums it in
+// registers instead of contended shared-memory atomics).
 template <class Q>
-__device__ __noinline__ void history_start(const TransportParams& P, const Block& B, const Q qs,
-                                           const uint64_t* sstart, int s, uint64_t h, DevStatus* st)
+__device__ __noinline__ double history_start(const TransportParams& P, const Block& B, const Q qs,
+                                             const uint64_t* sstart, int s, uint64_t h, DevStatus* st,
+                                             bool tally_w0 = true)
 {
     Slot& S = qs.slot(s);
     int lo = 0, hi = P.n_bins; // last bin b with start[b] <= h (skips empty bins)
@@ -939,11 +964,13 @@ __device__ __noinline__ void history_start(const TransportParams& P, const Block
     S.gen = 0;
     S.pending = 1;
     S.n_var = 0;
-    ledger_add(P, B, 0, w0, st, bin);
+    if (tally_w0)
+        ledger_add(P, B, 0, w0, st, bin);
     S.target = -nl_log(slot_uniform(&rng, P.k0, P.k1, P.angle));
     S.rng = rng;
     qs.push_free(s);
     qs.claim(s);
+    return w0;
 }
 
 // Scoring-ray set-up (REF run_history :166-183): geometry, p(theta), e_out,

@@ -54,6 +54,22 @@ namespace {
 #ifndef XSW_REFILL
 #define XSW_REFILL 8
 #endif
+// minimum resident blocks per SM of the latency-bound kernels: register caps
+// that trade a few spills for occupancy (XSCAT_KTIME, C3, one pipeline, same
+// box: set-up 84.6 -> 72.5 ms at 64 registers, scoring 26.6 -> 22.0 ms at 40,
+// events 60.0 -> 53.0 ms at 80; admission is faster uncapped)
+#ifndef XSW_SETUP_MINB
+#define XSW_SETUP_MINB 8
+#endif
+#ifndef XSW_SCORE_MINB
+#define XSW_SCORE_MINB 12
+#endif
+#ifndef XSW_EVENT_MINB
+#define XSW_EVENT_MINB 6
+#endif
+#ifndef XSW_ADMIT_MINB
+#define XSW_ADMIT_MINB 1
+#endif
 #ifndef XSW_BLOCK_UNROLL
 #define XSW_BLOCK_UNROLL 0 // two block steps per loop trip
 #endif
@@ -171,6 +187,20 @@ struct GlobalQ {
         ctl->free_stack[atomicAdd(&ctl->free_top, 1)] = (uint32_t)s;
     }
     __device__ __forceinline__ void fence() const { __threadfence(); }
+    // statistics straight into the block's shared accumulators (folding them
+    // per warp at the flush points, like the pushes, measured slower: event
+    // kernel 58 -> 67 ms per C3 projection)
+    __device__ __forceinline__ void ledger(const TransportParams& P, const Block& B, int k, double w,
+                                           DevStatus* st, int bin) const
+    {
+        ledger_add(P, B, k, w, st, bin);
+    }
+    __device__ __forceinline__ void bin_total(const TransportParams& P, const Block& B, int bin, double t,
+                                              DevStatus* st) const
+    {
+        bin_total_add(P, B, bin, t, st);
+    }
+    __device__ __forceinline__ void history_done(const Block& B) const { sadd(B.diag + 2, 1); }
 };
 
 __device__ __forceinline__ void deferred_reset(Deferred& d)
@@ -179,8 +209,11 @@ __device__ __forceinline__ void deferred_reset(Deferred& d)
 }
 
 // All 32 lanes, converged: one reservation per queue for the warp's pushes.
-__device__ __forceinline__ void flush_deferred(WaveCtl* ctl, int out, Deferred& d, uint32_t n_slots, DevStatus* st)
+__device__ __forceinline__ void flush_deferred(const TransportParams& P, const Block& B, WaveCtl* ctl, int out,
+                                               Deferred& d, uint32_t n_slots, DevStatus* st)
 {
+    (void)P;
+    (void)B;
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
     WaveQueue& q = ctl->q[out];
@@ -286,7 +319,7 @@ __device__ __forceinline__ void load_mu(const WaveRays& R, uint32_t i, MuTab<FMT
 
 // ------------------------------------------------------------------ set-up
 template <int FMT, bool REG, bool SKIP>
-__global__ void __launch_bounds__(kBlock) wave_setup(const __grid_constant__ TransportParams P,
+__global__ void __launch_bounds__(kBlock, XSW_SETUP_MINB) wave_setup(const __grid_constant__ TransportParams P,
                                                      const __grid_constant__ WaveArgs A)
 {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -489,7 +522,7 @@ __global__ void __launch_bounds__(kBlock, SKIP ? XSW_WALK_BLOCKS : XSW_EXACT_BLO
 // lanes' scores per slot (exact integer limb sums) and touches each slot's
 // total and pending count once.
 
-__global__ void __launch_bounds__(kBlock) wave_score(const __grid_constant__ TransportParams P,
+__global__ void __launch_bounds__(kBlock, XSW_SCORE_MINB) wave_score(const __grid_constant__ TransportParams P,
                                                      const __grid_constant__ WaveArgs A)
 {
     extern __shared__ __align__(16) unsigned long long acc[];
@@ -553,7 +586,7 @@ __global__ void __launch_bounds__(kBlock) wave_score(const __grid_constant__ Tra
                 finalize_history(P, B, qs, s, var_base_of(P, s), st);
         }
         __syncwarp();
-        flush_deferred(ctl, A.cur ^ 1, def, A.n_slots, P.status);
+        flush_deferred(P, B, ctl, A.cur ^ 1, def, A.n_slots, P.status);
     }
     flush_stats(P, B);
 }
@@ -561,7 +594,7 @@ __global__ void __launch_bounds__(kBlock) wave_score(const __grid_constant__ Tra
 // Free paths: the history's event (REF run_history :141-223), which pushes
 // the next wave's scoring rays and free path.
 template <int FMT>
-__global__ void __launch_bounds__(kBlock) wave_event(const __grid_constant__ TransportParams P,
+__global__ void __launch_bounds__(kBlock, XSW_EVENT_MINB) wave_event(const __grid_constant__ TransportParams P,
                                                      const __grid_constant__ WaveArgs A)
 {
     extern __shared__ __align__(16) unsigned long long acc[];
@@ -595,7 +628,7 @@ __global__ void __launch_bounds__(kBlock) wave_event(const __grid_constant__ Tra
         if ((uint32_t)lane < take)
             event_continue(P, B, qs, (int)sl, var_base_of(P, (int)sl), P.status);
         __syncwarp();
-        flush_deferred(ctl, A.cur ^ 1, def, A.n_slots, P.status);
+        flush_deferred(P, B, ctl, A.cur ^ 1, def, A.n_slots, P.status);
     };
     auto select = [&](bool active, uint32_t i) { // selection phase for the lanes with `active`
         int kind = K_NONE, s = 0;
@@ -609,7 +642,7 @@ __global__ void __launch_bounds__(kBlock) wave_event(const __grid_constant__ Tra
                 kind = event_select<FMT>(P, B, qs, s, true, __ldcs(&R.res[i]), vx, vy, vz, var_base_of(P, s), P.status);
         }
         __syncwarp();
-        flush_deferred(ctl, A.cur ^ 1, def, A.n_slots, P.status);
+        flush_deferred(P, B, ctl, A.cur ^ 1, def, A.n_slots, P.status);
         const unsigned mc = __ballot_sync(kFull, kind == K_COMPTON);
         const unsigned mr = __ballot_sync(kFull, kind == K_RAYLEIGH);
         if (kind == K_COMPTON)
@@ -638,7 +671,7 @@ __global__ void __launch_bounds__(kBlock) wave_event(const __grid_constant__ Tra
                 history_event<FMT>(P, B, qs, s, false, 0.0, 0, 0, 0, var_base_of(P, s), P.status);
         }
         __syncwarp(); // reconverge before the warp-synchronous gather
-        flush_deferred(ctl, A.cur ^ 1, def, A.n_slots, P.status);
+        flush_deferred(P, B, ctl, A.cur ^ 1, def, A.n_slots, P.status);
         const unsigned hm = __ballot_sync(kFull, hit);
         if (hit)
             hb[nb + __popc(hm & lt_mask)] = i;
@@ -688,7 +721,7 @@ __global__ void wave_plan(const __grid_constant__ TransportParams P, const __gri
     ++ctl->waves;
 }
 
-__global__ void __launch_bounds__(kBlock) wave_admit(const __grid_constant__ TransportParams P,
+__global__ void __launch_bounds__(kBlock, XSW_ADMIT_MINB) wave_admit(const __grid_constant__ TransportParams P,
                                                      const __grid_constant__ WaveArgs A)
 {
     extern __shared__ __align__(16) unsigned long long acc[];
@@ -707,16 +740,37 @@ __global__ void __launch_bounds__(kBlock) wave_admit(const __grid_constant__ Tra
     const uint32_t qb = ctl->admit_q;
     Deferred def;
     deferred_reset(def);
+    // the histories' initial weights (REF WeightLedger::initial): limb sums in
+    // registers, one warp reduction at the end (every admitted history adds to
+    // the same three words: shared-memory atomics there serialise)
+    unsigned long long w0l[3] = {0ull, 0ull, 0ull};
     const uint32_t stride = gridDim.x * blockDim.x;
     for (uint32_t i0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); i0 < k; i0 += stride) {
         const uint32_t i = i0 + (threadIdx.x & 31u);
         if (i < k) {
             const int s = (int)ctl->free_stack[top + i];
             const GlobalQ qs{A.slots, ctl, A.cur, (int)(qb + i), &def};
-            history_start(P, B, qs, sstart, s, base + i, P.status);
+            const double w0 = history_start(P, B, qs, sstart, s, base + i, P.status, false);
+            uint64_t l0, l1, l2;
+            if (w0 != 0.0) {
+                if (quantize(ldexp(w0, -P.log2_w), l0, l1, l2)) {
+                    w0l[0] += l0;
+                    w0l[1] += l1;
+                    w0l[2] += l2;
+                } else {
+                    raise(P.status, XS_E_RUNTIME, kErrTallyOverflow, 0, 0.0, w0);
+                }
+            }
         }
         __syncwarp();
-        flush_deferred(ctl, A.cur, def, A.n_slots, P.status);
+        flush_deferred(P, B, ctl, A.cur, def, A.n_slots, P.status);
+    }
+    for (int j = 0; j < 3; ++j) {
+        unsigned long long v = w0l[j];
+        for (int o = 16; o > 0; o >>= 1)
+            v += __shfl_xor_sync(kFull, v, o);
+        if ((threadIdx.x & 31) == 0)
+            red_add(P.accum + P.off_ledger + j, v);
     }
     flush_stats(P, B);
 }
@@ -1134,6 +1188,10 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
         XSW_CHECK(cudaGetLastError());
         launches += 3;
     }
+    // XSCAT_KTIME=1: CUDA events around every kernel of the wave (per-kernel
+    // device time in xs_launch_stats; meaningful with one pipeline)
+    const bool ktime = std::getenv("XSCAT_KTIME") != nullptr;
+    const int kEv = ktime ? 6 : 2;
     const int check_every = 4;
     for (;;) {
         for (int k = 0; k < check_every; ++k)
@@ -1143,7 +1201,7 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
                     continue;
                 cudaStream_t ps = w.stream;
                 WaveArgs& A = w.A;
-                while (w.ev.size() < 2 * (size_t)(w.waves + 1)) {
+                while (w.ev.size() < (size_t)kEv * (size_t)(w.waves + 1)) {
                     cudaEvent_t v;
                     XSW_CHECK(cudaEventCreate(&v));
                     w.ev.push_back(v);
@@ -1161,20 +1219,29 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
 #else
                 auto dbg_wait = [](const char*) {};
 #endif
+                cudaEvent_t* ev = &w.ev[(size_t)kEv * w.waves]; // [walk start, walk end(, ...)]
+                if (ktime)
+                    XSW_CHECK(cudaEventRecord(ev[2], ps));
                 K.setup<<<g_setup, kBlock, mu_smem, ps>>>(w.P, A);
                 dbg_wait("setup");
-                XSW_CHECK(cudaEventRecord(w.ev[2 * w.waves], ps));
+                XSW_CHECK(cudaEventRecord(ev[0], ps));
                 K.walk<<<g_walk, kBlock, mu_smem, ps>>>(w.P, A);
                 dbg_wait("walk");
-                XSW_CHECK(cudaEventRecord(w.ev[2 * w.waves + 1], ps));
+                XSW_CHECK(cudaEventRecord(ev[1], ps));
                 wave_score<<<g_score, kBlock, stat_smem, ps>>>(w.P, A);
                 dbg_wait("score");
+                if (ktime)
+                    XSW_CHECK(cudaEventRecord(ev[3], ps));
                 K.event<<<g_work, kBlock, stat_smem, ps>>>(w.P, A);
                 dbg_wait("event");
+                if (ktime)
+                    XSW_CHECK(cudaEventRecord(ev[4], ps));
                 A.cur = w.cur ^ 1;
                 wave_plan<<<1, 1, 0, ps>>>(w.P, A);
                 wave_admit<<<g_admit, kBlock, admit_smem, ps>>>(w.P, A);
                 dbg_wait("admit");
+                if (ktime)
+                    XSW_CHECK(cudaEventRecord(ev[5], ps));
                 w.cur ^= 1;
                 ++w.waves;
                 launches += 6;
@@ -1224,9 +1291,20 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
         XSW_CHECK(cudaStreamWaitEvent(s, w.join, 0));
         XSW_CHECK(cudaStreamSynchronize(w.stream));
         for (uint32_t i = 0; i < w.waves; ++i) {
+            const cudaEvent_t* ev = &w.ev[(size_t)kEv * i];
             float ms = 0.f;
-            XSW_CHECK(cudaEventElapsedTime(&ms, w.ev[2 * i], w.ev[2 * i + 1]));
+            XSW_CHECK(cudaEventElapsedTime(&ms, ev[0], ev[1]));
             walk += ms;
+            if (ktime && info) {
+                XSW_CHECK(cudaEventElapsedTime(&ms, ev[2], ev[0]));
+                info->setup_ms += ms;
+                XSW_CHECK(cudaEventElapsedTime(&ms, ev[1], ev[3]));
+                info->score_ms += ms;
+                XSW_CHECK(cudaEventElapsedTime(&ms, ev[3], ev[4]));
+                info->event_ms += ms;
+                XSW_CHECK(cudaEventElapsedTime(&ms, ev[4], ev[5]));
+                info->admit_ms += ms;
+            }
         }
         waves = std::max(waves, w.waves);
     }

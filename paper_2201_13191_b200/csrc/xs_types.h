@@ -133,6 +133,7 @@ struct WaveInfo {
     int32_t walk_blocks_per_sm;
     uint32_t launches;
     float walk_ms; // summed device time of the walk kernels
+    float setup_ms, score_ms, event_ms, admit_ms; // XSCAT_KTIME: the other kernels (plan + admit)
 };
 
 // Angular interpolation plan entry (REF postprocess.cpp:160-192).
