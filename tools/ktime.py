@@ -20,5 +20,8 @@ for _ in range(reps):
     ks = ("setup_ms", "walk_ms", "score_ms", "event_ms", "admit_ms")
     tot = sum(s[k] for k in ks)
     print(f"lib={os.environ.get('XSCAT_LIB', 'product')} pipes={os.environ.get('XSCAT_WAVE_PIPES', '2')} "
-          f"transport {s['kernel_ms']:.1f} ms | " + " ".join(f"{k[:-3]} {s[k]:.1f} ({100 * s[k] / tot:.0f}%)" for k in ks),
+          f"transport {s['kernel_ms']:.1f} ms | " + " ".join(f"{k[:-3]} {s[k]:.1f} ({100 * s[k] / tot:.0f}%)" for k in ks)
+          + f" | iters/hist {s['walk_iterations'] / s['histories']:.1f} uniform {s['uniform_iterations'] / max(1, s['walk_iterations']):.2f}"
+          f" lanes {s['walk_iterations'] / max(1, s['walk_lane_slots']):.2f} visits/hist "
+          f"{(s['free_path_steps'] + s['scoring_steps']) / s['histories']:.0f} rays/hist {s['scoring_rays'] / s['histories']:.2f}",
           flush=True)
