@@ -423,9 +423,33 @@ __global__ void __launch_bounds__(kBlock, SKIP ? XSW_WALK_BLOCKS : XSW_EXACT_BLO
         cnt[threadIdx.x] = 0u;
     __syncthreads();
     uint32_t c_wit = 0;
+    // A lane that ends its ray keeps the result in its walker registers until
+    // the warp next refills (or the loop ends): the stores then run once per
+    // refill instead of in a divergent branch of almost every iteration.
+    bool has_result = false;
+    auto store_result = [&]() {
+        const bool score = ray < n_s;
+        if (score) {
+            __stcs(&R.res[ray], w.depth);
+        } else {
+            const bool hit = w.hit != 0;
+            __stcs(&R.res[ray], hit ? hit_t(w) : 0.0);
+            R.res_hit[ray] = hit ? 1 : 0;
+            __stcs(&R.res_vox[ray], w.ix);
+            __stcs(&R.res_vox[R.cap + ray], w.iy);
+            __stcs(&R.res_vox[2ull * R.cap + ray], w.iz);
+        }
+        atomicAdd(&cnt[score ? 1 : 0], w.steps + w.skipped);
+        atomicAdd(&cnt[2], w.steps);
+        if (w.ucells)
+            atomicAdd(&cnt[3], w.ucells);
+        has_result = false;
+    };
     for (;;) {
         const unsigned idle = __ballot_sync(kFull, !walking);
         if (!drained && (idle == kFull || __popc(idle) >= (SKIP ? kRefill : XSW_REFILL_EXACT))) {
+            if (has_result)
+                store_result();
             uint32_t base = 0;
             if (lane == 0)
                 base = atomicAdd(&ctl->cursor, (uint32_t)__popc(idle));
@@ -487,25 +511,11 @@ __global__ void __launch_bounds__(kBlock, SKIP ? XSW_WALK_BLOCKS : XSW_EXACT_BLO
                 walking = walk_step<FMT, REG, SKIP>(P, tab, w);
                 ++w.steps;
             }
-            if (!walking) {
-                const bool score = ray < n_s;
-                if (score) {
-                    __stcs(&R.res[ray], w.depth);
-                } else {
-                    const bool hit = w.hit != 0;
-                    __stcs(&R.res[ray], hit ? hit_t(w) : 0.0);
-                    R.res_hit[ray] = hit ? 1 : 0;
-                    __stcs(&R.res_vox[ray], w.ix);
-                    __stcs(&R.res_vox[R.cap + ray], w.iy);
-                    __stcs(&R.res_vox[2ull * R.cap + ray], w.iz);
-                }
-                atomicAdd(&cnt[score ? 1 : 0], w.steps + w.skipped);
-                atomicAdd(&cnt[2], w.steps);
-                if (w.ucells)
-                    atomicAdd(&cnt[3], w.ucells);
-            }
+            has_result = !walking;
         }
     }
+    if (has_result)
+        store_result();
     unsigned long long* diag = P.accum + P.off_diag;
     if (lane == 0)
         red_add(diag + 6, 32ull * c_wit);
