@@ -199,6 +199,7 @@ def gpu_arm(args):
     t0 = time.time()
     w = configs.c3(photons=args.photons)
     g, spec, cfg, resp = w.geometry, w.spectrum, w.config, w.response
+    cfg.step_voxels = args.step
     log(f"[rank {rank}] scene built in {time.time() - t0:.1f}s")
     ctx = X.Context(device)
     stream = torch.cuda.current_stream()
@@ -344,7 +345,8 @@ def gpu_arm(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "histories": n_hist, "splitting": cfg.splitting,
+            "config": {"workload": WORKLOAD + (f", step_voxels {args.step} (march)" if args.step > 1 else ""),
+                       "histories": n_hist, "splitting": cfg.splitting,
                        "detector": [g.nu, g.nv], "phantom": list(w.phantom.dims),
                        "parallelism": (f"photon batches x{ws}, ncclReduce of the fixed-point tallies "
                                        "inside libxscatgpu (xs_simulate_scatter_stats_mgpu)") if ws > 1
@@ -457,6 +459,9 @@ def main():
     ap.add_argument("--workload", default="c3", choices=["c3", "c4"],
                     help="c3: one 1e8-photon projection (the BASELINE metric); c4: angle-sharded full scan")
     ap.add_argument("--angles", type=int, default=360)
+    ap.add_argument("--step", type=int, default=1,
+                    help="SimConfig.step_voxels (REF's march mode for > 1, trace.cpp:116-134; "
+                         "the paper's production setting is 2-3, PAPER.md:920-933)")
     args = ap.parse_args()
     args.photons = int(args.photons)
     if args.impl == "reference":

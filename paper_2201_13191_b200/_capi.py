@@ -354,6 +354,23 @@ SIGNATURES = {
 }
 
 
+def _preload_nccl():
+    """libxscatgpu.so links libnccl.so.2 (its multi-GPU entry points).  When
+    PyTorch's newer NCCL wheel is installed, load that one first: the process
+    then holds a single NCCL that both libxscatgpu and torch (imported before
+    or after) resolve against."""
+    try:
+        import importlib.util
+        spec = importlib.util.find_spec("nvidia.nccl")
+        for d in (spec.submodule_search_locations or []) if spec else []:
+            p = pathlib.Path(d) / "lib" / "libnccl.so.2"
+            if p.exists():
+                C.CDLL(str(p), mode=C.RTLD_GLOBAL)
+                return
+    except Exception:
+        pass
+
+
 def lib():
     """Load libxscatgpu.so (fails loudly when it has not been built)."""
     global _lib
@@ -361,6 +378,7 @@ def lib():
         if not LIB_PATH.exists():
             raise I.XscatError(f"CUDA library missing: {LIB_PATH} (run `make` or "
                                "__graft_entry__.build())")
+        _preload_nccl()
         L = C.CDLL(str(LIB_PATH))
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(L, name)

@@ -674,7 +674,7 @@ void accumulate(xs_context* c, const xs_geometry& g, int angle, const xs_spectru
     P.grab = c->grab;
     P.status = c->status.p;
 
-    if (c->engine == 1 && cfg.step_voxels <= 1) { // wavefront engine (wavefront.cu)
+    if (c->engine == 1) { // wavefront engine (wavefront.cu)
         uint32_t n_slots = c->wave_slots;
         if (cfg.track_variance) {
             const uint64_t cap = (uint64_t)cfg.splitting * (uint64_t)cfg.max_interactions;

@@ -318,7 +318,11 @@ __device__ __forceinline__ void load_mu(const WaveRays& R, uint32_t i, MuTab<FMT
 }
 
 // ------------------------------------------------------------------ set-up
-template <int FMT, bool REG, bool SKIP>
+// MARCH (step_voxels > 1, REF trace.cpp:116-134): scoring rays are midpoint
+// marches; their walker state is the origin (tn planes), the direction (dt
+// planes), t0, t1 and the sample count (vox plane 1), flagged 128.  Free paths
+// are always exact Siddon walks (REF trace.cpp:189-230).
+template <int FMT, bool REG, bool SKIP, bool MARCH>
 __global__ void __launch_bounds__(kBlock, XSW_SETUP_MINB) wave_setup(const __grid_constant__ TransportParams P,
                                                      const __grid_constant__ WaveArgs A)
 {
@@ -356,7 +360,7 @@ __global__ void __launch_bounds__(kBlock, XSW_SETUP_MINB) wave_setup(const __gri
             __stcs(&R.pre[i], score_setup(P, S, pix, o, to_det, e_out, st));
             if (tab.energy != e_out) // REF trace_attenuation builds MuField(e_out)
                 tab.fill_impl(P, e_out, st, S.bin);
-            walking = walk_begin_impl<FMT, SKIP>(P, w, o, to_det, CUDART_INF, false, st, S.bin);
+            walking = walk_begin_impl<FMT, SKIP>(P, w, o, to_det, CUDART_INF, MARCH, st, S.bin);
             ++c_rays;
         } else { // REF trace.cpp:189-230
             const Slot& S = A.slots[in.free[i - n_s]];
@@ -374,6 +378,18 @@ __global__ void __launch_bounds__(kBlock, XSW_SETUP_MINB) wave_setup(const __gri
         __stcs(&R.t[i], w.t);
         __stcs(&R.texit[i], w.texit);
         __stcs(&R.target[i], w.target);
+        if (MARCH && w.march) {
+            __stcs(&R.tn[i], w.ox);
+            __stcs(&R.tn[R.cap + i], w.oy);
+            __stcs(&R.tn[2ull * R.cap + i], w.oz);
+            __stcs(&R.dt[i], w.rx);
+            __stcs(&R.dt[R.cap + i], w.ry);
+            __stcs(&R.dt[2ull * R.cap + i], w.rz);
+            __stcs(&R.vox[R.cap + i], w.iy); // samples
+            R.flags[i] = (uint8_t)(64 | 128);
+            store_mu(R, i, tab);
+            continue;
+        }
         __stcs(&R.tn[i], w.tnx);
         __stcs(&R.tn[R.cap + i], w.tny);
         __stcs(&R.tn[2ull * R.cap + i], w.tnz);
@@ -397,7 +413,7 @@ __global__ void __launch_bounds__(kBlock, XSW_SETUP_MINB) wave_setup(const __gri
 }
 
 // -------------------------------------------------------------------- walk
-template <int FMT, bool REG, bool SKIP>
+template <int FMT, bool REG, bool SKIP, bool MARCH>
 __global__ void __launch_bounds__(kBlock, SKIP ? XSW_WALK_BLOCKS : XSW_EXACT_BLOCKS) wave_walk(const __grid_constant__ TransportParams P,
                                                     const __grid_constant__ WaveArgs A)
 {
@@ -459,8 +475,32 @@ __global__ void __launch_bounds__(kBlock, SKIP ? XSW_WALK_BLOCKS : XSW_EXACT_BLO
                 const uint32_t r = base + (uint32_t)__popc(idle & lt_mask);
                 if (r < n) {
                     const uint8_t f = R.flags[r];
-                    if (f & 64) {
+                    if (MARCH && (f & 128)) { // REF trace.cpp:116-134
                         ray = r;
+                        w.march = 1;
+                        w.t = __ldcs(&R.t[r]);
+                        w.texit = __ldcs(&R.texit[r]);
+                        w.target = __ldcs(&R.target[r]);
+                        w.ox = __ldcs(&R.tn[r]);
+                        w.oy = __ldcs(&R.tn[R.cap + r]);
+                        w.oz = __ldcs(&R.tn[2ull * R.cap + r]);
+                        w.rx = __ldcs(&R.dt[r]);
+                        w.ry = __ldcs(&R.dt[R.cap + r]);
+                        w.rz = __ldcs(&R.dt[2ull * R.cap + r]);
+                        w.ix = 0;
+                        w.iy = __ldcs(&R.vox[R.cap + r]);
+                        w.dtx = P.march_h;
+                        load_mu(R, r, tab);
+                        w.depth = 0.0;
+                        w.hit = 0;
+                        w.steps = 0;
+                        w.skipped = 0;
+                        w.ucells = 0;
+                        walking = true;
+                    } else if (f & 64) {
+                        ray = r;
+                        if (MARCH)
+                            w.march = 0;
                         w.t = __ldcs(&R.t[r]);
                         w.texit = __ldcs(&R.texit[r]);
                         w.target = __ldcs(&R.target[r]);
@@ -807,26 +847,32 @@ struct WaveSet {
     WaveFn setup, walk, event;
 };
 
-template <int FMT, bool REG, bool SKIP>
+template <int FMT, bool REG, bool SKIP, bool MARCH>
 WaveSet wave_set()
 {
-    return {wave_setup<FMT, REG, SKIP>, wave_walk<FMT, REG, SKIP>, wave_event<FMT>};
+    return {wave_setup<FMT, REG, SKIP, MARCH>, wave_walk<FMT, REG, SKIP, MARCH>, wave_event<FMT>};
 }
 
-WaveSet wave_kernels_for(const TransportParams& P)
+template <bool MARCH>
+WaveSet wave_kernels_m(const TransportParams& P)
 {
     const bool skip = P.skip != 0 && P.G.ubit != 0;
     if (P.G.fmt == kFmtP4) {
         if (use_reg_w(P))
-            return skip ? wave_set<kFmtP4, true, true>() : wave_set<kFmtP4, true, false>();
-        return skip ? wave_set<kFmtP4, false, true>() : wave_set<kFmtP4, false, false>();
+            return skip ? wave_set<kFmtP4, true, true, MARCH>() : wave_set<kFmtP4, true, false, MARCH>();
+        return skip ? wave_set<kFmtP4, false, true, MARCH>() : wave_set<kFmtP4, false, false, MARCH>();
     }
     if (P.G.fmt == kFmtP8) {
         if (use_reg_w(P))
-            return skip ? wave_set<kFmtP8, true, true>() : wave_set<kFmtP8, true, false>();
-        return skip ? wave_set<kFmtP8, false, true>() : wave_set<kFmtP8, false, false>();
+            return skip ? wave_set<kFmtP8, true, true, MARCH>() : wave_set<kFmtP8, true, false, MARCH>();
+        return skip ? wave_set<kFmtP8, false, true, MARCH>() : wave_set<kFmtP8, false, false, MARCH>();
     }
-    return wave_set<kFmtRaw, false, false>();
+    return wave_set<kFmtRaw, false, false, MARCH>();
+}
+
+WaveSet wave_kernels_for(const TransportParams& P)
+{
+    return P.step_voxels > 1 ? wave_kernels_m<true>(P) : wave_kernels_m<false>(P);
 }
 
 template <class T>

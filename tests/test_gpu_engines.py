@@ -128,3 +128,30 @@ def test_wide_four_bit_palette_on_the_voxel_walk(orc):
     assert np.array_equal(out[0].variance, out[1].variance)
     assert out[0].ledger == out[1].ledger
     _replay_compare(out[1], orc.simulate_scatter_stats(ph, g, 1, spec, resp, cfg))
+
+
+@pytest.mark.parametrize("kind", ["p4reg", "p8", "raw"])
+@pytest.mark.parametrize("step", [2, 3])
+def test_march_mode_on_the_wavefront_engine(orc, kind, step):
+    """REF's march mode (step_voxels > 1, trace.cpp:116-134: the scoring rays
+    are midpoint samples, free paths stay exact Siddon walks) on the
+    wavefront engine: bit-identical to the megakernel, replayed against the
+    oracle."""
+    ph = _phantom(kind)
+    g = I.make_circular_geometry(100.0, 60.0, 32, 24, 0.8, 4)
+    spec, resp = I.kramers_spectrum(150.0), I.detector_response()
+    cfg = I.SimConfig(photons_total=20000, splitting=5, seed=606 + step, step_voxels=step,
+                      roulette_wmin_rel=2.0, roulette_survival=0.6, track_variance=True)
+    ctx = X.projector.Context(0)
+    proj = X.Projector(ph, resp, ctx=ctx)
+    out = {}
+    for engine in (0, 1):
+        ctx.set_option("engine", engine)
+        out[engine] = proj.scatter_stats(g, 2, spec, cfg)
+        assert out[engine].stats["engine"] == engine
+    a, b = out[0], out[1]
+    assert np.array_equal(a.image, b.image) and np.array_equal(a.variance, b.variance)
+    assert a.total == b.total and a.ledger == b.ledger
+    for k in ("free_path_steps", "scoring_steps", "scoring_rays", "interactions"):
+        assert a.stats[k] == b.stats[k], k
+    _replay_compare(b, orc.simulate_scatter_stats(ph, g, 2, spec, resp, cfg))
