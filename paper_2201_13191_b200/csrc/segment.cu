@@ -349,20 +349,26 @@ __global__ void __launch_bounds__(kThr) phantom_scan(const uint8_t* __restrict__
                                                      ScanArgs S, SegCtl* ctl)
 {
     unsigned long long last = kEmpty;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < S.n; i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint8_t id = ids[i];
-        const float d = dens[i];
-        if (!voxel_ok(id, d, S)) {
-            atomicMin(&ctl->first_bad, (unsigned long long)i);
-            continue;
+    // warp-uniform trip count: the key matching below runs with every lane of
+    // the warp at the same loop iteration (full mask, no __activemask())
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u); i0 < S.n; i0 += stride) {
+        const uint64_t i = i0 + (threadIdx.x & 31u);
+        unsigned long long key = kEmpty; // (never a real key: ids are < 2^8)
+        if (i < S.n) {
+            const uint8_t id = ids[i];
+            const float d = dens[i];
+            if (!voxel_ok(id, d, S))
+                atomicMin(&ctl->first_bad, (unsigned long long)i);
+            else
+                key = ((unsigned long long)id << 32) | __float_as_uint(d);
         }
-        const unsigned long long key = ((unsigned long long)id << 32) | __float_as_uint(d);
-        if (key == last)
-            continue;
-        last = key;
+        const bool fresh = key != kEmpty && key != last;
+        if (key != kEmpty)
+            last = key;
         // one insert per distinct key of the warp
-        const unsigned m = __match_any_sync(__activemask(), key);
-        if ((threadIdx.x & 31) == __ffs(m) - 1)
+        const unsigned m = __match_any_sync(0xffffffffu, fresh ? key : kEmpty);
+        if (fresh && (threadIdx.x & 31) == __ffs(m) - 1)
             pair_insert(ctl, key);
     }
 }
