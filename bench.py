@@ -319,21 +319,61 @@ def gpu_arm(args):
                        "xs_simulate_scatter_stats_mgpu with a host image: this rank's photon "
                        "batch, ncclReduce, finalize, image D2H on rank 0"}
 
+    # ---------------- per-kernel device times of one projection, untimed: one
+    # pipeline (the two pipelines' kernels overlap, so their summed event
+    # intervals are not kernel durations) with CUDA events around every
+    # kernel of every wave (XSCAT_KTIME, on the launching streams)
+    kernels = None
+    if rank == 0 and not args.no_ktime:
+        os.environ["XSCAT_KTIME"] = "1"
+        ctx.set_option("wave_pipes", 1)
+        proj.scatter_stats(g, 0, spec, cfg)
+        ks = proj.scatter_stats(g, 0, spec, cfg).stats
+        ctx.set_option("wave_pipes", 2)
+        del os.environ["XSCAT_KTIME"]
+        names = ("setup_ms", "walk_ms", "score_ms", "event_ms", "admit_ms")
+        tot = sum(ks[k] for k in names)
+        kernels = {"pipelines": 1, "transport_ms": ks["kernel_ms"],
+                   **{k: ks[k] for k in names},
+                   "shares": {k[:-3]: ks[k] / tot for k in names},
+                   "walk_iterations_per_history": ks["walk_iterations"] / ks["histories"],
+                   "walk_lane_occupancy": ks["walk_iterations"] / max(1, ks["walk_lane_slots"]),
+                   "uniform_block_share": ks["uniform_iterations"] / max(1, ks["walk_iterations"])}
+
     if rank == 0:
         hbm, kind = peaks()
         steps_vox = (last or {}).get("free_path_steps", 0) + (last or {}).get("scoring_steps", 0)
         alg_bytes = 5.0 * steps_vox  # REF voxel layout: u8 id + f32 density per visit
         # dominant kernel = the walk (every voxel visit happens there): its
-        # summed device time over the projection's waves, CUDA events on the
-        # launching stream (xs_last_launch_stats.walk_ms)
-        achieved = alg_bytes / (walk_ms_max / 1e3) / 1e9 if walk_ms_max > 0 else 0.0
-        traffic = None
+        # device time over the projection's waves, CUDA events on the launching
+        # stream -- from the one-pipeline pass (a kernel duration); else the
+        # timed two-pipeline sum (inflated by the overlap)
+        walk_s = (kernels["walk_ms"] if kernels else walk_ms_max) / 1e3
+        achieved = alg_bytes / walk_s / 1e9 if walk_s > 0 else 0.0
+        traffic, prof = None, {}
         tp = ROOT / "profiles" / "bench_kernel_ncu.json"
         if tp.exists():
             try:
-                traffic = json.loads(tp.read_text()).get("walk_dram_bytes_per_projection")
+                prof = json.loads(tp.read_text())
+                traffic = prof.get("walk_dram_bytes_per_projection")
             except Exception:
-                traffic = None
+                prof = {}
+        # the walk is issue-bound: warp instructions per iteration and issue
+        # utilisation from the committed ncu capture of the same kernel, the
+        # iteration count from this run (device counters)
+        issue = None
+        if kernels and prof.get("walk_warp_instructions_per_warp_iteration"):
+            it = kernels["walk_iterations_per_history"] * n_hist
+            warp_it = it / max(kernels["walk_lane_occupancy"], 1e-9) / 32.0
+            wi = warp_it * prof["walk_warp_instructions_per_warp_iteration"]
+            clk = (clocks.get("sm_mhz") or prof.get("sm_mhz") or 1965.0) * 1e6
+            peak_issue = 148 * 4 * clk  # warp instructions per second (4 schedulers / SM)
+            issue = {"achieved_warp_inst_per_s": wi / walk_s, "peak_warp_inst_per_s": peak_issue,
+                     "frac": wi / walk_s / peak_issue,
+                     "warp_instructions_per_warp_iteration": prof["walk_warp_instructions_per_warp_iteration"],
+                     "ncu_issue_active": prof.get("walk_issue_active_pct"),
+                     "note": "walk warp instructions = device-counted iterations / lane occupancy / 32 "
+                             "x instructions per warp iteration (ncu, profiles/bench_kernel_ncu.json)"}
         cpu = None
         if ws == 1 and not args.no_cpu:
             try:
@@ -359,14 +399,20 @@ def gpu_arm(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic,
                          "peak_kind": kind,
-                         "kernel": "wave_walk (summed over the projection's waves)",
+                         "kernel": "wave_walk (every wave of one projection, one pipeline)",
                          "algorithmic_bytes_per_projection": alg_bytes,
                          "voxel_visits_per_projection": steps_vox,
-                         "walk_ms": walk_ms_max, "transport_ms": kernel_ms_max,
-                         "note": "5 B per REF voxel visit (u8 id + f32 density) / walk-kernel "
-                                 "time; traffic = ncu DRAM bytes of the same walk launches. The "
-                                 "device grid is an 8-bit palette (1 B/voxel) with uniform "
-                                 "blocks crossed without loads, so the walk is issue-bound"},
+                         "walk_ms": walk_s * 1e3, "walk_ms_two_pipelines_summed": walk_ms_max,
+                         "transport_ms": kernel_ms_max,
+                         "kernels": kernels,
+                         "issue": issue,
+                         "walker_state_dram_share": prof.get("walker_state_dram_share"),
+                         "note": "5 B per REF voxel visit (u8 id + f32 density, SURVEY.md 8(d)) / "
+                                 "walk-kernel time; traffic = ncu DRAM bytes of the same walk "
+                                 "launches, mostly walker-state streaming. The device grid is an "
+                                 "8-bit palette (1 B/voxel) with uniform blocks crossed without "
+                                 "loads, so the REF byte model does not bind: the walk is "
+                                 "issue-bound (see 'issue')"},
             "cpu_baseline": cpu,
             "clocks": clocks,
             "wall_s": wall,
@@ -454,6 +500,7 @@ def main():
     ap.add_argument("--photons", type=float, default=1e8)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-ktime", action="store_true", help="skip the untimed per-kernel timing pass")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-seconds", type=float, default=10.0)
     ap.add_argument("--workload", default="c3", choices=["c3", "c4"],
