@@ -95,7 +95,7 @@ struct WarpQ {
 // per-warp shared memory: slots, header, scoring + free-path FIFOs (8-aligned)
 __host__ __device__ inline size_t warp_bytes_of(int H, int qlen)
 {
-    return ((size_t)H * sizeof(Slot) + sizeof(WarpHdr) + (size_t)(qlen + kFreeQ) * 4 + 7) & ~(size_t)7;
+    return ((size_t)H * sizeof(Slot) + sizeof(WarpHdr) + (size_t)(qlen + kFreeQ) * 4 + 15) & ~(size_t)15;
 }
 
 // =================================================================== kernel
@@ -115,7 +115,8 @@ __global__ void __launch_bounds__(kBlock, XSD_MIN_BLOCKS) transport_kernel(const
     B.ledger = B.bins + 8 * P.n_bins;
     B.diag = B.ledger + 24;
     uint64_t* sstart = reinterpret_cast<uint64_t*>(B.diag + 8);
-    unsigned char* p = reinterpret_cast<unsigned char*>(sstart + P.n_bins + 1);
+    // (slots are 16-byte aligned: Slot is read and written with 16-byte accesses)
+    unsigned char* p = reinterpret_cast<unsigned char*>(sstart + P.n_bins + 1 + ((P.n_bins + 1) & 1));
     const size_t warp_bytes = warp_bytes_of(H, P.queue_len);
     unsigned char* wbase = p + (size_t)warp * warp_bytes;
     Slot* slots = reinterpret_cast<Slot*>(wbase);
@@ -307,7 +308,7 @@ size_t transport_smem_bytes(const TransportParams& P)
 {
     const size_t warp_bytes = warp_bytes_of(P.slots_per_warp, P.queue_len);
     const int n_tab = P.G.fmt == kFmtP4 ? P.n_pal : P.n_mats;
-    return (size_t)(8 * P.n_bins + 32) * 8 + (size_t)(P.n_bins + 1) * 8 + kWarps * warp_bytes +
+    return (size_t)(8 * P.n_bins + 32) * 8 + (size_t)(P.n_bins + 2) * 8 + kWarps * warp_bytes +
            (use_reg(P) ? 0 : (size_t)n_tab * kBlock * 8);
 }
 

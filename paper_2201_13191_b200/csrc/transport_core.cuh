@@ -10,6 +10,7 @@
 // so both engines run the identical arithmetic per history.
 #pragma once
 #include <cmath>
+#include <cstddef>
 
 #include "physics.cuh"
 
@@ -30,7 +31,7 @@ struct SlotRng {
     uint32_t photon, bin, block, pos, b0, b1, b2, b3;
 };
 
-struct __align__(8) Slot {
+struct __align__(16) Slot { // (16: the wavefront admission writes it with 16-byte stores)
     double px, py, pz, dx, dy, dz; // photon position (= last interaction point) / direction
     double E, W, wmin, target;     // energy, weight, roulette floor, -ln u of the pending free path
     double ix, iy, iz;             // incoming direction at it
@@ -42,6 +43,10 @@ struct __align__(8) Slot {
     int32_t pending;               // queued/in-flight scoring rays + 1 while alive
     int32_t n_var;                 // variance scratch entries
 };
+
+static_assert(sizeof(Slot) == 208 && offsetof(Slot, T) == 128 && offsetof(Slot, rng) == 152 &&
+                  offsetof(Slot, bin) == 184 && offsetof(Slot, pending) == 200,
+              "history_start's 16-byte stores assume this Slot layout");
 
 // Philox4x32-10 block for counter {block, photon, bin, angle} and key
 // {k0, k1} (REF rng.hpp:29-60).
@@ -950,24 +955,44 @@ __device__ __noinline__ double history_start(const TransportParams& P, const Blo
     const double cos_psi = -dot(dir, v3(P.normal[0], P.normal[1], P.normal[2]));
     const double em_weight = P.det_area * cos_psi / d2;
     const double w0 = __ldg(P.bin_weight + bin) * em_weight / (double)__ldg(P.bin_count + bin);
-    S.px = src.x;
-    S.py = src.y;
-    S.pz = src.z;
-    S.dx = dir.x;
-    S.dy = dir.y;
-    S.dz = dir.z;
-    S.E = __ldg(P.bin_energy + bin);
-    S.W = w0;
-    S.wmin = P.wmin_rel * w0;
-    S.T[0] = S.T[1] = S.T[2] = 0ull;
-    S.bin = bin;
-    S.gen = 0;
-    S.pending = 1;
-    S.n_var = 0;
+    const double E = __ldg(P.bin_energy + bin);
     if (tally_w0)
         ledger_add(P, B, 0, w0, st, bin);
-    S.target = -nl_log(slot_uniform(&rng, P.k0, P.k1, P.angle));
-    S.rng = rng;
+    const double target_mfp = -nl_log(slot_uniform(&rng, P.k0, P.k1, P.angle));
+    if constexpr (Q::kBatchScores) {
+        // global slot (wavefront engine): the fields this writes, as 16-byte
+        // stores (a warp's scattered slots cost one L1 wavefront per lane per
+        // store instruction; the interaction record ix..pref is left alone)
+        double2* q = reinterpret_cast<double2*>(&S);
+        q[0] = make_double2(src.x, src.y);
+        q[1] = make_double2(src.z, dir.x);
+        q[2] = make_double2(dir.y, dir.z);
+        q[3] = make_double2(E, w0);
+        q[4] = make_double2(P.wmin_rel * w0, target_mfp);
+        uint4* u = reinterpret_cast<uint4*>(&S.T[0]);
+        u[0] = make_uint4(0u, 0u, 0u, 0u);                                   // T[0], T[1]
+        u[1] = make_uint4(0u, 0u, rng.photon, rng.bin);                       // T[2], rng
+        u[2] = make_uint4(rng.block, rng.pos, rng.b0, rng.b1);
+        u[3] = make_uint4(rng.b2, rng.b3, (uint32_t)bin, 0u);                 // ..., bin, gen
+        u[4] = make_uint4(0u, 0u, 1u, 0u); // kind, mat (set by the interaction), pending, n_var
+    } else {
+        S.px = src.x;
+        S.py = src.y;
+        S.pz = src.z;
+        S.dx = dir.x;
+        S.dy = dir.y;
+        S.dz = dir.z;
+        S.E = E;
+        S.W = w0;
+        S.wmin = P.wmin_rel * w0;
+        S.T[0] = S.T[1] = S.T[2] = 0ull;
+        S.bin = bin;
+        S.gen = 0;
+        S.pending = 1;
+        S.n_var = 0;
+        S.target = target_mfp;
+        S.rng = rng;
+    }
     qs.push_free(s);
     qs.claim(s);
     return w0;

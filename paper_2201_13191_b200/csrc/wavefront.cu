@@ -186,7 +186,11 @@ struct GlobalQ {
         }
         ctl->free_stack[atomicAdd(&ctl->free_top, 1)] = (uint32_t)s;
     }
-    __device__ __forceinline__ void fence() const { __threadfence(); }
+    // (end_history's hand-off: in the wavefront engine only the event kernel
+    // ends histories through it, one event per history per launch, and the
+    // finalizer of a history it does not end runs in a later launch; kernel
+    // boundaries order the writes, so no fence is needed)
+    __device__ __forceinline__ void fence() const {}
     // statistics straight into the block's shared accumulators (folding them
     // per warp at the flush points, like the pushes, measured slower: event
     // kernel 58 -> 67 ms per C3 projection)
@@ -263,13 +267,19 @@ __device__ __forceinline__ uint64_t var_base_of(const TransportParams& P, int s)
 
 // Shared-memory statistics of a block (bins, ledger, diagnostics), flushed to
 // the global accumulator when the block ends.
+// Layout: bins (8 per bin), diag (8), then one 24-word ledger per warp: every
+// history end adds to a ledger word, and 64-bit shared atomics are
+// compare-and-swap loops, so per-warp copies keep the contention inside a warp.
+constexpr int kStatWarps = kBlock / 32;
+__host__ __device__ constexpr size_t stat_words(int n_bins) { return 8 * (size_t)n_bins + 8 + 24 * kStatWarps; }
+
 __device__ __forceinline__ Block block_stats(const TransportParams& P, unsigned long long* smem)
 {
     Block B;
     B.bins = smem;
-    B.ledger = B.bins + 8 * P.n_bins;
-    B.diag = B.ledger + 24;
-    for (int i = threadIdx.x; i < 8 * P.n_bins + 32; i += blockDim.x)
+    B.diag = B.bins + 8 * P.n_bins;
+    B.ledger = B.diag + 8 + 24 * (threadIdx.x >> 5);
+    for (int i = threadIdx.x; i < (int)stat_words(P.n_bins); i += blockDim.x)
         B.bins[i] = 0ull;
     __syncthreads();
     return B;
@@ -281,9 +291,14 @@ __device__ __forceinline__ void flush_stats(const TransportParams& P, const Bloc
     for (int i = threadIdx.x; i < 8 * P.n_bins; i += blockDim.x)
         if (B.bins[i])
             red_add(P.accum + P.off_bins + i, B.bins[i]);
-    for (int i = threadIdx.x; i < 24; i += blockDim.x)
-        if (B.ledger[i])
-            red_add(P.accum + P.off_ledger + i, B.ledger[i]);
+    const unsigned long long* led = B.diag + 8; // every warp's ledger
+    for (int i = threadIdx.x; i < 24; i += blockDim.x) {
+        unsigned long long v = 0;
+        for (int w = 0; w < kStatWarps; ++w)
+            v += led[24 * w + i];
+        if (v)
+            red_add(P.accum + P.off_ledger + i, v);
+    }
     for (int i = threadIdx.x; i < 8; i += blockDim.x)
         if (B.diag[i])
             red_add(P.accum + P.off_diag + i, B.diag[i]);
@@ -705,11 +720,13 @@ __global__ void __launch_bounds__(kBlock, XSW_EVENT_MINB) wave_event(const __gri
         cont(cb, nc, false);
         cont(rb, nr, false);
     };
-    for (;;) {
-        uint32_t base = 0;
-        if (lane == 0)
-            base = atomicAdd(&ctl->ev_cursor, 32u);
-        base = __shfl_sync(kFull, base, 0) + n_s;
+    for (uint32_t base = 0, end = 0;; base += 32) {
+        if (base >= end) { // 4 warp-chunks per cursor reservation
+            if (lane == 0)
+                base = atomicAdd(&ctl->ev_cursor, 128u);
+            base = __shfl_sync(kFull, base, 0) + n_s;
+            end = base + 128u;
+        }
         if (base >= n)
             break;
         const uint32_t i = base + (uint32_t)lane;
@@ -781,7 +798,7 @@ __global__ void __launch_bounds__(kBlock, XSW_ADMIT_MINB) wave_admit(const __gri
         return;
     // the bin search of history_start runs on a shared-memory copy of the
     // bin offsets (after the block statistics)
-    uint64_t* sstart = reinterpret_cast<uint64_t*>(acc + 8 * P.n_bins + 32);
+    uint64_t* sstart = reinterpret_cast<uint64_t*>(acc + stat_words(P.n_bins));
     for (int i = threadIdx.x; i <= P.n_bins; i += blockDim.x)
         sstart[i] = P.bin_start[i];
     const Block B = block_stats(P, acc); // (synchronises)
@@ -1183,7 +1200,7 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
 
     const WaveSet K = wave_kernels_for(P);
     const size_t mu_smem = use_reg_w(P) ? 0 : (size_t)n_mu * kBlock * 8;
-    const size_t stat_smem = (size_t)(8 * P.n_bins + 32) * 8;
+    const size_t stat_smem = stat_words(P.n_bins) * 8;
     XSW_CHECK(cudaFuncSetAttribute((const void*)K.setup, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)std::max<size_t>(mu_smem, 1)));
     XSW_CHECK(cudaFuncSetAttribute((const void*)K.walk, cudaFuncAttributeMaxDynamicSharedMemorySize,
