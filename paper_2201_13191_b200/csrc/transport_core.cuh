@@ -151,14 +151,17 @@ __device__ __forceinline__ void rng_skip(SlotRng& r, uint32_t n, uint32_t k0, ui
 // mu table has the same energy knots (true for the reference's bundled data,
 // checked at upload) the knot search and log(e) are shared; the arithmetic
 // is that of tab_loglog (REF table.hpp:57-69), so values are identical.
+// When the knots differ (e.g. a material with an absorption edge), each table
+// gets its own knot search but log(e) is still computed once.
 struct SharedLog {
     int i;
-    bool exact, ok;
+    bool exact, ok, has_le;
     double le;
     __device__ __forceinline__ void init(const TransportParams& P, double e, DevStatus* st, int bin,
                                          bool enabled = true)
     {
         ok = false;
+        has_le = false;
         if (!P.shared_mu_grid || !enabled)
             return;
         const Tab t = mtab(P, P.mats[P.grid_mat].mu);
@@ -167,13 +170,36 @@ struct SharedLog {
             return;
         }
         le = exact ? 0.0 : nl_log(e);
+        has_le = !exact;
         ok = true;
     }
     __device__ __forceinline__ double eval(const TransportParams& P, TabDesc d, double e, DevStatus* st,
-                                           int bin) const
+                                           int bin)
     {
-        if (!ok)
-            return loglog_or_fail(P, d, e, st, bin);
+        if (!ok) { // tab_loglog (REF table.hpp:57-69) with the shared log(e)
+            const Tab t = mtab(P, d);
+            int j;
+            bool ex;
+            if (!tab_locate(t, e, j, ex)) {
+                raise(st, XS_E_OUT_OF_RANGE, kErrTableRange, bin, e, 0.0);
+                return 0.0;
+            }
+            if (ex)
+                return __ldg(t.y + j);
+            const double y0 = __ldg(t.y + j), y1 = __ldg(t.y + j + 1);
+            if (y0 <= 0.0 || y1 <= 0.0) {
+                const double x0 = __ldg(t.x + j), x1 = __ldg(t.x + j + 1);
+                const double u = (e - x0) / (x1 - x0);
+                return y0 + u * (y1 - y0);
+            }
+            if (!has_le) {
+                le = nl_log(e);
+                has_le = true;
+            }
+            const double lx0 = __ldg(t.lx + j), lx1 = __ldg(t.lx + j + 1);
+            const double u = (le - lx0) / (lx1 - lx0);
+            return nl_exp(__ldg(t.ly + j) + u * (__ldg(t.ly + j + 1) - __ldg(t.ly + j)));
+        }
         const Tab t = mtab(P, d);
         if (exact)
             return __ldg(t.y + i);
