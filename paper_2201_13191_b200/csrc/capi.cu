@@ -2213,6 +2213,16 @@ int xs_segment_to_scene(xs_context* c, const float* volume, const int32_t dims[3
         ph.n_materials = n_materials;
         ph.materials = materials;
         upload_phantom_impl(c, &ph, true);
+        if (const char* dir = std::getenv("XSCAT_DUMP_SCENE")) { // diagnostics: the segmented ids
+            static int k = 0;
+            std::vector<uint8_t> ids(n_out);
+            cuda_check(cudaMemcpy(ids.data(), c->seg_ids.p, n_out, cudaMemcpyDeviceToHost), "dump");
+            const std::string path = std::string(dir) + "/scene_" + std::to_string(k++) + ".u8";
+            if (FILE* f = std::fopen(path.c_str(), "wb")) {
+                std::fwrite(ids.data(), 1, n_out, f);
+                std::fclose(f);
+            }
+        }
     });
 }
 

@@ -97,3 +97,38 @@ def test_loop_errors():
     # a flat measurement: constant FDK volume -> Otsu fails inside the first iteration
     with pytest.raises(I.XscatError, match="iteration 1, stage segmentation: otsu: degenerate histogram"):
         X.run_iterative_correction(raw, np.ones((16, 16)), g, spec, resp, cfg, [w])
+
+
+def test_c5_shape_offset_input_clamps_match_reference(ref):
+    """Round 1's C5 input (primary + 3% of the flat field as "scatter") makes
+    the loop's first segmentation lose most of the body, and the smoothed /
+    up-sampled scatter of that phantom rings below zero: about 4.5% of the
+    pixels were clamped in iteration 1 at full size.  The reduced-size C5
+    (C3-shaped Al/Fe head at 128^3, 256^2, 90 views, MC 64^2 on every 2nd view)
+    through REF's own loop shows the same: the clamps come from the algorithm
+    on this input, not from the device.  Counts and statistics must agree."""
+    al, fe = I.material("aluminum"), I.material("iron")
+    n = 128
+    ph = S.make_cylinder_head_phantom(n, 12.8 / n, al, 2.699, fe, 7.874)
+    det = 256
+    from paper_2201_13191_b200 import configs
+    g = I.make_circular_geometry(configs.SDD, configs.SOD, det, det, configs.pitch(det), 90)
+    spec, resp = I.kramers_spectrum(150.0), I.detector_response()
+    proj = X.Projector(ph, resp)
+    raw = proj.run_scan(g, spec, I.SimConfig(), list(range(90)), X.PRIMARY).primary.images.copy()
+    empty = I.make_empty_phantom(n, n, n, ph.voxel_size, [al, fe])
+    flat = X.Projector(empty, resp).primary(g, 0, spec)
+    raw += 0.03 * flat
+    cfg = CorrectionConfig(n_iterations=2, simulate_every_kth_angle=2, mc_nu=64, mc_nv=64,
+                           recon_dims=(n, n, n), n_classes=3,
+                           class_map=[ClassSpec(0, 0.0), ClassSpec(1, 2.699), ClassSpec(2, 7.874)],
+                           sim=I.SimConfig(photons_total=100_000, splitting=10, seed=77))
+    dev = X.run_iterative_correction(X.ProjectionStack(g.angles, raw), flat, g, spec, resp, cfg, [al, fe])
+    vol, stack, reps = ref.run_iterative_correction(raw, flat, g, spec, resp, cfg, [al, fe])
+    for a, b in zip(dev.reports, reps):
+        print(a.iteration, a.negative_scatter_clamped, b.negative_scatter_clamped, a.mean_scatter_fraction,
+              b.mean_scatter_fraction)
+        assert abs(a.negative_scatter_clamped - b.negative_scatter_clamped) <= max(2, b.negative_scatter_clamped // 100)
+        assert a.mean_scatter_fraction == pytest.approx(b.mean_scatter_fraction, rel=1e-6)
+        assert a.ncc_to_previous == pytest.approx(b.ncc_to_previous, rel=1e-6)
+    assert reps[0].negative_scatter_clamped > 0.01 * raw.size  # the input's pathology, in REF too

@@ -7,12 +7,16 @@ B200 through xs_run_iterative_correction, every stage on the device.
   3 iterations.
 
 The measurement is synthesised on the device: the object's primary at 2048^2
-plus a smooth scatter-like offset (3% of the flat field).  Prints the
-per-iteration stage times (REF IterationReport) and, with --ref, REF's cost of
-the same stages on this host's cores from bounded samples, scaled by the
-operation count.
+plus its scatter, simulated by the projector itself at the MC grid (every 2nd
+view, 1e7 photons, split 10), SG-smoothed, angle-interpolated and up-sampled
+exactly as the loop does (so the loop's fixed point is the true object).
+--offset instead adds a flat 3% of the flat field as "scatter" (round 1's
+input: the loop then drifts to unphysical, speckled segmentations whose
+transport cannot skip uniform blocks).  Prints the per-iteration stage times
+(REF IterationReport) and, with --ref, REF's cost of the same stages on this
+host's cores from bounded samples, scaled by the operation count.
 
-usage: python tools/bench_loop.py [n_iterations] [--ref]
+usage: python tools/bench_loop.py [n_iterations] [--ref] [--offset]
 """
 import ctypes as C
 import json
@@ -31,6 +35,7 @@ from paper_2201_13191_b200.projector import ClassSpec, CorrectionConfig  # noqa:
 
 n_iter = int(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1].isdigit() else 3
 with_ref = "--ref" in sys.argv
+offset_scatter = "--offset" in sys.argv
 N_VIEWS, NU, MC, RECON = 720, 2048, 512, 512
 
 t_setup = time.time()
@@ -60,8 +65,34 @@ ctx.upload(empty, resp)
 flat = torch.empty((NU, NU), dtype=torch.float64, device="cuda")
 ctx.check(A.lib().xs_primary_device(ctx.h, C.byref(gp), 0, C.byref(sp), C.byref(simp), C.c_void_p(flat.data_ptr())))
 torch.cuda.synchronize()
-raw += 0.03 * flat  # scatter-like low-frequency offset
-torch.cuda.synchronize()
+if offset_scatter:
+    raw += 0.03 * flat  # scatter-like low-frequency offset (round 1's input)
+else:  # the object's own scatter, through the loop's post-processing chain
+    ctx.upload(ph, resp)
+    gm = I.make_circular_geometry(configs.SDD, configs.SOD, MC, MC, configs.pitch(MC), N_VIEWS)
+    gmp = pk.geometry(gm)
+    sub_idx = list(range(0, N_VIEWS, 2))
+    ssub = (C.c_int32 * len(sub_idx))(*sub_idx)
+    scat = torch.empty((len(sub_idx), MC, MC), dtype=torch.float64, device="cuda")
+    ctx.check(A.lib().xs_run_scan_device(ctx.h, C.byref(gmp), C.byref(sp), C.byref(simp), ssub, len(sub_idx), 1,
+                                         None, C.c_void_p(scat.data_ptr()), None))
+    win, order = X.default_sg_spec(MC, MC).window, X.default_sg_spec(MC, MC).polyorder
+    ctx.check(A.lib().xs_sg_smooth(ctx.h, C.c_void_p(scat.data_ptr()), C.c_void_p(scat.data_ptr()), MC, MC,
+                                   len(sub_idx), win, order, 1))
+    full = torch.empty((N_VIEWS, MC, MC), dtype=torch.float64, device="cuda")
+    src_a = np.ascontiguousarray(np.asarray(g.angles)[sub_idx])
+    tgt_a = np.ascontiguousarray(np.asarray(g.angles))
+    ctx.check(A.lib().xs_interpolate_angles(ctx.h, C.c_void_p(scat.data_ptr()), A.dptr(src_a), len(sub_idx),
+                                            C.c_void_p(full.data_ptr()), A.dptr(tgt_a), N_VIEWS, MC, MC, 1))
+    del scat
+    for v0 in range(0, N_VIEWS, 90):  # up-sample in slabs (24 GB at full size)
+        up = torch.empty((90, NU, NU), dtype=torch.float64, device="cuda")
+        ctx.check(A.lib().xs_upsample_image(ctx.h, C.c_void_p(full[v0:v0 + 90].data_ptr()), MC, MC, 90,
+                                            C.c_void_p(up.data_ptr()), NU, NU, 1))
+        raw[v0:v0 + 90] += up.clamp_(min=0.0)
+        del up
+    del full
+    torch.cuda.synchronize()
 setup_s = time.time() - t_setup
 
 mats = [None, al, fe]
@@ -78,7 +109,9 @@ torch.cuda.synchronize()
 total = time.time() - t0
 R = X.projector.reports_from(reps, n_iter)
 out = {"config": "C5: 720 x 2048^2 views, MC 512^2 on every 2nd view (360 x 1e7, split 10) + 720 primaries, "
-                 "recon 512^3, 3 classes", "n_iterations": n_iter, "loop_seconds": total,
+                 "recon 512^3, 3 classes", "measurement": "primary + 3% flat offset" if offset_scatter else
+                 "primary + the object's MC scatter through the loop's SG / interpolation / up-sampling",
+       "n_iterations": n_iter, "loop_seconds": total,
        "loop_seconds_incl_initial_ln_fbp": total, "setup_seconds": setup_s,
        "peak_mem_gb": torch.cuda.max_memory_allocated() / 2 ** 30,
        "reports": [r.__dict__ for r in R]}
