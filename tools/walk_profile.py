@@ -26,8 +26,8 @@ for r in csv.reader(open(launches)):
     if m in tot and "wave_walk" in d.get("Kernel Name", ""):
         v = float(d["Metric Value"].replace(",", ""))
         unit = d.get("Metric Unit", "")
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-6, "usecond": 1e-3,
-                 "msecond": 1.0}.get(unit, 1.0)
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-6, "ns": 1e-6,
+                 "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0}.get(unit, 1.0)
         tot[m] += v * scale
         n_launch.add(d["ID"])
 
@@ -59,8 +59,10 @@ res = {
     "walk_warps_active_pct": num("sm__warps_active.avg.pct_of_peak_sustained_active"),
     "walk_l2_hit_pct": num("lts__t_sector_hit_rate.pct"),
     "walk_registers": num("launch__registers_per_thread"),
-    "full_capture_duration_ms": num("gpu__time_duration.sum") / (1e3 if "usecond" in rows[1][rows[0].index("gpu__time_duration.sum")] else 1.0),
-    "full_capture_dram_read_bytes": num("dram__bytes_read.sum"),
+    "full_capture_duration_ms": num("gpu__time_duration.sum") * {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3,
+                                                                  "usecond": 1e-3}.get(rows[1][rows[0].index("gpu__time_duration.sum")], 1.0),
+    "full_capture_dram_read_bytes": num("dram__bytes_read.sum") * {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(
+        rows[1][rows[0].index("dram__bytes_read.sum")], 1.0),
 }
 # walker state read by the walk per ray: t, texit, target, tn x3, dt x3, rd x3, 4 mu (fp64),
 # 3 voxel indices (i32), flags (u8) = 141 B; rays per projection from the bench line if given
