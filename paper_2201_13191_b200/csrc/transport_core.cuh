@@ -636,9 +636,10 @@ __device__ __forceinline__ void bin_total_add(const TransportParams& P, const Bl
 
 // History end (REF run_history :225-241): bin statistics from the exact
 // fixed-point history total, per-pixel grouping for the variance, free slot.
+// release = false: the caller frees the slot itself.
 template <class Q>
 __device__ __noinline__ void finalize_history(const TransportParams& P, const Block& B, const Q qs, int s,
-                                              uint64_t var_base, DevStatus* st)
+                                              uint64_t var_base, DevStatus* st, bool release = true)
 {
     Slot& S = qs.slot(s);
     const double t = dequantize(S.T[0], S.T[1], S.T[2], P.log2_img);
@@ -670,7 +671,8 @@ __device__ __noinline__ void finalize_history(const TransportParams& P, const Bl
         }
     }
     qs.history_done(B);
-    qs.release(s);
+    if (release)
+        qs.release(s);
 }
 
 template <class Q>

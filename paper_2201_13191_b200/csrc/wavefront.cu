@@ -27,6 +27,8 @@
 // rays need, so the interaction record needs no double buffering.  Tallies
 // are the same fixed-point integers as the megakernel's, so both engines give
 // bit-identical images and statistics.
+#include <cuda/atomic>
+
 #include <algorithm>
 #include <cstdio>
 #include <unistd.h>
@@ -595,9 +597,11 @@ __global__ void __launch_bounds__(kBlock, XSW_SCORE_MINB) wave_score(const __gri
     const WaveQueue& in = ctl->q[A.cur];
     const uint32_t n_s = ctl->n_score;
     const Block B = block_stats(P, acc);
+    // the only push of this kernel is a finished history's slot, recorded here
+    // (no pointer to the record escapes: it stays in registers)
     Deferred def;
     deferred_reset(def);
-    const GlobalQ qs{A.slots, ctl, A.cur ^ 1, -1, &def};
+    const GlobalQ qs{A.slots, ctl, A.cur ^ 1, -1, nullptr};
     const WaveRays& R = A.R;
     DevStatus* st = P.status;
     const int lane = threadIdx.x & 31;
@@ -645,10 +649,14 @@ __global__ void __launch_bounds__(kBlock, XSW_SCORE_MINB) wave_score(const __gri
             sadd(&S.T[0], ((uint64_t)b0 << 16) + a0);
             sadd(&S.T[1], ((uint64_t)b1 << 16) + a1);
             sadd(&S.T[2], ((uint64_t)b2 << 16) + a2);
-            __threadfence(); // the slot's tallies / scratch before the hand-off
+            // hand-off: release this warp's tallies / scratch, and the last one
+            // to count down acquires every other warp's before finalizing
             const int cnt = __popc(grp);
-            if (atomicSub(&S.pending, cnt) == cnt)
-                finalize_history(P, B, qs, s, var_base_of(P, s), st);
+            cuda::atomic_ref<int, cuda::thread_scope_device> pending(S.pending);
+            if (pending.fetch_sub(cnt, cuda::memory_order_acq_rel) == cnt) {
+                finalize_history(P, B, qs, s, var_base_of(P, s), st, false);
+                def.rel_slot = s;
+            }
         }
         __syncwarp();
         flush_deferred(P, B, ctl, A.cur ^ 1, def, A.n_slots, P.status);
