@@ -225,6 +225,18 @@ int xs_run_scan_mgpu(xs_context* c, const xs_geometry* g, const xs_spectrum* spe
         };
         int my0, my1;
         share(cm->rank, my0, my1);
+        if (!gather || cm->n == 1) { // no exchange: this rank's range through xs_run_scan
+            // (its D2H and host copies overlap the next angle's transport)
+            if (my1 <= my0)
+                return;
+            const int st = xs_run_scan(c, g, spec, cfg, subset + my0, my1 - my0, what,
+                                       primary_out ? primary_out + (size_t)my0 * np : nullptr,
+                                       scatter_out ? scatter_out + (size_t)my0 * np : nullptr,
+                                       seconds ? seconds + my0 : nullptr);
+            if (st != XS_OK)
+                fail(st, "%s", xs_last_error(c));
+            return;
+        }
         // rounds of up to kChunk angles per rank: compute on the device, copy this
         // rank's images out, then (gather) the root receives the round's images of
         // every other rank

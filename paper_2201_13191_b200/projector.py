@@ -229,14 +229,21 @@ class Projector:
 
     def run_scan_mgpu(self, g: I.ScanGeometry, spec: I.Spectrum, cfg: I.SimConfig,
                       angle_subset: Sequence[int], what: int = BOTH, gather: bool = True,
-                      root: int = 0) -> ScanResult:
+                      root: int = 0, primary_out: Optional[np.ndarray] = None,
+                      scatter_out: Optional[np.ndarray] = None) -> ScanResult:
         """xs_run_scan_mgpu: this rank's angle range (all of them on the root
-        with gather)."""
+        with gather).  primary_out / scatter_out: caller-owned (n, nv, nu)
+        float64 arrays to fill (reused across calls), else allocated here."""
         pk = A.Packed()
         sub = np.ascontiguousarray(np.asarray(angle_subset, dtype=np.int32))
         n = int(sub.size)
-        prim = np.zeros((max(n, 1), g.nv, g.nu)) if what != SCATTER else None
-        scat = np.zeros((max(n, 1), g.nv, g.nu)) if what != PRIMARY else None
+        prim = scat = None
+        if what != SCATTER:
+            prim = primary_out if primary_out is not None else np.zeros((max(n, 1), g.nv, g.nu))
+        if what != PRIMARY:
+            scat = scatter_out if scatter_out is not None else np.zeros((max(n, 1), g.nv, g.nu))
+        for a in (prim, scat):
+            assert a is None or (a.dtype == np.float64 and a.flags.c_contiguous and a.size >= n * g.nu * g.nv)
         secs = np.zeros(max(n, 1))
         self.ctx.check(A.lib().xs_run_scan_mgpu(
             self.ctx.h, C.byref(pk.geometry(g)), C.byref(pk.spectrum(spec)),

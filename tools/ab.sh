@@ -5,4 +5,5 @@
 set -e
 name=$1; shift
 make -j16 lib OBJDIR=build_ab/$name/obj LIBDIR=build_ab/$name NVEXTRA="$*" > build_ab/$name.log 2>&1 || { mkdir -p build_ab; make -j16 lib OBJDIR=build_ab/$name/obj LIBDIR=build_ab/$name NVEXTRA="$*"; }
+rm -rf build_ab/$name/obj
 echo build_ab/$name/libxscatgpu.so

@@ -8,4 +8,5 @@ tmp=$(mktemp -d)
 git worktree add -q --detach $tmp $rev
 make -C $tmp -j16 lib OBJDIR=$root/build_ab/$name/obj LIBDIR=$root/build_ab/$name NVEXTRA="$*" > $root/build_ab/$name.log 2>&1
 git worktree remove --force $tmp
+rm -rf build_ab/$name/obj
 echo build_ab/$name/libxscatgpu.so
