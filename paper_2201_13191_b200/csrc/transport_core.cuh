@@ -127,6 +127,30 @@ __device__ __forceinline__ double rng_uniform_at(const SlotRng& r, uint32_t j, u
     return (k & 1) ? words_to_uniform(o2, o3) : words_to_uniform(o0, o1);
 }
 
+// Draws j and j + 1 (a scoring ray's pixel, REF run_history :162-164): one
+// Philox block when both lie in the same block, two otherwise.
+__device__ __forceinline__ void rng_pair_at(const SlotRng& r, uint32_t j, uint32_t k0, uint32_t k1, uint32_t angle,
+                                            double& u0, double& u1)
+{
+    const uint32_t m0 = (4u - r.pos) >> 1; // draws left in the buffered block
+    uint32_t w[4];                         // the block holding draw j (its words)
+    uint32_t q;                            // j's word offset in it (0 or 2)
+    if (j < m0) {
+        w[0] = r.b0, w[1] = r.b1, w[2] = r.b2, w[3] = r.b3;
+        q = r.pos + 2 * j;
+    } else {
+        const uint32_t k = j - m0;
+        philox_block(r.block + (k >> 1), r.photon, r.bin, angle, k0, k1, w[0], w[1], w[2], w[3]);
+        q = (k & 1) ? 2u : 0u;
+    }
+    u0 = q == 0 ? words_to_uniform(w[0], w[1]) : words_to_uniform(w[2], w[3]);
+    if (q == 0) { // j + 1 is the block's second draw
+        u1 = words_to_uniform(w[2], w[3]);
+        return;
+    }
+    u1 = rng_uniform_at(r, j + 1, k0, k1, angle); // j + 1 starts the next block
+}
+
 // Advance the stream past n draws (the state slot_uniform would leave).
 __device__ __forceinline__ void rng_skip(SlotRng& r, uint32_t n, uint32_t k0, uint32_t k1, uint32_t angle)
 {

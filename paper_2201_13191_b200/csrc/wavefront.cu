@@ -369,8 +369,9 @@ __global__ void __launch_bounds__(kBlock, XSW_SETUP_MINB) wave_setup(const __gri
             const uint32_t b = i / (uint32_t)P.splitting, k = i - b * (uint32_t)P.splitting;
             const ScoreBatch& sb = in.batch[b];
             const Slot& S = A.slots[sb.slot];
-            const uint32_t pix = score_pixel(P, rng_uniform_at(sb.rng, 2 * k, P.k0, P.k1, P.angle),
-                                             rng_uniform_at(sb.rng, 2 * k + 1, P.k0, P.k1, P.angle));
+            double uu, uv;
+            rng_pair_at(sb.rng, 2 * k, P.k0, P.k1, P.angle, uu, uv);
+            const uint32_t pix = score_pixel(P, uu, uv);
             __stcs(&R.pix[i], pix);
             V3 o, to_det;
             double e_out;
