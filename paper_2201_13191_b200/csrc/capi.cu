@@ -945,7 +945,7 @@ int xs_ctx_create(int32_t device, xs_context** out)
         if (const char* e = std::getenv("XSCAT_ENGINE"))
             c->engine = std::atoi(e) != 0;
         if (const char* e = std::getenv("XSCAT_WAVE_PIPES"))
-            c->wave_pipes = std::max(1, std::min(2, std::atoi(e)));
+            c->wave_pipes = std::max(1, std::min(4, std::atoi(e)));
         if (const char* e = std::getenv("XSCAT_WAVE_SLOTS"))
             c->wave_slots = (uint32_t)std::max(1, std::atoi(e));
         *out = c;
@@ -1042,7 +1042,7 @@ int xs_ctx_set_option(xs_context* c, const char* key, int64_t value)
         } else if (k == "compact_palette") {
             c->compact_palette = value != 0;
         } else if (k == "wave_pipes") {
-            c->wave_pipes = (int)std::max<int64_t>(1, std::min<int64_t>(2, value));
+            c->wave_pipes = (int)std::max<int64_t>(1, std::min<int64_t>(4, value));
         } else if (k == "wave_slots") {
             c->wave_slots = (uint32_t)std::max<int64_t>(1, std::min<int64_t>(1 << 24, value));
         } else {

@@ -455,6 +455,15 @@ __global__ void __launch_bounds__(kBlock, SKIP ? XSW_WALK_BLOCKS : XSW_EXACT_BLO
     __shared__ unsigned int cnt[4];
     if (threadIdx.x < 4)
         cnt[threadIdx.x] = 0u;
+    unsigned long long* diag = P.accum + P.off_diag;
+    constexpr int kCntSlot[4] = {0, 1, 5, 7}; // diag words: free-path visits, scoring visits, iterations, uniform
+    // u32 counters (64-bit shared atomics are CAS loops: +12% walk time); a
+    // counter that passes 2^31 is moved to the global u64 word right away
+    auto count = [&](int k, uint32_t v) {
+        const uint32_t old = atomicAdd(&cnt[k], v);
+        if (old + v >= (1u << 31))
+            red_add(diag + kCntSlot[k], atomicExch(&cnt[k], 0u));
+    };
     __syncthreads();
     uint32_t c_wit = 0;
     // A lane that ends its ray keeps the result in its walker registers until
@@ -473,10 +482,10 @@ __global__ void __launch_bounds__(kBlock, SKIP ? XSW_WALK_BLOCKS : XSW_EXACT_BLO
             __stcs(&R.res_vox[R.cap + ray], w.iy);
             __stcs(&R.res_vox[2ull * R.cap + ray], w.iz);
         }
-        atomicAdd(&cnt[score ? 1 : 0], w.steps + w.skipped);
-        atomicAdd(&cnt[2], w.steps);
+        count(score ? 1 : 0, w.steps + w.skipped);
+        count(2, w.steps);
         if (w.ucells)
-            atomicAdd(&cnt[3], w.ucells);
+            count(3, w.ucells);
         has_result = false;
     };
     for (;;) {
@@ -574,14 +583,11 @@ __global__ void __launch_bounds__(kBlock, SKIP ? XSW_WALK_BLOCKS : XSW_EXACT_BLO
     }
     if (has_result)
         store_result();
-    unsigned long long* diag = P.accum + P.off_diag;
     if (lane == 0)
         red_add(diag + 6, 32ull * c_wit);
     __syncthreads();
-    if (threadIdx.x < 4) { // free-path visits, scoring visits, iterations, uniform iterations
-        const int slot[4] = {0, 1, 5, 7};
-        red_add(diag + slot[threadIdx.x], cnt[threadIdx.x]);
-    }
+    if (threadIdx.x < 4)
+        red_add(diag + kCntSlot[threadIdx.x], cnt[threadIdx.x]);
 }
 
 // ---------------------------------------------------------------- complete
@@ -982,8 +988,10 @@ struct WavePipe {
     }
 };
 
+constexpr int kMaxPipes = 4;
+
 struct WaveEngine {
-    WavePipe pipe[2];
+    WavePipe pipe[kMaxPipes];
     unsigned long long* next_h = nullptr;
     cudaEvent_t fork = nullptr;
 };
@@ -1173,7 +1181,7 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
         n_slots = (uint32_t)n_hist;
     if (n_slots < 1)
         n_slots = 1;
-    n_pipes = n_pipes < 1 ? 1 : (n_pipes > 2 ? 2 : n_pipes);
+    n_pipes = n_pipes < 1 ? 1 : (n_pipes > kMaxPipes ? kMaxPipes : n_pipes);
     if (n_slots < 2)
         n_pipes = 1;
     // per-lane mu table entries: palette codes (4-bit palette, up to 16) or
