@@ -660,6 +660,7 @@ void accumulate(xs_context* c, const xs_geometry& g, int angle, const xs_spectru
     }
     P.march_h = cfg.step_voxels *
                 std::min({c->grid.hx, c->grid.hy, c->grid.hz}); // REF trace.cpp:117
+    P.march_ih = 1.0 / P.march_h;
     P.accum = d_accum;
     P.off_image = plan.layout.off_image;
     P.off_var = plan.layout.off_variance;

@@ -421,6 +421,10 @@ __device__ __forceinline__ bool walk_begin_impl(const TransportParams& P, Walk& 
         w.iy = n < 1 ? 1 : n;
         w.ix = 0;
         w.dtx = P.march_h;
+        // 1 / direction for the block march (walk_step); 0 for axes that do not move
+        w.rdx = d.x != 0.0 ? 1.0 / d.x : 0.0;
+        w.rdy = d.y != 0.0 ? 1.0 / d.y : 0.0;
+        w.rdz = d.z != 0.0 ? 1.0 / d.z : 0.0;
         return true;
     }
     w.march = 0;
@@ -500,11 +504,42 @@ __device__ __forceinline__ bool walk_step(const TransportParams& P, const MuTab<
         const double tb = w.texit < ta + w.dtx ? w.texit : ta + w.dtx;
         const double tm = 0.5 * (ta + tb);
         const double px = w.ox + w.rx * tm, py = w.oy + w.ry * tm, pz = w.oz + w.rz * tm;
+        const int vx = voxel_of(px, G.ox, G.ihx, G.nx), vy = voxel_of(py, G.oy, G.ihy, G.ny),
+                  vz = voxel_of(pz, G.oz, G.ihz, G.nz);
         int code;
         float dens = 0.f;
-        fetch<FMT>(G, voxel_of(px, G.ox, G.ihx, G.nx), voxel_of(py, G.oy, G.ihy, G.ny),
-                   voxel_of(pz, G.oz, G.ihz, G.nz), code, dens);
-        w.depth += tab.mu(P, code & ~G.ubit, dens) * (tb - ta);
+        fetch<FMT>(G, vx, vy, vz, code, dens);
+        const double mu = tab.mu(P, code & ~G.ubit, dens);
+        if (SKIP) {
+            // Block march: every later sample whose midpoint still lies in this
+            // sample's uniform block (level bits) has the same mu, so their
+            // segments are summed in one step (rounding-level change, like the
+            // block walk).  Only for blocks that hold several samples.
+            const int um = (1 << ((G.lvl_log2 >> (((uint32_t)code >> G.lvl_shift) << 2)) & 0xFu)) - 1;
+            if (um + 1 >= 2 * P.step_voxels) {
+                // the block's exit along the ray: the face ahead on each moving axis
+                const double fx = G.ox + (double)(w.rx > 0.0 ? (vx | um) + 1 : (vx & ~um)) * G.hx;
+                const double fy = G.oy + (double)(w.ry > 0.0 ? (vy | um) + 1 : (vy & ~um)) * G.hy;
+                const double fz = G.oz + (double)(w.rz > 0.0 ? (vz | um) + 1 : (vz & ~um)) * G.hz;
+                double tblk = w.rdx != 0.0 ? (fx - w.ox) * w.rdx : CUDART_INF;
+                const double tyb = w.rdy != 0.0 ? (fy - w.oy) * w.rdy : CUDART_INF;
+                const double tzb = w.rdz != 0.0 ? (fz - w.oz) * w.rdz : CUDART_INF;
+                tblk = tyb < tblk ? tyb : tblk;
+                tblk = tzb < tblk ? tzb : tblk;
+                // the last sample j with midpoint t0 + (j + 1/2) h before the exit
+                int j2 = (int)floor((tblk - w.t) * P.march_ih - 0.5);
+                j2 = j2 > w.iy - 1 ? w.iy - 1 : j2;
+                if (j2 > w.ix) {
+                    const double te = w.t + (j2 + 1) * w.dtx;
+                    w.depth += mu * ((w.texit < te ? w.texit : te) - ta);
+                    w.skipped += (uint32_t)(j2 - w.ix);
+                    ++w.ucells;
+                    w.ix = j2 + 1;
+                    return w.ix < w.iy;
+                }
+            }
+        }
+        w.depth += mu * (tb - ta);
         return ++w.ix < w.iy;
     }
     const int code = decode<FMT>(w.raw, w.shift);

@@ -404,6 +404,11 @@ __global__ void __launch_bounds__(kBlock, XSW_SETUP_MINB) wave_setup(const __gri
             __stcs(&R.dt[R.cap + i], w.ry);
             __stcs(&R.dt[2ull * R.cap + i], w.rz);
             __stcs(&R.vox[R.cap + i], w.iy); // samples
+            if (SKIP) { // 1 / direction for the block march
+                __stcs(&R.rd[i], w.rdx);
+                __stcs(&R.rd[R.cap + i], w.rdy);
+                __stcs(&R.rd[2ull * R.cap + i], w.rdz);
+            }
             R.flags[i] = (uint8_t)(64 | 128);
             store_mu(R, i, tab);
             continue;
@@ -517,6 +522,11 @@ __global__ void __launch_bounds__(kBlock, SKIP ? XSW_WALK_BLOCKS : XSW_EXACT_BLO
                         w.ix = 0;
                         w.iy = __ldcs(&R.vox[R.cap + r]);
                         w.dtx = P.march_h;
+                        if (SKIP) {
+                            w.rdx = __ldcs(&R.rd[r]);
+                            w.rdy = __ldcs(&R.rd[R.cap + r]);
+                            w.rdz = __ldcs(&R.rd[2ull * R.cap + r]);
+                        }
                         load_mu(R, r, tab);
                         w.depth = 0.0;
                         w.hit = 0;

@@ -102,6 +102,7 @@ struct TransportParams {
     int32_t track_var;
     int32_t var_cap;
     double march_h;
+    double march_ih; // 1 / march_h
     int32_t skip;           // 1: cross uniform macro cells in one step
     int32_t shared_mu_grid; // all materials' mu tables share grid_mat's energy knots
     int32_t shared_e_grid;  // ... and so do their sigma_incoh / sigma_coh / sigma_pe tables
