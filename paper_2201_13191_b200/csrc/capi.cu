@@ -577,6 +577,7 @@ void validate_call(const xs_geometry& g, int angle, const xs_spectrum& spec,
 void accumulate(xs_context* c, const xs_geometry& g, int angle, const xs_spectrum& spec,
                 const xs_sim_config& cfg, uint64_t h0, uint64_t h1, unsigned long long* d_accum)
 {
+    const xsi::Range range("xscat: scatter transport");
     require_scene(c);
     const Plan plan = make_plan(g, spec, cfg);
     if (h1 > plan.n_hist)
@@ -778,6 +779,7 @@ void finalize(xs_context* c, const xs_geometry& g, const xs_spectrum& spec, cons
               const unsigned long long* const* srcs, int n_src, uint64_t h0, uint64_t h1,
               xs_scatter_result* out, double* d_image)
 {
+    const xsi::Range range("xscat: finalize");
     const Plan plan = make_plan(g, spec, cfg);
     if (h1 > plan.n_hist)
         h1 = plan.n_hist;
@@ -835,6 +837,7 @@ void finalize(xs_context* c, const xs_geometry& g, const xs_spectrum& spec, cons
 
 void primary(xs_context* c, const xs_geometry& g, int angle, const xs_spectrum& spec, double* d_image)
 {
+    const xsi::Range range("xscat: primary");
     require_scene(c);
     const int nb = spec.n_bins, nm = c->n_mats;
     // REF simulate_primary :343-353 (host glibc loglog, exactly REF's values)
@@ -1341,6 +1344,7 @@ static void upload_phantom_staged(xs_context* c, const xs_phantom* ph)
 int xs_upload_phantom(xs_context* c, const xs_phantom* ph)
 {
     return guard(c, [&] {
+        const xsi::Range range("xscat: upload phantom");
         if (c->upload_path == 1)
             upload_phantom_staged(c, ph);
         else
@@ -2264,6 +2268,7 @@ static void call_status(xs_context* c, int st)
 
 static void loop_stage(xs_context* c, int iteration, const char* name, const std::function<void()>& f)
 {
+    const xsi::Range range(name);
     try {
         f();
     } catch (const Error& e) { // REF correction.cpp:22-31

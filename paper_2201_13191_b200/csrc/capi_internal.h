@@ -5,12 +5,23 @@
 
 #include <cuda_runtime.h>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <cstdint>
 #include <functional>
 
 #include "../../include/xscat_gpu.h"
 
 namespace xsi {
+
+// NVTX range for Nsight timelines (header-only NVTX 3: a no-op unless a tool
+// is attached).
+struct Range {
+    explicit Range(const char* name) { nvtxRangePushA(name); }
+    ~Range() { nvtxRangePop(); }
+    Range(const Range&) = delete;
+    Range& operator=(const Range&) = delete;
+};
 
 // The correction loop's scans, delegated (xs_group_run_iterative_correction
 // shards them by angle over the group's devices).  Outputs are device

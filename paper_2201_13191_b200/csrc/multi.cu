@@ -195,8 +195,10 @@ int xs_simulate_scatter_stats_mgpu(xs_context* c, const xs_geometry* g, int32_t 
             xsi::cuda(cudaMemsetAsync(acc, 0, L.words * 8, s), "memset accum");
             xsi::accumulate(c, *g, angle_idx, *spec, *cfg, h0, h1, acc); // validates like REF
         });
-        if (cm->n > 1)
+        if (cm->n > 1) {
+            const xsi::Range range("xscat: ncclReduce of the tallies");
             nccl_check(ncclReduce(acc, acc, L.words, ncclUint64, ncclSum, root, cm->comm, s), "ncclReduce");
+        }
         if (cm->rank == root) {
             const unsigned long long* src = acc;
             xsi::finalize(c, *g, *spec, *cfg, &src, 1, 0, n, out, d_image);
@@ -278,6 +280,7 @@ int xs_run_scan_mgpu(xs_context* c, const xs_geometry* g, const xs_spectrum* spe
             });
             if (!do_gather)
                 continue;
+            const xsi::Range range("xscat: scan gather");
             nccl_check(ncclGroupStart(), "ncclGroupStart");
             for (int r = 0; r < cm->n; ++r) {
                 int a0, a1;

@@ -36,6 +36,7 @@
 #include <cstring>
 #include <vector>
 
+#include "capi_internal.h"
 #include "transport_core.cuh"
 
 namespace xsd {
@@ -1293,6 +1294,7 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
     const bool ktime = std::getenv("XSCAT_KTIME") != nullptr;
     const int kEv = ktime ? 6 : 2;
     const int check_every = 4;
+    const xsi::Range range("xscat: wavefront waves");
     for (;;) {
         for (int k = 0; k < check_every; ++k)
             for (int p = 0; p < n_pipes; ++p) {
