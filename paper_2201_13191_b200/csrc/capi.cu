@@ -46,6 +46,8 @@ cudaError_t launch_correction_tail(const double* primary, const double* scatter,
 cudaError_t launch_walk_probe(const TransportParams& P, unsigned long long* iters, cudaStream_t s);
 cudaError_t launch_mark_levels(uint8_t* vox, const Grid& G, int fmt, const int* edges, int n_levels,
                                void* scratch, int sm_count, cudaStream_t s);
+cudaError_t launch_run_field(uint8_t* vox, const Grid& G, int axis, int sign, int shift, int cap, int sm_count,
+                             cudaStream_t s);
 size_t seg_ctl_bytes();
 size_t otsu_scratch_bytes(int bins, int n_classes);
 cudaError_t launch_seg_reset(void* ctl, cudaStream_t s);
@@ -243,6 +245,9 @@ struct xs_context {
     int lvl_edge1 = 8;                      // ... with one level bit
     std::vector<int> lvl_edges3{2, 4, 8, 16, 32, 64, 128}; // ... with three (8-bit palette; edge 2 = 2^3 sub-blocks of mixed bricks)
     bool compact_palette = false;           // 4-bit palette for <= 8 pairs (half the bytes, fewer level bits)
+    bool runs = true;                       // run field in the spare P8 bits (Grid::run_*)
+    int run_bits = 0;                       // of the uploaded grid
+    int run_key = -1;                       // axis * 2 + (sign > 0) the field holds; -1: none
     uint32_t wave_slots = 1u << 22;  // live histories of the wavefront engine (2^20 -> 2^22: +6% on C3)
     int wave_pipes = 2;              // concurrent wavefront pipelines (streams)
     xsd::WaveEngine* wave = nullptr;
@@ -574,6 +579,29 @@ void validate_call(const xs_geometry& g, int angle, const xs_spectrum& spec,
     check_angle(g, angle, who);
 }
 
+// The run field (Grid::run_*) for this projection's travel direction,
+// source -> detector: the dominant in-plane axis and its sign.  Rewritten
+// only when that changes (four times per full circle).
+void ensure_runs(xs_context* c, const xsh::Frame& f)
+{
+    if (!c->run_bits)
+        return;
+    const double dx = f.center[0] - f.src[0], dy = f.center[1] - f.src[1];
+    const int axis = std::fabs(dx) >= std::fabs(dy) ? 0 : 1;
+    const int sign = (axis == 0 ? dx : dy) > 0.0 ? 1 : -1;
+    const int key = axis * 2 + (sign > 0 ? 1 : 0);
+    const int cap = (1 << c->run_bits) - 1;
+    if (key != c->run_key) {
+        cuda_check(xsd::launch_run_field(c->vox.p, c->grid, axis, sign, c->grid.run_shift, cap, c->sm_count,
+                                         c->stream),
+                   "run field");
+        c->run_key = key;
+    }
+    c->grid.run_axis = axis;
+    c->grid.run_sign = sign;
+    c->grid.run_mask = cap;
+}
+
 void accumulate(xs_context* c, const xs_geometry& g, int angle, const xs_spectrum& spec,
                 const xs_sim_config& cfg, uint64_t h0, uint64_t h1, unsigned long long* d_accum)
 {
@@ -601,6 +629,7 @@ void accumulate(xs_context* c, const xs_geometry& g, int angle, const xs_spectru
     cuda_check(cudaMemsetAsync(c->pool.p, 0, 8, s), "memset");
     cuda_check(cudaMemsetAsync(c->status.p, 0, sizeof(xsd::DevStatus), s), "memset");
 
+    ensure_runs(c, xsh::frame_of(g, angle));
     xsd::TransportParams P;
     std::memset(&P, 0, sizeof P);
     P.G = c->grid;
@@ -946,6 +975,8 @@ int xs_ctx_create(int32_t device, xs_context** out)
         }
         if (const char* e = std::getenv("XSCAT_P4"))
             c->compact_palette = std::atoi(e) != 0;
+        if (const char* e = std::getenv("XSCAT_RUNS"))
+            c->runs = std::atoi(e) != 0;
         if (const char* e = std::getenv("XSCAT_ENGINE"))
             c->engine = std::atoi(e) != 0;
         if (const char* e = std::getenv("XSCAT_WAVE_PIPES"))
@@ -1045,6 +1076,8 @@ int xs_ctx_set_option(xs_context* c, const char* key, int64_t value)
             c->engine = value != 0;
         } else if (k == "compact_palette") {
             c->compact_palette = value != 0;
+        } else if (k == "runs") { // run field of the block walk (P8); applies at the next upload
+            c->runs = value != 0;
         } else if (k == "wave_pipes") {
             c->wave_pipes = (int)std::max<int64_t>(1, std::min<int64_t>(4, value));
         } else if (k == "wave_slots") {
@@ -1175,9 +1208,16 @@ static void upload_phantom_impl(xs_context* c, const xs_phantom* ph, bool on_dev
                 edges = c->lvl_edges2;
             else if (lvl_bits == 3)
                 edges = c->lvl_edges3;
+            // runs: the spare bits between the palette index and the level
+            const int run_bits =
+                (fmt == xsd::kFmtP8 && c->runs && lvl_bits == 3) ? std::min(3, width - need - lvl_bits) : 0;
             const int code_bits = width - lvl_bits;
             G.lvl_shift = code_bits;
             G.ubit = lvl_bits ? (((1 << lvl_bits) - 1) << code_bits) : 0;
+            G.run_shift = code_bits - run_bits;
+            G.ubit |= ((1 << run_bits) - 1) << G.run_shift;
+            c->run_bits = run_bits;
+            c->run_key = -1;
             for (size_t l = 0; l < edges.size(); ++l) {
                 int lg = 0;
                 while ((1 << lg) < edges[l])
@@ -1253,6 +1293,7 @@ static void upload_phantom_impl(xs_context* c, const xs_phantom* ph, bool on_dev
             G.ubit = 0;
             G.lvl_shift = 4;
             G.lvl_log2 = 0;
+            c->run_bits = 0;
             const size_t vb4 = n_bricks * 32;
             if (on_device) {
                 cuda_check(xsd::launch_phantom_encode(ph->material_id, ph->density, c->seg_pal.p, n_pairs, G,
@@ -1402,6 +1443,8 @@ int xs_ctx_copy_scene(xs_context* dst, const xs_context* src)
         std::memcpy(dst->pal_mat, src->pal_mat, sizeof dst->pal_mat);
         std::memcpy(dst->pal_dens, src->pal_dens, sizeof dst->pal_dens);
         dst->skip_pays = src->skip_pays;
+        dst->run_bits = src->run_bits;
+        dst->run_key = src->run_key;
         dst->last_upload_bytes = 0;
         dst->have_phantom = true;
         if (src->have_response) {

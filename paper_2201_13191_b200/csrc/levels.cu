@@ -129,7 +129,50 @@ __global__ void mark_subbricks(uint8_t* __restrict__ vox, Grid G, int bb, int lv
     }
 }
 
+// Runs (Grid::run_*), P8 only: every voxel gets the count of the voxels
+// after it along the run axis, in the run direction, with the same palette
+// index (capped).  Only the run bits are rewritten; a byte's palette bits,
+// which the neighbours read, never change.
+__global__ void run_field(uint8_t* __restrict__ vox, Grid G, int axis, int sign, int shift, int cap)
+{
+    const uint64_t n = (uint64_t)G.nx * G.ny * G.nz;
+    const uint32_t pal = (1u << shift) - 1u;
+    const uint32_t rbits = (uint32_t)cap << shift;
+    const uint32_t sy = (uint32_t)G.nbx << 6, sz = (uint32_t)G.nbx * (uint32_t)G.nby << 6;
+    auto cell = [&](int x, int y, int z) {
+        return ((uint32_t)(x >> 2) << 6) + (uint32_t)(x & 3) + (uint32_t)(y >> 2) * sy + ((uint32_t)(y & 3) << 2) +
+               (uint32_t)(z >> 2) * sz + ((uint32_t)(z & 3) << 4);
+    };
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
+        // consecutive threads walk the run axis' neighbours (coalesced enough:
+        // x-fastest order for both axes, the y run reads 4-voxel brick rows)
+        const int x = (int)(v % G.nx), y = (int)((v / G.nx) % G.ny), z = (int)(v / ((uint64_t)G.nx * G.ny));
+        const uint32_t c0 = cell(x, y, z);
+        const uint32_t b = vox[c0];
+        const uint32_t code = b & pal;
+        int r = 0;
+        int px = x, py = y;
+        while (r < cap) {
+            px += axis == 0 ? sign : 0;
+            py += axis == 1 ? sign : 0;
+            if ((uint32_t)px >= (uint32_t)G.nx || (uint32_t)py >= (uint32_t)G.ny)
+                break;
+            if ((vox[cell(px, py, z)] & pal) != code)
+                break;
+            ++r;
+        }
+        vox[c0] = (uint8_t)((b & ~rbits) | ((uint32_t)r << shift));
+    }
+}
+
 } // namespace
+
+cudaError_t launch_run_field(uint8_t* vox, const Grid& G, int axis, int sign, int shift, int cap, int sm_count,
+                             cudaStream_t s)
+{
+    run_field<<<sm_count * 8, 256, 0, s>>>(vox, G, axis, sign, shift, cap);
+    return cudaGetLastError();
+}
 
 // scratch: int16 per brick plus the (smaller) level tables; returns the
 // bytes needed when scratch == nullptr

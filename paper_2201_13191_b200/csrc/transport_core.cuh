@@ -551,13 +551,13 @@ __device__ __forceinline__ bool walk_step(const TransportParams& P, const MuTab<
         // uniform and mixed cells do not diverge.
         const int c = code & ~G.ubit;
         const int um = (1 << ((G.lvl_log2 >> (((uint32_t)code >> G.lvl_shift) << 2)) & 0xFu)) - 1;
-        const int kx = (w.sx > 0 ? ~w.ix : w.ix) & um;
-        const int ky = (w.sy > 0 ? ~w.iy : w.iy) & um;
-        const int kz = (w.sz > 0 ? ~w.iz : w.iz) & um;
+        int kx = (w.sx > 0 ? ~w.ix : w.ix) & um;
+        int ky = (w.sy > 0 ? ~w.iy : w.iy) & um;
+        int kz = (w.sz > 0 ? ~w.iz : w.iz) & um;
         // the block's exit face per axis (k = 0: the next boundary, tn itself)
-        const double ex = w.tnx + u2d_small(kx) * w.dtx;
-        const double ey = w.tny + u2d_small(ky) * w.dty;
-        const double ez = w.tnz + u2d_small(kz) * w.dtz;
+        double ex = w.tnx + u2d_small(kx) * w.dtx;
+        double ey = w.tny + u2d_small(ky) * w.dty;
+        double ez = w.tnz + u2d_small(kz) * w.dtz;
         double tm = ex;
         if (ey < tm)
             tm = ey;
@@ -565,6 +565,32 @@ __device__ __forceinline__ bool walk_step(const TransportParams& P, const MuTab<
             tm = ez;
         if (w.texit < tm)
             tm = w.texit;
+        bool multi = um != 0;
+        {
+            // The run ahead (Grid::run_*): a 1-voxel-wide box of r + 1 voxels
+            // along the run axis, when the ray moves in the run's direction.
+            // Taken instead of the block when it reaches further.
+            const bool ax = G.run_axis == 0;
+            int r = ((uint32_t)code >> G.run_shift) & G.run_mask;
+            r = (ax ? w.sx : w.sy) == G.run_sign ? r : 0;
+            const double ra = (ax ? w.tnx : w.tny) + u2d_small(r) * (ax ? w.dtx : w.dty);
+            const double ro = ax ? w.tny : w.tnx;
+            double tr = ra < ro ? ra : ro;
+            if (w.tnz < tr)
+                tr = w.tnz;
+            if (w.texit < tr)
+                tr = w.texit;
+            if (tr > tm) {
+                tm = tr;
+                kx = ax ? r : 0;
+                ky = ax ? 0 : r;
+                kz = 0;
+                ex = ax ? ra : ro;
+                ey = ax ? ro : ra;
+                ez = w.tnz;
+                multi = true;
+            }
+        }
         const double mu = tab.mu(P, c, w.dens);
         const double seg = mu * (tm - w.t);
         const double nd = w.depth + seg;
@@ -590,7 +616,7 @@ __device__ __forceinline__ bool walk_step(const TransportParams& P, const MuTab<
         w.tnx = w.tnx + u2d_small(nx) * w.dtx;
         w.tny = w.tny + u2d_small(ny) * w.dty;
         w.tnz = w.tnz + u2d_small(nz) * w.dtz;
-        if (um) {
+        if (multi) {
             w.skipped += (uint32_t)(nx + ny + nz) - 1u;
             ++w.ucells;
         }

@@ -43,6 +43,15 @@ struct Grid {
     int32_t ubit;
     int32_t lvl_shift;
     uint32_t lvl_log2;
+    // Runs (P8 block walk, spare bits between the palette index and the
+    // level): the number of voxels after this one, along axis run_axis (0: x,
+    // 1: y) in direction run_sign, that hold the same palette index, capped
+    // at run_mask.  Set for the travel direction of the current projection
+    // (levels.cu run_field); run_mask = 0: no runs.
+    int32_t run_shift;
+    int32_t run_mask;
+    int32_t run_axis;
+    int32_t run_sign;
     int32_t pad_;
 };
 

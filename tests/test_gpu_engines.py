@@ -155,3 +155,32 @@ def test_march_mode_on_the_wavefront_engine(orc, kind, step):
     for k in ("free_path_steps", "scoring_steps", "scoring_rays", "interactions"):
         assert a.stats[k] == b.stats[k], k
     _replay_compare(b, orc.simulate_scatter_stats(ph, g, 2, spec, resp, cfg))
+
+
+@pytest.mark.parametrize("angle", [0, 1, 2, 4, 6])
+def test_run_field_every_travel_direction(orc, angle):
+    """The run field (Grid::run_*: same-code run lengths along the dominant
+    travel axis of the projection, in the spare 8-bit-palette bits) for the
+    four axis directions and the diagonal tie: fewer walk iterations than
+    the block walk without runs, both engines bitwise, replayed against the
+    oracle."""
+    ph = S.make_rods_phantom(32, 10.0 / 32, 4.5, 8.0, I.material("water"), 1.0, 4, 0.6, 3.0,
+                             I.material("iron"), 7.874)  # 3 palette entries: 3 run bits
+    g = I.make_circular_geometry(100.0, 60.0, 32, 24, 0.8, 8)
+    spec, resp = I.kramers_spectrum(150.0), I.detector_response()
+    cfg = I.SimConfig(photons_total=20000, splitting=5, seed=77 + angle, track_variance=True)
+    out = {}
+    for runs in (0, 1):
+        ctx = X.projector.Context(0)
+        ctx.set_option("walk_mode", 1)
+        ctx.set_option("runs", runs)
+        proj = X.Projector(ph, resp, ctx=ctx)
+        for engine in (0, 1):
+            ctx.set_option("engine", engine)
+            out[runs, engine] = proj.scatter_stats(g, angle, spec, cfg)
+        assert _format_of(out[runs, 1].stats) == "p8"
+    a, b = out[1, 0], out[1, 1]
+    assert np.array_equal(a.image, b.image) and np.array_equal(a.variance, b.variance)
+    assert a.total == b.total and a.ledger == b.ledger
+    assert b.stats["walk_iterations"] < 0.95 * out[0, 1].stats["walk_iterations"]
+    _replay_compare(b, orc.simulate_scatter_stats(ph, g, angle, spec, resp, cfg))
