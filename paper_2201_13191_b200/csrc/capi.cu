@@ -667,6 +667,8 @@ void accumulate(xs_context* c, const xs_geometry& g, int angle, const xs_spectru
     P.max_inter = cfg.max_interactions;
     P.track_var = cfg.track_variance ? 1 : 0;
     P.skip = c->macro_skip == 2 ? (c->skip_pays ? 1 : 0) : c->macro_skip;
+    if (P.step_voxels > 1) // march mode: the free paths' block walk without runs
+        P.G.run_mask = 0;
     { // shared energy knots of the mu tables (REF bundle: yes)
         int first = -1;
         bool same = true;

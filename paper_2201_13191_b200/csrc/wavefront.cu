@@ -437,7 +437,7 @@ __global__ void __launch_bounds__(kBlock, XSW_SETUP_MINB) wave_setup(const __gri
 }
 
 // -------------------------------------------------------------------- walk
-template <int FMT, bool REG, bool SKIP, bool MARCH>
+template <int FMT, bool REG, bool SKIP, bool MARCH, int RUN>
 __global__ void __launch_bounds__(kBlock, SKIP ? XSW_WALK_BLOCKS : XSW_EXACT_BLOCKS) wave_walk(const __grid_constant__ TransportParams P,
                                                     const __grid_constant__ WaveArgs A)
 {
@@ -581,12 +581,12 @@ __global__ void __launch_bounds__(kBlock, SKIP ? XSW_WALK_BLOCKS : XSW_EXACT_BLO
         }
         ++c_wit;
         if (walking) {
-            walking = walk_step<FMT, REG, SKIP>(P, tab, w);
+            walking = walk_step<FMT, REG, SKIP, RUN>(P, tab, w);
             ++w.steps;
             // the voxel walk takes a second step per loop trip (halves the per-step
             // loop overhead: -21% walk time on speckled phantoms)
             if ((!SKIP || XSW_BLOCK_UNROLL) && walking) {
-                walking = walk_step<FMT, REG, SKIP>(P, tab, w);
+                walking = walk_step<FMT, REG, SKIP, RUN>(P, tab, w);
                 ++w.steps;
             }
             has_result = !walking;
@@ -890,10 +890,18 @@ struct WaveSet {
     WaveFn setup, walk, event;
 };
 
-template <int FMT, bool REG, bool SKIP, bool MARCH>
+template <int FMT, bool REG, bool SKIP, bool MARCH, int RUN = 0>
 WaveSet wave_set()
 {
-    return {wave_setup<FMT, REG, SKIP, MARCH>, wave_walk<FMT, REG, SKIP, MARCH>, wave_event<FMT>};
+    return {wave_setup<FMT, REG, SKIP, MARCH>, wave_walk<FMT, REG, SKIP, MARCH, RUN>, wave_event<FMT>};
+}
+
+// the walk with the run field along x / y (8-bit palette, block walk, the
+// walker's exact steps: free paths and scoring rays alike)
+template <bool REG>
+WaveSet wave_set_runs(const Grid& G)
+{
+    return G.run_axis == 0 ? wave_set<kFmtP8, REG, true, false, 1>() : wave_set<kFmtP8, REG, true, false, 2>();
 }
 
 template <bool MARCH>
@@ -906,6 +914,8 @@ WaveSet wave_kernels_m(const TransportParams& P)
         return skip ? wave_set<kFmtP4, false, true, MARCH>() : wave_set<kFmtP4, false, false, MARCH>();
     }
     if (P.G.fmt == kFmtP8) {
+        if (!MARCH && skip && P.G.run_mask)
+            return use_reg_w(P) ? wave_set_runs<true>(P.G) : wave_set_runs<false>(P.G);
         if (use_reg_w(P))
             return skip ? wave_set<kFmtP8, true, true, MARCH>() : wave_set<kFmtP8, true, false, MARCH>();
         return skip ? wave_set<kFmtP8, false, true, MARCH>() : wave_set<kFmtP8, false, false, MARCH>();
@@ -1061,7 +1071,7 @@ __global__ void __launch_bounds__(kBlock) walk_probe(const __grid_constant__ Tra
             continue;
         bool walking = true;
         while (walking) {
-            walking = walk_step<FMT, true, SKIP>(P, tab, w);
+            walking = walk_step<FMT, true, SKIP, 0>(P, tab, w);
             ++n_it;
         }
     }
