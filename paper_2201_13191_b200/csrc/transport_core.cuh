@@ -252,37 +252,40 @@ struct MuTab {
     __device__ __forceinline__ void fill_impl(const TransportParams& P, double e, DevStatus* st, int bin)
     {
         energy = e;
-        if (FMT == kFmtP4 || REG) { // per palette entry (REG: <= 4 entries, either palette width)
+        if (REG) { // <= 4 palette entries in registers; one table evaluation per entry
             double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3_ = 0.0;
-            if (!REG)
-                for (int c = 0; c < P.n_pal; ++c)
-                    T[c * kBlock] = 0.0;
+            SharedLog sl;
+            sl.init(P, e, st, bin);
+            for (int c = 0; c < P.n_pal; ++c) {
+                const int m = P.pal_mat[c];
+                double mu = 0.0;
+                if (m >= 1 && m < P.n_mats && P.mats[m].has_tables)
+                    mu = sl.eval(P, P.mats[m].mu, e, st, bin) * (double)P.pal_dens[c];
+                if (c == 0)
+                    v0 = mu;
+                else if (c == 1)
+                    v1 = mu;
+                else if (c == 2)
+                    v2 = mu;
+                else
+                    v3_ = mu;
+            }
+            t0 = v0;
+            t1 = v1;
+            t2 = v2;
+            t3 = v3_;
+        } else if (FMT == kFmtP4) { // per palette entry
+            for (int c = 0; c < P.n_pal; ++c)
+                T[c * kBlock] = 0.0;
             SharedLog sl;
             sl.init(P, e, st, bin);
             for (int m = 1; m < P.n_mats; ++m) {
                 const MatDesc& md = P.mats[m];
                 const double ma = md.has_tables ? sl.eval(P, md.mu, e, st, bin) : 0.0;
                 for (int c = 0; c < P.n_pal; ++c)
-                    if (P.pal_mat[c] == m) {
-                        const double mu = ma * (double)P.pal_dens[c];
-                        if (REG) {
-                            if (c == 0)
-                                v0 = mu;
-                            else if (c == 1)
-                                v1 = mu;
-                            else if (c == 2)
-                                v2 = mu;
-                            else
-                                v3_ = mu;
-                        } else {
-                            T[c * kBlock] = mu;
-                        }
-                    }
+                    if (P.pal_mat[c] == m)
+                        T[c * kBlock] = ma * (double)P.pal_dens[c];
             }
-            t0 = v0;
-            t1 = v1;
-            t2 = v2;
-            t3 = v3_;
         } else {
             T[0] = 0.0;
             SharedLog sl;
