@@ -73,8 +73,9 @@ namespace {
 #ifndef XSW_ADMIT_MINB
 #define XSW_ADMIT_MINB 1
 #endif
-#ifndef XSW_BLOCK_UNROLL
-#define XSW_BLOCK_UNROLL 0 // two block steps per loop trip
+#ifndef XSW_INNER
+#define XSW_INNER 3 // block steps per walk-loop trip between the warp's refill checks
+                    // (C3 walk: 1 -> 212, 2 -> 200, 3 -> 193, 4 -> 204, 5 -> 201 ms)
 #endif
 constexpr int kRefill = XSW_REFILL; // idle lanes that trigger a warp's refill in the walk kernel
 
@@ -579,13 +580,21 @@ __global__ void __launch_bounds__(kBlock, SKIP ? XSW_WALK_BLOCKS : XSW_EXACT_BLO
                 break;
             continue;
         }
-        ++c_wit;
+        // lane slots: the steps a full trip takes (an exact count -- the
+        // warp's longest trip -- costs a warp reduction per trip, +5% walk time)
+        c_wit += SKIP ? XSW_INNER : 2;
         if (walking) {
             walking = walk_step<FMT, REG, SKIP, RUN>(P, tab, w);
             ++w.steps;
             // the voxel walk takes a second step per loop trip (halves the per-step
-            // loop overhead: -21% walk time on speckled phantoms)
-            if ((!SKIP || XSW_BLOCK_UNROLL) && walking) {
+            // loop overhead: -21% walk time on speckled phantoms); the block walk
+            // up to XSW_INNER steps between the warp's refill checks
+            if (!SKIP && walking) {
+                walking = walk_step<FMT, REG, SKIP, RUN>(P, tab, w);
+                ++w.steps;
+            }
+#pragma unroll 1
+            for (int j = 1; j < (SKIP ? XSW_INNER : 1) && walking; ++j) {
                 walking = walk_step<FMT, REG, SKIP, RUN>(P, tab, w);
                 ++w.steps;
             }
