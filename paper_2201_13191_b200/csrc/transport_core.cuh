@@ -485,11 +485,29 @@ __device__ __forceinline__ int d2i_trunc_small(double x) // trunc(x) for 0 <= x 
 // axes with tn == tm cross (trace.cpp:146-153).  Axes that do not move carry
 // finite sentinels (tn = dt = 1e300, rd = 1e-300; start_axis<true>) so the
 // estimate is 0 and tn + 0 * dt stays tn.
+#ifndef XS_WALK_FMA
+#define XS_WALK_FMA 1
+#endif
+// t-plane arithmetic of the block step, fused: tn + k dt with k = 0 or 1 is
+// the same single rounding as REF's tn + dt, so voxel steps stay exact
+__device__ __forceinline__ double plane_at(double tn, uint32_t k, double dt)
+{
+#if XS_WALK_FMA
+    return __fma_rn(u2d_small(k), dt, tn);
+#else
+    return tn + u2d_small(k) * dt;
+#endif
+}
 __device__ __forceinline__ int cross_n(double tn, double e, double rd, double tm, int k)
 {
     // 2^52 + 1 + q rounded toward zero: its low word is trunc(q + 1) for q >= -1,
     // and negative (0xFFFFFFFx) just below, which the clamp turns into 0
+    // (the count matters only for k > 0, inside blocks)
+#if XS_WALK_FMA
+    const int est = __double2loint(__fma_rz(tm - tn, rd, 4503599627370497.0));
+#else
     const int est = __double2loint(__dadd_rz((tm - tn) * rd, 4503599627370497.0));
+#endif
     const int n = est < 0 ? 0 : (est > k ? k : est);
     return e <= tm ? k + 1 : n;
 }
@@ -560,9 +578,9 @@ __device__ __forceinline__ bool walk_step(const TransportParams& P, const MuTab<
         int ky = (w.sy > 0 ? ~w.iy : w.iy) & um;
         int kz = (w.sz > 0 ? ~w.iz : w.iz) & um;
         // the block's exit face per axis (k = 0: the next boundary, tn itself)
-        double ex = w.tnx + u2d_small(kx) * w.dtx;
-        double ey = w.tny + u2d_small(ky) * w.dty;
-        double ez = w.tnz + u2d_small(kz) * w.dtz;
+        double ex = plane_at(w.tnx, kx, w.dtx);
+        double ey = plane_at(w.tny, ky, w.dty);
+        double ez = plane_at(w.tnz, kz, w.dtz);
         double tm = ex;
         if (ey < tm)
             tm = ey;
@@ -580,7 +598,7 @@ __device__ __forceinline__ bool walk_step(const TransportParams& P, const MuTab<
             const bool ax = RUN == 1 ? true : RUN == 2 ? false : G.run_axis == 0;
             int r = ((uint32_t)code >> G.run_shift) & G.run_mask;
             r = (ax ? w.sx : w.sy) == G.run_sign ? r : 0;
-            const double ra = (ax ? w.tnx : w.tny) + u2d_small(r) * (ax ? w.dtx : w.dty);
+            const double ra = plane_at(ax ? w.tnx : w.tny, r, ax ? w.dtx : w.dty);
             const double ro = ax ? w.tny : w.tnx;
             double tr = ra < ro ? ra : ro;
             if (w.tnz < tr)
@@ -620,9 +638,9 @@ __device__ __forceinline__ bool walk_step(const TransportParams& P, const MuTab<
         w.depth = nd;
         w.t = tm;
         // (n = 0: tn + 0 * dt == tn, dt finite)
-        w.tnx = w.tnx + u2d_small(nx) * w.dtx;
-        w.tny = w.tny + u2d_small(ny) * w.dty;
-        w.tnz = w.tnz + u2d_small(nz) * w.dtz;
+        w.tnx = plane_at(w.tnx, nx, w.dtx);
+        w.tny = plane_at(w.tny, ny, w.dty);
+        w.tnz = plane_at(w.tnz, nz, w.dtz);
         if (multi) {
             w.skipped += (uint32_t)(nx + ny + nz) - 1u;
             ++w.ucells;

@@ -27,7 +27,6 @@
 // rays need, so the interaction record needs no double buffering.  Tallies
 // are the same fixed-point integers as the megakernel's, so both engines give
 // bit-identical images and statistics.
-#include <cuda/atomic>
 
 #include <algorithm>
 #include <cstdio>
@@ -102,6 +101,8 @@ struct WaveCtl {
     WaveQueue q[2];
     uint32_t* free_stack; // released slots, [0, free_top)
     int32_t free_top;
+    uint32_t* fin;        // histories whose last scoring ray the wave's scoring kernel counted
+    uint32_t n_fin;       //   down, finalized by the wave's event kernel (reset by set-up)
     uint32_t cursor;      // walk kernel work cursor
     uint32_t ev_cursor;   // event kernel work cursor
     uint32_t setup_cursor; // set-up kernel work cursor (reset by wave_plan)
@@ -354,6 +355,7 @@ __global__ void __launch_bounds__(kBlock, XSW_SETUP_MINB) wave_setup(const __gri
         ctl->ev_cursor = 0;
         ctl->n_rays = n;
         ctl->n_score = n_s;
+        ctl->n_fin = 0;
         ctl->q[A.cur ^ 1].n_batch = 0;
         ctl->q[A.cur ^ 1].n_free = 0;
     }
@@ -624,11 +626,6 @@ __global__ void __launch_bounds__(kBlock, XSW_SCORE_MINB) wave_score(const __gri
     const WaveQueue& in = ctl->q[A.cur];
     const uint32_t n_s = ctl->n_score;
     const Block B = block_stats(P, acc);
-    // the only push of this kernel is a finished history's slot, recorded here
-    // (no pointer to the record escapes: it stays in registers)
-    Deferred def;
-    deferred_reset(def);
-    const GlobalQ qs{A.slots, ctl, A.cur ^ 1, -1, nullptr};
     const WaveRays& R = A.R;
     DevStatus* st = P.status;
     const int lane = threadIdx.x & 31;
@@ -676,17 +673,17 @@ __global__ void __launch_bounds__(kBlock, XSW_SCORE_MINB) wave_score(const __gri
             sadd(&S.T[0], ((uint64_t)b0 << 16) + a0);
             sadd(&S.T[1], ((uint64_t)b1 << 16) + a1);
             sadd(&S.T[2], ((uint64_t)b2 << 16) + a2);
-            // hand-off: release this warp's tallies / scratch, and the last one
-            // to count down acquires every other warp's before finalizing
-            const int cnt = __popc(grp);
-            cuda::atomic_ref<int, cuda::thread_scope_device> pending(S.pending);
-            if (pending.fetch_sub(cnt, cuda::memory_order_acq_rel) == cnt) {
-                finalize_history(P, B, qs, s, var_base_of(P, s), st, false);
-                def.rel_slot = s;
+            // the last count-down hands the history to this wave's event
+            // kernel, which finalizes it: the kernel boundary orders every
+            // warp's tallies and scratch before it, so no fence is needed here
+            // (an acquire/release hand-off in this kernel cost 39% of its stall
+            // samples in memory barriers)
+            if (atomicSub(&S.pending, __popc(grp)) == __popc(grp)) {
+                const uint32_t k = atomicAdd(&ctl->n_fin, 1u);
+                if (XS_GUARD(k < A.n_slots, st, 19.0))
+                    ctl->fin[k] = (uint32_t)s;
             }
         }
-        __syncwarp();
-        flush_deferred(P, B, ctl, A.cur ^ 1, def, A.n_slots, P.status);
     }
     flush_stats(P, B);
 }
@@ -709,6 +706,19 @@ __global__ void __launch_bounds__(kBlock, XSW_EVENT_MINB) wave_event(const __gri
     uint32_t c_int = 0;
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
+    { // histories the scoring kernel ended: finalize and release (REF run_history :225-241)
+        const uint32_t n_fin = ctl->n_fin, n_warps = (gridDim.x * blockDim.x) >> 5;
+        for (uint32_t b = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32u; b < n_fin; b += n_warps * 32u) {
+            const uint32_t k = b + (uint32_t)lane;
+            if (k < n_fin) {
+                const int s = (int)ctl->fin[k];
+                if (XS_GUARD((uint32_t)s < A.n_slots, P.status, 20.0))
+                    finalize_history(P, B, qs, s, var_base_of(P, s), P.status);
+            }
+            __syncwarp();
+            flush_deferred(P, B, ctl, A.cur ^ 1, def, A.n_slots, P.status);
+        }
+    }
     // Escapes (no interaction) are cheap and run where they are found.  The
     // interactions are gathered per warp and their selection phase (event_select)
     // runs 32 at a time; its Compton and Rayleigh continuations are gathered
@@ -1148,7 +1158,7 @@ static double pipe_bytes(uint32_t n_slots, int splitting, int n_mu)
 {
     const double cap = (double)n_slots * ((double)splitting + 1.0);
     const double per_ray = (3 + 3 + 3 + n_mu + 2) * 8.0 + 3 * 8.0 + 7 * 4.0 + 2.0;
-    const double per_slot = (double)sizeof(Slot) + 4.0 + 2.0 * (sizeof(ScoreBatch) + 4.0);
+    const double per_slot = (double)sizeof(Slot) + 8.0 + 2.0 * (sizeof(ScoreBatch) + 4.0);
     return cap * per_ray + (double)n_slots * per_slot;
 }
 
@@ -1159,7 +1169,7 @@ static cudaError_t pipe_prepare(WavePipe& w, const TransportParams& P, uint32_t 
     if (cap >= (1ull << 32))
         return cudaErrorInvalidValue;
     XSW_CHECK(grow(w.slots, w.n_slots_have, n_slots));
-    XSW_CHECK(grow(w.stack, w.stack_have, n_slots));
+    XSW_CHECK(grow(w.stack, w.stack_have, 2 * (size_t)n_slots)); // free stack | finalize list
     XSW_CHECK(grow(w.ctl, w.ctl_have, 1));
     for (int b = 0; b < 2; ++b) {
         XSW_CHECK(grow(w.sq[b], w.sq_have[b], (size_t)n_slots));
@@ -1296,6 +1306,7 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
             init.q[b].free = w.fq[b];
         }
         init.free_stack = w.stack;
+        init.fin = w.stack + per;
         XSW_CHECK(cudaMemcpyAsync(w.ctl, &init, sizeof init, cudaMemcpyHostToDevice, ps));
         wave_init<<<sm_count, 256, 0, ps>>>(w.ctl, w.stack, per, P.h_begin);
         w.A.next_h = e->next_h;
