@@ -43,18 +43,21 @@ srows = list(csv.reader(io.StringIO(sass)))
 h = srows[1]
 ie, src = h.index("Instructions Executed"), h.index("Source")
 votes = [int(r[ie]) for r in srows[2:] if len(r) > ie and "VOTE.ANY" in r[src] and r[ie].isdigit()]
-warp_it = max(votes)
+# a loop trip (one loop-top vote) is XSW_INNER = 3 block steps (wavefront.cu): per warp step slot
+steps_per_trip = 3
+warp_it = max(votes) * steps_per_trip
 res = {
     "kernel": d.get("Kernel Name", "wave_walk")[:120],
     "source": "tools/profile_round.sh: ncu launch metrics over every walk launch of the bench run, and one "
-              "--set full launch (instructions per warp iteration = sm instructions / executions of the "
-              "loop-top VOTE.ANY)",
+              "--set full launch (instructions per warp step slot = sm instructions / (executions of the "
+              "loop-top VOTE.ANY x 3 steps per trip))",
     "walk_launches_per_projection": len(n_launch) / n_proj,
     "walk_dram_bytes_read_per_projection": tot["dram__bytes_read.sum"] / n_proj,
     "walk_dram_bytes_write_per_projection": tot["dram__bytes_write.sum"] / n_proj,
     "walk_dram_bytes_per_projection": (tot["dram__bytes_read.sum"] + tot["dram__bytes_write.sum"]) / n_proj,
     "walk_time_ms_per_projection_under_ncu": tot["gpu__time_duration.sum"] / n_proj,
     "walk_warp_instructions_per_warp_iteration": inst / warp_it,
+    "walk_steps_per_loop_trip": steps_per_trip,
     "walk_issue_active_pct": num("smsp__issue_active.avg.pct_of_peak_sustained_active"),
     "walk_warps_active_pct": num("sm__warps_active.avg.pct_of_peak_sustained_active"),
     "walk_l2_hit_pct": num("lts__t_sector_hit_rate.pct"),
