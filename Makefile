@@ -14,19 +14,26 @@ CXXFLAGS := -O2 -std=c++17 -fPIC -ffp-contract=off -Iinclude
 
 CU_SRCS  := $(SRC)/capi.cu $(SRC)/transport.cu $(SRC)/wavefront.cu $(SRC)/levels.cu $(SRC)/correct.cu $(SRC)/fbp.cu $(SRC)/segment.cu $(SRC)/primary.cu $(SRC)/postprocess.cu $(SRC)/multi.cu
 CU_OBJS  := $(patsubst $(SRC)/%.cu,$(OBJDIR)/%.o,$(CU_SRCS))
-CPP_OBJS := $(OBJDIR)/host_common.o
+CPP_OBJS := $(OBJDIR)/host_common.o $(OBJDIR)/files.o
 HDRS     := $(wildcard $(SRC)/*.h $(SRC)/*.cuh) include/xscat_gpu.h
 
-.PHONY: all lib oracle clean
-all: lib oracle
+.PHONY: all lib cli oracle clean
+all: lib cli oracle
 
 lib: $(LIBDIR)/libxscatgpu.so
+
+# the reference CLI's simulate / inspect commands over the C ABI (native host code)
+cli: $(PKG)/bin/xscat_b200
+
+$(PKG)/bin/xscat_b200: $(PKG)/cli/xscat_b200.cpp include/xscat_gpu.h $(LIBDIR)/libxscatgpu.so
+	@mkdir -p $(PKG)/bin
+	$(CXX_HOST) -O2 -std=c++17 -Iinclude -o $@ $< -L$(LIBDIR) -lxscatgpu -Wl,-rpath,'$$ORIGIN/../lib'
 
 $(OBJDIR)/%.o: $(SRC)/%.cu $(HDRS)
 	@mkdir -p $(OBJDIR)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $@.ptxas.log || (cat $@.ptxas.log; exit 1)
 
-$(OBJDIR)/host_common.o: $(SRC)/host_common.cpp $(HDRS)
+$(OBJDIR)/%.o: $(SRC)/%.cpp $(HDRS)
 	@mkdir -p $(OBJDIR)
 	$(CXX_HOST) $(CXXFLAGS) -c $< -o $@
 
@@ -38,5 +45,5 @@ oracle:
 	$(MAKE) -C oracle
 
 clean:
-	rm -rf $(OBJDIR) $(LIBDIR)
+	rm -rf $(OBJDIR) $(LIBDIR) $(PKG)/bin
 	$(MAKE) -C oracle clean

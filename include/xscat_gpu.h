@@ -658,6 +658,62 @@ int xs_group_run_iterative_correction(xs_group* grp, const double* raw_intensity
                                       double* corrected_stack, xs_iteration_report* reports,
                                       int32_t device_ptrs);
 
+/* ------------------------------------------------------ files and inputs
+ * The reference's file formats and text inputs (
+ * csrc/files.cpp).  Same byte layouts, accepted inputs and error messages. */
+
+/* XPRJ1 projection stack (REF detector_image.cpp:33-87): "XPRJ1", u32 nu, nv,
+ * n_angles, then n_angles images of nu*nv f32.  load: images has
+ * n_angles*nu*nv doubles (REF load_stack widens the f32 values);
+ * save: REF save_stack narrows to f32. */
+int xs_stack_file_info(const char* path, int32_t* nu, int32_t* nv, int32_t* n_angles);
+int xs_stack_file_load(const char* path, double* images);
+int xs_stack_file_save(const char* path, int32_t nu, int32_t nv, int32_t n_angles, const double* images);
+
+/* XVOX1 voxel phantom (REF phantom.cpp:74-161): "XVOX1", u32 dims[3], f64
+ * voxel_size[3], f64 origin[3], u32 n_materials, u8 ids, f32 densities.
+ * info: REF load_phantom_header.  read: REF load_phantom's file part;
+ * n_materials_given = the caller's material list length with vacuum (REF
+ * fails when the header declares more); the handle owns the voxel arrays
+ * its view points to (materials NULL: the caller attaches its list), and
+ * xs_validate_phantom completes REF load_phantom. */
+typedef struct xs_phantom_file xs_phantom_file;
+int xs_phantom_file_info(const char* path, int32_t dims[3], double voxel_size[3], double origin[3],
+                         uint32_t* n_materials);
+int xs_phantom_file_read(const char* path, uint32_t n_materials_given, xs_phantom_file** out);
+const xs_phantom* xs_phantom_file_get(const xs_phantom_file* f);
+void xs_phantom_file_free(xs_phantom_file* f);
+int xs_phantom_file_save(const char* path, const xs_phantom* ph);
+/* REF validate_phantom (phantom.cpp:33-56) on the host (REF load_phantom runs
+ * it after reading; xs_upload_phantom runs the same checks on the device). */
+int xs_validate_phantom(const xs_phantom* ph);
+
+/* XVOL1 volume (REF volume.cpp:22-62): "XVOL1", u32 dims[3], f64
+ * voxel_size[3], f32 values, x fastest. */
+int xs_volume_file_info(const char* path, int32_t dims[3], double voxel_size[3]);
+int xs_volume_file_load(const char* path, float* values);
+int xs_volume_file_save(const char* path, const int32_t dims[3], const double voxel_size[3], const float* values);
+
+/* Material table file (REF load_material, material.cpp:129-213, with
+ * validate_material :57-97); the handle owns the tables its view points to. */
+typedef struct xs_material_file xs_material_file;
+int xs_material_file_load(const char* path, xs_material_file** out);
+const xs_material* xs_material_file_get(const xs_material_file* f);
+void xs_material_file_free(xs_material_file* f);
+
+/* Spectrum CSV (keV, weight; REF load_spectrum, spectrum.cpp:32-60). */
+typedef struct xs_spectrum_file xs_spectrum_file;
+int xs_spectrum_file_load(const char* path, xs_spectrum_file** out);
+const xs_spectrum* xs_spectrum_file_get(const xs_spectrum_file* f);
+void xs_spectrum_file_free(xs_spectrum_file* f);
+
+/* Detector response CSV (keV, dqe, deposit_keV; REF load_detector_response,
+ * detector_response.cpp:50-79). */
+typedef struct xs_response_file xs_response_file;
+int xs_response_file_load(const char* path, xs_response_file** out);
+const xs_response* xs_response_file_get(const xs_response_file* f);
+void xs_response_file_free(xs_response_file* f);
+
 #ifdef __cplusplus
 }
 #endif

@@ -20,7 +20,9 @@
 #include "xscat/recon.hpp"
 #include "xscat/material.hpp"
 #include "xscat/postprocess.hpp"
+#include "xscat/run_config.hpp"
 #include "xscat/samplers.hpp"
+#include "xscat/volume.hpp"
 #include "xscat/synthetic.hpp"
 #include "xscat/trace.hpp"
 #include "xscat/transport.hpp"
@@ -699,6 +701,142 @@ int xr_run_iterative_correction(const double* raw, const double* flat, const xs_
             x.ncc_to_previous = r.ncc_to_previous;
             x.negative_scatter_clamped = r.negative_scatter_clamped;
         }
+    });
+}
+
+
+// ------------------------------------------------------ files
+// REF save_stack (detector_image.cpp:33-51)
+int xr_save_stack(const char* path, int32_t nu, int32_t nv, int32_t n, const double* images)
+{
+    return guarded([&] {
+        ProjectionStack s = make_stack(nu, nv, std::vector<double>(n, 0.0));
+        for (int a = 0; a < n; ++a)
+            s.images[a].values.assign(images + (size_t)a * nu * nv, images + (size_t)(a + 1) * nu * nv);
+        save_stack(s, path);
+    });
+}
+
+// REF load_stack (:53-87): header + widened values
+int xr_load_stack(const char* path, int32_t* nu, int32_t* nv, int32_t* n, double* images, int64_t cap)
+{
+    return guarded([&] {
+        const ProjectionStack s = load_stack(path);
+        *nu = s.nu;
+        *nv = s.nv;
+        *n = s.n_angles();
+        const size_t np = (size_t)s.nu * s.nv;
+        if (images && (int64_t)(np * s.images.size()) <= cap)
+            for (size_t a = 0; a < s.images.size(); ++a)
+                std::memcpy(images + a * np, s.images[a].values.data(), np * sizeof(double));
+    });
+}
+
+// REF save_phantom (phantom.cpp:74-93)
+int xr_save_phantom(const char* path, const xs_phantom* ph)
+{
+    return guarded([&] { save_phantom(phantom(*ph), path); });
+}
+
+// REF load_phantom (:120-161) with `n_files` copies of the given material
+int xr_load_phantom(const char* path, const xs_material* m, int32_t n_files, int32_t* dims, double* voxel,
+                    double* origin, uint8_t* ids, float* dens)
+{
+    return guarded([&] {
+        std::vector<Material> mats;
+        for (int i = 0; i < n_files; ++i)
+            mats.push_back(material(*m));
+        const VoxelPhantom ph = load_phantom(path, mats);
+        export_phantom(ph, dims, voxel, origin, ids, dens);
+    });
+}
+
+// REF save_volume / load_volume (volume.cpp:22-62)
+int xr_save_volume(const char* path, const int32_t* dims, const double* voxel, const float* values)
+{
+    return guarded([&] {
+        Volume v = make_volume(dims[0], dims[1], dims[2], {voxel[0], voxel[1], voxel[2]});
+        std::memcpy(v.values.data(), values, v.values.size() * sizeof(float));
+        save_volume(v, path);
+    });
+}
+
+int xr_load_volume(const char* path, int32_t* dims, double* voxel, float* values, int64_t cap)
+{
+    return guarded([&] {
+        const Volume v = load_volume(path);
+        for (int a = 0; a < 3; ++a)
+            dims[a] = v.dims[a];
+        voxel[0] = v.voxel_size.x;
+        voxel[1] = v.voxel_size.y;
+        voxel[2] = v.voxel_size.z;
+        if (values && (int64_t)v.values.size() <= cap)
+            std::memcpy(values, v.values.data(), v.values.size() * sizeof(float));
+    });
+}
+
+// REF load_material (material.cpp:129-213): the six tables, concatenated
+// x then y per table in section order; counts[6]
+int xr_load_material(const char* path, double* header, int32_t* counts, double* xy, int64_t cap)
+{
+    return guarded([&] {
+        const Material m = load_material(path);
+        header[0] = m.z_eff;
+        header[1] = m.density_ref;
+        const Table1D* t[6] = {&m.mu, &m.sigma_incoh, &m.sigma_coh, &m.sigma_pe, &m.s_factor, &m.f_factor};
+        int64_t k = 0;
+        for (int i = 0; i < 6; ++i) {
+            counts[i] = (int32_t)t[i]->size();
+            for (double v : t[i]->xs())
+                if (k < cap)
+                    xy[k++] = v;
+            for (double v : t[i]->ys())
+                if (k < cap)
+                    xy[k++] = v;
+        }
+    });
+}
+
+// REF load_spectrum (spectrum.cpp:32-60)
+int xr_load_spectrum(const char* path, double* e, double* w, int32_t* n, int32_t cap)
+{
+    return guarded([&] {
+        const Spectrum s = load_spectrum(path);
+        *n = (int32_t)s.bins.size();
+        for (int32_t i = 0; i < *n && i < cap; ++i) {
+            e[i] = s.bins[i].energy_kev;
+            w[i] = s.bins[i].weight;
+        }
+    });
+}
+
+// REF load_detector_response (detector_response.cpp:50-79)
+int xr_load_response(const char* path, double* e, double* dqe, double* dep, int32_t* n, int32_t cap)
+{
+    return guarded([&] {
+        const DetectorResponse r = load_detector_response(path);
+        *n = (int32_t)r.dqe.size();
+        for (int32_t i = 0; i < *n && i < cap; ++i) {
+            e[i] = r.dqe.xs()[i];
+            dqe[i] = r.dqe.ys()[i];
+            dep[i] = r.deposit.ys()[i];
+        }
+    });
+}
+
+// REF parse_ini + build_run_config + validate_run_config (run_config.cpp:84-230):
+// the collected problems, one per line (empty: valid)
+int xr_config_problems(const char* path, char* out, int32_t cap)
+{
+    return guarded([&] {
+        std::vector<std::string> errors;
+        const std::filesystem::path p = path;
+        const RunConfig cfg = build_run_config(parse_ini(p), p.parent_path(), errors);
+        validate_run_config(cfg, errors);
+        std::string all;
+        for (const auto& e : errors)
+            all += e + "\n";
+        std::snprintf(out, (size_t)cap, "%s", all.c_str());
     });
 }
 

@@ -345,6 +345,30 @@ SIGNATURES = {
                                                     C.POINTER(XsCorrectionConfig), C.c_int32,
                                                     C.POINTER(XsMaterial), _P, _P,
                                                     C.POINTER(XsIterationReport), C.c_int32]),
+    # files and inputs (csrc/files.cpp)
+    "xs_stack_file_info": (C.c_int, [C.c_char_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                     C.POINTER(C.c_int32)]),
+    "xs_stack_file_load": (C.c_int, [C.c_char_p, c_double_p]),
+    "xs_stack_file_save": (C.c_int, [C.c_char_p, C.c_int32, C.c_int32, C.c_int32, c_double_p]),
+    "xs_phantom_file_info": (C.c_int, [C.c_char_p, C.POINTER(C.c_int32), c_double_p, c_double_p,
+                                       C.POINTER(C.c_uint32)]),
+    "xs_phantom_file_read": (C.c_int, [C.c_char_p, C.c_uint32, C.POINTER(_P)]),
+    "xs_phantom_file_get": (C.POINTER(XsPhantom), [_P]),
+    "xs_phantom_file_free": (None, [_P]),
+    "xs_phantom_file_save": (C.c_int, [C.c_char_p, C.POINTER(XsPhantom)]),
+    "xs_validate_phantom": (C.c_int, [C.POINTER(XsPhantom)]),
+    "xs_volume_file_info": (C.c_int, [C.c_char_p, C.POINTER(C.c_int32), c_double_p]),
+    "xs_volume_file_load": (C.c_int, [C.c_char_p, _P]),
+    "xs_volume_file_save": (C.c_int, [C.c_char_p, C.POINTER(C.c_int32), c_double_p, _P]),
+    "xs_material_file_load": (C.c_int, [C.c_char_p, C.POINTER(_P)]),
+    "xs_material_file_get": (C.POINTER(XsMaterial), [_P]),
+    "xs_material_file_free": (None, [_P]),
+    "xs_spectrum_file_load": (C.c_int, [C.c_char_p, C.POINTER(_P)]),
+    "xs_spectrum_file_get": (C.POINTER(XsSpectrum), [_P]),
+    "xs_spectrum_file_free": (None, [_P]),
+    "xs_response_file_load": (C.c_int, [C.c_char_p, C.POINTER(_P)]),
+    "xs_response_file_get": (C.POINTER(XsResponse), [_P]),
+    "xs_response_file_free": (None, [_P]),
     "xs_correction_config_default": (None, [C.POINTER(XsCorrectionConfig)]),
     "xs_run_iterative_correction": (C.c_int, [_P, _P, _P, C.POINTER(XsGeometry),
                                               C.POINTER(XsSpectrum),

@@ -1,0 +1,589 @@
+// xscat_b200 — the reference CLI's `simulate` and `inspect` commands on the
+// B200 library (SURVEY.md §8(f) rank 4; REF tools/main.cpp:83-130, :298-330).
+//
+//   xscat_b200 simulate --config run.ini [--what primary|scatter|both]
+//                       [--angles a:b | i,j,...] [--seed N] [--threads N]
+//   xscat_b200 inspect --file f.xvox|f.xprj|f.xvol [--slice N] [--export out.pgm|out.csv]
+//
+// Native host code over the C ABI (include/xscat_gpu.h): the run configuration
+// grammar and validation (REF run_config.cpp:84-247), the input loaders and
+// file formats (csrc/files.cpp), the scan (xs_run_scan, or an xs_group when
+// XSCAT_DEVICES lists several devices) and REF's outputs: primary.xprj,
+// scatter.xprj and timing.csv in output_dir.  Messages and exit codes are
+// REF's: 0 ok, 2 validation or usage error, 3 runtime error.
+#include <algorithm>
+#include <cctype>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <filesystem>
+#include <fstream>
+#include <iostream>
+#include <map>
+#include <optional>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "xscat_gpu.h"
+
+namespace fs = std::filesystem;
+
+namespace {
+
+constexpr int kExitValidation = 2;
+constexpr int kExitRuntime = 3;
+
+struct Failure { // a runtime error: "error: <msg>", exit 3
+    std::string msg;
+};
+
+void check(int status, const char* (*msg)())
+{
+    if (status != XS_OK)
+        throw Failure{msg()};
+}
+
+const char* lib_error() { return xs_last_error(nullptr); }
+
+std::string strip(const std::string& s)
+{
+    size_t a = 0, b = s.size();
+    while (a < b && std::isspace(static_cast<unsigned char>(s[a])))
+        ++a;
+    while (b > a && std::isspace(static_cast<unsigned char>(s[b - 1])))
+        --b;
+    return s.substr(a, b - a);
+}
+
+std::vector<std::string> comma_list(const std::string& s)
+{
+    std::vector<std::string> out;
+    std::string item;
+    std::istringstream in(s);
+    while (std::getline(in, item, ','))
+        if (!(item = strip(item)).empty())
+            out.push_back(item);
+    return out;
+}
+
+// ------------------------------------------------------------ run config
+// [section] blocks of key = value lines, '#' comments (REF run_config.cpp:84-113)
+using Ini = std::map<std::string, std::map<std::string, std::string>>;
+
+Ini read_ini(const fs::path& path)
+{
+    std::ifstream in(path);
+    if (!in)
+        throw Failure{"cannot open config file " + path.string()};
+    Ini ini;
+    std::string section, line;
+    for (int no = 1; std::getline(in, line); ++no) {
+        if (const size_t h = line.find('#'); h != std::string::npos)
+            line.erase(h);
+        line = strip(line);
+        if (line.empty())
+            continue;
+        if (line.front() == '[') {
+            if (line.back() != ']')
+                throw Failure{path.string() + ":" + std::to_string(no) + ": malformed section header"};
+            section = strip(line.substr(1, line.size() - 2));
+            continue;
+        }
+        const size_t eq = line.find('=');
+        if (eq == std::string::npos)
+            throw Failure{path.string() + ":" + std::to_string(no) + ": expected key = value"};
+        ini[section][strip(line.substr(0, eq))] = strip(line.substr(eq + 1));
+    }
+    return ini;
+}
+
+struct RunConfig { // REF run_config.hpp:16-45
+    fs::path materials_dir, spectrum, response, phantom, output_dir = ".";
+    std::vector<std::string> materials;
+    double sdd = 0.0, sod = 0.0, pitch = 0.0;
+    int nu = 0, nv = 0, n_angles = 0;
+    xs_sim_config sim{};
+    int n_iterations = 3, every_kth = 2, n_classes = 3;
+    std::vector<std::string> class_map;
+    int threads = 1;
+};
+
+// Keys, defaults and error texts of REF build_run_config (run_config.cpp:117-171).
+class Reader {
+public:
+    Reader(const Ini& ini, std::vector<std::string>& errors) : ini_(ini), errors_(errors) {}
+    std::string str(const std::string& sec, const std::string& key, const std::string& dflt, bool required)
+    {
+        if (auto s = ini_.find(sec); s != ini_.end())
+            if (auto k = s->second.find(key); k != s->second.end())
+                return strip(k->second);
+        if (required)
+            errors_.push_back("missing required key [" + sec + "] " + key);
+        return dflt;
+    }
+    double num(const std::string& sec, const std::string& key, double dflt, bool required = false)
+    {
+        const std::string v = str(sec, key, "", required);
+        if (v.empty())
+            return dflt;
+        try {
+            size_t used = 0;
+            const double x = std::stod(v, &used);
+            if (used != v.size())
+                throw std::invalid_argument(v);
+            return x;
+        } catch (...) {
+            errors_.push_back("[" + sec + "] " + key + ": cannot parse number '" + v + "'");
+            return dflt;
+        }
+    }
+    long long integer(const std::string& sec, const std::string& key, long long dflt, bool required = false)
+    {
+        return static_cast<long long>(num(sec, key, static_cast<double>(dflt), required));
+    }
+
+private:
+    const Ini& ini_;
+    std::vector<std::string>& errors_;
+};
+
+RunConfig build_config(const Ini& ini, const fs::path& base, std::vector<std::string>& errors)
+{
+    Reader r(ini, errors);
+    RunConfig c;
+    auto at = [&](const std::string& p) -> fs::path {
+        if (p.empty())
+            return {};
+        const fs::path q(p);
+        return q.is_absolute() ? q : base / q;
+    };
+    c.materials_dir = at(r.str("paths", "materials_dir", "", true));
+    c.materials = comma_list(r.str("paths", "materials", "", true));
+    c.spectrum = at(r.str("paths", "spectrum", "", true));
+    c.response = at(r.str("paths", "detector_response", "", true));
+    c.phantom = at(r.str("paths", "phantom", "", true));
+    c.output_dir = at(r.str("paths", "output_dir", ".", false));
+
+    c.sdd = r.num("geometry", "sdd_cm", 0.0, true);
+    c.sod = r.num("geometry", "sod_cm", 0.0, true);
+    c.nu = static_cast<int>(r.integer("geometry", "det_nu", 0, true));
+    c.nv = static_cast<int>(r.integer("geometry", "det_nv", 0, true));
+    c.pitch = r.num("geometry", "pixel_pitch_cm", 0.0, true);
+    c.n_angles = static_cast<int>(r.integer("geometry", "n_angles", 0, true));
+
+    xs_sim_config_default(&c.sim);
+    c.sim.photons_total = static_cast<uint64_t>(r.integer("sim", "photons_total", 10000));
+    c.sim.splitting = static_cast<int>(r.integer("sim", "splitting", 1));
+    c.sim.roulette_survival = r.num("sim", "roulette_survival", 0.5);
+    c.sim.roulette_wmin_rel = r.num("sim", "roulette_wmin_rel", 1e-3);
+    c.sim.step_voxels = static_cast<int>(r.integer("sim", "step_voxels", 1));
+    c.sim.max_interactions = static_cast<int>(r.integer("sim", "max_interactions", 50));
+    c.sim.seed = static_cast<uint64_t>(r.integer("sim", "seed", 0));
+
+    c.n_iterations = static_cast<int>(r.integer("correction", "n_iterations", 3));
+    c.every_kth = static_cast<int>(r.integer("correction", "simulate_every_kth_angle", 2));
+    r.integer("correction", "mc_nu", 0);
+    r.integer("correction", "mc_nv", 0);
+    r.integer("correction", "recon_dim", 64);
+    c.n_classes = static_cast<int>(r.integer("correction", "n_classes", 3));
+    c.class_map = comma_list(r.str("correction", "class_map", "", false));
+    r.integer("correction", "sg_window", 15);
+    r.integer("correction", "sg_polyorder", 3);
+    r.integer("correction", "sg_auto_window", 1);
+    c.threads = static_cast<int>(r.integer("run", "threads", 1));
+    return c;
+}
+
+// REF validate_run_config (run_config.cpp:173-230), in its order
+void validate_config(const RunConfig& c, std::vector<std::string>& errors)
+{
+    auto file = [&](const fs::path& p, const std::string& what) {
+        if (!p.empty() && !fs::exists(p))
+            errors.push_back(what + " does not exist: " + p.string());
+    };
+    if (!c.materials_dir.empty() && !fs::is_directory(c.materials_dir))
+        errors.push_back("materials_dir is not a directory: " + c.materials_dir.string());
+    if (c.materials.empty())
+        errors.push_back("no material files listed");
+    for (const auto& m : c.materials)
+        file(c.materials_dir / m, "material file");
+    file(c.spectrum, "spectrum file");
+    file(c.response, "detector response file");
+    file(c.phantom, "phantom file");
+    if (!(c.sod > 0.0) || !(c.sdd > c.sod))
+        errors.push_back("geometry: require 0 < sod_cm < sdd_cm");
+    if (c.nu <= 0 || c.nv <= 0)
+        errors.push_back("geometry: det_nu/det_nv must be positive");
+    if (!(c.pitch > 0.0))
+        errors.push_back("geometry: pixel_pitch_cm must be positive");
+    if (c.n_angles < 1)
+        errors.push_back("geometry: n_angles must be >= 1");
+    if (c.sim.photons_total < 1)
+        errors.push_back("sim: photons_total must be >= 1");
+    if (c.sim.splitting < 1)
+        errors.push_back("sim: splitting must be >= 1");
+    if (!(c.sim.roulette_survival > 0.0 && c.sim.roulette_survival <= 1.0))
+        errors.push_back("sim: roulette_survival must lie in (0,1]");
+    if (c.sim.step_voxels < 1)
+        errors.push_back("sim: step_voxels must be >= 1");
+    if (c.sim.max_interactions < 1)
+        errors.push_back("sim: max_interactions must be >= 1");
+    if (c.n_iterations < 1)
+        errors.push_back("correction: n_iterations must be >= 1");
+    if (c.every_kth < 1)
+        errors.push_back("correction: simulate_every_kth_angle must be >= 1");
+    if (c.n_classes < 2 || c.n_classes > 4)
+        errors.push_back("correction: n_classes must be in [2,4]");
+    if (!c.class_map.empty() && static_cast<int>(c.class_map.size()) != c.n_classes)
+        errors.push_back("correction: class_map must list exactly n_classes entries");
+    for (const auto& e : c.class_map)
+        if (e.find(':') == std::string::npos)
+            errors.push_back("correction: class_map entry '" + e + "' must be material:density");
+    if (c.threads < 1)
+        errors.push_back("run: threads must be >= 1");
+}
+
+// --------------------------------------------------------------- inputs
+// REF load_inputs (run_config.cpp:232-266) through the library's loaders
+struct Inputs {
+    std::vector<xs_material_file*> files;
+    std::vector<xs_material> materials; // [0] = vacuum
+    xs_spectrum_file* spectrum = nullptr;
+    xs_response_file* response = nullptr;
+    xs_phantom_file* phantom_file = nullptr;
+    xs_phantom phantom{};
+    std::vector<double> angles;
+    xs_geometry geometry{};
+    ~Inputs()
+    {
+        for (auto* f : files)
+            xs_material_file_free(f);
+        xs_spectrum_file_free(spectrum);
+        xs_response_file_free(response);
+        xs_phantom_file_free(phantom_file);
+    }
+};
+
+void load_inputs(const RunConfig& c, Inputs& in)
+{
+    xs_material vacuum{};
+    vacuum.name = "vacuum";
+    in.materials.push_back(vacuum);
+    for (const auto& m : c.materials) {
+        xs_material_file* f = nullptr;
+        check(xs_material_file_load((c.materials_dir / m).string().c_str(), &f), lib_error);
+        in.files.push_back(f);
+        in.materials.push_back(*xs_material_file_get(f));
+    }
+    check(xs_spectrum_file_load(c.spectrum.string().c_str(), &in.spectrum), lib_error);
+    check(xs_response_file_load(c.response.string().c_str(), &in.response), lib_error);
+
+    check(xs_phantom_file_read(c.phantom.string().c_str(), (uint32_t)in.materials.size(), &in.phantom_file),
+          lib_error);
+    xs_phantom& p = in.phantom;
+    p = *xs_phantom_file_get(in.phantom_file);
+    p.n_materials = (int32_t)in.materials.size();
+    p.materials = in.materials.data();
+    check(xs_validate_phantom(&p), lib_error); // REF load_phantom (phantom.cpp:159)
+
+    // REF make_circular_geometry (scan_geometry.cpp:28-42)
+    in.angles.resize(c.n_angles);
+    for (int i = 0; i < c.n_angles; ++i)
+        in.angles[i] = 2.0 * 3.14159265358979323846 * i / c.n_angles;
+    in.geometry = xs_geometry{c.sdd, c.sod, c.nu, c.nv, c.pitch, c.n_angles, in.angles.data()};
+
+    // the class map must name loaded materials (REF resolves it on every command)
+    for (const auto& e : c.class_map) {
+        const std::string name = e.substr(0, e.find(':'));
+        std::stod(e.substr(e.find(':') + 1));
+        if (name == "air" || name == "vacuum")
+            continue;
+        bool found = false;
+        for (size_t i = 1; i < in.materials.size(); ++i)
+            found = found || name == in.materials[i].name;
+        if (!found)
+            throw Failure{"class_map references unknown material '" + name + "'"};
+    }
+}
+
+// ------------------------------------------------------------- commands
+struct Flags {
+    std::string config;
+    std::optional<uint64_t> seed;
+    std::optional<int> threads;
+};
+
+RunConfig config_or_exit(const Flags& f)
+{
+    const fs::path path = f.config;
+    const Ini ini = read_ini(path);
+    std::vector<std::string> errors;
+    RunConfig c = build_config(ini, path.parent_path(), errors);
+    if (f.seed)
+        c.sim.seed = *f.seed;
+    if (f.threads)
+        c.threads = *f.threads;
+    validate_config(c, errors);
+    if (!errors.empty()) {
+        std::cerr << "config validation failed (" << errors.size() << " problems):\n";
+        for (const auto& e : errors)
+            std::cerr << "  - " << e << "\n";
+        std::exit(kExitValidation);
+    }
+    return c;
+}
+
+// "a:b" (half-open range) or a comma list; all angles when the flag is absent
+std::vector<int> angle_subset(const std::string& text, int n, bool given)
+{
+    std::vector<int> out;
+    if (!given) {
+        for (int i = 0; i < n; ++i)
+            out.push_back(i);
+        return out;
+    }
+    if (const size_t colon = text.find(':'); colon != std::string::npos) {
+        for (int i = std::stoi(text.substr(0, colon)), e = std::stoi(text.substr(colon + 1)); i < e; ++i)
+            out.push_back(i);
+        return out;
+    }
+    std::string item;
+    std::istringstream in(text);
+    while (std::getline(in, item, ','))
+        if (!item.empty())
+            out.push_back(std::stoi(item));
+    return out;
+}
+
+std::vector<int32_t> devices_from_env()
+{
+    std::vector<int32_t> d;
+    if (const char* e = std::getenv("XSCAT_DEVICES"))
+        for (const auto& s : comma_list(e))
+            d.push_back(std::stoi(s));
+    return d;
+}
+
+int cmd_simulate(const Flags& flags, const std::string& what, const std::string& angles, bool angles_given)
+{
+    const RunConfig c = config_or_exit(flags);
+    Inputs in;
+    load_inputs(c, in);
+    std::printf("effective seed: %llu\n", static_cast<unsigned long long>(c.sim.seed));
+    int32_t q = 2; // ScanQuantity order: primary, scatter, both
+    if (what == "primary")
+        q = 0;
+    else if (what == "scatter")
+        q = 1;
+    else if (what != "both") {
+        std::cerr << "--what must be primary|scatter|both\n";
+        return kExitValidation;
+    }
+    const std::vector<int> subset = angle_subset(angles, c.n_angles, angles_given);
+    if (subset.empty()) {
+        std::cerr << "usage error: empty angle list\n";
+        return kExitValidation;
+    }
+    for (int a : subset)
+        if (a < 0 || a >= c.n_angles) {
+            std::cerr << "angle index " << a << " out of range\n";
+            return kExitValidation;
+        }
+    fs::create_directories(c.output_dir);
+
+    const size_t np = (size_t)c.nu * c.nv, n = subset.size();
+    std::vector<double> prim(q != 1 ? n * np : 0), scat(q != 0 ? n * np : 0), secs(n);
+    const std::vector<int32_t> sub(subset.begin(), subset.end());
+    const std::vector<int32_t> devs = devices_from_env();
+    if (devs.size() >= 2) { // one process, several devices (REF PAPER.md:215)
+        xs_group* g = nullptr;
+        check(xs_group_create(devs.data(), (int32_t)devs.size(), &g), lib_error);
+        auto err = [g] { return std::string(xs_group_last_error(g)); };
+        int st = xs_group_upload_phantom(g, &in.phantom);
+        if (st == XS_OK)
+            st = xs_group_upload_response(g, xs_response_file_get(in.response));
+        if (st == XS_OK)
+            st = xs_group_run_scan(g, &in.geometry, xs_spectrum_file_get(in.spectrum), &c.sim, sub.data(),
+                                   (int32_t)n, q, prim.empty() ? nullptr : prim.data(),
+                                   scat.empty() ? nullptr : scat.data(), secs.data());
+        const std::string msg = st == XS_OK ? "" : err();
+        xs_group_destroy(g);
+        if (st != XS_OK)
+            throw Failure{msg};
+    } else {
+        const char* dev = std::getenv("XSCAT_DEVICE");
+        xs_context* ctx = nullptr;
+        check(xs_ctx_create(dev ? std::atoi(dev) : 0, &ctx), lib_error);
+        int st = xs_upload_phantom(ctx, &in.phantom);
+        if (st == XS_OK)
+            st = xs_upload_response(ctx, xs_response_file_get(in.response));
+        if (st == XS_OK)
+            st = xs_run_scan(ctx, &in.geometry, xs_spectrum_file_get(in.spectrum), &c.sim, sub.data(), (int32_t)n,
+                             q, prim.empty() ? nullptr : prim.data(), scat.empty() ? nullptr : scat.data(),
+                             secs.data());
+        const std::string msg = st == XS_OK ? "" : xs_last_error(ctx);
+        xs_ctx_destroy(ctx);
+        if (st != XS_OK)
+            throw Failure{msg};
+    }
+    if (q != 1)
+        check(xs_stack_file_save((c.output_dir / "primary.xprj").string().c_str(), c.nu, c.nv, (int32_t)n,
+                                 prim.data()),
+              lib_error);
+    if (q != 0)
+        check(xs_stack_file_save((c.output_dir / "scatter.xprj").string().c_str(), c.nu, c.nv, (int32_t)n,
+                                 scat.data()),
+              lib_error);
+    std::ofstream timing(c.output_dir / "timing.csv");
+    timing << "angle_idx,seconds\n";
+    double total = 0.0;
+    for (size_t i = 0; i < n; ++i) {
+        timing << subset[i] << "," << secs[i] << "\n";
+        total += secs[i];
+    }
+    timing << "total," << total << "\n";
+    std::printf("simulated %zu angles in %.2f s (%.3f s/projection)\n", n, total, total / n);
+    return 0;
+}
+
+bool ends_with(const std::string& s, const char* suf)
+{
+    const size_t k = std::char_traits<char>::length(suf);
+    return s.size() >= k && s.compare(s.size() - k, k, suf) == 0;
+}
+
+int cmd_inspect(const std::string& path, int slice, const std::string& out)
+{
+    if (ends_with(path, ".xvox")) {
+        int32_t d[3];
+        double vs[3], o[3];
+        uint32_t nm = 0;
+        check(xs_phantom_file_info(path.c_str(), d, vs, o, &nm), lib_error);
+        std::printf("XVOX1 phantom: dims %d x %d x %d, voxel %.4f x %.4f x %.4f cm, "
+                    "origin (%.3f, %.3f, %.3f), %u materials\n",
+                    d[0], d[1], d[2], vs[0], vs[1], vs[2], o[0], o[1], o[2], nm);
+    } else if (ends_with(path, ".xprj")) {
+        int32_t nu = 0, nv = 0, na = 0;
+        check(xs_stack_file_info(path.c_str(), &nu, &nv, &na), lib_error);
+        std::vector<double> img((size_t)nu * nv * na);
+        check(xs_stack_file_load(path.c_str(), img.data()), lib_error); // (REF loads the stack)
+        std::printf("XPRJ1 stack: %d x %d pixels, %d angles\n", nu, nv, na);
+    } else if (ends_with(path, ".xvol")) {
+        int32_t d[3];
+        double vs[3];
+        check(xs_volume_file_info(path.c_str(), d, vs), lib_error);
+        std::vector<float> v((size_t)d[0] * d[1] * d[2]);
+        check(xs_volume_file_load(path.c_str(), v.data()), lib_error);
+        std::printf("XVOL1 volume: dims %d x %d x %d, voxel %.4f x %.4f x %.4f cm\n", d[0], d[1], d[2], vs[0],
+                    vs[1], vs[2]);
+        if (!out.empty()) {
+            const int iz = slice < 0 ? d[2] / 2 : slice;
+            if (iz < 0 || iz >= d[2]) // REF volume_slice_z
+                throw Failure{"volume_slice_z: slice index out of range"};
+            const size_t plane = (size_t)d[0] * d[1];
+            const float* s = v.data() + (size_t)iz * plane;
+            if (ends_with(out, ".csv")) { // REF save_slice_csv
+                std::ofstream f(out);
+                if (!f)
+                    throw Failure{"cannot write " + out};
+                for (int y = 0; y < d[1]; ++y)
+                    for (int x = 0; x < d[0]; ++x)
+                        f << (double)s[(size_t)y * d[0] + x] << (x + 1 == d[0] ? '\n' : ',');
+            } else { // REF save_slice_pgm, range from the slice
+                double lo = *std::min_element(s, s + plane), hi = *std::max_element(s, s + plane);
+                if (!(hi > lo))
+                    hi = lo + 1.0;
+                std::ofstream f(out, std::ios::binary);
+                if (!f)
+                    throw Failure{"cannot write " + out};
+                f << "P5\n" << d[0] << " " << d[1] << "\n255\n";
+                for (size_t i = 0; i < plane; ++i) {
+                    const double t = std::clamp(((double)s[i] - lo) / (hi - lo), 0.0, 1.0);
+                    const unsigned char b = static_cast<unsigned char>(t * 255.0 + 0.5);
+                    f.write(reinterpret_cast<const char*>(&b), 1);
+                }
+            }
+            std::printf("wrote slice %d to %s\n", iz, out.c_str());
+        }
+    } else {
+        std::cerr << "unknown file type (expected .xvox/.xprj/.xvol)\n";
+        return kExitValidation;
+    }
+    return 0;
+}
+
+int usage(const std::string& why)
+{
+    std::cerr << why << "\n"
+              << "usage: xscat_b200 simulate --config FILE [--what primary|scatter|both] [--angles a:b|i,j,...]\n"
+              << "                            [--seed N] [--threads N]\n"
+              << "       xscat_b200 inspect --file FILE [--slice N] [--export out.pgm|out.csv]\n";
+    return kExitValidation;
+}
+
+} // namespace
+
+int main(int argc, char** argv)
+{
+    if (argc < 2)
+        return usage("a subcommand is required");
+    const std::string cmd = argv[1];
+    std::map<std::string, std::string> opt;
+    for (int i = 2; i < argc; ++i) {
+        std::string a = argv[i];
+        if (a.rfind("--", 0) != 0)
+            return usage("unexpected argument: " + a);
+        std::string value;
+        if (const size_t eq = a.find('='); eq != std::string::npos) {
+            value = a.substr(eq + 1);
+            a = a.substr(0, eq);
+        } else if (i + 1 < argc) {
+            value = argv[++i];
+        } else {
+            return usage(a + ": missing value");
+        }
+        opt[a] = value;
+    }
+    auto allowed = [&](std::initializer_list<const char*> names) -> std::string {
+        for (const auto& [k, v] : opt)
+            if (std::none_of(names.begin(), names.end(), [&](const char* n) { return k == n; }))
+                return k;
+        return "";
+    };
+    try {
+        Flags flags;
+        try {
+            if (opt.count("--seed"))
+                flags.seed = std::stoull(opt["--seed"]);
+            if (opt.count("--threads"))
+                flags.threads = std::stoi(opt["--threads"]);
+        } catch (const std::exception&) {
+            return usage("--seed / --threads: not a number");
+        }
+        if (cmd == "simulate") {
+            if (const std::string bad = allowed({"--config", "--seed", "--threads", "--what", "--angles"}); !bad.empty())
+                return usage("simulate: unknown option " + bad);
+            if (!opt.count("--config"))
+                return usage("simulate: --config is required");
+            flags.config = opt["--config"];
+            return cmd_simulate(flags, opt.count("--what") ? opt["--what"] : "both", opt["--angles"],
+                                opt.count("--angles") > 0);
+        }
+        if (cmd == "inspect") {
+            if (const std::string bad = allowed({"--file", "--slice", "--export", "--seed", "--threads"}); !bad.empty())
+                return usage("inspect: unknown option " + bad);
+            if (!opt.count("--file"))
+                return usage("inspect: --file is required");
+            return cmd_inspect(opt["--file"], opt.count("--slice") ? std::stoi(opt["--slice"]) : -1, opt["--export"]);
+        }
+        return usage("unknown subcommand '" + cmd + "' (this build: simulate, inspect)");
+    } catch (const Failure& e) {
+        std::cerr << "error: " << e.msg << "\n";
+        return kExitRuntime;
+    } catch (const std::exception& e) {
+        std::cerr << "error: " << e.what() << "\n";
+        return kExitRuntime;
+    }
+}
