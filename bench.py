@@ -410,9 +410,11 @@ def gpu_arm(args):
                          "note": "5 B per REF voxel visit (u8 id + f32 density, SURVEY.md 8(d)) / "
                                  "walk-kernel time; traffic = ncu DRAM bytes of the same walk "
                                  "launches, mostly walker-state streaming. The device grid is an "
-                                 "8-bit palette (1 B/voxel) with uniform blocks crossed without "
-                                 "loads, so the REF byte model does not bind: the walk is "
-                                 "issue-bound (see 'issue')"},
+                                 "8-bit palette (1 B/voxel) with uniform blocks and same-code runs "
+                                 "crossed without loads, so the REF byte model does not bind (frac "
+                                 "> 1 means the walk crosses REF's voxel visits faster than HBM "
+                                 "could stream REF's bytes for them): the walk is issue-bound, see "
+                                 "'issue' (achieved / peak warp instructions per second)"},
             "cpu_baseline": cpu,
             "clocks": clocks,
             "wall_s": wall,
