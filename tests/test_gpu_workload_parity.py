@@ -75,6 +75,27 @@ def test_c3_scene_replay_1e6(orc, c3_scene, walk):
     _ledger_close(gpu, cpu)
 
 
+def test_c4_scan_angle_sharded_replay_vs_oracle(orc):
+    """C4 (BASELINE configs[3]: the 360-angle scan of the C3 scene),
+    angle-sharded over a device group, at four angles spread over the circle
+    -- the walk's run field then takes each travel direction (-x, -y, +x,
+    +y) -- and 2e5 photons each: every scan image replays the oracle's
+    projection at that angle (same criterion as _replay_compare)."""
+    w = configs.c4(photons=200_000)
+    subset = [0, 100, 190, 280]
+    grp = X.Group([0, 0], w.phantom, w.response)
+    scan = grp.run_scan(w.geometry, w.spectrum, w.config, subset, X.SCATTER)
+    atol = 1024.0 * tally_quantum(w.geometry, w.spectrum)
+    for k, a in enumerate(subset):
+        cpu = orc.simulate_scatter_stats(w.phantom, w.geometry, a, w.spectrum, w.response, w.config, CORES)
+        img, ref = scan.scatter.images[k].ravel(), np.asarray(cpu["image"]).ravel()
+        nz = ref > 0
+        bad = np.abs(img[nz] - ref[nz]) > 1e-9 * ref[nz] + atol
+        assert np.mean(bad) <= 1e-3, (a, np.mean(bad))
+        assert np.all(np.abs(img[~nz]) <= atol), a
+        assert abs(img.sum() - ref.sum()) <= 1e-6 * ref.sum(), a
+
+
 @pytest.mark.parametrize("walk", [0, 1])
 def test_c3_history_ranges_bitwise_vs_oracle(orc, c3_scene, walk):
     """C3 scene, three ranges of 2000 histories (low, middle and high
