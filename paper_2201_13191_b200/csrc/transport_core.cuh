@@ -239,7 +239,9 @@ struct SharedLog {
     }
 };
 
-template <int FMT, bool REG>
+// SM (walk kernel only): the <= 4 palette entries of REG in shared memory
+// (T[c * kBlock]) instead of registers, for walk occupancy.
+template <int FMT, bool REG, bool SM = false>
 struct MuTab {
     double t0, t1, t2, t3;
     double* T;
@@ -299,6 +301,8 @@ struct MuTab {
 
     __device__ __forceinline__ double mu(const TransportParams& P, int code, float dens) const
     {
+        if (REG && SM)
+            return T[(code & 3) * kBlock];
         if (REG) {
             const double lo = (code & 1) ? t1 : t0;
             const double hi = (code & 1) ? t3 : t2;
@@ -517,8 +521,8 @@ __device__ __forceinline__ int cross_n(double tn, double e, double rd, double tm
 // only in the next step.
 // RUN: the run field (Grid::run_*) is used along x (1), y (2), the axis the
 // grid says (3, runtime), or not at all (0).
-template <int FMT, bool REG, bool SKIP, int RUN = 3>
-__device__ __forceinline__ bool walk_step(const TransportParams& P, const MuTab<FMT, REG>& tab,
+template <int FMT, bool REG, bool SKIP, int RUN = 3, bool SM = false>
+__device__ __forceinline__ bool walk_step(const TransportParams& P, const MuTab<FMT, REG, SM>& tab,
                                           Walk& w)
 {
     const Grid& G = P.G;

@@ -51,7 +51,7 @@ namespace {
 #define XSW_REFILL_EXACT 4 // the voxel walk refills sooner (its steps are short): -3%
 #endif
 #ifndef XSW_EXACT_BLOCKS
-#define XSW_EXACT_BLOCKS (XSW_WALK_BLOCKS + 1)
+#define XSW_EXACT_BLOCKS 7 // the voxel walk: 72 registers
 #endif
 #ifndef XSW_REFILL
 #define XSW_REFILL 8
@@ -72,6 +72,9 @@ namespace {
 #ifndef XSW_ADMIT_MINB
 #define XSW_ADMIT_MINB 1
 #endif
+#ifndef XSW_WALK_MU_SMEM
+#define XSW_WALK_MU_SMEM 1 // walk: the register mu table (<= 4 palette entries) in shared memory
+#endif
 #ifndef XSW_INNER
 #define XSW_INNER 3 // block steps per walk-loop trip between the warp's refill checks
                     // (C3 walk: 1 -> 212, 2 -> 200, 3 -> 193, 4 -> 204, 5 -> 201 ms)
@@ -79,8 +82,9 @@ namespace {
 constexpr int kRefill = XSW_REFILL; // idle lanes that trigger a warp's refill in the walk kernel
 
 #ifndef XSW_WALK_BLOCKS
-#define XSW_WALK_BLOCKS 6 // resident walk blocks per SM (<= 80 registers; 7-8 spill or slow the macro walk;
-                          // the exact walk is lighter and runs one more)
+#define XSW_WALK_BLOCKS 7 // resident block-walk blocks per SM (8-bit palette): 72 registers, no
+                          // spills once the register mu table lives in shared memory (C3 walk
+                          // 189 -> 178 ms; 8 blocks spill); the 4-bit and march walks keep 6
 #endif
 
 // A history's scoring rays of one interaction: the slot and its Philox
@@ -323,10 +327,13 @@ __device__ __forceinline__ void store_mu(const WaveRays& R, uint32_t i, const Mu
     }
 }
 
-template <int FMT, bool REG>
-__device__ __forceinline__ void load_mu(const WaveRays& R, uint32_t i, MuTab<FMT, REG>& tab)
+template <int FMT, bool REG, bool SM>
+__device__ __forceinline__ void load_mu(const WaveRays& R, uint32_t i, MuTab<FMT, REG, SM>& tab)
 {
-    if (REG) {
+    if (REG && SM) {
+        for (int c = 0; c < 4; ++c)
+            tab.T[c * kBlock] = __ldcs(&R.mu[(uint64_t)c * R.cap + i]);
+    } else if (REG) {
         tab.t0 = __ldcs(&R.mu[i]);
         tab.t1 = __ldcs(&R.mu[R.cap + i]);
         tab.t2 = __ldcs(&R.mu[2ull * R.cap + i]);
@@ -440,8 +447,13 @@ __global__ void __launch_bounds__(kBlock, XSW_SETUP_MINB) wave_setup(const __gri
 }
 
 // -------------------------------------------------------------------- walk
+constexpr int walk_min_blocks(int fmt, bool skip, bool march)
+{
+    return !skip ? XSW_EXACT_BLOCKS : (fmt == kFmtP8 && !march ? XSW_WALK_BLOCKS : 6);
+}
+
 template <int FMT, bool REG, bool SKIP, bool MARCH, int RUN>
-__global__ void __launch_bounds__(kBlock, SKIP ? XSW_WALK_BLOCKS : XSW_EXACT_BLOCKS) wave_walk(const __grid_constant__ TransportParams P,
+__global__ void __launch_bounds__(kBlock, walk_min_blocks(FMT, SKIP, MARCH)) wave_walk(const __grid_constant__ TransportParams P,
                                                     const __grid_constant__ WaveArgs A)
 {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -451,7 +463,7 @@ __global__ void __launch_bounds__(kBlock, SKIP ? XSW_WALK_BLOCKS : XSW_EXACT_BLO
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
     const Grid& G = P.G;
-    MuTab<FMT, REG> tab;
+    MuTab<FMT, REG, REG && XSW_WALK_MU_SMEM> tab;
     tab.T = reinterpret_cast<double*>(smem) + threadIdx.x;
     tab.energy = -1.0;
     Walk w;
@@ -586,18 +598,18 @@ __global__ void __launch_bounds__(kBlock, SKIP ? XSW_WALK_BLOCKS : XSW_EXACT_BLO
         // warp's longest trip -- costs a warp reduction per trip, +5% walk time)
         c_wit += SKIP ? XSW_INNER : 2;
         if (walking) {
-            walking = walk_step<FMT, REG, SKIP, RUN>(P, tab, w);
+            walking = walk_step<FMT, REG, SKIP, RUN, REG && XSW_WALK_MU_SMEM>(P, tab, w);
             ++w.steps;
             // the voxel walk takes a second step per loop trip (halves the per-step
             // loop overhead: -21% walk time on speckled phantoms); the block walk
             // up to XSW_INNER steps between the warp's refill checks
             if (!SKIP && walking) {
-                walking = walk_step<FMT, REG, SKIP, RUN>(P, tab, w);
+                walking = walk_step<FMT, REG, SKIP, RUN, REG && XSW_WALK_MU_SMEM>(P, tab, w);
                 ++w.steps;
             }
 #pragma unroll 1
             for (int j = 1; j < (SKIP ? XSW_INNER : 1) && walking; ++j) {
-                walking = walk_step<FMT, REG, SKIP, RUN>(P, tab, w);
+                walking = walk_step<FMT, REG, SKIP, RUN, REG && XSW_WALK_MU_SMEM>(P, tab, w);
                 ++w.steps;
             }
             has_result = !walking;
@@ -1257,11 +1269,12 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
 
     const WaveSet K = wave_kernels_for(P);
     const size_t mu_smem = use_reg_w(P) ? 0 : (size_t)n_mu * kBlock * 8;
+    const size_t walk_smem = use_reg_w(P) ? (XSW_WALK_MU_SMEM ? (size_t)4 * kBlock * 8 : 0) : mu_smem;
     const size_t stat_smem = stat_words(P.n_bins) * 8;
     XSW_CHECK(cudaFuncSetAttribute((const void*)K.setup, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)std::max<size_t>(mu_smem, 1)));
     XSW_CHECK(cudaFuncSetAttribute((const void*)K.walk, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)std::max<size_t>(mu_smem, 1)));
+                                   (int)std::max<size_t>(walk_smem, 1)));
     XSW_CHECK(cudaFuncSetAttribute((const void*)K.event, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)stat_smem));
     XSW_CHECK(cudaFuncSetAttribute((const void*)wave_score, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1270,7 +1283,7 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
     XSW_CHECK(cudaFuncSetAttribute((const void*)wave_admit, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)admit_smem));
     int walk_per_sm = 0;
-    XSW_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&walk_per_sm, K.walk, kBlock, mu_smem));
+    XSW_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&walk_per_sm, K.walk, kBlock, walk_smem));
     if (walk_per_sm < 1)
         walk_per_sm = 1;
     int walk_use = walk_per_sm;
@@ -1357,7 +1370,7 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
                 K.setup<<<g_setup, kBlock, mu_smem, ps>>>(w.P, A);
                 dbg_wait("setup");
                 XSW_CHECK(cudaEventRecord(ev[0], ps));
-                K.walk<<<g_walk, kBlock, mu_smem, ps>>>(w.P, A);
+                K.walk<<<g_walk, kBlock, walk_smem, ps>>>(w.P, A);
                 dbg_wait("walk");
                 XSW_CHECK(cudaEventRecord(ev[1], ps));
                 wave_score<<<g_score, kBlock, stat_smem, ps>>>(w.P, A);
