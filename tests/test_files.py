@@ -155,7 +155,9 @@ def cli(*args, cwd=None):
 @pytest.mark.parametrize("name", sorted(GOLD["config"]))
 def test_cli_config_validation_matches_reference(name):
     case, cfg = GOLD["config"][name], OUT / "cfg"
-    r = cli("simulate", "--config", cfg / name)
+    # (an invalid --what stops a valid configuration after its inputs load,
+    # before any device work or output in the fixture tree)
+    r = cli("simulate", "--config", cfg / name, "--what", "nothing")
     if not case["ok"]:  # REF parse_ini throws: a runtime error
         assert r.returncode == 3
         assert r.stderr == "error: " + case["error"].replace("{dir}", str(cfg)) + "\n"
@@ -164,8 +166,9 @@ def test_cli_config_validation_matches_reference(name):
         assert r.returncode == 2
         assert r.stderr == f"config validation failed ({len(probs)} problems):\n" + "".join(
             f"  - {p}\n" for p in probs)
-    else:  # valid: inputs load, the seed is reported, then the device call
-        assert r.stdout.startswith("effective seed: 1234\n")
+    else:  # valid: inputs load and the seed is reported
+        assert r.returncode == 2 and r.stdout == "effective seed: 1234\n"
+        assert r.stderr == "--what must be primary|scatter|both\n"
 
 
 def test_cli_usage_errors_and_overrides():

@@ -24,7 +24,7 @@ CLI = ROOT / "paper_2201_13191_b200" / "bin" / "xscat_b200"
 
 def _run(tmp_path, args, env=None):
     work = tmp_path / "cfg"
-    shutil.copytree(CFG, work)
+    shutil.copytree(CFG, work, ignore=shutil.ignore_patterns("out"))
     import os
     e = dict(os.environ, **(env or {}))
     r = subprocess.run([str(CLI), "simulate", "--config", str(work / "good.ini"), *args], capture_output=True,
