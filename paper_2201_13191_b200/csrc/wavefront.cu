@@ -59,9 +59,11 @@ namespace {
 // minimum resident blocks per SM of the latency-bound kernels: register caps
 // that trade a few spills for occupancy (XSCAT_KTIME, C3, one pipeline, same
 // box: set-up 84.6 -> 72.5 ms at 64 registers, scoring 26.6 -> 22.0 ms at 40,
-// events 60.0 -> 53.0 ms at 80; admission is faster uncapped)
+// events 60.0 -> 53.0 ms at 80; admission is faster uncapped; later, with the
+// walk at seven blocks: set-up 67.1 -> 65.8 ms at 72 registers, events and
+// scoring unchanged at 5 / 7 and 10 / 16 blocks)
 #ifndef XSW_SETUP_MINB
-#define XSW_SETUP_MINB 8
+#define XSW_SETUP_MINB 7
 #endif
 #ifndef XSW_SCORE_MINB
 #define XSW_SCORE_MINB 12
