@@ -293,9 +293,9 @@ def gpu_arm(args):
         def e2e_step():
             pk = A.Packed()
             A.check(A.lib().xs_upload_phantom(ctx.h, A.C.byref(pk.phantom(w.phantom))), ctx.h)
-            r = proj.scatter_stats_mgpu(g, 0, spec, cfg, root=0, host_image=rank == 0)
-            if rank == 0:
-                img_h[:] = r.image.ravel()
+            # the image lands in the caller's host buffer (img_h, reused)
+            proj.scatter_stats_mgpu(g, 0, spec, cfg, root=0, host_image=rank == 0,
+                                    image_out=img_h if rank == 0 else None)
             torch.cuda.synchronize()
 
         e2e_step()

@@ -210,11 +210,15 @@ class Projector:
     # photon batches / angle ranges over the context's NCCL communicator
     def scatter_stats_mgpu(self, g: I.ScanGeometry, angle_idx: int, spec: I.Spectrum,
                            cfg: I.SimConfig, root: int = 0, d_image_ptr: int = 0,
-                           host_image: bool = True) -> SimResult:
+                           host_image: bool = True, image_out: Optional[np.ndarray] = None) -> SimResult:
         """xs_simulate_scatter_stats_mgpu: every rank calls it; the root's
-        result holds the whole projection, the others only `histories`."""
+        result holds the whole projection, the others only `histories`.
+        image_out: a caller-owned float64 host buffer of nu*nv pixels to fill
+        (reused across calls), else one is allocated."""
         pk = A.Packed()
-        img = np.empty(g.nu * g.nv) if host_image else None
+        if image_out is not None:
+            assert image_out.dtype == np.float64 and image_out.flags.c_contiguous and image_out.size == g.nu * g.nv
+        img = (image_out.reshape(-1) if image_out is not None else np.empty(g.nu * g.nv)) if host_image else None
         var = np.empty(g.nu * g.nv) if cfg.track_variance and host_image else None
         res = A.XsScatterResult()
         res.image = A.dptr(img) if img is not None else None
