@@ -98,8 +98,11 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_reference_rate(budget_s=15.0, calib=4000):
-    """REF simulate_scatter_stats on this host's cores (bounded C3 sample)."""
+def cpu_reference_rate(budget_s=15.0, calib=4000, reps=2):
+    """REF simulate_scatter_stats on this host's cores (bounded C3 sample):
+    the sample grows until one call takes >= budget/2, then `reps` more calls
+    of that size give the rate (histories / their summed time), the way the
+    reference arm times its steps."""
     sys.path.insert(0, str(ROOT / "tests"))
     import oracle_lib  # test infrastructure: the CPU baseline leg only
     from paper_2201_13191_b200 import configs
@@ -148,9 +151,13 @@ def cpu_reference_rate(budget_s=15.0, calib=4000):
     while dt < 0.5 * budget_s and n < 20_000_000:
         n = int(n * min(16.0, max(2.0, budget_s / max(dt, 1e-3))))
         dt, h = run(n)
-    return {"value": h / dt, "unit": UNIT, "cores": cores, "kind": kind,
-            "sample": f"C3 scene (bounded sample), {h} of 1e8 histories per call in {dt:.1f} s "
-                      f"with {cores} threads; includes REF's fixed 64-chunk 2048^2 image cost"}, \
+    samples = [run(n) for _ in range(reps)] if reps > 0 else [(dt, h)]
+    T, H = sum(d for d, _ in samples), sum(x for _, x in samples)
+    rates = [x / d for d, x in samples]
+    return {"value": H / T, "unit": UNIT, "cores": cores, "kind": kind,
+            "sample": f"C3 scene (bounded sample): {len(samples)} calls of {samples[0][1]} of 1e8 "
+                      f"histories, {T:.1f} s with {cores} threads (per call {min(rates):.3g}-{max(rates):.3g} "
+                      f"hist/s); includes REF's fixed 64-chunk 2048^2 image cost"}, \
         (kind, lib, run, n)
 
 
@@ -158,7 +165,7 @@ def reference_arm(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
-    base, (kind, lib, run, n) = cpu_reference_rate(budget_s=args.ref_seconds)
+    base, (kind, lib, run, n) = cpu_reference_rate(budget_s=args.ref_seconds, reps=0)
     for _ in range(args.warmup):
         run(max(1000, n // 4))
     times, hist = [], 0
