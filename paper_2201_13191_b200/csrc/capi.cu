@@ -606,6 +606,7 @@ void accumulate(xs_context* c, const xs_geometry& g, int angle, const xs_spectru
                 const xs_sim_config& cfg, uint64_t h0, uint64_t h1, unsigned long long* d_accum)
 {
     const xsi::Range range("xscat: scatter transport");
+    const auto tA = std::chrono::steady_clock::now();
     require_scene(c);
     const Plan plan = make_plan(g, spec, cfg);
     if (h1 > plan.n_hist)
@@ -726,10 +727,17 @@ void accumulate(xs_context* c, const xs_geometry& g, int angle, const xs_spectru
         if (!c->wave)
             c->wave = xsd::wave_create();
         xsd::WaveInfo info{};
+        const auto tB = std::chrono::steady_clock::now();
         cuda_check(xsd::wave_run(c->wave, P, c->sm_count, n_slots, s, &info, c->ev0, c->wave_pipes),
                    "wavefront transport");
+        const auto tC = std::chrono::steady_clock::now();
         cuda_check(cudaEventRecord(c->ev1, s), "event");
         check_status(c, angle, &spec);
+        if (std::getenv("XSCAT_TIMING")) {
+            auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+            std::fprintf(stderr, "[xscat] accumulate: before %.1f ms, wave_run %.1f ms, status %.1f ms\n",
+                         ms(tA, tB), ms(tB, tC), ms(tC, std::chrono::steady_clock::now()));
+        }
         float ms = 0.f;
         cuda_check(cudaEventElapsedTime(&ms, c->ev0, c->ev1), "event time");
         c->last.kernel_ms = ms;

@@ -26,6 +26,9 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -185,6 +188,7 @@ int xs_simulate_scatter_stats_mgpu(xs_context* c, const xs_geometry* g, int32_t 
         xs_accum_layout L{};
         uint64_t n = 0, h0 = 0, h1 = 0;
         unsigned long long* acc = nullptr;
+        const auto t0 = std::chrono::steady_clock::now();
         agreed(c, cm, [&] {
             xsi::accumulate(c, *g, angle_idx, *spec, *cfg, 0, 0, nullptr); // REF's validation and messages
             n = xsi::history_count(*g, *spec, *cfg);
@@ -199,9 +203,16 @@ int xs_simulate_scatter_stats_mgpu(xs_context* c, const xs_geometry* g, int32_t 
             const xsi::Range range("xscat: ncclReduce of the tallies");
             nccl_check(ncclReduce(acc, acc, L.words, ncclUint64, ncclSum, root, cm->comm, s), "ncclReduce");
         }
+        const auto t1 = std::chrono::steady_clock::now();
         if (cm->rank == root) {
             const unsigned long long* src = acc;
             xsi::finalize(c, *g, *spec, *cfg, &src, 1, 0, n, out, d_image);
+            if (std::getenv("XSCAT_TIMING")) {
+                const auto t2 = std::chrono::steady_clock::now();
+                std::fprintf(stderr, "[xscat] mgpu: accumulate %.1f ms, finalize %.1f ms\n",
+                             std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                             std::chrono::duration<double, std::milli>(t2 - t1).count());
+            }
         } else {
             xsi::cuda(cudaStreamSynchronize(s), "reduce");
             out->histories = h1 - h0;

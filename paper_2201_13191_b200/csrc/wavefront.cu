@@ -29,6 +29,7 @@
 // bit-identical images and statistics.
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <unistd.h>
 #include <cstdlib>
@@ -1048,6 +1049,11 @@ struct WaveEngine {
     WavePipe pipe[kMaxPipes];
     unsigned long long* next_h = nullptr;
     cudaEvent_t fork = nullptr;
+    // the last memory-clamp decision: (requested slots, splitting, n_mu,
+    // pipes) -> slots; repeated calls reuse it (the buffers are already held)
+    // instead of asking cudaMemGetInfo, which took up to 63 ms per call
+    uint64_t clamp_key[4] = {0, 0, 0, 0};
+    uint32_t clamp_slots = 0;
 };
 
 namespace {
@@ -1230,6 +1236,7 @@ static cudaError_t pipe_prepare(WavePipe& w, const TransportParams& P, uint32_t 
 cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint32_t n_slots,
                      cudaStream_t s, WaveInfo* info, cudaEvent_t start, int n_pipes)
 {
+    const auto host_t0 = std::chrono::steady_clock::now();
     const uint64_t n_hist = P.h_end - P.h_begin;
     if (n_slots > n_hist)
         n_slots = (uint32_t)n_hist;
@@ -1241,7 +1248,10 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
     // per-lane mu table entries: palette codes (4-bit palette, up to 16) or
     // materials (8-bit palette / raw ids, up to kMaxMaterials)
     const int n_mu = use_reg_w(P) ? 4 : (P.G.fmt == kFmtP4 ? std::max(P.n_pal, 1) : kMaxMaterials);
-    { // live histories are bounded by device memory: the walker state grows
+    const uint64_t key[4] = {n_slots, (uint64_t)P.splitting, (uint64_t)n_mu, (uint64_t)n_pipes};
+    if (e->clamp_slots && std::equal(key, key + 4, e->clamp_key)) {
+        n_slots = e->clamp_slots;
+    } else { // live histories are bounded by device memory: the walker state grows
       // with splitting (n_slots * (splitting + 1) ray entries), so a large
       // splitting factor gets fewer slots instead of failing the run
         size_t free_b = 0, total_b = 0;
@@ -1253,7 +1263,10 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
             while (n_slots > 4096 && (double)n_pipes * pipe_bytes((n_slots + n_pipes - 1) / n_pipes, P.splitting, n_mu) > budget)
                 n_slots >>= 1;
         }
+        std::copy(key, key + 4, e->clamp_key);
+        e->clamp_slots = n_slots;
     }
+    const auto host_ta = std::chrono::steady_clock::now();
     const uint32_t per = (n_slots + n_pipes - 1) / n_pipes;
     for (int p = 0; p < n_pipes; ++p) {
         WavePipe& w = e->pipe[p];
@@ -1264,6 +1277,7 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
             w.P.var_val = P.var_val + (size_t)p * per * P.var_cap;
         }
     }
+    const auto host_tb = std::chrono::steady_clock::now();
     if (!e->next_h)
         XSW_CHECK(cudaMalloc(&e->next_h, sizeof(unsigned long long)));
     if (!e->fork)
@@ -1305,6 +1319,7 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
     XSW_CHECK(resident((const void*)wave_score, stat_smem, &g_score));
     XSW_CHECK(resident((const void*)wave_admit, admit_smem, &g_admit));
 
+    const auto host_t1 = std::chrono::steady_clock::now();
     if (start) // buffers are allocated: the timed region starts here
         XSW_CHECK(cudaEventRecord(start, s));
     XSW_CHECK(cudaMemcpyAsync(e->next_h, &P.h_begin, sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
@@ -1338,7 +1353,9 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
     // device time in xs_launch_stats; meaningful with one pipeline)
     const bool ktime = std::getenv("XSCAT_KTIME") != nullptr;
     const int kEv = ktime ? 6 : 2;
-    const int check_every = 4;
+    int check_every = 4;
+    if (const char* v = std::getenv("XSCAT_CHECK_EVERY")) // experiment: waves between host checks
+        check_every = std::max(1, std::min(64, std::atoi(v)));
     const xsi::Range range("xscat: wavefront waves");
     for (;;) {
         for (int k = 0; k < check_every; ++k)
@@ -1430,6 +1447,7 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
             break;
         }
     }
+    const auto host_t2 = std::chrono::steady_clock::now();
     uint32_t waves = 0;
     float walk = 0.f;
     for (int p = 0; p < n_pipes; ++p) {
@@ -1461,6 +1479,13 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
         info->walk_blocks_per_sm = walk_per_sm;
         info->launches = launches;
         info->walk_ms = walk;
+    }
+    if (std::getenv("XSCAT_TIMING")) {
+        const auto t3 = std::chrono::steady_clock::now();
+        auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+        std::fprintf(stderr, "[xscat] wave_run: prepare %.1f ms (memory %.1f, buffers %.1f, kernels %.1f), waves %.1f ms (%u waves), tail %.1f ms\n",
+                     ms(host_t0, host_t1), ms(host_t0, host_ta), ms(host_ta, host_tb), ms(host_tb, host_t1),
+                     ms(host_t1, host_t2), waves, ms(host_t2, t3));
     }
     return cudaSuccess;
 }
