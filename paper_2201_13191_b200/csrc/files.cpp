@@ -372,8 +372,11 @@ int xs_phantom_file_read(const char* path, uint32_t n_materials_given, xs_phanto
         if (n_materials_given < h.n_materials)
             raise(std::string(path) + ": header declares " + std::to_string(h.n_materials) +
                   " materials, only " + std::to_string(n_materials_given) + " provided");
+        // (more voxels than the file holds -- or a product past 64 bits -- : the
+        // read below would fail)
+        if ((double)h.d[0] * (double)h.d[1] * (double)h.d[2] > 1e15)
+            raise(std::string(path) + ": truncated voxel data");
         const uint64_t n = count3(h.d);
-        // (more voxels than the file holds: the read below would fail)
         std::streamoff left = 0;
         if (in) {
             const std::streamoff at = in.tellg();
