@@ -1,8 +1,11 @@
-// xscat_b200 — the reference CLI's `simulate` and `inspect` commands on the
-// B200 library (SURVEY.md §8(f) rank 4; REF tools/main.cpp:83-130, :298-330).
+// xscat_b200 — the reference CLI's `simulate`, `reconstruct`, `correct` and
+// `inspect` commands on the B200 library (REF
+// tools/main.cpp:83-180, :298-330).
 //
 //   xscat_b200 simulate --config run.ini [--what primary|scatter|both]
 //                       [--angles a:b | i,j,...] [--seed N] [--threads N]
+//   xscat_b200 reconstruct --config run.ini --stack s.xprj [--flat f.xprj] --out v.xvol [--dim N]
+//   xscat_b200 correct --config run.ini --raw raw.xprj --flat flat.xprj [--seed N]
 //   xscat_b200 inspect --file f.xvox|f.xprj|f.xvol [--slice N] [--export out.pgm|out.csv]
 //
 // Native host code over the C ABI (include/xscat_gpu.h): the run configuration
@@ -106,6 +109,7 @@ struct RunConfig { // REF run_config.hpp:16-45
     int nu = 0, nv = 0, n_angles = 0;
     xs_sim_config sim{};
     int n_iterations = 3, every_kth = 2, n_classes = 3;
+    int mc_nu = 0, mc_nv = 0, recon_dim = 64, sg_window = 15, sg_polyorder = 3, sg_auto = 1;
     std::vector<std::string> class_map;
     int threads = 1;
 };
@@ -184,14 +188,14 @@ RunConfig build_config(const Ini& ini, const fs::path& base, std::vector<std::st
 
     c.n_iterations = static_cast<int>(r.integer("correction", "n_iterations", 3));
     c.every_kth = static_cast<int>(r.integer("correction", "simulate_every_kth_angle", 2));
-    r.integer("correction", "mc_nu", 0);
-    r.integer("correction", "mc_nv", 0);
-    r.integer("correction", "recon_dim", 64);
+    c.mc_nu = static_cast<int>(r.integer("correction", "mc_nu", 0));
+    c.mc_nv = static_cast<int>(r.integer("correction", "mc_nv", 0));
+    c.recon_dim = static_cast<int>(r.integer("correction", "recon_dim", 64));
     c.n_classes = static_cast<int>(r.integer("correction", "n_classes", 3));
     c.class_map = comma_list(r.str("correction", "class_map", "", false));
-    r.integer("correction", "sg_window", 15);
-    r.integer("correction", "sg_polyorder", 3);
-    r.integer("correction", "sg_auto_window", 1);
+    c.sg_window = static_cast<int>(r.integer("correction", "sg_window", 15));
+    c.sg_polyorder = static_cast<int>(r.integer("correction", "sg_polyorder", 3));
+    c.sg_auto = r.integer("correction", "sg_auto_window", 1) != 0 ? 1 : 0;
     c.threads = static_cast<int>(r.integer("run", "threads", 1));
     return c;
 }
@@ -256,6 +260,7 @@ struct Inputs {
     xs_phantom phantom{};
     std::vector<double> angles;
     xs_geometry geometry{};
+    std::vector<xs_class_spec> classes; // the resolved class map
     ~Inputs()
     {
         for (auto* f : files)
@@ -294,17 +299,21 @@ void load_inputs(const RunConfig& c, Inputs& in)
         in.angles[i] = 2.0 * 3.14159265358979323846 * i / c.n_angles;
     in.geometry = xs_geometry{c.sdd, c.sod, c.nu, c.nv, c.pitch, c.n_angles, in.angles.data()};
 
-    // the class map must name loaded materials (REF resolves it on every command)
+    // the class map names loaded materials (REF resolves it on every command)
     for (const auto& e : c.class_map) {
         const std::string name = e.substr(0, e.find(':'));
-        std::stod(e.substr(e.find(':') + 1));
-        if (name == "air" || name == "vacuum")
-            continue;
-        bool found = false;
-        for (size_t i = 1; i < in.materials.size(); ++i)
-            found = found || name == in.materials[i].name;
-        if (!found)
-            throw Failure{"class_map references unknown material '" + name + "'"};
+        const double density = std::stod(e.substr(e.find(':') + 1));
+        xs_class_spec cs{0, 0.0};
+        if (name != "air" && name != "vacuum") {
+            int id = -1;
+            for (size_t i = 1; i < in.materials.size(); ++i)
+                if (name == in.materials[i].name)
+                    id = (int)i;
+            if (id < 0)
+                throw Failure{"class_map references unknown material '" + name + "'"};
+            cs = xs_class_spec{id, density};
+        }
+        in.classes.push_back(cs);
     }
 }
 
@@ -448,6 +457,162 @@ int cmd_simulate(const Flags& flags, const std::string& what, const std::string&
     return 0;
 }
 
+// A projection stack file (REF load_stack): images widened to double;
+// `angles` (may be empty) must have one entry per image.
+struct Stack {
+    int32_t nu = 0, nv = 0, n = 0;
+    std::vector<double> images;
+};
+
+Stack load_stack(const std::string& path, const std::vector<double>& angles)
+{
+    Stack st;
+    check(xs_stack_file_info(path.c_str(), &st.nu, &st.nv, &st.n), lib_error);
+    if (!angles.empty() && (int)angles.size() != st.n)
+        throw Failure{path + ": angle list size does not match file (" + std::to_string(angles.size()) + " vs " +
+                      std::to_string(st.n) + ")"};
+    st.images.resize((size_t)st.nu * st.nv * st.n);
+    check(xs_stack_file_load(path.c_str(), st.images.data()), lib_error);
+    return st;
+}
+
+// The context every device command runs on (XSCAT_DEVICE, default 0).
+struct Device {
+    xs_context* ctx = nullptr;
+    Device()
+    {
+        const char* dev = std::getenv("XSCAT_DEVICE");
+        check(xs_ctx_create(dev ? std::atoi(dev) : 0, &ctx), lib_error);
+    }
+    ~Device() { xs_ctx_destroy(ctx); }
+    void ok(int st) const
+    {
+        if (st != XS_OK)
+            throw Failure{xs_last_error(ctx)};
+    }
+};
+
+// REF cmd_reconstruct (tools/main.cpp:132-152): FDK (Hann) of a stack, after
+// the ln conversion against a flat field when one is given.
+int cmd_reconstruct(const Flags& flags, const std::string& stack_path, const std::string& flat_path,
+                    const std::string& out_path, int dim)
+{
+    const RunConfig c = config_or_exit(flags);
+    Inputs in;
+    load_inputs(c, in);
+    Stack st = load_stack(stack_path, in.angles);
+    Device d;
+    if (!flat_path.empty()) {
+        const Stack flat = load_stack(flat_path, {});
+        if (flat.n < 1)
+            throw Failure{"vector::_M_range_check: __n (which is 0) >= this->size() (which is 0)"};
+        if (flat.nu != st.nu || flat.nv != st.nv)
+            throw Failure{"intensity_to_attenuation: flatfield dims mismatch"};
+        std::vector<double> att(st.images.size());
+        d.ok(xs_intensity_to_attenuation(d.ctx, st.images.data(), flat.images.data(), st.nu, st.nv, st.n, att.data(), 0));
+        st.images.swap(att);
+    }
+    const int32_t dims[3] = {dim, dim, dim};
+    double voxel[3];
+    xs_default_voxel_size(&in.geometry, dims, voxel);
+    std::vector<float> vol((size_t)dim * dim * dim);
+    d.ok(xs_fbp_reconstruct(d.ctx, st.images.data(), in.angles.data(), st.n, st.nu, st.nv, &in.geometry, dims, voxel,
+                            1, vol.data(), 0));
+    check(xs_volume_file_save(out_path.c_str(), dims, voxel, vol.data()), lib_error);
+    std::printf("wrote %s (%dx%dx%d)\n", out_path.c_str(), dim, dim, dim);
+    return 0;
+}
+
+// REF cmd_correct (tools/main.cpp:154-180): the iterative correction loop,
+// then corrected.xvol, corrected.xprj, iterations.txt and summary.csv.
+int cmd_correct(const Flags& flags, const std::string& raw_path, const std::string& flat_path)
+{
+    const RunConfig c = config_or_exit(flags);
+    Inputs in;
+    load_inputs(c, in);
+    std::printf("effective seed: %llu\n", static_cast<unsigned long long>(c.sim.seed));
+    const Stack raw = load_stack(raw_path, in.angles);
+    const Stack flat = load_stack(flat_path, {});
+    if (flat.n < 1)
+        throw Failure{"vector::_M_range_check: __n (which is 0) >= this->size() (which is 0)"};
+    fs::create_directories(c.output_dir);
+
+    xs_correction_config cc;
+    xs_correction_config_default(&cc);
+    cc.n_iterations = c.n_iterations;
+    cc.simulate_every_kth_angle = c.every_kth;
+    cc.mc_nu = c.mc_nu;
+    cc.mc_nv = c.mc_nv;
+    cc.recon_dims[0] = cc.recon_dims[1] = cc.recon_dims[2] = c.recon_dim;
+    cc.n_classes = c.n_classes;
+    cc.class_map = in.classes.empty() ? nullptr : in.classes.data();
+    cc.sim = c.sim;
+    cc.sg_window = c.sg_window;
+    cc.sg_polyorder = c.sg_polyorder;
+    cc.sg_auto_window = c.sg_auto;
+    // REF: flatfield dims against the raw stack (intensity_to_attenuation)
+    if (flat.nu != raw.nu || flat.nv != raw.nv)
+        throw Failure{"intensity_to_attenuation: flatfield dims mismatch"};
+    if (raw.nu != c.nu || raw.nv != c.nv)
+        throw Failure{"iteration 1, stage correction: correct_projections: stack dims mismatch"};
+
+    const int n_it = std::max(c.n_iterations, 0);
+    std::vector<xs_iteration_report> reports((size_t)std::max(n_it, 1));
+    const int32_t dims[3] = {c.recon_dim, c.recon_dim, c.recon_dim};
+    std::vector<float> vol((size_t)c.recon_dim * c.recon_dim * c.recon_dim);
+    std::vector<double> stack(raw.images.size());
+    Device d;
+    d.ok(xs_upload_response(d.ctx, xs_response_file_get(in.response)));
+    d.ok(xs_run_iterative_correction(d.ctx, raw.images.data(), flat.images.data(), &in.geometry,
+                                     xs_spectrum_file_get(in.spectrum), &cc, (int32_t)in.materials.size(),
+                                     in.materials.data(), vol.data(), stack.data(), reports.data(), 0));
+    double voxel[3];
+    xs_default_voxel_size(&in.geometry, dims, voxel); // REF correction.cpp:160
+    check(xs_volume_file_save((c.output_dir / "corrected.xvol").string().c_str(), dims, voxel, vol.data()),
+          lib_error);
+    check(xs_stack_file_save((c.output_dir / "corrected.xprj").string().c_str(), raw.nu, raw.nv, raw.n,
+                             stack.data()),
+          lib_error);
+    { // REF write_reports (correction.cpp:88-108)
+        std::ofstream out(c.output_dir / "iterations.txt");
+        if (!out)
+            throw Failure{"cannot write report " + (c.output_dir / "iterations.txt").string()};
+        for (int k = 0; k < n_it; ++k) {
+            const xs_iteration_report& r = reports[k];
+            out << "iteration=" << r.iteration << "\n"
+                << "seconds_fbp=" << r.seconds_fbp << "\n"
+                << "seconds_segmentation=" << r.seconds_segmentation << "\n"
+                << "seconds_mc_scatter=" << r.seconds_mc_scatter << "\n"
+                << "seconds_mc_primary=" << r.seconds_mc_primary << "\n"
+                << "seconds_postprocess=" << r.seconds_postprocess << "\n"
+                << "seconds_correction=" << r.seconds_correction << "\n"
+                << "seconds_total=" << r.seconds_total << "\n"
+                << "mc_seconds_per_projection=" << r.mc_seconds_per_projection << "\n"
+                << "mean_scatter_fraction=" << r.mean_scatter_fraction << "\n"
+                << "ncc_to_previous=" << r.ncc_to_previous << "\n"
+                << "negative_scatter_clamped=" << r.negative_scatter_clamped << "\n\n";
+        }
+    }
+    { // REF write_summary_csv (correction.cpp:110-123)
+        std::ofstream out(c.output_dir / "summary.csv");
+        if (!out)
+            throw Failure{"cannot write summary " + (c.output_dir / "summary.csv").string()};
+        out << "iteration,photons,splitting,step_size,mc_time_per_projection_s,"
+               "mc_time_per_iteration_s,correction_time_per_iteration_s\n";
+        for (int k = 0; k < n_it; ++k) {
+            const xs_iteration_report& r = reports[k];
+            out << r.iteration << "," << c.sim.photons_total << "," << c.sim.splitting << "," << c.sim.step_voxels
+                << "," << r.mc_seconds_per_projection << "," << (r.seconds_mc_scatter + r.seconds_mc_primary) << ","
+                << r.seconds_total << "\n";
+        }
+    }
+    for (int k = 0; k < n_it; ++k)
+        std::printf("iteration %d: %.1f s total, %.3f s/projection MC, scatter fraction %.3f, NCC %.5f\n",
+                    reports[k].iteration, reports[k].seconds_total, reports[k].mc_seconds_per_projection,
+                    reports[k].mean_scatter_fraction, reports[k].ncc_to_previous);
+    return 0;
+}
+
 bool ends_with(const std::string& s, const char* suf)
 {
     const size_t k = std::char_traits<char>::length(suf);
@@ -519,6 +684,8 @@ int usage(const std::string& why)
     std::cerr << why << "\n"
               << "usage: xscat_b200 simulate --config FILE [--what primary|scatter|both] [--angles a:b|i,j,...]\n"
               << "                            [--seed N] [--threads N]\n"
+              << "       xscat_b200 reconstruct --config FILE --stack S.xprj [--flat F.xprj] --out V.xvol [--dim N]\n"
+              << "       xscat_b200 correct --config FILE --raw R.xprj --flat F.xprj [--seed N] [--threads N]\n"
               << "       xscat_b200 inspect --file FILE [--slice N] [--export out.pgm|out.csv]\n";
     return kExitValidation;
 }
@@ -571,6 +738,24 @@ int main(int argc, char** argv)
             return cmd_simulate(flags, opt.count("--what") ? opt["--what"] : "both", opt["--angles"],
                                 opt.count("--angles") > 0);
         }
+        if (cmd == "reconstruct") {
+            if (const std::string bad = allowed({"--config", "--seed", "--threads", "--stack", "--flat", "--out", "--dim"});
+                !bad.empty())
+                return usage("reconstruct: unknown option " + bad);
+            if (!opt.count("--config") || !opt.count("--stack") || !opt.count("--out"))
+                return usage("reconstruct: --config, --stack and --out are required");
+            flags.config = opt["--config"];
+            return cmd_reconstruct(flags, opt["--stack"], opt["--flat"], opt["--out"],
+                                   opt.count("--dim") ? std::stoi(opt["--dim"]) : 64);
+        }
+        if (cmd == "correct") {
+            if (const std::string bad = allowed({"--config", "--seed", "--threads", "--raw", "--flat"}); !bad.empty())
+                return usage("correct: unknown option " + bad);
+            if (!opt.count("--config") || !opt.count("--raw") || !opt.count("--flat"))
+                return usage("correct: --config, --raw and --flat are required");
+            flags.config = opt["--config"];
+            return cmd_correct(flags, opt["--raw"], opt["--flat"]);
+        }
         if (cmd == "inspect") {
             if (const std::string bad = allowed({"--file", "--slice", "--export", "--seed", "--threads"}); !bad.empty())
                 return usage("inspect: unknown option " + bad);
@@ -578,7 +763,7 @@ int main(int argc, char** argv)
                 return usage("inspect: --file is required");
             return cmd_inspect(opt["--file"], opt.count("--slice") ? std::stoi(opt["--slice"]) : -1, opt["--export"]);
         }
-        return usage("unknown subcommand '" + cmd + "' (this build: simulate, inspect)");
+        return usage("unknown subcommand '" + cmd + "' (this build: simulate, reconstruct, correct, inspect)");
     } catch (const Failure& e) {
         std::cerr << "error: " << e.msg << "\n";
         return kExitRuntime;

@@ -216,3 +216,14 @@ def test_cli_inspect_prints_reference_headers(tmp_path):
     assert pgm[:len(head)] == head and np.array_equal(np.frombuffer(pgm[len(head):], np.uint8), want.ravel())
     r = cli("inspect", "--file", OUT / "ref_volume.xvol", "--slice", 5, "--export", tmp_path / "x.csv")
     assert r.returncode == 3 and r.stderr == "error: volume_slice_z: slice index out of range\n"
+
+
+def test_cli_reconstruct_and_correct_usage_and_input_errors():
+    good, stack = OUT / "cfg" / "good.ini", OUT / "ref_stack.xprj"  # a 2-image stack; good.ini has 8 angles
+    assert cli("reconstruct", "--config", good, "--stack", stack).returncode == 2  # --out missing
+    assert cli("correct", "--config", good, "--raw", stack).returncode == 2  # --flat missing
+    r = cli("reconstruct", "--config", good, "--stack", stack, "--out", "/tmp/never.xvol")
+    assert r.returncode == 3 and r.stderr == f"error: {stack}: angle list size does not match file (8 vs 2)\n"
+    r = cli("correct", "--config", good, "--raw", stack, "--flat", stack)
+    assert r.returncode == 3 and r.stdout == "effective seed: 1234\n"
+    assert r.stderr == f"error: {stack}: angle list size does not match file (8 vs 2)\n"
