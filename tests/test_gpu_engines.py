@@ -184,3 +184,31 @@ def test_run_field_every_travel_direction(orc, angle):
     assert a.total == b.total and a.ledger == b.ledger
     assert b.stats["walk_iterations"] < 0.95 * out[0, 1].stats["walk_iterations"]
     _replay_compare(b, orc.simulate_scatter_stats(ph, g, angle, spec, resp, cfg))
+
+
+@pytest.mark.parametrize("angle", [2, 5])
+def test_run_field_two_bits_shared_mu_table(orc, angle):
+    """5..8 palette entries on the 8-bit palette: two run bits (runs capped at
+    3) and the per-material mu table in shared memory (not the register
+    one): both engines bitwise, replayed against the oracle."""
+    ph = _phantom("p4")  # 5..8 (material, density) pairs
+    g = I.make_circular_geometry(100.0, 60.0, 32, 24, 0.8, 8)
+    spec, resp = I.kramers_spectrum(150.0), I.detector_response()
+    cfg = I.SimConfig(photons_total=20000, splitting=5, seed=99 + angle, track_variance=True)
+    ctx = X.projector.Context(0)
+    ctx.set_option("walk_mode", 1)
+    proj = X.Projector(ph, resp, ctx=ctx)
+    out = {}
+    for engine in (0, 1):
+        ctx.set_option("engine", engine)
+        out[engine] = proj.scatter_stats(g, angle, spec, cfg)
+    a, b = out[0], out[1]
+    assert _format_of(b.stats) == "p8" and 5 <= b.stats["palette_size"] <= 8
+    assert np.array_equal(a.image, b.image) and np.array_equal(a.variance, b.variance)
+    assert a.total == b.total and a.ledger == b.ledger
+    off = X.projector.Context(0)  # the same walk without the run field
+    off.set_option("walk_mode", 1)
+    off.set_option("runs", 0)
+    c = X.Projector(ph, resp, ctx=off).scatter_stats(g, angle, spec, cfg)
+    assert b.stats["walk_iterations"] < c.stats["walk_iterations"]
+    _replay_compare(b, orc.simulate_scatter_stats(ph, g, angle, spec, resp, cfg))
