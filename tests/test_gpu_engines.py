@@ -212,3 +212,30 @@ def test_run_field_two_bits_shared_mu_table(orc, angle):
     c = X.Projector(ph, resp, ctx=off).scatter_stats(g, angle, spec, cfg)
     assert b.stats["walk_iterations"] < c.stats["walk_iterations"]
     _replay_compare(b, orc.simulate_scatter_stats(ph, g, angle, spec, resp, cfg))
+
+
+def test_large_splitting_clamps_live_histories_and_stays_exact():
+    """Splitting 500 with 2e6 histories: the walker state of every history in
+    flight would need ~150 GB, so the wavefront engine lowers its live-history
+    count to the memory it has and remembers the decision per
+    request; the image equals a run with a small fixed slot count bit for
+    bit (the slot count never changes results), and a following
+    small-splitting call takes the full count again."""
+    ph = _phantom("p4reg")
+    g = I.make_circular_geometry(100.0, 60.0, 32, 24, 0.8, 4)
+    spec, resp = I.kramers_spectrum(150.0), I.detector_response()
+    cfg = I.SimConfig(photons_total=2_000_000, splitting=500, seed=8)
+    n = X.history_count(spec, cfg.photons_total)
+    ctx = X.projector.Context(0)
+    proj = X.Projector(ph, resp, ctx=ctx)
+    big = proj.scatter_stats(g, 1, spec, cfg)
+    assert big.stats["live_histories"] < n  # clamped
+    small_cfg = I.SimConfig(photons_total=20000, splitting=5, seed=8)
+    assert proj.scatter_stats(g, 1, spec, small_cfg).stats["live_histories"] >= X.history_count(spec, 20000)
+    again = proj.scatter_stats(g, 1, spec, cfg)
+    assert again.stats["live_histories"] == big.stats["live_histories"]
+    ctx.set_option("wave_slots", 65536)
+    fixed = proj.scatter_stats(g, 1, spec, cfg)
+    assert fixed.stats["live_histories"] <= 65536 + 2
+    for r in (again, fixed):
+        assert np.array_equal(big.image, r.image) and big.total == r.total and big.ledger == r.ledger
