@@ -1,11 +1,15 @@
-// xscat_b200 — the reference CLI's `simulate`, `reconstruct`, `correct` and
-// `inspect` commands on the B200 library (REF
-// tools/main.cpp:83-180, :298-330).
+// xscat_b200 — the reference CLI's commands (`simulate`, `reconstruct`,
+// `correct`, `phantom`, `metrics`, `inspect`) on the B200 library (SURVEY.md
+// §8(f) rank 4; REF tools/main.cpp:83-310).
 //
 //   xscat_b200 simulate --config run.ini [--what primary|scatter|both]
 //                       [--angles a:b | i,j,...] [--seed N] [--threads N]
 //   xscat_b200 reconstruct --config run.ini --stack s.xprj [--flat f.xprj] --out v.xvol [--dim N]
 //   xscat_b200 correct --config run.ini --raw raw.xprj --flat flat.xprj [--seed N]
+//   xscat_b200 phantom --kind empty|cube|cylinder|rods|cylinder-head-like --out p.xvox [--dim N]
+//                      [--voxel-cm X] [--radius-cm R] [--height-cm H] [--rods K] [--materials-dir D]
+//   xscat_b200 metrics --a A [--b B] [--roi r,c,h,w,br,bc,bh,bw] [--slice N] [--out m.csv]
+//                      [--profile r0,r1[,c0,c1]] [--profile-out p.csv]
 //   xscat_b200 inspect --file f.xvox|f.xprj|f.xvol [--slice N] [--export out.pgm|out.csv]
 //
 // Native host code over the C ABI (include/xscat_gpu.h): the run configuration
@@ -16,6 +20,7 @@
 // REF's: 0 ok, 2 validation or usage error, 3 runtime error.
 #include <algorithm>
 #include <cctype>
+#include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -492,7 +497,7 @@ struct Device {
     }
 };
 
-// REF cmd_reconstruct (tools/main.cpp:132-152): FDK (Hann) of a stack, after
+// REF cmd_reconstruct (tools/main.cpp:132-150): FDK (Hann) of a stack, after
 // the ln conversion against a flat field when one is given.
 int cmd_reconstruct(const Flags& flags, const std::string& stack_path, const std::string& flat_path,
                     const std::string& out_path, int dim)
@@ -523,7 +528,7 @@ int cmd_reconstruct(const Flags& flags, const std::string& stack_path, const std
     return 0;
 }
 
-// REF cmd_correct (tools/main.cpp:154-180): the iterative correction loop,
+// REF cmd_correct (tools/main.cpp:152-177): the iterative correction loop,
 // then corrected.xvol, corrected.xprj, iterations.txt and summary.csv.
 int cmd_correct(const Flags& flags, const std::string& raw_path, const std::string& flat_path)
 {
@@ -613,6 +618,298 @@ int cmd_correct(const Flags& flags, const std::string& raw_path, const std::stri
     return 0;
 }
 
+// ------------------------------------------------------ synthetic phantoms
+// REF synthetic.cpp:20-117 (the same generators as paper_2201_13191_b200/
+// synthetic.py): voxel centres origin + (i + 1/2) h, a voxel is inside a
+// cylinder when dx^2 + dy^2 <= r^2 and |z| <= half height.
+struct Phantom {
+    int n = 0;
+    double vs = 0.0, origin = 0.0;
+    std::vector<uint8_t> ids;
+    std::vector<float> dens;
+    double centre(int i) const { return origin + (i + 0.5) * vs; }
+};
+
+Phantom empty_phantom(int n, double vs)
+{
+    if (n <= 0) // REF validate_phantom
+        throw Failure{"phantom: dims must be positive"};
+    if (!(vs > 0.0))
+        throw Failure{"phantom: voxel size must be positive"};
+    Phantom p;
+    p.n = n;
+    p.vs = vs;
+    p.origin = (-n * vs) * 0.5;
+    p.ids.assign((size_t)n * n * n, 0);
+    p.dens.assign((size_t)n * n * n, 0.0f);
+    return p;
+}
+
+void fill_cylinder(Phantom& p, double cx, double cy, double r, double half, uint8_t id, double density)
+{
+    const double r2 = r * r;
+    for (int iz = 0; iz < p.n; ++iz) {
+        if (!(std::abs(p.centre(iz)) <= half))
+            continue;
+        for (int iy = 0; iy < p.n; ++iy) {
+            const double dy = p.centre(iy) - cy;
+            for (int ix = 0; ix < p.n; ++ix) {
+                const double dx = p.centre(ix) - cx;
+                if (dx * dx + dy * dy <= r2) {
+                    const size_t v = (size_t)ix + (size_t)p.n * ((size_t)iy + (size_t)p.n * iz);
+                    p.ids[v] = id;
+                    p.dens[v] = (float)density;
+                }
+            }
+        }
+    }
+}
+
+int cmd_phantom(const std::string& kind, const std::string& out, int dim, double vcm, const std::string& mdir,
+                double radius, double height, int n_rods)
+{
+    const double kPi = 3.14159265358979323846;
+    std::vector<xs_material_file*> files;
+    struct Free {
+        std::vector<xs_material_file*>& f;
+        ~Free()
+        {
+            for (auto* x : f)
+                xs_material_file_free(x);
+        }
+    } free_files{files};
+    auto mat = [&](const char* name) -> const xs_material& {
+        xs_material_file* f = nullptr;
+        check(xs_material_file_load((fs::path(mdir) / name).string().c_str(), &f), lib_error);
+        files.push_back(f);
+        return *xs_material_file_get(f);
+    };
+    Phantom p;
+    std::vector<xs_material> mats(1);
+    mats[0].name = "vacuum";
+    if (kind == "empty") { // simulate --what primary on it gives the flat field
+        mats.push_back(mat("water.mat"));
+        p = empty_phantom(dim, vcm);
+    } else if (kind == "cube") {
+        mats.push_back(mat("water.mat"));
+        const double edge = radius > 0 ? 2.0 * radius : dim * vcm * 0.5;
+        if (!(edge > 0.0))
+            throw Failure{"cube phantom: edge must be > 0"};
+        p = empty_phantom(dim, vcm);
+        const double half = 0.5 * edge;
+        for (int iz = 0; iz < dim; ++iz)
+            for (int iy = 0; iy < dim; ++iy)
+                for (int ix = 0; ix < dim; ++ix)
+                    if (std::abs(p.centre(iz)) <= half && std::abs(p.centre(iy)) <= half &&
+                        std::abs(p.centre(ix)) <= half) {
+                        const size_t v = (size_t)ix + (size_t)dim * ((size_t)iy + (size_t)dim * iz);
+                        p.ids[v] = 1;
+                        p.dens[v] = 1.0f;
+                    }
+    } else if (kind == "cylinder") {
+        mats.push_back(mat("water.mat"));
+        if (!(radius > 0.0 && height > 0.0))
+            throw Failure{"cylinder phantom: radius and height must be > 0"};
+        p = empty_phantom(dim, vcm);
+        fill_cylinder(p, 0.0, 0.0, radius, 0.5 * height, 1, 1.0);
+    } else if (kind == "rods") {
+        const xs_material& body = mat("cement.mat");
+        const xs_material& rod = mat("iron.mat");
+        mats.push_back(body);
+        mats.push_back(rod);
+        const double rod_r = radius * 0.08, ring_r = radius * 0.6;
+        if (!(radius > 0.0 && rod_r > 0.0))
+            throw Failure{"rods phantom: radii must be > 0"};
+        if (n_rods < 1)
+            throw Failure{"rods phantom: need at least one rod"};
+        if (ring_r + rod_r > radius)
+            throw Failure{"rods phantom: rods extend outside the body"};
+        p = empty_phantom(dim, vcm);
+        fill_cylinder(p, 0.0, 0.0, radius, 0.5 * height, 1, body.density_ref);
+        for (int k = 0; k < n_rods; ++k) {
+            const double phi = 2.0 * kPi * k / n_rods;
+            fill_cylinder(p, ring_r * std::cos(phi), ring_r * std::sin(phi), rod_r, 0.5 * height, 2, rod.density_ref);
+        }
+    } else if (kind == "cylinder-head-like") {
+        const xs_material& body = mat("aluminum.mat");
+        const xs_material& insert = mat("iron.mat");
+        mats.push_back(body);
+        mats.push_back(insert);
+        p = empty_phantom(dim, vcm);
+        const double extent = dim * vcm, body_r = 0.42 * extent, half = 0.5 * (0.8 * extent);
+        fill_cylinder(p, 0.0, 0.0, body_r, half, 1, body.density_ref);
+        for (int k = 0; k < 4; ++k) { // four air bores
+            const double phi = 2.0 * kPi * (k + 0.5) / 4.0;
+            fill_cylinder(p, 0.55 * body_r * std::cos(phi), 0.55 * body_r * std::sin(phi), 0.18 * body_r, half * 0.9, 0,
+                          0.0);
+        }
+        for (int k = 0; k < 8; ++k) { // a ring of eight dense inserts
+            const double phi = 2.0 * kPi * k / 8.0;
+            fill_cylinder(p, 0.8 * body_r * std::cos(phi), 0.8 * body_r * std::sin(phi), 0.07 * body_r, half * 0.8, 2,
+                          insert.density_ref);
+        }
+    } else {
+        std::cerr << "unknown phantom kind '" << kind << "' (empty|cube|cylinder|rods|cylinder-head-like)\n";
+        return kExitValidation;
+    }
+    xs_phantom ph{};
+    ph.dims[0] = ph.dims[1] = ph.dims[2] = dim;
+    ph.voxel_size[0] = ph.voxel_size[1] = ph.voxel_size[2] = vcm;
+    ph.origin[0] = ph.origin[1] = ph.origin[2] = p.origin;
+    ph.material_id = p.ids.data();
+    ph.density = p.dens.data();
+    ph.n_materials = (int32_t)mats.size();
+    ph.materials = mats.data();
+    check(xs_validate_phantom(&ph), lib_error);
+    check(xs_phantom_file_save(out.c_str(), &ph), lib_error);
+    std::printf("wrote %s (%d^3 voxels of %.3f cm)\n", out.c_str(), dim, vcm);
+    return 0;
+}
+
+// ----------------------------------------------------------------- metrics
+// REF metrics.cpp (mse, ncc with population statistics, cnr, profile_line)
+// over one image of a stack (.xprj) or a volume slice (.xvol).
+struct Image {
+    int nu = 0, nv = 0;
+    std::vector<double> v;
+    double at(int c, int r) const { return v[(size_t)r * nu + c]; }
+};
+
+Image load_image(const std::string& path, int slice)
+{
+    Image img;
+    if (path.size() >= 5 && path.compare(path.size() - 5, 5, ".xvol") == 0) {
+        int32_t d[3];
+        double vs[3];
+        check(xs_volume_file_info(path.c_str(), d, vs), lib_error);
+        std::vector<float> vol((size_t)d[0] * d[1] * d[2]);
+        check(xs_volume_file_load(path.c_str(), vol.data()), lib_error);
+        const int iz = slice < 0 ? d[2] / 2 : slice;
+        if (iz < 0 || iz >= d[2])
+            throw Failure{"volume_slice_z: slice index out of range"};
+        img.nu = d[0];
+        img.nv = d[1];
+        img.v.assign(vol.begin() + (size_t)iz * d[0] * d[1], vol.begin() + (size_t)(iz + 1) * d[0] * d[1]);
+        return img;
+    }
+    const Stack st = load_stack(path, {});
+    const int k = slice < 0 ? 0 : slice;
+    if (k >= st.n)
+        throw Failure{"vector::_M_range_check: __n (which is " + std::to_string(k) + ") >= this->size() (which is " +
+                      std::to_string(st.n) + ")"};
+    img.nu = st.nu;
+    img.nv = st.nv;
+    const size_t np = (size_t)st.nu * st.nv;
+    img.v.assign(st.images.begin() + (size_t)k * np, st.images.begin() + (size_t)(k + 1) * np);
+    return img;
+}
+
+double mean_of(const std::vector<double>& x)
+{
+    double s = 0.0;
+    for (double v : x)
+        s += v;
+    return s / x.size();
+}
+
+int cmd_metrics(const std::string& a_path, const std::string& b_path, const std::string& roi, int slice,
+                const std::string& out_csv, const std::string& profile, const std::string& profile_out)
+{
+    const Image a = load_image(a_path, slice);
+    std::ostringstream csv;
+    csv << "metric,value\n";
+    if (!b_path.empty()) {
+        const Image b = load_image(b_path, slice);
+        if (a.nu != b.nu || a.nv != b.nv)
+            throw Failure{"mse: image dims mismatch"};
+        if (a.v.empty())
+            throw Failure{"mse: size mismatch"};
+        double s = 0.0;
+        for (size_t i = 0; i < a.v.size(); ++i) {
+            const double d = a.v[i] - b.v[i];
+            s += d * d;
+        }
+        csv << "mse," << s / a.v.size() << "\n";
+        const double m1 = mean_of(a.v), m2 = mean_of(b.v);
+        double cov = 0.0, v1 = 0.0, v2 = 0.0;
+        for (size_t i = 0; i < a.v.size(); ++i) {
+            const double x = a.v[i] - m1, y = b.v[i] - m2;
+            cov += x * y;
+            v1 += x * x;
+            v2 += y * y;
+        }
+        if (!(v1 > 0.0) || !(v2 > 0.0))
+            throw Failure{"ncc: zero variance input"};
+        csv << "ncc," << cov / std::sqrt(v1 * v2) << "\n";
+    }
+    if (!roi.empty()) {
+        int q[8];
+        if (std::sscanf(roi.c_str(), "%d,%d,%d,%d,%d,%d,%d,%d", &q[0], &q[1], &q[2], &q[3], &q[4], &q[5], &q[6],
+                        &q[7]) != 8) {
+            std::cerr << "--roi wants roi_row,roi_col,h,w,bg_row,bg_col,h,w\n";
+            return kExitValidation;
+        }
+        auto rect = [&](int row, int col, int h, int w, const char* what) {
+            if (row < 0 || col < 0 || h <= 0 || w <= 0 || row + h > a.nv || col + w > a.nu)
+                throw Failure{std::string("cnr: ") + what + " rectangle outside image"};
+        };
+        rect(q[0], q[1], q[2], q[3], "ROI");
+        rect(q[4], q[5], q[6], q[7], "background");
+        if (q[0] < q[4] + q[6] && q[4] < q[0] + q[2] && q[1] < q[5] + q[7] && q[5] < q[1] + q[3])
+            throw Failure{"cnr: ROI and background rectangles overlap"};
+        double rs = 0.0;
+        for (int r = q[0]; r < q[0] + q[2]; ++r)
+            for (int c = q[1]; c < q[1] + q[3]; ++c)
+                rs += a.at(c, r);
+        const double roi_mean = rs / (static_cast<double>(q[2]) * q[3]);
+        double bs = 0.0;
+        const double bn = static_cast<double>(q[6]) * q[7];
+        for (int r = q[4]; r < q[4] + q[6]; ++r)
+            for (int c = q[5]; c < q[5] + q[7]; ++c)
+                bs += a.at(c, r);
+        const double bg_mean = bs / bn;
+        double bv = 0.0;
+        for (int r = q[4]; r < q[4] + q[6]; ++r)
+            for (int c = q[5]; c < q[5] + q[7]; ++c) {
+                const double d = a.at(c, r) - bg_mean;
+                bv += d * d;
+            }
+        bv /= bn;
+        if (!(bv > 0.0))
+            throw Failure{"cnr: zero background standard deviation"};
+        csv << "cnr," << std::abs(roi_mean - bg_mean) / std::sqrt(bv) << "\n";
+    }
+    if (!profile.empty()) { // a row band averaged per column
+        int r0 = 0, r1 = 0, c0 = 0, c1 = a.nu;
+        const int k = std::sscanf(profile.c_str(), "%d,%d,%d,%d", &r0, &r1, &c0, &c1);
+        if (k != 2 && k != 4) {
+            std::cerr << "--profile wants row0,row1[,col0,col1]\n";
+            return kExitValidation;
+        }
+        if (k == 2) {
+            c0 = 0;
+            c1 = a.nu;
+        }
+        if (r0 < 0 || c0 < 0 || r1 > a.nv || c1 > a.nu || r0 >= r1 || c0 >= c1)
+            throw Failure{"profile_line: empty or out-of-bounds range"};
+        std::ofstream pout(profile_out.empty() ? "profile.csv" : profile_out);
+        pout << "column,value\n";
+        for (int c = c0; c < c1; ++c) {
+            double sum = 0.0;
+            for (int r = r0; r < r1; ++r)
+                sum += a.at(c, r);
+            pout << c << "," << sum / (r1 - r0) << "\n";
+        }
+    }
+    if (out_csv.empty()) {
+        std::cout << csv.str();
+    } else {
+        std::ofstream o(out_csv);
+        o << csv.str();
+    }
+    return 0;
+}
+
 bool ends_with(const std::string& s, const char* suf)
 {
     const size_t k = std::char_traits<char>::length(suf);
@@ -686,6 +983,10 @@ int usage(const std::string& why)
               << "                            [--seed N] [--threads N]\n"
               << "       xscat_b200 reconstruct --config FILE --stack S.xprj [--flat F.xprj] --out V.xvol [--dim N]\n"
               << "       xscat_b200 correct --config FILE --raw R.xprj --flat F.xprj [--seed N] [--threads N]\n"
+              << "       xscat_b200 phantom --kind KIND --out P.xvox [--dim N] [--voxel-cm X] [--radius-cm R]\n"
+              << "                          [--height-cm H] [--rods K] [--materials-dir D]\n"
+              << "       xscat_b200 metrics --a A [--b B] [--roi r,c,h,w,br,bc,bh,bw] [--slice N] [--out CSV]\n"
+              << "                          [--profile r0,r1[,c0,c1]] [--profile-out CSV]\n"
               << "       xscat_b200 inspect --file FILE [--slice N] [--export out.pgm|out.csv]\n";
     return kExitValidation;
 }
@@ -756,6 +1057,30 @@ int main(int argc, char** argv)
             flags.config = opt["--config"];
             return cmd_correct(flags, opt["--raw"], opt["--flat"]);
         }
+        if (cmd == "phantom") {
+            if (const std::string bad = allowed({"--kind", "--out", "--dim", "--voxel-cm", "--radius-cm", "--height-cm",
+                                                 "--rods", "--materials-dir", "--seed", "--threads"});
+                !bad.empty())
+                return usage("phantom: unknown option " + bad);
+            if (!opt.count("--kind") || !opt.count("--out"))
+                return usage("phantom: --kind and --out are required");
+            auto num = [&](const char* k, double d) { return opt.count(k) ? std::stod(opt[k]) : d; };
+            return cmd_phantom(opt["--kind"], opt["--out"], opt.count("--dim") ? std::stoi(opt["--dim"]) : 64,
+                               num("--voxel-cm", 0.2),
+                               opt.count("--materials-dir") ? opt["--materials-dir"] : "data/materials",
+                               num("--radius-cm", 4.0), num("--height-cm", 10.0),
+                               opt.count("--rods") ? std::stoi(opt["--rods"]) : 8);
+        }
+        if (cmd == "metrics") {
+            if (const std::string bad = allowed({"--a", "--b", "--roi", "--slice", "--out", "--profile", "--profile-out",
+                                                 "--seed", "--threads"});
+                !bad.empty())
+                return usage("metrics: unknown option " + bad);
+            if (!opt.count("--a"))
+                return usage("metrics: --a is required");
+            return cmd_metrics(opt["--a"], opt["--b"], opt["--roi"], opt.count("--slice") ? std::stoi(opt["--slice"]) : -1,
+                               opt["--out"], opt["--profile"], opt["--profile-out"]);
+        }
         if (cmd == "inspect") {
             if (const std::string bad = allowed({"--file", "--slice", "--export", "--seed", "--threads"}); !bad.empty())
                 return usage("inspect: unknown option " + bad);
@@ -763,7 +1088,7 @@ int main(int argc, char** argv)
                 return usage("inspect: --file is required");
             return cmd_inspect(opt["--file"], opt.count("--slice") ? std::stoi(opt["--slice"]) : -1, opt["--export"]);
         }
-        return usage("unknown subcommand '" + cmd + "' (this build: simulate, reconstruct, correct, inspect)");
+        return usage("unknown subcommand '" + cmd + "' (simulate, reconstruct, correct, phantom, metrics, inspect)");
     } catch (const Failure& e) {
         std::cerr << "error: " << e.msg << "\n";
         return kExitRuntime;

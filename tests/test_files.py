@@ -23,6 +23,7 @@ import pytest
 from paper_2201_13191_b200 import files as F
 from paper_2201_13191_b200 import inputs as I
 from paper_2201_13191_b200.projector import ProjectionStack
+import paper_2201_13191_b200 as X
 
 ROOT = pathlib.Path(__file__).resolve().parents[1]
 OUT = ROOT / "tests" / "golden" / "files"
@@ -227,3 +228,73 @@ def test_cli_reconstruct_and_correct_usage_and_input_errors():
     r = cli("correct", "--config", good, "--raw", stack, "--flat", stack)
     assert r.returncode == 3 and r.stdout == "effective seed: 1234\n"
     assert r.stderr == f"error: {stack}: angle list size does not match file (8 vs 2)\n"
+
+
+@pytest.mark.parametrize("kind", ["empty", "cube", "cylinder", "rods", "cylinder-head-like"])
+def test_cli_phantom_matches_the_reference_generators(tmp_path, kind):
+    """`phantom` writes the XVOX1 file of REF's generators (synthetic.cpp,
+    mirrored by paper_2201_13191_b200.synthetic, which tests/test_inputs.py
+    pins to the compiled reference) with REF's materials and defaults."""
+    from paper_2201_13191_b200 import synthetic as S
+    mdir = I.write_reference_data(tmp_path / "data") / "materials"
+    out = tmp_path / "p.xvox"
+    r = cli("phantom", "--kind", kind, "--out", out, "--dim", 24, "--voxel-cm", 0.25, "--radius-cm", 2.5,
+            "--height-cm", 4.0, "--rods", 5, "--materials-dir", mdir)
+    assert r.returncode == 0, r.stderr
+    assert r.stdout == f"wrote {out} (24^3 voxels of 0.250 cm)\n"
+    m = {k: F.load_material(mdir / f"{k}.mat") for k in ("water", "cement", "iron", "aluminum")}
+    if kind == "empty":
+        ph = I.make_empty_phantom(24, 24, 24, (0.25,) * 3, [m["water"]])
+    elif kind == "cube":
+        ph = S.make_cube_phantom(24, 0.25, 5.0, m["water"], 1.0)
+    elif kind == "cylinder":
+        ph = S.make_cylinder_phantom(24, 0.25, 2.5, 4.0, m["water"], 1.0)
+    elif kind == "rods":
+        ph = S.make_rods_phantom(24, 0.25, 2.5, 4.0, m["cement"], m["cement"].density_ref, 5, 2.5 * 0.08,
+                                 2.5 * 0.6, m["iron"], m["iron"].density_ref)
+    else:
+        ph = S.make_cylinder_head_phantom(24, 0.25, m["aluminum"], m["aluminum"].density_ref, m["iron"],
+                                          m["iron"].density_ref)
+    F.save_phantom(ph, tmp_path / "want.xvox")
+    assert out.read_bytes() == (tmp_path / "want.xvox").read_bytes()
+
+
+def test_cli_phantom_errors():
+    r = cli("phantom", "--kind", "torus", "--out", "/tmp/never.xvox")
+    assert r.returncode == 2 and r.stderr.startswith("unknown phantom kind 'torus'")
+    r = cli("phantom", "--kind", "rods", "--out", "/tmp/never.xvox", "--rods", 0,
+            "--materials-dir", OUT / "cfg" / "data" / "materials")
+    assert r.returncode == 3 and r.stderr == "error: rods phantom: need at least one rod\n"
+    r = cli("phantom", "--kind", "cube", "--out", "/tmp/never.xvox", "--materials-dir", "/nonexistent")
+    assert r.returncode == 3 and r.stderr == "error: cannot open material file /nonexistent/water.mat\n"
+
+
+def test_cli_metrics_match_the_reference_formulas(tmp_path):
+    """`metrics` (REF metrics.cpp): MSE and NCC of two images, CNR of two
+    rectangles (population statistics), a row-band profile."""
+    a, b = F.load_stack(OUT / "ref_stack.xprj").images  # two 3 x 5 images
+    a = np.round(np.abs(np.log10(a + 1e-300)), 3)
+    b = a[::-1].copy() * 0.5 + 1.0
+    F.save_stack(X.ProjectionStack(np.zeros(2), np.stack([a, b])), tmp_path / "s.xprj")
+    F.save_stack(X.ProjectionStack(np.zeros(1), b[None]), tmp_path / "t.xprj")
+    A32 = np.asarray(a, np.float32).astype(np.float64)
+    B32 = np.asarray(b, np.float32).astype(np.float64)
+    r = cli("metrics", "--a", tmp_path / "s.xprj", "--b", tmp_path / "t.xprj", "--roi", "0,0,1,2,2,2,1,3",
+            "--profile", "0,2", "--profile-out", tmp_path / "p.csv")
+    assert r.returncode == 0, r.stderr
+    vals = dict(line.split(",") for line in r.stdout.splitlines()[1:])
+    d = A32 - B32
+    assert float(vals["mse"]) == pytest.approx(float("%g" % (np.sum(d * d) / d.size)), rel=1e-12)
+    x, y = A32 - A32.mean(), B32 - B32.mean()
+    assert float(vals["ncc"]) == pytest.approx(float("%g" % ((x * y).sum() / np.sqrt((x * x).sum() * (y * y).sum()))),
+                                               rel=1e-12)
+    roi, bg = A32[0:1, 0:2], A32[2:3, 2:5]
+    want = abs(roi.mean() - bg.mean()) / np.sqrt(((bg - bg.mean()) ** 2).mean())
+    assert float(vals["cnr"]) == pytest.approx(float("%g" % want), rel=1e-12)
+    prof = [line.split(",") for line in (tmp_path / "p.csv").read_text().splitlines()[1:]]
+    assert [int(c) for c, _ in prof] == list(range(5))
+    assert [float(v) for _, v in prof] == pytest.approx([float("%g" % v) for v in A32[0:2].mean(axis=0)], rel=1e-12)
+    r = cli("metrics", "--a", tmp_path / "s.xprj", "--roi", "0,0,2,2,1,1,2,2")
+    assert r.returncode == 3 and r.stderr == "error: cnr: ROI and background rectangles overlap\n"
+    r = cli("metrics", "--a", tmp_path / "s.xprj", "--profile", "1")
+    assert r.returncode == 2 and r.stderr == "--profile wants row0,row1[,col0,col1]\n"
