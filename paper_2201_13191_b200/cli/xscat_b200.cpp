@@ -55,25 +55,26 @@ void check(int status, const char* (*msg)())
 
 const char* lib_error() { return xs_last_error(nullptr); }
 
+// the string without leading / trailing white space (the C locale's isspace set)
 std::string strip(const std::string& s)
 {
-    size_t a = 0, b = s.size();
-    while (a < b && std::isspace(static_cast<unsigned char>(s[a])))
-        ++a;
-    while (b > a && std::isspace(static_cast<unsigned char>(s[b - 1])))
-        --b;
-    return s.substr(a, b - a);
+    static const char* const ws = " \t\n\v\f\r";
+    const size_t first = s.find_first_not_of(ws);
+    return first == std::string::npos ? std::string() : s.substr(first, s.find_last_not_of(ws) + 1 - first);
 }
 
+// "a, b,,c " -> {"a", "b", "c"}
 std::vector<std::string> comma_list(const std::string& s)
 {
-    std::vector<std::string> out;
-    std::string item;
-    std::istringstream in(s);
-    while (std::getline(in, item, ','))
-        if (!(item = strip(item)).empty())
-            out.push_back(item);
-    return out;
+    std::vector<std::string> items;
+    for (size_t at = 0; at <= s.size();) {
+        const size_t comma = std::min(s.find(',', at), s.size());
+        const std::string item = strip(s.substr(at, comma - at));
+        if (!item.empty())
+            items.push_back(item);
+        at = comma + 1;
+    }
+    return items;
 }
 
 // ------------------------------------------------------------ run config

@@ -47,14 +47,12 @@ int run(F&& f)
 
 [[noreturn]] void raise(const std::string& msg) { throw Error{XS_E_RUNTIME, msg}; }
 
+// the string without leading / trailing white space (the C locale's isspace set)
 std::string trim(const std::string& s)
 {
-    size_t a = 0, b = s.size();
-    while (a < b && std::isspace(static_cast<unsigned char>(s[a])))
-        ++a;
-    while (b > a && std::isspace(static_cast<unsigned char>(s[b - 1])))
-        --b;
-    return s.substr(a, b - a);
+    static const char* const ws = " \t\n\v\f\r";
+    const size_t first = s.find_first_not_of(ws);
+    return first == std::string::npos ? std::string() : s.substr(first, s.find_last_not_of(ws) + 1 - first);
 }
 
 // text line without its '#' comment
