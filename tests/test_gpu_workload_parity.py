@@ -75,6 +75,22 @@ def test_c3_scene_replay_1e6(orc, c3_scene, walk):
     _ledger_close(gpu, cpu)
 
 
+@pytest.mark.parametrize("step", [2, 3])
+def test_c3_scene_march_mode_replay(orc, c3_scene, step):
+    """REF's march mode (step_voxels > 1, trace.cpp:116-134) on the C3 scene:
+    the block march (midpoint samples summed inside uniform blocks) replayed
+    against the oracle's midpoint samples at 2e5 photons."""
+    w = configs.c3(photons=200_000, phantom=c3_scene.phantom)
+    cfg = w.config
+    cfg.step_voxels = step
+    proj = X.Projector(w.phantom, w.response, ctx=X.projector.Context(0))
+    gpu = proj.scatter_stats(w.geometry, 0, w.spectrum, cfg)
+    cpu = orc.simulate_scatter_stats(w.phantom, w.geometry, 0, w.spectrum, w.response, cfg, CORES)
+    assert gpu.histories == cpu["histories"]
+    _replay_compare(gpu, cpu, quantum=tally_quantum(w.geometry, w.spectrum))
+    _ledger_close(gpu, cpu)
+
+
 def test_c4_scan_angle_sharded_replay_vs_oracle(orc):
     """C4 (BASELINE configs[3]: the 360-angle scan of the C3 scene),
     angle-sharded over a device group, at four angles spread over the circle
