@@ -913,7 +913,7 @@ __device__ __noinline__ int event_select(const TransportParams& P, const Block& 
     atomicAdd(&S.pending, P.splitting);
     if constexpr (Q::kBatchScores) {
         // one batch entry; the set-up kernel draws its pixels in parallel
-        qs.push_score_batch(s, rng);
+        qs.push_score_batch(s, rng, kind);
         rng_skip(rng, 2u * (uint32_t)P.splitting, P.k0, P.k1, P.angle);
     } else {
         const uint32_t qbase = qs.reserve_scores(P.splitting);

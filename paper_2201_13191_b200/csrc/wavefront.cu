@@ -98,11 +98,20 @@ struct ScoreBatch {
     SlotRng rng;
 };
 
-struct WaveQueue {
-    ScoreBatch* batch; // one per interaction, splitting rays each
+struct alignas(8) WaveQueue {
+    ScoreBatch* batch; // one per interaction, splitting rays each: Compton from the
+                       // front, Rayleigh from the back (batch[cap - 1 - k]), so set-up
+                       // warps rarely mix the two kinds' branches
     uint32_t* free;    // slot
-    uint32_t n_batch, n_free;
+    uint32_t n_batch, n_batch_r; // (one 64-bit word: a warp reserves both ends in one atomic)
+    uint32_t n_free, cap;
 };
+
+// batch b of a wave's scoring work (Compton batches first, then Rayleigh)
+__device__ __forceinline__ const ScoreBatch& batch_at(const WaveQueue& q, uint32_t b)
+{
+    return b < q.n_batch ? q.batch[b] : q.batch[q.cap - 1u - (b - q.n_batch)];
+}
 
 struct WaveCtl {
     WaveQueue q[2];
@@ -151,7 +160,7 @@ struct WaveArgs {
 // some inputs.  Each lane records at most one push of each kind per window
 // and the kernel flushes them with full-warp ballots (flush_deferred).
 struct Deferred {
-    int32_t batch_slot, free_slot, rel_slot;
+    int32_t batch_slot, free_slot, rel_slot, batch_rayleigh;
     SlotRng rng;
 };
 
@@ -164,15 +173,16 @@ struct GlobalQ {
     Deferred* def;  // this lane's deferred pushes
     __device__ __forceinline__ Slot& slot(int s) const { return slots[s]; }
     static constexpr bool kBatchScores = true;
-    __device__ __forceinline__ void push_score_batch(int s, const SlotRng& r) const
+    __device__ __forceinline__ void push_score_batch(int s, const SlotRng& r, int kind) const
     {
         if (def->batch_slot < 0) {
             def->batch_slot = s;
+            def->batch_rayleigh = kind == K_RAYLEIGH ? 1 : 0;
             def->rng = r;
             return;
         }
         WaveQueue& q = ctl->q[out]; // (a second push in one window: not aggregated)
-        const uint32_t i = atomicAdd(&q.n_batch, 1u);
+        const uint32_t i = kind == K_RAYLEIGH ? q.cap - 1u - atomicAdd(&q.n_batch_r, 1u) : atomicAdd(&q.n_batch, 1u);
         q.batch[i].slot = (uint32_t)s;
         q.batch[i].rng = r;
     }
@@ -222,6 +232,7 @@ struct GlobalQ {
 __device__ __forceinline__ void deferred_reset(Deferred& d)
 {
     d.batch_slot = d.free_slot = d.rel_slot = -1;
+    d.batch_rayleigh = 0;
 }
 
 // All 32 lanes, converged: one reservation per queue for the warp's pushes.
@@ -234,14 +245,18 @@ __device__ __forceinline__ void flush_deferred(const TransportParams& P, const B
     const unsigned lt = (1u << lane) - 1u;
     WaveQueue& q = ctl->q[out];
     const unsigned mb = __ballot_sync(kFull, d.batch_slot >= 0);
-    if (mb) {
-        uint32_t base = 0;
+    if (mb) { // Compton batches from the front, Rayleigh ones from the back
+        const unsigned mr = __ballot_sync(kFull, d.batch_slot >= 0 && d.batch_rayleigh), mc = mb & ~mr;
+        unsigned long long both = 0;
         if (lane == 0)
-            base = atomicAdd(&q.n_batch, (uint32_t)__popc(mb));
-        base = __shfl_sync(kFull, base, 0);
+            both = atomicAdd(reinterpret_cast<unsigned long long*>(&q.n_batch),
+                             (unsigned long long)__popc(mc) | ((unsigned long long)__popc(mr) << 32));
+        both = __shfl_sync(kFull, both, 0);
+        const uint32_t bc = (uint32_t)both, br = (uint32_t)(both >> 32);
         if (d.batch_slot >= 0) {
-            const uint32_t i = base + (uint32_t)__popc(mb & lt);
-            if (XS_GUARD(i < n_slots, st, 16.0)) {
+            const uint32_t k = d.batch_rayleigh ? br + (uint32_t)__popc(mr & lt) : bc + (uint32_t)__popc(mc & lt);
+            if (XS_GUARD(k < n_slots, st, 16.0)) {
+                const uint32_t i = d.batch_rayleigh ? q.cap - 1u - k : k;
                 q.batch[i].slot = (uint32_t)d.batch_slot;
                 q.batch[i].rng = d.rng;
             }
@@ -359,7 +374,7 @@ __global__ void __launch_bounds__(kBlock, XSW_SETUP_MINB) wave_setup(const __gri
     extern __shared__ __align__(16) unsigned char smem[];
     WaveCtl* ctl = A.ctl;
     const WaveQueue& in = ctl->q[A.cur];
-    const uint32_t n_s = in.n_batch * (uint32_t)P.splitting, n = n_s + in.n_free;
+    const uint32_t n_s = (in.n_batch + in.n_batch_r) * (uint32_t)P.splitting, n = n_s + in.n_free;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         ctl->cursor = 0;
         ctl->ev_cursor = 0;
@@ -367,6 +382,7 @@ __global__ void __launch_bounds__(kBlock, XSW_SETUP_MINB) wave_setup(const __gri
         ctl->n_score = n_s;
         ctl->n_fin = 0;
         ctl->q[A.cur ^ 1].n_batch = 0;
+        ctl->q[A.cur ^ 1].n_batch_r = 0;
         ctl->q[A.cur ^ 1].n_free = 0;
     }
     MuTab<FMT, REG> tab;
@@ -381,7 +397,7 @@ __global__ void __launch_bounds__(kBlock, XSW_SETUP_MINB) wave_setup(const __gri
         bool walking;
         if (i < n_s) { // REF run_history :162-183
             const uint32_t b = i / (uint32_t)P.splitting, k = i - b * (uint32_t)P.splitting;
-            const ScoreBatch& sb = in.batch[b];
+            const ScoreBatch& sb = batch_at(in, b);
             const Slot& S = A.slots[sb.slot];
             double uu, uv;
             rng_pair_at(sb.rng, 2 * k, P.k0, P.k1, P.angle, uu, uv);
@@ -650,9 +666,9 @@ __global__ void __launch_bounds__(kBlock, XSW_SCORE_MINB) wave_score(const __gri
         const uint32_t i = base + (uint32_t)lane;
         int s = -1;
         uint64_t l0 = 0, l1 = 0, l2 = 0;
-        const bool is_score = i < n_s && XS_GUARD(in.batch[i / (uint32_t)P.splitting].slot < A.n_slots, st, 13.0);
+        const bool is_score = i < n_s && XS_GUARD(batch_at(in, i / (uint32_t)P.splitting).slot < A.n_slots, st, 13.0);
         if (is_score) {
-            s = (int)in.batch[i / (uint32_t)P.splitting].slot;
+            s = (int)batch_at(in, i / (uint32_t)P.splitting).slot;
             const uint32_t pix = __ldcs(&R.pix[i]);
             const double x = __ldcs(&R.pre[i]) * nl_exp(-__ldcs(&R.res[i]));
             if (!isfinite(x)) {
@@ -909,8 +925,8 @@ __global__ void wave_init(WaveCtl* ctl, uint32_t* stack, uint32_t n_slots, unsig
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         ctl->free_top = (int32_t)n_slots;
         ctl->next_h = h_begin; // this pipeline's last view of the shared counter
-        ctl->q[0].n_batch = ctl->q[0].n_free = 0;
-        ctl->q[1].n_batch = ctl->q[1].n_free = 0;
+        ctl->q[0].n_batch = ctl->q[0].n_free = ctl->q[0].n_batch_r = 0;
+        ctl->q[1].n_batch = ctl->q[1].n_free = ctl->q[1].n_batch_r = 0;
         ctl->waves = 0;
         ctl->live = 0;
     }
@@ -1333,6 +1349,7 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
         std::memset(&init, 0, sizeof init);
         for (int b = 0; b < 2; ++b) {
             init.q[b].batch = w.sq[b];
+            init.q[b].cap = per;
             init.q[b].free = w.fq[b];
         }
         init.free_stack = w.stack;
@@ -1427,7 +1444,8 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
             const WaveCtl& h = *w.host_ctl;
             // nothing left to admit (the shared counter, as this pipeline last saw it,
             // is past the end) and no history in flight
-            w.done = h.live == 0 && h.next_h >= P.h_end && h.q[w.cur].n_batch == 0 && h.q[w.cur].n_free == 0;
+            w.done = h.live == 0 && h.next_h >= P.h_end && h.q[w.cur].n_batch == 0 && h.q[w.cur].n_batch_r == 0 &&
+                     h.q[w.cur].n_free == 0;
             all_done = all_done && w.done;
         }
         if (hs.code != 0 || all_done)
