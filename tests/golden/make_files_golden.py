@@ -159,7 +159,8 @@ def main():
                                                "values": hexs(buf)})
 
     # ---- material tables: the bundled water table, then edits of it
-    data = I.write_reference_data(OUT / "data")
+    import tempfile
+    data = I.write_reference_data(pathlib.Path(tempfile.mkdtemp()) / "data")  # (copied into cfg/ below)
     water_txt = (data / "materials" / "water.mat").read_text()
     lines = water_txt.splitlines()
 
