@@ -1344,7 +1344,8 @@ static void upload_phantom_impl(xs_context* c, const xs_phantom* ph, bool on_dev
     }
 }
 
-// Host arrays through pinned staging: a ring of pinned buffers; worker
+// Host arrays through pinned staging (arrays the caller page-locked are
+// copied directly): a ring of pinned buffers; worker
 // threads copy their share of a chunk of the id / density arrays into the
 // chunk's buffer, and the last one to finish queues its DMA, while the others
 // go on to the next chunk.  Only the first chunk's copy is not hidden behind
@@ -1359,6 +1360,26 @@ static void upload_phantom_staged(xs_context* c, const xs_phantom* ph)
     }
     constexpr int kRing = 4;
     const size_t n = (size_t)ph->dims[0] * ph->dims[1] * ph->dims[2];
+    auto pinned = [](const void* p) {
+        cudaPointerAttributes a{};
+        if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        return a.type == cudaMemoryTypeHost;
+    };
+    if (pinned(ph->material_id) && pinned(ph->density)) { // page-locked by the caller: straight DMA
+        c->seg_ids.reserve(n);
+        c->seg_dens.reserve(n);
+        cuda_check(cudaMemcpyAsync(c->seg_ids.p, ph->material_id, n, cudaMemcpyHostToDevice, c->stream), "H2D");
+        cuda_check(cudaMemcpyAsync(c->seg_dens.p, ph->density, n * 4, cudaMemcpyHostToDevice, c->stream), "H2D");
+        xs_phantom dp = *ph;
+        dp.material_id = c->seg_ids.p;
+        dp.density = c->seg_dens.p;
+        upload_phantom_impl(c, &dp, true);
+        c->last_upload_bytes = n * 5;
+        return;
+    }
     const size_t chunk = std::min(n, (size_t)8 << 20); // voxels per chunk (40 MB of ids + densities)
     c->seg_ids.reserve(n);
     c->seg_dens.reserve(n);

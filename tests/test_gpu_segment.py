@@ -200,3 +200,40 @@ def test_staged_upload_matches_host_encoder(kind):
             ctx.upload(bad, resp)
         ctx.close()
     assert np.array_equal(out[0][0], out[1][0]) and out[0][1] == out[1][1]
+
+
+def _pinned(ph):
+    """The phantom with its id / density arrays in page-locked host memory."""
+    import dataclasses
+    import torch
+    ids = torch.from_numpy(np.ascontiguousarray(ph.material_id)).pin_memory().numpy()
+    dens = torch.from_numpy(np.ascontiguousarray(ph.density)).pin_memory().numpy()
+    return dataclasses.replace(ph, material_id=ids, density=dens)
+
+
+def test_pinned_and_multi_chunk_uploads_match_host_encoder():
+    """xs_upload_phantom with caller-pinned arrays (straight DMA) and with a
+    phantom of several 8M-voxel staging chunks (the pinned ring, 2.6 chunks)
+    gives the host encoder's grid: identical primary and scatter images."""
+    ph, g, angle, spec, resp, cfg = poly()
+    zi = np.arange(336) * 32 // 336  # 32^3 -> 256 x 256 x 336 (x fastest), same extent
+    up = lambda a: a.reshape(32, 32, 32).repeat(8, 1).repeat(8, 2)[zi].reshape(-1)
+    vs = ph.voxel_size
+    big = I.VoxelPhantom((256, 256, 336), (vs[0] / 8, vs[1] / 8, vs[2] * 32 / 336), ph.origin,
+                         up(ph.material_id), up(ph.density), ph.materials)
+    for phantom in (ph, big):
+        out = []
+        for path, arrays in ((0, phantom), (1, phantom), (1, _pinned(phantom))):
+            ctx = X.Context(0)
+            ctx.set_option("upload_path", path)
+            prim = X.Projector(arrays, resp, ctx=ctx).primary(g, angle, spec)  # (uploads)
+            out.append((prim, *_scatter(ctx, g, angle, spec, cfg)))
+            ctx.close()
+        for o in out[1:]:
+            assert np.array_equal(o[0], out[0][0]) and np.array_equal(o[1], out[0][1]) and o[2] == out[0][2]
+    bad = _pinned(rods(16))
+    bad.density[100], bad.material_id[100] = 0.5, 0
+    ctx = X.Context(0)
+    with pytest.raises(I.XscatError, match="vacuum voxel with nonzero density"):
+        ctx.upload(bad, resp)
+    ctx.close()
