@@ -99,8 +99,26 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_reference_rate(budget_s=15.0, calib=4000, reps=2):
-    """REF simulate_scatter_stats on this host's cores (bounded C3 sample):
+def workload_for(name, photons=None, phantom=None):
+    """SURVEY.md 8(d) workloads: C1 / C2 (the smaller parity configs), C3 (the
+    BASELINE metric's projection, the default)."""
+    from paper_2201_13191_b200 import configs
+    if name == "c1":
+        return configs.c1(photons=photons)
+    if name == "c2":
+        return configs.c2(photons=photons)
+    return configs.c3(photons=photons, phantom=phantom)
+
+
+def workload_text(w):
+    if w.name == "C3":
+        return WORKLOAD
+    return f"{w.name}: {w.description}"
+
+
+def cpu_reference_rate(budget_s=15.0, calib=4000, reps=2, workload="c3"):
+    """REF simulate_scatter_stats on this host's cores (bounded sample of the
+    workload's projection, C3 by default):
     the sample grows until one call takes >= budget/2, then `reps` more calls
     of that size give the rate (histories / their summed time), the way the
     reference arm times its steps."""
@@ -118,7 +136,14 @@ def cpu_reference_rate(budget_s=15.0, calib=4000, reps=2):
         lib = oracle_lib.oracle()
         kind = "port"
     cores = os.cpu_count() or 1
-    w = configs.c3(photons=calib)
+    import dataclasses
+    w = workload_for(workload, calib)
+    w_full = workload_for(workload, None, phantom=w.phantom)
+    W = w.name
+
+    def cfg_of(n):
+        return dataclasses.replace(w.config, photons_total=int(n))
+
     pk = A.Packed()
     ph, resp = pk.phantom(w.phantom), pk.response(w.response)
     g, spec = pk.geometry(w.geometry), pk.spectrum(w.spectrum)
@@ -128,7 +153,7 @@ def cpu_reference_rate(budget_s=15.0, calib=4000, reps=2):
         scene = lib.L.xr_scene_create(C.byref(ph), C.byref(resp))
 
         def run(n):
-            cfg = pk.config(configs.c3(photons=n, phantom=w.phantom).config)
+            cfg = pk.config(cfg_of(n))
             res = A.XsScatterResult()
             res.image = A.dptr(img)
             t = time.perf_counter()
@@ -139,7 +164,7 @@ def cpu_reference_rate(budget_s=15.0, calib=4000, reps=2):
             return dt, res.histories
     else:
         def run(n):
-            cfg = configs.c3(photons=n, phantom=w.phantom).config
+            cfg = cfg_of(n)
             t = time.perf_counter()
             r = lib.simulate_scatter_stats(w.phantom, w.geometry, 0, w.spectrum, w.response, cfg,
                                            cores)
@@ -156,9 +181,10 @@ def cpu_reference_rate(budget_s=15.0, calib=4000, reps=2):
     T, H = sum(d for d, _ in samples), sum(x for _, x in samples)
     rates = [x / d for d, x in samples]
     return {"value": H / T, "unit": UNIT, "cores": cores, "kind": kind,
-            "sample": f"C3 scene (bounded sample): {len(samples)} calls of {samples[0][1]} of 1e8 "
-                      f"histories, {T:.1f} s with {cores} threads (per call {min(rates):.3g}-{max(rates):.3g} "
-                      f"hist/s); includes REF's fixed 64-chunk 2048^2 image cost"}, \
+            "sample": f"{W} scene (bounded sample): {len(samples)} calls of {samples[0][1]} of "
+                      f"{w_full.config.photons_total:.0e} histories, {T:.1f} s with {cores} threads (per call "
+                      f"{min(rates):.3g}-{max(rates):.3g} hist/s); includes REF's fixed 64-chunk "
+                      f"{w.geometry.nu}^2 image cost"}, \
         (kind, lib, run, n)
 
 
@@ -166,7 +192,9 @@ def reference_arm(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
-    base, (kind, lib, run, n) = cpu_reference_rate(budget_s=args.ref_seconds, reps=0)
+    base, (kind, lib, run, n) = cpu_reference_rate(budget_s=args.ref_seconds, reps=0,
+                                                    workload=args.workload)
+    w = workload_for(args.workload, 1000)
     for _ in range(args.warmup):
         run(max(1000, n // 4))
     times, hist = [], 0
@@ -180,8 +208,8 @@ def reference_arm(args):
             "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": WORKLOAD, "histories_per_step": n, "sampled": True},
-            "sec_per_projection": 1e8 / value,
+            "config": {"workload": workload_text(w), "histories_per_step": n, "sampled": True},
+            "sec_per_projection": workload_for(args.workload, None, phantom=w.phantom).config.photons_total / value,
             "cpu_baseline": {**base, "value": value},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -205,7 +233,7 @@ def gpu_arm(args):
     torch.cuda.set_device(device)
 
     t0 = time.time()
-    w = configs.c3(photons=args.photons)
+    w = workload_for(args.workload, args.photons)
     g, spec, cfg, resp = w.geometry, w.spectrum, w.config, w.response
     cfg.step_voxels = args.step
     log(f"[rank {rank}] scene built in {time.time() - t0:.1f}s")
@@ -366,7 +394,7 @@ def gpu_arm(args):
         achieved = alg_bytes / walk_s / 1e9 if walk_s > 0 else 0.0
         traffic, prof = None, {}
         tp = ROOT / "profiles" / "bench_kernel_ncu.json"
-        if tp.exists():
+        if tp.exists() and w.name == "C3":  # the committed ncu capture is of the C3 walk
             try:
                 prof = json.loads(tp.read_text())
                 traffic = prof.get("walk_dram_bytes_per_projection")
@@ -391,7 +419,7 @@ def gpu_arm(args):
         cpu = None
         if ws == 1 and not args.no_cpu:
             try:
-                cpu, _ = cpu_reference_rate(budget_s=args.cpu_seconds)
+                cpu, _ = cpu_reference_rate(budget_s=args.cpu_seconds, workload=args.workload)
             except Exception as e:  # pragma: no cover
                 cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                        "sample": f"failed: {e}"}
@@ -399,7 +427,7 @@ def gpu_arm(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD + (f", step_voxels {args.step} (march)" if args.step > 1 else ""),
+            "config": {"workload": workload_text(w) + (f", step_voxels {args.step} (march)" if args.step > 1 else ""),
                        "histories": n_hist, "splitting": cfg.splitting,
                        "detector": [g.nu, g.nv], "phantom": list(w.phantom.dims),
                        "parallelism": (f"photon batches x{ws}, ncclReduce of the fixed-point tallies "
@@ -517,20 +545,22 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--photons", type=float, default=1e8)
+    ap.add_argument("--photons", type=float, default=None,
+                    help="histories per step (default: the workload's, 1e8 for C3)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-ktime", action="store_true", help="skip the untimed per-kernel timing pass")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-seconds", type=float, default=10.0)
-    ap.add_argument("--workload", default="c3", choices=["c3", "c4"],
-                    help="c3: one 1e8-photon projection (the BASELINE metric); c4: angle-sharded full scan")
+    ap.add_argument("--workload", default="c3", choices=["c1", "c2", "c3", "c4"],
+                    help="c3: one 1e8-photon projection (the BASELINE metric); c1 / c2: the smaller "
+                         "SURVEY.md 8(d) projections; c4: angle-sharded full scan")
     ap.add_argument("--angles", type=int, default=360)
     ap.add_argument("--step", type=int, default=1,
                     help="SimConfig.step_voxels (REF's march mode for > 1, trace.cpp:116-134; "
                          "the paper's production setting is 2-3, PAPER.md:920-933)")
     args = ap.parse_args()
-    args.photons = int(args.photons)
+    args.photons = int(args.photons) if args.photons else None
     if args.impl == "reference":
         return reference_arm(args)
     if args.workload == "c4":

@@ -1392,6 +1392,10 @@ static void upload_phantom_staged(xs_context* c, const xs_phantom* ph)
     for (cudaEvent_t& e : c->up_done)
         if (!e)
             cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    // the DMAs into seg_ids / seg_dens run on copy_stream: order them after
+    // whatever the context's stream still has queued on those buffers
+    cuda_check(cudaEventRecord(c->up_done[0], c->stream), "event");
+    cuda_check(cudaStreamWaitEvent(c->copy_stream, c->up_done[0], 0), "event");
     const size_t n_chunks = (n + chunk - 1) / chunk;
     const unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
     std::atomic<unsigned> arrived[kRing];
