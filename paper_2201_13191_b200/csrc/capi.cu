@@ -70,6 +70,8 @@ WaveEngine* wave_create();
 void wave_destroy(WaveEngine* e);
 cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint32_t n_slots, cudaStream_t s,
                      WaveInfo* info, cudaEvent_t start, int n_pipes);
+cudaError_t wave_run_jobs(WaveEngine* e, const TransportParams* jobs, int n_jobs, int sm_count, uint32_t n_slots,
+                          cudaStream_t s, WaveInfo* info, cudaEvent_t start, int n_pipes);
 cudaError_t launch_finalize_image(const unsigned long long* const* srcs, int n_src, uint64_t off_image,
                                   uint64_t off_var, uint64_t npix, int log2_img, double n_hist, int track_var,
                                   double* image, double* var, cudaStream_t s);
@@ -252,6 +254,12 @@ struct xs_context {
     uint32_t wave_slots = 1u << 22;  // live histories of the wavefront engine (2^20 -> 2^22: +6% on C3)
     int wave_pipes = 2;              // concurrent wavefront pipelines (streams)
     xsd::WaveEngine* wave = nullptr;
+    // device scans: up to scan_jobs consecutive angles in one engine run, a
+    // drained pipeline taking the next angle (scan_group); 1 = angle by angle
+    static constexpr int kMaxScanJobs = 32;
+    int scan_jobs = 8;
+    DevBuf<unsigned long long> job_accum[kMaxScanJobs];
+    DevBuf<double> job_img; // images of a group whose caller keeps none
 
     // multi-GPU (multi.cu): the NCCL communicator of xs_ctx_comm_init, and
     // the scan delegate a group installs on its root so the correction
@@ -583,6 +591,16 @@ void validate_call(const xs_geometry& g, int angle, const xs_spectrum& spec,
 // The run field (Grid::run_*) for this projection's travel direction,
 // source -> detector: the dominant in-plane axis and its sign.  Rewritten
 // only when that changes (four times per full circle).
+// the run field's key (axis * 2 + sign) for a projection: angles with equal
+// keys share the field and can run in one engine call
+int run_key_of(const xsh::Frame& f)
+{
+    const double dx = f.center[0] - f.src[0], dy = f.center[1] - f.src[1];
+    const int axis = std::fabs(dx) >= std::fabs(dy) ? 0 : 1;
+    const int sign = (axis == 0 ? dx : dy) > 0.0 ? 1 : -1;
+    return axis * 2 + (sign > 0 ? 1 : 0);
+}
+
 void ensure_runs(xs_context* c, const xsh::Frame& f)
 {
     if (!c->run_bits)
@@ -604,7 +622,8 @@ void ensure_runs(xs_context* c, const xsh::Frame& f)
 }
 
 void accumulate(xs_context* c, const xs_geometry& g, int angle, const xs_spectrum& spec,
-                const xs_sim_config& cfg, uint64_t h0, uint64_t h1, unsigned long long* d_accum)
+                const xs_sim_config& cfg, uint64_t h0, uint64_t h1, unsigned long long* d_accum,
+                xsd::TransportParams* params_only = nullptr)
 {
     const xsi::Range range("xscat: scatter transport");
     const auto tA = std::chrono::steady_clock::now();
@@ -708,6 +727,10 @@ void accumulate(xs_context* c, const xs_geometry& g, int angle, const xs_spectru
     P.pool = c->pool.p;
     P.grab = c->grab;
     P.status = c->status.p;
+    if (params_only) { // a scan group runs this projection with others (scan_group)
+        *params_only = P;
+        return;
+    }
 
     if (c->engine == 1) { // wavefront engine (wavefront.cu)
         uint32_t n_slots = c->wave_slots;
@@ -1094,6 +1117,8 @@ int xs_ctx_set_option(xs_context* c, const char* key, int64_t value)
             c->runs = value != 0;
         } else if (k == "wave_pipes") {
             c->wave_pipes = (int)std::max<int64_t>(1, std::min<int64_t>(4, value));
+        } else if (k == "scan_jobs") { // angles per engine run in device scans (1: one at a time)
+            c->scan_jobs = (int)std::max<int64_t>(1, std::min<int64_t>(xs_context::kMaxScanJobs, value));
         } else if (k == "wave_slots") {
             c->wave_slots = (uint32_t)std::max<int64_t>(1, std::min<int64_t>(1 << 24, value));
         } else {
@@ -1586,6 +1611,61 @@ int xs_simulate_primary(xs_context* c, const xs_geometry* g, int32_t angle, cons
 
 // run_scan with device outputs (images stay in HBM for the loop's tail):
 // same validation, order and error text as xs_run_scan.
+// Several angles of a device scan in one wavefront run (wave_run_jobs): each
+// pipeline transports one angle at a time into that angle's accumulator and
+// takes the next angle as soon as its current one has drained.  Histories and
+// tallies are the same as angle by angle, so the images are bit-identical.
+// Returns false, with nothing written, when an angle fails validation or the
+// transport raises a device error: the caller then runs the group angle by
+// angle, which reports REF's error for the first failing angle.
+static bool scan_group(xs_context* c, const xs_geometry& g, const xs_spectrum& spec, const xs_sim_config& cfg,
+                       const int32_t* angles, int m, double* d_scatter)
+{
+    try {
+        for (int k = 0; k < m; ++k)
+            validate_call(g, angles[k], spec, cfg, "simulate_scatter");
+    } catch (const Error&) {
+        return false;
+    }
+    const Plan plan = make_plan(g, spec, cfg);
+    if (plan.n_hist == 0)
+        return false;
+    const size_t np = (size_t)g.nu * g.nv;
+    std::vector<xsd::TransportParams> jobs(m);
+    for (int k = 0; k < m; ++k) {
+        c->job_accum[k].reserve(plan.layout.words);
+        cuda_check(cudaMemsetAsync(c->job_accum[k].p, 0, plan.layout.words * 8, c->stream), "memset");
+        accumulate(c, g, angles[k], spec, cfg, 0, plan.n_hist, c->job_accum[k].p, &jobs[k]);
+    }
+    if (!c->wave)
+        c->wave = xsd::wave_create();
+    xsd::WaveInfo info{};
+    cuda_check(xsd::wave_run_jobs(c->wave, jobs.data(), m, c->sm_count, c->wave_slots, c->stream, &info, c->ev0,
+                                  c->wave_pipes),
+               "wavefront transport");
+    cuda_check(cudaEventRecord(c->ev1, c->stream), "event");
+    xsd::DevStatus st;
+    cuda_check(cudaMemcpyAsync(&st, c->status.p, sizeof st, cudaMemcpyDeviceToHost, c->stream), "status readback");
+    cuda_check(cudaStreamSynchronize(c->stream), "kernel execution");
+    if (st.code != 0)
+        return false;
+    float ms = 0.f;
+    cuda_check(cudaEventElapsedTime(&ms, c->ev0, c->ev1), "event time");
+    if (!d_scatter)
+        c->job_img.reserve(np);
+    for (int k = 0; k < m; ++k) {
+        xs_scatter_result r{};
+        finalize(c, g, spec, cfg, c->job_accum[k].p, 0, plan.n_hist, &r, d_scatter ? d_scatter + (size_t)k * np : c->job_img.p);
+    }
+    c->last.kernel_ms = ms;
+    c->last.engine = 1;
+    c->last.waves = info.waves;
+    c->last.live_histories = info.n_slots;
+    c->last.walk_ms = info.walk_ms;
+    c->last.launches = info.launches;
+    return true;
+}
+
 static void scan_device_impl(xs_context* c, const xs_geometry* g, const xs_spectrum* spec, const xs_sim_config* cfg,
                              const int32_t* subset, int32_t n_subset, int32_t what, double* d_primary,
                              double* d_scatter, double* seconds)
@@ -1599,10 +1679,40 @@ static void scan_device_impl(xs_context* c, const xs_geometry* g, const xs_spect
             fail(XS_E_OUT_OF_RANGE, "run_scan: angle index %d out of range", subset[i]);
     const bool want_primary = what != 1, want_scatter = what != 0;
     const size_t np = (size_t)g->nu * g->nv;
+    // groups of consecutive angles that share the run field (scan_group)
+    const bool grouped = want_scatter && c->engine == 1 && c->scan_jobs > 1 && c->wave_pipes > 1 &&
+                         !cfg->track_variance && cfg->step_voxels == 1;
+    int group_end = 0;  // angles [group_begin, group_end) were transported by a group ...
+    int group_begin = 0;
+    int single_end = 0; // ... angles before this one go one at a time (their group failed)
     for (int i = 0; i < n_subset; ++i) {
         const auto t0 = std::chrono::steady_clock::now();
+        if (grouped && i >= group_end && i >= single_end) {
+            int m = 1;
+            if (subset[i] >= 0 && subset[i] < g->n_angles) {
+                const int key = run_key_of(xsh::frame_of(*g, subset[i]));
+                while (m < c->scan_jobs && i + m < n_subset && subset[i + m] >= 0 && subset[i + m] < g->n_angles &&
+                       run_key_of(xsh::frame_of(*g, subset[i + m])) == key)
+                    ++m;
+            }
+            bool ok = false;
+            if (m > 1) {
+                try { // (any failure: the angles go one at a time and report REF's error)
+                    ok = scan_group(c, *g, *spec, *cfg, subset + i, m, d_scatter ? d_scatter + (size_t)i * np : nullptr);
+                } catch (const Error&) {
+                    ok = false;
+                }
+            }
+            if (ok) {
+                group_begin = i;
+                group_end = i + m;
+            } else {
+                single_end = i + m;
+            }
+        }
+        const bool in_group = i >= group_begin && i < group_end;
         try {
-            if (want_scatter) {
+            if (want_scatter && !in_group) {
                 validate_call(*g, subset[i], *spec, *cfg, "simulate_scatter");
                 const Plan plan = make_plan(*g, *spec, *cfg);
                 c->accum.reserve(plan.layout.words);
@@ -1673,54 +1783,91 @@ int xs_run_scan(xs_context* c, const xs_geometry* g, const xs_spectrum* spec, co
             drain(0);
             drain(1);
         }};
-        for (int i = 0; i < n_subset; ++i) {
+        // units of one angle, or of a group of consecutive angles transported in
+        // one engine run (scan_group); unit u uses image / staging buffer pair u & 1
+        const bool grouped = want_scatter && c->engine == 1 && c->scan_jobs > 1 && c->wave_pipes > 1 &&
+                             !cfg->track_variance && cfg->step_voxels == 1;
+        int single_end = 0; // angles before this one go one at a time (their group failed)
+        for (int i = 0, u = 0; i < n_subset; ++u) {
             const auto t0 = std::chrono::steady_clock::now();
-            try {
-                if (want_scatter) {
-                    validate_call(*g, subset[i], *spec, *cfg, "simulate_scatter");
-                    const Plan plan = make_plan(*g, *spec, *cfg);
-                    const int b = i & 1;
-                    drain(b); // angle i - 2's copy out of this buffer pair
-                    c->accum.reserve(plan.layout.words);
-                    cuda_check(cudaMemsetAsync(c->accum.p, 0, plan.layout.words * 8, c->stream), "memset");
-                    accumulate(c, *g, subset[i], *spec, *cfg, 0, plan.n_hist, c->accum.p);
-                    xs_scatter_result r{};
-                    c->scan_img[b].reserve(np);
-                    finalize(c, *g, *spec, *cfg, c->accum.p, 0, plan.n_hist, &r, c->scan_img[b].p);
-                    if (scatter_out) {
-                        c->scan_pin[b].reserve(np);
-                        cuda_check(cudaEventRecord(c->scan_ev[b], c->stream), "event");
-                        cuda_check(cudaStreamWaitEvent(c->copy_stream, c->scan_ev[b], 0), "wait");
-                        cuda_check(cudaMemcpyAsync(c->scan_pin[b].p, c->scan_img[b].p, np * 8, cudaMemcpyDeviceToHost,
-                                                   c->copy_stream),
-                                   "D2H image");
-                        cuda_check(cudaEventRecord(c->scan_done[b], c->copy_stream), "event");
-                        double* dst = scatter_out + (size_t)i * np;
-                        const double* src = c->scan_pin[b].p;
-                        cudaEvent_t done = c->scan_done[b];
-                        copier[b] = std::thread([dst, src, np, done] {
-                            cudaEventSynchronize(done);
-                            std::memcpy(dst, src, np * 8);
-                        });
+            const int b = u & 1;
+            int m = 1;
+            if (want_scatter) {
+                drain(b); // unit u - 2's copy out of this buffer pair
+                bool ok = false;
+                if (grouped && i >= single_end) {
+                    const int key = run_key_of(xsh::frame_of(*g, subset[i]));
+                    while (m < c->scan_jobs && i + m < n_subset && run_key_of(xsh::frame_of(*g, subset[i + m])) == key)
+                        ++m;
+                    if (m > 1) {
+                        try { // (any failure: the angles go one at a time and report REF's error)
+                            c->scan_img[b].reserve((size_t)m * np);
+                            ok = scan_group(c, *g, *spec, *cfg, subset + i, m, c->scan_img[b].p);
+                        } catch (const Error&) {
+                            ok = false;
+                        }
+                        if (!ok) {
+                            single_end = i + m;
+                            m = 1;
+                        }
                     }
-                    // the next angle's transport overwrites only the accumulator, and
-                    // its finalize writes the other image buffer
                 }
-                if (want_primary) {
-                    validate_call(*g, subset[i], *spec, *cfg, "simulate_primary");
-                    c->img.reserve(np);
-                    primary(c, *g, subset[i], *spec, c->img.p);
-                    if (primary_out)
-                        cuda_check(cudaMemcpyAsync(primary_out + (size_t)i * np, c->img.p, np * 8,
-                                                   cudaMemcpyDeviceToHost, c->stream),
-                                   "D2H");
-                    cuda_check(cudaStreamSynchronize(c->stream), "D2H");
+                if (!ok) {
+                    try {
+                        validate_call(*g, subset[i], *spec, *cfg, "simulate_scatter");
+                        const Plan plan = make_plan(*g, *spec, *cfg);
+                        c->accum.reserve(plan.layout.words);
+                        cuda_check(cudaMemsetAsync(c->accum.p, 0, plan.layout.words * 8, c->stream), "memset");
+                        accumulate(c, *g, subset[i], *spec, *cfg, 0, plan.n_hist, c->accum.p);
+                        xs_scatter_result r{};
+                        c->scan_img[b].reserve(np);
+                        finalize(c, *g, *spec, *cfg, c->accum.p, 0, plan.n_hist, &r, c->scan_img[b].p);
+                    } catch (const Error& e) {
+                        fail(XS_E_RUNTIME, "run_scan: angle index %d: %s", subset[i], e.msg.c_str());
+                    }
                 }
-            } catch (const Error& e) {
-                fail(XS_E_RUNTIME, "run_scan: angle index %d: %s", subset[i], e.msg.c_str());
+                if (scatter_out) {
+                    const size_t n_img = (size_t)m * np;
+                    c->scan_pin[b].reserve(n_img);
+                    cuda_check(cudaEventRecord(c->scan_ev[b], c->stream), "event");
+                    cuda_check(cudaStreamWaitEvent(c->copy_stream, c->scan_ev[b], 0), "wait");
+                    cuda_check(cudaMemcpyAsync(c->scan_pin[b].p, c->scan_img[b].p, n_img * 8, cudaMemcpyDeviceToHost,
+                                               c->copy_stream),
+                               "D2H image");
+                    cuda_check(cudaEventRecord(c->scan_done[b], c->copy_stream), "event");
+                    double* dst = scatter_out + (size_t)i * np;
+                    const double* src = c->scan_pin[b].p;
+                    cudaEvent_t done = c->scan_done[b];
+                    copier[b] = std::thread([dst, src, n_img, done] {
+                        cudaEventSynchronize(done);
+                        std::memcpy(dst, src, n_img * 8);
+                    });
+                }
+                // the next unit's transport overwrites only the accumulators, and
+                // its finalize writes the other image buffer
             }
-            if (seconds)
-                seconds[i] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            for (int k = i; k < i + m; ++k) {
+                try {
+                    if (want_primary) {
+                        validate_call(*g, subset[k], *spec, *cfg, "simulate_primary");
+                        c->img.reserve(np);
+                        primary(c, *g, subset[k], *spec, c->img.p);
+                        if (primary_out)
+                            cuda_check(cudaMemcpyAsync(primary_out + (size_t)k * np, c->img.p, np * 8,
+                                                       cudaMemcpyDeviceToHost, c->stream),
+                                       "D2H");
+                        cuda_check(cudaStreamSynchronize(c->stream), "D2H");
+                    }
+                } catch (const Error& e) {
+                    fail(XS_E_RUNTIME, "run_scan: angle index %d: %s", subset[k], e.msg.c_str());
+                }
+            }
+            if (seconds) { // a group's time is shared by its angles
+                const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+                for (int k = i; k < i + m; ++k)
+                    seconds[k] = dt / m;
+            }
+            i += m;
         }
     });
 }

@@ -1047,7 +1047,8 @@ struct WavePipe {
     WaveArgs A;
     TransportParams P;
     int cur = 0;
-    uint32_t waves = 0;
+    uint32_t waves = 0;     // waves launched in this call (every job)
+    uint32_t job_waves = 0; // ... for the current job
     bool done = false;
 
     size_t bytes_held() const
@@ -1269,10 +1270,18 @@ static cudaError_t pipe_prepare(WavePipe& w, const TransportParams& P, uint32_t 
     return cudaSuccess;
 }
 
-cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint32_t n_slots,
-                     cudaStream_t s, WaveInfo* info, cudaEvent_t start, int n_pipes)
+// jobs: one projection (n_jobs = 1: its histories shared by every pipeline
+// through one counter), or several projections of the same scene, run field,
+// palette and sizes that differ only in angle, accumulator and status (a scan):
+// each pipeline then runs one job at a time with its own counter and takes the
+// next job as soon as its current one has drained, so one projection's ramp-down
+// overlaps the other pipelines' steady state.
+cudaError_t wave_run_jobs(WaveEngine* e, const TransportParams* jobs, int n_jobs, int sm_count, uint32_t n_slots,
+                          cudaStream_t s, WaveInfo* info, cudaEvent_t start, int n_pipes)
 {
     const auto host_t0 = std::chrono::steady_clock::now();
+    const TransportParams& P = jobs[0];
+    const bool multi = n_jobs > 1;
     const uint64_t n_hist = P.h_end - P.h_begin;
     if (n_slots > n_hist)
         n_slots = (uint32_t)n_hist;
@@ -1281,6 +1290,8 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
     n_pipes = n_pipes < 1 ? 1 : (n_pipes > kMaxPipes ? kMaxPipes : n_pipes);
     if (n_slots < 2)
         n_pipes = 1;
+    if (multi && n_pipes > n_jobs)
+        n_pipes = n_jobs;
     // per-lane mu table entries: palette codes (4-bit palette, up to 16) or
     // materials (8-bit palette / raw ids, up to kMaxMaterials)
     const int n_mu = use_reg_w(P) ? 4 : (P.G.fmt == kFmtP4 ? std::max(P.n_pal, 1) : kMaxMaterials);
@@ -1307,15 +1318,11 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
     for (int p = 0; p < n_pipes; ++p) {
         WavePipe& w = e->pipe[p];
         XSW_CHECK(pipe_prepare(w, P, per, n_mu));
-        w.P = P;
-        if (P.track_var) { // scratch: var_cap entries per slot, pipelines side by side
-            w.P.var_pix = P.var_pix + (size_t)p * per * P.var_cap;
-            w.P.var_val = P.var_val + (size_t)p * per * P.var_cap;
-        }
+        w.waves = 0;
     }
     const auto host_tb = std::chrono::steady_clock::now();
-    if (!e->next_h)
-        XSW_CHECK(cudaMalloc(&e->next_h, sizeof(unsigned long long)));
+    if (!e->next_h) // history counters: one per pipeline (jobs), the first shared (one projection)
+        XSW_CHECK(cudaMalloc(&e->next_h, kMaxPipes * sizeof(unsigned long long)));
     if (!e->fork)
         XSW_CHECK(cudaEventCreateWithFlags(&e->fork, cudaEventDisableTiming));
 
@@ -1358,13 +1365,22 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
     const auto host_t1 = std::chrono::steady_clock::now();
     if (start) // buffers are allocated: the timed region starts here
         XSW_CHECK(cudaEventRecord(start, s));
-    XSW_CHECK(cudaMemcpyAsync(e->next_h, &P.h_begin, sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
+    if (!multi)
+        XSW_CHECK(cudaMemcpyAsync(e->next_h, &P.h_begin, sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
     XSW_CHECK(cudaEventRecord(e->fork, s));
     uint32_t launches = 0;
-    for (int p = 0; p < n_pipes; ++p) {
+    // start job j on pipeline p (its stream is ordered after the fork)
+    auto start_job = [&](int p, int j) -> cudaError_t {
         WavePipe& w = e->pipe[p];
         cudaStream_t ps = w.stream;
-        XSW_CHECK(cudaStreamWaitEvent(ps, e->fork, 0));
+        w.P = jobs[j];
+        if (w.P.track_var) { // scratch: var_cap entries per slot, pipelines side by side
+            w.P.var_pix = jobs[j].var_pix + (size_t)p * per * jobs[j].var_cap;
+            w.P.var_val = jobs[j].var_val + (size_t)p * per * jobs[j].var_cap;
+        }
+        unsigned long long* cnt = multi ? e->next_h + p : e->next_h;
+        if (multi)
+            XSW_CHECK(cudaMemcpyAsync(cnt, &jobs[j].h_begin, sizeof(unsigned long long), cudaMemcpyHostToDevice, ps));
         WaveCtl init;
         std::memset(&init, 0, sizeof init);
         for (int b = 0; b < 2; ++b) {
@@ -1375,16 +1391,22 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
         init.free_stack = w.stack;
         init.fin = w.stack + per;
         XSW_CHECK(cudaMemcpyAsync(w.ctl, &init, sizeof init, cudaMemcpyHostToDevice, ps));
-        wave_init<<<sm_count, 256, 0, ps>>>(w.ctl, w.stack, per, P.h_begin);
-        w.A.next_h = e->next_h;
+        wave_init<<<sm_count, 256, 0, ps>>>(w.ctl, w.stack, per, jobs[j].h_begin);
+        w.A.next_h = cnt;
         w.cur = 0;
-        w.waves = 0;
+        w.job_waves = 0;
         w.done = false;
         w.A.cur = 0;
         wave_plan<<<1, 1, 0, ps>>>(w.P, w.A);
         wave_admit<<<g_admit, kBlock, admit_smem, ps>>>(w.P, w.A);
         XSW_CHECK(cudaGetLastError());
         launches += 3;
+        return cudaSuccess;
+    };
+    int next_job = 0;
+    for (int p = 0; p < n_pipes; ++p) {
+        XSW_CHECK(cudaStreamWaitEvent(e->pipe[p].stream, e->fork, 0));
+        XSW_CHECK(start_job(p, multi ? next_job++ : 0));
     }
     // XSCAT_KTIME=1: CUDA events around every kernel of the wave (per-kernel
     // device time in xs_launch_stats; meaningful with one pipeline)
@@ -1445,6 +1467,7 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
                     XSW_CHECK(cudaEventRecord(ev[5], ps));
                 w.cur ^= 1;
                 ++w.waves;
+                ++w.job_waves;
                 launches += 6;
             }
         XSW_CHECK(cudaGetLastError());
@@ -1453,8 +1476,13 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
             if (!w.done)
                 XSW_CHECK(cudaMemcpyAsync(w.host_ctl, w.ctl, sizeof(WaveCtl), cudaMemcpyDeviceToHost, w.stream));
         }
-        DevStatus hs;
-        XSW_CHECK(cudaMemcpyAsync(&hs, P.status, sizeof hs, cudaMemcpyDeviceToHost, e->pipe[0].stream));
+        DevStatus hs[kMaxPipes]; // (jobs may share one status record)
+        for (int p = 0; p < n_pipes; ++p) {
+            hs[p].code = 0;
+            if (!e->pipe[p].done) // (read after the stream synchronize below)
+                XSW_CHECK(cudaMemcpyAsync(&hs[p], e->pipe[p].P.status, sizeof(DevStatus), cudaMemcpyDeviceToHost,
+                                          e->pipe[p].stream));
+        }
         bool all_done = true;
         for (int p = 0; p < n_pipes; ++p) {
             WavePipe& w = e->pipe[p];
@@ -1464,24 +1492,36 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
             const WaveCtl& h = *w.host_ctl;
             // nothing left to admit (the shared counter, as this pipeline last saw it,
             // is past the end) and no history in flight
-            w.done = h.live == 0 && h.next_h >= P.h_end && h.q[w.cur].n_batch == 0 && h.q[w.cur].n_batch_r == 0 &&
+            w.done = h.live == 0 && h.next_h >= w.P.h_end && h.q[w.cur].n_batch == 0 && h.q[w.cur].n_batch_r == 0 &&
                      h.q[w.cur].n_free == 0;
+        }
+        bool failed = false;
+        for (int p = 0; p < n_pipes; ++p)
+            failed = failed || hs[p].code != 0;
+        if (failed)
+            break;
+        for (int p = 0; p < n_pipes; ++p) { // a drained pipeline takes the next job
+            WavePipe& w = e->pipe[p];
+            if (w.done && multi && next_job < n_jobs)
+                XSW_CHECK(start_job(p, next_job++));
             all_done = all_done && w.done;
         }
-        if (hs.code != 0 || all_done)
+        if (all_done)
             break;
         // every wave advances each live history by one free path: a history
         // needs at most max_interactions + 1 of them, so the run cannot need
         // more waves than this unless the pipeline state is corrupt
         uint32_t max_w = 0;
         for (int p = 0; p < n_pipes; ++p)
-            max_w = std::max(max_w, e->pipe[p].waves);
+            max_w = std::max(max_w, e->pipe[p].job_waves);
         const uint64_t bound = 4ull * ((n_hist + n_slots - 1) / n_slots + 1) * (uint64_t)(P.max_inter + 2) + 64;
         if (max_w > bound) {
             DevStatus bad{};
             bad.code = XS_E_RUNTIME;
             bad.what = kErrStuck;
-            XSW_CHECK(cudaMemcpyAsync(P.status, &bad, sizeof bad, cudaMemcpyHostToDevice, e->pipe[0].stream));
+            for (int p = 0; p < n_pipes; ++p)
+                XSW_CHECK(cudaMemcpyAsync(e->pipe[p].P.status, &bad, sizeof bad, cudaMemcpyHostToDevice,
+                                          e->pipe[p].stream));
             break;
         }
     }
@@ -1528,5 +1568,11 @@ cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint
     return cudaSuccess;
 }
 #undef XSW_CHECK
+
+cudaError_t wave_run(WaveEngine* e, const TransportParams& P, int sm_count, uint32_t n_slots, cudaStream_t s,
+                     WaveInfo* info, cudaEvent_t start, int n_pipes)
+{
+    return wave_run_jobs(e, &P, 1, sm_count, n_slots, s, info, start, n_pipes);
+}
 
 } // namespace xsd
