@@ -251,7 +251,7 @@ struct xs_context {
     bool runs = true;                       // run field in the spare P8 bits (Grid::run_*)
     int run_bits = 0;                       // of the uploaded grid
     int run_key = -1;                       // axis * 2 + (sign > 0) the field holds; -1: none
-    uint32_t wave_slots = 1u << 22;  // live histories of the wavefront engine (2^20 -> 2^22: +6% on C3)
+    uint32_t wave_slots = 1u << 23;  // live histories of the wavefront engine (2^20 -> 2^22: +6% on C3; 2^23: -1% on C3 and C4)
     int wave_pipes = 2;              // concurrent wavefront pipelines (streams)
     xsd::WaveEngine* wave = nullptr;
     // device scans: up to scan_jobs consecutive angles in one engine run, a

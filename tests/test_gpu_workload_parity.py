@@ -11,7 +11,7 @@ Two kinds of check:
   ledger to 1e-6).
   - C3 scene (512^3 Al/Fe cylinder head, 2048^2, 150 kVp / 65 bins,
     splitting 20) at 1e6 photons, in the default walk (uniform blocks
-    crossed in one step, 7 levels up to 128 voxels, 8-bit palette, 2^22
+    crossed in one step, 7 levels up to 128 voxels, 8-bit palette, the default
     slots in flight) and the strict voxel walk;
   - C2 at its full 1e7 photons;
   - C3 history ranges against the oracle's per-range accumulator: the

@@ -1,6 +1,6 @@
 """C4-style scan (C3 phantom and panel, 1e7 histories per angle) with several
 angles per wavefront run: seconds per angle for scan_jobs x wave_pipes.
-usage: python tools/scan_jobs_probe.py [n_angles]"""
+usage: [XSCAT_WAVE_SLOTS=n] python tools/scan_jobs_probe.py [n_angles] [JOBSxPIPES ...]"""
 import sys
 import time
 import pathlib
@@ -18,7 +18,9 @@ proj = X.Projector(w.phantom, w.response, ctx=ctx)
 sub = list(range(n))
 out = np.empty((n, w.geometry.nv, w.geometry.nu))
 ref = None
-for jobs, pipes in ((1, 2), (8, 2), (16, 2), (1, 3), (8, 3), (16, 3), (24, 3), (16, 4)):
+CASES = [(int(a), int(b)) for a, b in (c.split('x') for c in sys.argv[2:])] or \
+    [(1, 2), (8, 2), (16, 2), (1, 3), (8, 3), (16, 3), (24, 3), (16, 4)]
+for jobs, pipes in CASES:
     ctx.set_option("scan_jobs", jobs)
     ctx.set_option("wave_pipes", pipes)
     proj.run_scan(w.geometry, w.spectrum, w.config, sub, X.SCATTER)  # warm: buffers at full size
