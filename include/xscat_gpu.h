@@ -352,7 +352,7 @@ int xs_ctx_synchronize(xs_context* ctx);
  *                 kernels over global queues); 0: persistent megakernel.
  *                 Both give bit-identical results.  step_voxels > 1
  *                 (REF's march mode) always runs the megakernel
- *   "wave_slots"  histories in flight in the wavefront engine (2^23)
+ *   "wave_slots"  histories in flight in the wavefront engine (2^24)
  *   "wave_pipes"  concurrent wavefront pipelines on their own streams (2)
  *   "compact_palette" 1: 4-bit voxel palette for <= 8 (material, density)
  *                 pairs (half the bytes); 0 (default): 8-bit palette, which

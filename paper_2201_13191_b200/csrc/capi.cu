@@ -251,7 +251,7 @@ struct xs_context {
     bool runs = true;                       // run field in the spare P8 bits (Grid::run_*)
     int run_bits = 0;                       // of the uploaded grid
     int run_key = -1;                       // axis * 2 + (sign > 0) the field holds; -1: none
-    uint32_t wave_slots = 1u << 23;  // live histories of the wavefront engine (2^20 -> 2^22: +6% on C3; 2^23: -1% on C3 and C4)
+    uint32_t wave_slots = 1u << 24;  // live histories of the wavefront engine (2^20 -> 2^22: +6% on C3; 2^23, 2^24: -1% each)
     int wave_pipes = 2;              // concurrent wavefront pipelines (streams)
     xsd::WaveEngine* wave = nullptr;
     // device scans: up to scan_jobs consecutive angles in one engine run, a
@@ -1120,7 +1120,7 @@ int xs_ctx_set_option(xs_context* c, const char* key, int64_t value)
         } else if (k == "scan_jobs") { // angles per engine run in device scans (1: one at a time)
             c->scan_jobs = (int)std::max<int64_t>(1, std::min<int64_t>(xs_context::kMaxScanJobs, value));
         } else if (k == "wave_slots") {
-            c->wave_slots = (uint32_t)std::max<int64_t>(1, std::min<int64_t>(1 << 24, value));
+            c->wave_slots = (uint32_t)std::max<int64_t>(1, std::min<int64_t>(1 << 25, value));
         } else {
             fail(XS_E_INVALID_ARGUMENT, "xs_ctx_set_option: unknown option '%s'", k.c_str());
         }
